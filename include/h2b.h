@@ -1,0 +1,163 @@
+/*
+ * h2b.h — C ABI of the B200-native H² matvec + Krylov hot path.
+ *
+ * The reference (`h2vie`, pure Python) has no C ABI on this path; its
+ * operator boundary is Python:
+ *   matvec(h2, x)                 /root/reference/pkg/src/h2vie/arith.py:108-117
+ *   matmat_apply(h2, X, col_block) arith.py:120-130
+ *   bicgstab_solve(apply, rhs, tol, max_iter, seed, shadow)   arith.py:605-689
+ * and its only native FFI precedent is
+ *   assemble_block_raw(centers, chi, k0, volume, diag, rows, cols, out) -> int
+ *                                  /root/reference/pkg/src/h2vie/_kernel_core.pyx:13-47
+ * (caller-allocated output, integer status).  This header follows that
+ * precedent: plain pointers and sizes, caller-owned I/O, int status
+ * (H2B_OK = 0, negative = error, message via h2b_last_error()), no C++
+ * exceptions and no torch types across the boundary.  The Python drop-in
+ * (`paper_1703_01175_b200`) binds it with ctypes; INTEGRATION.md shows the
+ * binding a maintainer of the reference would add.
+ *
+ * Index space: every vector argument named *_perm is in the cluster-permuted
+ * order of the reference (`xp = x[tree.perm]`, arith.py:113-114); complex
+ * values are interleaved (re, im) doubles (numpy complex128 / cuDoubleComplex).
+ * Multi-RHS blocks are (N, q) row-major, i.e. numpy `X[perm]` C-order.
+ */
+#ifndef H2B_H
+#define H2B_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define H2B_OK 0
+#define H2B_EINVAL (-1)   /* bad argument / shape (reference raises ValueError) */
+#define H2B_ECUDA (-2)    /* CUDA runtime error */
+#define H2B_ENOMEM (-3)   /* device allocation failed */
+#define H2B_ESTATE (-4)   /* handle not fully uploaded */
+#define H2B_ENODEV (-5)   /* no sm_100 (B200) device: there is no CPU fallback */
+
+typedef struct h2b_ctx* h2b_handle;
+
+/* Level-packed operator description (host pointers, copied by h2b_create).
+ * Mirrors paper_1703_01175_b200/pack.py::PackedH2; each table restates one
+ * reference structure:
+ *   clusters   clustering.py:24-45 (start/stop/level/child_lo/child_hi/parent)
+ *   ranks      build.py:76 (NestedBasis.rank)
+ *   couplings  build.py:294-309 (dict (t,s) -> S, sorted admissible order)
+ *   near-field build.py:321-324 (dict (t,s) -> D, sorted inadmissible order)
+ * P = num_clusters, packed index = level-major ordinal (tree.levels order). */
+typedef struct h2b_layout {
+  int64_t n;             /* number of unknowns N */
+  int32_t depth;         /* tree.depth */
+  int32_t num_clusters;  /* P */
+  const int32_t* level_ptr;   /* [depth+1] */
+  const int32_t* c_start;     /* [P] start in permuted index space */
+  const int32_t* c_size;      /* [P] */
+  const int32_t* c_rank;      /* [P] k_c (0 allowed) */
+  const int32_t* c_child_lo;  /* [P] packed index or -1 */
+  const int32_t* c_child_hi;  /* [P] */
+  const int32_t* c_parent;    /* [P] packed index or -1 */
+  const int64_t* c_xhat_off;  /* [P+1] prefix sum of ranks */
+  const int64_t* c_v_off;     /* [P] element offset of V_c in vbuf (-1: non-leaf) */
+  const int64_t* c_t_off;     /* [P] element offset of (T_lo,T_hi) in tbuf (-1: leaf) */
+  int64_t n_coupling;
+  const int64_t* s_row_ptr;   /* [P+1] CSR over packed target */
+  const int32_t* s_col;       /* [n_coupling] packed source */
+  const int64_t* s_off;       /* [n_coupling] element offset in sbuf */
+  int64_t n_near;
+  const int64_t* d_row_ptr;   /* [P+1] */
+  const int32_t* d_col;       /* [n_near] packed source leaf */
+  const int64_t* d_off;       /* [n_near] element offset in dbuf */
+  const int64_t* perm;        /* [N] tree.perm */
+  int64_t v_elems, t_elems, s_elems, d_elems;  /* payload sizes (complex elements) */
+} h2b_layout;
+
+/* payload sections for h2b_upload */
+#define H2B_SEC_V 0  /* leaf bases     */
+#define H2B_SEC_T 1  /* transfers      */
+#define H2B_SEC_S 2  /* couplings      */
+#define H2B_SEC_D 3  /* near-field     */
+
+/* Library/ABI version and the device it will run on. */
+int h2b_version(void);
+const char* h2b_last_error(void);
+/* 1 if a device with compute capability 10.x is visible, 0 otherwise. */
+int h2b_device_ok(int device);
+
+/* Create a handle and copy the index tables to `device`.  Replaces the
+ * construction of the reference H2Matrix object as the matvec's input
+ * (build.py:135-145). */
+int h2b_create(const h2b_layout* layout, int device, h2b_handle* out);
+/* Copy `bytes` of host payload into section `sec` at byte offset `offset`
+ * (chunked uploads allowed).  All four sections must be covered before use. */
+int h2b_upload(h2b_handle h, int sec, const void* src, size_t bytes, size_t offset);
+int h2b_destroy(h2b_handle h);
+/* Device bytes held by the handle (payloads + tables + workspace). */
+int64_t h2b_device_bytes(h2b_handle h);
+
+/* y_perm = S x_perm for q right-hand sides, DEVICE pointers, (N, q) row-major.
+ * Replaces arith._apply_perm (arith.py:52-104).  Stream-ordered on `stream`
+ * (a cudaStream_t; NULL = legacy default).  No allocation after the first
+ * call with a given q.  x_perm and y_perm must not alias. */
+int h2b_matvec_perm(h2b_handle h, const void* x_perm, void* y_perm, int q, void* stream);
+
+/* y = S x with HOST buffers in the ORIGINAL ordering, (N, q) row-major:
+ * the drop-in for arith.matvec / arith.matmat_apply (arith.py:108-130).
+ * Includes host->device copy, the permutation gather, the matvec, the
+ * scatter and device->host copy; synchronous. */
+int h2b_matvec_host(h2b_handle h, const void* x, void* y, int q);
+
+/* Permutation helpers on device buffers: out[i,:] = in[perm[i],:] (gather,
+ * arith.py:113) and out[perm[i],:] = in[i,:] (scatter, arith.py:116). */
+int h2b_gather_perm(h2b_handle h, const void* in, void* out, int q, void* stream);
+int h2b_scatter_perm(h2b_handle h, const void* in, void* out, int q, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Krylov solvers, fully on device (operator = the handle's matvec).
+ * Both work in the permuted space (a permutation preserves inner products,
+ * so iteration counts are unchanged).  DEVICE pointers, length N.
+ * --------------------------------------------------------------------- */
+typedef struct h2b_report {
+  int32_t iterations;     /* SolveReport.iterations (arith.py:39-44) */
+  int32_t converged;      /* SolveReport.converged */
+  int32_t n_history;      /* entries written to `history` */
+  int32_t matvecs;        /* operator applications performed */
+  double wall_time;       /* seconds, host clock around the solve */
+} h2b_report;
+
+/* Restarted GMRES(restart), CGS2 Arnoldi, x0 = 0 — restates
+ * oracle/krylov_oracle.py::gmres_solve (new: the reference has no GMRES).
+ * history: host array of >= max_iter doubles (may be NULL). */
+int h2b_gmres(h2b_handle h, const void* b_perm, void* x_perm, int restart, double tol,
+              int max_iter, double* history, h2b_report* report, void* stream);
+
+/* BiCGStab, a line-by-line restatement of arith.bicgstab_solve
+ * (arith.py:605-689) incl. the single rho-breakdown restart; the restart's
+ * random perturbation (numpy default_rng(seed)) cannot be drawn on device,
+ * so the caller passes it pre-drawn in `restart_noise_perm` (N complex,
+ * permuted order, already multiplied by ||b|| 1e-8), or NULL to fail on
+ * breakdown.  shadow_perm may be NULL (shadow = r0). */
+int h2b_bicgstab(h2b_handle h, const void* b_perm, void* x_perm, double tol, int max_iter,
+                 const void* shadow_perm, const void* restart_noise_perm,
+                 double* history, h2b_report* report, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Fused Krylov vector kernels (device pointers, complex128, length n),
+ * exposed for solvers driven from the host language.
+ * --------------------------------------------------------------------- */
+/* out[j] = sum_i conj(V[j*ldv + i]) * w[i], j < nv  (deterministic order) */
+int h2b_zdotc_multi(const void* V, int64_t ldv, int nv, const void* w, int64_t n,
+                    void* out_dev, void* stream);
+/* w[i] -= sum_j V[j*ldv + i] * h[j]; if nrm2_out != NULL also writes ||w||^2 */
+int h2b_zgemv_sub(const void* V, int64_t ldv, int nv, const void* h_dev, void* w, int64_t n,
+                  double* nrm2_out_dev, void* stream);
+/* y = a*x + b*y with complex scalars given by value (re, im) */
+int h2b_zaxpby(int64_t n, double ar, double ai, const void* x, double br, double bi, void* y,
+               void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* H2B_H */

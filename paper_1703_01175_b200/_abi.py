@@ -1,0 +1,111 @@
+"""ctypes binding of the C ABI in include/h2b.h (libh2b.so, built in-tree).
+
+There is deliberately no fallback: if the library is missing or no
+compute-capability-10 device is visible, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libh2b.so")
+
+H2B_OK, H2B_EINVAL, H2B_ECUDA, H2B_ENOMEM, H2B_ESTATE, H2B_ENODEV = 0, -1, -2, -3, -4, -5
+SEC_V, SEC_T, SEC_S, SEC_D = 0, 1, 2, 3
+
+EXPORTED = (
+    "h2b_version", "h2b_last_error", "h2b_device_ok", "h2b_create", "h2b_upload",
+    "h2b_destroy", "h2b_device_bytes", "h2b_matvec_perm", "h2b_matvec_host",
+    "h2b_gather_perm", "h2b_scatter_perm", "h2b_gmres", "h2b_bicgstab",
+    "h2b_zdotc_multi", "h2b_zgemv_sub", "h2b_zaxpby",
+)
+
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+
+
+class Layout(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64), ("depth", C.c_int32), ("num_clusters", C.c_int32),
+        ("level_ptr", _i32p), ("c_start", _i32p), ("c_size", _i32p), ("c_rank", _i32p),
+        ("c_child_lo", _i32p), ("c_child_hi", _i32p), ("c_parent", _i32p),
+        ("c_xhat_off", _i64p), ("c_v_off", _i64p), ("c_t_off", _i64p),
+        ("n_coupling", C.c_int64), ("s_row_ptr", _i64p), ("s_col", _i32p), ("s_off", _i64p),
+        ("n_near", C.c_int64), ("d_row_ptr", _i64p), ("d_col", _i32p), ("d_off", _i64p),
+        ("perm", _i64p),
+        ("v_elems", C.c_int64), ("t_elems", C.c_int64), ("s_elems", C.c_int64),
+        ("d_elems", C.c_int64),
+    ]
+
+
+class Report(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("n_history", C.c_int32),
+                ("matvecs", C.c_int32), ("wall_time", C.c_double)]
+
+
+class H2BError(RuntimeError):
+    """A non-OK status from libh2b; .code holds the H2B_* value."""
+
+    def __init__(self, msg, code):
+        super().__init__(msg)
+        self.code = code
+
+
+_lib = None
+
+
+def lib():
+    """Load libh2b.so once; raise if it is missing (no CPU fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `make` (or __graft_entry__.build()) first; "
+                          "the H2 hot path has no CPU fallback")
+    L = C.CDLL(LIB_PATH)
+    vp = C.c_void_p
+    L.h2b_version.restype = C.c_int
+    L.h2b_last_error.restype = C.c_char_p
+    L.h2b_device_ok.argtypes = [C.c_int]
+    L.h2b_create.argtypes = [C.POINTER(Layout), C.c_int, C.POINTER(vp)]
+    L.h2b_upload.argtypes = [vp, C.c_int, vp, C.c_size_t, C.c_size_t]
+    L.h2b_destroy.argtypes = [vp]
+    L.h2b_device_bytes.argtypes = [vp]
+    L.h2b_device_bytes.restype = C.c_int64
+    L.h2b_matvec_perm.argtypes = [vp, vp, vp, C.c_int, vp]
+    L.h2b_matvec_host.argtypes = [vp, vp, vp, C.c_int]
+    L.h2b_gather_perm.argtypes = [vp, vp, vp, C.c_int, vp]
+    L.h2b_scatter_perm.argtypes = [vp, vp, vp, C.c_int, vp]
+    L.h2b_gmres.argtypes = [vp, vp, vp, C.c_int, C.c_double, C.c_int, C.POINTER(C.c_double),
+                            C.POINTER(Report), vp]
+    L.h2b_bicgstab.argtypes = [vp, vp, vp, C.c_double, C.c_int, vp, vp, C.POINTER(C.c_double),
+                               C.POINTER(Report), vp]
+    L.h2b_zdotc_multi.argtypes = [vp, C.c_int64, C.c_int, vp, C.c_int64, vp, vp]
+    L.h2b_zgemv_sub.argtypes = [vp, C.c_int64, C.c_int, vp, vp, C.c_int64, vp, vp]
+    L.h2b_zaxpby.argtypes = [C.c_int64, C.c_double, C.c_double, vp, C.c_double, C.c_double, vp, vp]
+    _lib = L
+    return L
+
+
+def check(rc, what=""):
+    if rc != H2B_OK:
+        msg = lib().h2b_last_error().decode(errors="replace")
+        if rc == H2B_EINVAL:
+            raise ValueError(f"{what}: {msg}")
+        raise H2BError(f"{what}: {msg} (status {rc})", rc)
+    return rc
+
+
+def exported_symbols():
+    """Names from include/h2b.h that the loaded library actually exports."""
+    L = lib()
+    out = []
+    for name in EXPORTED:
+        try:
+            getattr(L, name)
+            out.append(name)
+        except AttributeError:
+            pass
+    return out

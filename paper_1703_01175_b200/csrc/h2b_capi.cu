@@ -1,0 +1,240 @@
+// extern "C" surface of libh2b.so (declared in include/h2b.h).
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+
+#include "h2b_common.cuh"
+
+static thread_local std::string g_last_error;
+
+void h2b_set_error(const std::string& msg) { g_last_error = msg; }
+
+#define REQUIRE(cond, code, msg) \
+  do {                           \
+    if (!(cond)) {               \
+      h2b_set_error(msg);        \
+      return code;               \
+    }                            \
+  } while (0)
+
+namespace {
+
+template <typename T>
+int upload_table(T** dst, const T* src, int64_t count, int64_t* acc) {
+  const size_t bytes = sizeof(T) * (size_t)std::max<int64_t>(count, 1);
+  H2B_CUDA_TRY(cudaMalloc((void**)dst, bytes));
+  if (count > 0) H2B_CUDA_TRY(cudaMemcpy(*dst, src, sizeof(T) * count, cudaMemcpyHostToDevice));
+  *acc += (int64_t)bytes;
+  return H2B_OK;
+}
+
+void free_ctx(h2b_ctx* h) {
+  void* ptrs[] = {h->c_start, h->c_size_d, h->c_rank_d, h->c_lo,   h->c_hi,   h->c_parent,
+                  h->c_xoff,  h->c_voff,   h->c_toff,   h->s_row_ptr, h->s_off, h->d_row_ptr,
+                  h->d_off,   h->s_col,    h->d_col,    h->perm,   h->leaves, h->xhat,
+                  h->yhat,    h->kry,      h->buf[0],   h->buf[1], h->buf[2], h->buf[3],
+                  h->hxp,     h->hyp};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (h->hx) cudaFreeHost(h->hx);
+  if (h->hy) cudaFreeHost(h->hy);
+  delete h;
+}
+
+int ready(h2b_ctx* h) {
+  REQUIRE(h, H2B_EINVAL, "null handle");
+  for (int s = 0; s < 4; ++s)
+    REQUIRE(h->sec_uploaded[s] >= h->sec_elems[s], H2B_ESTATE,
+            "payload section " + std::to_string(s) + " not fully uploaded");
+  return H2B_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int h2b_version(void) { return 1; }
+
+const char* h2b_last_error(void) { return g_last_error.c_str(); }
+
+int h2b_device_ok(int device) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return 0;
+  return prop.major == 10 ? 1 : 0;
+}
+
+int h2b_create(const h2b_layout* L, int device, h2b_handle* out) {
+  REQUIRE(L && out, H2B_EINVAL, "h2b_create: null argument");
+  *out = nullptr;
+  REQUIRE(h2b_device_ok(device), H2B_ENODEV,
+          "h2b_create: no compute-capability 10.x (B200/sm_100a) device " + std::to_string(device) +
+              " — the H2 hot path has no CPU fallback");
+  REQUIRE(L->n > 0 && L->depth > 0 && L->num_clusters > 0, H2B_EINVAL, "h2b_create: empty operator");
+  REQUIRE(L->n_coupling >= 0 && L->n_near > 0, H2B_EINVAL, "h2b_create: bad block counts");
+  H2B_CUDA_TRY(cudaSetDevice(device));
+  h2b_ctx* h = new h2b_ctx();
+  h->device = device;
+  h->n = L->n;
+  h->depth = L->depth;
+  h->P = L->num_clusters;
+  h->K = L->c_xhat_off[L->num_clusters];
+  h->n_coupling = L->n_coupling;
+  h->n_near = L->n_near;
+  h->sec_elems[0] = L->v_elems;
+  h->sec_elems[1] = L->t_elems;
+  h->sec_elems[2] = L->s_elems;
+  h->sec_elems[3] = L->d_elems;
+  const int P = h->P;
+  h->level_ptr.assign(L->level_ptr, L->level_ptr + h->depth + 1);
+  h->c_rank.assign(L->c_rank, L->c_rank + P);
+  h->c_child_lo.assign(L->c_child_lo, L->c_child_lo + P);
+  h->c_size.assign(L->c_size, L->c_size + P);
+  if (h->level_ptr[0] != 0 || h->level_ptr[h->depth] != P) {
+    delete h;
+    h2b_set_error("h2b_create: level_ptr does not cover the clusters");
+    return H2B_EINVAL;
+  }
+  // leaves, schedule
+  int uni = -1;
+  for (int p = 0; p < P; ++p)
+    if (h->c_child_lo[p] < 0) {
+      h->h_leaves.push_back(p);
+      const int sz = h->c_size[p];
+      uni = (uni == -1 || uni == sz) ? sz : 0;
+    }
+  h->uniform_leaf = uni > 0 ? uni : 0;
+  h->n_leaves = (int)h->h_leaves.size();
+  for (int l = h->depth - 1; l >= 0; --l) {
+    bool any = false;
+    for (int p = h->level_ptr[l]; p < h->level_ptr[l + 1]; ++p) any |= h->c_rank[p] > 0;
+    if (any) h->up_levels.push_back(l);
+  }
+  for (int l = 0; l < h->depth; ++l) {
+    bool any = false;
+    for (int p = h->level_ptr[l]; p < h->level_ptr[l + 1]; ++p)
+      any |= (h->c_rank[p] > 0 && h->c_child_lo[p] >= 0);
+    if (any) h->down_levels.push_back(l);
+  }
+  // near-field fast path needs every near block to be uniform (n x n), which holds when all
+  // leaves share one size; it also needs 32-byte alignment, guaranteed for even sizes.
+  int64_t acc = 0;
+  int rc = H2B_OK;
+#define UP(dst, src, cnt) \
+  if (!rc) rc = upload_table(&h->dst, src, cnt, &acc)
+  UP(c_start, L->c_start, P);
+  UP(c_size_d, L->c_size, P);
+  UP(c_rank_d, L->c_rank, P);
+  UP(c_lo, L->c_child_lo, P);
+  UP(c_hi, L->c_child_hi, P);
+  UP(c_parent, L->c_parent, P);
+  UP(c_xoff, L->c_xhat_off, P + 1);
+  UP(c_voff, L->c_v_off, P);
+  UP(c_toff, L->c_t_off, P);
+  UP(s_row_ptr, L->s_row_ptr, P + 1);
+  UP(s_col, L->s_col, L->n_coupling);
+  UP(s_off, L->s_off, L->n_coupling);
+  UP(d_row_ptr, L->d_row_ptr, P + 1);
+  UP(d_col, L->d_col, L->n_near);
+  UP(d_off, L->d_off, L->n_near);
+  UP(perm, L->perm, L->n);
+  UP(leaves, h->h_leaves.data(), (int64_t)h->h_leaves.size());
+#undef UP
+  for (int s = 0; s < 4 && !rc; ++s) {
+    const size_t bytes = 16 * (size_t)std::max<int64_t>(h->sec_elems[s], 2);
+    cudaError_t e = cudaMalloc(&h->buf[s], bytes);
+    if (e != cudaSuccess) {
+      h2b_set_error(std::string("h2b_create: payload allocation: ") + cudaGetErrorString(e));
+      rc = e == cudaErrorMemoryAllocation ? H2B_ENOMEM : H2B_ECUDA;
+    }
+    acc += bytes;
+  }
+  if (rc) {
+    free_ctx(h);
+    return rc;
+  }
+  h->device_bytes = acc;
+  *out = h;
+  return H2B_OK;
+}
+
+int h2b_upload(h2b_handle h, int sec, const void* src, size_t bytes, size_t offset) {
+  REQUIRE(h, H2B_EINVAL, "null handle");
+  REQUIRE(sec >= 0 && sec < 4, H2B_EINVAL, "h2b_upload: bad section");
+  REQUIRE(bytes % 16 == 0 && offset % 16 == 0, H2B_EINVAL, "h2b_upload: unaligned size/offset");
+  REQUIRE((int64_t)((offset + bytes) / 16) <= h->sec_elems[sec], H2B_EINVAL,
+          "h2b_upload: beyond section end");
+  if (bytes == 0) return H2B_OK;
+  REQUIRE(src, H2B_EINVAL, "h2b_upload: null source");
+  H2B_CUDA_TRY(cudaSetDevice(h->device));
+  H2B_CUDA_TRY(cudaMemcpy((char*)h->buf[sec] + offset, src, bytes, cudaMemcpyHostToDevice));
+  h->sec_uploaded[sec] = std::max<int64_t>(h->sec_uploaded[sec], (int64_t)((offset + bytes) / 16));
+  return H2B_OK;
+}
+
+int h2b_destroy(h2b_handle h) {
+  if (!h) return H2B_OK;
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  free_ctx(h);
+  return H2B_OK;
+}
+
+int64_t h2b_device_bytes(h2b_handle h) { return h ? h->device_bytes : -1; }
+
+int h2b_matvec_perm(h2b_handle h, const void* x_perm, void* y_perm, int q, void* stream) {
+  int rc = ready(h);
+  if (rc) return rc;
+  REQUIRE(q >= 1, H2B_EINVAL, "h2b_matvec_perm: q must be >= 1");
+  REQUIRE(x_perm && y_perm && x_perm != y_perm, H2B_EINVAL,
+          "h2b_matvec_perm: null or aliased buffers");
+  return h2b_run_matvec(h, (const double2*)x_perm, (double2*)y_perm, q, (cudaStream_t)stream);
+}
+
+int h2b_matvec_host(h2b_handle h, const void* x, void* y, int q) {
+  int rc = ready(h);
+  if (rc) return rc;
+  REQUIRE(q >= 1, H2B_EINVAL, "h2b_matvec_host: q must be >= 1");
+  REQUIRE(x && y, H2B_EINVAL, "h2b_matvec_host: null buffer");
+  H2B_CUDA_TRY(cudaSetDevice(h->device));
+  const size_t bytes = (size_t)16 * h->n * q;
+  if (h->hws_q < q) {
+    if (h->hxp) cudaFree(h->hxp);
+    if (h->hyp) cudaFree(h->hyp);
+    h->hxp = h->hyp = nullptr;
+    h->hws_q = 0;
+    H2B_CUDA_TRY(cudaMalloc(&h->hxp, 2 * bytes));
+    H2B_CUDA_TRY(cudaMalloc(&h->hyp, 2 * bytes));
+    h->hws_q = q;
+  }
+  double2* dx = h->hxp;                  // original order
+  double2* dxp = h->hxp + h->n * q;      // permuted
+  double2* dyp = h->hyp;                 // permuted
+  double2* dy = h->hyp + h->n * q;       // original order
+  cudaStream_t st = 0;
+  H2B_CUDA_TRY(cudaMemcpyAsync(dx, x, bytes, cudaMemcpyHostToDevice, st));
+  if ((rc = h2b_launch_gather(h->perm, h->n, dx, dxp, q, st))) return rc;
+  if ((rc = h2b_run_matvec(h, dxp, dyp, q, st))) return rc;
+  if ((rc = h2b_launch_scatter(h->perm, h->n, dyp, dy, q, st))) return rc;
+  H2B_CUDA_TRY(cudaMemcpyAsync(y, dy, bytes, cudaMemcpyDeviceToHost, st));
+  H2B_CUDA_TRY(cudaStreamSynchronize(st));
+  return H2B_OK;
+}
+
+int h2b_gather_perm(h2b_handle h, const void* in, void* out, int q, void* stream) {
+  REQUIRE(h && in && out && q >= 1, H2B_EINVAL, "h2b_gather_perm: bad arguments");
+  return h2b_launch_gather(h->perm, h->n, (const double2*)in, (double2*)out, q, (cudaStream_t)stream);
+}
+
+int h2b_scatter_perm(h2b_handle h, const void* in, void* out, int q, void* stream) {
+  REQUIRE(h && in && out && q >= 1, H2B_EINVAL, "h2b_scatter_perm: bad arguments");
+  return h2b_launch_scatter(h->perm, h->n, (const double2*)in, (double2*)out, q, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,554 @@
+// Krylov solvers around the H² matvec, on device (sm_100a).
+//
+// * GMRES(m) with CGS2 Arnoldi — new component (the reference has no GMRES,
+//   SURVEY.md §0 finding 1); restates oracle/krylov_oracle.py::gmres_solve.
+// * BiCGStab — restates the reference's own solver line by line
+//   (/root/reference/pkg/src/h2vie/arith.py:605-689).
+//
+// Vector work is done by fused reduction kernels with a deterministic
+// two-stage (per-CTA partial, then fixed-order final sum) reduction, so the
+// same inputs always produce the same bits.  The tiny (m+1)xm Hessenberg /
+// Givens algebra runs on the host from scalars copied back once per step.
+#include <math.h>
+
+#include <algorithm>
+#include <chrono>
+#include <complex>
+#include <vector>
+
+#include "h2b_common.cuh"
+
+namespace {
+
+constexpr int RT = 256;      // threads per reduction CTA
+constexpr int RB_MAX = 296;  // max reduction CTAs (2 per SM)
+constexpr int MAXV = 8;      // max pairs per fused dot launch
+
+__device__ __forceinline__ double2 block_sum2(double2 v, double2* sm) {
+  v = warp_sum2(v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) sm[warp] = v;
+  __syncthreads();
+  double2 s = make_double2(0.0, 0.0);
+  if (threadIdx.x == 0)
+    for (int w = 0; w < RT / 32; ++w) s = cadd(s, sm[w]);
+  return s;  // valid in thread 0
+}
+
+struct DotPairs {
+  const double2* a[MAXV];
+  const double2* b[MAXV];
+  int np;
+};
+
+// partial[j*gridDim + block] = Σ_{i in block's slice} conj(a_j[i]) b_j[i]
+__global__ void __launch_bounds__(RT) k_dots_partial(DotPairs d, int64_t n, double2* partial) {
+  __shared__ double2 sm[RT / 32];
+  for (int j = 0; j < d.np; ++j) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int64_t i = blockIdx.x * (int64_t)RT + threadIdx.x; i < n; i += (int64_t)gridDim.x * RT)
+      cfma_conj(acc, d.a[j][i], d.b[j][i]);
+    double2 s = block_sum2(acc, sm);
+    if (threadIdx.x == 0) partial[j * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+// multi-dot against the rows of a basis: partial[j*grid+blk] = Σ conj(V[j*ldv+i]) w[i]
+__global__ void __launch_bounds__(RT) k_basis_dots_partial(const double2* __restrict__ V, int64_t ldv,
+                                                           int nv, const double2* __restrict__ w,
+                                                           int64_t n, double2* partial) {
+  __shared__ double2 sm[RT / 32];
+  for (int j = 0; j < nv; ++j) {
+    const double2* vj = V + j * ldv;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int64_t i = blockIdx.x * (int64_t)RT + threadIdx.x; i < n; i += (int64_t)gridDim.x * RT)
+      cfma_conj(acc, vj[i], w[i]);
+    double2 s = block_sum2(acc, sm);
+    if (threadIdx.x == 0) partial[j * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+// out[j] = Σ_blk partial[j*nb + blk] in fixed order (one warp per j)
+__global__ void k_reduce_partials(const double2* __restrict__ partial, int nb, int nv,
+                                  double2* __restrict__ out) {
+  const int j = blockIdx.x;
+  if (j >= nv) return;
+  const int lane = threadIdx.x;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int b = lane; b < nb; b += 32) acc = cadd(acc, partial[j * nb + b]);
+  acc = warp_sum2(acc);
+  if (lane == 0) out[j] = acc;
+}
+
+// w[i] -= Σ_j V[j*ldv+i] h[j]; optional partial of ||w||^2 (stored in .x)
+__global__ void __launch_bounds__(RT) k_basis_sub(const double2* __restrict__ V, int64_t ldv, int nv,
+                                                  const double2* __restrict__ hcoef, double2* w,
+                                                  int64_t n, double2* nrm_partial) {
+  __shared__ double2 sm[RT / 32];
+  __shared__ double2 hs[64];
+  for (int j = threadIdx.x; j < nv && j < 64; j += RT) hs[j] = hcoef[j];
+  __syncthreads();
+  double2 nrm = make_double2(0.0, 0.0);
+  for (int64_t i = blockIdx.x * (int64_t)RT + threadIdx.x; i < n; i += (int64_t)gridDim.x * RT) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int j = 0; j < nv; ++j) cfma(acc, V[j * ldv + i], j < 64 ? hs[j] : hcoef[j]);
+    double2 wi = w[i];
+    wi.x -= acc.x;
+    wi.y -= acc.y;
+    w[i] = wi;
+    nrm.x = fma(wi.x, wi.x, nrm.x);
+    nrm.x = fma(wi.y, wi.y, nrm.x);
+  }
+  if (nrm_partial) {
+    double2 s = block_sum2(nrm, sm);
+    if (threadIdx.x == 0) nrm_partial[blockIdx.x] = s;
+  }
+}
+
+struct Lin3 {
+  double2 c[3];
+  const double2* x[3];
+  int nx;
+};
+
+// out = Σ c_k x_k (x_k may alias out); optional partial ||out||^2
+__global__ void __launch_bounds__(RT) k_lincomb(Lin3 L, double2* out, int64_t n, double2* nrm_partial) {
+  __shared__ double2 sm[RT / 32];
+  double2 nrm = make_double2(0.0, 0.0);
+  for (int64_t i = blockIdx.x * (int64_t)RT + threadIdx.x; i < n; i += (int64_t)gridDim.x * RT) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = 0; k < L.nx; ++k) cfma(acc, L.c[k], L.x[k][i]);
+    out[i] = acc;
+    nrm.x = fma(acc.x, acc.x, nrm.x);
+    nrm.x = fma(acc.y, acc.y, nrm.x);
+  }
+  if (nrm_partial) {
+    double2 s = block_sum2(nrm, sm);
+    if (threadIdx.x == 0) nrm_partial[blockIdx.x] = s;
+  }
+}
+
+int nblocks(int64_t n) {
+  int64_t b = (n + RT * 4 - 1) / (RT * 4);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, RB_MAX));
+}
+
+typedef std::complex<double> cplx;
+
+// scratch shared by the exported vector kernels (per process, single device)
+struct Scratch {
+  double2* partial = nullptr;  // RB_MAX * 64
+  double2* vals = nullptr;     // 256 device scalars
+  double2* host = nullptr;     // 256 pinned host scalars
+  int device = -1;
+};
+Scratch g_scratch;
+
+int scratch_ready() {
+  int dev = 0;
+  H2B_CUDA_TRY(cudaGetDevice(&dev));
+  if (g_scratch.partial && g_scratch.device == dev) return H2B_OK;
+  H2B_CUDA_TRY(cudaMalloc(&g_scratch.partial, sizeof(double2) * RB_MAX * 64));
+  H2B_CUDA_TRY(cudaMalloc(&g_scratch.vals, sizeof(double2) * 256));
+  H2B_CUDA_TRY(cudaMallocHost(&g_scratch.host, sizeof(double2) * 256));
+  g_scratch.device = dev;
+  return H2B_OK;
+}
+
+// ---- device-side building blocks used by the solvers -----------------------
+struct Ops {
+  cudaStream_t st;
+  int64_t n;
+  int nb;
+  double2 *partial, *vals, *host;
+
+  // vals[0..np) = vdot(a_j, b_j); copies back to host[0..np) when `fetch`
+  int dots(std::initializer_list<std::pair<const double2*, const double2*>> pairs, bool fetch) {
+    DotPairs d;
+    d.np = 0;
+    for (auto& pr : pairs) {
+      d.a[d.np] = pr.first;
+      d.b[d.np] = pr.second;
+      ++d.np;
+    }
+    k_dots_partial<<<nb, RT, 0, st>>>(d, n, partial);
+    H2B_CHECK_LAUNCH();
+    k_reduce_partials<<<d.np, 32, 0, st>>>(partial, nb, d.np, vals);
+    H2B_CHECK_LAUNCH();
+    if (fetch) return fetch_vals(d.np);
+    return H2B_OK;
+  }
+  int fetch_vals(int cnt) {
+    H2B_CUDA_TRY(cudaMemcpyAsync(host, vals, sizeof(double2) * cnt, cudaMemcpyDeviceToHost, st));
+    H2B_CUDA_TRY(cudaStreamSynchronize(st));
+    return H2B_OK;
+  }
+  // out = Σ c_k x_k ; if nrm: vals[slot] = ||out||^2
+  int lincomb(double2* out, std::initializer_list<std::pair<cplx, const double2*>> terms, int nrm_slot) {
+    Lin3 L;
+    L.nx = 0;
+    for (auto& t : terms) {
+      L.c[L.nx] = make_double2(t.first.real(), t.first.imag());
+      L.x[L.nx] = t.second;
+      ++L.nx;
+    }
+    k_lincomb<<<nb, RT, 0, st>>>(L, out, n, nrm_slot >= 0 ? partial : nullptr);
+    H2B_CHECK_LAUNCH();
+    if (nrm_slot >= 0) {
+      k_reduce_partials<<<1, 32, 0, st>>>(partial, nb, 1, vals + nrm_slot);
+      H2B_CHECK_LAUNCH();
+    }
+    return H2B_OK;
+  }
+};
+
+#define TRY(x)          \
+  do {                  \
+    int _rc = (x);      \
+    if (_rc) return _rc; \
+  } while (0)
+
+struct KryWs {
+  double2* base = nullptr;
+  size_t bytes = 0;
+};
+
+int krylov_ws(h2b_ctx* h, size_t bytes, double2** out) {
+  if (h->kry_bytes < bytes) {
+    if (h->kry) cudaFree(h->kry);
+    h->device_bytes -= h->kry_bytes;
+    h->kry = nullptr;
+    h->kry_bytes = 0;
+    H2B_CUDA_TRY(cudaMalloc(&h->kry, bytes));
+    h->kry_bytes = bytes;
+    h->device_bytes += bytes;
+  }
+  *out = (double2*)h->kry;
+  return H2B_OK;
+}
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+// ===========================================================================
+// exported vector kernels
+// ===========================================================================
+extern "C" int h2b_zdotc_multi(const void* V, int64_t ldv, int nv, const void* w, int64_t n,
+                               void* out_dev, void* stream) {
+  if (nv < 1 || nv > 64 || n < 0 || !V || !w || !out_dev) {
+    h2b_set_error("h2b_zdotc_multi: bad arguments (need 1 <= nv <= 64)");
+    return H2B_EINVAL;
+  }
+  TRY(scratch_ready());
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nb = nblocks(n);
+  k_basis_dots_partial<<<nb, RT, 0, st>>>((const double2*)V, ldv, nv, (const double2*)w, n,
+                                          g_scratch.partial);
+  H2B_CHECK_LAUNCH();
+  k_reduce_partials<<<nv, 32, 0, st>>>(g_scratch.partial, nb, nv, (double2*)out_dev);
+  H2B_CHECK_LAUNCH();
+  return H2B_OK;
+}
+
+extern "C" int h2b_zgemv_sub(const void* V, int64_t ldv, int nv, const void* h_dev, void* w,
+                             int64_t n, double* nrm2_out_dev, void* stream) {
+  if (nv < 0 || nv > 64 || n < 0 || !w) {
+    h2b_set_error("h2b_zgemv_sub: bad arguments (need 0 <= nv <= 64)");
+    return H2B_EINVAL;
+  }
+  TRY(scratch_ready());
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nb = nblocks(n);
+  k_basis_sub<<<nb, RT, 0, st>>>((const double2*)V, ldv, nv, (const double2*)h_dev, (double2*)w, n,
+                                 nrm2_out_dev ? g_scratch.partial : nullptr);
+  H2B_CHECK_LAUNCH();
+  if (nrm2_out_dev) {
+    k_reduce_partials<<<1, 32, 0, st>>>(g_scratch.partial, nb, 1, g_scratch.vals);
+    H2B_CHECK_LAUNCH();
+    H2B_CUDA_TRY(cudaMemcpyAsync(nrm2_out_dev, g_scratch.vals, sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  return H2B_OK;
+}
+
+extern "C" int h2b_zaxpby(int64_t n, double ar, double ai, const void* x, double br, double bi,
+                          void* y, void* stream) {
+  if (n < 0 || !x || !y) {
+    h2b_set_error("h2b_zaxpby: bad arguments");
+    return H2B_EINVAL;
+  }
+  Lin3 L;
+  L.nx = 2;
+  L.c[0] = make_double2(ar, ai);
+  L.x[0] = (const double2*)x;
+  L.c[1] = make_double2(br, bi);
+  L.x[1] = (const double2*)y;
+  k_lincomb<<<nblocks(n), RT, 0, (cudaStream_t)stream>>>(L, (double2*)y, n, nullptr);
+  H2B_CHECK_LAUNCH();
+  return H2B_OK;
+}
+
+// ===========================================================================
+// GMRES(m), CGS2, x0 = 0
+// ===========================================================================
+extern "C" int h2b_gmres(h2b_handle h, const void* b_perm, void* x_perm, int restart, double tol,
+                         int max_iter, double* history, h2b_report* report, void* stream) {
+  if (!h || !b_perm || !x_perm || !report) {
+    h2b_set_error("h2b_gmres: null argument");
+    return H2B_EINVAL;
+  }
+  if (!(tol > 0.0 && tol < 1.0) || max_iter < 1 || restart < 1 || restart > 63) {
+    h2b_set_error("h2b_gmres: need 0 < tol < 1, max_iter >= 1, 1 <= restart <= 63");
+    return H2B_EINVAL;
+  }
+  const double t0 = now_s();
+  TRY(scratch_ready());
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = h->n;
+  const int m = restart;
+  double2* ws = nullptr;
+  // V: (m+1) x n basis, r, tmp
+  TRY(krylov_ws(h, sizeof(double2) * (size_t)n * (m + 3), &ws));
+  double2* V = ws;
+  double2* r = ws + (size_t)n * (m + 1);
+  double2* tmp = r + n;
+  const double2* b = (const double2*)b_perm;
+  double2* x = (double2*)x_perm;
+  Ops ops{st, n, nblocks(n), g_scratch.partial, g_scratch.vals, g_scratch.host};
+  double2* hvals = g_scratch.vals;  // device scalars
+
+  *report = h2b_report{0, 0, 0, 0, 0.0};
+  TRY(ops.dots({{b, b}}, true));
+  const double bnrm = sqrt(g_scratch.host[0].x);
+  H2B_CUDA_TRY(cudaMemsetAsync(x, 0, sizeof(double2) * n, st));
+  if (bnrm == 0.0) {
+    report->converged = 1;
+    report->wall_time = now_s() - t0;
+    H2B_CUDA_TRY(cudaStreamSynchronize(st));
+    return H2B_OK;
+  }
+  H2B_CUDA_TRY(cudaMemcpyAsync(r, b, sizeof(double2) * n, cudaMemcpyDeviceToDevice, st));
+  int it = 0, matvecs = 0, nh = 0;
+  bool converged = false;
+  std::vector<cplx> H((size_t)(m + 1) * m), g(m + 1), sn(m), y(m);
+  std::vector<double> cs(m);
+  double beta = bnrm;
+  while (it < max_iter) {
+    if (it > 0) {
+      TRY(ops.dots({{r, r}}, true));
+      beta = sqrt(g_scratch.host[0].x);
+    }
+    std::fill(H.begin(), H.end(), cplx(0));
+    std::fill(g.begin(), g.end(), cplx(0));
+    g[0] = beta;
+    TRY(ops.lincomb(V, {{cplx(1.0 / beta), r}}, -1));
+    int j_done = 0;
+    bool est_ok = false;
+    for (int j = 0; j < m; ++j) {
+      double2* w = V + (size_t)n * (j + 1);
+      TRY(h2b_run_matvec(h, V + (size_t)n * j, w, 1, st));
+      ++it;
+      ++matvecs;
+      // CGS2: h1 = V^H w ; w -= V h1 ; h2 = V^H w ; w -= V h2 (+ ||w||^2)
+      k_basis_dots_partial<<<ops.nb, RT, 0, st>>>(V, n, j + 1, w, n, ops.partial);
+      k_reduce_partials<<<j + 1, 32, 0, st>>>(ops.partial, ops.nb, j + 1, hvals);
+      k_basis_sub<<<ops.nb, RT, 0, st>>>(V, n, j + 1, hvals, w, n, nullptr);
+      k_basis_dots_partial<<<ops.nb, RT, 0, st>>>(V, n, j + 1, w, n, ops.partial);
+      k_reduce_partials<<<j + 1, 32, 0, st>>>(ops.partial, ops.nb, j + 1, hvals + 64);
+      k_basis_sub<<<ops.nb, RT, 0, st>>>(V, n, j + 1, hvals + 64, w, n, ops.partial);
+      k_reduce_partials<<<1, 32, 0, st>>>(ops.partial, ops.nb, 1, hvals + 128);
+      H2B_CHECK_LAUNCH();
+      H2B_CUDA_TRY(cudaMemcpyAsync(g_scratch.host, hvals, sizeof(double2) * 129,
+                                   cudaMemcpyDeviceToHost, st));
+      H2B_CUDA_TRY(cudaStreamSynchronize(st));
+      std::vector<cplx> hc(j + 1);
+      for (int i = 0; i <= j; ++i)
+        hc[i] = cplx(g_scratch.host[i].x, g_scratch.host[i].y) +
+                cplx(g_scratch.host[64 + i].x, g_scratch.host[64 + i].y);
+      const double hn = sqrt(g_scratch.host[128].x);
+      for (int i = 0; i < j; ++i) {
+        const cplx a = hc[i], bb = hc[i + 1];
+        hc[i] = cs[i] * a + sn[i] * bb;
+        hc[i + 1] = -std::conj(sn[i]) * a + cs[i] * bb;
+      }
+      // Givens rotation zeroing hn below hc[j]
+      double c;
+      cplx s, rr;
+      if (hn == 0.0) {
+        c = 1.0; s = 0.0; rr = hc[j];
+      } else if (hc[j] == cplx(0)) {
+        c = 0.0; s = 1.0; rr = hn;
+      } else {
+        const double t = hypot(std::abs(hc[j]), hn);
+        const cplx ph = hc[j] / std::abs(hc[j]);
+        c = std::abs(hc[j]) / t;
+        s = ph * hn / t;
+        rr = ph * t;
+      }
+      cs[j] = c;
+      sn[j] = s;
+      for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = hc[i];
+      H[(size_t)j * m + j] = rr;
+      g[j + 1] = -std::conj(s) * g[j];
+      g[j] = c * g[j];
+      const double res = std::abs(g[j + 1]) / bnrm;
+      if (history && nh < max_iter) history[nh] = res;
+      ++nh;
+      j_done = j + 1;
+      if (res <= tol) {
+        est_ok = true;
+        break;
+      }
+      if (it >= max_iter || hn == 0.0) break;
+      TRY(ops.lincomb(w, {{cplx(1.0 / hn), w}}, -1));
+    }
+    (void)est_ok;
+    // back substitution, x += V y
+    for (int i = j_done - 1; i >= 0; --i) {
+      cplx acc = g[i];
+      for (int l = i + 1; l < j_done; ++l) acc -= H[(size_t)i * m + l] * y[l];
+      y[i] = acc / H[(size_t)i * m + i];
+    }
+    for (int i = 0; i < j_done; ++i) g_scratch.host[i] = make_double2(-y[i].real(), -y[i].imag());
+    H2B_CUDA_TRY(cudaMemcpyAsync(hvals, g_scratch.host, sizeof(double2) * j_done, cudaMemcpyHostToDevice, st));
+    k_basis_sub<<<ops.nb, RT, 0, st>>>(V, n, j_done, hvals, x, n, nullptr);
+    H2B_CHECK_LAUNCH();
+    // true residual r = b - A x
+    TRY(h2b_run_matvec(h, x, tmp, 1, st));
+    ++matvecs;
+    TRY(ops.lincomb(r, {{cplx(1.0), b}, {cplx(-1.0), tmp}}, 0));
+    TRY(ops.fetch_vals(1));
+    const double true_res = sqrt(g_scratch.host[0].x) / bnrm;
+    if (true_res <= tol) {
+      converged = true;
+      break;
+    }
+  }
+  report->iterations = it;
+  report->converged = converged ? 1 : 0;
+  report->n_history = nh < max_iter ? nh : max_iter;
+  report->matvecs = matvecs;
+  report->wall_time = now_s() - t0;
+  return H2B_OK;
+}
+
+// ===========================================================================
+// BiCGStab (arith.py:605-689)
+// ===========================================================================
+extern "C" int h2b_bicgstab(h2b_handle h, const void* b_perm, void* x_perm, double tol, int max_iter,
+                            const void* shadow_perm, const void* restart_noise_perm, double* history,
+                            h2b_report* report, void* stream) {
+  if (!h || !b_perm || !x_perm || !report) {
+    h2b_set_error("h2b_bicgstab: null argument");
+    return H2B_EINVAL;
+  }
+  if (!(tol > 0.0 && tol < 1.0)) {
+    h2b_set_error("tol must be in (0, 1)");
+    return H2B_EINVAL;
+  }
+  if (max_iter < 1) {
+    h2b_set_error("max_iter must be >= 1");
+    return H2B_EINVAL;
+  }
+  const double t0 = now_s();
+  TRY(scratch_ready());
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = h->n;
+  double2* ws = nullptr;
+  TRY(krylov_ws(h, sizeof(double2) * (size_t)n * 6, &ws));
+  double2 *r = ws, *rh = ws + n, *p = ws + 2 * n, *v = ws + 3 * n, *s = ws + 4 * n, *t = ws + 5 * n;
+  const double2* b = (const double2*)b_perm;
+  double2* x = (double2*)x_perm;
+  Ops ops{st, n, nblocks(n), g_scratch.partial, g_scratch.vals, g_scratch.host};
+  auto H = [&](int i) { return cplx(g_scratch.host[i].x, g_scratch.host[i].y); };
+  *report = h2b_report{0, 0, 0, 0, 0.0};
+
+  TRY(ops.dots({{b, b}}, true));
+  const double bnrm = sqrt(H(0).real());
+  H2B_CUDA_TRY(cudaMemsetAsync(x, 0, sizeof(double2) * n, st));
+  if (bnrm == 0.0) {
+    H2B_CUDA_TRY(cudaStreamSynchronize(st));
+    report->converged = 1;
+    report->wall_time = now_s() - t0;
+    return H2B_OK;
+  }
+  H2B_CUDA_TRY(cudaMemcpyAsync(r, b, sizeof(double2) * n, cudaMemcpyDeviceToDevice, st));
+  H2B_CUDA_TRY(cudaMemcpyAsync(rh, shadow_perm ? shadow_perm : b, sizeof(double2) * n,
+                               cudaMemcpyDeviceToDevice, st));
+  H2B_CUDA_TRY(cudaMemsetAsync(v, 0, sizeof(double2) * n, st));
+  H2B_CUDA_TRY(cudaMemsetAsync(p, 0, sizeof(double2) * n, st));
+  cplx rho = 1.0, alpha = 1.0, omega = 1.0;
+  bool converged = false, restarted = false, p_zero = true;
+  int it = 0, matvecs = 0, nh = 0;
+  const double eps = 2.220446049250313e-16;
+  const double breakdown = eps * eps;
+  while (it < max_iter) {
+    ++it;
+    TRY(ops.dots({{rh, r}}, true));
+    cplx rho_new = H(0);
+    if (std::abs(rho_new) < breakdown * std::max(1.0, bnrm * bnrm)) {
+      if (restarted || !restart_noise_perm) break;
+      TRY(ops.lincomb(rh, {{cplx(1.0), r}, {cplx(1.0), (const double2*)restart_noise_perm}}, -1));
+      rho = alpha = omega = 1.0;
+      H2B_CUDA_TRY(cudaMemsetAsync(v, 0, sizeof(double2) * n, st));
+      H2B_CUDA_TRY(cudaMemsetAsync(p, 0, sizeof(double2) * n, st));
+      p_zero = true;
+      restarted = true;
+      TRY(ops.dots({{rh, r}}, true));
+      rho_new = H(0);
+      if (std::abs(rho_new) < breakdown * std::max(1.0, bnrm * bnrm)) break;
+    }
+    if (it == 1 || p_zero) {
+      H2B_CUDA_TRY(cudaMemcpyAsync(p, r, sizeof(double2) * n, cudaMemcpyDeviceToDevice, st));
+      p_zero = false;
+    } else {
+      const cplx beta = (rho_new / rho) * (alpha / omega);
+      TRY(ops.lincomb(p, {{cplx(1.0), r}, {beta, p}, {-beta * omega, v}}, -1));
+    }
+    TRY(h2b_run_matvec(h, p, v, 1, st));
+    ++matvecs;
+    TRY(ops.dots({{rh, v}}, true));
+    const cplx denom = H(0);
+    if (denom == cplx(0)) break;
+    alpha = rho_new / denom;
+    TRY(ops.lincomb(s, {{cplx(1.0), r}, {-alpha, v}}, 0));
+    TRY(ops.fetch_vals(1));
+    const double s_nrm = sqrt(H(0).real());
+    if (s_nrm / bnrm <= tol) {
+      TRY(ops.lincomb(x, {{cplx(1.0), x}, {alpha, p}}, -1));
+      if (history && nh < max_iter) history[nh] = s_nrm / bnrm;
+      ++nh;
+      converged = true;
+      break;
+    }
+    TRY(h2b_run_matvec(h, s, t, 1, st));
+    ++matvecs;
+    TRY(ops.dots({{t, t}, {t, s}}, true));
+    const double tt = H(0).real();
+    if (tt == 0.0) break;
+    omega = H(1) / tt;
+    if (omega == cplx(0)) break;
+    TRY(ops.lincomb(x, {{cplx(1.0), x}, {alpha, p}, {omega, s}}, -1));
+    TRY(ops.lincomb(r, {{cplx(1.0), s}, {-omega, t}}, 0));
+    TRY(ops.fetch_vals(1));
+    rho = rho_new;
+    const double rel = sqrt(H(0).real()) / bnrm;
+    if (history && nh < max_iter) history[nh] = rel;
+    ++nh;
+    if (rel <= tol) {
+      converged = true;
+      break;
+    }
+    if (!std::isfinite(rel)) break;
+  }
+  H2B_CUDA_TRY(cudaStreamSynchronize(st));
+  report->iterations = it;
+  report->converged = converged ? 1 : 0;
+  report->n_history = nh < max_iter ? nh : max_iter;
+  report->matvecs = matvecs;
+  report->wall_time = now_s() - t0;
+  return H2B_OK;
+}

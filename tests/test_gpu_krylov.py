@@ -1,0 +1,72 @@
+"""GPU Krylov solvers: BiCGStab vs the reference's own runs, GMRES vs the oracle/scipy."""
+
+import numpy as np
+import pytest
+
+from conftest import load_config, load_golden, rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", ["rod164", "cube2"])
+@pytest.mark.parametrize("tag,tol", [("e3", 1e-3), ("e6", 1e-6)])
+def test_bicgstab_matches_reference_run(name, tag, tol):
+    from paper_1703_01175_b200 import bicgstab_solve
+    pk, ex = load_golden(name)
+    x, rep = bicgstab_solve(pk, ex["bicg_rhs"], tol=tol, max_iter=400)
+    assert rep.converged == bool(ex[f"bicg_{tag}_conv"])
+    assert abs(rep.iterations - int(ex[f"bicg_{tag}_iters"])) <= 1
+    assert rep.residual_history[-1] <= tol
+    assert rel(x, ex[f"bicg_{tag}_x"]) <= 1e-6
+
+
+def test_bicgstab_edge_cases():
+    from paper_1703_01175_b200 import bicgstab_solve
+    pk, ex = load_golden("rod164")
+    x, rep = bicgstab_solve(pk, np.zeros(pk.n), tol=1e-3)
+    assert rep.iterations == 0 and rep.converged and not np.any(x)
+    with pytest.raises(ValueError):
+        bicgstab_solve(pk, np.ones(pk.n), tol=0.0)
+    with pytest.raises(ValueError):
+        bicgstab_solve(pk, np.ones(pk.n), tol=1e-3, max_iter=0)
+    _, rep = bicgstab_solve(pk, np.ones(pk.n, dtype=complex), tol=1e-14, max_iter=1)
+    assert not rep.converged and rep.iterations == 1
+
+
+@pytest.mark.parametrize("name,restart", [("rod164", 30), ("cube2", 10), ("plate32", 20),
+                                          ("line2048", 30)])
+def test_gmres_matches_oracle(name, restart):
+    from oracle import h2_oracle as ho
+    from oracle import krylov_oracle as ko
+    from paper_1703_01175_b200 import gmres_solve
+    pk, ex = load_golden(name)
+    b = ex["x"][:, 0]
+    xo, ro = ko.gmres_solve(lambda v: ho.matvec(pk, v), b, tol=1e-8, restart=restart, max_iter=2000)
+    x, rep = gmres_solve(pk, b, tol=1e-8, restart=restart, max_iter=2000)
+    assert rep.converged and ro.converged
+    assert abs(rep.iterations - ro.iterations) <= 1
+    assert rel(x, xo) <= 1e-6
+    assert np.allclose(rep.residual_history[:10], ro.residual_history[:10], rtol=1e-6)
+
+
+def test_gmres_identity_and_zero():
+    from paper_1703_01175_b200 import gmres_solve
+    pk, ex = load_golden("identity")
+    b = ex["x"][:, 0]
+    x, rep = gmres_solve(pk, b, tol=1e-10, restart=5)
+    assert rep.converged and rep.iterations == 1 and np.allclose(x, b)
+    x, rep = gmres_solve(pk, np.zeros(pk.n), tol=1e-3)
+    assert rep.converged and rep.iterations == 0 and not np.any(x)
+
+
+def test_gmres_config1_iteration_count():
+    """BASELINE config 1: GMRES(30) to 1e-6 — 245 iterations on the CPU oracle (±1)."""
+    from paper_1703_01175_b200 import as_operator, gmres_solve
+    pk, ex = load_config(1)
+    b = ex["x"][:, 0]
+    x, rep = gmres_solve(as_operator(pk), b, tol=1e-6, restart=30, max_iter=2000)
+    assert rep.converged
+    assert abs(rep.iterations - int(ex["gmres_iters"])) <= 1
+    assert rel(x, ex["gmres_x"]) <= 1e-5
+    op = as_operator(pk)
+    assert np.linalg.norm(op.matvec(x) - b) / np.linalg.norm(b) <= 1e-6

@@ -1,0 +1,133 @@
+"""GPU parity of the H² matvec against the reference's own outputs (golden) and the oracle."""
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_NAMES, load_config, load_golden, rel
+
+pytestmark = pytest.mark.gpu
+
+
+def _op(name):
+    from paper_1703_01175_b200 import as_operator
+    pk, ex = load_golden(name)
+    return as_operator(pk), pk, ex
+
+
+@pytest.mark.parametrize("name", GOLDEN_NAMES)
+def test_matvec_matches_reference(name):
+    op, pk, ex = _op(name)
+    for j in range(ex["x"].shape[1]):
+        assert rel(op.matvec(ex["x"][:, j]), ex["y"][:, j]) <= 1e-12
+
+
+@pytest.mark.parametrize("name", GOLDEN_NAMES)
+def test_matmat_matches_reference(name):
+    from paper_1703_01175_b200 import matmat_apply
+    op, pk, ex = _op(name)
+    assert rel(matmat_apply(pk, ex["xm"]), ex["ym"]) <= 1e-12
+    assert rel(matmat_apply(pk, ex["xm"], col_block=2), ex["ym_cb2"]) <= 1e-12
+    # single column equals matvec (test_arith.py:64-68)
+    y1 = matmat_apply(pk, ex["x"][:, :1])[:, 0]
+    assert np.allclose(y1, op.matvec(ex["x"][:, 0]), atol=1e-14, rtol=0)
+
+
+@pytest.mark.parametrize("name", GOLDEN_NAMES)
+def test_matvec_matches_oracle(name):
+    from oracle import h2_oracle as ho
+    op, pk, ex = _op(name)
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal(pk.n) + 1j * rng.standard_normal(pk.n)
+    assert rel(op.matvec(x), ho.matvec(pk, x)) <= 1e-12
+
+
+def test_zero_maps_to_zero_exactly():
+    op, pk, ex = _op("rod164")
+    assert np.array_equal(op.matvec(np.zeros(pk.n)), np.zeros(pk.n))
+    assert np.array_equal(op.matmat(np.zeros((pk.n, 3))), np.zeros((pk.n, 3)))
+
+
+def test_identity_model_is_identity_exactly():
+    op, pk, ex = _op("identity")
+    x = ex["x"][:, 0]
+    assert np.array_equal(op.matvec(x), x)
+
+
+@pytest.mark.parametrize("name", ["rod164", "cube2"])
+def test_within_compression_tolerance_of_dense(name):
+    op, pk, ex = _op(name)
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        x = rng.standard_normal(pk.n) + 1j * rng.standard_normal(pk.n)
+        ref = ex["dense"] @ x
+        assert rel(op.matvec(x), ref) <= 10 * pk.meta["eps_acc"]
+
+
+def test_identity_columns_reconstruct_dense():
+    op, pk, ex = _op("rod164")
+    rec = op.matmat(np.eye(pk.n, dtype=complex))
+    assert rel(rec, ex["dense"]) <= 10 * pk.meta["eps_acc"]
+
+
+def test_linearity():
+    op, pk, ex = _op("rod164")
+    rng = np.random.default_rng(5)
+    x1 = rng.standard_normal(pk.n) + 1j * rng.standard_normal(pk.n)
+    x2 = rng.standard_normal(pk.n) + 1j * rng.standard_normal(pk.n)
+    lhs = op.matvec(2.0 * x1 + 3j * x2)
+    rhs = 2.0 * op.matvec(x1) + 3j * op.matvec(x2)
+    assert np.linalg.norm(lhs - rhs) <= 1e-12 * np.linalg.norm(lhs)
+
+
+def test_dimension_mismatch_rejected():
+    from paper_1703_01175_b200 import matmat_apply, matvec
+    op, pk, ex = _op("rod164")
+    with pytest.raises(ValueError):
+        matvec(pk, np.zeros(pk.n + 1))
+    with pytest.raises(ValueError):
+        matmat_apply(pk, np.zeros(pk.n))
+
+
+def test_inputs_not_mutated_and_deterministic():
+    op, pk, ex = _op("line2048")
+    x = ex["x"][:, 0].copy()
+    y1 = op.matvec(x)
+    y2 = op.matvec(x)
+    assert np.array_equal(x, ex["x"][:, 0])
+    assert np.array_equal(y1, y2)  # bitwise reproducible
+
+
+def test_device_perm_path_matches_host_path():
+    import torch
+    op, pk, ex = _op("plate32")
+    x = ex["x"][:, 0]
+    xp = torch.from_numpy(x[pk.perm].copy()).cuda()
+    yp = op.matvec_perm(xp).cpu().numpy()
+    y = np.empty_like(yp)
+    y[pk.perm] = yp
+    assert rel(y, ex["y"][:, 0]) <= 1e-12
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_baseline_config_matches_reference(k):
+    from paper_1703_01175_b200 import as_operator
+    pk, ex = load_config(k)
+    op = as_operator(pk)
+    for j in range(ex["x"].shape[1]):
+        assert rel(op.matvec(ex["x"][:, j]), ex["y"][:, j]) <= 1e-10
+    assert np.array_equal(pk.perm, ex["ref_perm"])
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_baseline_config_size_independent_properties(k):
+    """At full size: linearity, zero, and the multi-RHS path agreeing with single-RHS."""
+    from paper_1703_01175_b200 import as_operator
+    pk, ex = load_config(k)
+    op = as_operator(pk)
+    x1, x2 = ex["x"][:, 0], ex["x"][:, 1]
+    y1, y2 = op.matvec(x1), op.matvec(x2)
+    lhs = op.matvec(2.0 * x1 - 0.5j * x2)
+    assert np.linalg.norm(lhs - (2.0 * y1 - 0.5j * y2)) <= 1e-12 * np.linalg.norm(lhs)
+    Y = op.matmat(np.stack([x1, x2], 1))
+    assert rel(Y[:, 0], y1) <= 1e-13 and rel(Y[:, 1], y2) <= 1e-13
+    assert not np.any(op.matvec(np.zeros(pk.n)))
