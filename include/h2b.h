@@ -109,6 +109,25 @@ int h2b_matvec_perm(h2b_handle h, const void* x_perm, void* y_perm, int q, void*
  * scatter and device->host copy; synchronous. */
 int h2b_matvec_host(h2b_handle h, const void* x, void* y, int q);
 
+/* Profiling split of h2b_matvec_perm: phase 0 = near-field only (y overwritten,
+ * arith.py:100-104), phase 1 = far field only (y accumulated, arith.py:58-99). */
+int h2b_matvec_phase(h2b_handle h, int phase, const void* x_perm, void* y_perm, int q,
+                     void* stream);
+
+/* Run the one-time device preparation (transposes, panel index, schedule)
+ * now instead of at the first matvec. */
+int h2b_prepare_handle(h2b_handle h);
+
+#define H2B_OPT_GRAPHS 1      /* 1 (default): replay each matvec as a CUDA graph */
+int h2b_set_option(h2b_handle h, int option, int value);
+
+#define H2B_Q_LAUNCHES_Q1 1   /* kernels per single-RHS matvec */
+#define H2B_Q_SPAN_MODE 2     /* 1 if the q=1 far field uses staged subtree spans */
+#define H2B_Q_SPLIT_LEVEL 3   /* tree level at which spans are rooted */
+#define H2B_Q_TOP_STAGED 4    /* 1 if levels above the split run as one staged CTA */
+#define H2B_Q_DEVICE_BYTES 5
+int h2b_query(h2b_handle h, int what, int64_t* out);
+
 /* Permutation helpers on device buffers: out[i,:] = in[perm[i],:] (gather,
  * arith.py:113) and out[perm[i],:] = in[i,:] (scatter, arith.py:116). */
 int h2b_gather_perm(h2b_handle h, const void* in, void* out, int q, void* stream);

@@ -31,15 +31,20 @@ int upload_table(T** dst, const T* src, int64_t count, int64_t* acc) {
 }
 
 void free_ctx(h2b_ctx* h) {
-  void* ptrs[] = {h->c_start, h->c_size_d, h->c_rank_d, h->c_lo,   h->c_hi,   h->c_parent,
-                  h->c_xoff,  h->c_voff,   h->c_toff,   h->s_row_ptr, h->s_off, h->d_row_ptr,
-                  h->d_off,   h->s_col,    h->d_col,    h->perm,   h->leaves, h->xhat,
-                  h->yhat,    h->kry,      h->buf[0],   h->buf[1], h->buf[2], h->buf[3],
-                  h->hxp,     h->hyp};
+  h2b_release_graphs(h);
+  void* ptrs[] = {h->c_start_d, h->c_size_d, h->c_rank_d, h->c_lo,      h->c_hi,
+                  h->c_parent,  h->c_xoff_d, h->c_voff_d, h->c_toff_d,  h->s_row_ptr_d,
+                  h->s_off_d,   h->d_row_ptr_d, h->d_off_d, h->s_col_d, h->d_col_d,
+                  h->perm,      h->leaves,   h->xhat,     h->yhat,      h->kry,
+                  h->buf[0],    h->buf[1],   h->buf[2],   h->buf[3],    h->hxp,
+                  h->hyp,       h->vT,       h->tT,       h->s_prow,    h->s_xcol,
+                  h->couple_targets, h->span_heads, h->span_copies, h->span_outs,
+                  h->span_ops, h->near_items, h->near_blks, h->couple_items};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  if (h->hx) cudaFreeHost(h->hx);
-  if (h->hy) cudaFreeHost(h->hy);
+  if (h->far_stream) cudaStreamDestroy(h->far_stream);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   delete h;
 }
 
@@ -96,6 +101,17 @@ int h2b_create(const h2b_layout* L, int device, h2b_handle* out) {
   h->c_rank.assign(L->c_rank, L->c_rank + P);
   h->c_child_lo.assign(L->c_child_lo, L->c_child_lo + P);
   h->c_size.assign(L->c_size, L->c_size + P);
+  h->c_child_hi.assign(L->c_child_hi, L->c_child_hi + P);
+  h->c_start.assign(L->c_start, L->c_start + P);
+  h->c_xoff.assign(L->c_xhat_off, L->c_xhat_off + P + 1);
+  h->c_voff.assign(L->c_v_off, L->c_v_off + P);
+  h->c_toff.assign(L->c_t_off, L->c_t_off + P);
+  h->s_row_ptr.assign(L->s_row_ptr, L->s_row_ptr + P + 1);
+  h->s_off.assign(L->s_off, L->s_off + L->n_coupling);
+  h->s_col.assign(L->s_col, L->s_col + L->n_coupling);
+  h->d_row_ptr.assign(L->d_row_ptr, L->d_row_ptr + P + 1);
+  h->d_off.assign(L->d_off, L->d_off + L->n_near);
+  h->d_col.assign(L->d_col, L->d_col + L->n_near);
   if (h->level_ptr[0] != 0 || h->level_ptr[h->depth] != P) {
     delete h;
     h2b_set_error("h2b_create: level_ptr does not cover the clusters");
@@ -128,21 +144,21 @@ int h2b_create(const h2b_layout* L, int device, h2b_handle* out) {
   int rc = H2B_OK;
 #define UP(dst, src, cnt) \
   if (!rc) rc = upload_table(&h->dst, src, cnt, &acc)
-  UP(c_start, L->c_start, P);
+  UP(c_start_d, L->c_start, P);
   UP(c_size_d, L->c_size, P);
   UP(c_rank_d, L->c_rank, P);
   UP(c_lo, L->c_child_lo, P);
   UP(c_hi, L->c_child_hi, P);
   UP(c_parent, L->c_parent, P);
-  UP(c_xoff, L->c_xhat_off, P + 1);
-  UP(c_voff, L->c_v_off, P);
-  UP(c_toff, L->c_t_off, P);
-  UP(s_row_ptr, L->s_row_ptr, P + 1);
-  UP(s_col, L->s_col, L->n_coupling);
-  UP(s_off, L->s_off, L->n_coupling);
-  UP(d_row_ptr, L->d_row_ptr, P + 1);
-  UP(d_col, L->d_col, L->n_near);
-  UP(d_off, L->d_off, L->n_near);
+  UP(c_xoff_d, L->c_xhat_off, P + 1);
+  UP(c_voff_d, L->c_v_off, P);
+  UP(c_toff_d, L->c_t_off, P);
+  UP(s_row_ptr_d, L->s_row_ptr, P + 1);
+  UP(s_col_d, L->s_col, L->n_coupling);
+  UP(s_off_d, L->s_off, L->n_coupling);
+  UP(d_row_ptr_d, L->d_row_ptr, P + 1);
+  UP(d_col_d, L->d_col, L->n_near);
+  UP(d_off_d, L->d_off, L->n_near);
   UP(perm, L->perm, L->n);
   UP(leaves, h->h_leaves.data(), (int64_t)h->h_leaves.size());
 #undef UP
@@ -166,6 +182,7 @@ int h2b_create(const h2b_layout* L, int device, h2b_handle* out) {
 
 int h2b_upload(h2b_handle h, int sec, const void* src, size_t bytes, size_t offset) {
   REQUIRE(h, H2B_EINVAL, "null handle");
+  REQUIRE(!h->prepared, H2B_ESTATE, "h2b_upload: payload is immutable after the first matvec");
   REQUIRE(sec >= 0 && sec < 4, H2B_EINVAL, "h2b_upload: bad section");
   REQUIRE(bytes % 16 == 0 && offset % 16 == 0, H2B_EINVAL, "h2b_upload: unaligned size/offset");
   REQUIRE((int64_t)((offset + bytes) / 16) <= h->sec_elems[sec], H2B_EINVAL,
@@ -225,6 +242,47 @@ int h2b_matvec_host(h2b_handle h, const void* x, void* y, int q) {
   H2B_CUDA_TRY(cudaMemcpyAsync(y, dy, bytes, cudaMemcpyDeviceToHost, st));
   H2B_CUDA_TRY(cudaStreamSynchronize(st));
   return H2B_OK;
+}
+
+int h2b_matvec_phase(h2b_handle h, int phase, const void* x_perm, void* y_perm, int q,
+                     void* stream) {
+  int rc = ready(h);
+  if (rc) return rc;
+  REQUIRE(q >= 1 && (phase == 0 || phase == 1), H2B_EINVAL, "h2b_matvec_phase: bad phase/q");
+  REQUIRE(x_perm && y_perm && x_perm != y_perm, H2B_EINVAL, "h2b_matvec_phase: bad buffers");
+  return h2b_run_phase(h, phase, (const double2*)x_perm, (double2*)y_perm, q, (cudaStream_t)stream);
+}
+
+int h2b_prepare_handle(h2b_handle h) {
+  int rc = ready(h);
+  if (rc) return rc;
+  H2B_CUDA_TRY(cudaSetDevice(h->device));
+  return h2b_prepare(h);
+}
+
+int h2b_set_option(h2b_handle h, int option, int value) {
+  REQUIRE(h, H2B_EINVAL, "null handle");
+  if (option == H2B_OPT_GRAPHS) {
+    h->use_graphs = value ? 1 : 0;
+    h2b_release_graphs(h);
+    return H2B_OK;
+  }
+  h2b_set_error("h2b_set_option: unknown option");
+  return H2B_EINVAL;
+}
+
+int h2b_query(h2b_handle h, int what, int64_t* out) {
+  REQUIRE(h && out, H2B_EINVAL, "h2b_query: null argument");
+  switch (what) {
+    case H2B_Q_LAUNCHES_Q1: *out = h->launches_q1; return H2B_OK;
+    case H2B_Q_SPAN_MODE: *out = h->span_mode; return H2B_OK;
+    case H2B_Q_SPLIT_LEVEL: *out = h->ls; return H2B_OK;
+    case H2B_Q_TOP_STAGED: *out = h->top_staged; return H2B_OK;
+    case H2B_Q_DEVICE_BYTES: *out = h->device_bytes; return H2B_OK;
+    default: break;
+  }
+  h2b_set_error("h2b_query: unknown key");
+  return H2B_EINVAL;
 }
 
 int h2b_gather_perm(h2b_handle h, const void* in, void* out, int q, void* stream) {

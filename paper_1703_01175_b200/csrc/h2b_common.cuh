@@ -4,7 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/h2b.h"
@@ -18,15 +20,32 @@ void h2b_set_error(const std::string& msg);
   do {                                                                              \
     cudaError_t _e = (expr);                                                        \
     if (_e != cudaSuccess) {                                                        \
+      cudaGetLastError(); /* do not leave a non-sticky error for the next check */   \
       h2b_set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));            \
       return _e == cudaErrorMemoryAllocation ? H2B_ENOMEM : H2B_ECUDA;              \
     }                                                                               \
   } while (0)
 
-#define H2B_CHECK_LAUNCH() H2B_CUDA_TRY(cudaGetLastError())
+#define H2B_STR2(x) #x
+#define H2B_STR(x) H2B_STR2(x)
+#define H2B_CHECK_LAUNCH()                                                          \
+  do {                                                                              \
+    cudaError_t _e = cudaGetLastError();                                            \
+    if (_e != cudaSuccess) {                                                        \
+      h2b_set_error(std::string("kernel launch at " __FILE__ ":" H2B_STR(__LINE__) ": ") + \
+                    cudaGetErrorString(_e));                                        \
+      return H2B_ECUDA;                                                             \
+    }                                                                               \
+  } while (0)
+
+#define H2B_TRY(x)        \
+  do {                    \
+    int _rc = (x);        \
+    if (_rc) return _rc;  \
+  } while (0)
 
 // ---------------------------------------------------------------------------
-// complex128 arithmetic on interleaved double2 (no fast-math, exact FMA order)
+// complex128 arithmetic on interleaved double2 (no fast-math)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 
@@ -78,8 +97,63 @@ __device__ __forceinline__ cd2 ld_cached256(const double2* p) {
 }
 
 // ---------------------------------------------------------------------------
+// span programs: a span is a piece of the cluster tree (a subtree below the
+// split level, the levels above it, or a single cluster) processed by ONE CTA
+// entirely in shared memory.  The host resolves everything at prepare time
+// into three descriptor lists per span: bulk copies global->smem (payload,
+// inputs and the op list itself), ops (small panel GEMVs on smem offsets,
+// grouped into levels separated by __syncthreads) and copies smem->global.
+// ---------------------------------------------------------------------------
+enum SpanSrc : int32_t { SRC_V = 0, SRC_T, SRC_VT, SRC_TT, SRC_X, SRC_XHAT, SRC_YHAT, SRC_OPS, SRC_N };
+struct SpanCopy {        // global (base[kind] + src) <-> smem[smem], elems double2
+  int64_t src;
+  int32_t kind, elems, smem, pad;
+};
+struct SpanOp {          // out[c] (+)= sum_r P[r*w+c] in[r], c < w, r < R
+  int32_t pay, in, out, R, w, flags, pad0, pad1;
+};
+constexpr int OP_ACC = 1;       // accumulate into out
+constexpr int OP_OUT_Y = 2;     // out is an element offset into global y, not smem
+constexpr int SPAN_MAXLEV = 24;
+struct SpanHead {
+  int32_t copy_first, n_copy, out_first, n_out;
+  int32_t ops_smem, n_ops, smem_elems, nlev;
+  int32_t lvl[SPAN_MAXLEV + 1];  // op boundaries of each level, execution order
+  int32_t pad[3];
+};
+struct SpanLaunch {      // one kernel launch of the far-field chain
+  int32_t head_first, n_heads, smem_elems, big;  // big: 1024-thread CTA
+  int32_t level;         // >= 0: per-level fallback kernel for this level instead
+};
+
+// near-field work lists (q = 1 fast path)
+struct NearItem {        // one CTA: RB rows of one target leaf
+  int64_t y_off;         // first permuted row written by the CTA
+  int32_t b_first, nb;   // partner-block range in the NearBlk list (shared by the leaf's items)
+  int32_t row0, pad;     // first row of the item within the leaf
+};
+struct NearBlk {
+  int64_t d_off;         // element offset of the partner block D_{t,s}
+  int64_t x_off;         // first permuted column of the partner leaf
+};
+// coupling work list
+struct CoupleItem {
+  int64_t panel;         // element offset of the target's S^T panel (R x w)
+  int64_t xcol;          // offset into s_xcol of the panel's first row
+  int64_t out;           // x̂/ŷ offset of the target
+  int32_t R, w;
+};
+
+// ---------------------------------------------------------------------------
 // handle
 // ---------------------------------------------------------------------------
+struct GraphKey {
+  const void* x;
+  void* y;
+  int q;
+  bool operator<(const GraphKey& o) const { return std::tie(x, y, q) < std::tie(o.x, o.y, o.q); }
+};
+
 struct h2b_ctx {
   int device = 0;
   int64_t n = 0;
@@ -89,40 +163,106 @@ struct h2b_ctx {
   int64_t n_coupling = 0, n_near = 0;
   int64_t sec_elems[4] = {0, 0, 0, 0};
   int64_t sec_uploaded[4] = {0, 0, 0, 0};
-  int uniform_leaf = 0;  // leaf size if all leaves share it, else 0
+  bool prepared = false;  // device-side transposes / tables done
+  int uniform_leaf = 0;   // leaf size if all leaves share it, else 0
 
-  // host copies of the tables (scheduling decisions)
-  std::vector<int32_t> level_ptr, c_rank, c_child_lo, c_size;
+  // host copies of the tables
+  std::vector<int32_t> level_ptr, c_rank, c_child_lo, c_child_hi, c_size, c_start;
+  std::vector<int64_t> c_xoff, c_voff, c_toff, s_row_ptr, s_off, d_row_ptr;
+  std::vector<int32_t> s_col, d_col;
+  std::vector<int64_t> d_off;
   std::vector<int32_t> up_levels;    // levels with any k>0 cluster (deepest first)
   std::vector<int32_t> down_levels;  // levels with any non-leaf k>0 cluster (root first)
   std::vector<int32_t> h_leaves;
 
   // device tables
-  int32_t *c_start = nullptr, *c_size_d = nullptr, *c_rank_d = nullptr, *c_lo = nullptr,
+  int32_t *c_start_d = nullptr, *c_size_d = nullptr, *c_rank_d = nullptr, *c_lo = nullptr,
           *c_hi = nullptr, *c_parent = nullptr;
-  int64_t *c_xoff = nullptr, *c_voff = nullptr, *c_toff = nullptr;
-  int64_t *s_row_ptr = nullptr, *s_off = nullptr, *d_row_ptr = nullptr, *d_off = nullptr;
-  int32_t *s_col = nullptr, *d_col = nullptr;
+  int64_t *c_xoff_d = nullptr, *c_voff_d = nullptr, *c_toff_d = nullptr;
+  int64_t *s_row_ptr_d = nullptr, *s_off_d = nullptr, *d_row_ptr_d = nullptr, *d_off_d = nullptr;
+  int64_t* s_prow = nullptr;  // [P] first coupling-panel row of each target
+  int32_t* s_xcol = nullptr;  // [panel rows] x̂ index feeding each panel row
+  int32_t *s_col_d = nullptr, *d_col_d = nullptr;
   int64_t* perm = nullptr;
   int32_t* leaves = nullptr;
   int n_leaves = 0;
-  // payloads
+  int32_t* couple_targets = nullptr;  // clusters with k > 0
+  int n_couple_targets = 0;
+  // payloads: V, T, Sᵀ (transposed in place), D ; plus transposed copies Vᵀ, Tᵀ
   double2* buf[4] = {nullptr, nullptr, nullptr, nullptr};
+  double2 *vT = nullptr, *tT = nullptr;
+  // q = 1 far-field programs
+  int span_mode = 0;  // 0: per-level kernels only, 1: span programs
+  int ls = 0, top_staged = 0;
+  std::vector<SpanLaunch> up_prog, down_prog_head, down_prog_tail;
+  SpanHead* span_heads = nullptr;
+  SpanCopy* span_copies = nullptr;
+  SpanCopy* span_outs = nullptr;
+  SpanOp* span_ops = nullptr;
+  // near / coupling work lists
+  NearItem* near_items = nullptr;
+  NearBlk* near_blks = nullptr;
+  int n_near_items = 0, near_rb = 0;
+  CoupleItem* couple_items = nullptr;
+  int n_couple_items = 0, couple_warp_mode = 0;
   // workspace (grown on demand, per q)
   double2 *xhat = nullptr, *yhat = nullptr;
   int64_t ws_q = 0;
-  double2 *hx = nullptr, *hy = nullptr, *hxp = nullptr, *hyp = nullptr;  // host-path staging
+  double2 *hxp = nullptr, *hyp = nullptr;  // host-path staging
   int64_t hws_q = 0;
+  // streams / events / graphs
+  cudaStream_t far_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  int use_graphs = 1;
   // krylov workspace
   void* kry = nullptr;
   size_t kry_bytes = 0;
   int64_t device_bytes = 0;
+  int launches_q1 = 0;  // kernels per q=1 matvec (reported to the bench)
 };
 
 // implemented in h2b_matvec.cu
+int h2b_prepare(h2b_ctx* h);
 int h2b_ensure_workspace(h2b_ctx* h, int q);
 int h2b_run_matvec(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st);
+int h2b_run_phase(h2b_ctx* h, int phase, const double2* xp, double2* yp, int q, cudaStream_t st);
 int h2b_launch_gather(const int64_t* perm, int64_t n, const double2* in, double2* out, int q,
                       cudaStream_t st);
 int h2b_launch_scatter(const int64_t* perm, int64_t n, const double2* in, double2* out, int q,
                        cudaStream_t st);
+void h2b_release_graphs(h2b_ctx* h);
+
+// ---------------------------------------------------------------------------
+// Blackwell async bulk copy (TMA 1-D, cp.async.bulk) + mbarrier helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase), "r"(0x989680u)
+      : "memory");
+}
+// global -> shared bulk copy completing on `bar` (bytes % 16 == 0, 16-B aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}

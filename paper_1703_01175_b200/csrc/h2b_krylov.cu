@@ -346,7 +346,7 @@ extern "C" int h2b_gmres(h2b_handle h, const void* b_perm, void* x_perm, int res
     g[0] = beta;
     TRY(ops.lincomb(V, {{cplx(1.0 / beta), r}}, -1));
     int j_done = 0;
-    bool est_ok = false;
+  
     for (int j = 0; j < m; ++j) {
       double2* w = V + (size_t)n * (j + 1);
       TRY(h2b_run_matvec(h, V + (size_t)n * j, w, 1, st));
@@ -399,13 +399,13 @@ extern "C" int h2b_gmres(h2b_handle h, const void* b_perm, void* x_perm, int res
       ++nh;
       j_done = j + 1;
       if (res <= tol) {
-        est_ok = true;
+
         break;
       }
       if (it >= max_iter || hn == 0.0) break;
       TRY(ops.lincomb(w, {{cplx(1.0 / hn), w}}, -1));
     }
-    (void)est_ok;
+
     // back substitution, x += V y
     for (int i = j_done - 1; i >= 0; --i) {
       cplx acc = g[i];

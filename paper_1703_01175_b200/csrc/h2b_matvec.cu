@@ -1,248 +1,24 @@
-// H² matvec kernels for sm_100a (B200).
+// Orchestration of one H² matvec on sm_100a (B200): y_perm = S x_perm.
 //
-// Restates the four phases of the reference `_apply_perm`
-// (/root/reference/pkg/src/h2vie/arith.py:52-104) on the level-packed layout
-// (paper_1703_01175_b200/pack.py):
-//   (1) forward  x̂_c = V_cᵀ x_c (leaves), x̂_t = T_loᵀ x̂_lo + T_hiᵀ x̂_hi   arith.py:58-71
-//   (2) coupling ŷ_t = Σ_s S^{t,s} x̂_s                                      arith.py:72-81
-//   (3) backward ŷ_child += T_child ŷ_t ; y_c += V_c ŷ_c (leaves)           arith.py:82-99
-//   (4) near     y_t += Σ_s D_{t,s} x_s                                      arith.py:100-104
-// Plain transpose (not conjugate) in (1), as in the reference (arith.py:10-12).
-//
-// Execution plan: the near-field (the byte-dominant phase) runs on the
-// caller's stream and overwrites y; the far-field chain (1)-(3) runs on a
-// forked stream concurrently and the leaf back-transform joins it (it adds
-// into y after the near-field finished).
+// Restates the reference `_apply_perm` (/root/reference/pkg/src/h2vie/
+// arith.py:52-104).  The near-field phase (h2b_near.cu, byte-dominant) runs
+// on the caller's stream and overwrites y; the far field (h2b_far.cu) runs
+// concurrently on a high-priority side stream; the last far-field launch,
+// which adds the leaf back-transform into y, runs after both joined.  The
+// whole sequence is captured once per (x, y, q) into a CUDA graph and
+// replayed, so a matvec costs one graph launch on the host.
 #include <algorithm>
 
 #include "h2b_common.cuh"
 
+int h2b_launch_near(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st);
+int h2b_launch_span(h2b_ctx* h, const SpanLaunch& L, bool up, const double2* xp, double2* yp, int q,
+                    cudaStream_t st);
+int h2b_launch_coupling(h2b_ctx* h, int q, cudaStream_t st);
+int h2b_launch_far_levels_head(h2b_ctx* h, const double2* xp, int q, cudaStream_t st, int* nl);
+int h2b_launch_leaf_back(h2b_ctx* h, double2* yp, int q, cudaStream_t st);
+
 namespace {
-
-constexpr int NT = 256;  // threads per CTA for all matvec kernels
-constexpr int NWARP = NT / 32;
-
-// ---------------------------------------------------------------------------
-// near-field, q = 1, uniform leaf size NS (32 or 64): each lane streams
-// 32-byte chunks (2 complex) of the contiguous row panel of its target leaf;
-// partial sums stay in registers across all partner blocks and are reduced
-// across the LPR lanes of a row once at the end.
-// ---------------------------------------------------------------------------
-template <int NS>
-__global__ void __launch_bounds__(NT) k_near_q1(const int32_t* __restrict__ leaves,
-                                                 const int32_t* __restrict__ c_start,
-                                                 const int64_t* __restrict__ d_row_ptr,
-                                                 const int32_t* __restrict__ d_col,
-                                                 const int64_t* __restrict__ d_off,
-                                                 const double2* __restrict__ dbuf,
-                                                 const double2* __restrict__ x,
-                                                 double2* __restrict__ y) {
-  constexpr int LPR = NS / 2;          // lanes per row
-  constexpr int RPW = 32 / LPR;        // rows per warp instruction
-  constexpr int RSTEP = NWARP * RPW;   // row stride between a thread's rows
-  constexpr int R = NS / RSTEP;        // rows per thread
-  const int t = leaves[blockIdx.x];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int col = (lane % LPR) * 2;
-  const int row0 = warp * RPW + lane / LPR;
-  double2 acc[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) acc[r] = make_double2(0.0, 0.0);
-  const int64_t b0 = d_row_ptr[t], b1 = d_row_ptr[t + 1];
-#pragma unroll 2
-  for (int64_t b = b0; b < b1; ++b) {
-    const double2* D = dbuf + d_off[b] + (int64_t)row0 * NS + col;
-    const cd2 xv = ld_cached256(x + c_start[d_col[b]] + col);
-    cd2 dv[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) dv[r] = ld_stream256(D + (int64_t)r * RSTEP * NS);
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      cfma(acc[r], dv[r].a, xv.a);
-      cfma(acc[r], dv[r].b, xv.b);
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-#pragma unroll
-    for (int m = LPR / 2; m > 0; m >>= 1) acc[r] = cadd(acc[r], shfl_xor2(acc[r], m));
-  }
-  if ((lane % LPR) == 0) {
-    double2* yt = y + c_start[t] + row0;
-#pragma unroll
-    for (int r = 0; r < R; ++r) yt[r * RSTEP] = acc[r];
-  }
-}
-
-// near-field, any sizes, any q: warp per (row, column)
-__global__ void __launch_bounds__(NT) k_near_generic(const int32_t* __restrict__ leaves,
-                                                      const int32_t* __restrict__ c_start,
-                                                      const int32_t* __restrict__ c_size,
-                                                      const int64_t* __restrict__ d_row_ptr,
-                                                      const int32_t* __restrict__ d_col,
-                                                      const int64_t* __restrict__ d_off,
-                                                      const double2* __restrict__ dbuf,
-                                                      const double2* __restrict__ x,
-                                                      double2* __restrict__ y, int q) {
-  const int t = leaves[blockIdx.x];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nt = c_size[t];
-  const int64_t t0 = c_start[t];
-  const int64_t b0 = d_row_ptr[t], b1 = d_row_ptr[t + 1];
-  for (int i = warp; i < nt; i += NWARP) {
-    for (int c = 0; c < q; ++c) {
-      double2 acc = make_double2(0.0, 0.0);
-      for (int64_t b = b0; b < b1; ++b) {
-        const int s = d_col[b];
-        const int ns = c_size[s];
-        const int64_t s0 = c_start[s];
-        const double2* D = dbuf + d_off[b] + (int64_t)i * ns;
-        for (int j = lane; j < ns; j += 32) cfma(acc, D[j], x[(s0 + j) * q + c]);
-      }
-      acc = warp_sum2(acc);
-      if (lane == 0) y[(t0 + i) * q + c] = acc;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// small dense products used by the far field (CTA-cooperative)
-// ---------------------------------------------------------------------------
-// out[j*q+c] = Σ_i A[i*k+j] in[i*q+c]   (A row-major m x k; "Aᵀ in")
-__device__ void cta_coldot(const double2* __restrict__ A, int m, int k,
-                           const double2* __restrict__ in, int q, double2* __restrict__ out,
-                           double2* smem) {
-  const int tid = threadIdx.x;
-  if (k <= NT) {
-    const int G = NT / k;
-    const int g = tid / k, j = tid % k;
-    for (int c = 0; c < q; ++c) {
-      double2 acc = make_double2(0.0, 0.0);
-      if (g < G)
-        for (int i = g; i < m; i += G) cfma(acc, A[(int64_t)i * k + j], in[(int64_t)i * q + c]);
-      if (g < G) smem[g * k + j] = acc;
-      __syncthreads();
-      for (int jj = tid; jj < k; jj += NT) {
-        double2 s = smem[jj];
-        for (int gg = 1; gg < G; ++gg) s = cadd(s, smem[gg * k + jj]);
-        out[(int64_t)jj * q + c] = s;
-      }
-      __syncthreads();
-    }
-  } else {
-    for (int j = tid; j < k; j += NT)
-      for (int c = 0; c < q; ++c) {
-        double2 acc = make_double2(0.0, 0.0);
-        for (int i = 0; i < m; ++i) cfma(acc, A[(int64_t)i * k + j], in[(int64_t)i * q + c]);
-        out[(int64_t)j * q + c] = acc;
-      }
-  }
-}
-
-// out[i*q+c] += Σ_j A[i*k+j] in[j*q+c]   (A row-major m x k; warp per row)
-__device__ void cta_rowdot_acc(const double2* __restrict__ A, int m, int k,
-                               const double2* __restrict__ in, int q, double2* __restrict__ out) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = warp; i < m; i += NWARP)
-    for (int c = 0; c < q; ++c) {
-      double2 acc = make_double2(0.0, 0.0);
-      for (int j = lane; j < k; j += 32) cfma(acc, A[(int64_t)i * k + j], in[(int64_t)j * q + c]);
-      acc = warp_sum2(acc);
-      if (lane == 0) out[(int64_t)i * q + c] = cadd(out[(int64_t)i * q + c], acc);
-    }
-}
-
-// (1) forward transform of one level: leaves V_cᵀ x_c, non-leaves [T_lo;T_hi]ᵀ [x̂_lo;x̂_hi]
-// (children are adjacent in their level list, so x̂_lo, x̂_hi are contiguous)
-__global__ void __launch_bounds__(NT) k_up_level(int p_begin, const int32_t* __restrict__ c_start,
-                                                 const int32_t* __restrict__ c_size,
-                                                 const int32_t* __restrict__ c_rank,
-                                                 const int32_t* __restrict__ c_lo,
-                                                 const int32_t* __restrict__ c_hi,
-                                                 const int64_t* __restrict__ c_xoff,
-                                                 const int64_t* __restrict__ c_voff,
-                                                 const int64_t* __restrict__ c_toff,
-                                                 const double2* __restrict__ vbuf,
-                                                 const double2* __restrict__ tbuf,
-                                                 const double2* __restrict__ x, double2* xhat,
-                                                 int q) {
-  __shared__ double2 smem[NT];
-  const int p = p_begin + blockIdx.x;
-  const int k = c_rank[p];
-  if (k == 0) return;
-  const int lo = c_lo[p];
-  if (lo < 0) {
-    cta_coldot(vbuf + c_voff[p], c_size[p], k, x + (int64_t)c_start[p] * q, q,
-               xhat + c_xoff[p] * q, smem);
-  } else {
-    const int m = c_rank[lo] + c_rank[c_hi[p]];
-    cta_coldot(tbuf + c_toff[p], m, k, xhat + c_xoff[lo] * q, q, xhat + c_xoff[p] * q, smem);
-  }
-}
-
-// (2) coupling: ŷ_t = Σ_b S_b x̂_{s_b}, overwrite (zeros when no block)
-__global__ void __launch_bounds__(NT) k_coupling(const int32_t* __restrict__ c_rank,
-                                                 const int64_t* __restrict__ c_xoff,
-                                                 const int64_t* __restrict__ s_row_ptr,
-                                                 const int32_t* __restrict__ s_col,
-                                                 const int64_t* __restrict__ s_off,
-                                                 const double2* __restrict__ sbuf,
-                                                 const double2* __restrict__ xhat,
-                                                 double2* __restrict__ yhat, int q) {
-  const int t = blockIdx.x;
-  const int kt = c_rank[t];
-  if (kt == 0) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t b0 = s_row_ptr[t], b1 = s_row_ptr[t + 1];
-  double2* yt = yhat + c_xoff[t] * q;
-  for (int i = warp; i < kt; i += NWARP)
-    for (int c = 0; c < q; ++c) {
-      double2 acc = make_double2(0.0, 0.0);
-      for (int64_t b = b0; b < b1; ++b) {
-        const int s = s_col[b];
-        const int ks = c_rank[s];
-        const double2* S = sbuf + s_off[b] + (int64_t)i * ks;
-        const double2* xs = xhat + c_xoff[s] * q;
-        for (int j = lane; j < ks; j += 32) cfma(acc, S[j], xs[(int64_t)j * q + c]);
-      }
-      acc = warp_sum2(acc);
-      if (lane == 0) yt[(int64_t)i * q + c] = acc;
-    }
-}
-
-// (3a) backward transfer of one level: [ŷ_lo;ŷ_hi] += [T_lo;T_hi] ŷ_p
-__global__ void __launch_bounds__(NT) k_down_level(int p_begin, const int32_t* __restrict__ c_rank,
-                                                   const int32_t* __restrict__ c_lo,
-                                                   const int32_t* __restrict__ c_hi,
-                                                   const int64_t* __restrict__ c_xoff,
-                                                   const int64_t* __restrict__ c_toff,
-                                                   const double2* __restrict__ tbuf,
-                                                   double2* yhat, int q) {
-  const int p = p_begin + blockIdx.x;
-  const int k = c_rank[p];
-  const int lo = c_lo[p];
-  if (k == 0 || lo < 0) return;
-  const int m = c_rank[lo] + c_rank[c_hi[p]];
-  if (m == 0) return;
-  cta_rowdot_acc(tbuf + c_toff[p], m, k, yhat + c_xoff[p] * q, q, yhat + c_xoff[lo] * q);
-}
-
-// (3b) leaf back-transform: y_c += V_c ŷ_c
-__global__ void __launch_bounds__(NT) k_leaf_back(const int32_t* __restrict__ leaves,
-                                                  const int32_t* __restrict__ c_start,
-                                                  const int32_t* __restrict__ c_size,
-                                                  const int32_t* __restrict__ c_rank,
-                                                  const int64_t* __restrict__ c_xoff,
-                                                  const int64_t* __restrict__ c_voff,
-                                                  const double2* __restrict__ vbuf,
-                                                  const double2* __restrict__ yhat, double2* y,
-                                                  int q) {
-  const int p = leaves[blockIdx.x];
-  const int k = c_rank[p];
-  if (k == 0) return;
-  cta_rowdot_acc(vbuf + c_voff[p], c_size[p], k, yhat + c_xoff[p] * q, q,
-                 y + (int64_t)c_start[p] * q);
-}
 
 __global__ void k_gather(const int64_t* __restrict__ perm, int64_t n, const double2* __restrict__ in,
                          double2* __restrict__ out, int q) {
@@ -269,6 +45,56 @@ int grid_for(int64_t tot) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
 }
 
+bool use_programs(const h2b_ctx* h, int q) { return q == 1 && h->span_mode == 1; }
+
+// far field up to the join (everything that does not write y)
+int launch_far_head(h2b_ctx* h, const double2* xp, int q, cudaStream_t st, int* nl) {
+  if (!use_programs(h, q)) return h2b_launch_far_levels_head(h, xp, q, st, nl);
+  for (const SpanLaunch& L : h->up_prog) {
+    H2B_TRY(h2b_launch_span(h, L, true, xp, nullptr, q, st));
+    ++*nl;
+  }
+  H2B_TRY(h2b_launch_coupling(h, q, st));
+  ++*nl;
+  for (const SpanLaunch& L : h->down_prog_head) {
+    H2B_TRY(h2b_launch_span(h, L, false, xp, nullptr, q, st));
+    ++*nl;
+  }
+  return H2B_OK;
+}
+
+// far field after the join (adds into y)
+int launch_far_tail(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st, int* nl) {
+  if (!use_programs(h, q)) {
+    H2B_TRY(h2b_launch_leaf_back(h, yp, q, st));
+    ++*nl;
+    return H2B_OK;
+  }
+  for (const SpanLaunch& L : h->down_prog_tail) {
+    H2B_TRY(h2b_launch_span(h, L, false, xp, yp, q, st));
+    ++*nl;
+  }
+  return H2B_OK;
+}
+
+int enqueue_matvec(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st, int* nl) {
+  *nl = 0;
+  if (h->K == 0) {
+    H2B_TRY(h2b_launch_near(h, xp, yp, q, st));
+    ++*nl;
+    return H2B_OK;
+  }
+  H2B_CUDA_TRY(cudaEventRecord(h->ev_fork, st));
+  H2B_CUDA_TRY(cudaStreamWaitEvent(h->far_stream, h->ev_fork, 0));
+  H2B_TRY(h2b_launch_near(h, xp, yp, q, st));
+  ++*nl;
+  H2B_TRY(launch_far_head(h, xp, q, h->far_stream, nl));
+  H2B_CUDA_TRY(cudaEventRecord(h->ev_join, h->far_stream));
+  H2B_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_join, 0));
+  H2B_TRY(launch_far_tail(h, xp, yp, q, st, nl));
+  return H2B_OK;
+}
+
 }  // namespace
 
 int h2b_launch_gather(const int64_t* perm, int64_t n, const double2* in, double2* out, int q,
@@ -285,59 +111,77 @@ int h2b_launch_scatter(const int64_t* perm, int64_t n, const double2* in, double
   return H2B_OK;
 }
 
+void h2b_release_graphs(h2b_ctx* h) {
+  for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+  h->graphs.clear();
+}
+
 int h2b_ensure_workspace(h2b_ctx* h, int q) {
   if (q <= h->ws_q) return H2B_OK;
+  h2b_release_graphs(h);  // captured graphs hold the old workspace pointers
   if (h->xhat) cudaFree(h->xhat);
   if (h->yhat) cudaFree(h->yhat);
   h->xhat = h->yhat = nullptr;
-  h->device_bytes -= 2 * 16 * h->K * h->ws_q;
+  h->device_bytes -= 2 * 16 * std::max<int64_t>(h->K, 1) * h->ws_q;
   h->ws_q = 0;
   const size_t bytes = (size_t)16 * std::max<int64_t>(h->K, 1) * q;
   H2B_CUDA_TRY(cudaMalloc(&h->xhat, bytes));
   H2B_CUDA_TRY(cudaMalloc(&h->yhat, bytes));
   h->ws_q = q;
-  h->device_bytes += 2 * 16 * h->K * q;
+  h->device_bytes += 2 * 16 * std::max<int64_t>(h->K, 1) * q;
   return H2B_OK;
 }
 
 int h2b_run_matvec(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st) {
-  int rc = h2b_ensure_workspace(h, q);
-  if (rc) return rc;
-  const double2 *vbuf = h->buf[H2B_SEC_V], *tbuf = h->buf[H2B_SEC_T], *sbuf = h->buf[H2B_SEC_S],
-                *dbuf = h->buf[H2B_SEC_D];
-  // (4) near-field: overwrites every row of y (each leaf owns its diagonal block)
-  if (q == 1 && h->uniform_leaf == 32) {
-    k_near_q1<32><<<h->n_leaves, NT, 0, st>>>(h->leaves, h->c_start, h->d_row_ptr, h->d_col,
-                                                h->d_off, dbuf, xp, yp);
-  } else if (q == 1 && h->uniform_leaf == 64) {
-    k_near_q1<64><<<h->n_leaves, NT, 0, st>>>(h->leaves, h->c_start, h->d_row_ptr, h->d_col,
-                                                h->d_off, dbuf, xp, yp);
-  } else {
-    k_near_generic<<<h->n_leaves, NT, 0, st>>>(h->leaves, h->c_start, h->c_size_d, h->d_row_ptr,
-                                               h->d_col, h->d_off, dbuf, xp, yp, q);
+  H2B_TRY(h2b_prepare(h));
+  H2B_TRY(h2b_ensure_workspace(h, q));
+  int nl = 0;
+  if (!h->use_graphs) {
+    H2B_TRY(enqueue_matvec(h, xp, yp, q, st, &nl));
+    if (q == 1) h->launches_q1 = nl;
+    return H2B_OK;
   }
-  H2B_CHECK_LAUNCH();
-  if (h->K == 0) return H2B_OK;
-  // (1) forward, deepest level first
-  for (int l : h->up_levels) {
-    const int p0 = h->level_ptr[l], np = h->level_ptr[l + 1] - p0;
-    k_up_level<<<np, NT, 0, st>>>(p0, h->c_start, h->c_size_d, h->c_rank_d, h->c_lo, h->c_hi,
-                                  h->c_xoff, h->c_voff, h->c_toff, vbuf, tbuf, xp, h->xhat, q);
-    H2B_CHECK_LAUNCH();
+  const GraphKey key{xp, yp, q};
+  auto it = h->graphs.find(key);
+  if (it == h->graphs.end()) {
+    if (h->graphs.size() >= 64) h2b_release_graphs(h);
+    cudaStream_t cs = nullptr;
+    H2B_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    H2B_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    const int rc = enqueue_matvec(h, xp, yp, q, cs, &nl);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cs, &g);
+    cudaStreamDestroy(cs);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) {
+      h2b_set_error(std::string("graph capture: ") + cudaGetErrorString(e));
+      return H2B_ECUDA;
+    }
+    cudaGraphExec_t ex = nullptr;
+    e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+      h2b_set_error(std::string("graph instantiate: ") + cudaGetErrorString(e));
+      return H2B_ECUDA;
+    }
+    if (q == 1) h->launches_q1 = nl;
+    it = h->graphs.emplace(key, ex).first;
   }
-  // (2) coupling
-  k_coupling<<<h->P, NT, 0, st>>>(h->c_rank_d, h->c_xoff, h->s_row_ptr, h->s_col, h->s_off, sbuf,
-                                  h->xhat, h->yhat, q);
-  H2B_CHECK_LAUNCH();
-  // (3) backward, root level first
-  for (int l : h->down_levels) {
-    const int p0 = h->level_ptr[l], np = h->level_ptr[l + 1] - p0;
-    k_down_level<<<np, NT, 0, st>>>(p0, h->c_rank_d, h->c_lo, h->c_hi, h->c_xoff, h->c_toff, tbuf,
-                                    h->yhat, q);
-    H2B_CHECK_LAUNCH();
-  }
-  k_leaf_back<<<h->n_leaves, NT, 0, st>>>(h->leaves, h->c_start, h->c_size_d, h->c_rank_d,
-                                          h->c_xoff, h->c_voff, vbuf, h->yhat, yp, q);
-  H2B_CHECK_LAUNCH();
+  H2B_CUDA_TRY(cudaGraphLaunch(it->second, st));
   return H2B_OK;
+}
+
+// phase 0: near-field only (y overwritten); phase 1: far field only (y accumulated);
+// both serialised on `st` so they can be timed one by one.
+int h2b_run_phase(h2b_ctx* h, int phase, const double2* xp, double2* yp, int q, cudaStream_t st) {
+  H2B_TRY(h2b_prepare(h));
+  H2B_TRY(h2b_ensure_workspace(h, q));
+  int nl = 0;
+  if (phase == 0) return h2b_launch_near(h, xp, yp, q, st);
+  if (h->K == 0) return H2B_OK;
+  H2B_TRY(launch_far_head(h, xp, q, st, &nl));
+  return launch_far_tail(h, xp, yp, q, st, &nl);
 }
