@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 H² matvec hot path (BASELINE.json metric).
+
+Metric: H² matvec unknowns·RHS/s (complex128).  Workload: BASELINE config 2
+(configs[1]: 1-D line of 65,536 points over 2048 λ, leaf 32, η = 1, tol 1e-4,
+one complex128 N(0,1) RHS) — the operator built by the reference builder and
+shipped packed as data/cfg2.npz (tools/make_golden.py).
+
+* ``value``   whole-job unknowns/s of the device matvec, x and y resident in
+              HBM, L2 flushed (256 MiB write) before every timed step, each
+              step timed with CUDA events on the launching stream.
+* ``e2e``     the same metric through the reference-facing call with HOST
+              buffers (h2b_matvec_host: pinned H2D, gather, matvec, scatter,
+              D2H), wall clock per call.
+* ``roofline`` the near-field kernel (the byte-dominant one): algorithmic bytes
+              (16·E_D + 32·N) / its average event-timed duration, against the
+              measured HBM copy bandwidth in MEASURED_PEAKS.json.
+* ``cpu_baseline`` the reference algorithm restated on the CPU
+              (oracle/h2_oracle.py, a faithful port of arith.matvec) timed on
+              this host, 1 thread.
+``--impl reference`` times that CPU port alone and prints the same line.
+Multi-GPU (torchrun): every rank runs an independent replica of the matvec
+("replicas", weak scaling); the max over ranks of the device time is used.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # the reference CPU path is single-threaded
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "H2 matvec unknowns*RHS/s (complex128)"
+UNIT = "unknowns*RHS/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="h2b", choices=["h2b", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="budget of the CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def config_desc(k, pk):
+    names = {1: "cfg1 cube 16^3 (N=4096), leaf 32, tol 1e-4",
+             2: "cfg2 line 2048 lambda at 32 pts/lambda (N=65536), leaf 32, tol 1e-4",
+             3: "cfg3 plate 512^2 (N=262144), leaf 64, tol 1e-4"}
+    return {"workload": names.get(k, f"cfg{k}"), "N": int(pk.n), "q": 1, "eta": 1.0,
+            "operator_bytes_alg": int(pk.algorithmic_bytes()),
+            "operator": f"data/cfg{k}.npz (built by the reference h2vie builder, packed)"}
+
+
+def load(k):
+    from paper_1703_01175_b200.pack import load_packed
+    path = os.path.join(ROOT, "data", f"cfg{k}.npz")
+    if not os.path.exists(path):
+        return None, None
+    return load_packed(path, with_extra=True)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_port_time(pk, x, budget_s):
+    """Mean seconds per matvec of the restated reference CPU path over a bounded sample."""
+    from oracle import h2_oracle as ho
+    ho.matvec(pk, x)  # warm
+    n, t0 = 0, time.perf_counter()
+    while True:
+        ho.matvec(pk, x)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or n >= 1000:
+            return el / n, n
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [c.strip() for c in l.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def run_reference(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    pk, ex = load(a.config)
+    if pk is None:
+        print(json.dumps({"impl": "reference", "unavailable": f"data/cfg{a.config}.npz missing"}))
+        return 0
+    x = ex["x"][:, 0]
+    from oracle import h2_oracle as ho
+    for _ in range(max(1, a.warmup)):
+        ho.matvec(pk, x)
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        ho.matvec(pk, x)
+    dt = (time.perf_counter() - t0) / a.steps
+    v = pk.n / dt
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "complex128 (f64)",
+            "data": "synthetic N(0,1) RHS (seed 0) on the reference-built operator",
+            "config": config_desc(a.config, pk), "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+                             "sample": f"{a.steps} full matvecs of cfg{a.config} (oracle/h2_oracle.py "
+                                       "restates arith.matvec loop-for-loop; numpy/OpenBLAS 1 thread)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    import ctypes as C
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    from paper_1703_01175_b200 import H2Operator, _abi
+
+    pk, ex = load(a.config)
+    if pk is None:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "error": f"data/cfg{a.config}.npz missing"}))
+        return 1
+    op = H2Operator(pk, device=local)
+    L = _abi.lib()
+    _abi.check(L.h2b_prepare_handle(op.handle), "prepare")
+    x = torch.from_numpy(ex["x"][pk.perm, 0].copy()).to(dev)
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream(dev)
+    sh = C.c_void_p(stream.cuda_stream)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def mv():
+        _abi.check(L.h2b_matvec_perm(op.handle, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), 1, sh))
+
+    def near():
+        _abi.check(L.h2b_matvec_phase(op.handle, 0, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), 1, sh))
+
+    def timed(fn, k):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+        for s, e in ev:
+            flush.zero_()  # evict L2 (126 MB) before every timed step; not timed
+            s.record(stream)
+            fn()
+            e.record(stream)
+        torch.cuda.synchronize(dev)
+        return sum(s.elapsed_time(e) for s, e in ev) / k  # ms
+
+    for _ in range(max(3, a.warmup)):
+        mv()
+        near()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        time.sleep(0.25)  # let the sampler start
+        ms = timed(mv, a.steps)
+        ms_near = timed(near, a.steps)
+        for _ in range(3):  # keep the device busy for a few more clock samples
+            timed(mv, a.steps)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        t = torch.tensor([ms, ms_near], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms, ms_near = float(t[0]), float(t[1])
+    # parity guard on the measured output (recompute: the last timed call was the near phase)
+    mv()
+    torch.cuda.synchronize(dev)
+    yp = y.cpu().numpy()
+    yy = np.empty_like(yp)
+    yy[pk.perm] = yp
+    relerr = float(np.linalg.norm(yy - ex["y"][:, 0]) / np.linalg.norm(ex["y"][:, 0]))
+
+    # end-to-end through the host-buffer C-ABI call (pinned host memory)
+    xh = torch.from_numpy(ex["x"][:, 0].copy()).pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+
+    def e2e_call():
+        _abi.check(L.h2b_matvec_host(op.handle, C.c_void_p(xh.data_ptr()), C.c_void_p(yh.data_ptr()), 1))
+
+    for _ in range(3):
+        e2e_call()
+    t_e2e = []
+    for _ in range(a.steps):
+        t0 = time.perf_counter()
+        e2e_call()
+        t_e2e.append(time.perf_counter() - t0)
+    e2e_s = float(np.mean(t_e2e))
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t[0])
+
+    nlaunch = C.c_int64()
+    _abi.check(L.h2b_query(op.handle, _abi.Q_LAUNCHES_Q1, C.byref(nlaunch)))
+    peak, peak_src = peaks()
+    near_bytes = pk.near_bytes(1)
+    achieved = near_bytes / (ms_near * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "near_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(f"cfg{a.config}")
+        except Exception:
+            traffic = None
+    unknowns = pk.n * 1
+    line = {
+        "metric": METRIC,
+        "value": world * unknowns / (ms * 1e-3),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "complex128 (f64)",
+        "data": "synthetic: reference-built operator of BASELINE config, N(0,1) RHS (seed 0)",
+        "config": dict(config_desc(a.config, pk), l2="flushed (256 MiB write) before every timed step",
+                       parallelism=f"replicas x{world}"),
+        "achieved_gbs_total": pk.algorithmic_bytes(1) / (ms * 1e-3) / 1e9,
+        "hbm_frac_total": pk.algorithmic_bytes(1) / (ms * 1e-3) / 1e9 / peak,
+        "roofline": {"bound": "hbm", "kernel": "k_near_q1 (near-field, 16 E_D + 32 N bytes)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src, "ms_per_launch": ms_near,
+                     "alg_bytes_per_launch": near_bytes},
+        "e2e": {"value": world * unknowns / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * pk.n,
+                "d2h_bytes_per_step": 16 * pk.n, "ms_per_call": e2e_s * 1e3},
+        "gpu_launches": int(nlaunch.value) * a.steps,
+        "gpu_launches_per_step": int(nlaunch.value),
+        "clocks": clk.summary(),
+        "parity_relerr_vs_reference": relerr,
+    }
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        t_cpu, n_cpu = cpu_port_time(pk, ex["x"][:, 0], a.cpu_seconds)
+        line["cpu_baseline"] = {"value": pk.n / t_cpu, "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": f"{n_cpu} full cfg{a.config} matvecs in {t_cpu * n_cpu:.1f} s "
+                                          "(oracle/h2_oracle.py restates arith.matvec loop-for-loop)",
+                                "cpu": os.cpu_count()}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
