@@ -119,13 +119,27 @@ int h2b_matvec_phase(h2b_handle h, int phase, const void* x_perm, void* y_perm, 
 int h2b_prepare_handle(h2b_handle h);
 
 #define H2B_OPT_GRAPHS 1      /* 1 (default): replay each matvec as a CUDA graph */
+#define H2B_OPT_MEGA 2        /* 1 (default): single persistent launch per q=1 matvec
+                                 (set before the first matvec) */
+#define H2B_OPT_TRACE 3       /* 1: record a per-task timeline of the persistent kernel */
 int h2b_set_option(h2b_handle h, int option, int value);
+
+/* Per-task timeline of the last persistent-kernel matvec (tracing on): for task i,
+ * out[10i..10i+9] = {type (0 near, 1 span, 2 coupling), arg, t_claim, t_ready,
+ * t_staged, t_level0, t_level1, t_computed (spans only; else 0), t_done
+ * (ns, %globaltimer), smid | cta << 32}. */
+int h2b_get_trace(h2b_handle h, int64_t* out, int64_t max_tasks);
 
 #define H2B_Q_LAUNCHES_Q1 1   /* kernels per single-RHS matvec */
 #define H2B_Q_SPAN_MODE 2     /* 1 if the q=1 far field uses staged subtree spans */
 #define H2B_Q_SPLIT_LEVEL 3   /* tree level at which spans are rooted */
 #define H2B_Q_TOP_STAGED 4    /* 1 if levels above the split run as one staged CTA */
 #define H2B_Q_DEVICE_BYTES 5
+#define H2B_Q_MEGA 6          /* 1 if q=1 matvecs run as one persistent kernel */
+#define H2B_Q_MEGA_TASKS 7    /* tasks in its graph */
+#define H2B_Q_MEGA_GRID 8     /* CTAs it launches */
+#define H2B_Q_MEGA_TIERS 9    /* tiers of span programs */
+#define H2B_Q_DEVICE_ERROR 10 /* nonzero if a dependency wait ever timed out (a bug) */
 int h2b_query(h2b_handle h, int what, int64_t* out);
 
 /* Permutation helpers on device buffers: out[i,:] = in[perm[i],:] (gather,

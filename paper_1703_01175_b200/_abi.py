@@ -20,10 +20,11 @@ EXPORTED = (
     "h2b_destroy", "h2b_device_bytes", "h2b_matvec_perm", "h2b_matvec_host",
     "h2b_gather_perm", "h2b_scatter_perm", "h2b_gmres", "h2b_bicgstab",
     "h2b_zdotc_multi", "h2b_zgemv_sub", "h2b_zaxpby", "h2b_matvec_phase",
-    "h2b_prepare_handle", "h2b_set_option", "h2b_query",
+    "h2b_prepare_handle", "h2b_set_option", "h2b_query", "h2b_get_trace",
 )
-OPT_GRAPHS = 1
+OPT_GRAPHS, OPT_MEGA, OPT_TRACE = 1, 2, 3
 Q_LAUNCHES_Q1, Q_SPAN_MODE, Q_SPLIT_LEVEL, Q_TOP_STAGED, Q_DEVICE_BYTES = 1, 2, 3, 4, 5
+Q_MEGA, Q_MEGA_TASKS, Q_MEGA_GRID, Q_MEGA_TIERS, Q_DEVICE_ERROR = 6, 7, 8, 9, 10
 
 _i32p = C.POINTER(C.c_int32)
 _i64p = C.POINTER(C.c_int64)
@@ -91,6 +92,7 @@ def lib():
     L.h2b_prepare_handle.argtypes = [vp]
     L.h2b_set_option.argtypes = [vp, C.c_int, C.c_int]
     L.h2b_query.argtypes = [vp, C.c_int, C.POINTER(C.c_int64)]
+    L.h2b_get_trace.argtypes = [vp, C.POINTER(C.c_int64), C.c_int64]
     L.h2b_zaxpby.argtypes = [C.c_int64, C.c_double, C.c_double, vp, C.c_double, C.c_double, vp, vp]
     _lib = L
     return L

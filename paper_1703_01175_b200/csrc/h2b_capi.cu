@@ -39,7 +39,9 @@ void free_ctx(h2b_ctx* h) {
                   h->buf[0],    h->buf[1],   h->buf[2],   h->buf[3],    h->hxp,
                   h->hyp,       h->vT,       h->tT,       h->s_prow,    h->s_xcol,
                   h->couple_targets, h->span_heads, h->span_copies, h->span_outs,
-                  h->span_ops, h->near_items, h->near_blks, h->couple_items};
+                  h->span_ops, h->near_items, h->near_blks, h->couple_items, h->tasks, h->deps,
+                  h->near_tasks, h->leaf_items, h->couple_groups, h->ctrl, h->flags, h->trace,
+                  h->rec_pool, h->l2_prefetch};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->far_stream) cudaStreamDestroy(h->far_stream);
@@ -267,6 +269,23 @@ int h2b_set_option(h2b_handle h, int option, int value) {
     h2b_release_graphs(h);
     return H2B_OK;
   }
+  if (option == H2B_OPT_TRACE) {
+    REQUIRE(h->prepared && h->mega, H2B_ESTATE, "h2b_set_option(H2B_OPT_TRACE): needs a prepared "
+                                                "persistent-kernel handle");
+    h2b_release_graphs(h);  // captured launches hold the old trace pointer
+    if (h->trace) cudaFree(h->trace);
+    h->trace = nullptr;
+    if (value) {
+      H2B_CUDA_TRY(cudaMalloc(&h->trace, sizeof(uint64_t) * 8 * std::max(h->n_tasks, 1)));
+      H2B_CUDA_TRY(cudaMemset(h->trace, 0, sizeof(uint64_t) * 8 * std::max(h->n_tasks, 1)));
+    }
+    return H2B_OK;
+  }
+  if (option == H2B_OPT_MEGA) {
+    REQUIRE(!h->prepared, H2B_ESTATE, "h2b_set_option(H2B_OPT_MEGA): set before the first matvec");
+    h->use_mega = value ? 1 : 0;
+    return H2B_OK;
+  }
   h2b_set_error("h2b_set_option: unknown option");
   return H2B_EINVAL;
 }
@@ -279,10 +298,43 @@ int h2b_query(h2b_handle h, int what, int64_t* out) {
     case H2B_Q_SPLIT_LEVEL: *out = h->ls; return H2B_OK;
     case H2B_Q_TOP_STAGED: *out = h->top_staged; return H2B_OK;
     case H2B_Q_DEVICE_BYTES: *out = h->device_bytes; return H2B_OK;
+    case H2B_Q_MEGA: *out = h->mega; return H2B_OK;
+    case H2B_Q_MEGA_TASKS: *out = h->n_tasks; return H2B_OK;
+    case H2B_Q_MEGA_GRID: *out = h->mega_grid; return H2B_OK;
+    case H2B_Q_MEGA_TIERS: *out = h->mega_tiers; return H2B_OK;
+    case H2B_Q_DEVICE_ERROR: {
+      MegaCtrl c{};
+      if (h->ctrl) H2B_CUDA_TRY(cudaMemcpy(&c, h->ctrl, sizeof(c), cudaMemcpyDeviceToHost));
+      *out = c.error;
+      return H2B_OK;
+    }
     default: break;
   }
   h2b_set_error("h2b_query: unknown key");
   return H2B_EINVAL;
+}
+
+int h2b_get_trace(h2b_handle h, int64_t* out, int64_t max_tasks) {
+  REQUIRE(h && out, H2B_EINVAL, "h2b_get_trace: null argument");
+  REQUIRE(h->trace, H2B_ESTATE, "h2b_get_trace: tracing is off (H2B_OPT_TRACE)");
+  const int64_t n = std::min<int64_t>(max_tasks, h->n_tasks);
+  std::vector<uint64_t> t(8 * (size_t)n);
+  H2B_CUDA_TRY(cudaDeviceSynchronize());
+  H2B_CUDA_TRY(cudaMemcpy(t.data(), h->trace, sizeof(uint64_t) * 8 * n, cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t* o = out + 10 * i;
+    o[0] = h->h_tasks[i].type;
+    o[1] = h->h_tasks[i].arg;
+    o[2] = (int64_t)t[8 * i + 0];  // claim
+    o[3] = (int64_t)t[8 * i + 1];  // ready
+    o[4] = (int64_t)t[8 * i + 2];  // staged (spans)
+    o[5] = (int64_t)t[8 * i + 6];  // end of level 0 (spans)
+    o[6] = (int64_t)t[8 * i + 7];  // end of level 1 (spans)
+    o[7] = (int64_t)t[8 * i + 5];  // compute done (spans)
+    o[8] = (int64_t)t[8 * i + 3];  // done
+    o[9] = (int64_t)t[8 * i + 4];  // smid | cta << 32
+  }
+  return H2B_OK;
 }
 
 int h2b_gather_perm(h2b_handle h, const void* in, void* out, int q, void* stream) {

@@ -104,10 +104,13 @@ __device__ __forceinline__ cd2 ld_cached256(const double2* p) {
 // inputs and the op list itself), ops (small panel GEMVs on smem offsets,
 // grouped into levels separated by __syncthreads) and copies smem->global.
 // ---------------------------------------------------------------------------
-enum SpanSrc : int32_t { SRC_V = 0, SRC_T, SRC_VT, SRC_TT, SRC_X, SRC_XHAT, SRC_YHAT, SRC_OPS, SRC_N };
-struct SpanCopy {        // global (base[kind] + src) <-> smem[smem], elems double2
+enum SpanSrc : int32_t {
+  SRC_V = 0, SRC_T, SRC_VT, SRC_TT, SRC_X, SRC_XHAT, SRC_YHAT, SRC_OPS, SRC_OUTS, SRC_N
+};
+struct SpanCopy {        // global (base[kind] + src) <-> smem[smem], elems double2 (32 bytes)
   int64_t src;
   int32_t kind, elems, smem, pad;
+  int64_t pad2;
 };
 struct SpanOp {          // out[c] (+)= sum_r P[r*w+c] in[r], c < w, r < R
   int32_t pay, in, out, R, w, flags, pad0, pad1;
@@ -142,6 +145,40 @@ struct CoupleItem {
   int64_t xcol;          // offset into s_xcol of the panel's first row
   int64_t out;           // x̂/ŷ offset of the target
   int32_t R, w;
+};
+
+// ---------------------------------------------------------------------------
+// persistent matvec kernel (q = 1): one launch executes a task graph.  CTAs
+// claim tasks in queue order from an atomic counter; a task waits only on
+// tasks with smaller ids (claimed by running CTAs), so progress is guaranteed.
+// Completion flags are epoch-stamped, so nothing is reset between matvecs.
+// ---------------------------------------------------------------------------
+enum TaskType : int32_t { T_NEAR = 0, T_SPAN = 1, T_COUPLE = 2 };
+struct Task {
+  int32_t type, arg;        // arg: near task / span head / couple group index
+  int32_t dep_first, n_dep; // ranges [dep_first, dep_first + n_dep) of DepRange
+  int64_t rec_off;          // self-contained task record: 16-byte slots in the record pool
+  int32_t rec_len, pad;     // (bulk-loaded into shared memory one task ahead)
+};
+// Record layouts (16-byte slots):
+//   near:   {n_blocks, n_leaves, row0, 0} | n_leaves x {y_off:i64, nb:i32, 0} |
+//           n_blocks x {d_off:i64 (row0 applied), x_off:i64}
+//   span:   SpanHead (9 slots) | n_copy x SpanCopy (2 slots each)
+//   couple: {n_items, cta_mode, 0, 0} | n_items x CoupleItem (2 slots each)
+constexpr int REC_SLOTS = 256;  // 4 KB per record buffer
+constexpr int NEAR_REC_MAXB = 160;
+struct DepRange {
+  int32_t lo, hi;           // task ids [lo, hi) that must be complete
+};
+struct NearTask {
+  int32_t leaf_first, n_leaves;  // consecutive entries of the leaf work list
+  int32_t row0, pad;             // first row (when one leaf is split across tasks)
+};
+struct CoupleGroup {
+  int32_t item_first, n_items, cta_mode, pad;
+};
+struct MegaCtrl {
+  uint32_t next, exited, epoch, error;
 };
 
 // ---------------------------------------------------------------------------
@@ -199,6 +236,23 @@ struct h2b_ctx {
   SpanCopy* span_copies = nullptr;
   SpanCopy* span_outs = nullptr;
   SpanOp* span_ops = nullptr;
+  // persistent-kernel task graph (q = 1)
+  int mega = 0;                  // 1: q = 1 matvec is one persistent launch
+  int mega_ns = 0, mega_r = 1;   // near variant (0 generic, 32, 64) and rows per thread
+  int mega_grid = 0, mega_smem = 0, n_tasks = 0;
+  Task* tasks = nullptr;
+  int4* rec_pool = nullptr;      // task records
+  int4* l2_prefetch = nullptr;   // {ptr lo/hi, bytes} ranges warmed into L2 at kernel start
+  int n_prefetch = 0;
+  DepRange* deps = nullptr;
+  NearTask* near_tasks = nullptr;
+  NearItem* leaf_items = nullptr;  // per leaf: y offset, partner-block range
+  CoupleGroup* couple_groups = nullptr;
+  MegaCtrl* ctrl = nullptr;
+  uint32_t* flags = nullptr;
+  int mega_tiers = 0;
+  uint64_t* trace = nullptr;           // optional per-task timeline (H2B_OPT_TRACE)
+  std::vector<Task> h_tasks;           // host copy of the task list
   // near / coupling work lists
   NearItem* near_items = nullptr;
   NearBlk* near_blks = nullptr;
@@ -215,6 +269,7 @@ struct h2b_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int use_graphs = 1;
+  int use_mega = 1;  // plan the persistent single-launch kernel for q = 1
   // krylov workspace
   void* kry = nullptr;
   size_t kry_bytes = 0;

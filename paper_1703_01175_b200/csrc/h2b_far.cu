@@ -13,19 +13,12 @@
 // transposed coupling panels (one warp or one CTA per target).
 // Any q: per-level kernels reading global memory (also the fallback for
 // clusters whose working set does not fit in shared memory).
-#include "h2b_panel.cuh"
+#include "h2b_span.cuh"
 
 namespace {
 
 constexpr int NT = 256;
 constexpr int TOP_NT = 1024;
-
-struct SpanBases {
-  const double2* src[SRC_N];  // V, T, Vᵀ, Tᵀ, x, x̂, ŷ, ops
-  double2* xhat;
-  double2* yhat;
-  double2* y;
-};
 
 template <int NTH>
 __global__ void __launch_bounds__(NTH) k_span(const SpanHead* __restrict__ heads, int head_base,
@@ -34,43 +27,9 @@ __global__ void __launch_bounds__(NTH) k_span(const SpanHead* __restrict__ heads
   extern __shared__ __align__(16) double2 sm[];
   __shared__ double2 red[NTH];
   __shared__ uint64_t bar;
-  const SpanHead* hd = heads + head_base + blockIdx.x;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    mbar_arrive_expect_tx(&bar, (uint32_t)hd->pad[0]);  // total staged bytes (host-computed)
-  }
+  if (threadIdx.x == 0) mbar_init(&bar, 1);
   __syncthreads();
-  // the span's working set streams in with TMA bulk copies, one copy per thread
-  for (int i = threadIdx.x; i < hd->n_copy; i += NTH) {
-    const SpanCopy c = copies[hd->copy_first + i];
-    bulk_g2s(sm + c.smem, B.src[c.kind] + c.src, 16u * (uint32_t)c.elems, &bar);
-  }
-  mbar_wait(&bar, 0);
-  const SpanOp* ops = reinterpret_cast<const SpanOp*>(sm + hd->ops_smem);
-  const int warp = threadIdx.x >> 5;
-  constexpr int NW = NTH / 32;
-  const int nlev = hd->nlev;
-  for (int lv = 0; lv < nlev; ++lv) {
-    const int o1 = hd->lvl[lv + 1];
-    for (int i = hd->lvl[lv] + warp; i < o1; i += NW) {
-      const SpanOp op = ops[i];
-      const double2* P = sm + op.pay;
-      const double2* in = sm + op.in;
-      auto inf = [in](int r) { return in[r]; };
-      double2* out = (op.flags & OP_OUT_Y) ? B.y + op.out : sm + op.out;
-      if (op.flags & OP_ACC)
-        warp_panel<true>(P, op.R, op.w, inf, out, red + warp * 32);
-      else
-        warp_panel<false>(P, op.R, op.w, inf, out, red + warp * 32);
-    }
-    __syncthreads();
-  }
-  const int n_out = hd->n_out;
-  for (int i = 0; i < n_out; ++i) {
-    const SpanCopy c = outs[hd->out_first + i];
-    double2* dst = (c.kind == SRC_XHAT ? B.xhat : B.yhat) + c.src;
-    for (int e = threadIdx.x; e < c.elems; e += NTH) dst[e] = sm[c.smem + e];
-  }
+  run_span<NTH>(heads + head_base + blockIdx.x, copies, outs, B, sm, red, &bar, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -206,6 +165,7 @@ SpanBases bases_of(const h2b_ctx* h, const double2* xp, double2* yp) {
   B.src[SRC_XHAT] = h->xhat;
   B.src[SRC_YHAT] = h->yhat;
   B.src[SRC_OPS] = reinterpret_cast<const double2*>(h->span_ops);
+  B.src[SRC_OUTS] = reinterpret_cast<const double2*>(h->span_outs);
   B.xhat = h->xhat;
   B.yhat = h->yhat;
   B.y = yp;

@@ -17,6 +17,7 @@ int h2b_launch_span(h2b_ctx* h, const SpanLaunch& L, bool up, const double2* xp,
 int h2b_launch_coupling(h2b_ctx* h, int q, cudaStream_t st);
 int h2b_launch_far_levels_head(h2b_ctx* h, const double2* xp, int q, cudaStream_t st, int* nl);
 int h2b_launch_leaf_back(h2b_ctx* h, double2* yp, int q, cudaStream_t st);
+int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st);
 
 namespace {
 
@@ -79,6 +80,11 @@ int launch_far_tail(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStrea
 
 int enqueue_matvec(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st, int* nl) {
   *nl = 0;
+  if (q == 1 && h->mega) {  // the whole matvec is one persistent launch
+    H2B_TRY(h2b_launch_mega(h, xp, yp, st));
+    *nl = 1;
+    return H2B_OK;
+  }
   if (h->K == 0) {
     H2B_TRY(h2b_launch_near(h, xp, yp, q, st));
     ++*nl;

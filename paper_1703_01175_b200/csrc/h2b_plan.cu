@@ -5,11 +5,15 @@
 //   * the q = 1 far-field schedule: span programs (h2b_common.cuh) chosen by
 //     a small cost model over the split level `ls`.
 #include <algorithm>
+#include <cstring>
 #include <functional>
 
 #include "h2b_common.cuh"
+#include "h2b_panel.cuh"
 
 int h2b_far_init_attributes(int smem_cap_bytes);
+int h2b_mega_set_smem(int ns, int r, int bytes);
+int h2b_mega_occupancy(int ns, int r, int smem_bytes, int* blocks_per_sm);
 int h2b_near_rows_per_item(int ns, int r);
 
 namespace {
@@ -73,15 +77,15 @@ struct SB {  // a span under construction
   }
   int in(int kind, int64_t src, int64_t e) {
     const int o = alloc((int)e);
-    if (e > 0) cp.push_back({src, kind, (int32_t)e, o, 0});
+    if (e > 0) cp.push_back({src, kind, (int32_t)e, o, 0, 0});
     return o;
   }
   void outc(int kind, int64_t dst, int64_t e, int o) {
-    if (e > 0) out.push_back({dst, kind, (int32_t)e, o, 0});
+    if (e > 0) out.push_back({dst, kind, (int32_t)e, o, 0, 0});
   }
   void level() { lv.emplace_back(); }
   void op(int pay, int in_, int out_, int R, int w, int flags) {
-    lv.back().push_back(SpanOp{pay, in_, out_, R, w, flags, 0, 0});
+    lv.back().push_back(SpanOp{pay, in_, out_, R, w, flags, panel_shift(w), 0});
   }
 };
 
@@ -92,8 +96,11 @@ bool finish(Prog& P, SB& s, int* smem_out) {
   if ((int)s.lv.size() > SPAN_MAXLEV) return false;
   const int op_first = (int)P.ops.size();
   const int ops_smem = s.in(SRC_OPS, 2 * (int64_t)op_first, 2 * (int64_t)n_ops);
+  // the write-back descriptors travel with the working set too (no serial global loads later)
+  const int outs_smem = s.in(SRC_OUTS, 2 * (int64_t)P.outs.size(), 2 * (int64_t)s.out.size());
   if (s.smem > SPAN_BUDGET) return false;
   SpanHead hd{};
+  hd.pad[1] = outs_smem;
   hd.copy_first = (int)P.copies.size();
   hd.n_copy = (int)s.cp.size();
   hd.out_first = (int)P.outs.size();
@@ -142,6 +149,10 @@ std::vector<Lvl> desc_ranges(const h2b_ctx* h, int r, int max_levels) {
 }
 
 int m_of(const h2b_ctx* h, int p) { return h->c_rank[h->c_child_lo[p]] + h->c_rank[h->c_child_hi[p]]; }
+
+int level_of(const h2b_ctx* h, int p) {
+  return (int)(std::upper_bound(h->level_ptr.begin(), h->level_ptr.end(), p) - h->level_ptr.begin()) - 1;
+}
 
 // payload ranges of a level range: V of its leaves, T of its non-leaves
 void pay_ranges(const h2b_ctx* h, Lvl L, int64_t& vb, int64_t& ve, int64_t& tb, int64_t& te) {
@@ -386,6 +397,353 @@ bool plan_with_split(const h2b_ctx* h, int ls, Plan& pl) {
   return true;
 }
 
+// ------------------------- persistent-kernel task graph -------------------------
+constexpr int MEGA_BUDGET = 6000;  // double2 elements (96 KB): two CTAs per SM
+
+std::vector<DepRange> to_ranges(std::vector<int> ids) {
+  std::sort(ids.begin(), ids.end());
+  ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+  std::vector<DepRange> out;
+  for (int v : ids) {
+    if (!out.empty() && out.back().hi == v)
+      out.back().hi = v + 1;
+    else
+      out.push_back({v, v + 1});
+  }
+  return out;
+}
+
+// does every span of a tier fit the budget?  (built into a scratch program)
+bool tier_fits(const h2b_ctx* h, int root_level, int nl, bool input_last, int budget) {
+  Prog P;
+  int sm = 0;
+  for (int r = h->level_ptr[root_level]; r < h->level_ptr[root_level + 1]; ++r) {
+    if (!build_subtree_span(h, P, r, nl, true, input_last, &sm)) return false;
+    if (!build_subtree_span(h, P, r, nl, false, input_last, &sm)) return false;
+  }
+  return sm <= budget;
+}
+
+struct MegaPlan {
+  Prog prog;
+  std::vector<Task> tasks;
+  std::vector<DepRange> deps;
+  std::vector<NearTask> near_tasks;
+  std::vector<NearItem> leaf_items;
+  std::vector<CoupleGroup> groups;
+  std::vector<CoupleItem> citems;
+  std::vector<int4> recs;
+  int ns = 0, r = 1, smem = 0, tiers = 0;
+};
+
+bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
+               const std::vector<int32_t>& targets, int grid_est, MegaPlan& mp) {
+  const int L = h->depth;
+  int min_leaf = L - 1;
+  for (int p = 0; p < h->P; ++p)
+    if (h->c_child_lo[p] < 0) min_leaf = std::min(min_leaf, level_of(h, p));
+  // ---- tiers: bottom split ls, then upper splits up to the root -----------------
+  int ls = -1;
+  for (int l = 0; l <= min_leaf && ls < 0; ++l)
+    if (tier_fits(h, l, L - l, false, MEGA_BUDGET)) ls = l;
+  if (ls < 0) return false;
+  std::vector<int> splits = {ls};  // bottom-up list of tier roots
+  while (splits.back() > 0) {
+    const int cur = splits.back();
+    int s = -1;
+    for (int c = 0; c < cur && s < 0; ++c)
+      if (tier_fits(h, c, cur - c + 1, true, MEGA_BUDGET)) s = c;
+    if (s < 0) return false;
+    splits.push_back(s);
+  }
+  const int m = (int)splits.size();  // tier 0 = bottom
+  mp.tiers = m;
+  // ---- span programs ---------------------------------------------------------------
+  struct SpanRef {
+    int root, up_head, dn_head;  // head index or -1 when the span has no ops
+  };
+  std::vector<std::vector<SpanRef>> tier(m);
+  Prog& P = mp.prog;
+  int smem = 0;
+  for (int i = 0; i < m; ++i) {
+    const int rl = splits[i];
+    const bool bottom = i == 0;
+    const int nl = bottom ? L - rl : splits[i - 1] - rl + 1;
+    for (int r = h->level_ptr[rl]; r < h->level_ptr[rl + 1]; ++r) {
+      SpanRef s{r, -1, -1};
+      for (int dir = 0; dir < 2; ++dir) {
+        const size_t h0 = P.heads.size();
+        if (!build_subtree_span(h, P, r, nl, dir == 0, !bottom, &smem)) return false;
+        if (P.heads.back().n_ops == 0) {  // nothing to do: drop it again
+          P.ops.resize(P.ops.size() - 0);
+          P.copies.resize(P.heads.back().copy_first);
+          P.outs.resize(P.heads.back().out_first);
+          P.heads.resize(h0);
+        } else {
+          (dir == 0 ? s.up_head : s.dn_head) = (int)h0;
+        }
+      }
+      tier[i].push_back(s);
+    }
+  }
+  mp.smem = 16 * smem;
+  // ---- task list -------------------------------------------------------------------
+  // self-contained task records (see Task in h2b_common.cuh)
+  auto push_slots = [&](const void* data, size_t bytes) {
+    const size_t n = (bytes + 15) / 16;
+    const size_t at = mp.recs.size();
+    mp.recs.resize(at + n, int4{0, 0, 0, 0});
+    std::memcpy(mp.recs.data() + at, data, bytes);
+  };
+  auto make_record = [&](int type, int arg) -> bool {
+    if (type == T_SPAN) {
+      SpanHead hd = mp.prog.heads[arg];
+      const int c0 = hd.copy_first;
+      hd.copy_first = 0;  // copies follow the head inside the record
+      push_slots(&hd, sizeof(SpanHead));
+      push_slots(mp.prog.copies.data() + c0, sizeof(SpanCopy) * hd.n_copy);
+    } else if (type == T_COUPLE) {
+      const CoupleGroup& g = mp.groups[arg];
+      const int4 hdr{g.n_items, g.cta_mode, 0, 0};
+      push_slots(&hdr, sizeof(hdr));
+      push_slots(mp.citems.data() + g.item_first, sizeof(CoupleItem) * g.n_items);
+    } else if (mp.ns == 0) {
+      const int4 hdr{arg, 0, 0, 0};
+      push_slots(&hdr, sizeof(hdr));
+    } else {
+      const NearTask& nt = mp.near_tasks[arg];
+      std::vector<int64_t> lv, bl;
+      for (int li = nt.leaf_first; li < nt.leaf_first + nt.n_leaves; ++li) {
+        const int t = h->h_leaves[li];
+        const int64_t b0 = h->d_row_ptr[t], b1 = h->d_row_ptr[t + 1];
+        lv.push_back(h->c_start[t]);
+        lv.push_back(b1 - b0);
+        for (int64_t b = b0; b < b1; ++b) {
+          bl.push_back(h->d_off[b] + (int64_t)nt.row0 * mp.ns);
+          bl.push_back(h->c_start[h->d_col[b]]);
+        }
+      }
+      const int4 hdr{(int)(bl.size() / 2), nt.n_leaves, nt.row0, 0};
+      push_slots(&hdr, sizeof(hdr));
+      push_slots(lv.data(), 8 * lv.size());
+      push_slots(bl.data(), 8 * bl.size());
+    }
+    return true;
+  };
+  auto add_task = [&](int type, int arg, const std::vector<int>& dep_ids) {
+    Task t{type, arg, (int)mp.deps.size(), 0, (int64_t)mp.recs.size(), 0, 0};
+    make_record(type, arg);
+    t.rec_len = (int)((int64_t)mp.recs.size() - t.rec_off);
+    for (auto& rg : to_ranges(dep_ids)) mp.deps.push_back(rg);
+    t.n_dep = (int)mp.deps.size() - t.dep_first;
+    mp.tasks.push_back(t);
+    return (int)mp.tasks.size() - 1;
+  };
+  // the clusters a span computes (for producer / consumer maps)
+  auto span_clusters = [&](int tier_i, int root, bool with_input) {
+    const bool bottom = tier_i == 0;
+    const int nl = bottom ? L - splits[tier_i] : splits[tier_i - 1] - splits[tier_i] + 1;
+    auto R = desc_ranges(h, root, nl);
+    std::vector<int> cl;
+    const int n = (int)R.size() - ((bottom || with_input) ? 0 : 1);
+    for (int i = 0; i < n; ++i)
+      for (int p = R[i].a; p < R[i].b; ++p) cl.push_back(p);
+    return cl;
+  };
+  // ---- near-field work list (leaf order) --------------------------------------------
+  const int ns = h->uniform_leaf;
+  const int nleaves = (int)h->h_leaves.size();
+  std::vector<int> leaf_pos(h->P, -1);
+  for (int i = 0; i < nleaves; ++i) leaf_pos[h->h_leaves[i]] = i;
+  for (int i = 0; i < nleaves; ++i) {
+    const int t = h->h_leaves[i];
+    mp.leaf_items.push_back({(int64_t)h->c_start[t], (int32_t)h->d_row_ptr[t],
+                             (int32_t)(h->d_row_ptr[t + 1] - h->d_row_ptr[t]), 0, 0});
+  }
+  std::vector<NearTask>& nts = mp.near_tasks;
+  std::vector<int> nt_of_leaf_last(nleaves, -1);
+  if (ns == 32 || ns == 64) {
+    const double avg_nb = (double)h->n_near / std::max(1, nleaves);
+    const double row_bytes = ns * 16.0 * avg_nb;
+    const int rpp = 256 / (ns / 2);  // rows per pass of a 256-thread CTA
+    int R = 1;
+    while (R * 2 * rpp <= ns && R * 2 <= (ns == 32 ? 2 : 8) && R * 2 * rpp * row_bytes <= 96e3) R *= 2;
+    mp.ns = ns;
+    mp.r = R;
+    const int rb = R * rpp;
+    if (rb < ns) {
+      for (int i = 0; i < nleaves; ++i)
+        for (int r0 = 0; r0 < ns; r0 += rb) {
+          nts.push_back({i, 1, r0, 0});
+          nt_of_leaf_last[i] = (int)nts.size() - 1;
+        }
+    } else {
+      // group whole leaves into tasks of ~192 KB, bounded by the record size
+      const int per = std::max(1, (int)(192e3 / (ns * row_bytes) + 0.5));
+      int i = 0;
+      while (i < nleaves) {
+        int c = 0, blocks = 0;
+        while (i + c < nleaves && c < per && c < 64) {
+          const int t = h->h_leaves[i + c];
+          const int nb = (int)(h->d_row_ptr[t + 1] - h->d_row_ptr[t]);
+          if (c > 0 && blocks + nb > NEAR_REC_MAXB) break;
+          blocks += nb;
+          ++c;
+        }
+        nts.push_back({i, c, 0, 0});
+        for (int j = i; j < i + c; ++j) nt_of_leaf_last[j] = (int)nts.size() - 1;
+        i += c;
+      }
+    }
+    for (int i = 0; i < nleaves; ++i) {  // a single leaf must fit a record too
+      const int t = h->h_leaves[i];
+      if (h->d_row_ptr[t + 1] - h->d_row_ptr[t] > NEAR_REC_MAXB) return false;
+    }
+  } else {
+    mp.ns = 0;
+    mp.r = 1;
+    for (int i = 0; i < nleaves; ++i) {
+      nts.push_back({i, 1, 0, 0});
+      nt_of_leaf_last[i] = (int)nts.size() - 1;
+    }
+  }
+  std::vector<int> nt_first_of_leaf(nleaves, -1);  // near tasks covering a leaf are consecutive
+  for (size_t k = 0; k < nts.size(); ++k)
+    for (int j = nts[k].leaf_first; j < nts[k].leaf_first + nts[k].n_leaves; ++j)
+      if (nt_first_of_leaf[j] < 0) nt_first_of_leaf[j] = (int)k;
+  std::vector<int> nt_task(nts.size(), -1);
+  auto emit_near = [&](size_t k) {
+    nt_task[k] = add_task(T_NEAR, ns == 32 || ns == 64 ? (int)k : nts[k].leaf_first, {});
+  };
+  // Queue order: the far-field tasks are spaced out by waves of near tasks (taken from the END
+  // of the leaf order, whose backward spans come last) so that a far task is usually claimed
+  // after its dependencies finished instead of parking a CTA.
+  const size_t nn = nts.size();
+  const size_t wave = (size_t)std::max(1, grid_est);
+  const size_t n_early = std::min(nn, (5 * wave) / 2);
+  size_t early_next = nn - n_early;
+  auto emit_early = [&](size_t cnt) {
+    for (size_t c = 0; c < cnt && early_next < nn; ++c) emit_near(early_next++);
+  };
+  std::vector<int> up_task(h->P, -1), up_of_span_root(h->P, -1);
+  // A. forward spans, bottom tier first (upper tiers after one wave of near-field work)
+  for (int i = 0; i < m; ++i) {
+    if (i == 1) emit_early(wave);
+    for (auto& s : tier[i]) {
+      std::vector<int> deps;
+      if (i > 0)  // children spans: tier i-1 spans rooted inside this span's input level
+        for (int p : span_clusters(i, s.root, true))
+          if (up_of_span_root[p] >= 0 && level_of(h, p) == splits[i - 1]) deps.push_back(up_of_span_root[p]);
+      if (s.up_head < 0) continue;
+      const int id = add_task(T_SPAN, s.up_head, deps);
+      up_of_span_root[s.root] = id;
+      for (int p : span_clusters(i, s.root, false)) up_task[p] = id;
+    }
+  }
+  emit_early(m > 1 ? wave / 2 : wave + wave / 2);
+  // B. coupling groups (targets in packed order; panels + gathered x̂ bounded by the budget)
+  std::vector<int> group_task(h->P, -1);
+  int couple_smem = 0;
+  {
+    const int64_t cap = 4000;  // double2 elements per warp-mode group (64 KB)
+    size_t i = 0;
+    while (i < citems_all.size()) {
+      const int64_t e0 = (int64_t)citems_all[i].R * citems_all[i].w + citems_all[i].R;
+      CoupleGroup g{(int)mp.citems.size(), 0, 0, 0};
+      std::vector<int> members;
+      int64_t elems = 0;
+      if (e0 > 3000) {  // a big panel: the whole CTA streams it
+        if (citems_all[i].R > MEGA_BUDGET) return false;
+        g.cta_mode = 1;
+        mp.citems.push_back(citems_all[i]);
+        members.push_back(targets[i]);
+        elems = citems_all[i].R;
+        ++i;
+      } else {
+        while (i < citems_all.size() && (int)members.size() < 64) {
+          const int64_t e = (int64_t)citems_all[i].R * citems_all[i].w + citems_all[i].R;
+          if (e > 3000 || elems + e > cap) break;
+          mp.citems.push_back(citems_all[i]);
+          members.push_back(targets[i]);
+          elems += e;
+          ++i;
+        }
+      }
+      couple_smem = std::max<int>(couple_smem, (int)elems);
+      g.n_items = (int)members.size();
+      std::vector<int> deps;
+      for (int t : members)
+        for (int64_t b = h->s_row_ptr[t]; b < h->s_row_ptr[t + 1]; ++b) {
+          const int s = h->s_col[b];
+          if (h->c_rank[s] > 0 && up_task[s] >= 0) deps.push_back(up_task[s]);
+        }
+      mp.groups.push_back(g);
+      const int id = add_task(T_COUPLE, (int)mp.groups.size() - 1, deps);
+      for (int t : members) group_task[t] = id;
+    }
+  }
+  mp.smem = std::max(mp.smem, 16 * couple_smem);
+  emit_early(nn);  // the rest of the early wave
+  // C. backward spans of the upper tiers, root tier first
+  std::vector<int> dn_writer(h->P, -1);  // task that last wrote ŷ of a tier root
+  auto down_deps = [&](int tier_i, const SpanRef& s) {
+    std::vector<int> deps;
+    if (dn_writer[s.root] >= 0) deps.push_back(dn_writer[s.root]);
+    for (int p : span_clusters(tier_i, s.root, true))
+      if (group_task[p] >= 0) deps.push_back(group_task[p]);
+    return deps;
+  };
+  for (int i = m - 1; i >= 1; --i)
+    for (auto& s : tier[i]) {
+      if (s.dn_head < 0) continue;
+      const int id = add_task(T_SPAN, s.dn_head, down_deps(i, s));
+      // this span writes back ŷ of its input level: the lower tier's roots
+      auto R = desc_ranges(h, s.root, splits[i - 1] - splits[i] + 1);
+      for (int p = R.back().a; p < R.back().b; ++p) dn_writer[p] = id;
+    }
+  // D. the remaining near-field tasks in leaf order, each bottom backward span emitted once
+  //    the near tasks of its own leaves and of the next span's leaves are in the queue
+  const size_t n_late = nn - n_early;
+  std::vector<int> span_need;  // last late near-task index a bottom span waits for (-1: none)
+  for (auto& s : tier[0]) {
+    int need = -1;
+    for (int p : span_clusters(0, s.root, true))
+      if (leaf_pos[p] >= 0)
+        for (int k = nt_first_of_leaf[leaf_pos[p]]; k <= nt_of_leaf_last[leaf_pos[p]]; ++k)
+          if ((size_t)k < n_late) need = std::max(need, k);
+    span_need.push_back(need);
+  }
+  size_t next_bd = 0;
+  auto emit_bd = [&](size_t j) {
+    const SpanRef& s = tier[0][j];
+    if (s.dn_head < 0) return;
+    std::vector<int> deps = down_deps(0, s);
+    for (int p : span_clusters(0, s.root, true))
+      if (leaf_pos[p] >= 0)
+        for (int k = nt_first_of_leaf[leaf_pos[p]]; k <= nt_of_leaf_last[leaf_pos[p]]; ++k)
+          deps.push_back(nt_task[k]);
+    add_task(T_SPAN, s.dn_head, deps);
+  };
+  auto flush_bd = [&](long k) {
+    while (next_bd < tier[0].size()) {
+      const size_t gate = std::min(next_bd + 1, tier[0].size() - 1);
+      if (span_need[gate] <= k && span_need[next_bd] <= k) {
+        emit_bd(next_bd);
+        ++next_bd;
+      } else {
+        break;
+      }
+    }
+  };
+  flush_bd(-1);
+  for (size_t k = 0; k < n_late; ++k) {
+    emit_near(k);
+    flush_bd((long)k);
+  }
+  while (next_bd < tier[0].size()) emit_bd(next_bd++);
+  return true;
+}
+
 bool plan_per_level(const h2b_ctx* h, Plan& pl) {
   pl = Plan();
   pl.ls = -1;
@@ -509,9 +867,72 @@ int h2b_prepare(h2b_ctx* h) {
     h->n_near_items = (int)items.size();
     h->near_rb = rb;
   }
+  // ---- q = 1 persistent single-launch task graph ----------------------------------------
+  h->mega = 0;
+  if (h->use_mega) {
+    MegaPlan mp;
+    int sms_est = 148;
+    cudaDeviceGetAttribute(&sms_est, cudaDevAttrMultiProcessorCount, h->device);
+    if (plan_mega(h, citems, targets, 2 * sms_est, mp)) {
+      H2B_TRY(to_device(&h->span_heads, mp.prog.heads, &acc));
+      H2B_TRY(to_device(&h->span_copies, mp.prog.copies, &acc));
+      H2B_TRY(to_device(&h->span_outs, mp.prog.outs, &acc));
+      H2B_TRY(to_device(&h->span_ops, mp.prog.ops, &acc));
+      H2B_TRY(to_device(&h->tasks, mp.tasks, &acc));
+      H2B_TRY(to_device(&h->deps, mp.deps, &acc));
+      H2B_TRY(to_device(&h->near_tasks, mp.near_tasks, &acc));
+      H2B_TRY(to_device(&h->leaf_items, mp.leaf_items, &acc));
+      H2B_TRY(to_device(&h->couple_groups, mp.groups, &acc));
+      H2B_TRY(to_device(&h->rec_pool, mp.recs, &acc));
+      {  // far-field operands warmed into L2 at every launch (64 KB pieces)
+        std::vector<int4> pf;
+        auto add = [&](const void* p, int64_t bytes) {
+          for (int64_t o = 0; o < bytes; o += 65536) {
+            const uint64_t a = (uint64_t)p + o;
+            pf.push_back(int4{(int)(uint32_t)a, (int)(uint32_t)(a >> 32),
+                              (int)std::min<int64_t>(65536, bytes - o), 0});
+          }
+        };
+        add(h->buf[H2B_SEC_V], 16 * h->sec_elems[0]);
+        add(h->buf[H2B_SEC_T], 16 * h->sec_elems[1]);
+        add(h->vT, 16 * h->sec_elems[0]);
+        add(h->tT, 16 * h->sec_elems[1]);
+        add(h->buf[H2B_SEC_S], 16 * h->sec_elems[2]);
+        add(h->s_xcol, 4 * (int64_t)xcol.size() / 16 * 16);
+        H2B_TRY(to_device(&h->l2_prefetch, pf, &acc));
+        h->n_prefetch = (int)pf.size();
+      }
+      if (!mp.citems.empty()) {  // grouped order of the coupling work items
+        cudaFree(h->couple_items);
+        h->couple_items = nullptr;
+        H2B_TRY(to_device(&h->couple_items, mp.citems, &acc));
+      }
+      H2B_CUDA_TRY(cudaMalloc(&h->ctrl, sizeof(MegaCtrl)));
+      H2B_CUDA_TRY(cudaMemset(h->ctrl, 0, sizeof(MegaCtrl)));
+      H2B_CUDA_TRY(cudaMalloc(&h->flags, sizeof(uint32_t) * std::max<size_t>(mp.tasks.size(), 1)));
+      H2B_CUDA_TRY(cudaMemset(h->flags, 0, sizeof(uint32_t) * std::max<size_t>(mp.tasks.size(), 1)));
+      h->n_tasks = (int)mp.tasks.size();
+      h->h_tasks = mp.tasks;
+      h->mega_ns = mp.ns;
+      h->mega_r = mp.r;
+      // near-field stages use the whole budget (2 CTAs per SM still fit)
+      h->mega_smem = std::max(mp.smem, mp.ns > 0 ? 16 * MEGA_BUDGET : 16);
+      h->mega_tiers = mp.tiers;
+      H2B_TRY(h2b_mega_set_smem(mp.ns, mp.r, 100 * 1024));
+      int per_sm = 0, sms = 0;
+      H2B_TRY(h2b_mega_occupancy(mp.ns, mp.r, h->mega_smem, &per_sm));
+      H2B_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+      h->mega_grid = std::max(1, std::min(per_sm * sms, h->n_tasks));
+      h->mega = per_sm > 0 ? 1 : 0;
+    }
+  }
+  if (h->mega) {  // the multi-kernel programs below are still planned for phase timing
+    h->device_bytes += acc;
+    acc = 0;
+  }
   // ---- q = 1 far-field schedule ---------------------------------------------------
   h->span_mode = 0;
-  if (h->K > 0) {
+  if (h->K > 0 && !h->mega) {
     Plan best;
     int min_leaf_level = h->depth;
     for (int l = 0; l < h->depth; ++l)

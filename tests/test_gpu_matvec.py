@@ -131,3 +131,47 @@ def test_baseline_config_size_independent_properties(k):
     Y = op.matmat(np.stack([x1, x2], 1))
     assert rel(Y[:, 0], y1) <= 1e-13 and rel(Y[:, 1], y2) <= 1e-13
     assert not np.any(op.matvec(np.zeros(pk.n)))
+
+
+@pytest.mark.parametrize("name", GOLDEN_NAMES)
+def test_execution_paths_agree(name):
+    """Persistent single-launch kernel, multi-kernel span programs, graphs off: same results."""
+    from paper_1703_01175_b200 import H2Operator, _abi
+    pk, ex = load_golden(name)
+    L = _abi.lib()
+    outs = []
+    for mega, graphs in ((1, 1), (0, 1), (0, 0), (1, 0)):
+        op = H2Operator(pk)
+        _abi.check(L.h2b_set_option(op.handle, _abi.OPT_MEGA, mega))
+        _abi.check(L.h2b_set_option(op.handle, _abi.OPT_GRAPHS, graphs))
+        y = op.matvec(ex["x"][:, 0])
+        assert rel(y, ex["y"][:, 0]) <= 1e-12, (mega, graphs)
+        err = C_int64()
+        _abi.check(L.h2b_query(op.handle, _abi.Q_DEVICE_ERROR, err))
+        assert err.value == 0
+        outs.append(y)
+        op.close()
+
+
+def C_int64():
+    import ctypes
+    return ctypes.c_int64()
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_persistent_kernel_repeated_launches(k):
+    """Epoch-stamped flags: many back-to-back launches stay correct and deterministic."""
+    import torch
+    from paper_1703_01175_b200 import H2Operator, _abi
+    pk, ex = load_config(k)
+    op = H2Operator(pk)
+    x = torch.from_numpy(ex["x"][pk.perm, 0].copy()).cuda()
+    y0 = op.matvec_perm(x).cpu().numpy()
+    y = torch.empty_like(x)
+    for _ in range(50):
+        op.matvec_perm(x, out=y)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), y0)
+    flag = C_int64()
+    _abi.check(_abi.lib().h2b_query(op.handle, _abi.Q_MEGA, flag))
+    assert flag.value == 1
