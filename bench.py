@@ -7,7 +7,7 @@ one complex128 N(0,1) RHS) — the operator built by the reference builder and
 shipped packed as data/cfg2.npz (tools/make_golden.py).
 
 * ``value``   whole-job unknowns/s of the device matvec, x and y resident in
-              HBM, L2 flushed (256 MiB write) before every timed step, each
+              HBM, L2 flushed (256 MiB write, then 256 MiB read so no dirty lines remain) before every timed step, each
               step timed with CUDA events on the launching stream.
 * ``e2e``     the same metric through the reference-facing call with HOST
               buffers (h2b_matvec_host: pinned H2D, gather, matvec, scatter,
@@ -235,7 +235,8 @@ def main():
     y = torch.empty_like(x)
     stream = torch.cuda.current_stream(dev)
     sh = C.c_void_p(stream.cuda_stream)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    from paper_1703_01175_b200.timing import L2Flusher
+    flush = L2Flusher(dev)
 
     def mv():
         _abi.check(L.h2b_matvec_perm(op.handle, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), 1, sh))
@@ -244,7 +245,7 @@ def main():
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
         for s, e in ev:
             if flush_l2:
-                flush.zero_()  # evict L2 (126 MB) before every timed step; not timed
+                flush.flush()  # evict L2 (126 MB) before every timed step; not timed
             s.record(stream)
             fn()
             e.record(stream)
@@ -321,7 +322,7 @@ def main():
         "vs_baseline": None,
         "dtype": "complex128 (f64)",
         "data": "synthetic: reference-built operator of BASELINE config, N(0,1) RHS (seed 0)",
-        "config": dict(config_desc(a.config, pk), l2="flushed (256 MiB write) before every timed step",
+        "config": dict(config_desc(a.config, pk), l2="flushed before every timed step (256 MiB write + 256 MiB read: clean L2)",
                        parallelism=f"replicas x{world}"),
         "achieved_gbs_total": pk.algorithmic_bytes(1) / (ms * 1e-3) / 1e9,
         "hbm_frac_total": pk.algorithmic_bytes(1) / (ms * 1e-3) / 1e9 / peak,

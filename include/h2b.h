@@ -122,6 +122,8 @@ int h2b_prepare_handle(h2b_handle h);
 #define H2B_OPT_MEGA 2        /* 1 (default): single persistent launch per q=1 matvec
                                  (set before the first matvec) */
 #define H2B_OPT_TRACE 3       /* 1: record a per-task timeline of the persistent kernel */
+#define H2B_OPT_DEBUG 4       /* profiling only, results are WRONG: bit 0 skips far-field task
+                                 bodies, bit 1 near-field task bodies of the persistent kernel */
 int h2b_set_option(h2b_handle h, int option, int value);
 
 /* Per-task timeline of the last persistent-kernel matvec (tracing on): for task i,

@@ -41,7 +41,7 @@ void free_ctx(h2b_ctx* h) {
                   h->couple_targets, h->span_heads, h->span_copies, h->span_outs,
                   h->span_ops, h->near_items, h->near_blks, h->couple_items, h->tasks, h->deps,
                   h->near_tasks, h->leaf_items, h->couple_groups, h->ctrl, h->flags, h->trace,
-                  h->rec_pool, h->l2_prefetch};
+                  h->rec_pool, h->l2_prefetch, h->cta_lists, h->task_list};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->far_stream) cudaStreamDestroy(h->far_stream);
@@ -279,6 +279,11 @@ int h2b_set_option(h2b_handle h, int option, int value) {
       H2B_CUDA_TRY(cudaMalloc(&h->trace, sizeof(uint64_t) * 8 * std::max(h->n_tasks, 1)));
       H2B_CUDA_TRY(cudaMemset(h->trace, 0, sizeof(uint64_t) * 8 * std::max(h->n_tasks, 1)));
     }
+    return H2B_OK;
+  }
+  if (option == H2B_OPT_DEBUG) {
+    h->mega_debug = value;
+    h2b_release_graphs(h);
     return H2B_OK;
   }
   if (option == H2B_OPT_MEGA) {

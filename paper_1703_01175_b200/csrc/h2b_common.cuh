@@ -251,6 +251,11 @@ struct h2b_ctx {
   MegaCtrl* ctrl = nullptr;
   uint32_t* flags = nullptr;
   int mega_tiers = 0;
+  int mega_debug = 0;                  // H2B_OPT_DEBUG (profiling only: results are wrong)
+  int2* cta_lists = nullptr;           // per CTA {first, count} into task_list
+  int* task_list = nullptr;            // static per-CTA task runs (global topological order)
+  double mega_est_us = 0.0;            // planner's makespan estimate
+  int mega_blob_slots = 0;             // largest per-CTA task blob (16-byte slots)
   uint64_t* trace = nullptr;           // optional per-task timeline (H2B_OPT_TRACE)
   std::vector<Task> h_tasks;           // host copy of the task list
   // near / coupling work lists
@@ -302,16 +307,23 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
   asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-      "@P1 bra DONE_%=;\n\t"
-      "bra WAIT_%=;\n"
-      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
-      "r"(phase), "r"(0x989680u)
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
       : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  // try_wait without a suspend-time hint: the default (short) timeout keeps the waiting warps
+  // responsive to a completing transaction.  A phase that never completes is a bug: trap
+  // (the launch fails with an error) instead of hanging the GPU.
+  for (uint32_t spins = 0; !mbar_try_wait(bar, phase);)
+    if (++spins == (1u << 26)) __trap();
 }
 // global -> shared bulk copy completing on `bar` (bytes % 16 == 0, 16-B aligned)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {

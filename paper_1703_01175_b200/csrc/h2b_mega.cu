@@ -50,6 +50,9 @@ struct MegaArgs {
   double2* yhat;
   uint64_t* trace;  // optional: per task {claim, ready, staged, done, smid} (globaltimer ns)
   int smem_elems;   // dynamic shared memory (double2) of the launch
+  int debug;        // profiling aid: task bodies to skip (H2B_OPT_DEBUG)
+  const int2* cta_lists;  // per CTA: {first, count} into task_list
+  const int* task_list;   // task ids, each CTA's run in global topological order
 };
 
 __device__ __forceinline__ uint64_t gtimer() {
@@ -91,9 +94,25 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 // ---------------------------------------------------------------------------
 // near-field rows of a run of leaves (record in shared memory), TMA ring
 // ---------------------------------------------------------------------------
+// The ring persists across the CTA's consecutive near tasks: once the current
+// task's remaining blocks are all in flight, its refills already stream the
+// NEXT task's first blocks (its record was prefetched when it was claimed), so
+// the HBM stream of a CTA does not drain between tasks.  `ring` is the stage of
+// the current task's block 0; `carry` how many of its blocks the previous task
+// issued; returns how many of `next`'s blocks this task issued.
 template <int NS, int R>
-__device__ __forceinline__ void near_task(const MegaArgs& A, const int4* rec, double2* sm,
-                                          uint64_t* fbar, uint32_t& fphase, int nst, uint64_t pol) {
+__device__ __forceinline__ void issue_block(const MegaArgs& A, const int64_t* bl, int i, double2* st,
+                                            uint64_t* bar, uint64_t pol) {
+  constexpr int RB = R * (MNT / (NS / 2));
+  mbar_arrive_expect_tx(bar, 16u * (RB * NS));
+  bulk_g2s_hint(st, A.dbuf + bl[2 * i], 16u * RB * NS, bar, pol);
+}
+
+template <int NS, int R>
+__device__ __forceinline__ int near_task(const MegaArgs& A, const int4* rec, const int4* next,
+                                         uint64_t* next_bar, uint32_t next_parity, double2* sm,
+                                         uint64_t* fbar, uint32_t& fphase, int nst, uint64_t pol,
+                                         uint32_t& ring, int carry) {
   constexpr int LPR = NS / 2;
   constexpr int RPP = MNT / LPR;
   constexpr int RB = R * RPP;        // rows of the task's slice of each block
@@ -101,27 +120,49 @@ __device__ __forceinline__ void near_task(const MegaArgs& A, const int4* rec, do
   const int nb = rec[0].x, nl = rec[0].y, row0 = rec[0].z;
   const int64_t* lv = reinterpret_cast<const int64_t*>(rec + 1);        // {y_off, nb} per leaf
   const int64_t* bl = reinterpret_cast<const int64_t*>(rec + 1 + nl);   // {d_off, x_off} per block
+  // the next task's record is read by thread 0 only, when it first needs it
+  int nb_next = -1;
+  const int64_t* bl_next = nullptr;
+  auto next_ready = [&]() {
+    if (nb_next < 0) {
+      if (next) {
+        if (next_bar) mbar_wait(next_bar, next_parity);
+        nb_next = next[0].x;
+        bl_next = reinterpret_cast<const int64_t*>(next + 1 + next[0].y);
+      } else {
+        nb_next = 0;
+      }
+    }
+    return nb_next;
+  };
   const int r0 = threadIdx.x / LPR;
   const int col = (threadIdx.x % LPR) * 2;
-  const int pre = min(nst, nb);
-  if (threadIdx.x == 0)
-    for (int i = 0; i < pre; ++i) {
-      double2* st = sm + (size_t)i * STG;
-      mbar_arrive_expect_tx(&fbar[i], 16u * STG);
-      bulk_g2s_hint(st, A.dbuf + bl[2 * i], 16u * RB * NS, &fbar[i], pol);
-      bulk_g2s(st + RB * NS, A.x + bl[2 * i + 1], 16u * NS, &fbar[i]);
+  int carry_out = 0;
+  if (threadIdx.x == 0) {
+    // blocks [0, carry) are in flight already; fill the ring up to nst blocks
+    for (int i = carry; i < min(nst, nb); ++i) {
+      const int s = (ring + i) % nst;
+      issue_block<NS, R>(A, bl, i, sm + (size_t)s * STG, &fbar[s], pol);
     }
+    for (int q = 0; nb + q < nst && q < next_ready(); ++q) {  // a short task: start the next one too
+      const int s = (ring + nb + q) % nst;
+      issue_block<NS, R>(A, bl_next, q, sm + (size_t)s * STG, &fbar[s], pol);
+      carry_out = q + 1;
+    }
+  }
   int li = 0;
   int leaf_end = (int)lv[1];
   double2 acc[R][2];
 #pragma unroll
   for (int r = 0; r < R; ++r) acc[r][0] = acc[r][1] = make_double2(0.0, 0.0);
   for (int i = 0; i < nb; ++i) {
-    const int s = i % nst;
+    const int s = (ring + i) % nst;
+    // the partner's x segment (L1/L2-resident input) is loaded while the stage is in flight
+    const cd2 xv = ld_cached256(A.x + bl[2 * i + 1] + col);
     mbar_wait(&fbar[s], (fphase >> s) & 1u);
     fphase ^= 1u << s;
     const double2* st = sm + (size_t)s * STG;
-    const double2 xa = st[RB * NS + col], xb = st[RB * NS + col + 1];
+    const double2 xa = xv.a, xb = xv.b;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const double2* d = st + (r0 + r * RPP) * NS + col;
@@ -140,14 +181,19 @@ __device__ __forceinline__ void near_task(const MegaArgs& A, const int4* rec, do
       }
       if (++li < nl) leaf_end += (int)lv[2 * li + 1];
     }
-    __syncthreads();  // stage s fully read: refill it
-    if (threadIdx.x == 0 && i + nst < nb) {
-      double2* sd = sm + (size_t)s * STG;
-      mbar_arrive_expect_tx(&fbar[s], 16u * STG);
-      bulk_g2s_hint(sd, A.dbuf + bl[2 * (i + nst)], 16u * RB * NS, &fbar[s], pol);
-      bulk_g2s(sd + RB * NS, A.x + bl[2 * (i + nst) + 1], 16u * NS, &fbar[s]);
+    __syncthreads();  // stage s fully read: refill it (this task's block i + nst, or the next task's)
+    if (threadIdx.x == 0) {
+      const int j = i + nst;
+      if (j < nb) {
+        issue_block<NS, R>(A, bl, j, sm + (size_t)s * STG, &fbar[s], pol);
+      } else if (j - nb >= carry_out && j - nb < next_ready()) {
+        issue_block<NS, R>(A, bl_next, j - nb, sm + (size_t)s * STG, &fbar[s], pol);
+        carry_out = j - nb + 1;
+      }
     }
   }
+  ring = (ring + nb) % nst;
+  return carry_out;  // meaningful in thread 0, the only thread that issues copies
 }
 
 // near-field of one leaf with arbitrary block shapes (warp per row); record: {leaf index}
@@ -231,115 +277,130 @@ __device__ __forceinline__ void couple_task(const MegaArgs& A, const int4* rec, 
 
 template <int NS, int R>
 __global__ void __launch_bounds__(MNT, 2) k_mega(MegaArgs A) {
+  // dynamic shared memory: [work area: near ring / span working set / coupling panels][this
+  // CTA's blob: its task list, dependency ranges and task records, one bulk copy]
   extern __shared__ __align__(16) double2 sm[];
   __shared__ double2 red[MNT];
-  __shared__ __align__(16) int4 recbuf[2][REC_SLOTS];
-  __shared__ uint64_t bar, rbar[2];
-  __shared__ uint64_t fbar[NST_MAX];
-  __shared__ int s_next;
   __shared__ uint32_t s_epoch;
-  uint32_t fphase = 0, phase = 0, rphase = 0;
+  __shared__ __align__(128) uint64_t bar, bbar;
+  __shared__ uint64_t fbar[NST_MAX];
+  uint32_t fphase = 0, phase = 0;
+  uint32_t ring = 0;  // near-field ring position (persists across the CTA's near tasks)
+  int carry = 0;      // blocks of the upcoming near task already in flight
   const int nst = NS > 0 ? max(1, min(NST_MAX, A.smem_elems / (R * (MNT / (NS / 2)) * NS + NS))) : 1;
   const uint64_t pol = policy_evict_first();
+  int4* blob = reinterpret_cast<int4*>(sm + A.smem_elems);
+  const int2 lst = A.cta_lists[blockIdx.x];  // {blob offset, blob length} in 16-byte slots
   if (threadIdx.x == 0) {
     for (int i = 0; i < NST_MAX; ++i) mbar_init(&fbar[i], 1);
     mbar_init(&bar, 1);
-    mbar_init(&rbar[0], 1);
-    mbar_init(&rbar[1], 1);
+    mbar_init(&bbar, 1);
     s_epoch = *(volatile uint32_t*)&A.ctrl->epoch;
+    if (lst.y > 0) {
+      mbar_arrive_expect_tx(&bbar, 16u * lst.y);
+      bulk_g2s(blob, A.recs + lst.x, 16u * lst.y, &bbar);
+    }
   }
   // warm the far-field operands into L2: every CTA's TMA unit takes an equal strided share
   // (a prefetch occupies the issuing SM's TMA unit, so it must not pile up on a few SMs)
   if (threadIdx.x == 0)
-  for (int i = blockIdx.x; i < A.n_prefetch; i += gridDim.x) {
-    const int4 r = A.prefetch[i];
-    const uint64_t p = (uint64_t)(uint32_t)r.x | ((uint64_t)(uint32_t)r.y << 32);
-    prefetch_l2(reinterpret_cast<const void*>(p), (uint32_t)r.z);
-  }
-  __syncthreads();
-  const uint32_t done = s_epoch + 1;
-  // claim the first task and start loading its record
-  if (threadIdx.x == 0) {
-    const int t = (int)atomicAdd(&A.ctrl->next, 1u);
-    s_next = t;
-    if (t < A.n_tasks) {
-      const Task tk = A.tasks[t];
-      mbar_arrive_expect_tx(&rbar[0], 16u * tk.rec_len);
-      bulk_g2s(recbuf[0], A.recs + tk.rec_off, 16u * tk.rec_len, &rbar[0]);
+    for (int i = blockIdx.x; i < A.n_prefetch; i += gridDim.x) {
+      const int4 r = A.prefetch[i];
+      const uint64_t p = (uint64_t)(uint32_t)r.x | ((uint64_t)(uint32_t)r.y << 32);
+      prefetch_l2(reinterpret_cast<const void*>(p), (uint32_t)r.z);
     }
-  }
   __syncthreads();
-  int t = s_next, buf = 0;
-  while (t < A.n_tasks) {
-    __syncthreads();  // everyone has read s_next
+  if (lst.y > 0) mbar_wait(&bbar, 0);
+  const uint32_t done = s_epoch + 1;
+  // This CTA's static task list (planned on the host, sorted in the global topological order:
+  // the lowest unfinished task is always at the head of some CTA's list, so no CTA can wait
+  // forever).  Near-field CTAs own a contiguous run of row panels and never wait.
+  const int n_my = lst.y > 0 ? blob[0].x : 0;
+  for (int k = 0; k < n_my; ++k) {
+    const int4 e0 = blob[1 + 2 * k], e1 = blob[2 + 2 * k];
+    const int t = e0.x, type = e0.y;
+    const int4* rec = blob + e0.z;
+    const int2* deps = reinterpret_cast<const int2*>(blob + e1.x);
+    const int n_dep = e1.y;
     if (A.trace && threadIdx.x == 0) {
       A.trace[8 * t] = gtimer();
       A.trace[8 * t + 4] = smid() | ((uint64_t)blockIdx.x << 32);
     }
-    const Task tk = A.tasks[t];
-    mbar_wait(&rbar[buf], (rphase >> buf) & 1u);  // this task's record is in shared memory
-    rphase ^= 1u << buf;
-    const int4* rec = recbuf[buf];
-    // static operands stream in while the dependencies are still outstanding
     const SpanHead* hd = reinterpret_cast<const SpanHead*>(rec);
     const SpanCopy* cps = reinterpret_cast<const SpanCopy*>(rec + (sizeof(SpanHead) + 15) / 16);
-    if (tk.type == T_SPAN)
-      span_stage_static<MNT>(hd, cps, A.B, sm, &bar);
-    else if (tk.type == T_COUPLE)
-      couple_stage_static(A, rec, sm, &bar);
-    // dependencies: every thread checks a share of the flags
-    for (int i = tk.dep_first; i < tk.dep_first + tk.n_dep; ++i) {
-      const DepRange rg = A.deps[i];
-      for (int d = rg.lo + threadIdx.x; d < rg.hi; d += MNT) {
-        long spins = 0;
-        while (ld_acquire(A.flags + d) != done) {
-          if (++spins > (1l << 26)) {  // never expected: report instead of hanging the GPU
-            atomicExch(&A.ctrl->error, 1u);
-            break;
+    // profiling aid (H2B_OPT_DEBUG): bit 0 skips far-field task bodies, bit 1 near-field ones
+    const bool skip = ((A.debug & 1) && type != T_NEAR) || ((A.debug & 2) && type == T_NEAR);
+    if (type != T_NEAR) {
+      // Every far-field task starts from a freshly initialised transaction barrier (parity 0).
+      // Carrying one barrier's parity across a CTA's mixed span / coupling tasks was measured
+      // to lose phase sync under load (1-3% of launches read a staging area before its bulk
+      // copies had landed); the previous task ended with a CTA barrier, so no thread still
+      // waits on the old phase and none of its copies is in flight.
+      if (threadIdx.x == 0) {
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&bar)) : "memory");
+        mbar_init(&bar, 1);
+      }
+      phase = 0;
+      // static operands stream in while the dependencies are still outstanding
+      if (!skip && type == T_SPAN)
+        span_stage_static<MNT>(hd, cps, A.B, sm, &bar);
+      else if (!skip)
+        couple_stage_static(A, rec, sm, &bar);
+    }
+    // dependencies: warp 0 polls (lanes share the flags) with a backoff, so waiting CTAs do not
+    // flood L2 with requests next to the near-field stream; the other warps wait at the barrier
+    if (threadIdx.x < 32)
+      for (int i = 0; i < n_dep; ++i) {
+        const int2 rg = deps[i];
+        for (int d = rg.x + threadIdx.x; d < rg.y; d += 32) {
+          long spins = 0;
+          while (ld_acquire(A.flags + d) != done) {
+            if (++spins > (1l << 24)) {  // never expected: report instead of hanging the GPU
+              atomicExch(&A.ctrl->error, 1u);
+              break;
+            }
+            __nanosleep(256);
           }
-          __nanosleep(32);
         }
       }
-    }
-    __syncthreads();  // dependencies met
-    // only now claim the next task (a claim must not wait behind a blocked task) and prefetch
-    // its record behind this task's execution
-    if (threadIdx.x == 0) {
-      const int tn = (int)atomicAdd(&A.ctrl->next, 1u);
-      s_next = tn;
-      if (tn < A.n_tasks) {
-        const Task tn_k = A.tasks[tn];
-        mbar_arrive_expect_tx(&rbar[buf ^ 1], 16u * tn_k.rec_len);
-        bulk_g2s(recbuf[buf ^ 1], A.recs + tn_k.rec_off, 16u * tn_k.rec_len, &rbar[buf ^ 1]);
-      }
-    }
-    // order the acquires before the async-proxy (TMA) reads of the produced data
-    asm volatile("fence.proxy.async.global;" ::: "memory");
     __syncthreads();
+    // order the acquires (made visible to every thread by the barrier) before the async-proxy
+    // (TMA) reads of the produced data: the fence follows the barrier in the issuing thread
+    if (n_dep) asm volatile("fence.proxy.async.global;" ::: "memory");
     if (A.trace && threadIdx.x == 0) A.trace[8 * t + 1] = gtimer();
-    if (tk.type == T_NEAR) {
-      if constexpr (NS == 0)
+    if (skip) {
+      // profiling aid only (H2B_OPT_DEBUG): this task's body is skipped
+    } else if (type == T_NEAR) {
+      if constexpr (NS == 0) {
         near_task_generic(A, rec[0].x);
-      else
-        near_task<NS, R>(A, rec, sm, fbar, fphase, nst, pol);
-    } else if (tk.type == T_SPAN) {
+      } else {
+        const bool next_near = k + 1 < n_my && blob[1 + 2 * (k + 1)].y == T_NEAR && !(A.debug & 2);
+        carry = near_task<NS, R>(A, rec, next_near ? blob + blob[1 + 2 * (k + 1)].z : nullptr, nullptr, 0,
+                                 sm, fbar, fphase, nst, pol, ring, carry);
+      }
+    } else if (type == T_SPAN) {
       span_finish<MNT>(hd, cps, A.B, sm, &bar, phase, A.trace ? A.trace + 8 * t + 2 : nullptr);
-      phase ^= 1u;
     } else {
       couple_task(A, rec, red, sm, &bar, phase);
     }
+    if (type != T_NEAR) {
+      // x̂ / ŷ written here with generic stores are read by other CTAs' TMA (async proxy), and
+      // this task's generic shared-memory writes precede the next task's TMA writes
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    // publish completion from a thread that does not feed the near-field ring (thread 0); a
+    // release at GPU scope costs ~0.4 us, so a near-field CTA publishes only its last panel
+    // (the planner points every dependency on its panels there)
+    if (threadIdx.x == 32 && e1.z) {
       __threadfence();
       st_release(A.flags + t, done);
       if (A.trace) A.trace[8 * t + 3] = gtimer();
     }
-    t = s_next;
-    buf ^= 1;
   }
   if (threadIdx.x == 0) {
-    if (atomicAdd(&A.ctrl->exited, 1u) == gridDim.x - 1) {  // last CTA out resets the queue
-      A.ctrl->next = 0;
+    if (atomicAdd(&A.ctrl->exited, 1u) == gridDim.x - 1) {  // last CTA out advances the epoch
       A.ctrl->exited = 0;
       __threadfence();
       A.ctrl->epoch = s_epoch + 1;
@@ -349,8 +410,18 @@ __global__ void __launch_bounds__(MNT, 2) k_mega(MegaArgs A) {
 
 template <int NS, int R>
 int launch(h2b_ctx* h, const MegaArgs& A, cudaStream_t st) {
-  k_mega<NS, R><<<h->mega_grid, MNT, h->mega_smem, st>>>(A);
-  H2B_CHECK_LAUNCH();
+  // cooperative launch: all CTAs co-resident (far-field CTAs wait on near-field CTAs)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(h->mega_grid);
+  cfg.blockDim = dim3(MNT);
+  cfg.dynamicSmemBytes = h->mega_smem + 16 * h->mega_blob_slots;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  H2B_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_mega<NS, R>, A));
   return H2B_OK;
 }
 
@@ -426,6 +497,9 @@ int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st)
   A.yhat = h->yhat;
   A.trace = h->trace;
   A.smem_elems = h->mega_smem / 16;
+  A.debug = h->mega_debug;
+  A.cta_lists = h->cta_lists;
+  A.task_list = h->task_list;
   const int ns = h->mega_ns, r = h->mega_r;
   if (ns == 32 && r == 1) return launch<32, 1>(h, A, st);
   if (ns == 32 && r == 2) return launch<32, 2>(h, A, st);

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstring>
 #include <functional>
+#include <queue>
 
 #include "h2b_common.cuh"
 #include "h2b_panel.cuh"
@@ -398,7 +399,8 @@ bool plan_with_split(const h2b_ctx* h, int ls, Plan& pl) {
 }
 
 // ------------------------- persistent-kernel task graph -------------------------
-constexpr int MEGA_BUDGET = 6000;  // double2 elements (96 KB): two CTAs per SM
+constexpr int MEGA_BUDGET = 5800;  // double2 elements (92.8 KB) of work area per CTA
+constexpr int MEGA_BLOB_MAX = 1024;  // 16-byte slots (16 KB) of per-CTA task blob
 
 std::vector<DepRange> to_ranges(std::vector<int> ids) {
   std::sort(ids.begin(), ids.end());
@@ -433,7 +435,10 @@ struct MegaPlan {
   std::vector<CoupleGroup> groups;
   std::vector<CoupleItem> citems;
   std::vector<int4> recs;
-  int ns = 0, r = 1, smem = 0, tiers = 0;
+  std::vector<int2> cta_lists;
+  std::vector<int> task_list;
+  int ns = 0, r = 1, smem = 0, tiers = 0, blob_slots = 0;
+  double est_makespan = 0.0;
 };
 
 bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
@@ -489,11 +494,12 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
   mp.smem = 16 * smem;
   // ---- task list -------------------------------------------------------------------
   // self-contained task records (see Task in h2b_common.cuh)
+  std::vector<int4>* rec_out = &mp.recs;
   auto push_slots = [&](const void* data, size_t bytes) {
     const size_t n = (bytes + 15) / 16;
-    const size_t at = mp.recs.size();
-    mp.recs.resize(at + n, int4{0, 0, 0, 0});
-    std::memcpy(mp.recs.data() + at, data, bytes);
+    const size_t at = rec_out->size();
+    rec_out->resize(at + n, int4{0, 0, 0, 0});
+    std::memcpy(rec_out->data() + at, data, bytes);
   };
   auto make_record = [&](int type, int arg) -> bool {
     if (type == T_SPAN) {
@@ -530,14 +536,18 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
     }
     return true;
   };
-  auto add_task = [&](int type, int arg, const std::vector<int>& dep_ids) {
-    Task t{type, arg, (int)mp.deps.size(), 0, (int64_t)mp.recs.size(), 0, 0};
-    make_record(type, arg);
-    t.rec_len = (int)((int64_t)mp.recs.size() - t.rec_off);
-    for (auto& rg : to_ranges(dep_ids)) mp.deps.push_back(rg);
-    t.n_dep = (int)mp.deps.size() - t.dep_first;
-    mp.tasks.push_back(t);
-    return (int)mp.tasks.size() - 1;
+  // ---- logical task graph; the queue order is decided afterwards by a simulation --------
+  struct LTask {
+    int type, arg;
+    std::vector<int> deps;  // logical ids
+    double dur;             // estimated run time (us)
+  };
+  std::vector<LTask> lt;
+  const double G = (double)std::max(1, grid_est);
+  const double cta_bw = 6.5e6 / G;  // bytes per microsecond per CTA when all CTAs stream
+  auto add_l = [&](int type, int arg, std::vector<int> deps, double dur) {
+    lt.push_back({type, arg, std::move(deps), dur});
+    return (int)lt.size() - 1;
   };
   // the clusters a span computes (for producer / consumer maps)
   auto span_clusters = [&](int tier_i, int root, bool with_input) {
@@ -550,6 +560,7 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
       for (int p = R[i].a; p < R[i].b; ++p) cl.push_back(p);
     return cl;
   };
+  auto span_dur = [&](int head) { return 2.0 + 0.7 * mp.prog.heads[head].nlev; };
   // ---- near-field work list (leaf order) --------------------------------------------
   const int ns = h->uniform_leaf;
   const int nleaves = (int)h->h_leaves.size();
@@ -561,7 +572,12 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
                              (int32_t)(h->d_row_ptr[t + 1] - h->d_row_ptr[t]), 0, 0});
   }
   std::vector<NearTask>& nts = mp.near_tasks;
+  std::vector<double> nt_bytes;
   std::vector<int> nt_of_leaf_last(nleaves, -1);
+  auto leaf_nb = [&](int i) {
+    const int t = h->h_leaves[i];
+    return (int)(h->d_row_ptr[t + 1] - h->d_row_ptr[t]);
+  };
   if (ns == 32 || ns == 64) {
     const double avg_nb = (double)h->n_near / std::max(1, nleaves);
     const double row_bytes = ns * 16.0 * avg_nb;
@@ -575,35 +591,35 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
       for (int i = 0; i < nleaves; ++i)
         for (int r0 = 0; r0 < ns; r0 += rb) {
           nts.push_back({i, 1, r0, 0});
+          nt_bytes.push_back(16.0 * rb * ns * leaf_nb(i));
           nt_of_leaf_last[i] = (int)nts.size() - 1;
         }
     } else {
-      // group whole leaves into tasks of ~192 KB, bounded by the record size
-      const int per = std::max(1, (int)(192e3 / (ns * row_bytes) + 0.5));
+      // group whole leaves into tasks of ~96 KB (the ring streams on across task boundaries)
+      const int per = std::max(1, (int)(96e3 / (ns * row_bytes) + 0.5));
       int i = 0;
       while (i < nleaves) {
         int c = 0, blocks = 0;
         while (i + c < nleaves && c < per && c < 64) {
-          const int t = h->h_leaves[i + c];
-          const int nb = (int)(h->d_row_ptr[t + 1] - h->d_row_ptr[t]);
+          const int nb = leaf_nb(i + c);
           if (c > 0 && blocks + nb > NEAR_REC_MAXB) break;
           blocks += nb;
           ++c;
         }
         nts.push_back({i, c, 0, 0});
+        nt_bytes.push_back(16.0 * ns * ns * blocks);
         for (int j = i; j < i + c; ++j) nt_of_leaf_last[j] = (int)nts.size() - 1;
         i += c;
       }
     }
-    for (int i = 0; i < nleaves; ++i) {  // a single leaf must fit a record too
-      const int t = h->h_leaves[i];
-      if (h->d_row_ptr[t + 1] - h->d_row_ptr[t] > NEAR_REC_MAXB) return false;
-    }
+    for (int i = 0; i < nleaves; ++i)  // a single leaf must fit a record too
+      if (leaf_nb(i) > NEAR_REC_MAXB) return false;
   } else {
     mp.ns = 0;
     mp.r = 1;
     for (int i = 0; i < nleaves; ++i) {
       nts.push_back({i, 1, 0, 0});
+      nt_bytes.push_back(16.0 * h->c_size[h->h_leaves[i]] * 64.0 * leaf_nb(i));
       nt_of_leaf_last[i] = (int)nts.size() - 1;
     }
   }
@@ -611,38 +627,25 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
   for (size_t k = 0; k < nts.size(); ++k)
     for (int j = nts[k].leaf_first; j < nts[k].leaf_first + nts[k].n_leaves; ++j)
       if (nt_first_of_leaf[j] < 0) nt_first_of_leaf[j] = (int)k;
-  std::vector<int> nt_task(nts.size(), -1);
-  auto emit_near = [&](size_t k) {
-    nt_task[k] = add_task(T_NEAR, ns == 32 || ns == 64 ? (int)k : nts[k].leaf_first, {});
-  };
-  // Queue order: the far-field tasks are spaced out by waves of near tasks (taken from the END
-  // of the leaf order, whose backward spans come last) so that a far task is usually claimed
-  // after its dependencies finished instead of parking a CTA.
-  const size_t nn = nts.size();
-  const size_t wave = (size_t)std::max(1, grid_est);
-  const size_t n_early = std::min(nn, (5 * wave) / 2);
-  size_t early_next = nn - n_early;
-  auto emit_early = [&](size_t cnt) {
-    for (size_t c = 0; c < cnt && early_next < nn; ++c) emit_near(early_next++);
-  };
+  const int n_near = (int)nts.size();
+  for (int k = 0; k < n_near; ++k)
+    add_l(T_NEAR, ns == 32 || ns == 64 ? k : nts[k].leaf_first, {}, 0.5 + nt_bytes[k] / cta_bw);
+  // ---- far-field tasks in topological order ---------------------------------------------
   std::vector<int> up_task(h->P, -1), up_of_span_root(h->P, -1);
-  // A. forward spans, bottom tier first (upper tiers after one wave of near-field work)
-  for (int i = 0; i < m; ++i) {
-    if (i == 1) emit_early(wave);
+  for (int i = 0; i < m; ++i)  // A. forward spans, bottom tier first
     for (auto& s : tier[i]) {
       std::vector<int> deps;
       if (i > 0)  // children spans: tier i-1 spans rooted inside this span's input level
         for (int p : span_clusters(i, s.root, true))
           if (up_of_span_root[p] >= 0 && level_of(h, p) == splits[i - 1]) deps.push_back(up_of_span_root[p]);
       if (s.up_head < 0) continue;
-      const int id = add_task(T_SPAN, s.up_head, deps);
+      const int id = add_l(T_SPAN, s.up_head, deps, span_dur(s.up_head));
       up_of_span_root[s.root] = id;
       for (int p : span_clusters(i, s.root, false)) up_task[p] = id;
     }
-  }
-  emit_early(m > 1 ? wave / 2 : wave + wave / 2);
   // B. coupling groups (targets in packed order; panels + gathered x̂ bounded by the budget)
   std::vector<int> group_task(h->P, -1);
+  std::vector<std::vector<int>> group_members;  // targets of each coupling group (plan check)
   int couple_smem = 0;
   {
     const int64_t cap = 4000;  // double2 elements per warp-mode group (64 KB)
@@ -651,13 +654,14 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
       const int64_t e0 = (int64_t)citems_all[i].R * citems_all[i].w + citems_all[i].R;
       CoupleGroup g{(int)mp.citems.size(), 0, 0, 0};
       std::vector<int> members;
-      int64_t elems = 0;
+      int64_t elems = 0, pelems = 0;
       if (e0 > 3000) {  // a big panel: the whole CTA streams it
         if (citems_all[i].R > MEGA_BUDGET) return false;
         g.cta_mode = 1;
         mp.citems.push_back(citems_all[i]);
         members.push_back(targets[i]);
         elems = citems_all[i].R;
+        pelems = (int64_t)citems_all[i].R * citems_all[i].w;
         ++i;
       } else {
         while (i < citems_all.size() && (int)members.size() < 64) {
@@ -666,6 +670,7 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
           mp.citems.push_back(citems_all[i]);
           members.push_back(targets[i]);
           elems += e;
+          pelems += (int64_t)citems_all[i].R * citems_all[i].w;
           ++i;
         }
       }
@@ -674,17 +679,17 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
       std::vector<int> deps;
       for (int t : members)
         for (int64_t b = h->s_row_ptr[t]; b < h->s_row_ptr[t + 1]; ++b) {
-          const int s = h->s_col[b];
-          if (h->c_rank[s] > 0 && up_task[s] >= 0) deps.push_back(up_task[s]);
+          const int sc = h->s_col[b];
+          if (h->c_rank[sc] > 0 && up_task[sc] >= 0) deps.push_back(up_task[sc]);
         }
       mp.groups.push_back(g);
-      const int id = add_task(T_COUPLE, (int)mp.groups.size() - 1, deps);
+      group_members.push_back(members);
+      const int id = add_l(T_COUPLE, (int)mp.groups.size() - 1, deps, 1.5 + 16.0 * pelems / 2e4);
       for (int t : members) group_task[t] = id;
     }
   }
   mp.smem = std::max(mp.smem, 16 * couple_smem);
-  emit_early(nn);  // the rest of the early wave
-  // C. backward spans of the upper tiers, root tier first
+  // C. backward spans, root tier first; D. bottom tier after the near tasks of its leaves
   std::vector<int> dn_writer(h->P, -1);  // task that last wrote ŷ of a tier root
   auto down_deps = [&](int tier_i, const SpanRef& s) {
     std::vector<int> deps;
@@ -696,51 +701,209 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
   for (int i = m - 1; i >= 1; --i)
     for (auto& s : tier[i]) {
       if (s.dn_head < 0) continue;
-      const int id = add_task(T_SPAN, s.dn_head, down_deps(i, s));
-      // this span writes back ŷ of its input level: the lower tier's roots
+      const int id = add_l(T_SPAN, s.dn_head, down_deps(i, s), span_dur(s.dn_head));
       auto R = desc_ranges(h, s.root, splits[i - 1] - splits[i] + 1);
-      for (int p = R.back().a; p < R.back().b; ++p) dn_writer[p] = id;
+      for (int p = R.back().a; p < R.back().b; ++p) dn_writer[p] = id;  // writes back the input level
     }
-  // D. the remaining near-field tasks in leaf order, each bottom backward span emitted once
-  //    the near tasks of its own leaves and of the next span's leaves are in the queue
-  const size_t n_late = nn - n_early;
-  std::vector<int> span_need;  // last late near-task index a bottom span waits for (-1: none)
   for (auto& s : tier[0]) {
-    int need = -1;
-    for (int p : span_clusters(0, s.root, true))
-      if (leaf_pos[p] >= 0)
-        for (int k = nt_first_of_leaf[leaf_pos[p]]; k <= nt_of_leaf_last[leaf_pos[p]]; ++k)
-          if ((size_t)k < n_late) need = std::max(need, k);
-    span_need.push_back(need);
-  }
-  size_t next_bd = 0;
-  auto emit_bd = [&](size_t j) {
-    const SpanRef& s = tier[0][j];
-    if (s.dn_head < 0) return;
+    if (s.dn_head < 0) continue;
     std::vector<int> deps = down_deps(0, s);
     for (int p : span_clusters(0, s.root, true))
       if (leaf_pos[p] >= 0)
-        for (int k = nt_first_of_leaf[leaf_pos[p]]; k <= nt_of_leaf_last[leaf_pos[p]]; ++k)
-          deps.push_back(nt_task[k]);
-    add_task(T_SPAN, s.dn_head, deps);
-  };
-  auto flush_bd = [&](long k) {
-    while (next_bd < tier[0].size()) {
-      const size_t gate = std::min(next_bd + 1, tier[0].size() - 1);
-      if (span_need[gate] <= k && span_need[next_bd] <= k) {
-        emit_bd(next_bd);
-        ++next_bd;
+        for (int k = nt_first_of_leaf[leaf_pos[p]]; k <= nt_of_leaf_last[leaf_pos[p]]; ++k) deps.push_back(k);
+    add_l(T_SPAN, s.dn_head, deps, span_dur(s.dn_head));
+  }
+  // ---- static schedule -----------------------------------------------------------------
+  // CTA roles: the first g_near CTAs stream the near field (contiguous runs of row panels of
+  // ~equal bytes, never waiting); the others run the far-field tasks, assigned by list
+  // scheduling (earliest-ready task to the earliest-free CTA) against estimated durations.
+  // Global order = near panels, then far tasks in assignment order; every CTA's list is
+  // sorted by it and every dependency points to an earlier task.
+  const int nl_all = (int)lt.size();
+  const int n_far = nl_all - n_near;
+  const int g_total = std::max(2, grid_est);
+  int g_near = std::max(1, std::min(n_near, g_total / 2));
+  if (const char* e = getenv("H2B_DEBUG_GNEAR")) g_near = std::max(1, std::min(n_near, atoi(e)));  // profiling
+  int g_far = n_far > 0 ? g_total - g_near : 0;
+  if (n_far == 0) g_near = std::min(n_near, g_total);
+  std::vector<double> fin(nl_all, 0.0);
+  std::vector<std::vector<int>> lists(g_near + g_far);
+  {
+    double tot = 0.0;
+    for (int k = 0; k < n_near; ++k) tot += nt_bytes[k];
+    const double per_cta = tot / g_near, bw = 6.5e6 / g_near;
+    double acc = 0.0, cta_t = 0.0;
+    int c = 0;
+    for (int k = 0; k < n_near; ++k) {
+      if (c < g_near - 1 && acc >= per_cta * (c + 1)) {
+        ++c;
+        cta_t = 0.0;
+      }
+      acc += nt_bytes[k];
+      cta_t += 1.0 + nt_bytes[k] / bw;
+      fin[k] = cta_t;
+      lists[c].push_back(k);
+    }
+  }
+  std::vector<int> order;  // far tasks in assignment order
+  if (n_far > 0) {
+    std::vector<int> missing(nl_all, 0);
+    std::vector<std::vector<int>> users(nl_all);
+    for (int id = n_near; id < nl_all; ++id)
+      for (int d : lt[id].deps)
+        if (d >= n_near) {
+          ++missing[id];
+          users[d].push_back(id);
+        }
+    auto ready_time = [&](int id) {
+      double r = 0.0;
+      for (int d : lt[id].deps) r = std::max(r, fin[d]);
+      return r;
+    };
+    using QE = std::pair<double, int>;
+    std::priority_queue<QE, std::vector<QE>, std::greater<QE>> cand, cta_free;
+    for (int id = n_near; id < nl_all; ++id)
+      if (missing[id] == 0) cand.push({ready_time(id), id});
+    for (int c = 0; c < g_far; ++c) cta_free.push({0.0, g_near + c});
+    while (!cand.empty()) {
+      const auto [rt, id] = cand.top();
+      cand.pop();
+      const auto [ft, c] = cta_free.top();
+      cta_free.pop();
+      fin[id] = std::max(rt, ft) + lt[id].dur;
+      cta_free.push({fin[id], c});
+      lists[c].push_back(id);
+      order.push_back(id);
+      for (int u : users[id])
+        if (--missing[u] == 0) cand.push({ready_time(u), u});
+    }
+    if ((int)order.size() != n_far) return false;  // cycle: cannot happen
+  }
+  // ---- emit: global task table (flags, tracing) + one self-contained blob per CTA --------
+  std::vector<int> qid(nl_all, -1);
+  for (int k = 0; k < n_near; ++k) qid[k] = k;
+  for (int i = 0; i < n_far; ++i) qid[order[i]] = n_near + i;
+  std::vector<int> by_q(nl_all);
+  for (int id = 0; id < nl_all; ++id) by_q[qid[id]] = id;
+  for (int pos = 0; pos < nl_all; ++pos) {
+    const LTask& l = lt[by_q[pos]];
+    mp.tasks.push_back(Task{l.type, l.arg, 0, 0, 0, 0, 0});
+  }
+  std::vector<int> near_run_last(n_near, -1);  // last panel of the near CTA run holding k
+  for (int c = 0; c < g_near; ++c)
+    for (int k : lists[c]) near_run_last[k] = lists[c].back();
+  mp.blob_slots = 0;
+  for (auto& l : lists) {
+    // [header][2 entry slots per task][dependency ranges][records]
+    std::vector<int4> blob(1 + 2 * l.size(), int4{0, 0, 0, 0});
+    blob[0] = int4{(int)l.size(), 0, 0, 0};
+    for (size_t i = 0; i < l.size(); ++i) {
+      const LTask& lk = lt[l[i]];
+      std::vector<int> dq;
+      for (int d : lk.deps) dq.push_back(qid[d < n_near ? near_run_last[d] : d]);
+      const auto rg = to_ranges(dq);
+      const int dep_off = (int)blob.size();
+      for (size_t j = 0; j < rg.size(); j += 2) {
+        int4 v{rg[j].lo, rg[j].hi, 0, 0};
+        if (j + 1 < rg.size()) v.z = rg[j + 1].lo, v.w = rg[j + 1].hi;
+        blob.push_back(v);
+      }
+      std::vector<int4> rec;
+      rec_out = &rec;
+      make_record(lk.type, lk.arg);
+      const int rec_off = (int)blob.size();
+      blob.insert(blob.end(), rec.begin(), rec.end());
+      blob[1 + 2 * i] = int4{qid[l[i]], lk.type, rec_off, (int)rec.size()};
+      // near panels publish completion only at the end of their CTA's run
+      const bool publish = l[i] >= n_near || near_run_last[l[i]] == l[i];
+      blob[2 + 2 * i] = int4{dep_off, (int)rg.size(), publish ? 1 : 0, 0};
+    }
+    if ((int)blob.size() > MEGA_BLOB_MAX) return false;
+    mp.cta_lists.push_back({(int)mp.recs.size(), l.empty() ? 0 : (int)blob.size()});
+    if (!l.empty()) mp.recs.insert(mp.recs.end(), blob.begin(), blob.end());
+    mp.blob_slots = std::max(mp.blob_slots, (int)blob.size());
+  }
+  mp.est_makespan = *std::max_element(fin.begin(), fin.end());
+  if (getenv("H2B_VERIFY_PLAN")) {
+    // self-check (debugging aid): every two tasks that touch the same x̂ / ŷ / y elements, one
+    // of them writing, must be ordered by the schedule (CTA list order + dependency edges)
+    struct Acc {
+      int space;  // 0 x̂, 1 ŷ, 2 y
+      int64_t lo, hi;
+      bool w;
+      int q;
+    };
+    std::vector<Acc> acc;
+    for (int id = 0; id < nl_all; ++id) {
+      const LTask& l = lt[id];
+      const int q = qid[id];
+      if (l.type == T_NEAR) {
+        const int lf = ns == 32 || ns == 64 ? nts[l.arg].leaf_first : l.arg;
+        const int nlf = ns == 32 || ns == 64 ? nts[l.arg].n_leaves : 1;
+        const int rb = ns == 32 || ns == 64 ? mp.r * (256 / (ns / 2)) : 1 << 30;
+        for (int li = lf; li < lf + nlf; ++li) {
+          const int t = h->h_leaves[li];
+          const int64_t r0 = (int64_t)h->c_start[t] + (ns == 32 || ns == 64 ? nts[l.arg].row0 : 0);
+          acc.push_back({2, r0, std::min<int64_t>(r0 + rb, (int64_t)h->c_start[t] + h->c_size[t]), true, q});
+        }
+      } else if (l.type == T_SPAN) {
+        const SpanHead& hd = mp.prog.heads[l.arg];
+        int op_first = -1;
+        for (int c = hd.copy_first; c < hd.copy_first + hd.n_copy; ++c) {
+          const SpanCopy& cp = mp.prog.copies[c];
+          if (cp.kind == SRC_XHAT || cp.kind == SRC_YHAT)
+            acc.push_back({cp.kind == SRC_XHAT ? 0 : 1, cp.src, cp.src + cp.elems, false, q});
+          if (cp.kind == SRC_OPS) op_first = (int)(cp.src / 2);
+        }
+        for (int c = hd.out_first; c < hd.out_first + hd.n_out; ++c) {
+          const SpanCopy& cp = mp.prog.outs[c];
+          acc.push_back({cp.kind == SRC_XHAT ? 0 : 1, cp.src, cp.src + cp.elems, true, q});
+        }
+        for (int o = op_first; o >= 0 && o < op_first + hd.n_ops; ++o) {
+          const SpanOp& op = mp.prog.ops[o];
+          if (op.flags & OP_OUT_Y) acc.push_back({2, op.out, (int64_t)op.out + op.w, true, q});
+        }
       } else {
-        break;
+        for (int t : group_members[l.arg]) {
+          acc.push_back({1, h->c_xoff[t], h->c_xoff[t] + h->c_rank[t], true, q});
+          for (int64_t b = h->s_row_ptr[t]; b < h->s_row_ptr[t + 1]; ++b) {
+            const int sc = h->s_col[b];
+            acc.push_back({0, h->c_xoff[sc], h->c_xoff[sc] + h->c_rank[sc], false, q});
+          }
+        }
       }
     }
-  };
-  flush_bd(-1);
-  for (size_t k = 0; k < n_late; ++k) {
-    emit_near(k);
-    flush_bd((long)k);
+    // happens-before closure over queue ids (every edge goes to a larger id)
+    const int W = (nl_all + 63) / 64;
+    std::vector<std::vector<uint64_t>> reach(nl_all, std::vector<uint64_t>(W, 0));
+    std::vector<std::vector<int>> preds(nl_all);
+    for (auto& l : lists)
+      for (size_t i = 1; i < l.size(); ++i) preds[qid[l[i]]].push_back(qid[l[i - 1]]);
+    for (int id = 0; id < nl_all; ++id)
+      for (int d : lt[id].deps) preds[qid[id]].push_back(qid[d < n_near ? near_run_last[d] : d]);
+    for (int v = 0; v < nl_all; ++v)
+      for (int p : preds[v]) {
+        for (int w = 0; w < W; ++w) reach[v][w] |= reach[p][w];
+        reach[v][p / 64] |= 1ull << (p % 64);
+      }
+    auto before = [&](int a, int b) { return (reach[b][a / 64] >> (a % 64)) & 1ull; };
+    int bad = 0;
+    for (size_t i = 0; i < acc.size(); ++i) {
+      if (!acc[i].w) continue;
+      for (size_t j = 0; j < acc.size(); ++j) {
+        const Acc &a = acc[i], &b = acc[j];
+        if (i == j || a.space != b.space || a.q == b.q || b.hi <= a.lo || a.hi <= b.lo) continue;
+        if (b.w && j < i) continue;  // write/write pairs once
+        if (before(a.q, b.q) || before(b.q, a.q)) continue;
+        if (++bad <= 20)
+          fprintf(stderr, "plan check: unordered %s task %d (type %d arg %d) / %s task %d (type %d arg %d) on %s [%lld, %lld)\n",
+                  "write", a.q, mp.tasks[a.q].type, mp.tasks[a.q].arg, b.w ? "write" : "read", b.q,
+                  mp.tasks[b.q].type, mp.tasks[b.q].arg, a.space == 0 ? "xhat" : a.space == 1 ? "yhat" : "y",
+                  (long long)std::max(a.lo, b.lo), (long long)std::min(a.hi, b.hi));
+      }
+    }
+    fprintf(stderr, "plan check: %d tasks, %zu accesses, %d unordered conflicts\n", nl_all, acc.size(), bad);
   }
-  while (next_bd < tier[0].size()) emit_bd(next_bd++);
   return true;
 }
 
@@ -884,6 +1047,8 @@ int h2b_prepare(h2b_ctx* h) {
       H2B_TRY(to_device(&h->leaf_items, mp.leaf_items, &acc));
       H2B_TRY(to_device(&h->couple_groups, mp.groups, &acc));
       H2B_TRY(to_device(&h->rec_pool, mp.recs, &acc));
+      H2B_TRY(to_device(&h->cta_lists, mp.cta_lists, &acc));
+      h->mega_blob_slots = mp.blob_slots;
       {  // far-field operands warmed into L2 at every launch (64 KB pieces)
         std::vector<int4> pf;
         auto add = [&](const void* p, int64_t bytes) {
@@ -918,12 +1083,14 @@ int h2b_prepare(h2b_ctx* h) {
       // near-field stages use the whole budget (2 CTAs per SM still fit)
       h->mega_smem = std::max(mp.smem, mp.ns > 0 ? 16 * MEGA_BUDGET : 16);
       h->mega_tiers = mp.tiers;
-      H2B_TRY(h2b_mega_set_smem(mp.ns, mp.r, 100 * 1024));
+      H2B_TRY(h2b_mega_set_smem(mp.ns, mp.r, 16 * (MEGA_BUDGET + MEGA_BLOB_MAX)));
       int per_sm = 0, sms = 0;
-      H2B_TRY(h2b_mega_occupancy(mp.ns, mp.r, h->mega_smem, &per_sm));
+      H2B_TRY(h2b_mega_occupancy(mp.ns, mp.r, h->mega_smem + 16 * h->mega_blob_slots, &per_sm));
       H2B_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-      h->mega_grid = std::max(1, std::min(per_sm * sms, h->n_tasks));
-      h->mega = per_sm > 0 ? 1 : 0;
+      // the static schedule assumed 2 CTAs per SM: the launch must be fully co-resident
+      h->mega_grid = (int)mp.cta_lists.size();
+      h->mega = (per_sm > 0 && h->mega_grid <= per_sm * sms) ? 1 : 0;
+      h->mega_est_us = mp.est_makespan;
     }
   }
   if (h->mega) {  // the multi-kernel programs below are still planned for phase timing

@@ -25,9 +25,9 @@ template <int NTH>
 __device__ __forceinline__ void span_stage_static(const SpanHead* __restrict__ hd,
                                                   const SpanCopy* __restrict__ copies,
                                                   const SpanBases& B, double2* sm, uint64_t* bar) {
+  const int n_copy = hd->n_copy, c_first = hd->copy_first;
   if (threadIdx.x == 0) mbar_arrive_expect_tx(bar, (uint32_t)hd->pad[0]);  // total staged bytes
   __syncthreads();
-  const int n_copy = hd->n_copy, c_first = hd->copy_first;
   for (int i = threadIdx.x; i < n_copy; i += NTH) {
     const SpanCopy c = copies[c_first + i];
     if (!span_src_dynamic(c.kind)) bulk_g2s(sm + c.smem, B.src[c.kind] + c.src, 16u * (uint32_t)c.elems, bar);

@@ -175,3 +175,41 @@ def test_persistent_kernel_repeated_launches(k):
     flag = C_int64()
     _abi.check(_abi.lib().h2b_query(op.handle, _abi.Q_MEGA, flag))
     assert flag.value == 1
+
+
+def _stress(pk, launches, seed=1):
+    """`launches` persistent-kernel matvecs with a changing input, each compared with the
+    multi-kernel path: catches ordering races between tasks of the single launch."""
+    import torch
+    from paper_1703_01175_b200 import H2Operator, _abi
+    L = _abi.lib()
+    a, b = H2Operator(pk), H2Operator(pk)
+    _abi.check(L.h2b_set_option(b.handle, _abi.OPT_MEGA, 0))
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    V = torch.randn(17, pk.n, dtype=torch.complex128, device="cuda", generator=g)
+    y = torch.zeros(pk.n, dtype=torch.complex128, device="cuda")
+    worst = 0.0
+    for it in range(launches):
+        i = it % 16
+        a.matvec_perm(V[i], out=y)
+        yb = b.matvec_perm(V[i])
+        worst = max(worst, (torch.linalg.norm(y - yb) / torch.linalg.norm(yb)).item())
+        if it % 3 == 0:  # inputs rewritten between launches, as in a Krylov loop
+            V[i + 1].copy_(yb / torch.linalg.norm(yb))
+    err = C_int64()
+    _abi.check(L.h2b_query(a.handle, _abi.Q_DEVICE_ERROR, err))
+    assert err.value == 0
+    return worst
+
+
+@pytest.mark.parametrize("name", ["cube8", "line2048", "plate32"])
+def test_persistent_kernel_stress_golden(name):
+    pk, _ = load_golden(name)
+    assert _stress(pk, 300) <= 1e-13
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_persistent_kernel_stress_config(k):
+    pk, _ = load_config(k)
+    assert _stress(pk, 400) <= 1e-13

@@ -29,7 +29,10 @@ import time
 
 import numpy as np
 
-REF_SRC = "/root/reference/pkg/src"
+# H2VIE_SRC may point at a scratch copy of the reference with its Cython backend built
+# (cp -r /root/reference/pkg /tmp/h2ref && python setup.py build_ext --inplace): same code,
+# 2.5-4x faster block assembly for the large configs.
+REF_SRC = os.environ.get("H2VIE_SRC", "/root/reference/pkg/src")
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, REF_SRC)

@@ -1,0 +1,28 @@
+"""Time the persistent kernel with far-field or near-field task bodies skipped (profiling aid)."""
+import sys, os, ctypes as C
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_1703_01175_b200 import H2Operator, load_packed, _abi
+L = _abi.lib()
+for k in [int(a) for a in sys.argv[1:]] or [1, 2]:
+    pk, ex = load_packed(f"data/cfg{k}.npz", with_extra=True)
+    op = H2Operator(pk)
+    _abi.check(L.h2b_prepare_handle(op.handle))
+    x = torch.from_numpy(ex["x"][pk.perm, 0].copy()).cuda(); y = torch.empty_like(x)
+    from paper_1703_01175_b200.timing import L2Flusher
+    flush = L2Flusher("cuda")
+    res = {}
+    for dbg, name in ((0, "full"), (1, "near only"), (2, "far only"), (3, "no bodies")):
+        _abi.check(L.h2b_set_option(op.handle, 4, dbg))
+        for _ in range(3): op.matvec_perm(x, out=y)
+        tot = 0.0
+        for _ in range(20):
+            flush.flush()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(); op.matvec_perm(x, out=y); e.record(); torch.cuda.synchronize()
+            tot += s.elapsed_time(e)
+        res[name] = tot / 20 * 1e3
+    _abi.check(L.h2b_set_option(op.handle, 4, 0))
+    nb = pk.near_bytes()
+    print(f"cfg{k}: " + "  ".join(f"{n} {v:.1f} us" for n, v in res.items()) +
+          f"  | near-only {nb / res['near only'] / 1e3:.0f} GB/s")
