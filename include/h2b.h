@@ -142,6 +142,11 @@ int h2b_get_trace(h2b_handle h, int64_t* out, int64_t max_tasks);
 #define H2B_Q_MEGA_GRID 8     /* CTAs it launches */
 #define H2B_Q_MEGA_TIERS 9    /* tiers of span programs */
 #define H2B_Q_DEVICE_ERROR 10 /* nonzero if a dependency wait ever timed out (a bug) */
+#define H2B_Q_NEAR_TASKS 11   /* near-field tasks of the q=1 stream kernel */
+#define H2B_Q_NEAR_STAGES 12  /* TMA ring stages of the near-field stream kernel */
+#define H2B_Q_NEAR_SMEM 13    /* dynamic shared memory of the near-field stream kernel (bytes) */
+#define H2B_Q_MEGA_SMEM 14    /* dynamic shared memory of the far-field task-graph kernel (bytes) */
+#define H2B_Q_NEAR_VARIANT 15 /* 100 * leaf size + rows per thread of the near kernel (0: generic) */
 int h2b_query(h2b_handle h, int what, int64_t* out);
 
 /* Permutation helpers on device buffers: out[i,:] = in[perm[i],:] (gather,

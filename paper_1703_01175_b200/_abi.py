@@ -25,6 +25,7 @@ EXPORTED = (
 OPT_GRAPHS, OPT_MEGA, OPT_TRACE = 1, 2, 3
 Q_LAUNCHES_Q1, Q_SPAN_MODE, Q_SPLIT_LEVEL, Q_TOP_STAGED, Q_DEVICE_BYTES = 1, 2, 3, 4, 5
 Q_MEGA, Q_MEGA_TASKS, Q_MEGA_GRID, Q_MEGA_TIERS, Q_DEVICE_ERROR = 6, 7, 8, 9, 10
+Q_NEAR_TASKS, Q_NEAR_STAGES, Q_NEAR_SMEM, Q_MEGA_SMEM, Q_NEAR_VARIANT = 11, 12, 13, 14, 15
 
 _i32p = C.POINTER(C.c_int32)
 _i64p = C.POINTER(C.c_int64)

@@ -41,7 +41,7 @@ void free_ctx(h2b_ctx* h) {
                   h->couple_targets, h->span_heads, h->span_copies, h->span_outs,
                   h->span_ops, h->near_items, h->near_blks, h->couple_items, h->tasks, h->deps,
                   h->near_tasks, h->leaf_items, h->couple_groups, h->ctrl, h->flags, h->trace,
-                  h->rec_pool, h->l2_prefetch, h->cta_lists, h->task_list};
+                  h->rec_pool, h->l2_prefetch, h->cta_lists, h->task_list, h->near_recs, h->near_idx};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->far_stream) cudaStreamDestroy(h->far_stream);
@@ -307,6 +307,11 @@ int h2b_query(h2b_handle h, int what, int64_t* out) {
     case H2B_Q_MEGA_TASKS: *out = h->n_tasks; return H2B_OK;
     case H2B_Q_MEGA_GRID: *out = h->mega_grid; return H2B_OK;
     case H2B_Q_MEGA_TIERS: *out = h->mega_tiers; return H2B_OK;
+    case H2B_Q_NEAR_TASKS: *out = h->n_near_tasks; return H2B_OK;
+    case H2B_Q_NEAR_STAGES: *out = h->near_nst; return H2B_OK;
+    case H2B_Q_NEAR_SMEM: *out = h->near_smem; return H2B_OK;
+    case H2B_Q_MEGA_SMEM: *out = h->mega_smem + 16 * h->mega_blob_slots; return H2B_OK;
+    case H2B_Q_NEAR_VARIANT: *out = 100 * h->mega_ns + h->mega_r; return H2B_OK;
     case H2B_Q_DEVICE_ERROR: {
       MegaCtrl c{};
       if (h->ctrl) H2B_CUDA_TRY(cudaMemcpy(&c, h->ctrl, sizeof(c), cudaMemcpyDeviceToHost));

@@ -178,7 +178,9 @@ struct CoupleGroup {
   int32_t item_first, n_items, cta_mode, pad;
 };
 struct MegaCtrl {
-  uint32_t next, exited, epoch, error;
+  uint32_t next, exited, epoch, error;  // far-field task graph
+  uint32_t near_next, near_exited;      // near-field stream: task claim counter, CTAs done
+  uint32_t pad[2];
 };
 
 // ---------------------------------------------------------------------------
@@ -258,6 +260,10 @@ struct h2b_ctx {
   int mega_blob_slots = 0;             // largest per-CTA task blob (16-byte slots)
   uint64_t* trace = nullptr;           // optional per-task timeline (H2B_OPT_TRACE)
   std::vector<Task> h_tasks;           // host copy of the task list
+  // near-field stream kernel (runs beside the far-field task graph; both add into a zeroed y)
+  int4* near_recs = nullptr;           // near task records
+  int2* near_idx = nullptr;            // per near task {first slot, slots}
+  int n_near_tasks = 0, near_rec_max = 0, near_nst = 0, near_smem = 0, near_grid = 0;
   // near / coupling work lists
   NearItem* near_items = nullptr;
   NearBlk* near_blks = nullptr;

@@ -1,59 +1,27 @@
-// Persistent single-launch H² matvec (q = 1) for sm_100a.
+// Persistent single-RHS H² matvec for sm_100a: two concurrent persistent kernels.
 //
-// One launch executes the whole `_apply_perm` (reference arith.py:52-104) as a
-// task graph planned on the host (h2b_plan.cu):
-//   * T_SPAN   forward / backward span programs (subtrees or upper tiers of
-//              the cluster tree), staged with TMA bulk copies    arith.py:58-71, 82-99
-//   * T_COUPLE groups of coupling panels ŷ_t = Σ Sᵀ-panel x̂        arith.py:72-81
-//   * T_NEAR   near-field row panels streamed through a TMA ring   arith.py:100-104
-// CTAs (2 per SM) claim tasks in queue order from an atomic counter, one task
-// AHEAD: while a task runs, the self-contained record of the next one (its
-// descriptors: block lists, span copies, coupling items) is already being
-// bulk-copied into shared memory, so a task starts issuing its data loads
-// without a single dependent global round trip.  A task waits (acquire loads
-// on epoch-stamped completion flags) only on tasks with smaller ids; the
-// lowest unfinished task is always executing, so the schedule cannot
-// deadlock.  Data produced inside the launch is read through L2
-// (ld.global.cg / TMA), never through the non-coherent L1.  The near-field
-// stream is tagged L2::evict_first and the far-field operands are warmed into
-// L2 at launch (cp.async.bulk.prefetch.L2), so the latency-bound tree sweeps
-// do not queue behind the bandwidth-bound stream.
+// `_apply_perm` (reference arith.py:52-104) splits into two independent halves whose
+// results are both added into y (zeroed first):
+//   * k_near_stream  the near field y += D x (arith.py:100-104), bandwidth-bound: one CTA
+//                    per SM streams D row panels through a TMA ring; tasks (row panels of
+//                    a few leaves) are claimed dynamically from an atomic counter, one task
+//                    ahead, so all SMs finish within one task of each other.
+//   * k_mega         the far field (arith.py:58-99), latency-bound: a task graph planned on
+//                    the host (h2b_plan.cu) of T_SPAN forward/backward span programs
+//                    (subtrees or upper tiers of the cluster tree, staged with TMA bulk
+//                    copies) and T_COUPLE groups of coupling panels ŷ_t = Σ Sᵀ-panel x̂.
+//                    One CTA per SM runs a static, topologically sorted task list from its
+//                    own bulk-loaded "blob"; tasks wait on epoch-stamped completion flags.
+// Both kernels run at the same time (one CTA of each per SM: the planner splits the shared
+// memory), neither waits on the other, and each y element receives exactly one near and at
+// most one far contribution through atomicAdd, so the sum is deterministic (two-term
+// floating-point addition commutes).
 #include "h2b_span.cuh"
 
 namespace {
 
 constexpr int MNT = 256;  // threads per CTA
 constexpr int NST_MAX = 8;
-
-struct MegaArgs {
-  const Task* tasks;
-  const DepRange* deps;
-  const int4* recs;
-  const int4* prefetch;
-  int n_prefetch;
-  MegaCtrl* ctrl;
-  uint32_t* flags;
-  int n_tasks;
-  const double2* dbuf;
-  const double2* x;
-  double2* y;
-  // generic near (ragged leaves)
-  const int32_t *leaves, *c_start, *c_size, *d_col;
-  const int64_t *d_row_ptr, *d_off;
-  // spans
-  const SpanCopy* outs;
-  SpanBases B;
-  // coupling
-  const double2* sbuf;
-  const int32_t* xcol;
-  double2* xhat;
-  double2* yhat;
-  uint64_t* trace;  // optional: per task {claim, ready, staged, done, smid} (globaltimer ns)
-  int smem_elems;   // dynamic shared memory (double2) of the launch
-  int debug;        // profiling aid: task bodies to skip (H2B_OPT_DEBUG)
-  const int2* cta_lists;  // per CTA: {first, count} into task_list
-  const int* task_list;   // task ids, each CTA's run in global topological order
-};
 
 __device__ __forceinline__ uint64_t gtimer() {
   uint64_t t;
@@ -90,114 +58,49 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void atomic_add2(double2* p, double2 v) {
+  atomicAdd(&p->x, v.x);
+  atomicAdd(&p->y, v.y);
+}
 
-// ---------------------------------------------------------------------------
-// near-field rows of a run of leaves (record in shared memory), TMA ring
-// ---------------------------------------------------------------------------
-// The ring persists across the CTA's consecutive near tasks: once the current
-// task's remaining blocks are all in flight, its refills already stream the
-// NEXT task's first blocks (its record was prefetched when it was claimed), so
-// the HBM stream of a CTA does not drain between tasks.  `ring` is the stage of
-// the current task's block 0; `carry` how many of its blocks the previous task
-// issued; returns how many of `next`'s blocks this task issued.
+// ===========================================================================
+// near field: k_near_stream
+// ===========================================================================
+struct NearArgs {
+  const int4* recs;   // near task records (see Task in h2b_common.cuh)
+  const int2* idx;    // per task {first slot, slots}
+  int n_tasks;
+  MegaCtrl* ctrl;
+  const double2* dbuf;
+  const double2* x;
+  double2* y;
+  // generic leaves (record {leaf index})
+  const int32_t *leaves, *c_start, *c_size, *d_col;
+  const int64_t *d_row_ptr, *d_off;
+  int nst;        // ring stages
+  int rec_slots;  // slots of each of the two record buffers
+};
+
+// One CTA streams a sequence of near-field tasks as ONE continuous sequence of D blocks:
+// thread 0 (producer) keeps the nst-stage TMA ring full, walking ahead through the blocks of
+// the tasks whose records sit in NRB record buffers; all threads (consumers) process the
+// blocks in the same order.  A record buffer is refilled with a newly claimed task as soon as
+// its task is consumed, so the stream never drains at task boundaries however small the
+// tasks are.
+constexpr int NRB = 3;  // record buffers: the consumer's task and up to two claimed ahead
+
 template <int NS, int R>
-__device__ __forceinline__ void issue_block(const MegaArgs& A, const int64_t* bl, int i, double2* st,
+__device__ __forceinline__ void issue_block(const NearArgs& A, const int64_t* bl, int i, double2* st,
                                             uint64_t* bar, uint64_t pol) {
+  // one stage = the task's D slice of block i + the partner's x segment behind it
   constexpr int RB = R * (MNT / (NS / 2));
-  mbar_arrive_expect_tx(bar, 16u * (RB * NS));
+  mbar_arrive_expect_tx(bar, 16u * (RB * NS + NS));
   bulk_g2s_hint(st, A.dbuf + bl[2 * i], 16u * RB * NS, bar, pol);
+  bulk_g2s(st + RB * NS, A.x + bl[2 * i + 1], 16u * NS, bar);
 }
 
-template <int NS, int R>
-__device__ __forceinline__ int near_task(const MegaArgs& A, const int4* rec, const int4* next,
-                                         uint64_t* next_bar, uint32_t next_parity, double2* sm,
-                                         uint64_t* fbar, uint32_t& fphase, int nst, uint64_t pol,
-                                         uint32_t& ring, int carry) {
-  constexpr int LPR = NS / 2;
-  constexpr int RPP = MNT / LPR;
-  constexpr int RB = R * RPP;        // rows of the task's slice of each block
-  constexpr int STG = RB * NS + NS;  // stage: D slice + x segment (double2)
-  const int nb = rec[0].x, nl = rec[0].y, row0 = rec[0].z;
-  const int64_t* lv = reinterpret_cast<const int64_t*>(rec + 1);        // {y_off, nb} per leaf
-  const int64_t* bl = reinterpret_cast<const int64_t*>(rec + 1 + nl);   // {d_off, x_off} per block
-  // the next task's record is read by thread 0 only, when it first needs it
-  int nb_next = -1;
-  const int64_t* bl_next = nullptr;
-  auto next_ready = [&]() {
-    if (nb_next < 0) {
-      if (next) {
-        if (next_bar) mbar_wait(next_bar, next_parity);
-        nb_next = next[0].x;
-        bl_next = reinterpret_cast<const int64_t*>(next + 1 + next[0].y);
-      } else {
-        nb_next = 0;
-      }
-    }
-    return nb_next;
-  };
-  const int r0 = threadIdx.x / LPR;
-  const int col = (threadIdx.x % LPR) * 2;
-  int carry_out = 0;
-  if (threadIdx.x == 0) {
-    // blocks [0, carry) are in flight already; fill the ring up to nst blocks
-    for (int i = carry; i < min(nst, nb); ++i) {
-      const int s = (ring + i) % nst;
-      issue_block<NS, R>(A, bl, i, sm + (size_t)s * STG, &fbar[s], pol);
-    }
-    for (int q = 0; nb + q < nst && q < next_ready(); ++q) {  // a short task: start the next one too
-      const int s = (ring + nb + q) % nst;
-      issue_block<NS, R>(A, bl_next, q, sm + (size_t)s * STG, &fbar[s], pol);
-      carry_out = q + 1;
-    }
-  }
-  int li = 0;
-  int leaf_end = (int)lv[1];
-  double2 acc[R][2];
-#pragma unroll
-  for (int r = 0; r < R; ++r) acc[r][0] = acc[r][1] = make_double2(0.0, 0.0);
-  for (int i = 0; i < nb; ++i) {
-    const int s = (ring + i) % nst;
-    // the partner's x segment (L1/L2-resident input) is loaded while the stage is in flight
-    const cd2 xv = ld_cached256(A.x + bl[2 * i + 1] + col);
-    mbar_wait(&fbar[s], (fphase >> s) & 1u);
-    fphase ^= 1u << s;
-    const double2* st = sm + (size_t)s * STG;
-    const double2 xa = xv.a, xb = xv.b;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const double2* d = st + (r0 + r * RPP) * NS + col;
-      cfma(acc[r][0], d[0], xa);
-      cfma(acc[r][1], d[1], xb);
-    }
-    if (i + 1 == leaf_end) {  // last partner of this leaf: reduce and store its rows
-      const int64_t y_off = lv[2 * li];
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        double2 a = cadd(acc[r][0], acc[r][1]);
-#pragma unroll
-        for (int m = LPR / 2; m > 0; m >>= 1) a = cadd(a, shfl_xor2(a, m));
-        if ((threadIdx.x % LPR) == 0) A.y[y_off + row0 + r0 + r * RPP] = a;
-        acc[r][0] = acc[r][1] = make_double2(0.0, 0.0);
-      }
-      if (++li < nl) leaf_end += (int)lv[2 * li + 1];
-    }
-    __syncthreads();  // stage s fully read: refill it (this task's block i + nst, or the next task's)
-    if (threadIdx.x == 0) {
-      const int j = i + nst;
-      if (j < nb) {
-        issue_block<NS, R>(A, bl, j, sm + (size_t)s * STG, &fbar[s], pol);
-      } else if (j - nb >= carry_out && j - nb < next_ready()) {
-        issue_block<NS, R>(A, bl_next, j - nb, sm + (size_t)s * STG, &fbar[s], pol);
-        carry_out = j - nb + 1;
-      }
-    }
-  }
-  ring = (ring + nb) % nst;
-  return carry_out;  // meaningful in thread 0, the only thread that issues copies
-}
-
-// near-field of one leaf with arbitrary block shapes (warp per row); record: {leaf index}
-__device__ __forceinline__ void near_task_generic(const MegaArgs& A, int leaf_idx) {
+// near field of one leaf with arbitrary block shapes (warp per row); record: {leaf index}
+__device__ __forceinline__ void near_task_generic(const NearArgs& A, int leaf_idx) {
   const int t = A.leaves[leaf_idx];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nt = A.c_size[t];
@@ -213,9 +116,190 @@ __device__ __forceinline__ void near_task_generic(const MegaArgs& A, int leaf_id
       for (int j = lane; j < ns; j += 32) cfma(acc, D[j], xs[j]);
     }
     acc = warp_sum2(acc);
-    if (lane == 0) A.y[t0 + i] = acc;
+    if (lane == 0) atomic_add2(A.y + t0 + i, acc);
   }
 }
+
+// Warp-specialised: warps 0-7 consume D blocks (256 threads, as near_task_generic and the
+// block layout assume), warp 8 is the producer.  Its lane 0 claims tasks from the global
+// counter (one atomic per task), bulk-loads their records and keeps the nst-stage ring full;
+// the claim and record latencies stay off the consumers' path as long as the ring holds work.
+//   fbar[s] full  (producer arrive + TMA bytes)  ebar[s] empty (one arrive per consumer warp)
+//   rbar[b] record loaded (or end-of-stream mark)  rfree[b] record consumed (per consumer warp)
+constexpr int NEAR_THREADS = MNT + 32;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int NS, int R>
+__global__ void __launch_bounds__(NEAR_THREADS, 1) k_near_stream(NearArgs A) {
+  // dynamic shared memory: [ring: nst stages][NRB record buffers]
+  extern __shared__ __align__(16) double2 sm[];
+  __shared__ uint64_t fbar[NST_MAX], ebar[NST_MAX], rbar[NRB], rfree[NRB];
+  __shared__ int s_task[NRB];
+  constexpr int LPR = NS > 0 ? NS / 2 : 1;
+  constexpr int RPP = MNT / LPR;
+  constexpr int RB = R * RPP;                       // rows of a task's slice of each block
+  constexpr int STG = NS > 0 ? RB * NS + NS : 0;    // stage: D slice + x segment (double2)
+  const int nst = NS > 0 ? A.nst : 0;
+  int4* rbuf0 = reinterpret_cast<int4*>(sm + (size_t)nst * STG);
+  auto rbuf = [&](int b) { return rbuf0 + (size_t)b * A.rec_slots; };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NST_MAX; ++i) {
+      mbar_init(&fbar[i], 1);
+      mbar_init(&ebar[i], MNT / 32);
+    }
+    for (int b = 0; b < NRB; ++b) {
+      mbar_init(&rbar[b], 1);
+      mbar_init(&rfree[b], MNT / 32);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x >= MNT) {
+    // ---------------- producer (one lane) ----------------
+    if (threadIdx.x == MNT) {
+      const uint64_t pol = policy_evict_first();
+      int claimed = 0;  // records 0 .. claimed-1 claimed
+      bool end = false;
+      // claim record `claimed` into buffer claimed % NRB, given the counter value c (fetched
+      // early: the atomic's round trip overlaps the block issues of the record before)
+      auto finish_claim = [&](int c) {
+        const int b = claimed % NRB;
+        if (claimed >= NRB) mbar_wait(&rfree[b], ((claimed / NRB) - 1) & 1u);  // consumers done with it
+        if (end) c = A.n_tasks;
+        s_task[b] = c;
+        if (c < A.n_tasks) {
+          const int2 ix = A.idx[c];
+          mbar_arrive_expect_tx(&rbar[b], 16u * ix.y);
+          bulk_g2s(rbuf(b), A.recs + ix.x, 16u * ix.y, &rbar[b]);
+        } else {
+          end = true;
+          mbar_arrive(&rbar[b]);  // end of stream (s_task published by the arrive's release)
+        }
+        ++claimed;
+      };
+      for (int i = 0; i < NRB - 1; ++i) finish_claim((int)atomicAdd(&A.ctrl->near_next, 1u));
+      int issued = 0;
+      for (int q = 0;; ++q) {
+        // keep NRB - 1 records claimed beyond q: fetch the counter now, complete the claim after
+        // this record's blocks are issued
+        const bool want = claimed < q + NRB && !end;
+        const int pending = want ? (int)atomicAdd(&A.ctrl->near_next, 1u) : 0;
+        const int b = q % NRB;
+        mbar_wait(&rbar[b], (q / NRB) & 1u);
+        if (s_task[b] >= A.n_tasks) {
+          if (want) finish_claim(pending);  // (an unused claim past the end is harmless)
+          break;
+        }
+        if constexpr (NS > 0) {
+          const int4* r = rbuf(b);
+          const int nb = r[0].x;
+          const int64_t* bl = reinterpret_cast<const int64_t*>(r + 1 + r[0].y);
+          for (int j = 0; j < nb; ++j, ++issued) {
+            const int st = issued % nst;
+            if (issued >= nst) mbar_wait(&ebar[st], ((issued / nst) - 1) & 1u);
+            double2* sp = sm + (size_t)st * STG;
+            mbar_arrive_expect_tx(&fbar[st], 16u * (RB * NS + NS));
+            bulk_g2s_hint(sp, A.dbuf + bl[2 * j], 16u * RB * NS, &fbar[st], pol);
+            bulk_g2s(sp + RB * NS, A.x + bl[2 * j + 1], 16u * NS, &fbar[st]);
+          }
+        }
+        if (want) finish_claim(pending);
+      }
+      // every claimed record has been consumed or marked as the end; wait for the consumers to
+      // release the last buffers so no bulk copy is in flight at exit
+      for (int q = (claimed > NRB ? claimed - NRB : 0); q < claimed; ++q)
+        if (s_task[q % NRB] < A.n_tasks) mbar_wait(&rfree[q % NRB], (q / NRB) & 1u);
+      if (atomicAdd(&A.ctrl->near_exited, 1u) == gridDim.x - 1) {
+        A.ctrl->near_exited = 0;  // last CTA out resets the claim counter for the next launch
+        A.ctrl->near_next = 0;
+      }
+    }
+    return;
+  }
+  // ---------------- consumers: warps 0-7 ----------------
+  const int lane = threadIdx.x & 31;
+  if constexpr (NS == 0) {
+    // ragged leaves: one leaf per task, plain loads (record: {leaf index})
+    for (int q = 0;; ++q) {
+      const int b = q % NRB;
+      mbar_wait(&rbar[b], (q / NRB) & 1u);
+      if (s_task[b] >= A.n_tasks) break;
+      near_task_generic(A, rbuf(b)[0].x);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&rfree[b]);
+    }
+  } else {
+    const int r0 = threadIdx.x / LPR;
+    const int col = (threadIdx.x % LPR) * 2;
+    int consumed = 0;
+    for (int q = 0;; ++q) {
+      const int b = q % NRB;
+      mbar_wait(&rbar[b], (q / NRB) & 1u);
+      if (s_task[b] >= A.n_tasks) break;
+      const int4* rec = rbuf(b);
+      const int nb = rec[0].x, nl = rec[0].y, row0 = rec[0].z;
+      const int64_t* lv = reinterpret_cast<const int64_t*>(rec + 1);  // {y_off, nb} per leaf
+      int li = 0;
+      int leaf_end = (int)lv[1];
+      double2 acc[R][2];
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r][0] = acc[r][1] = make_double2(0.0, 0.0);
+      for (int i = 0; i < nb; ++i, ++consumed) {
+        const int st = consumed % nst;
+        mbar_wait(&fbar[st], (consumed / nst) & 1u);
+        const double2* sp = sm + (size_t)st * STG;
+        const double2 xa = sp[RB * NS + col], xb = sp[RB * NS + col + 1];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const double2* d = sp + (r0 + r * RPP) * NS + col;
+          cfma(acc[r][0], d[0], xa);
+          cfma(acc[r][1], d[1], xb);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ebar[st]);  // this warp is done with the stage
+        if (i + 1 == leaf_end) {  // last partner of this leaf: reduce and add its rows
+          const int64_t y_off = lv[2 * li];
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            double2 a = cadd(acc[r][0], acc[r][1]);
+#pragma unroll
+            for (int m = LPR / 2; m > 0; m >>= 1) a = cadd(a, shfl_xor2(a, m));
+            if ((threadIdx.x % LPR) == 0) atomic_add2(A.y + y_off + row0 + r0 + r * RPP, a);
+            acc[r][0] = acc[r][1] = make_double2(0.0, 0.0);
+          }
+          if (++li < nl) leaf_end += (int)lv[2 * li + 1];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&rfree[b]);  // this warp is done with the record
+    }
+  }
+}
+
+// ===========================================================================
+// far field: k_mega
+// ===========================================================================
+struct MegaArgs {
+  const int4* recs;
+  const int4* prefetch;
+  int n_prefetch;
+  MegaCtrl* ctrl;
+  uint32_t* flags;
+  int n_tasks;
+  // spans
+  SpanBases B;
+  // coupling
+  const double2* sbuf;
+  const int32_t* xcol;
+  double2* xhat;
+  double2* yhat;
+  uint64_t* trace;  // optional: per task {claim, ready, staged, done, smid} (globaltimer ns)
+  int smem_elems;   // dynamic shared memory (double2) of the work area
+  int debug;        // profiling aid (H2B_OPT_DEBUG)
+  const int2* cta_lists;  // per CTA: {blob offset, blob length} in 16-byte slots
+};
 
 // ---------------------------------------------------------------------------
 // coupling of a group of consecutive targets (record: group header + items).
@@ -275,24 +359,17 @@ __device__ __forceinline__ void couple_task(const MegaArgs& A, const int4* rec, 
   }
 }
 
-template <int NS, int R>
-__global__ void __launch_bounds__(MNT, 2) k_mega(MegaArgs A) {
-  // dynamic shared memory: [work area: near ring / span working set / coupling panels][this
-  // CTA's blob: its task list, dependency ranges and task records, one bulk copy]
+__global__ void __launch_bounds__(MNT, 1) k_mega(MegaArgs A) {
+  // dynamic shared memory: [work area: span working set / coupling panels][this CTA's blob:
+  // its task list, dependency ranges and task records, one bulk copy]
   extern __shared__ __align__(16) double2 sm[];
   __shared__ double2 red[MNT];
   __shared__ uint32_t s_epoch;
   __shared__ __align__(128) uint64_t bar, bbar;
-  __shared__ uint64_t fbar[NST_MAX];
-  uint32_t fphase = 0, phase = 0;
-  uint32_t ring = 0;  // near-field ring position (persists across the CTA's near tasks)
-  int carry = 0;      // blocks of the upcoming near task already in flight
-  const int nst = NS > 0 ? max(1, min(NST_MAX, A.smem_elems / (R * (MNT / (NS / 2)) * NS + NS))) : 1;
-  const uint64_t pol = policy_evict_first();
+  uint32_t phase = 0;
   int4* blob = reinterpret_cast<int4*>(sm + A.smem_elems);
   const int2 lst = A.cta_lists[blockIdx.x];  // {blob offset, blob length} in 16-byte slots
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NST_MAX; ++i) mbar_init(&fbar[i], 1);
     mbar_init(&bar, 1);
     mbar_init(&bbar, 1);
     s_epoch = *(volatile uint32_t*)&A.ctrl->epoch;
@@ -301,9 +378,9 @@ __global__ void __launch_bounds__(MNT, 2) k_mega(MegaArgs A) {
       bulk_g2s(blob, A.recs + lst.x, 16u * lst.y, &bbar);
     }
   }
-  // warm the far-field operands into L2: every CTA's TMA unit takes an equal strided share
-  // (a prefetch occupies the issuing SM's TMA unit, so it must not pile up on a few SMs)
-  if (threadIdx.x == 0)
+  // optional (H2B_OPT_DEBUG bit 6, measured slower on B200): warm the far-field operands into L2,
+  // every CTA's TMA unit taking an equal strided share
+  if (threadIdx.x == 0 && (A.debug & 64))
     for (int i = blockIdx.x; i < A.n_prefetch; i += gridDim.x) {
       const int4 r = A.prefetch[i];
       const uint64_t p = (uint64_t)(uint32_t)r.x | ((uint64_t)(uint32_t)r.y << 32);
@@ -314,7 +391,7 @@ __global__ void __launch_bounds__(MNT, 2) k_mega(MegaArgs A) {
   const uint32_t done = s_epoch + 1;
   // This CTA's static task list (planned on the host, sorted in the global topological order:
   // the lowest unfinished task is always at the head of some CTA's list, so no CTA can wait
-  // forever).  Near-field CTAs own a contiguous run of row panels and never wait.
+  // forever).
   const int n_my = lst.y > 0 ? blob[0].x : 0;
   for (int k = 0; k < n_my; ++k) {
     const int4 e0 = blob[1 + 2 * k], e1 = blob[2 + 2 * k];
@@ -328,27 +405,25 @@ __global__ void __launch_bounds__(MNT, 2) k_mega(MegaArgs A) {
     }
     const SpanHead* hd = reinterpret_cast<const SpanHead*>(rec);
     const SpanCopy* cps = reinterpret_cast<const SpanCopy*>(rec + (sizeof(SpanHead) + 15) / 16);
-    // profiling aid (H2B_OPT_DEBUG): bit 0 skips far-field task bodies, bit 1 near-field ones
-    const bool skip = ((A.debug & 1) && type != T_NEAR) || ((A.debug & 2) && type == T_NEAR);
-    if (type != T_NEAR) {
-      // Every far-field task starts from a freshly initialised transaction barrier (parity 0).
-      // Carrying one barrier's parity across a CTA's mixed span / coupling tasks was measured
-      // to lose phase sync under load (1-3% of launches read a staging area before its bulk
-      // copies had landed); the previous task ended with a CTA barrier, so no thread still
-      // waits on the old phase and none of its copies is in flight.
-      if (threadIdx.x == 0) {
-        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&bar)) : "memory");
-        mbar_init(&bar, 1);
-      }
-      phase = 0;
-      // static operands stream in while the dependencies are still outstanding
-      if (!skip && type == T_SPAN)
-        span_stage_static<MNT>(hd, cps, A.B, sm, &bar);
-      else if (!skip)
-        couple_stage_static(A, rec, sm, &bar);
+    // profiling aid (H2B_OPT_DEBUG bit 0): task bodies skipped, dependency skeleton only
+    const bool skip = A.debug & 1;
+    // Every task starts from a freshly initialised transaction barrier (parity 0).  Carrying one
+    // barrier's parity across a CTA's mixed span / coupling tasks was measured to lose phase
+    // sync under load (1-3% of launches read a staging area before its bulk copies had
+    // landed); the previous task ended with a CTA barrier, so no thread still waits on the old
+    // phase and none of its copies is in flight.
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&bar)) : "memory");
+      mbar_init(&bar, 1);
     }
-    // dependencies: warp 0 polls (lanes share the flags) with a backoff, so waiting CTAs do not
-    // flood L2 with requests next to the near-field stream; the other warps wait at the barrier
+    phase = 0;
+    // static operands stream in while the dependencies are still outstanding
+    if (!skip && type == T_SPAN)
+      span_stage_static<MNT>(hd, cps, A.B, sm, &bar);
+    else if (!skip)
+      couple_stage_static(A, rec, sm, &bar);
+    // dependencies: warp 0 polls (lanes share the flags) with a short backoff; the other warps
+    // wait at the barrier
     if (threadIdx.x < 32)
       for (int i = 0; i < n_dep; ++i) {
         const int2 rg = deps[i];
@@ -359,7 +434,7 @@ __global__ void __launch_bounds__(MNT, 2) k_mega(MegaArgs A) {
               atomicExch(&A.ctrl->error, 1u);
               break;
             }
-            __nanosleep(256);
+            __nanosleep(64);
           }
         }
       }
@@ -370,31 +445,16 @@ __global__ void __launch_bounds__(MNT, 2) k_mega(MegaArgs A) {
     if (A.trace && threadIdx.x == 0) A.trace[8 * t + 1] = gtimer();
     if (skip) {
       // profiling aid only (H2B_OPT_DEBUG): this task's body is skipped
-    } else if (type == T_NEAR) {
-      if constexpr (NS == 0) {
-        near_task_generic(A, rec[0].x);
-      } else {
-        const bool next_near = k + 1 < n_my && blob[1 + 2 * (k + 1)].y == T_NEAR && !(A.debug & 2);
-        carry = near_task<NS, R>(A, rec, next_near ? blob + blob[1 + 2 * (k + 1)].z : nullptr, nullptr, 0,
-                                 sm, fbar, fphase, nst, pol, ring, carry);
-      }
     } else if (type == T_SPAN) {
-      span_finish<MNT>(hd, cps, A.B, sm, &bar, phase, A.trace ? A.trace + 8 * t + 2 : nullptr);
+      span_finish<MNT>(hd, cps, A.B, sm, &bar, phase, A.trace ? A.trace + 8 * t + 2 : nullptr, 3);
     } else {
       couple_task(A, rec, red, sm, &bar, phase);
     }
-    if (type != T_NEAR) {
-      // x̂ / ŷ written here with generic stores are read by other CTAs' TMA (async proxy), and
-      // this task's generic shared-memory writes precede the next task's TMA writes
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
+    // this task's generic shared-memory writes precede the next task's TMA writes into the
+    // same work area (the consumers of x̂ / ŷ order their TMA reads after their acquire)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    // publish completion from a thread that does not feed the near-field ring (thread 0); a
-    // release at GPU scope costs ~0.4 us, so a near-field CTA publishes only its last panel
-    // (the planner points every dependency on its panels there)
-    if (threadIdx.x == 32 && e1.z) {
-      __threadfence();
+    if (threadIdx.x == 32) {  // publish completion (thread 32: warp 0 may still be polling)
       st_release(A.flags + t, done);
       if (A.trace) A.trace[8 * t + 3] = gtimer();
     }
@@ -408,36 +468,19 @@ __global__ void __launch_bounds__(MNT, 2) k_mega(MegaArgs A) {
   }
 }
 
-template <int NS, int R>
-int launch(h2b_ctx* h, const MegaArgs& A, cudaStream_t st) {
-  // cooperative launch: all CTAs co-resident (far-field CTAs wait on near-field CTAs)
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(h->mega_grid);
-  cfg.blockDim = dim3(MNT);
-  cfg.dynamicSmemBytes = h->mega_smem + 16 * h->mega_blob_slots;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  H2B_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_mega<NS, R>, A));
-  return H2B_OK;
-}
-
 }  // namespace
 
-int h2b_mega_occupancy(int ns, int r, int smem_bytes, int* blocks_per_sm) {
-  cudaError_t e;
-#define OCC(a, b) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_mega<a, b>, MNT, smem_bytes)
-  if (ns == 32 && r == 1) OCC(32, 1);
-  else if (ns == 32 && r == 2) OCC(32, 2);
-  else if (ns == 64 && r == 1) OCC(64, 1);
-  else if (ns == 64 && r == 2) OCC(64, 2);
-  else if (ns == 64 && r == 4) OCC(64, 4);
-  else if (ns == 64 && r == 8) OCC(64, 8);
-  else OCC(0, 1);
-#undef OCC
+int h2b_mega_static_smem() {
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, k_mega) != cudaSuccess) {
+    cudaGetLastError();
+    return 8192;
+  }
+  return (int)fa.sharedSizeBytes;
+}
+
+int h2b_mega_occupancy(int, int, int smem_bytes, int* blocks_per_sm) {
+  const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_mega, MNT, smem_bytes);
   if (e != cudaSuccess) {
     cudaGetLastError();
     h2b_set_error(std::string("occupancy: ") + cudaGetErrorString(e));
@@ -446,66 +489,128 @@ int h2b_mega_occupancy(int ns, int r, int smem_bytes, int* blocks_per_sm) {
   return H2B_OK;
 }
 
-int h2b_mega_set_smem(int ns, int r, int bytes) {
-#define ATTR(a, b) H2B_CUDA_TRY(cudaFuncSetAttribute(k_mega<a, b>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))
-  if (ns == 32 && r == 1) ATTR(32, 1);
-  else if (ns == 32 && r == 2) ATTR(32, 2);
-  else if (ns == 64 && r == 1) ATTR(64, 1);
-  else if (ns == 64 && r == 2) ATTR(64, 2);
-  else if (ns == 64 && r == 4) ATTR(64, 4);
-  else if (ns == 64 && r == 8) ATTR(64, 8);
-  else ATTR(0, 1);
-#undef ATTR
+// Both persistent kernels ask for the largest shared-memory carveout: with a smaller one
+// chosen for whichever starts first, the other would not fit beside it on the SM.
+int h2b_mega_set_smem(int, int, int bytes) {
+  H2B_CUDA_TRY(cudaFuncSetAttribute(k_mega, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  H2B_CUDA_TRY(cudaFuncSetAttribute(k_mega, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   return H2B_OK;
 }
 
+#define NEAR_VARIANTS(X) X(32, 1) X(32, 2) X(64, 1) X(64, 2) X(64, 4) X(64, 8)
+
+int h2b_near_stream_static_smem(int ns, int r, int* bytes) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaErrorInvalidValue;
+#define X(a, b) \
+  if (ns == a && r == b) e = cudaFuncGetAttributes(&fa, k_near_stream<a, b>);
+  NEAR_VARIANTS(X)
+#undef X
+  if (ns != 32 && ns != 64) e = cudaFuncGetAttributes(&fa, k_near_stream<0, 1>);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    h2b_set_error(std::string("near stream attributes: ") + cudaGetErrorString(e));
+    return H2B_ECUDA;
+  }
+  *bytes = (int)fa.sharedSizeBytes;
+  return H2B_OK;
+}
+
+int h2b_near_stream_set_smem(int ns, int r, int bytes) {
+#define X(a, b)                                                                                           \
+  if (ns == a && r == b) {                                                                                \
+    H2B_CUDA_TRY(cudaFuncSetAttribute(k_near_stream<a, b>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)); \
+    H2B_CUDA_TRY(cudaFuncSetAttribute(k_near_stream<a, b>, cudaFuncAttributePreferredSharedMemoryCarveout, 100)); \
+  }
+  NEAR_VARIANTS(X)
+#undef X
+  if (ns != 32 && ns != 64) {
+    H2B_CUDA_TRY(cudaFuncSetAttribute(k_near_stream<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    H2B_CUDA_TRY(cudaFuncSetAttribute(k_near_stream<0, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  }
+  return H2B_OK;
+}
+
+// y = 0; then k_near_stream on st and k_mega on h->far_stream, concurrently (fork / join)
 int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st) {
-  MegaArgs A;
-  A.tasks = h->tasks;
-  A.deps = h->deps;
-  A.recs = h->rec_pool;
-  A.prefetch = h->l2_prefetch;
-  A.n_prefetch = h->n_prefetch;
-  A.ctrl = h->ctrl;
-  A.flags = h->flags;
-  A.n_tasks = h->n_tasks;
-  A.dbuf = h->buf[H2B_SEC_D];
-  A.x = xp;
-  A.y = yp;
-  A.leaves = h->leaves;
-  A.c_start = h->c_start_d;
-  A.c_size = h->c_size_d;
-  A.d_col = h->d_col_d;
-  A.d_row_ptr = h->d_row_ptr_d;
-  A.d_off = h->d_off_d;
-  A.outs = h->span_outs;
-  A.B.src[SRC_V] = h->buf[H2B_SEC_V];
-  A.B.src[SRC_T] = h->buf[H2B_SEC_T];
-  A.B.src[SRC_VT] = h->vT;
-  A.B.src[SRC_TT] = h->tT;
-  A.B.src[SRC_X] = xp;
-  A.B.src[SRC_XHAT] = h->xhat;
-  A.B.src[SRC_YHAT] = h->yhat;
-  A.B.src[SRC_OPS] = reinterpret_cast<const double2*>(h->span_ops);
-  A.B.src[SRC_OUTS] = reinterpret_cast<const double2*>(h->span_outs);
-  A.B.xhat = h->xhat;
-  A.B.yhat = h->yhat;
-  A.B.y = yp;
-  A.sbuf = h->buf[H2B_SEC_S];
-  A.xcol = h->s_xcol;
-  A.xhat = h->xhat;
-  A.yhat = h->yhat;
-  A.trace = h->trace;
-  A.smem_elems = h->mega_smem / 16;
-  A.debug = h->mega_debug;
-  A.cta_lists = h->cta_lists;
-  A.task_list = h->task_list;
-  const int ns = h->mega_ns, r = h->mega_r;
-  if (ns == 32 && r == 1) return launch<32, 1>(h, A, st);
-  if (ns == 32 && r == 2) return launch<32, 2>(h, A, st);
-  if (ns == 64 && r == 1) return launch<64, 1>(h, A, st);
-  if (ns == 64 && r == 2) return launch<64, 2>(h, A, st);
-  if (ns == 64 && r == 4) return launch<64, 4>(h, A, st);
-  if (ns == 64 && r == 8) return launch<64, 8>(h, A, st);
-  return launch<0, 1>(h, A, st);
+  H2B_CUDA_TRY(cudaMemsetAsync(yp, 0, sizeof(double2) * h->n, st));
+  const bool run_far = h->mega_grid > 0 && !(h->mega_debug & 2);
+  const bool run_near = h->n_near_tasks > 0 && !(h->mega_debug & 4);
+  if (run_far) {
+    H2B_CUDA_TRY(cudaEventRecord(h->ev_fork, st));
+    H2B_CUDA_TRY(cudaStreamWaitEvent(h->far_stream, h->ev_fork, 0));
+    MegaArgs A;
+    A.recs = h->rec_pool;
+    A.prefetch = h->l2_prefetch;
+    A.n_prefetch = h->n_prefetch;
+    A.ctrl = h->ctrl;
+    A.flags = h->flags;
+    A.n_tasks = h->n_tasks;
+    A.B.src[SRC_V] = h->buf[H2B_SEC_V];
+    A.B.src[SRC_T] = h->buf[H2B_SEC_T];
+    A.B.src[SRC_VT] = h->vT;
+    A.B.src[SRC_TT] = h->tT;
+    A.B.src[SRC_X] = xp;
+    A.B.src[SRC_XHAT] = h->xhat;
+    A.B.src[SRC_YHAT] = h->yhat;
+    A.B.src[SRC_OPS] = reinterpret_cast<const double2*>(h->span_ops);
+    A.B.src[SRC_OUTS] = reinterpret_cast<const double2*>(h->span_outs);
+    A.B.xhat = h->xhat;
+    A.B.yhat = h->yhat;
+    A.B.y = yp;
+    A.sbuf = h->buf[H2B_SEC_S];
+    A.xcol = h->s_xcol;
+    A.xhat = h->xhat;
+    A.yhat = h->yhat;
+    A.trace = h->trace;
+    A.smem_elems = h->mega_smem / 16;
+    A.debug = h->mega_debug;
+    A.cta_lists = h->cta_lists;
+    // cooperative launch: all CTAs co-resident (they wait on one another)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(h->mega_grid);
+    cfg.blockDim = dim3(MNT);
+    cfg.dynamicSmemBytes = h->mega_smem + 16 * h->mega_blob_slots;
+    cfg.stream = h->far_stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    H2B_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_mega, A));
+  }
+  if (run_near) {
+    NearArgs N;
+    N.recs = h->near_recs;
+    N.idx = h->near_idx;
+    N.n_tasks = h->n_near_tasks;
+    N.ctrl = h->ctrl;
+    N.dbuf = h->buf[H2B_SEC_D];
+    N.x = xp;
+    N.y = yp;
+    N.leaves = h->leaves;
+    N.c_start = h->c_start_d;
+    N.c_size = h->c_size_d;
+    N.d_col = h->d_col_d;
+    N.d_row_ptr = h->d_row_ptr_d;
+    N.d_off = h->d_off_d;
+    N.nst = std::max(1, h->near_nst);
+    N.rec_slots = std::max(1, h->near_rec_max);  // NRB buffers of this size follow the ring
+    const int ns = h->mega_ns, r = h->mega_r;
+    bool launched = false;
+#define X(a, b)                                                                            \
+  if (!launched && ns == a && r == b) {                                                    \
+    k_near_stream<a, b><<<h->near_grid, NEAR_THREADS, h->near_smem, st>>>(N);                       \
+    launched = true;                                                                       \
+  }
+    NEAR_VARIANTS(X)
+#undef X
+    if (!launched) k_near_stream<0, 1><<<h->near_grid, NEAR_THREADS, h->near_smem, st>>>(N);
+    H2B_CHECK_LAUNCH();
+  }
+  if (run_far) {
+    H2B_CUDA_TRY(cudaEventRecord(h->ev_join, h->far_stream));
+    H2B_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_join, 0));
+  }
+  return H2B_OK;
 }

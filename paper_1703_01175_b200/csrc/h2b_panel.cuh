@@ -102,7 +102,8 @@ __device__ __forceinline__ void warp_panel_fast(const double2* P, int R, int w, 
 // One out-of-line copy of the warp panel GEMV for the persistent kernel, whose
 // task bodies otherwise overflow the instruction cache when CTAs switch between
 // task types.  mode 0: out = sum; 1: out += sum; 2: out += sum with out in global
-// memory written by another SM in the same launch (read through L2).
+// memory written by another SM in the same launch (read through L2); 3: atomic
+// out += sum in global memory (another kernel adds into it concurrently).
 static __device__ __noinline__ void panel_op(const double2* P, int R, int w, int sh, const double2* in,
                                       double2* out, int mode) {
   const int lane = threadIdx.x & 31;
@@ -112,6 +113,11 @@ static __device__ __noinline__ void panel_op(const double2* P, int R, int w, int
     if (mode == 2 && lane < w) prev = __ldcg(out + lane);
     const double2 s = warp_panel_sum(P, R, w, sh, inf);
     if (lane < w) {
+      if (mode == 3) {
+        atomicAdd(&out[lane].x, s.x);
+        atomicAdd(&out[lane].y, s.y);
+        return;
+      }
       if (mode == 1) prev = out[lane];
       out[lane] = mode ? cadd(prev, s) : s;
     }
@@ -126,6 +132,11 @@ static __device__ __noinline__ void panel_op(const double2* P, int R, int w, int
     }
     if (r < R) cfma(a0, P[r * w + c], in[r]);
     a0 = cadd(a0, a1);
+    if (mode == 3) {
+      atomicAdd(&out[c].x, a0.x);
+      atomicAdd(&out[c].y, a0.y);
+      continue;
+    }
     const double2 prev = mode == 2 ? __ldcg(out + c) : (mode == 1 ? out[c] : make_double2(0.0, 0.0));
     out[c] = mode ? cadd(prev, a0) : a0;
   }

@@ -15,6 +15,9 @@
 int h2b_far_init_attributes(int smem_cap_bytes);
 int h2b_mega_set_smem(int ns, int r, int bytes);
 int h2b_mega_occupancy(int ns, int r, int smem_bytes, int* blocks_per_sm);
+int h2b_mega_static_smem();
+int h2b_near_stream_static_smem(int ns, int r, int* bytes);
+int h2b_near_stream_set_smem(int ns, int r, int bytes);
 int h2b_near_rows_per_item(int ns, int r);
 
 namespace {
@@ -401,6 +404,7 @@ bool plan_with_split(const h2b_ctx* h, int ls, Plan& pl) {
 // ------------------------- persistent-kernel task graph -------------------------
 constexpr int MEGA_BUDGET = 5800;  // double2 elements (92.8 KB) of work area per CTA
 constexpr int MEGA_BLOB_MAX = 1024;  // 16-byte slots (16 KB) of per-CTA task blob
+constexpr double NEAR_TASK_BYTES = 64e3;  // target D bytes per near-field task
 
 std::vector<DepRange> to_ranges(std::vector<int> ids) {
   std::sort(ids.begin(), ids.end());
@@ -437,7 +441,9 @@ struct MegaPlan {
   std::vector<int4> recs;
   std::vector<int2> cta_lists;
   std::vector<int> task_list;
-  int ns = 0, r = 1, smem = 0, tiers = 0, blob_slots = 0;
+  std::vector<int4> near_recs;  // near-field task records (claimed dynamically by the stream kernel)
+  std::vector<int2> near_idx;   // per near task {first slot, slots} in near_recs
+  int ns = 0, r = 1, smem = 0, tiers = 0, blob_slots = 0, near_rec_max = 0;
   double est_makespan = 0.0;
 };
 
@@ -564,8 +570,6 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
   // ---- near-field work list (leaf order) --------------------------------------------
   const int ns = h->uniform_leaf;
   const int nleaves = (int)h->h_leaves.size();
-  std::vector<int> leaf_pos(h->P, -1);
-  for (int i = 0; i < nleaves; ++i) leaf_pos[h->h_leaves[i]] = i;
   for (int i = 0; i < nleaves; ++i) {
     const int t = h->h_leaves[i];
     mp.leaf_items.push_back({(int64_t)h->c_start[t], (int32_t)h->d_row_ptr[t],
@@ -573,7 +577,6 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
   }
   std::vector<NearTask>& nts = mp.near_tasks;
   std::vector<double> nt_bytes;
-  std::vector<int> nt_of_leaf_last(nleaves, -1);
   auto leaf_nb = [&](int i) {
     const int t = h->h_leaves[i];
     return (int)(h->d_row_ptr[t + 1] - h->d_row_ptr[t]);
@@ -583,7 +586,8 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
     const double row_bytes = ns * 16.0 * avg_nb;
     const int rpp = 256 / (ns / 2);  // rows per pass of a 256-thread CTA
     int R = 1;
-    while (R * 2 * rpp <= ns && R * 2 <= (ns == 32 ? 2 : 8) && R * 2 * rpp * row_bytes <= 96e3) R *= 2;
+    // tasks of ~NEAR_TASK_BYTES: claimed dynamically, so small tasks keep the tail short
+    while (R * 2 * rpp <= ns && R * 2 <= (ns == 32 ? 2 : 8) && R * 2 * rpp * row_bytes <= NEAR_TASK_BYTES) R *= 2;
     mp.ns = ns;
     mp.r = R;
     const int rb = R * rpp;
@@ -592,11 +596,10 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
         for (int r0 = 0; r0 < ns; r0 += rb) {
           nts.push_back({i, 1, r0, 0});
           nt_bytes.push_back(16.0 * rb * ns * leaf_nb(i));
-          nt_of_leaf_last[i] = (int)nts.size() - 1;
         }
     } else {
-      // group whole leaves into tasks of ~96 KB (the ring streams on across task boundaries)
-      const int per = std::max(1, (int)(96e3 / (ns * row_bytes) + 0.5));
+      // group whole leaves into tasks (the ring streams on across task boundaries)
+      const int per = std::max(1, (int)(NEAR_TASK_BYTES / (ns * row_bytes) + 0.5));
       int i = 0;
       while (i < nleaves) {
         int c = 0, blocks = 0;
@@ -608,7 +611,6 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
         }
         nts.push_back({i, c, 0, 0});
         nt_bytes.push_back(16.0 * ns * ns * blocks);
-        for (int j = i; j < i + c; ++j) nt_of_leaf_last[j] = (int)nts.size() - 1;
         i += c;
       }
     }
@@ -620,16 +622,20 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
     for (int i = 0; i < nleaves; ++i) {
       nts.push_back({i, 1, 0, 0});
       nt_bytes.push_back(16.0 * h->c_size[h->h_leaves[i]] * 64.0 * leaf_nb(i));
-      nt_of_leaf_last[i] = (int)nts.size() - 1;
     }
   }
-  std::vector<int> nt_first_of_leaf(nleaves, -1);  // near tasks covering a leaf are consecutive
-  for (size_t k = 0; k < nts.size(); ++k)
-    for (int j = nts[k].leaf_first; j < nts[k].leaf_first + nts[k].n_leaves; ++j)
-      if (nt_first_of_leaf[j] < 0) nt_first_of_leaf[j] = (int)k;
-  const int n_near = (int)nts.size();
-  for (int k = 0; k < n_near; ++k)
-    add_l(T_NEAR, ns == 32 || ns == 64 ? k : nts[k].leaf_first, {}, 0.5 + nt_bytes[k] / cta_bw);
+  // the near field runs in its own streaming kernel, concurrently with the far-field task
+  // graph (both accumulate into a zeroed y): its tasks are not part of the graph below
+  for (size_t k = 0; k < nts.size(); ++k) {
+    std::vector<int4> rec;
+    rec_out = &rec;
+    make_record(T_NEAR, ns == 32 || ns == 64 ? (int)k : nts[k].leaf_first);
+    mp.near_idx.push_back({(int)mp.near_recs.size(), (int)rec.size()});
+    mp.near_recs.insert(mp.near_recs.end(), rec.begin(), rec.end());
+    mp.near_rec_max = std::max(mp.near_rec_max, (int)rec.size());
+  }
+  rec_out = &mp.recs;
+  const int n_near = 0;
   // ---- far-field tasks in topological order ---------------------------------------------
   std::vector<int> up_task(h->P, -1), up_of_span_root(h->P, -1);
   for (int i = 0; i < m; ++i)  // A. forward spans, bottom tier first
@@ -649,6 +655,8 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
   int couple_smem = 0;
   {
     const int64_t cap = 4000;  // double2 elements per warp-mode group (64 KB)
+    int couple_items = 8;
+    if (const char* e = getenv("H2B_DEBUG_COUPLE_ITEMS")) couple_items = std::max(1, atoi(e));  // profiling
     size_t i = 0;
     while (i < citems_all.size()) {
       const int64_t e0 = (int64_t)citems_all[i].R * citems_all[i].w + citems_all[i].R;
@@ -664,9 +672,12 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
         pelems = (int64_t)citems_all[i].R * citems_all[i].w;
         ++i;
       } else {
-        while (i < citems_all.size() && (int)members.size() < 64) {
+        // a group is one round of the CTA's warps (8 panels), within one level: the coupling
+        // tasks sit on the far-field critical path, so many small tasks beat few big ones
+        const int lvl0 = level_of(h, targets[i]);
+        while (i < citems_all.size() && (int)members.size() < couple_items) {
           const int64_t e = (int64_t)citems_all[i].R * citems_all[i].w + citems_all[i].R;
-          if (e > 3000 || elems + e > cap) break;
+          if (e > 3000 || elems + e > cap || level_of(h, targets[i]) != lvl0) break;
           mp.citems.push_back(citems_all[i]);
           members.push_back(targets[i]);
           elems += e;
@@ -708,9 +719,6 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
   for (auto& s : tier[0]) {
     if (s.dn_head < 0) continue;
     std::vector<int> deps = down_deps(0, s);
-    for (int p : span_clusters(0, s.root, true))
-      if (leaf_pos[p] >= 0)
-        for (int k = nt_first_of_leaf[leaf_pos[p]]; k <= nt_of_leaf_last[leaf_pos[p]]; ++k) deps.push_back(k);
     add_l(T_SPAN, s.dn_head, deps, span_dur(s.dn_head));
   }
   // ---- static schedule -----------------------------------------------------------------
@@ -722,10 +730,8 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
   const int nl_all = (int)lt.size();
   const int n_far = nl_all - n_near;
   const int g_total = std::max(2, grid_est);
-  int g_near = std::max(1, std::min(n_near, g_total / 2));
-  if (const char* e = getenv("H2B_DEBUG_GNEAR")) g_near = std::max(1, std::min(n_near, atoi(e)));  // profiling
-  int g_far = n_far > 0 ? g_total - g_near : 0;
-  if (n_far == 0) g_near = std::min(n_near, g_total);
+  int g_near = 0;
+  int g_far = n_far > 0 ? g_total : 0;
   std::vector<double> fin(nl_all, 0.0);
   std::vector<std::vector<int>> lists(g_near + g_far);
   {
@@ -823,7 +829,26 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
     if (!l.empty()) mp.recs.insert(mp.recs.end(), blob.begin(), blob.end());
     mp.blob_slots = std::max(mp.blob_slots, (int)blob.size());
   }
-  mp.est_makespan = *std::max_element(fin.begin(), fin.end());
+  mp.est_makespan = fin.empty() ? 0.0 : *std::max_element(fin.begin(), fin.end());
+  if (const char* path = getenv("H2B_DUMP_PLAN")) {  // profiling aid: the schedule as text
+    if (FILE* f = fopen(path, "w")) {
+      fprintf(f, "# splits");
+      for (int sp : splits) fprintf(f, " %d", sp);
+      fprintf(f, "\n# qid type arg cta est_dur est_fin nlev : deps (queue ids)\n");
+      std::vector<int> cta_of(nl_all, -1);
+      for (size_t c = 0; c < lists.size(); ++c)
+        for (int id : lists[c]) cta_of[id] = (int)c;
+      for (int pos = 0; pos < nl_all; ++pos) {
+        const int id = by_q[pos];
+        const LTask& l = lt[id];
+        fprintf(f, "%d %d %d %d %.2f %.2f %d :", pos, l.type, l.arg, cta_of[id], l.dur, fin[id],
+                l.type == T_SPAN ? mp.prog.heads[l.arg].nlev : 0);
+        for (int d : l.deps) fprintf(f, " %d", qid[d < n_near ? near_run_last[d] : d]);
+        fprintf(f, "\n");
+      }
+      fclose(f);
+    }
+  }
   if (getenv("H2B_VERIFY_PLAN")) {
     // self-check (debugging aid): every two tasks that touch the same x̂ / ŷ / y elements, one
     // of them writing, must be ordered by the schedule (CTA list order + dependency edges)
@@ -1036,7 +1061,7 @@ int h2b_prepare(h2b_ctx* h) {
     MegaPlan mp;
     int sms_est = 148;
     cudaDeviceGetAttribute(&sms_est, cudaDevAttrMultiProcessorCount, h->device);
-    if (plan_mega(h, citems, targets, 2 * sms_est, mp)) {
+    if (plan_mega(h, citems, targets, sms_est, mp)) {
       H2B_TRY(to_device(&h->span_heads, mp.prog.heads, &acc));
       H2B_TRY(to_device(&h->span_copies, mp.prog.copies, &acc));
       H2B_TRY(to_device(&h->span_outs, mp.prog.outs, &acc));
@@ -1048,8 +1073,12 @@ int h2b_prepare(h2b_ctx* h) {
       H2B_TRY(to_device(&h->couple_groups, mp.groups, &acc));
       H2B_TRY(to_device(&h->rec_pool, mp.recs, &acc));
       H2B_TRY(to_device(&h->cta_lists, mp.cta_lists, &acc));
+      H2B_TRY(to_device(&h->near_recs, mp.near_recs, &acc));
+      H2B_TRY(to_device(&h->near_idx, mp.near_idx, &acc));
+      h->n_near_tasks = (int)mp.near_idx.size();
+      h->near_rec_max = mp.near_rec_max;
       h->mega_blob_slots = mp.blob_slots;
-      {  // far-field operands warmed into L2 at every launch (64 KB pieces)
+      {  // far-field operands that may be warmed into L2 at launch (64 KB pieces; off by default)
         std::vector<int4> pf;
         auto add = [&](const void* p, int64_t bytes) {
           for (int64_t o = 0; o < bytes; o += 65536) {
@@ -1080,15 +1109,30 @@ int h2b_prepare(h2b_ctx* h) {
       h->h_tasks = mp.tasks;
       h->mega_ns = mp.ns;
       h->mega_r = mp.r;
-      // near-field stages use the whole budget (2 CTAs per SM still fit)
-      h->mega_smem = std::max(mp.smem, mp.ns > 0 ? 16 * MEGA_BUDGET : 16);
       h->mega_tiers = mp.tiers;
-      H2B_TRY(h2b_mega_set_smem(mp.ns, mp.r, 16 * (MEGA_BUDGET + MEGA_BLOB_MAX)));
-      int per_sm = 0, sms = 0;
-      H2B_TRY(h2b_mega_occupancy(mp.ns, mp.r, h->mega_smem + 16 * h->mega_blob_slots, &per_sm));
+      int sms = 0;
       H2B_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
-      // the static schedule assumed 2 CTAs per SM: the launch must be fully co-resident
+      // far-field task graph: one CTA per SM, all co-resident (they wait on one another)
+      h->mega_smem = std::max(mp.smem, 16);
       h->mega_grid = (int)mp.cta_lists.size();
+      const int far_bytes = h->mega_smem + 16 * h->mega_blob_slots;
+      H2B_TRY(h2b_mega_set_smem(0, 0, 16 * (MEGA_BUDGET + MEGA_BLOB_MAX)));
+      int per_sm = 1;
+      if (h->mega_grid > 0) H2B_TRY(h2b_mega_occupancy(0, 0, far_bytes, &per_sm));
+      // near-field stream: one CTA per SM beside the far-field CTA, ring in the shared memory left
+      int near_static = 0;
+      H2B_TRY(h2b_near_stream_static_smem(mp.ns, mp.r, &near_static));
+      const int sm_total = 233472 - 2048;  // per SM, minus the per-CTA reservations of both kernels
+      const int far_total = h->mega_grid > 0 ? far_bytes + h2b_mega_static_smem() : 0;
+      const int rec_bytes = 3 * 16 * std::max(1, mp.near_rec_max);  // NRB record buffers
+      const int stg = mp.ns > 0 ? 16 * (mp.r * (256 / (mp.ns / 2)) * mp.ns + mp.ns) : 0;
+      int nst = stg > 0 ? std::min(8, (sm_total - far_total - near_static - rec_bytes) / stg) : 0;
+      if (mp.ns > 0 && nst < 2) nst = 2;  // still correct; the two kernels then share SMs less well
+      h->near_nst = nst;
+      h->near_smem = nst * stg + rec_bytes;
+      // the attribute is per kernel and process-wide: set the maximum, never a per-handle size
+      H2B_TRY(h2b_near_stream_set_smem(mp.ns, mp.r, 232448 - near_static));
+      h->near_grid = sms;
       h->mega = (per_sm > 0 && h->mega_grid <= per_sm * sms) ? 1 : 0;
       h->mega_est_us = mp.est_makespan;
     }

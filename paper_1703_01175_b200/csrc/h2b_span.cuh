@@ -39,7 +39,7 @@ __device__ __forceinline__ void span_stage_static(const SpanHead* __restrict__ h
 template <int NTH>
 __device__ __forceinline__ void span_finish(const SpanHead* __restrict__ hd, const SpanCopy* __restrict__ copies,
                                             const SpanBases& B, double2* sm, uint64_t* bar, uint32_t phase,
-                                            uint64_t* t_staged = nullptr) {
+                                            uint64_t* t_staged = nullptr, int y_mode = 2) {
   const int n_copy = hd->n_copy, c_first = hd->copy_first;
   for (int i = threadIdx.x; i < n_copy; i += NTH) {
     const SpanCopy c = copies[c_first + i];
@@ -59,10 +59,11 @@ __device__ __forceinline__ void span_finish(const SpanHead* __restrict__ hd, con
     const int o1 = hd->lvl[lv + 1];
     for (int i = hd->lvl[lv] + warp; i < o1; i += NW) {
       const SpanOp op = ops[i];
-      // y was written by the near-field (possibly on another SM): accumulate through L2
+      // y: written by the near field before (y_mode 2: accumulate through L2) or concurrently
+      // (y_mode 3: atomic add)
       const bool to_y = op.flags & OP_OUT_Y;
       panel_op(sm + op.pay, op.R, op.w, op.pad0, sm + op.in, to_y ? B.y + op.out : sm + op.out,
-               to_y ? 2 : ((op.flags & OP_ACC) ? 1 : 0));
+               to_y ? y_mode : ((op.flags & OP_ACC) ? 1 : 0));
     }
     __syncthreads();
     if (t_staged && threadIdx.x == 0 && lv < 2) {  // trace: end of the first two levels

@@ -12,7 +12,9 @@ for k in [int(a) for a in sys.argv[1:]] or [1, 2]:
     from paper_1703_01175_b200.timing import L2Flusher
     flush = L2Flusher("cuda")
     res = {}
-    for dbg, name in ((0, "full"), (1, "near only"), (2, "far only"), (3, "no bodies")):
+    modes = [(0, "full"), (2, "near alone"), (4, "far alone"), (1, "near + far skeleton"), (5, "far skeleton")]
+    modes += [(int(a), f"dbg{a}") for a in os.environ.get("EXTRA_DEBUG", "").split(",") if a]
+    for dbg, name in modes:
         _abi.check(L.h2b_set_option(op.handle, 4, dbg))
         for _ in range(3): op.matvec_perm(x, out=y)
         tot = 0.0
@@ -25,4 +27,4 @@ for k in [int(a) for a in sys.argv[1:]] or [1, 2]:
     _abi.check(L.h2b_set_option(op.handle, 4, 0))
     nb = pk.near_bytes()
     print(f"cfg{k}: " + "  ".join(f"{n} {v:.1f} us" for n, v in res.items()) +
-          f"  | near-only {nb / res['near only'] / 1e3:.0f} GB/s")
+          f"  | near alone {nb / res['near alone'] / 1e3:.0f} GB/s")

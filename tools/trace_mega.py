@@ -1,6 +1,8 @@
 """Record the persistent kernel's per-task timeline on data/cfg<k>.npz (L2 flushed first).
 usage: trace_mega.py K [debug]   (debug: H2B_OPT_DEBUG bits, profiling only)"""
 import sys, os, ctypes as C
+os.makedirs("gpurun_out", exist_ok=True)
+os.environ.setdefault("H2B_DUMP_PLAN", f"gpurun_out/plan_cfg{sys.argv[1] if len(sys.argv) > 1 else 2}.txt")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_1703_01175_b200 import H2Operator, load_packed, _abi
