@@ -41,7 +41,7 @@ void free_ctx(h2b_ctx* h) {
                   h->couple_targets, h->span_heads, h->span_copies, h->span_outs,
                   h->span_ops, h->near_items, h->near_blks, h->couple_items, h->tasks, h->deps,
                   h->near_tasks, h->leaf_items, h->couple_groups, h->ctrl, h->flags, h->trace,
-                  h->rec_pool, h->l2_prefetch, h->cta_lists, h->task_list, h->near_recs, h->near_idx};
+                  h->rec_pool, h->l2_prefetch, h->cta_lists, h->task_list, h->near_recs, h->near_idx, h->wbuf, h->ydeep};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->far_stream) cudaStreamDestroy(h->far_stream);

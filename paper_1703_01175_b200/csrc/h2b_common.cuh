@@ -117,6 +117,7 @@ struct SpanOp {          // out[c] (+)= sum_r P[r*w+c] in[r], c < w, r < R
 };
 constexpr int OP_ACC = 1;       // accumulate into out
 constexpr int OP_OUT_Y = 2;     // out is an element offset into global y, not smem
+constexpr int OP_OUT_YD = 4;    // with OP_OUT_Y: into y_deep instead (overwrite), see FlatRec
 constexpr int SPAN_MAXLEV = 24;
 struct SpanHead {
   int32_t copy_first, n_copy, out_first, n_out;
@@ -153,7 +154,17 @@ struct CoupleItem {
 // tasks with smaller ids (claimed by running CTAs), so progress is guaranteed.
 // Completion flags are epoch-stamped, so nothing is reset between matvecs.
 // ---------------------------------------------------------------------------
-enum TaskType : int32_t { T_NEAR = 0, T_SPAN = 1, T_COUPLE = 2 };
+enum TaskType : int32_t { T_NEAR = 0, T_SPAN = 1, T_COUPLE = 2, T_FLAT_UP = 3, T_FLAT_DOWN = 4 };
+// Flattened bottom tier (see plan_mega): for a cluster c at the split level ls,
+// W_c = [V_l T_l T_parent(l) ... ]_{leaves l of c} (n_c x k_c, row-major) maps the points of c
+// straight to x̂_c (T_FLAT_UP: x̂_c = W_cᵀ x_c) and ŷ_c straight back (T_FLAT_DOWN:
+// y_c += W_c ŷ_c + y_deep_c, y_deep = what the levels below ls add, written by "deep" spans).
+struct FlatRec {
+  int64_t w_off;    // element offset of W_c in the flattened-basis buffer
+  int64_t x_off;    // first point of c (x / y / y_deep offset)
+  int64_t hat_off;  // x̂ / ŷ offset of c
+  int32_t n, k;     // points and rank of c
+};
 struct Task {
   int32_t type, arg;        // arg: near task / span head / couple group index
   int32_t dep_first, n_dep; // ranges [dep_first, dep_first + n_dep) of DepRange
@@ -264,6 +275,10 @@ struct h2b_ctx {
   int4* near_recs = nullptr;           // near task records
   int2* near_idx = nullptr;            // per near task {first slot, slots}
   int n_near_tasks = 0, near_rec_max = 0, near_nst = 0, near_smem = 0, near_grid = 0;
+  // flattened bottom tier (0 = off): W buffer and the deep spans' y_deep
+  int mega_flat = 0;
+  double2* wbuf = nullptr;
+  double2* ydeep = nullptr;
   // near / coupling work lists
   NearItem* near_items = nullptr;
   NearBlk* near_blks = nullptr;

@@ -169,6 +169,7 @@ SpanBases bases_of(const h2b_ctx* h, const double2* xp, double2* yp) {
   B.xhat = h->xhat;
   B.yhat = h->yhat;
   B.y = yp;
+  B.ydeep = h->ydeep;
   return B;
 }
 

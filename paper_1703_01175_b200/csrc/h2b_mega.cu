@@ -38,6 +38,11 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -295,6 +300,11 @@ struct MegaArgs {
   const int32_t* xcol;
   double2* xhat;
   double2* yhat;
+  // flattened bottom tier
+  const double2* wbuf;
+  const double2* x;
+  double2* y;
+  const double2* ydeep;
   uint64_t* trace;  // optional: per task {claim, ready, staged, done, smid} (globaltimer ns)
   int smem_elems;   // dynamic shared memory (double2) of the work area
   int debug;        // profiling aid (H2B_OPT_DEBUG)
@@ -359,7 +369,51 @@ __device__ __forceinline__ void couple_task(const MegaArgs& A, const int4* rec, 
   }
 }
 
-__global__ void __launch_bounds__(MNT, 1) k_mega(MegaArgs A) {
+// ---------------------------------------------------------------------------
+// flattened bottom tier (FlatRec): W_c staged with x_c (up) or alone (down) before the
+// dependencies are met
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void flat_stage_static(const MegaArgs& A, const FlatRec& f, bool up, double2* sm,
+                                                  uint64_t* bar) {
+  if (threadIdx.x == 0) {
+    const uint32_t wb = 16u * (uint32_t)f.n * f.k;
+    mbar_arrive_expect_tx(bar, wb + (up ? 16u * f.n : 0u));
+    bulk_g2s(sm, A.wbuf + f.w_off, wb, bar);
+    if (up) bulk_g2s(sm + (size_t)f.n * f.k, A.x + f.x_off, 16u * f.n, bar);
+  }
+}
+
+// x̂_c = W_cᵀ x_c (whole CTA, column-major accumulation as in the span ops)
+__device__ __forceinline__ void flat_up(const MegaArgs& A, const FlatRec& f, double2* sm, uint64_t* bar,
+                                        double2* red) {
+  mbar_wait(bar, 0);
+  const double2* xs = sm + (size_t)f.n * f.k;
+  cta_panel_q<MNT>(sm, f.n, f.k, [=] __device__(int64_t r, int) { return xs[r]; }, A.xhat + f.hat_off, false, 1,
+                   red);
+}
+
+// y_c += W_c ŷ_c + y_deep_c, one thread per point, one atomic add per element
+__device__ __forceinline__ void flat_down(const MegaArgs& A, const FlatRec& f, double2* sm, uint64_t* bar,
+                                          double2* red) {
+  if (threadIdx.x < f.k) red[threadIdx.x] = __ldcg(A.yhat + f.hat_off + threadIdx.x);
+  mbar_wait(bar, 0);
+  __syncthreads();
+  for (int r = threadIdx.x; r < f.n; r += MNT) {
+    double2 a0 = __ldcg(A.ydeep + f.x_off + r), a1 = make_double2(0.0, 0.0);
+    const double2* w = sm + (size_t)r * f.k;
+    int c = 0;
+    for (; c + 1 < f.k; c += 2) {
+      cfma(a0, w[c], red[c]);
+      cfma(a1, w[c + 1], red[c + 1]);
+    }
+    if (c < f.k) cfma(a0, w[c], red[c]);
+    const double2 v = cadd(a0, a1);
+    atomicAdd(&A.y[f.x_off + r].x, v.x);
+    atomicAdd(&A.y[f.x_off + r].y, v.y);
+  }
+}
+
+__global__ void __launch_bounds__(MNT, 2) k_mega(MegaArgs A) {
   // dynamic shared memory: [work area: span working set / coupling panels][this CTA's blob:
   // its task list, dependency ranges and task records, one bulk copy]
   extern __shared__ __align__(16) double2 sm[];
@@ -418,12 +472,15 @@ __global__ void __launch_bounds__(MNT, 1) k_mega(MegaArgs A) {
     }
     phase = 0;
     // static operands stream in while the dependencies are still outstanding
+    const FlatRec& fr = *reinterpret_cast<const FlatRec*>(rec);
     if (!skip && type == T_SPAN)
       span_stage_static<MNT>(hd, cps, A.B, sm, &bar);
-    else if (!skip)
+    else if (!skip && type == T_COUPLE)
       couple_stage_static(A, rec, sm, &bar);
+    else if (!skip)
+      flat_stage_static(A, fr, type == T_FLAT_UP, sm, &bar);
     // dependencies: warp 0 polls (lanes share the flags) with a short backoff; the other warps
-    // wait at the barrier
+    // wait at the barrier.  A lane re-reads only the flag it is waiting for.
     if (threadIdx.x < 32)
       for (int i = 0; i < n_dep; ++i) {
         const int2 rg = deps[i];
@@ -447,8 +504,12 @@ __global__ void __launch_bounds__(MNT, 1) k_mega(MegaArgs A) {
       // profiling aid only (H2B_OPT_DEBUG): this task's body is skipped
     } else if (type == T_SPAN) {
       span_finish<MNT>(hd, cps, A.B, sm, &bar, phase, A.trace ? A.trace + 8 * t + 2 : nullptr, 3);
-    } else {
+    } else if (type == T_COUPLE) {
       couple_task(A, rec, red, sm, &bar, phase);
+    } else if (type == T_FLAT_UP) {
+      flat_up(A, fr, sm, &bar, red);
+    } else {
+      flat_down(A, fr, sm, &bar, red);
     }
     // this task's generic shared-memory writes precede the next task's TMA writes into the
     // same work area (the consumers of x̂ / ŷ order their TMA reads after their acquire)
@@ -533,7 +594,7 @@ int h2b_near_stream_set_smem(int ns, int r, int bytes) {
 
 // y = 0; then k_near_stream on st and k_mega on h->far_stream, concurrently (fork / join)
 int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st) {
-  H2B_CUDA_TRY(cudaMemsetAsync(yp, 0, sizeof(double2) * h->n, st));
+  if (!(h->mega_debug & 8)) H2B_CUDA_TRY(cudaMemsetAsync(yp, 0, sizeof(double2) * h->n, st));
   const bool run_far = h->mega_grid > 0 && !(h->mega_debug & 2);
   const bool run_near = h->n_near_tasks > 0 && !(h->mega_debug & 4);
   if (run_far) {
@@ -558,6 +619,11 @@ int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st)
     A.B.xhat = h->xhat;
     A.B.yhat = h->yhat;
     A.B.y = yp;
+    A.B.ydeep = h->ydeep;
+    A.wbuf = h->wbuf;
+    A.x = xp;
+    A.y = yp;
+    A.ydeep = h->ydeep;
     A.sbuf = h->buf[H2B_SEC_S];
     A.xcol = h->s_xcol;
     A.xhat = h->xhat;

@@ -8,6 +8,8 @@
 #include <cstring>
 #include <functional>
 #include <queue>
+#include <set>
+#include <tuple>
 
 #include "h2b_common.cuh"
 #include "h2b_panel.cuh"
@@ -52,6 +54,43 @@ __global__ void k_transpose_inplace(const BlockDesc* __restrict__ bl, double2* b
     const int64_t c = e / b.rows, r = e - c * b.rows;
     buf[b.off + e] = sm[r * b.cols + c];
   }
+}
+
+// flattened bases (prepare time): W rows of one leaf = V_l T_l T_parent(l) ... up to level ls
+struct FlatLeaf {
+  int64_t v_off, w_off;   // V_l in the V payload; first W element of the leaf's rows
+  int32_t n, k0;          // leaf size and rank
+  int32_t step_first, n_steps;
+};
+struct FlatStep {
+  int64_t t_off;          // the child's rows inside its parent's T block (rows x cols, row-major)
+  int32_t rows, cols;
+};
+__global__ void k_flatten(const FlatLeaf* __restrict__ leaves, const FlatStep* __restrict__ steps,
+                          const double2* __restrict__ vbuf, const double2* __restrict__ tbuf,
+                          double2* __restrict__ wbuf, int kmax) {
+  extern __shared__ double2 fs[];
+  const FlatLeaf L = leaves[blockIdx.x];
+  double2* a = fs;
+  double2* b = fs + (size_t)L.n * kmax;
+  int k = L.k0;
+  for (int e = threadIdx.x; e < L.n * k; e += blockDim.x) a[e] = vbuf[L.v_off + e];
+  __syncthreads();
+  for (int st = 0; st < L.n_steps; ++st) {
+    const FlatStep S = steps[L.step_first + st];
+    for (int e = threadIdx.x; e < L.n * S.cols; e += blockDim.x) {
+      const int i = e / S.cols, j = e - i * S.cols;
+      double2 acc = make_double2(0.0, 0.0);
+      for (int l = 0; l < S.rows; ++l) cfma(acc, a[i * k + l], tbuf[S.t_off + (int64_t)l * S.cols + j]);
+      b[i * S.cols + j] = acc;
+    }
+    __syncthreads();
+    double2* t = a;
+    a = b;
+    b = t;
+    k = S.cols;
+  }
+  for (int e = threadIdx.x; e < L.n * k; e += blockDim.x) wbuf[L.w_off + e] = a[e];
 }
 
 template <typename T>
@@ -192,8 +231,10 @@ struct Plan {
 double launch_cost(int smem_elems, int nlev) { return 2.0 + 16.0 * smem_elems / 100e3 + 0.3 * nlev; }
 
 // subtree span rooted at r covering levels [level(r), level(r) + nl): UP or DOWN program
+// deep (flattened bottom tier): the root's own level is left to the flat tasks: no x̂ output
+// for the root (up), no propagation from the root and leaf results into y_deep (down)
 bool build_subtree_span(const h2b_ctx* h, Prog& P, int r, int nl, bool up, bool input_last,
-                        int* smem_max) {
+                        int* smem_max, bool deep = false) {
   SB s;
   auto R = desc_ranges(h, r, nl);
   const int n = (int)R.size();
@@ -215,7 +256,7 @@ bool build_subtree_span(const h2b_ctx* h, Prog& P, int r, int nl, bool up, bool 
     if (up)
       xh[i] = (i < ncomp) ? s.alloc((int)xe) : s.in(SRC_XHAT, xb, xe);
     else
-      xh[i] = s.in(SRC_YHAT, xb, xe);
+      xh[i] = (deep && i == 0) ? s.alloc((int)xe) : s.in(SRC_YHAT, xb, xe);
   }
   auto emit_level = [&](int i) {
     s.level();
@@ -230,7 +271,7 @@ bool build_subtree_span(const h2b_ctx* h, Prog& P, int r, int nl, bool up, bool 
         if (up)
           s.op(pay, x_sm + (h->c_start[p] - h->c_start[r]), out_here, h->c_size[p], k, 0);
         else
-          s.op(pay, out_here, h->c_start[p], k, h->c_size[p], OP_ACC | OP_OUT_Y);
+          s.op(pay, out_here, h->c_start[p], k, h->c_size[p], deep ? (OP_OUT_Y | OP_OUT_YD) : (OP_ACC | OP_OUT_Y));
       } else {
         const int m = m_of(h, p);
         const int pay = ts[i] + (int)(h->c_toff[p] - tb[i]);
@@ -242,12 +283,13 @@ bool build_subtree_span(const h2b_ctx* h, Prog& P, int r, int nl, bool up, bool 
       }
     }
   };
+  const int first = deep ? 1 : 0;  // deep: the root level belongs to the flat tasks
   if (up)
-    for (int i = ncomp - 1; i >= 0; --i) emit_level(i);
+    for (int i = ncomp - 1; i >= first; --i) emit_level(i);
   else
-    for (int i = 0; i < ncomp; ++i) emit_level(i);
+    for (int i = first; i < ncomp; ++i) emit_level(i);
   if (up) {
-    for (int i = 0; i < ncomp; ++i)
+    for (int i = first; i < ncomp; ++i)
       s.outc(SRC_XHAT, h->c_xoff[R[i].a], h->c_xoff[R[i].b] - h->c_xoff[R[i].a], xh[i]);
   } else if (input_last) {
     const int i = n - 1;
@@ -402,7 +444,7 @@ bool plan_with_split(const h2b_ctx* h, int ls, Plan& pl) {
 }
 
 // ------------------------- persistent-kernel task graph -------------------------
-constexpr int MEGA_BUDGET = 5800;  // double2 elements (92.8 KB) of work area per CTA
+constexpr int MEGA_BUDGET = 5800;  // double2 elements (92.8 KB): largest work area of a far CTA
 constexpr int MEGA_BLOB_MAX = 1024;  // 16-byte slots (16 KB) of per-CTA task blob
 constexpr double NEAR_TASK_BYTES = 64e3;  // target D bytes per near-field task
 
@@ -444,11 +486,15 @@ struct MegaPlan {
   std::vector<int4> near_recs;  // near-field task records (claimed dynamically by the stream kernel)
   std::vector<int2> near_idx;   // per near task {first slot, slots} in near_recs
   int ns = 0, r = 1, smem = 0, tiers = 0, blob_slots = 0, near_rec_max = 0;
+  bool flat = false;
+  std::vector<FlatRec> flat_recs;  // per split-level cluster (flat mode)
+  int64_t flat_elems = 0;          // W buffer size (double2)
+  int flat_level = -1;             // ls
   double est_makespan = 0.0;
 };
 
 bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
-               const std::vector<int32_t>& targets, int grid_est, MegaPlan& mp) {
+               const std::vector<int32_t>& targets, int grid_est, int budget, MegaPlan& mp) {
   const int L = h->depth;
   int min_leaf = L - 1;
   for (int p = 0; p < h->P; ++p)
@@ -456,19 +502,36 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
   // ---- tiers: bottom split ls, then upper splits up to the root -----------------
   int ls = -1;
   for (int l = 0; l <= min_leaf && ls < 0; ++l)
-    if (tier_fits(h, l, L - l, false, MEGA_BUDGET)) ls = l;
+    if (tier_fits(h, l, L - l, false, budget)) ls = l;
   if (ls < 0) return false;
   std::vector<int> splits = {ls};  // bottom-up list of tier roots
   while (splits.back() > 0) {
     const int cur = splits.back();
     int s = -1;
     for (int c = 0; c < cur && s < 0; ++c)
-      if (tier_fits(h, c, cur - c + 1, true, MEGA_BUDGET)) s = c;
+      if (tier_fits(h, c, cur - c + 1, true, budget)) s = c;
     if (s < 0) return false;
     splits.push_back(s);
   }
   const int m = (int)splits.size();  // tier 0 = bottom
   mp.tiers = m;
+  // Flattened bottom tier: the critical chain then enters the upper tiers through one
+  // W_cᵀ x_c per split-level cluster instead of a sweep over all the levels below it, and
+  // leaves them through one W_c ŷ_c (plus y_deep from the deep spans, off the critical
+  // chain).  Needs every leaf on the deepest level, a few levels below ls and W_c (plus x_c)
+  // in the work area.
+  bool flat = m >= 2 && min_leaf == L - 1 && h->uniform_leaf > 0 && ls <= L - 3 && !getenv("H2B_NO_FLAT");
+  for (int r = h->level_ptr[ls]; flat && r < h->level_ptr[ls + 1]; ++r)
+    flat = h->c_rank[r] > 0 && (int64_t)h->c_size[r] * (h->c_rank[r] + 1) <= budget;
+  for (int p = h->level_ptr[ls]; flat && p < h->P; ++p)
+    if (h->c_child_lo[p] < 0) flat = h->c_rank[p] > 0;
+  if (flat) {  // the prepare-time product kernel keeps two (leaf x max rank) tiles in smem
+    int kmax = 1;
+    for (int p = 0; p < h->P; ++p) kmax = std::max(kmax, h->c_rank[p]);
+    flat = 2 * 16 * h->uniform_leaf * kmax <= 200 * 1024;
+  }
+  mp.flat = flat;
+  mp.flat_level = ls;
   // ---- span programs ---------------------------------------------------------------
   struct SpanRef {
     int root, up_head, dn_head;  // head index or -1 when the span has no ops
@@ -484,7 +547,7 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
       SpanRef s{r, -1, -1};
       for (int dir = 0; dir < 2; ++dir) {
         const size_t h0 = P.heads.size();
-        if (!build_subtree_span(h, P, r, nl, dir == 0, !bottom, &smem)) return false;
+        if (!build_subtree_span(h, P, r, nl, dir == 0, !bottom, &smem, flat && bottom)) return false;
         if (P.heads.back().n_ops == 0) {  // nothing to do: drop it again
           P.ops.resize(P.ops.size() - 0);
           P.copies.resize(P.heads.back().copy_first);
@@ -514,6 +577,8 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
       hd.copy_first = 0;  // copies follow the head inside the record
       push_slots(&hd, sizeof(SpanHead));
       push_slots(mp.prog.copies.data() + c0, sizeof(SpanCopy) * hd.n_copy);
+    } else if (type == T_FLAT_UP || type == T_FLAT_DOWN) {
+      push_slots(&mp.flat_recs[arg], sizeof(FlatRec));
     } else if (type == T_COUPLE) {
       const CoupleGroup& g = mp.groups[arg];
       const int4 hdr{g.n_items, g.cta_mode, 0, 0};
@@ -566,7 +631,8 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
       for (int p = R[i].a; p < R[i].b; ++p) cl.push_back(p);
     return cl;
   };
-  auto span_dur = [&](int head) { return 2.0 + 0.7 * mp.prog.heads[head].nlev; };
+  // estimated run times (us), calibrated on B200 traces: staging + ~1 us per level + write-back
+  auto span_dur = [&](int head) { return 3.5 + 1.0 * mp.prog.heads[head].nlev; };
   // ---- near-field work list (leaf order) --------------------------------------------
   const int ns = h->uniform_leaf;
   const int nleaves = (int)h->h_leaves.size();
@@ -637,13 +703,34 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
   rec_out = &mp.recs;
   const int n_near = 0;
   // ---- far-field tasks in topological order ---------------------------------------------
-  std::vector<int> up_task(h->P, -1), up_of_span_root(h->P, -1);
+  std::vector<int> up_task(h->P, -1), up_of_span_root(h->P, -1), flat_of(h->P, -1);
+  if (flat) {  // the flattened bases' records, one per split-level cluster
+    int64_t w = 0;
+    for (int r = h->level_ptr[ls]; r < h->level_ptr[ls + 1]; ++r) {
+      flat_of[r] = (int)mp.flat_recs.size();
+      mp.flat_recs.push_back(FlatRec{w, (int64_t)h->c_start[r], h->c_xoff[r], h->c_size[r], h->c_rank[r]});
+      w += (int64_t)h->c_size[r] * h->c_rank[r];
+      mp.smem = std::max(mp.smem, 16 * h->c_size[r] * (h->c_rank[r] + 1));
+    }
+    mp.flat_elems = w;
+  }
+  auto flat_dur = [&](int r) { return 3.0 + 16.0 * h->c_size[r] * h->c_rank[r] / 2e4; };
   for (int i = 0; i < m; ++i)  // A. forward spans, bottom tier first
     for (auto& s : tier[i]) {
       std::vector<int> deps;
       if (i > 0)  // children spans: tier i-1 spans rooted inside this span's input level
         for (int p : span_clusters(i, s.root, true))
           if (up_of_span_root[p] >= 0 && level_of(h, p) == splits[i - 1]) deps.push_back(up_of_span_root[p]);
+      if (flat && i == 0) {  // x̂ of the root straight from x; the deep span does the levels below
+        const int fid = add_l(T_FLAT_UP, flat_of[s.root], {}, flat_dur(s.root));
+        up_of_span_root[s.root] = fid;
+        up_task[s.root] = fid;
+        if (s.up_head < 0) continue;
+        const int id = add_l(T_SPAN, s.up_head, {}, span_dur(s.up_head));
+        for (int p : span_clusters(0, s.root, false))
+          if (p != s.root) up_task[p] = id;
+        continue;
+      }
       if (s.up_head < 0) continue;
       const int id = add_l(T_SPAN, s.up_head, deps, span_dur(s.up_head));
       up_of_span_root[s.root] = id;
@@ -655,8 +742,9 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
   int couple_smem = 0;
   {
     const int64_t cap = 4000;  // double2 elements per warp-mode group (64 KB)
-    int couple_items = 8;
+    int couple_items = 8, couple_items_deep = 32;
     if (const char* e = getenv("H2B_DEBUG_COUPLE_ITEMS")) couple_items = std::max(1, atoi(e));  // profiling
+    if (const char* e = getenv("H2B_DEBUG_COUPLE_DEEP")) couple_items_deep = std::max(1, atoi(e));
     size_t i = 0;
     while (i < citems_all.size()) {
       const int64_t e0 = (int64_t)citems_all[i].R * citems_all[i].w + citems_all[i].R;
@@ -664,7 +752,7 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
       std::vector<int> members;
       int64_t elems = 0, pelems = 0;
       if (e0 > 3000) {  // a big panel: the whole CTA streams it
-        if (citems_all[i].R > MEGA_BUDGET) return false;
+        if (citems_all[i].R > budget) return false;
         g.cta_mode = 1;
         mp.citems.push_back(citems_all[i]);
         members.push_back(targets[i]);
@@ -675,7 +763,10 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
         // a group is one round of the CTA's warps (8 panels), within one level: the coupling
         // tasks sit on the far-field critical path, so many small tasks beat few big ones
         const int lvl0 = level_of(h, targets[i]);
-        while (i < citems_all.size() && (int)members.size() < couple_items) {
+        // below the split level the couplings are off the critical chain (they only have to be
+        // done before the deep down spans): bigger groups there amortise the per-task overhead
+        const int max_items = lvl0 > ls ? couple_items_deep : couple_items;
+        while (i < citems_all.size() && (int)members.size() < max_items) {
           const int64_t e = (int64_t)citems_all[i].R * citems_all[i].w + citems_all[i].R;
           if (e > 3000 || elems + e > cap || level_of(h, targets[i]) != lvl0) break;
           mp.citems.push_back(citems_all[i]);
@@ -695,7 +786,7 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
         }
       mp.groups.push_back(g);
       group_members.push_back(members);
-      const int id = add_l(T_COUPLE, (int)mp.groups.size() - 1, deps, 1.5 + 16.0 * pelems / 2e4);
+      const int id = add_l(T_COUPLE, (int)mp.groups.size() - 1, deps, 3.5 + 16.0 * pelems / 2e4);
       for (int t : members) group_task[t] = id;
     }
   }
@@ -717,6 +808,18 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
       for (int p = R.back().a; p < R.back().b; ++p) dn_writer[p] = id;  // writes back the input level
     }
   for (auto& s : tier[0]) {
+    if (flat) {
+      // deep span: the levels below the root, from their couplings only, into y_deep; then the
+      // flat task adds W ŷ_root (ŷ_root complete once the tier above wrote it back) and y_deep
+      std::vector<int> deps, fdeps;
+      for (int p : span_clusters(0, s.root, true))
+        if (p != s.root && group_task[p] >= 0) deps.push_back(group_task[p]);
+      if (s.dn_head >= 0) fdeps.push_back(add_l(T_SPAN, s.dn_head, deps, span_dur(s.dn_head)));
+      if (dn_writer[s.root] >= 0) fdeps.push_back(dn_writer[s.root]);
+      if (group_task[s.root] >= 0) fdeps.push_back(group_task[s.root]);
+      add_l(T_FLAT_DOWN, flat_of[s.root], fdeps, flat_dur(s.root));
+      continue;
+    }
     if (s.dn_head < 0) continue;
     std::vector<int> deps = down_deps(0, s);
     add_l(T_SPAN, s.dn_head, deps, span_dur(s.dn_head));
@@ -766,22 +869,39 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
       for (int d : lt[id].deps) r = std::max(r, fin[d]);
       return r;
     };
-    using QE = std::pair<double, int>;
-    std::priority_queue<QE, std::vector<QE>, std::greater<QE>> cand, cta_free;
+    // upward rank: the longest estimated path from a task to the end (ids are topological)
+    std::vector<double> rank(nl_all, 0.0);
+    for (int id = nl_all - 1; id >= n_near; --id) {
+      double m = 0.0;
+      for (int u : users[id]) m = std::max(m, rank[u]);
+      rank[id] = lt[id].dur + m;
+    }
+    // list scheduling: the earliest-ready task first (the more critical one on ties), placed on
+    // a CTA that is free by then and whose previous task ends latest (best fit), so the
+    // critical chain never queues behind a task of another branch that waits for its inputs
+    double slack = 2.0;
+    if (const char* e = getenv("H2B_DEBUG_SLACK")) slack = atof(e);  // profiling
+    using QE = std::tuple<double, double, int>;  // ready time, -rank, id
+    std::priority_queue<QE, std::vector<QE>, std::greater<QE>> cand;
+    std::multiset<std::pair<double, int>> cta_free;
     for (int id = n_near; id < nl_all; ++id)
-      if (missing[id] == 0) cand.push({ready_time(id), id});
-    for (int c = 0; c < g_far; ++c) cta_free.push({0.0, g_near + c});
+      if (missing[id] == 0) cand.push({ready_time(id), -rank[id], id});
+    for (int c = 0; c < g_far; ++c) cta_free.insert({0.0, g_near + c});
     while (!cand.empty()) {
-      const auto [rt, id] = cand.top();
+      const auto [rt, nr, id] = cand.top();
       cand.pop();
-      const auto [ft, c] = cta_free.top();
-      cta_free.pop();
+      auto it = cta_free.upper_bound({rt, 1 << 30});
+      if (it != cta_free.begin()) --it;  // best fit: free by rt, latest such
+      const auto [ft, c] = *it;
+      cta_free.erase(it);
       fin[id] = std::max(rt, ft) + lt[id].dur;
-      cta_free.push({fin[id], c});
+      // the CTA counts as busy for `slack` times the estimate: run times vary under load, and a
+      // task that runs late must not hold up a critical one queued behind it on the same CTA
+      cta_free.insert({std::max(rt, ft) + slack * lt[id].dur, c});
       lists[c].push_back(id);
       order.push_back(id);
       for (int u : users[id])
-        if (--missing[u] == 0) cand.push({ready_time(u), u});
+        if (--missing[u] == 0) cand.push({ready_time(u), -rank[u], u});
     }
     if ((int)order.size() != n_far) return false;  // cycle: cannot happen
   }
@@ -832,7 +952,7 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
   mp.est_makespan = fin.empty() ? 0.0 : *std::max_element(fin.begin(), fin.end());
   if (const char* path = getenv("H2B_DUMP_PLAN")) {  // profiling aid: the schedule as text
     if (FILE* f = fopen(path, "w")) {
-      fprintf(f, "# splits");
+      fprintf(f, "# flat %d splits", (int)mp.flat);
       for (int sp : splits) fprintf(f, " %d", sp);
       fprintf(f, "\n# qid type arg cta est_dur est_fin nlev : deps (queue ids)\n");
       std::vector<int> cta_of(nl_all, -1);
@@ -853,7 +973,7 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
     // self-check (debugging aid): every two tasks that touch the same x̂ / ŷ / y elements, one
     // of them writing, must be ordered by the schedule (CTA list order + dependency edges)
     struct Acc {
-      int space;  // 0 x̂, 1 ŷ, 2 y
+      int space;  // 0 x̂, 1 ŷ, 2 y, 3 y_deep
       int64_t lo, hi;
       bool w;
       int q;
@@ -886,7 +1006,16 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
         }
         for (int o = op_first; o >= 0 && o < op_first + hd.n_ops; ++o) {
           const SpanOp& op = mp.prog.ops[o];
-          if (op.flags & OP_OUT_Y) acc.push_back({2, op.out, (int64_t)op.out + op.w, true, q});
+          if (op.flags & OP_OUT_Y)
+            acc.push_back({(op.flags & OP_OUT_YD) ? 3 : 2, op.out, (int64_t)op.out + op.w, true, q});
+        }
+      } else if (l.type == T_FLAT_UP || l.type == T_FLAT_DOWN) {
+        const FlatRec& f = mp.flat_recs[l.arg];
+        if (l.type == T_FLAT_UP) {
+          acc.push_back({0, f.hat_off, f.hat_off + f.k, true, q});
+        } else {
+          acc.push_back({1, f.hat_off, f.hat_off + f.k, false, q});
+          acc.push_back({3, f.x_off, f.x_off + f.n, false, q});
         }
       } else {
         for (int t : group_members[l.arg]) {
@@ -923,7 +1052,8 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
         if (++bad <= 20)
           fprintf(stderr, "plan check: unordered %s task %d (type %d arg %d) / %s task %d (type %d arg %d) on %s [%lld, %lld)\n",
                   "write", a.q, mp.tasks[a.q].type, mp.tasks[a.q].arg, b.w ? "write" : "read", b.q,
-                  mp.tasks[b.q].type, mp.tasks[b.q].arg, a.space == 0 ? "xhat" : a.space == 1 ? "yhat" : "y",
+                  mp.tasks[b.q].type, mp.tasks[b.q].arg,
+                  a.space == 0 ? "xhat" : a.space == 1 ? "yhat" : a.space == 2 ? "y" : "y_deep",
                   (long long)std::max(a.lo, b.lo), (long long)std::min(a.hi, b.hi));
       }
     }
@@ -1061,7 +1191,13 @@ int h2b_prepare(h2b_ctx* h) {
     MegaPlan mp;
     int sms_est = 148;
     cudaDeviceGetAttribute(&sms_est, cudaDevAttrMultiProcessorCount, h->device);
-    if (plan_mega(h, citems, targets, sms_est, mp)) {
+    // far-field CTAs per SM (each with a smaller work area) vs one: more CTAs keep the many
+    // short far-field tasks from queueing behind each other
+    int far_per_sm = 1;
+    if (const char* e = getenv("H2B_FAR_PER_SM")) far_per_sm = std::max(1, std::min(2, atoi(e)));
+    int budget = far_per_sm == 1 ? MEGA_BUDGET : 3900;
+    if (const char* e = getenv("H2B_MEGA_BUDGET")) budget = std::max(1000, std::min(MEGA_BUDGET, atoi(e)));
+    if (plan_mega(h, citems, targets, far_per_sm * sms_est, budget, mp)) {
       H2B_TRY(to_device(&h->span_heads, mp.prog.heads, &acc));
       H2B_TRY(to_device(&h->span_copies, mp.prog.copies, &acc));
       H2B_TRY(to_device(&h->span_outs, mp.prog.outs, &acc));
@@ -1076,6 +1212,51 @@ int h2b_prepare(h2b_ctx* h) {
       H2B_TRY(to_device(&h->near_recs, mp.near_recs, &acc));
       H2B_TRY(to_device(&h->near_idx, mp.near_idx, &acc));
       h->n_near_tasks = (int)mp.near_idx.size();
+      h->mega_flat = 0;
+      if (mp.flat) {  // flattened bases W (and the deep spans' y_deep)
+        std::vector<FlatLeaf> fl;
+        std::vector<FlatStep> fst;
+        int kmax = 1, nmax = 1;
+        for (int p = 0; p < P; ++p) kmax = std::max(kmax, h->c_rank[p]);
+        std::vector<int> parent(P, -1);
+        for (int p = 0; p < P; ++p)
+          if (h->c_child_lo[p] >= 0) parent[h->c_child_lo[p]] = parent[h->c_child_hi[p]] = p;
+        for (int t : h->h_leaves) {
+          int c = t;
+          FlatLeaf L{h->c_voff[t], 0, h->c_size[t], h->c_rank[t], (int)fst.size(), 0};
+          nmax = std::max(nmax, L.n);
+          while (level_of(h, c) > mp.flat_level) {
+            const int pp = parent[c];
+            const bool hi = h->c_child_hi[pp] == c;
+            const int64_t off = h->c_toff[pp] + (hi ? (int64_t)h->c_rank[h->c_child_lo[pp]] * h->c_rank[pp] : 0);
+            fst.push_back(FlatStep{off, h->c_rank[c], h->c_rank[pp]});
+            ++L.n_steps;
+            c = pp;
+          }
+          int64_t w0 = -1;
+          for (const FlatRec& r : mp.flat_recs)
+            if (r.x_off == h->c_start[c]) w0 = r.w_off;
+          L.w_off = w0 + (int64_t)(h->c_start[t] - h->c_start[c]) * h->c_rank[c];
+          fl.push_back(L);
+        }
+        const int fsm = 2 * 16 * nmax * kmax;  // <= 200 KB (checked by the planner)
+        {
+          H2B_CUDA_TRY(cudaMalloc(&h->wbuf, 16 * std::max<int64_t>(mp.flat_elems, 1)));
+          H2B_CUDA_TRY(cudaMalloc(&h->ydeep, 16 * std::max<int64_t>(h->n, 1)));
+          acc += 16 * (mp.flat_elems + h->n);
+          FlatLeaf* dl = nullptr;
+          FlatStep* ds = nullptr;
+          H2B_TRY(to_device(&dl, fl, nullptr));
+          H2B_TRY(to_device(&ds, fst, nullptr));
+          H2B_CUDA_TRY(cudaFuncSetAttribute(k_flatten, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm));
+          k_flatten<<<(int)fl.size(), 256, fsm>>>(dl, ds, h->buf[H2B_SEC_V], h->buf[H2B_SEC_T], h->wbuf, kmax);
+          H2B_CHECK_LAUNCH();
+          H2B_CUDA_TRY(cudaDeviceSynchronize());
+          cudaFree(dl);
+          cudaFree(ds);
+          h->mega_flat = 1;
+        }
+      }
       h->near_rec_max = mp.near_rec_max;
       h->mega_blob_slots = mp.blob_slots;
       {  // far-field operands that may be warmed into L2 at launch (64 KB pieces; off by default)
@@ -1123,7 +1304,7 @@ int h2b_prepare(h2b_ctx* h) {
       int near_static = 0;
       H2B_TRY(h2b_near_stream_static_smem(mp.ns, mp.r, &near_static));
       const int sm_total = 233472 - 2048;  // per SM, minus the per-CTA reservations of both kernels
-      const int far_total = h->mega_grid > 0 ? far_bytes + h2b_mega_static_smem() : 0;
+      const int far_total = h->mega_grid > 0 ? far_per_sm * (far_bytes + h2b_mega_static_smem() + 1024) : 0;
       const int rec_bytes = 3 * 16 * std::max(1, mp.near_rec_max);  // NRB record buffers
       const int stg = mp.ns > 0 ? 16 * (mp.r * (256 / (mp.ns / 2)) * mp.ns + mp.ns) : 0;
       int nst = stg > 0 ? std::min(8, (sm_total - far_total - near_static - rec_bytes) / stg) : 0;

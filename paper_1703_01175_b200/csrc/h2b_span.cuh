@@ -9,6 +9,7 @@ struct SpanBases {
   double2* xhat;
   double2* yhat;
   double2* y;
+  double2* ydeep;  // deep spans of a flattened bottom tier write here (overwrite)
 };
 
 // loads that must see data written earlier in the same kernel by other SMs
@@ -61,9 +62,10 @@ __device__ __forceinline__ void span_finish(const SpanHead* __restrict__ hd, con
       const SpanOp op = ops[i];
       // y: written by the near field before (y_mode 2: accumulate through L2) or concurrently
       // (y_mode 3: atomic add)
-      const bool to_y = op.flags & OP_OUT_Y;
-      panel_op(sm + op.pay, op.R, op.w, op.pad0, sm + op.in, to_y ? B.y + op.out : sm + op.out,
-               to_y ? y_mode : ((op.flags & OP_ACC) ? 1 : 0));
+      const bool to_y = op.flags & OP_OUT_Y, deep = op.flags & OP_OUT_YD;
+      panel_op(sm + op.pay, op.R, op.w, op.pad0, sm + op.in,
+               to_y ? (deep ? B.ydeep : B.y) + op.out : sm + op.out,
+               to_y ? (deep ? 0 : y_mode) : ((op.flags & OP_ACC) ? 1 : 0));
     }
     __syncthreads();
     if (t_staged && threadIdx.x == 0 && lv < 2) {  // trace: end of the first two levels

@@ -6,7 +6,7 @@ typ, arg, c, r, s, l0, l1, cd, d, sm = t.T
 t0 = c[c > 0].min()
 f = lambda v: np.where(v > 0, (v - t0) / 1e3, np.nan)
 c, r, s, l0, l1, cd, d = f(c), f(r), f(s), f(l0), f(l1), f(cd), f(d)
-names = {0: "near", 1: "span", 2: "couple"}
+names = {0: "near", 1: "span", 2: "couple", 3: "flatup", 4: "flatdn"}
 print(f"makespan {np.nanmax(d):.1f} us, tasks {len(t)}, CTAs {len(np.unique(sm >> 32))}")
 for ty in (0, 1, 2):
     m = typ == ty

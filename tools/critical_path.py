@@ -14,7 +14,7 @@ t = np.load(sys.argv[2])
 typ, arg, c, r, s, l0, l1, cd, d, sm = t.T.astype(np.float64)
 t0 = c[c > 0].min()
 us = lambda v: (v - t0) / 1e3
-names = {0: "near", 1: "span", 2: "couple"}
+names = {0: "near", 1: "span", 2: "couple", 3: "flatup", 4: "flatdn"}
 # walk back from the latest-finishing task through the dependency that finished last
 cur = int(np.nanargmax(np.where(d > 0, d, np.nan)))
 chain = []
