@@ -74,6 +74,8 @@ def config_desc(k, pk):
 def load(k):
     from paper_1703_01175_b200.pack import load_packed
     path = os.path.join(ROOT, "data", f"cfg{k}.npz")
+    if not os.path.exists(path):  # committed compact copy (near-field re-assembled on load)
+        path = os.path.join(ROOT, "fixtures", f"cfg{k}.npz")
     if not os.path.exists(path):
         return None, None
     return load_packed(path, with_extra=True)

@@ -135,6 +135,11 @@ class PackedH2:
         e = self.element_counts()
         return 16 * (e["E_V"] + e["E_T"] + e["E_S"] + e["E_D"]) + 32 * q * (self.n + e["K"])
 
+    def d_elems_expected(self):
+        """Near-field elements implied by the tables: sum n_t * n_s over inadmissible pairs."""
+        rows = np.repeat(np.arange(self.num_clusters), np.diff(self.d_row_ptr))
+        return int(np.sum(self.c_size[rows].astype(np.int64) * self.c_size[self.d_col].astype(np.int64)))
+
     def near_bytes(self, q=1):
         """Algorithmic bytes of the near-field phase alone: D once, x_s and y_t once."""
         return 16 * int(self.dbuf.size) + 32 * q * self.n
@@ -284,9 +289,15 @@ def validate(pk: PackedH2):
 # on-disk format: one uncompressed .npz (arrays) with a JSON header entry
 # ----------------------------------------------------------------------
 
-def save_packed(pk: PackedH2, path, extra=None):
-    arrays = {name: getattr(pk, name) for name in _INT_TABLES + _PAYLOADS}
+def save_packed(pk: PackedH2, path, extra=None, geometry=None):
+    """Write `pk` (+ extras).  With ``geometry`` (a `nearfield.geometry_arrays`
+    record) the near-field payload is NOT written: `load_packed` re-assembles it
+    from the geometry (nearfield.py), which keeps committed fixtures small."""
+    names = _INT_TABLES + (_PAYLOADS if geometry is None else _PAYLOADS[:3])
+    arrays = {name: getattr(pk, name) for name in names}
     head = dict(n=pk.n, depth=pk.depth, meta=pk.meta, version=FORMAT_VERSION)
+    if geometry is not None:
+        head["geometry"] = geometry
     arrays["__header__"] = np.frombuffer(json.dumps(head).encode(), dtype=np.uint8)
     for k, v in (extra or {}).items():
         arrays["extra__" + k] = np.asarray(v)
@@ -300,8 +311,17 @@ def load_packed(path, with_extra=False):
     head = json.loads(bytes(z["__header__"]).decode())
     if head.get("version") != FORMAT_VERSION:
         raise ValueError(f"{path}: unsupported packed-H2 format {head.get('version')}")
-    kw = {name: z[name] for name in _INT_TABLES + _PAYLOADS}
+    kw = {name: z[name] for name in _INT_TABLES + _PAYLOADS if name in z.files}
+    if "dbuf" not in kw:
+        if "geometry" not in head:
+            raise ValueError(f"{path}: no near-field payload and no geometry to rebuild it from")
+        kw["dbuf"] = np.zeros(0, np.complex128)
     pk = PackedH2(n=int(head["n"]), depth=int(head["depth"]), meta=head.get("meta", {}), **kw)
+    if "geometry" in head:
+        from .nearfield import assemble_near, geometry_arrays
+        pk.meta = dict(pk.meta, geometry=head["geometry"])
+        if pk.dbuf.size == 0 and pk.n_near:
+            pk.dbuf = assemble_near(pk, *geometry_arrays(head["geometry"]))
     if with_extra:
         extra = {k[len("extra__"):]: z[k] for k in z.files if k.startswith("extra__")}
         return pk, extra
