@@ -124,6 +124,8 @@ int h2b_prepare_handle(h2b_handle h);
 #define H2B_OPT_TRACE 3       /* 1: record a per-task timeline of the persistent kernel */
 #define H2B_OPT_DEBUG 4       /* profiling only, results are WRONG: bit 0 skips far-field task
                                  bodies, bit 1 near-field task bodies of the persistent kernel */
+#define H2B_OPT_MRHS 5        /* 1 (default): q >= 2 runs every phase as a grouped complex GEMM on
+                                 the FP64 tensor pipe (DMMA); 0: per-phase CUDA-core kernels */
 int h2b_set_option(h2b_handle h, int option, int value);
 
 /* Per-task timeline of the last persistent-kernel matvec (tracing on): for task i,
@@ -147,6 +149,7 @@ int h2b_get_trace(h2b_handle h, int64_t* out, int64_t max_tasks);
 #define H2B_Q_NEAR_SMEM 13    /* dynamic shared memory of the near-field stream kernel (bytes) */
 #define H2B_Q_MEGA_SMEM 14    /* dynamic shared memory of the far-field task-graph kernel (bytes) */
 #define H2B_Q_NEAR_VARIANT 15 /* 100 * leaf size + rows per thread of the near kernel (0: generic) */
+#define H2B_Q_MRHS_LAUNCHES 16 /* kernel launches of one multi-RHS (q >= 2) matvec */
 int h2b_query(h2b_handle h, int what, int64_t* out);
 
 /* Permutation helpers on device buffers: out[i,:] = in[perm[i],:] (gather,

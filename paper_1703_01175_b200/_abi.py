@@ -22,10 +22,11 @@ EXPORTED = (
     "h2b_zdotc_multi", "h2b_zgemv_sub", "h2b_zaxpby", "h2b_matvec_phase",
     "h2b_prepare_handle", "h2b_set_option", "h2b_query", "h2b_get_trace",
 )
-OPT_GRAPHS, OPT_MEGA, OPT_TRACE = 1, 2, 3
+OPT_GRAPHS, OPT_MEGA, OPT_TRACE, OPT_DEBUG, OPT_MRHS = 1, 2, 3, 4, 5
 Q_LAUNCHES_Q1, Q_SPAN_MODE, Q_SPLIT_LEVEL, Q_TOP_STAGED, Q_DEVICE_BYTES = 1, 2, 3, 4, 5
 Q_MEGA, Q_MEGA_TASKS, Q_MEGA_GRID, Q_MEGA_TIERS, Q_DEVICE_ERROR = 6, 7, 8, 9, 10
 Q_NEAR_TASKS, Q_NEAR_STAGES, Q_NEAR_SMEM, Q_MEGA_SMEM, Q_NEAR_VARIANT = 11, 12, 13, 14, 15
+Q_MRHS_LAUNCHES = 16
 
 _i32p = C.POINTER(C.c_int32)
 _i64p = C.POINTER(C.c_int64)

@@ -32,6 +32,7 @@ int upload_table(T** dst, const T* src, int64_t count, int64_t* acc) {
 
 void free_ctx(h2b_ctx* h) {
   h2b_release_graphs(h);
+  h2b_mrhs_free(h);
   void* ptrs[] = {h->c_start_d, h->c_size_d, h->c_rank_d, h->c_lo,      h->c_hi,
                   h->c_parent,  h->c_xoff_d, h->c_voff_d, h->c_toff_d,  h->s_row_ptr_d,
                   h->s_off_d,   h->d_row_ptr_d, h->d_off_d, h->s_col_d, h->d_col_d,
@@ -286,6 +287,11 @@ int h2b_set_option(h2b_handle h, int option, int value) {
     h2b_release_graphs(h);
     return H2B_OK;
   }
+  if (option == H2B_OPT_MRHS) {
+    h->use_mrhs = value ? 1 : 0;
+    h2b_release_graphs(h);
+    return H2B_OK;
+  }
   if (option == H2B_OPT_MEGA) {
     REQUIRE(!h->prepared, H2B_ESTATE, "h2b_set_option(H2B_OPT_MEGA): set before the first matvec");
     h->use_mega = value ? 1 : 0;
@@ -312,6 +318,7 @@ int h2b_query(h2b_handle h, int what, int64_t* out) {
     case H2B_Q_NEAR_SMEM: *out = h->near_smem; return H2B_OK;
     case H2B_Q_MEGA_SMEM: *out = h->mega_smem + 16 * h->mega_blob_slots; return H2B_OK;
     case H2B_Q_NEAR_VARIANT: *out = 100 * h->mega_ns + h->mega_r; return H2B_OK;
+    case H2B_Q_MRHS_LAUNCHES: *out = h2b_mrhs_launches(h); return H2B_OK;
     case H2B_Q_DEVICE_ERROR: {
       MegaCtrl c{};
       if (h->ctrl) H2B_CUDA_TRY(cudaMemcpy(&c, h->ctrl, sizeof(c), cudaMemcpyDeviceToHost));

@@ -204,6 +204,8 @@ struct GraphKey {
   bool operator<(const GraphKey& o) const { return std::tie(x, y, q) < std::tie(o.x, o.y, o.q); }
 };
 
+struct MrhsPlan;  // h2b_mrhs.cu
+
 struct h2b_ctx {
   int device = 0;
   int64_t n = 0;
@@ -301,6 +303,9 @@ struct h2b_ctx {
   size_t kry_bytes = 0;
   int64_t device_bytes = 0;
   int launches_q1 = 0;  // kernels per q=1 matvec (reported to the bench)
+  // multi-RHS (q >= 2) grouped complex GEMM plan on the FP64 tensor pipe (h2b_mrhs.cu)
+  MrhsPlan* mrhs = nullptr;
+  int use_mrhs = 1;
 };
 
 // implemented in h2b_matvec.cu
@@ -313,6 +318,11 @@ int h2b_launch_gather(const int64_t* perm, int64_t n, const double2* in, double2
 int h2b_launch_scatter(const int64_t* perm, int64_t n, const double2* in, double2* out, int q,
                        cudaStream_t st);
 void h2b_release_graphs(h2b_ctx* h);
+// implemented in h2b_mrhs.cu
+int h2b_mrhs_prepare(h2b_ctx* h);
+void h2b_mrhs_free(h2b_ctx* h);
+int h2b_mrhs_launches(const h2b_ctx* h);
+int h2b_launch_mrhs(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st, int* nl);
 
 // ---------------------------------------------------------------------------
 // Blackwell async bulk copy (TMA 1-D, cp.async.bulk) + mbarrier helpers

@@ -85,6 +85,8 @@ int enqueue_matvec(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream
     *nl = 1;
     return H2B_OK;
   }
+  if (q >= 2 && h->use_mrhs)  // all phases as grouped complex GEMMs on DMMA (h2b_mrhs.cu)
+    return h2b_launch_mrhs(h, xp, yp, q, st, nl);
   if (h->K == 0) {
     H2B_TRY(h2b_launch_near(h, xp, yp, q, st));
     ++*nl;
@@ -141,6 +143,7 @@ int h2b_ensure_workspace(h2b_ctx* h, int q) {
 int h2b_run_matvec(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st) {
   H2B_TRY(h2b_prepare(h));
   H2B_TRY(h2b_ensure_workspace(h, q));
+  if (q >= 2 && h->use_mrhs) H2B_TRY(h2b_mrhs_prepare(h));  // allocates: never inside a capture
   int nl = 0;
   if (!h->use_graphs) {
     H2B_TRY(enqueue_matvec(h, xp, yp, q, st, &nl));

@@ -28,7 +28,7 @@ for k in [int(a) for a in (sys.argv[1:] or ["1", "2"])]:
     err = np.max(np.abs(d - pk.dbuf)) / np.max(np.abs(pk.dbuf))
     print(f"cfg{k}: re-assembled near-field max rel deviation {err:.2e}")
     assert err < 1e-13
-    keep = {key: v for key, v in ex.items() if key not in ("ref_perm",)}
+    keep = dict(ex)
     out = os.path.join(ROOT, "fixtures", f"cfg{k}.npz")
     save_packed(pk, out, extra=keep, geometry=GEOM[k])
     print(f"  -> {out} {os.path.getsize(out) / 1e6:.1f} MB")
