@@ -200,6 +200,42 @@ int h2b_zgemv_sub(const void* V, int64_t ldv, int nv, const void* h_dev, void* w
 int h2b_zaxpby(int64_t n, double ar, double ai, const void* x, double br, double bi, void* y,
                void* stream);
 
+/* ---------------------------------------------------------------------
+ * Plan handles: a set of device payloads plus per-phase lists of grouped
+ * complex GEMM (q >= 2, FP64 tensor pipe) / GEMV (q = 1) work items, built by
+ * the host.  The subtree-partitioned multi-GPU matvec (SURVEY.md §8e,
+ * paper_1703_01175_b200/shard.py) runs one per rank: phase UP_OWN before the
+ * all-gather of x and x̂, the others after it.  Every vector is (rows, q)
+ * row-major complex128 on the device.
+ *   item: C[c_row + i, :] (+)= sum over its segments of A_seg[i, :] B_seg[:, :], i < m <= 64
+ *   seg:  A = payload[a_src][a_off + i*lda + j] (i < m, j < k <= 32),
+ *         B row j = (b_src buffer)[b_row + j]
+ * flags: seg  = a_src | b_src << 4 (b_src 0 x, 1 xhat, 2 yhat)
+ *        item = dst (0 x, 1 xhat, 2 yhat, 3 y) | 256 (accumulate)
+ * --------------------------------------------------------------------- */
+typedef struct h2b_mm_item {
+  int64_t c_row;
+  int32_t m, seg0, nseg, flags;
+  int64_t pad;
+} h2b_mm_item;
+typedef struct h2b_mm_seg {
+  int64_t a_off, b_row;
+  int32_t k, lda, flags, pad;
+} h2b_mm_seg;
+typedef struct h2b_plan_ctx* h2b_plan_handle;
+
+int h2b_plan_create(int device, int n_payloads, const int64_t* payload_elems, h2b_plan_handle* out);
+int h2b_plan_upload(h2b_plan_handle p, int payload, const void* src, size_t bytes, size_t offset);
+/* launch_items[i] = items of the i-th launch (launches run in order; items of one launch must
+ * write disjoint rows) */
+int h2b_plan_set_phase(h2b_plan_handle p, int phase, int n_launches, const int64_t* launch_items,
+                       const h2b_mm_item* items, int64_t n_items, const h2b_mm_seg* segs,
+                       int64_t n_segs);
+int h2b_plan_run(h2b_plan_handle p, int phase, const void* x, const void* xhat, void* yhat, void* y,
+                 int q, void* stream);
+int h2b_plan_destroy(h2b_plan_handle p);
+int64_t h2b_plan_device_bytes(h2b_plan_handle p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,6 +21,8 @@ EXPORTED = (
     "h2b_gather_perm", "h2b_scatter_perm", "h2b_gmres", "h2b_bicgstab",
     "h2b_zdotc_multi", "h2b_zgemv_sub", "h2b_zaxpby", "h2b_matvec_phase",
     "h2b_prepare_handle", "h2b_set_option", "h2b_query", "h2b_get_trace",
+    "h2b_plan_create", "h2b_plan_upload", "h2b_plan_set_phase", "h2b_plan_run",
+    "h2b_plan_destroy", "h2b_plan_device_bytes",
 )
 OPT_GRAPHS, OPT_MEGA, OPT_TRACE, OPT_DEBUG, OPT_MRHS = 1, 2, 3, 4, 5
 Q_LAUNCHES_Q1, Q_SPAN_MODE, Q_SPLIT_LEVEL, Q_TOP_STAGED, Q_DEVICE_BYTES = 1, 2, 3, 4, 5
@@ -49,6 +51,17 @@ class Layout(C.Structure):
 class Report(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("n_history", C.c_int32),
                 ("matvecs", C.c_int32), ("wall_time", C.c_double)]
+
+
+# plan handles (h2b_plan_*): numpy record layouts of h2b_mm_item / h2b_mm_seg
+import numpy as _np  # noqa: E402
+
+MM_ITEM = _np.dtype([("c_row", "<i8"), ("m", "<i4"), ("seg0", "<i4"), ("nseg", "<i4"),
+                     ("flags", "<i4"), ("pad", "<i8")])
+MM_SEG = _np.dtype([("a_off", "<i8"), ("b_row", "<i8"), ("k", "<i4"), ("lda", "<i4"),
+                    ("flags", "<i4"), ("pad", "<i4")])
+B_X, B_XHAT, B_YHAT, B_Y = 0, 1, 2, 3
+ITEM_ACC = 256
 
 
 class H2BError(RuntimeError):
@@ -96,6 +109,13 @@ def lib():
     L.h2b_query.argtypes = [vp, C.c_int, C.POINTER(C.c_int64)]
     L.h2b_get_trace.argtypes = [vp, C.POINTER(C.c_int64), C.c_int64]
     L.h2b_zaxpby.argtypes = [C.c_int64, C.c_double, C.c_double, vp, C.c_double, C.c_double, vp, vp]
+    L.h2b_plan_create.argtypes = [C.c_int, C.c_int, _i64p, C.POINTER(vp)]
+    L.h2b_plan_upload.argtypes = [vp, C.c_int, vp, C.c_size_t, C.c_size_t]
+    L.h2b_plan_set_phase.argtypes = [vp, C.c_int, C.c_int, _i64p, vp, C.c_int64, vp, C.c_int64]
+    L.h2b_plan_run.argtypes = [vp, C.c_int, vp, vp, vp, vp, C.c_int, vp]
+    L.h2b_plan_destroy.argtypes = [vp]
+    L.h2b_plan_device_bytes.argtypes = [vp]
+    L.h2b_plan_device_bytes.restype = C.c_int64
     _lib = L
     return L
 

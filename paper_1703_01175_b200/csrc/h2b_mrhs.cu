@@ -218,6 +218,71 @@ __global__ void __launch_bounds__(MM_THREADS, 1) k_zgemm_grouped(const MmItem* _
   }
 }
 
+// q = 1: the same item / segment lists as a grouped complex GEMV on the CUDA cores
+// (memory-bound).  Thread (row i, quarter g) accumulates 8 K-entries of each segment; the four
+// partial sums of a row are combined in a fixed order (deterministic).
+constexpr int MV_THREADS = 256;
+__global__ void __launch_bounds__(MV_THREADS) k_zgemv_grouped(const MmItem* __restrict__ items,
+                                                              const MmSeg* __restrict__ segs,
+                                                              MmBufs bf) {
+  __shared__ double2 red[4][MM_M];
+  const MmItem it = items[blockIdx.x];
+  double2 acc = make_double2(0.0, 0.0);
+  for (int sgi = 0; sgi < it.nseg; ++sgi) {
+    const MmSeg s = segs[it.seg0 + sgi];
+    const double2* A = pick_a(bf, s.flags & 15) + s.a_off;
+    const double2* B = pick_b(bf, (s.flags >> 4) & 15);
+    const bool gather = s.flags & SEG_GATHER;
+    int i, g;
+    if (s.flags & SEG_TRANS) { i = threadIdx.x & (MM_M - 1); g = threadIdx.x >> 6; }
+    else { i = threadIdx.x >> 2; g = threadIdx.x & 3; }
+    if (i < it.m) {
+      const int j0 = g * 8, j1 = min(s.k, j0 + 8);
+      double2 av[8], xv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + u;
+        if (j < j1) {
+          av[u] = (s.flags & SEG_TRANS) ? A[(int64_t)j * s.lda + i] : A[(int64_t)i * s.lda + j];
+          const int64_t row = gather ? (int64_t)__ldg(bf.gather + s.b_row + j) : s.b_row + j;
+          xv[u] = B[row];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j0 + u < j1) cfma(acc, av[u], xv[u]);
+    }
+  }
+  // all segments of an item share the A orientation (checked by h2b_plan_set_phase), so the
+  // thread's (row, quarter) is the same for every segment
+  int i, g;
+  if (it.nseg > 0 && (segs[it.seg0].flags & SEG_TRANS)) { i = threadIdx.x & (MM_M - 1); g = threadIdx.x >> 6; }
+  else { i = threadIdx.x >> 2; g = threadIdx.x & 3; }
+  red[g][i] = acc;
+  __syncthreads();
+  if (threadIdx.x < it.m) {
+    const int r = threadIdx.x;
+    const double2 v = cadd(cadd(red[0][r], red[1][r]), cadd(red[2][r], red[3][r]));
+    double2* o = pick_b(bf, it.flags & 15) + it.c_row + r;
+    *o = (it.flags & ITEM_ACC) ? cadd(*o, v) : v;
+  }
+}
+
+int run_grouped(const MmItem* items, int n_items, const MmSeg* segs, const MmBufs& bf, int q,
+                cudaStream_t st, int* nl) {
+  const int nct = (q + MM_N - 1) / MM_N;
+  for (int i0 = 0; i0 < n_items; i0 += 65535) {
+    const int cnt = std::min(65535, n_items - i0);
+    if (q == 1)
+      k_zgemv_grouped<<<cnt, MV_THREADS, 0, st>>>(items + i0, segs, bf);
+    else
+      k_zgemm_grouped<<<dim3(cnt, nct), MM_THREADS, MM_SMEM, st>>>(items + i0, segs, bf, q);
+    H2B_CHECK_LAUNCH();
+    ++*nl;
+  }
+  return H2B_OK;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -396,15 +461,163 @@ int h2b_launch_mrhs(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStrea
   bf.b[B_YHAT] = h->yhat;
   bf.y = yp;
   bf.gather = h->s_xcol;
-  const int nct = (q + MM_N - 1) / MM_N;
-  for (const int2& L : h->mrhs->launches) {
-    for (int i0 = 0; i0 < L.y; i0 += 65535) {  // grid.x limit is large, but keep launches bounded
-      const int cnt = std::min(65535, L.y - i0);
-      k_zgemm_grouped<<<dim3(cnt, nct), MM_THREADS, MM_SMEM, st>>>(h->mrhs->items + L.x + i0, h->mrhs->segs,
-                                                                  bf, q);
-      H2B_CHECK_LAUNCH();
-      ++*nl;
-    }
-  }
+  for (const int2& L : h->mrhs->launches)
+    H2B_TRY(run_grouped(h->mrhs->items + L.x, L.y, h->mrhs->segs, bf, q, st, nl));
   return H2B_OK;
 }
+
+// ---------------------------------------------------------------------------
+// generic plan handles (C-ABI h2b_plan_*): payloads + per-phase item/segment lists built by
+// the host (paper_1703_01175_b200/shard.py builds one per rank of a subtree partition)
+// ---------------------------------------------------------------------------
+static_assert(sizeof(MmItem) == sizeof(h2b_mm_item), "item layout");
+static_assert(sizeof(MmSeg) == sizeof(h2b_mm_seg), "segment layout");
+
+struct h2b_plan_ctx {
+  int device = 0;
+  int n_payloads = 0;
+  double2* pay[A_N] = {};
+  int64_t pay_elems[A_N] = {};
+  struct Phase {
+    std::vector<int2> launches;
+    MmItem* items = nullptr;
+    MmSeg* segs = nullptr;
+  };
+  std::vector<Phase> phases;
+  int64_t device_bytes = 0;
+};
+
+extern "C" int h2b_plan_create(int device, int n_payloads, const int64_t* payload_elems,
+                               h2b_plan_handle* out) {
+  if (!out || n_payloads < 0 || n_payloads > A_N || (n_payloads && !payload_elems)) {
+    h2b_set_error("h2b_plan_create: bad arguments (at most 6 payloads)");
+    return H2B_EINVAL;
+  }
+  if (!h2b_device_ok(device)) {
+    h2b_set_error("h2b_plan_create: no sm_100 device");
+    return H2B_ENODEV;
+  }
+  H2B_CUDA_TRY(cudaSetDevice(device));
+  auto* p = new h2b_plan_ctx();
+  p->device = device;
+  p->n_payloads = n_payloads;
+  for (int i = 0; i < n_payloads; ++i) {
+    p->pay_elems[i] = payload_elems[i];
+    cudaError_t e = cudaMalloc(&p->pay[i], 16 * (size_t)std::max<int64_t>(payload_elems[i], 1));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      for (int j = 0; j < i; ++j) cudaFree(p->pay[j]);
+      delete p;
+      h2b_set_error("h2b_plan_create: payload allocation failed");
+      return H2B_ENOMEM;
+    }
+    p->device_bytes += 16 * std::max<int64_t>(payload_elems[i], 1);
+  }
+  *out = p;
+  return H2B_OK;
+}
+
+extern "C" int h2b_plan_upload(h2b_plan_handle p, int payload, const void* src, size_t bytes, size_t offset) {
+  if (!p || payload < 0 || payload >= p->n_payloads || (!src && bytes) ||
+      offset + bytes > 16 * (size_t)p->pay_elems[payload]) {
+    h2b_set_error("h2b_plan_upload: bad arguments");
+    return H2B_EINVAL;
+  }
+  H2B_CUDA_TRY(cudaSetDevice(p->device));
+  if (bytes) H2B_CUDA_TRY(cudaMemcpy((char*)p->pay[payload] + offset, src, bytes, cudaMemcpyHostToDevice));
+  return H2B_OK;
+}
+
+extern "C" int h2b_plan_set_phase(h2b_plan_handle p, int phase, int n_launches, const int64_t* launch_items,
+                                  const h2b_mm_item* items, int64_t n_items, const h2b_mm_seg* segs,
+                                  int64_t n_segs) {
+  if (!p || phase < 0 || phase > 64 || n_launches < 0 || n_items < 0 || n_segs < 0) {
+    h2b_set_error("h2b_plan_set_phase: bad arguments");
+    return H2B_EINVAL;
+  }
+  int64_t tot = 0;
+  for (int i = 0; i < n_launches; ++i) tot += launch_items[i];
+  if (tot != n_items) {
+    h2b_set_error("h2b_plan_set_phase: launch item counts do not add up to n_items");
+    return H2B_EINVAL;
+  }
+  for (int64_t i = 0; i < n_items; ++i) {  // validate references (the kernel trusts them)
+    const h2b_mm_item& it = items[i];
+    if (it.m < 0 || it.m > MM_M || it.seg0 < 0 || it.nseg < 0 || it.seg0 + (int64_t)it.nseg > n_segs ||
+        (it.flags & 15) > B_N) {
+      h2b_set_error("h2b_plan_set_phase: item " + std::to_string(i) + " out of range");
+      return H2B_EINVAL;
+    }
+    for (int s = 1; s < it.nseg; ++s)
+      if ((segs[it.seg0 + s].flags ^ segs[it.seg0].flags) & SEG_TRANS) {
+        h2b_set_error("h2b_plan_set_phase: item " + std::to_string(i) + " mixes A orientations");
+        return H2B_EINVAL;
+      }
+  }
+  for (int64_t i = 0; i < n_segs; ++i) {
+    const h2b_mm_seg& sg = segs[i];
+    if (sg.k < 0 || sg.k > MM_K || (sg.flags & 15) >= p->n_payloads || ((sg.flags >> 4) & 15) >= B_N ||
+        (sg.flags & SEG_GATHER)) {
+      h2b_set_error("h2b_plan_set_phase: segment " + std::to_string(i) + " out of range");
+      return H2B_EINVAL;
+    }
+  }
+  H2B_CUDA_TRY(cudaSetDevice(p->device));
+  if ((int)p->phases.size() <= phase) p->phases.resize(phase + 1);
+  auto& ph = p->phases[phase];
+  cudaFree(ph.items);
+  cudaFree(ph.segs);
+  ph.items = nullptr;
+  ph.segs = nullptr;
+  ph.launches.clear();
+  H2B_CUDA_TRY(cudaMalloc(&ph.items, sizeof(MmItem) * std::max<int64_t>(n_items, 1)));
+  H2B_CUDA_TRY(cudaMalloc(&ph.segs, sizeof(MmSeg) * std::max<int64_t>(n_segs, 1)));
+  if (n_items) H2B_CUDA_TRY(cudaMemcpy(ph.items, items, sizeof(MmItem) * n_items, cudaMemcpyHostToDevice));
+  if (n_segs) H2B_CUDA_TRY(cudaMemcpy(ph.segs, segs, sizeof(MmSeg) * n_segs, cudaMemcpyHostToDevice));
+  int64_t first = 0;
+  for (int i = 0; i < n_launches; ++i) {
+    ph.launches.push_back(int2{(int)first, (int)launch_items[i]});
+    first += launch_items[i];
+  }
+  p->device_bytes += sizeof(MmItem) * n_items + sizeof(MmSeg) * n_segs;
+  return H2B_OK;
+}
+
+extern "C" int h2b_plan_run(h2b_plan_handle p, int phase, const void* x, const void* xhat, void* yhat,
+                            void* y, int q, void* stream) {
+  if (!p || phase < 0 || phase >= (int)p->phases.size() || q < 1) {
+    h2b_set_error("h2b_plan_run: bad arguments");
+    return H2B_EINVAL;
+  }
+  static bool attr = false;
+  if (!attr) {
+    H2B_CUDA_TRY(cudaFuncSetAttribute(k_zgemm_grouped, cudaFuncAttributeMaxDynamicSharedMemorySize, MM_SMEM));
+    attr = true;
+  }
+  MmBufs bf{};
+  for (int i = 0; i < A_N; ++i) bf.a[i] = p->pay[i];
+  bf.b[B_X] = const_cast<double2*>((const double2*)x);
+  bf.b[B_XHAT] = const_cast<double2*>((const double2*)xhat);
+  bf.b[B_YHAT] = (double2*)yhat;
+  bf.y = (double2*)y;
+  bf.gather = nullptr;
+  const auto& ph = p->phases[phase];
+  int nl = 0;
+  for (const int2& L : ph.launches)
+    H2B_TRY(run_grouped(ph.items + L.x, L.y, ph.segs, bf, q, (cudaStream_t)stream, &nl));
+  return H2B_OK;
+}
+
+extern "C" int h2b_plan_destroy(h2b_plan_handle p) {
+  if (!p) return H2B_OK;
+  cudaSetDevice(p->device);
+  for (auto& ph : p->phases) {
+    cudaFree(ph.items);
+    cudaFree(ph.segs);
+  }
+  for (int i = 0; i < p->n_payloads; ++i) cudaFree(p->pay[i]);
+  delete p;
+  return H2B_OK;
+}
+
+extern "C" int64_t h2b_plan_device_bytes(h2b_plan_handle p) { return p ? p->device_bytes : -1; }

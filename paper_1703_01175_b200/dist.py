@@ -1,0 +1,241 @@
+"""Multi-GPU H² matvec and GMRES: subtree partition + one all-gather per matvec.
+
+One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch).  Rank g
+holds the shard of `shard.plan_shard` (its subtree's bases, coupling rows and
+near-field rows) in a libh2b plan handle and the Krylov vectors' slice
+``[row0_g, row0_g + nrows_g)`` of the permuted index space.  Per matvec the
+only communication is ONE ``all_gather_into_tensor`` of the exchange buffer
+(each rank's x slice and its own x̂ values, SURVEY.md §8e (i)+(ii) fused into a
+single collective); per Arnoldi step of GMRES the dots and norms are
+``all_reduce`` sums of per-rank partials.
+
+The compute engine is pluggable so the host logic (partition, exchange
+layout, collectives, GMRES) is exercised unchanged by the CPU tests on gloo:
+`CudaPlanEngine` (the product: libh2b ``h2b_plan_run`` on the rank's GPU) or
+a test engine that interprets the same plan on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+
+import numpy as np
+
+from . import _abi
+from .krylov import SolveReport
+from .shard import (N_PAY, PH_COUPLE, PH_DOWN, PH_NEAR, PH_UP_OWN, PH_UP_TOP, PHASES, partition,
+                    plan_shard)
+
+_UPLOAD_CHUNK = 1 << 30
+
+
+class CudaPlanEngine:
+    """A shard plan resident on one B200 (libh2b plan handle)."""
+
+    def __init__(self, plan, device):
+        L = _abi.lib()
+        self.device = int(device)
+        elems = (C.c_int64 * N_PAY)(*[int(a.size) for a in plan.payloads])
+        h = C.c_void_p()
+        _abi.check(L.h2b_plan_create(self.device, N_PAY, elems, C.byref(h)), "h2b_plan_create")
+        self.handle = h
+        for i, a in enumerate(plan.payloads):
+            b = np.ascontiguousarray(a).view(np.uint8)
+            for off in range(0, b.size, _UPLOAD_CHUNK):
+                ch = b[off:off + _UPLOAD_CHUNK]
+                _abi.check(L.h2b_plan_upload(h, i, ch.ctypes.data, ch.size, off), "h2b_plan_upload")
+        for ph in PHASES:
+            counts, items, segs = plan.phases[ph]
+            _abi.check(L.h2b_plan_set_phase(h, ph, int(counts.size),
+                                            counts.ctypes.data_as(C.POINTER(C.c_int64)),
+                                            items.ctypes.data, int(items.size), segs.ctypes.data,
+                                            int(segs.size)), "h2b_plan_set_phase")
+
+    def run(self, phase, xbuf, yhat, y, q, stream=None):
+        torch = __import__("torch")
+        st = torch.cuda.current_stream(self.device) if stream is None else stream
+        _abi.check(_abi.lib().h2b_plan_run(self.handle, phase, C.c_void_p(xbuf.data_ptr()),
+                                           C.c_void_p(xbuf.data_ptr()), C.c_void_p(yhat.data_ptr()),
+                                           C.c_void_p(y.data_ptr()), int(q),
+                                           C.c_void_p(st.cuda_stream)), "h2b_plan_run")
+
+    def device_bytes(self):
+        return int(_abi.lib().h2b_plan_device_bytes(self.handle))
+
+    def close(self):
+        if self.handle:
+            _abi.lib().h2b_plan_destroy(self.handle)
+            self.handle = None
+
+
+class DistH2Operator:
+    """Rank-local view of the subtree-partitioned operator.
+
+    ``matvec_local(x_local)`` takes this rank's rows of x (permuted order,
+    (nrows,) or (nrows, q) complex128 torch tensor on the rank's device) and
+    returns its rows of y = S x.  Collective: every rank must call it.
+    """
+
+    def __init__(self, pk, group=None, device=None, engine=None, rank=None, world=None):
+        """``engine``: None (libh2b on ``device`` / the current CUDA device) or a factory
+        ``plan -> engine`` (the CPU tests pass the plan interpreter)."""
+        import torch
+        import torch.distributed as dist
+        self.group = group
+        if world is None:
+            world = dist.get_world_size(group) if dist.is_initialized() else 1
+        if rank is None:
+            rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.rank, self.world = int(rank), int(world)
+        self.part = partition(pk, self.world)
+        self.plan = plan_shard(pk, self.world, self.rank, self.part)
+        self.n = int(pk.n)
+        self.row0, self.nrows = self.plan.row0, self.plan.nrows
+        if engine is None:
+            dev = torch.cuda.current_device() if device is None else device
+            engine = CudaPlanEngine(self.plan, dev)
+            self.device = torch.device(f"cuda:{engine.device}")
+        else:
+            engine = engine(self.plan)
+            self.device = torch.device(getattr(engine, "device_name", "cpu"))
+        self.engine = engine
+        self._ws = {}
+
+    def _work(self, q):
+        import torch
+        if q not in self._ws:
+            z = lambda r: torch.zeros((r, q), dtype=torch.complex128, device=self.device)  # noqa: E731
+            self._ws[q] = (z(self.part.xlen), z(self.part.xlen), z(self.nrows),
+                           z(self.part.chunk))
+        return self._ws[q]
+
+    def exchange(self, xbuf, send, q):
+        """All-gather of every rank's chunk (x slice + own x̂) into the exchange buffer."""
+        import torch
+        import torch.distributed as dist
+        ch = self.part.chunk
+        g = self.rank
+        if self.world == 1:
+            return
+        send.copy_(xbuf[g * ch:(g + 1) * ch])
+        dist.all_gather_into_tensor(torch.view_as_real(xbuf[:self.world * ch]),
+                                    torch.view_as_real(send), group=self.group)
+
+    def matvec_local(self, x_local):
+        squeeze = x_local.dim() == 1
+        xl = x_local.reshape(self.nrows, -1)
+        q = xl.shape[1]
+        xbuf, yhat, y, send = self._work(q)
+        g, ch = self.rank, self.part.chunk
+        xbuf[g * ch:g * ch + self.nrows].copy_(xl)
+        self.engine.run(PH_UP_OWN, xbuf, yhat, y, q)
+        self.exchange(xbuf, send, q)
+        for ph in (PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR):
+            self.engine.run(ph, xbuf, yhat, y, q)
+        out = y.clone()
+        return out[:, 0] if squeeze else out
+
+    # ---- Krylov helper: global 2-norm over the row slices -------------------------
+    def norm(self, a):
+        import torch
+        import torch.distributed as dist
+        s = (a.real * a.real + a.imag * a.imag).sum().reshape(1)
+        if self.world > 1:
+            dist.all_reduce(s, group=self.group)
+        return float(torch.sqrt(s)[0])
+
+
+def _givens(a, b):
+    if b == 0.0:
+        return 1.0, 0.0 + 0.0j, a
+    if a == 0:
+        return 0.0, 1.0 + 0.0j, complex(b)
+    t = np.hypot(abs(a), b)
+    ph = a / abs(a)
+    return abs(a) / t, ph * b / t, ph * t
+
+
+def dist_gmres_solve(op: DistH2Operator, b_local, tol=1e-6, restart=30, max_iter=1000):
+    """Restarted GMRES(m), CGS2 Arnoldi, x0 = 0, on row-distributed vectors (collective).
+
+    Same recurrence and stopping rule as the single-GPU ``gmres_solve`` and the CPU
+    restatement (oracle/krylov_oracle.py::gmres_solve); the Arnoldi basis lives in
+    device memory as an (m+1, nrows) slice per rank; every inner product is a
+    per-rank partial summed by one all-reduce.
+    """
+    import torch
+    if not (0.0 < tol < 1.0):
+        raise ValueError("tol must be in (0, 1)")
+    if max_iter < 1 or restart < 1:
+        raise ValueError("max_iter and restart must be >= 1")
+    t0 = time.perf_counter()
+    b = b_local.to(op.device, torch.complex128)
+    bnrm = op.norm(b)
+    if bnrm == 0.0:
+        return torch.zeros_like(b), SolveReport(0, [], True, time.perf_counter() - t0)
+    m = int(restart)
+    x = torch.zeros_like(b)
+    r = b.clone()
+    V = torch.zeros((m + 1, op.nrows), dtype=torch.complex128, device=op.device)
+    it, history, converged = 0, [], False
+    while it < max_iter:
+        beta = op.norm(r)
+        H = np.zeros((m + 1, m), dtype=np.complex128)
+        cs = np.zeros(m)
+        sn = np.zeros(m, dtype=np.complex128)
+        g = np.zeros(m + 1, dtype=np.complex128)
+        g[0] = beta
+        V[0] = r / beta
+        j_done = 0
+        for j in range(m):
+            w = op.matvec_local(V[j])
+            it += 1
+            Vj = V[:j + 1]
+            h = _multi_dot(op, Vj, w)                                      # CGS pass 1
+            w = w - (h.unsqueeze(1) * Vj).sum(0)
+            h2 = _multi_dot(op, Vj, w)                                     # CGS pass 2
+            w = w - (h2.unsqueeze(1) * Vj).sum(0)
+            hh = (h + h2).cpu().numpy()
+            hn = op.norm(w)
+            for i in range(j):
+                a_, bb = hh[i], hh[i + 1]
+                hh[i] = cs[i] * a_ + sn[i] * bb
+                hh[i + 1] = -np.conj(sn[i]) * a_ + cs[i] * bb
+            c, s, rr = _givens(hh[j], hn)
+            cs[j], sn[j] = c, s
+            H[:j + 1, j] = hh[:j + 1]
+            H[j, j] = rr
+            g[j + 1] = -np.conj(s) * g[j]
+            g[j] = c * g[j]
+            res = abs(g[j + 1]) / bnrm
+            history.append(float(res))
+            j_done = j + 1
+            if res <= tol:
+                break
+            if it >= max_iter or hn == 0.0:
+                break
+            V[j + 1] = w / hn
+        y = np.zeros(j_done, dtype=np.complex128)
+        for i in range(j_done - 1, -1, -1):
+            y[i] = (g[i] - H[i, i + 1:j_done] @ y[i + 1:j_done]) / H[i, i]
+        yt = torch.from_numpy(y).to(op.device)
+        x = x + (yt.unsqueeze(1) * V[:j_done]).sum(0)
+        r = b - op.matvec_local(x)
+        true_res = op.norm(r) / bnrm
+        if true_res <= tol:
+            converged = True
+            break
+    return x, SolveReport(it, history, converged, time.perf_counter() - t0)
+
+
+def _multi_dot(op, Vj, w):
+    """h_i = Σ conj(V_i) w over all ranks, one all-reduce for all i."""
+    import torch
+    import torch.distributed as dist
+    h = (Vj.conj() * w.unsqueeze(0)).sum(1)
+    if op.world > 1:
+        r = torch.view_as_real(h).clone()
+        dist.all_reduce(r, group=op.group)
+        h = torch.view_as_complex(r)
+    return h

@@ -1,0 +1,276 @@
+"""Subtree partition of the H² operator across G ranks (one process per GPU).
+
+SURVEY.md §8(e): for G = 2^p ranks, rank g owns the level-p cluster
+``tree.levels[p][g]`` — a contiguous slice of the permuted index space
+(clustering.py:87 splits at ``start + (n+1)//2``, so slices differ by at
+most one point) — and everything below it: the leaf bases and transfers of
+its subtree, the coupling rows S^{t,s} of its targets t, the near-field rows
+D_{t,s} of its leaves.  Levels above p ("top") are tiny (the 3-D configs have
+k = 0 there) and are computed redundantly by every rank.
+
+One matvec on rank g (reference phases, arith.py:52-104):
+
+1. ``UP_OWN``   x̂ of its own clusters from its x slice           (arith.py:58-71)
+2. all-gather of the *exchange buffer* — per rank one chunk holding its x slice
+   followed by its x̂ values, padded to a common length so a single
+   ``all_gather_into_tensor`` lands every chunk in place (rank-major)
+3. ``UP_TOP``   x̂ of the top levels from the gathered level-p values
+4. ``COUPLE``   ŷ_t = Σ_s S^{t,s} x̂_s for t own or top            (arith.py:72-81)
+5. ``DOWN``     ŷ pushed down through the transfers into own clusters (arith.py:82-97)
+6. ``NEAR``     y_t = Σ_s D_{t,s} x_s + V_t ŷ_t for its own leaves  (arith.py:98-104)
+
+The plan is data: per phase a list of launches, each a list of work items
+(≤ 64 output rows) built from segments (an A block of ≤ 32 columns from one of
+six payloads times ≤ 32 rows of a vector buffer).  libh2b executes it
+(``h2b_plan_*``: grouped complex GEMM on the FP64 tensor pipe for q ≥ 2,
+grouped GEMV for q = 1); the CPU tests execute the same plan with a numpy
+interpreter to check the partition and exchange logic on gloo.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+MM_M, MM_K = 64, 32
+PH_UP_OWN, PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR = 0, 1, 2, 3, 4
+PHASES = (PH_UP_OWN, PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR)
+PAY_VT, PAY_TT, PAY_T, PAY_S, PAY_D, PAY_V = 0, 1, 2, 3, 4, 5
+N_PAY = 6
+B_X, B_XHAT, B_YHAT, B_Y = 0, 1, 2, 3
+ITEM_ACC = 256
+
+
+@dataclass
+class Partition:
+    """Row/skeleton ownership and the exchange-buffer layout shared by all ranks."""
+
+    G: int
+    p: int                  # partition level, G = 2**p
+    roots: np.ndarray       # [G] packed index of each rank's level-p cluster
+    row0: np.ndarray        # [G] first permuted row of each rank
+    nrows: np.ndarray       # [G] rows of each rank
+    owner: np.ndarray       # [P] owning rank of each cluster (-1: top level, computed by all)
+    hat: np.ndarray         # [P] exchange-buffer row of x̂_c / ŷ_c (-1 when k_c = 0)
+    chunk: int              # rows per rank chunk: nmax (x slice) + kmax (own x̂)
+    nmax: int
+    xlen: int               # G * chunk + Σ k over top clusters
+
+    def xrow(self, i):
+        """Exchange-buffer row of permuted point i."""
+        g = int(np.searchsorted(self.row0, i, side="right") - 1)
+        return g * self.chunk + (i - int(self.row0[g]))
+
+
+def partition(pk, G: int) -> Partition:
+    if G < 1 or (G & (G - 1)):
+        raise ValueError("the subtree partition needs a power-of-two number of ranks")
+    p = G.bit_length() - 1
+    P = pk.num_clusters
+    lev = pk.c_level
+    min_leaf = int(lev[pk.c_child_lo < 0].min())
+    if p > min_leaf or int(pk.level_ptr[p + 1] - pk.level_ptr[p]) != G:
+        raise ValueError(f"{G} ranks need {G} clusters on level {p} above every leaf")
+    roots = np.arange(pk.level_ptr[p], pk.level_ptr[p + 1], dtype=np.int64)
+    owner = np.full(P, -1, dtype=np.int64)
+    owner[roots] = np.arange(G)
+    for lvl in range(p + 1, pk.depth):  # parents precede children level by level
+        for c in range(pk.level_ptr[lvl], pk.level_ptr[lvl + 1]):
+            owner[c] = owner[pk.c_parent[c]]
+    row0 = pk.c_start[roots].astype(np.int64)
+    nrows = pk.c_size[roots].astype(np.int64)
+    kown = np.zeros(G, dtype=np.int64)
+    local = np.full(P, -1, dtype=np.int64)
+    for c in range(P):  # level-major order inside each rank
+        if owner[c] >= 0 and pk.c_rank[c] > 0:
+            local[c] = kown[owner[c]]
+            kown[owner[c]] += pk.c_rank[c]
+    nmax = int(nrows.max())
+    chunk = nmax + int(kown.max())
+    hat = np.full(P, -1, dtype=np.int64)
+    own = local >= 0
+    hat[own] = owner[own] * chunk + nmax + local[own]
+    t = G * chunk
+    for c in range(P):
+        if owner[c] < 0 and pk.c_rank[c] > 0:
+            hat[c] = t
+            t += int(pk.c_rank[c])
+    return Partition(G=G, p=p, roots=roots, row0=row0, nrows=nrows, owner=owner, hat=hat,
+                     chunk=chunk, nmax=nmax, xlen=t)
+
+
+@dataclass
+class ShardPlan:
+    rank: int
+    part: Partition
+    payloads: list                          # N_PAY complex128 arrays
+    phases: dict = field(default_factory=dict)  # phase -> (launch_counts, items, segs)
+
+    @property
+    def row0(self):
+        return int(self.part.row0[self.rank])
+
+    @property
+    def nrows(self):
+        return int(self.part.nrows[self.rank])
+
+    def payload_bytes(self):
+        return int(sum(a.nbytes for a in self.payloads))
+
+
+class _Builder:
+    def __init__(self):
+        from ._abi import MM_ITEM, MM_SEG
+        self._it, self._sg = MM_ITEM, MM_SEG
+        self.items, self.segs, self.counts = [], [], []
+        self._first = 0
+
+    def seg(self, a_src, a_off, lda, m0, k, b_src, b_row):
+        for k0 in range(0, k, MM_K):
+            self.segs.append((a_off + m0 * lda + k0, b_row + k0, min(MM_K, k - k0), lda,
+                              a_src | (b_src << 4), 0))
+
+    def begin(self):
+        return len(self.segs)
+
+    def end(self, s0, c_row, m, dst, acc=False):
+        self.items.append((c_row, m, s0, len(self.segs) - s0, dst | (ITEM_ACC if acc else 0), 0))
+
+    def launch(self):
+        n = len(self.items) - self._first
+        if n:
+            self.counts.append(n)
+        self._first = len(self.items)
+
+    def done(self):
+        self.launch()
+        return (np.asarray(self.counts, dtype=np.int64),
+                np.array(self.items, dtype=self._it), np.array(self.segs, dtype=self._sg))
+
+
+def plan_shard(pk, G: int, g: int, part: Partition | None = None) -> ShardPlan:
+    """Payloads and work lists of rank g of G (see the module docstring)."""
+    part = part or partition(pk, G)
+    if not 0 <= g < G:
+        raise ValueError("rank out of range")
+    own = part.owner == g
+    top = part.owner < 0
+    mine = own | top
+    k = pk.c_rank.astype(np.int64)
+    lo_of, hi_of = pk.c_child_lo, pk.c_child_hi
+    hat = part.hat
+    pays = [[] for _ in range(N_PAY)]
+    size = [0] * N_PAY
+
+    def put(which, mat):
+        off = size[which]
+        pays[which].append(np.ascontiguousarray(mat, dtype=np.complex128).ravel())
+        size[which] += mat.size
+        return off
+
+    def xrow_leaf(c):
+        o = int(part.owner[c])
+        return o * part.chunk + int(pk.c_start[c]) - int(part.row0[o])
+
+    def V(c):
+        n, kc = int(pk.c_size[c]), int(k[c])
+        return pk.vbuf[pk.c_v_off[c]:pk.c_v_off[c] + n * kc].reshape(n, kc)
+
+    def T(c):
+        m = int(k[lo_of[c]] + k[hi_of[c]])
+        return pk.tbuf[pk.c_t_off[c]:pk.c_t_off[c] + m * k[c]].reshape(m, int(k[c]))
+
+    def up(Bd, levels, sel):
+        for lvl in levels:
+            for c in range(pk.level_ptr[lvl], pk.level_ptr[lvl + 1]):
+                if not sel[c] or k[c] == 0:
+                    continue
+                kc = int(k[c])
+                if lo_of[c] < 0:
+                    n = int(pk.c_size[c])
+                    off = put(PAY_VT, V(c).T)
+                    for m0 in range(0, kc, MM_M):
+                        s0 = Bd.begin()
+                        Bd.seg(PAY_VT, off, n, m0, n, B_X, xrow_leaf(c))
+                        Bd.end(s0, hat[c] + m0, min(MM_M, kc - m0), B_XHAT)
+                else:
+                    lo, hi = int(lo_of[c]), int(hi_of[c])
+                    klo, khi = int(k[lo]), int(k[hi])
+                    off = put(PAY_TT, T(c).T) if klo + khi else 0
+                    for m0 in range(0, kc, MM_M):
+                        s0 = Bd.begin()
+                        if klo:
+                            Bd.seg(PAY_TT, off, klo + khi, m0, klo, B_XHAT, hat[lo])
+                        if khi:
+                            Bd.seg(PAY_TT, off + klo, klo + khi, m0, khi, B_XHAT, hat[hi])
+                        Bd.end(s0, hat[c] + m0, min(MM_M, kc - m0), B_XHAT)
+            Bd.launch()
+
+    phases = {}
+    Bd = _Builder()
+    up(Bd, range(pk.depth - 1, part.p - 1, -1), own)
+    phases[PH_UP_OWN] = Bd.done()
+    Bd = _Builder()
+    up(Bd, range(part.p - 1, -1, -1), top)
+    phases[PH_UP_TOP] = Bd.done()
+
+    Bd = _Builder()  # coupling: every own/top target with k > 0 (zero when it has no block)
+    for t in np.nonzero(mine & (k > 0))[0]:
+        kt = int(k[t])
+        blocks = []
+        for b in range(pk.s_row_ptr[t], pk.s_row_ptr[t + 1]):
+            s = int(pk.s_col[b])
+            if k[s] == 0:
+                continue
+            S = pk.sbuf[pk.s_off[b]:pk.s_off[b] + kt * k[s]].reshape(kt, int(k[s]))
+            blocks.append((put(PAY_S, S), s))
+        for m0 in range(0, kt, MM_M):
+            s0 = Bd.begin()
+            for off, s in blocks:
+                Bd.seg(PAY_S, off, int(k[s]), m0, int(k[s]), B_XHAT, hat[s])
+            Bd.end(s0, hat[t] + m0, min(MM_M, kt - m0), B_YHAT)
+    phases[PH_COUPLE] = Bd.done()
+
+    Bd = _Builder()  # downward, root first: [ŷ_lo; ŷ_hi] += [T_lo; T_hi] ŷ_c
+    for lvl in range(pk.depth - 1):
+        for c in range(pk.level_ptr[lvl], pk.level_ptr[lvl + 1]):
+            if not mine[c] or k[c] == 0 or lo_of[c] < 0:
+                continue
+            lo, hi = int(lo_of[c]), int(hi_of[c])
+            klo, khi, kc = int(k[lo]), int(k[hi]), int(k[c])
+            if klo + khi == 0 or not (mine[lo] or mine[hi]):
+                continue
+            off = put(PAY_T, T(c))
+            for ch, r0, kch in ((lo, 0, klo), (hi, klo, khi)):
+                if not mine[ch] or kch == 0:
+                    continue
+                for m0 in range(0, kch, MM_M):
+                    s0 = Bd.begin()
+                    Bd.seg(PAY_T, off + r0 * kc, kc, m0, kc, B_YHAT, hat[c])
+                    Bd.end(s0, hat[ch] + m0, min(MM_M, kch - m0), B_YHAT, acc=True)
+        Bd.launch()
+    phases[PH_DOWN] = Bd.done()
+
+    Bd = _Builder()  # near-field + leaf back-transform of own leaves -> local y rows
+    r0 = int(part.row0[g])
+    for t in np.nonzero(own & (lo_of < 0))[0]:
+        nt = int(pk.c_size[t])
+        blocks = []
+        for b in range(pk.d_row_ptr[t], pk.d_row_ptr[t + 1]):
+            s = int(pk.d_col[b])
+            ns = int(pk.c_size[s])
+            D = pk.dbuf[pk.d_off[b]:pk.d_off[b] + nt * ns].reshape(nt, ns)
+            blocks.append((put(PAY_D, D), s, ns))
+        voff = put(PAY_V, V(t)) if k[t] > 0 else -1
+        for m0 in range(0, nt, MM_M):
+            s0 = Bd.begin()
+            for off, s, ns in blocks:
+                Bd.seg(PAY_D, off, ns, m0, ns, B_X, xrow_leaf(s))
+            if voff >= 0:
+                Bd.seg(PAY_V, voff, int(k[t]), m0, int(k[t]), B_YHAT, hat[t])
+            Bd.end(s0, int(pk.c_start[t]) - r0 + m0, min(MM_M, nt - m0), B_Y)
+    phases[PH_NEAR] = Bd.done()
+
+    payloads = [np.concatenate(a) if a else np.zeros(0, np.complex128) for a in pays]
+    return ShardPlan(rank=g, part=part, payloads=payloads, phases=phases)

@@ -1,0 +1,88 @@
+"""Shard plans of the subtree partition executed by libh2b (h2b_plan_*) on one B200.
+
+The ranks of a G-way partition run one after another on cuda:0 and the all-gather is a
+device copy (no kernel waits on another rank's kernel), so the per-rank device programs are
+checked for G = 1..8 exactly as each GPU would run them; the multi-process collectives are
+covered on CPU/gloo by tests/test_dist.py."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN_NAMES, load_config, load_golden, rel
+
+pytestmark = pytest.mark.gpu
+
+
+def _ranks(pk):
+    from paper_1703_01175_b200.shard import partition
+    out = []
+    for G in (1, 2, 4, 8):
+        try:
+            partition(pk, G)
+            out.append(G)
+        except ValueError:
+            break
+    return out
+
+
+def _run_sharded(pk, G, X):
+    from paper_1703_01175_b200.dist import CudaPlanEngine
+    from paper_1703_01175_b200.shard import (PH_COUPLE, PH_DOWN, PH_NEAR, PH_UP_OWN, PH_UP_TOP,
+                                             partition, plan_shard)
+    part = partition(pk, G)
+    q = X.shape[1]
+    dev = torch.device("cuda:0")
+    Xd = torch.from_numpy(X).to(dev)
+    plans = [plan_shard(pk, G, g, part) for g in range(G)]
+    eng = [CudaPlanEngine(p, 0) for p in plans]
+    ch = part.chunk
+    bufs = []
+    for g, p in enumerate(plans):
+        xb = torch.zeros((part.xlen, q), dtype=torch.complex128, device=dev)
+        xb[g * ch:g * ch + p.nrows] = Xd[p.row0:p.row0 + p.nrows]
+        b = (xb, torch.zeros_like(xb), torch.zeros((p.nrows, q), dtype=torch.complex128, device=dev))
+        eng[g].run(PH_UP_OWN, *b, q)
+        bufs.append(b)
+    gathered = torch.cat([b[0][g * ch:(g + 1) * ch] for g, b in enumerate(bufs)])
+    Y = torch.empty_like(Xd)
+    for g, p in enumerate(plans):
+        bufs[g][0][:G * ch] = gathered
+        for ph in (PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR):
+            eng[g].run(ph, *bufs[g], q)
+        Y[p.row0:p.row0 + p.nrows] = bufs[g][2]
+    torch.cuda.synchronize()
+    for e in eng:
+        e.close()
+    return Y.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", GOLDEN_NAMES)
+@pytest.mark.parametrize("q", [1, 5, 64])
+def test_shard_plans_on_device_match_oracle(name, q):
+    from oracle import h2_oracle as ho
+    pk, _ = load_golden(name)
+    X = np.random.default_rng(q).standard_normal((pk.n, q)) * (1 + 0.5j)
+    ref = ho.matvec_perm(pk, X)
+    for G in _ranks(pk):
+        assert rel(_run_sharded(pk, G, X), ref) <= 1e-12, G
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_shard_plans_on_device_baseline_configs(k):
+    pk, ex = load_config(k)
+    xp = ex["x"][pk.perm][:, :1]
+    yp = ex["y"][pk.perm][:, :1]
+    for G in (1, 2, 4, 8):
+        assert rel(_run_sharded(pk, G, xp), yp) <= 1e-10, G
+
+
+def test_dist_operator_single_rank_gmres():
+    """DistH2Operator without a process group (world 1) on cuda:0: matvec and GMRES."""
+    from paper_1703_01175_b200.dist import DistH2Operator, dist_gmres_solve
+    pk, ex = load_config(1)
+    op = DistH2Operator(pk, device=0, rank=0, world=1)
+    xp = torch.from_numpy(ex["x"][pk.perm, 0].copy()).cuda()
+    assert rel(op.matvec_local(xp).cpu().numpy(), ex["y"][pk.perm, 0]) <= 1e-10
+    _, rep = dist_gmres_solve(op, xp, tol=1e-6, restart=30, max_iter=2000)
+    assert rep.converged and abs(rep.iterations - int(ex["gmres_iters"])) <= 1
