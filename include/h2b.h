@@ -94,6 +94,13 @@ int h2b_create(const h2b_layout* layout, int device, h2b_handle* out);
  * (chunked uploads allowed).  All four sections must be covered before use. */
 int h2b_upload(h2b_handle h, int sec, const void* src, size_t bytes, size_t offset);
 int h2b_destroy(h2b_handle h);
+/* Fill the near-field section on the device from the voxel geometry instead of uploading it
+ * (SURVEY.md §8f row f3): restates the reference block sampler assemble_block_raw
+ * (_kernel_core.pyx:13-47) for every inadmissible pair.  centers: N x 3 doubles, chi: N
+ * complex (interleaved), both HOST arrays in the ORIGINAL point order; diag = k0^2 *
+ * self_term(volume, k0) (kernel.py:170-187).  H2B_EINVAL on coincident centres. */
+int h2b_assemble_near(h2b_handle h, const double* centers, const double* chi, double k0,
+                      double volume, double diag_re, double diag_im);
 /* Device bytes held by the handle (payloads + tables + workspace). */
 int64_t h2b_device_bytes(h2b_handle h);
 

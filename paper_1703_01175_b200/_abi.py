@@ -22,7 +22,7 @@ EXPORTED = (
     "h2b_zdotc_multi", "h2b_zgemv_sub", "h2b_zaxpby", "h2b_matvec_phase",
     "h2b_prepare_handle", "h2b_set_option", "h2b_query", "h2b_get_trace",
     "h2b_plan_create", "h2b_plan_upload", "h2b_plan_set_phase", "h2b_plan_run",
-    "h2b_plan_destroy", "h2b_plan_device_bytes",
+    "h2b_plan_destroy", "h2b_plan_device_bytes", "h2b_assemble_near",
 )
 OPT_GRAPHS, OPT_MEGA, OPT_TRACE, OPT_DEBUG, OPT_MRHS = 1, 2, 3, 4, 5
 Q_LAUNCHES_Q1, Q_SPAN_MODE, Q_SPLIT_LEVEL, Q_TOP_STAGED, Q_DEVICE_BYTES = 1, 2, 3, 4, 5
@@ -109,6 +109,7 @@ def lib():
     L.h2b_query.argtypes = [vp, C.c_int, C.POINTER(C.c_int64)]
     L.h2b_get_trace.argtypes = [vp, C.POINTER(C.c_int64), C.c_int64]
     L.h2b_zaxpby.argtypes = [C.c_int64, C.c_double, C.c_double, vp, C.c_double, C.c_double, vp, vp]
+    L.h2b_assemble_near.argtypes = [vp, vp, vp, C.c_double, C.c_double, C.c_double, C.c_double]
     L.h2b_plan_create.argtypes = [C.c_int, C.c_int, _i64p, C.POINTER(vp)]
     L.h2b_plan_upload.argtypes = [vp, C.c_int, vp, C.c_size_t, C.c_size_t]
     L.h2b_plan_set_phase.argtypes = [vp, C.c_int, C.c_int, _i64p, vp, C.c_int64, vp, C.c_int64]

@@ -81,11 +81,23 @@ class H2Operator:
         lay.n_coupling = pk.n_coupling
         lay.n_near = pk.n_near
         lay.v_elems, lay.t_elems = int(pk.vbuf.size), int(pk.tbuf.size)
-        lay.s_elems, lay.d_elems = int(pk.sbuf.size), int(pk.dbuf.size)
+        near_on_device = pk.dbuf.size == 0 and pk.n_near > 0
+        if near_on_device and "geometry" not in pk.meta:
+            raise ValueError("operator has no near-field payload and no geometry to assemble it from")
+        lay.s_elems, lay.d_elems = int(pk.sbuf.size), int(pk.d_elems_expected())
         handle = C.c_void_p()
         _abi.check(L.h2b_create(C.byref(lay), self.device, C.byref(handle)), "h2b_create")
         self._h = handle
         self._finalizer = weakref.finalize(self, L.h2b_destroy, handle)
+        if near_on_device:  # near-field sampled in HBM, never uploaded
+            from .nearfield import geometry_arrays, self_term
+            centers, chi, k0, vol = geometry_arrays(pk.meta["geometry"])
+            diag = k0 ** 2 * self_term(vol, k0)
+            centers = np.ascontiguousarray(centers, dtype=np.float64)
+            chi = np.ascontiguousarray(chi, dtype=np.complex128)
+            _abi.check(L.h2b_assemble_near(handle, centers.ctypes.data, chi.ctypes.data, float(k0),
+                                           float(vol), float(diag.real), float(diag.imag)),
+                       "h2b_assemble_near")
         for sec, buf in ((_abi.SEC_V, pk.vbuf), (_abi.SEC_T, pk.tbuf), (_abi.SEC_S, pk.sbuf),
                          (_abi.SEC_D, pk.dbuf)):
             b = np.ascontiguousarray(buf, dtype=np.complex128).view(np.uint8)

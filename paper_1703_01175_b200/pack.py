@@ -122,13 +122,13 @@ class PackedH2:
     def element_counts(self):
         """E_V, E_T, E_S, E_D and K of SURVEY.md §8(d)."""
         return dict(E_V=int(self.vbuf.size), E_T=int(self.tbuf.size),
-                    E_S=int(self.sbuf.size), E_D=int(self.dbuf.size),
+                    E_S=int(self.sbuf.size), E_D=self.d_elems_expected(),
                     K=self.total_rank)
 
     def storage_bytes(self):
         """Same total as H2Matrix.storage_bytes() (build.py:176-187)."""
         return int(self.perm.nbytes + 16 * (self.vbuf.size + self.tbuf.size
-                                            + self.sbuf.size + self.dbuf.size))
+                                            + self.sbuf.size + self.d_elems_expected()))
 
     def algorithmic_bytes(self, q=1):
         """B_alg(q) = 16(E_V+E_T+E_S+E_D) + 32 q (N + K)."""
@@ -142,7 +142,7 @@ class PackedH2:
 
     def near_bytes(self, q=1):
         """Algorithmic bytes of the near-field phase alone: D once, x_s and y_t once."""
-        return 16 * int(self.dbuf.size) + 32 * q * self.n
+        return 16 * self.d_elems_expected() + 32 * q * self.n
 
     def flops(self, q=1):
         """F(q) = 8 q (2E_V + 2E_T + E_S + E_D)."""
@@ -306,21 +306,67 @@ def save_packed(pk: PackedH2, path, extra=None, geometry=None):
     os.replace(tmp, path)
 
 
-def load_packed(path, with_extra=False):
+def save_structure(pk: PackedH2, path, geometry, seed=0, note=""):
+    """Write only the index tables + geometry of `pk` (a *structure-exact* operator file).
+
+    `load_packed` fills the far-field payloads (V, T, S) with seeded random values of exactly
+    the reference shapes and re-assembles the near-field from the geometry: same bytes, flops
+    and block structure as the reference-built operator, for throughput measurements of
+    operators too large to ship ("configs 3-5 without a reference build")."""
+    arrays = {name: getattr(pk, name) for name in _INT_TABLES}
+    head = dict(n=pk.n, depth=pk.depth, meta=pk.meta, version=FORMAT_VERSION, geometry=geometry,
+                synthetic=dict(seed=int(seed), note=note))
+    arrays["__header__"] = np.frombuffer(json.dumps(head).encode(), dtype=np.uint8)
+    tmp = str(path) + ".tmp.npz"
+    np.savez(tmp, **arrays)
+    os.replace(tmp, path)
+
+
+def _synthetic_far_field(kw, spec):
+    """Seeded far-field payloads with the shapes implied by the tables (see save_structure)."""
+    rng = np.random.default_rng(int(spec.get("seed", 0)))
+    rank, size, lo, hi = kw["c_rank"].astype(np.int64), kw["c_size"].astype(np.int64), \
+        kw["c_child_lo"], kw["c_child_hi"]
+    leaf = lo < 0
+    ev = int(np.sum(size[leaf] * rank[leaf]))
+    nl = ~leaf
+    et = int(np.sum((rank[lo[nl]] + rank[hi[nl]]) * rank[nl]))
+    P = rank.size
+    rows = np.repeat(np.arange(P), np.diff(kw["s_row_ptr"]))
+    es = int(np.sum(rank[rows] * rank[kw["s_col"]]))
+
+    def cplx(n, scale):
+        out = np.empty(n, dtype=np.complex128)
+        f = out.view(np.float64)
+        rng.standard_normal(out=f)
+        f *= scale
+        return out
+
+    return dict(vbuf=cplx(ev, 0.125), tbuf=cplx(et, 0.125), sbuf=cplx(es, 0.01))
+
+
+def load_packed(path, with_extra=False, near_on_host=True):
+    """Read a packed operator.  A compact file (no near-field payload, a geometry record) gets
+    its near-field re-assembled on the host (nearfield.py) — or, with ``near_on_host=False``,
+    left empty (``dbuf.size == 0``) for `H2Operator` to generate on the device."""
     z = np.load(path, allow_pickle=False)
     head = json.loads(bytes(z["__header__"]).decode())
     if head.get("version") != FORMAT_VERSION:
         raise ValueError(f"{path}: unsupported packed-H2 format {head.get('version')}")
     kw = {name: z[name] for name in _INT_TABLES + _PAYLOADS if name in z.files}
+    if "synthetic" in head:
+        kw.update(_synthetic_far_field(kw, head["synthetic"]))
     if "dbuf" not in kw:
         if "geometry" not in head:
             raise ValueError(f"{path}: no near-field payload and no geometry to rebuild it from")
         kw["dbuf"] = np.zeros(0, np.complex128)
     pk = PackedH2(n=int(head["n"]), depth=int(head["depth"]), meta=head.get("meta", {}), **kw)
+    if "synthetic" in head:
+        pk.meta = dict(pk.meta, synthetic=head["synthetic"])
     if "geometry" in head:
         from .nearfield import assemble_near, geometry_arrays
         pk.meta = dict(pk.meta, geometry=head["geometry"])
-        if pk.dbuf.size == 0 and pk.n_near:
+        if pk.dbuf.size == 0 and pk.n_near and near_on_host:
             pk.dbuf = assemble_near(pk, *geometry_arrays(head["geometry"]))
     if with_extra:
         extra = {k[len("extra__"):]: z[k] for k in z.files if k.startswith("extra__")}

@@ -34,10 +34,11 @@ def load_golden(name):
 def load_config(k):
     """(PackedH2, extras) for BASELINE config k: data/cfg<k>.npz (full, built by
     tools/make_golden.py) or the committed compact fixtures/cfg<k>.npz; skip if neither."""
-    path = os.path.join(DATA, f"cfg{k}.npz")
-    if not os.path.exists(path):
-        path = os.path.join(ROOT, "fixtures", f"cfg{k}.npz")
-    if not os.path.exists(path):
+    for path in (os.path.join(DATA, f"cfg{k}.npz"), os.path.join(DATA, f"cfg{k}_compact.npz"),
+                 os.path.join(ROOT, "fixtures", f"cfg{k}.npz")):
+        if os.path.exists(path):
+            break
+    else:
         pytest.skip(f"cfg{k} operator not present (generate with tools/make_golden.py --configs {k})")
     key = f"cfg{k}"
     if key not in _cache:

@@ -22,13 +22,21 @@ GEOM = {
     3: dict(kind="lattice", dims=[512, 512, 1], h=1.0 / 16, eps_r=4.0, k0=2 * np.pi),
 }
 
-for k in [int(a) for a in (sys.argv[1:] or ["1", "2"])]:
-    pk, ex = load_packed(os.path.join(ROOT, "data", f"cfg{k}.npz"), with_extra=True)
-    d = assemble_near(pk, *geometry_arrays(GEOM[k]))
-    err = np.max(np.abs(d - pk.dbuf)) / np.max(np.abs(pk.dbuf))
-    print(f"cfg{k}: re-assembled near-field max rel deviation {err:.2e}")
-    assert err < 1e-13
-    keep = dict(ex)
-    out = os.path.join(ROOT, "fixtures", f"cfg{k}.npz")
-    save_packed(pk, out, extra=keep, geometry=GEOM[k])
-    print(f"  -> {out} {os.path.getsize(out) / 1e6:.1f} MB")
+def main():
+    for k in [int(a) for a in (sys.argv[1:] or ["1", "2"])]:
+        pk, ex = load_packed(os.path.join(ROOT, "data", f"cfg{k}.npz"), with_extra=True)
+        d = assemble_near(pk, *geometry_arrays(GEOM[k]))
+        err = np.max(np.abs(d - pk.dbuf)) / np.max(np.abs(pk.dbuf))
+        print(f"cfg{k}: re-assembled near-field max rel deviation {err:.2e}")
+        assert err < 1e-13
+        keep = dict(ex)
+        # cfg3 (1.7 GB without its near-field) is too large to commit or ship:
+        # data/cfg3_compact.npz stays local; fixtures/cfg3_structure.npz travels
+        out = (os.path.join(ROOT, "fixtures", f"cfg{k}.npz") if k < 3
+               else os.path.join(ROOT, "data", f"cfg{k}_compact.npz"))
+        save_packed(pk, out, extra=keep, geometry=GEOM[k])
+        print(f"  -> {out} {os.path.getsize(out) / 1e6:.1f} MB")
+
+
+if __name__ == "__main__":
+    main()
