@@ -80,9 +80,9 @@ int launch_far_tail(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStrea
 
 int enqueue_matvec(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st, int* nl) {
   *nl = 0;
-  if (q == 1 && h->mega) {  // the whole matvec is one persistent launch
+  if (q == 1 && h->mega) {  // far-field task graph || near-field stream: two concurrent launches
     H2B_TRY(h2b_launch_mega(h, xp, yp, st));
-    *nl = 1;
+    *nl = (h->mega_grid > 0 ? 1 : 0) + (h->n_near_tasks > 0 ? 1 : 0);
     return H2B_OK;
   }
   if (q >= 2 && h->use_mrhs)  // all phases as grouped complex GEMMs on DMMA (h2b_mrhs.cu)
