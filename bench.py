@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="budget of the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gmres", action="store_true")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="use the subtree-partitioned path even on one GPU (always on for N > 1)")
     return ap.parse_args()
 
 
@@ -225,6 +227,98 @@ def run_reference(a):
     return 0
 
 
+def run_partitioned(a, pk, ex, rank, world, local):
+    """N GPUs, one process each: the operator is partitioned by subtree (SURVEY.md §8e,
+    paper_1703_01175_b200/dist.py) — each rank owns a contiguous slice of rows and the
+    matching bases / coupling rows / near-field rows; one NCCL all-gather of x and x̂ per
+    matvec.  Total work is fixed (the whole operator), so scaling is "strong"."""
+    import torch
+    import torch.distributed as dist
+    from paper_1703_01175_b200.dist import DistH2Operator
+    from paper_1703_01175_b200.shard import PHASES
+    from paper_1703_01175_b200.timing import L2Flusher
+    dev = torch.device(f"cuda:{local}")
+    op = DistH2Operator(pk, device=local, rank=rank, world=world)
+    sl = slice(op.row0, op.row0 + op.nrows)
+    xp_full = ex["x"][pk.perm, 0]
+    xl = torch.from_numpy(xp_full[sl].copy()).to(dev)
+    stream = torch.cuda.current_stream(dev)
+    flush = L2Flusher(dev)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(3, a.warmup)):
+        op.matvec_local(xl)
+    barrier()
+    with ClockSampler(local) as clk:
+        time.sleep(0.25)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(a.steps)]
+        for s, e in ev:
+            flush.flush()
+            if world > 1:
+                dist.barrier()  # all ranks start the step together (the all-gather couples them)
+            s.record(stream)
+            y = op.matvec_local(xl)
+            e.record(stream)
+        barrier()
+    ms = sum(s.elapsed_time(e) for s, e in ev) / a.steps
+    # end to end: pinned host slice in, host slice out, every step
+    xh = torch.from_numpy(xp_full[sl].copy()).pin_memory()
+    t_e2e = []
+    for _ in range(a.steps):
+        barrier()
+        t0 = time.perf_counter()
+        yh = op.matvec_local(xh.to(dev, non_blocking=True)).cpu()
+        t_e2e.append(time.perf_counter() - t0)
+    e2e_s = float(np.mean(t_e2e))
+    t = torch.tensor([ms, e2e_s], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, e2e_s = float(t[0]), float(t[1])
+    # parity: gather every rank's rows on rank 0
+    yl = y.cpu().numpy()
+    parts = [None] * world
+    if world > 1:
+        dist.all_gather_object(parts, (op.row0, yl))
+    else:
+        parts = [(op.row0, yl)]
+    launches = sum(int(op.plan.phases[ph][0].size) for ph in PHASES)
+    if rank == 0:
+        yp = np.concatenate([p[1] for p in sorted(parts, key=lambda p: p[0])])
+        relerr = (float(np.linalg.norm(yp - ex["y"][pk.perm, 0]) / np.linalg.norm(ex["y"][:, 0]))
+                  if "y" in ex else None)
+        peak, peak_src = peaks()
+        alg = pk.algorithmic_bytes(1)
+        line = {
+            "metric": METRIC, "value": pk.n / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "complex128 (f64)",
+            "data": "synthetic: reference-built operator of BASELINE config, N(0,1) RHS (seed 0)",
+            "config": dict(config_desc(a.config, pk), parallelism=f"subtree partition x{world} "
+                           "(level-log2(N) clusters), one NCCL all-gather of x and x-hat per matvec",
+                           l2="flushed before every timed step"),
+            "roofline": {"bound": "hbm", "kernel": "whole partitioned matvec step (grouped GEMV "
+                         "plan kernels per rank, max over ranks)", "achieved": alg / (ms * 1e-3) / 1e9,
+                         "peak": peak * world, "unit": "GB/s",
+                         "frac": alg / (ms * 1e-3) / 1e9 / (peak * world), "traffic": None,
+                         "peak_source": peak_src + f" x {world} GPUs"},
+            "e2e": {"value": pk.n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * pk.n,
+                    "d2h_bytes_per_step": 16 * pk.n, "ms_per_call": e2e_s * 1e3},
+            "gpu_launches": launches * a.steps, "gpu_launches_per_step": launches,
+            "clocks": clk.summary(), "parity_relerr_vs_reference": relerr,
+            "exchange_bytes_per_step": 16 * op.part.chunk * world,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     a = parse()
     if a.impl == "reference":
@@ -245,6 +339,8 @@ def main():
         if rank == 0:
             print(json.dumps({"metric": METRIC, "error": f"data/cfg{a.config}.npz missing"}))
         return 1
+    if world > 1 or a.partitioned:
+        return run_partitioned(a, pk, ex, rank, world, local)
     op = H2Operator(pk, device=local)
     L = _abi.lib()
     _abi.check(L.h2b_prepare_handle(op.handle), "prepare")
