@@ -5,7 +5,7 @@ with numpy, with exactly the semantics of the device kernels behind
 ``h2b_plan_run`` (h2b_mrhs.cu: k_zgemm_grouped / k_zgemv_grouped):
 
     item: C[c_row + i, :] (+)= Σ_seg A_seg[i, :k] @ B_seg[b_row : b_row + k, :],  i < m
-    A_seg[i, j] = payload[a_src][a_off + i*lda + j]
+    A_seg[i, j] = payload[a_src][a_off + i*lda + j]   (transposed segments: a_off + j*lda + i)
 
 It lets the CPU tests (gloo, world_size 2) run the distributed operator's
 host logic — partition, exchange-buffer layout, all-gather, GMRES
@@ -34,7 +34,10 @@ class NumpyPlanEngine:
             for sg in segs[it["seg0"]:it["seg0"] + it["nseg"]]:
                 k, lda, off = int(sg["k"]), int(sg["lda"]), int(sg["a_off"])
                 a_src, b_src = int(sg["flags"]) & 15, (int(sg["flags"]) >> 4) & 15
-                idx = off + np.arange(m)[:, None] * lda + np.arange(k)[None, :]
+                if int(sg["flags"]) & 256:   # SEG_TRANS: A[i, j] = payload[a_off + j*lda + i]
+                    idx = off + np.arange(m)[:, None] + np.arange(k)[None, :] * lda
+                else:
+                    idx = off + np.arange(m)[:, None] * lda + np.arange(k)[None, :]
                 A = pays[a_src][idx]
                 Bm = bufs[b_src][int(sg["b_row"]):int(sg["b_row"]) + k]
                 acc += A @ Bm

@@ -32,11 +32,14 @@
 
 namespace {
 
-constexpr int MM_THREADS = 256;  // 8 warps: 4 (rows of C_r) x 2 (columns)
+constexpr int MM_WARPS = 16;                  // MMA warps (4 per SM sub-partition)
+constexpr int MM_THREADS = 32 * (MM_WARPS + 1);  // + one producer warp (TMA issue, pad zeroing)
+constexpr int MM_TPW = 128 / MM_WARPS;  // max 8x8 tiles per warp (8 q-tiles x 16 n-tiles / warps)
 constexpr int MM_M = 64;         // complex rows per item
 constexpr int MM_N = 64;         // complex columns per tile
 constexpr int MM_K = 32;         // complex K per stage
 constexpr int MM_AST = 34;       // A row stride (complex): 68 doubles -> conflict-free fragments
+constexpr int MM_TST = 68;       // transposed-A row stride: 32 rows x 68 = the same 2176 elements
 constexpr int MM_STAGES = 3;
 constexpr int MM_A_ELEMS = MM_M * MM_AST;
 constexpr int MM_B_ELEMS = MM_K * MM_N;
@@ -85,12 +88,9 @@ __device__ __forceinline__ double2* pick_b(const MmBufs& bf, int id) {
   return id == B_N ? bf.y : p;
 }
 
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+__device__ __forceinline__ void mm_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -98,37 +98,85 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// stage one K-chunk (segment) into shared memory: A -> [MM_M][MM_AST], B -> [MM_K][MM_N]
-__device__ __forceinline__ void stage_seg(const MmSeg& s, const MmBufs& bf, int m, int q, int col0,
-                                          double2* st) {
-  const uint32_t sa = smem_u32(st), sb = smem_u32(st + MM_A_ELEMS);
-  const double2* A = pick_a(bf, s.flags & 15);
+// Staging of one K-chunk (segment) with TMA bulk copies (cp.async.bulk, one copy per
+// contiguous row, completion counted on the stage's mbarrier): a handful of large requests per
+// stage instead of thousands of 16-byte ones, so a single CTA per SM keeps enough bytes in flight.
+//   A row-major (non-trans): smem [i][j] stride MM_AST, row i = k elements of source row i
+//   A transposed (SEG_TRANS): smem [j][i] stride MM_TST, row j = m elements of source row j
+//   B: smem [r][c] stride MM_N, row r = qv elements of x / x̂ / ŷ row (contiguous or gathered)
+// Shapes are not multiples of the MMA tiles, so the few pad elements the MMA reads (rows m..m4,
+// column / row k when k is odd, columns qv..q8) are zeroed by the consumer after the copies land
+// (they are disjoint from the copied bytes).
+__device__ __forceinline__ void issue_seg(const MmSeg& s, const MmBufs& bf, int m, int q, int col0, int qv,
+                                          double2* st, uint64_t* bar) {
+  const int lane = threadIdx.x & 31;
+  const double2* A = pick_a(bf, s.flags & 15) + s.a_off;
   const double2* B = pick_b(bf, (s.flags >> 4) & 15);
   const bool trans = s.flags & SEG_TRANS;
-  // A: 64 x 32 complex
-#pragma unroll
-  for (int u = 0; u < (MM_M * MM_K) / MM_THREADS; ++u) {
-    const int e = threadIdx.x + u * MM_THREADS;
-    int i, j;
-    if (trans) { i = e & (MM_M - 1); j = e >> 6; }  // consecutive threads: consecutive i (coalesced)
-    else { j = e & (MM_K - 1); i = e >> 5; }
-    const bool ok = i < m && j < s.k;
-    const double2* src = A + s.a_off + (trans ? (int64_t)j * s.lda + i : (int64_t)i * s.lda + j);
-    cp_async16(sa + 16 * (i * MM_AST + j), ok ? src : A, ok ? 16 : 0);
-  }
-  // B: 32 rows x 64 columns
-#pragma unroll
-  for (int u = 0; u < (MM_K * MM_N) / MM_THREADS; ++u) {
-    const int e = threadIdx.x + u * MM_THREADS;
-    const int c = e & (MM_N - 1), r = e >> 6;
-    const bool ok = r < s.k && col0 + c < q;
-    int64_t row = 0;
-    if (ok) row = (s.flags & SEG_GATHER) ? (int64_t)__ldg(bf.gather + s.b_row + r) : s.b_row + r;
-    const double2* src = B + row * q + col0 + c;
-    cp_async16(sb + 16 * (r * MM_N + c), ok ? src : B, ok ? 16 : 0);
+  const int na = trans ? s.k : m;          // A rows to copy
+  const int la = trans ? m : s.k;          // elements per A row
+  if (lane == 0) mbar_arrive_expect_tx(bar, 16u * (uint32_t)(na * la + s.k * qv));
+  __syncwarp();
+  double2* As = st;
+  double2* Bs = st + MM_A_ELEMS;
+  for (int r = lane; r < na; r += 32)
+    bulk_g2s(As + r * (trans ? MM_TST : MM_AST), A + (int64_t)r * s.lda, 16u * la, bar);
+  for (int r = lane; r < s.k; r += 32) {
+    const int64_t row = (s.flags & SEG_GATHER) ? (int64_t)__ldg(bf.gather + s.b_row + r) : s.b_row + r;
+    bulk_g2s(Bs + r * MM_N, B + row * q + col0, 16u * qv, bar);
   }
 }
 
+__device__ __forceinline__ void zero_pads(const MmSeg& s, int m, int qv, double2* st, int lane) {
+  const double2 z = make_double2(0.0, 0.0);
+  const bool trans = s.flags & SEG_TRANS;
+  const int m4 = (m + 3) & ~3, k = s.k, k2 = (k + 1) & ~1, q8 = (qv + 7) & ~7;
+  double2* As = st;
+  double2* Bs = st + MM_A_ELEMS;
+  // A: rows (non-trans) / columns (trans) m..m4 for every j < k2; j = k (odd k) for i < m
+  for (int e = lane; e < (m4 - m) * k2; e += 32) {
+    const int i = m + e / k2, j = e % k2;
+    As[trans ? j * MM_TST + i : i * MM_AST + j] = z;
+  }
+  if (k & 1)
+    for (int i = lane; i < m; i += 32) As[trans ? k * MM_TST + i : i * MM_AST + k] = z;
+  // B: columns qv..q8 of rows < k2; row k (odd k) for columns < qv
+  for (int e = lane; e < (q8 - qv) * k2; e += 32) {
+    const int r = e / (q8 - qv), c = qv + e % (q8 - qv);
+    Bs[r * MM_N + c] = z;
+  }
+  if (k & 1)
+    for (int c = lane; c < qv; c += 32) Bs[k * MM_N + c] = z;
+}
+
+// One staged chunk: nks k4-steps of NU 8x8 tiles per warp (A fragment: B_rᵀ, shared by the NU
+// tiles; B fragments: A_rᵀ, with the lane's re/im pick and sign bit folded into the address/XOR).
+template <int NU>
+__device__ __forceinline__ void mma_chunk(double (&acc)[MM_TPW][2], const double* Bs, const double* bq,
+                                          int a_off, int si, int sj, int nks, int jo, int G,
+                                          unsigned long long neg) {
+#pragma unroll 2
+  for (int ks = 0; ks < nks; ++ks) {
+    const int j = ks * 2 + jo;
+    const double af = Bs[j * (2 * MM_N) + a_off];
+    const double* bp = bq + j * sj;
+    double bv[NU];
+#pragma unroll
+    for (int u = 0; u < NU; ++u)
+      bv[u] = __longlong_as_double(__double_as_longlong(bp[u * G * 4 * si]) ^ neg);
+#pragma unroll
+    for (int u = 0; u < NU; ++u) dmma(acc[u][0], acc[u][1], af, bv[u]);
+  }
+}
+
+// The MMA runs on the TRANSPOSED real product, C_rᵀ (q x 2m) = B_rᵀ (q x 2k) A_rᵀ (2k x 2m):
+// its M dimension is the column tile (64 of the q right-hand sides, always full at q >= 64) and
+// its N dimension is 2m in steps of 8, so an item with m rows costs ceil(m/4) n-tiles instead of
+// a full 64-row tile (ranks k_t ~ 12-84 at cfg3: the coupling/transfer phases would otherwise
+// waste ~40 % of the tensor work on padding).  Tiles (8 q-rows x 8 real columns) are dealt to
+// the 8 warps so every SM sub-partition gets the same share: warp w owns q-tile mt = w % MTP
+// and the n-tiles nt = w / MTP + G u (MTP = q-tiles rounded up to a power of two, G = 8 / MTP).
+// Each lane's accumulator pair is then (re, im) of one complex output element.
 __global__ void __launch_bounds__(MM_THREADS, 1) k_zgemm_grouped(const MmItem* __restrict__ items,
                                                                  const MmSeg* __restrict__ segs,
                                                                  MmBufs bf, int q) {
@@ -136,86 +184,100 @@ __global__ void __launch_bounds__(MM_THREADS, 1) k_zgemm_grouped(const MmItem* _
   const MmItem it = items[blockIdx.x];
   const int col0 = blockIdx.y * MM_N;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = warp & 3, wn = warp >> 2;
+  const int qv = min(MM_N, q - col0);          // valid columns of this tile
+  const int MT = (qv + 7) >> 3;                // q-tiles of 8
+  const int MTP = MT <= 1 ? 1 : MT <= 2 ? 2 : MT <= 4 ? 4 : 8;
+  const int G = MM_WARPS / MTP;
+  const int mt = warp % MTP, ng = warp / MTP;
+  const int NT = (2 * it.m + 7) >> 3;          // real n-tiles of 8 (<= 16)
+  const bool active = mt < MT;
+  const int nu = NT > ng ? (NT - ng + G - 1) / G : 0;  // n-tiles of this warp
   // lane-constant fragment geometry
-  const int fr = lane >> 2, kk = lane & 3;
-  const int b = kk & 1, jo = kk >> 1;
-  // A fragment of m-tile mt: C_r row R = wm*32 + mt*8 + fr -> complex row i = R>>1, part a = R&1
-  const int a = fr & 1;
-  const int a_pick = a ^ b;                                           // 0: re, 1: im
-  const unsigned long long a_neg = (a == 0 && b == 1) ? 0x8000000000000000ull : 0ull;  // -im
-  int a_base[4];
-#pragma unroll
-  for (int mt = 0; mt < 4; ++mt) a_base[mt] = (((wm * 32 + mt * 8 + fr) >> 1) * MM_AST) * 2 + a_pick;
-  int b_base[4];
-#pragma unroll
-  for (int nt = 0; nt < 4; ++nt) b_base[nt] = (wn * 32 + nt * 8 + fr) * 2 + b;
+  const int kk = lane & 3, b = kk & 1, jo = kk >> 1;
+  // A operand (B_rᵀ, m8 x k4 row): row c = mt*8 + lane/4, col kr -> complex row j, part b
+  const int a_off = (mt * 8 + (lane >> 2)) * 2 + b;
+  // B operand (A_rᵀ, k4 x n8 col): col n = nt*8 + lane/4 -> complex row i = nt*4 + lane/8, part
+  // a = (lane/4)&1; value {re, -im; im, re}[a][b] of A[i][j]
+  const int a = (lane >> 2) & 1;
+  const int pick = a ^ b;
+  const unsigned long long neg = (a == 0 && b == 1) ? 0x8000000000000000ull : 0ull;
 
-  double acc[4][4][2];
+  double acc[MM_TPW][2];
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  for (int u = 0; u < MM_TPW; ++u) acc[u][0] = acc[u][1] = 0.0;
 
-  const int ns = it.nseg;
-  // prologue: stages 0 .. MM_STAGES-2
-#pragma unroll
-  for (int s = 0; s < MM_STAGES - 1; ++s) {
-    if (s < ns) stage_seg(segs[it.seg0 + s], bf, it.m, q, col0, sm + s * MM_STAGE_ELEMS);
-    cp_commit();
-  }
-  for (int s = 0; s < ns; ++s) {
-    cp_wait<MM_STAGES - 2>();
-    __syncthreads();  // stage s visible to all; stage s-1 no longer read by anyone
-    {
-      const int sn = s + MM_STAGES - 1;
-      if (sn < ns) stage_seg(segs[it.seg0 + sn], bf, it.m, q, col0, sm + (sn % MM_STAGES) * MM_STAGE_ELEMS);
-      cp_commit();
+  __shared__ __align__(8) uint64_t full[MM_STAGES], empty[MM_STAGES];
+  if (threadIdx.x == 0)
+    for (int i = 0; i < MM_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], MM_WARPS);
     }
-    const double* As = reinterpret_cast<const double*>(sm + (s % MM_STAGES) * MM_STAGE_ELEMS);
-    const double* Bs = As + 2 * MM_A_ELEMS;
-#pragma unroll 4
-    for (int ks = 0; ks < (2 * MM_K) / 4; ++ks) {
-      const int j = ks * 2 + jo;  // complex K index of this lane
-      double af[4], bfr[4];
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
-        af[mt] = __longlong_as_double(__double_as_longlong(As[a_base[mt] + 2 * j]) ^ a_neg);
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) bfr[nt] = Bs[j * (2 * MM_N) + b_base[nt]];
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bfr[nt]);
-    }
-  }
-  cp_wait<0>();
   __syncthreads();
-  // epilogue: C_r fragments -> complex tile in shared memory -> global (coalesced)
-  double* Cs = reinterpret_cast<double*>(sm);
+  const int ns = it.nseg;
+  if (warp == MM_WARPS) {
+    // producer: wait until the buffer's previous chunk is consumed, zero its pads, copy
+    for (int s = 0; s < ns; ++s) {
+      const int buf = s % MM_STAGES;
+      if (s >= MM_STAGES) mbar_wait(&empty[buf], (uint32_t)(s / MM_STAGES - 1) & 1u);
+      const MmSeg sg = segs[it.seg0 + s];
+      double2* st = sm + buf * MM_STAGE_ELEMS;
+      zero_pads(sg, it.m, qv, st, lane);
+      __syncwarp();
+      // order the generic-proxy pad stores (this chunk's and the buffer's earlier ones) before
+      // the async-proxy TMA writes into the same buffer
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_seg(sg, bf, it.m, q, col0, qv, st, &full[buf]);  // lane 0 arrives (release) first
+    }
+  } else {
+    for (int s = 0; s < ns; ++s) {
+      const int buf = s % MM_STAGES;
+      const int kc = segs[it.seg0 + s].k;
+      const bool tr = segs[it.seg0 + s].flags & SEG_TRANS;
+      mbar_wait(&full[buf], (uint32_t)(s / MM_STAGES) & 1u);
+      if (active) {
+        const double* As = reinterpret_cast<const double*>(sm + buf * MM_STAGE_ELEMS);
+        const double* Bs = As + 2 * MM_A_ELEMS;
+        const int nks = (2 * kc + 3) >> 2;         // k4 steps holding data (the rest is padding)
+        // B-operand offsets: row-major A[i][j] -> i*AST + j, transposed -> j*TST + i (x2 doubles)
+        const int si = tr ? 2 : 2 * MM_AST;
+        const int sj = tr ? 2 * MM_TST : 2;
+        const double* bq = As + (lane >> 3) * si + pick + ng * 4 * si;
+        switch (nu) {  // compile-time tile counts: no predicated-off DMMA, no early exits
+#define MMC(NU) case NU: mma_chunk<NU>(acc, Bs, bq, a_off, si, sj, nks, jo, G, neg); break;
+          MMC(1) MMC(2) MMC(3) MMC(4) MMC(5) MMC(6) MMC(7) MMC(8)
+#undef MMC
+          default: break;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mm_arrive(&empty[buf]);
+    }
+  }
+  __syncthreads();
+  // epilogue: lane holds C_rᵀ[c][n..n+1] = (re, im) of C[i][c], i = nt*4 + lane%4
+  double2* Cs = sm;
+  if (active) {
+    const int c = mt * 8 + (lane >> 2);
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt) {
-    const int R = wm * 32 + mt * 8 + fr;
-    const int i = R >> 1, part = R & 1;
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
-      const int c = wn * 32 + nt * 8 + 2 * kk;
-      Cs[(i * MM_N + c) * 2 + part] = acc[mt][nt][0];
-      Cs[(i * MM_N + c + 1) * 2 + part] = acc[mt][nt][1];
+    for (int u = 0; u < MM_TPW; ++u) {
+      if (u >= nu) break;
+      Cs[((ng + G * u) * 4 + kk) * MM_N + c] = make_double2(acc[u][0], acc[u][1]);
     }
   }
   __syncthreads();
   const int dst_id = it.flags & 15;
   double2* C = pick_b(bf, dst_id);
   const bool accum = it.flags & ITEM_ACC;
-  const double2* Ct = reinterpret_cast<const double2*>(sm);
   for (int e = threadIdx.x; e < it.m * MM_N; e += MM_THREADS) {
     const int i = e >> 6, c = e & (MM_N - 1);
-    if (col0 + c >= q) continue;
+    if (c >= qv) continue;
     double2* o = C + (it.c_row + i) * q + col0 + c;
-    const double2 v = Ct[i * MM_N + c];
+    const double2 v = Cs[i * MM_N + c];
     *o = accum ? cadd(*o, v) : v;
   }
+  // the next CTA on this SM fills the same shared memory with TMA: order this CTA's generic
+  // stores (epilogue tile, pads) before any async-proxy write
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // q = 1: the same item / segment lists as a grouped complex GEMV on the CUDA cores
