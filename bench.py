@@ -197,6 +197,57 @@ def gmres_bench(rank, world, local):
     return out
 
 
+def mrhs_bench(rank, local, q=64):
+    """Multi-RHS leg (BASELINE cfg5 style, 64 right-hand sides) on the real cfg1 operator:
+    the matvec on the FP64 tensor pipe (h2b_mrhs.cu) timed with CUDA events, and a block
+    GMRES(30) solve to 1e-6 of 64 seeded N(0,1) right-hand sides (host in, host out)."""
+    if rank != 0:
+        return None
+    pk, ex = load(1)
+    if pk is None:
+        return None
+    import ctypes as C
+    import torch
+    from paper_1703_01175_b200 import H2Operator, _abi, block_gmres_solve
+    op = H2Operator(pk, device=local)
+    L = _abi.lib()
+    rng = np.random.default_rng(64)
+    B = rng.standard_normal((pk.n, q)) + 1j * rng.standard_normal((pk.n, q))
+    dev = torch.device(f"cuda:{local}")
+    xd = torch.from_numpy(B[pk.perm]).to(dev)
+    yd = torch.empty_like(xd)
+    st = torch.cuda.current_stream(dev)
+
+    def mv():
+        _abi.check(L.h2b_matvec_perm(op.handle, C.c_void_p(xd.data_ptr()), C.c_void_p(yd.data_ptr()), q,
+                                     C.c_void_p(st.cuda_stream)))
+    for _ in range(3):
+        mv()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(20):
+        mv()
+    e1.record(st)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / 20
+    nl = C.c_int64()
+    _abi.check(L.h2b_query(op.handle, _abi.Q_MRHS_LAUNCHES, C.byref(nl)))
+    block_gmres_solve(op, B, tol=1e-6, restart=30, max_iter=2)  # warm-up (cuSOLVER/cuBLAS handles)
+    X, rep = block_gmres_solve(op, B, tol=1e-6, restart=30, max_iter=600)
+    res = np.linalg.norm(op.matmat(X) - B, axis=0) / np.linalg.norm(B, axis=0)
+    fp64_peak = 37.1e12  # measured DMMA/DFMA throughput, profiles/r01_fp64_peak.json
+    out = {"config": f"cfg1 cube 16^3 (N=4096), q={q} seeded N(0,1) right-hand sides",
+           "matvec_ms": ms, "value": pk.n * q / (ms * 1e-3), "unit": "unknowns*RHS/s",
+           "tflops": pk.flops(q) / (ms * 1e-3) / 1e12,
+           "frac_fp64_peak": pk.flops(q) / (ms * 1e-3) / fp64_peak,
+           "kernel": "k_zgemm_grouped (DMMA m8n8k4, FP64 tensor pipe)", "launches": int(nl.value),
+           "block_gmres": {"restart": 30, "tol": 1e-6, "iterations": rep.iterations,
+                           "solve_s": rep.wall_time, "converged": rep.converged,
+                           "max_true_rel_residual": float(res.max())}}
+    op.close()
+    return out
+
+
 def run_reference(a):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -463,6 +514,9 @@ def main():
     gm = gmres_bench(rank, world, local) if not a.no_gmres else None
     if gm:
         line["gmres"] = gm
+    mr = mrhs_bench(rank, local) if not a.no_gmres else None
+    if mr:
+        line["multi_rhs"] = mr
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         t_cpu, n_cpu = cpu_port_time(pk, ex["x"][:, 0], a.cpu_seconds)
         line["cpu_baseline"] = {"value": pk.n / t_cpu, "unit": UNIT, "cores": 1, "kind": "port",
