@@ -88,14 +88,15 @@ __device__ __forceinline__ double2* pick_b(const MmBufs& bf, int id) {
   return id == B_N ? bf.y : p;
 }
 
-__device__ __forceinline__ void mm_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void mm_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 // Staging of one K-chunk (segment) with TMA bulk copies (cp.async.bulk, one copy per
@@ -115,7 +116,10 @@ __device__ __forceinline__ void issue_seg(const MmSeg& s, const MmBufs& bf, int 
   const bool trans = s.flags & SEG_TRANS;
   const int na = trans ? s.k : m;          // A rows to copy
   const int la = trans ? m : s.k;          // elements per A row
+  // every producer lane arrives (count 32): each lane's own pad stores are released by its own
+  // arrive; lane 0 also announces the transaction bytes
   if (lane == 0) mbar_arrive_expect_tx(bar, 16u * (uint32_t)(na * la + s.k * qv));
+  else mm_arrive(bar);
   __syncwarp();
   double2* As = st;
   double2* Bs = st + MM_A_ELEMS;
@@ -183,14 +187,17 @@ __global__ void __launch_bounds__(MM_THREADS, 1) k_zgemm_grouped(const MmItem* _
   extern __shared__ __align__(16) double2 sm[];
   const MmItem it = items[blockIdx.x];
   const int col0 = blockIdx.y * MM_N;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp 0 is the producer; MMA warps are numbered 0..MM_WARPS-1 from threadIdx 32 on
+  const int lane = threadIdx.x & 31;
+  const bool producer = threadIdx.x < 32;
+  const int warp = producer ? MM_WARPS : (threadIdx.x >> 5) - 1;
   const int qv = min(MM_N, q - col0);          // valid columns of this tile
   const int MT = (qv + 7) >> 3;                // q-tiles of 8
   const int MTP = MT <= 1 ? 1 : MT <= 2 ? 2 : MT <= 4 ? 4 : 8;
   const int G = MM_WARPS / MTP;
   const int mt = warp % MTP, ng = warp / MTP;
   const int NT = (2 * it.m + 7) >> 3;          // real n-tiles of 8 (<= 16)
-  const bool active = mt < MT;
+  const bool active = !producer && mt < MT;   // the producer warp owns no tiles
   const int nu = NT > ng ? (NT - ng + G - 1) / G : 0;  // n-tiles of this warp
   // lane-constant fragment geometry
   const int kk = lane & 3, b = kk & 1, jo = kk >> 1;
@@ -209,12 +216,12 @@ __global__ void __launch_bounds__(MM_THREADS, 1) k_zgemm_grouped(const MmItem* _
   __shared__ __align__(8) uint64_t full[MM_STAGES], empty[MM_STAGES];
   if (threadIdx.x == 0)
     for (int i = 0; i < MM_STAGES; ++i) {
-      mbar_init(&full[i], 1);
+      mbar_init(&full[i], 32);
       mbar_init(&empty[i], MM_WARPS);
     }
   __syncthreads();
   const int ns = it.nseg;
-  if (warp == MM_WARPS) {
+  if (producer) {
     // producer: wait until the buffer's previous chunk is consumed, zero its pads, copy
     for (int s = 0; s < ns; ++s) {
       const int buf = s % MM_STAGES;
@@ -280,51 +287,73 @@ __global__ void __launch_bounds__(MM_THREADS, 1) k_zgemm_grouped(const MmItem* _
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// q = 1: the same item / segment lists as a grouped complex GEMV on the CUDA cores
-// (memory-bound).  Thread (row i, quarter g) accumulates 8 K-entries of each segment; the four
-// partial sums of a row are combined in a fixed order (deterministic).
-constexpr int MV_THREADS = 256;
-__global__ void __launch_bounds__(MV_THREADS) k_zgemv_grouped(const MmItem* __restrict__ items,
-                                                              const MmSeg* __restrict__ segs,
-                                                              MmBufs bf) {
-  __shared__ double2 red[4][MM_M];
+// q = 1: the same item / segment lists as a grouped complex GEMV on the CUDA cores (memory-
+// bound).  512 threads: thread (row i, part g of 8) accumulates 4 K-entries of each segment
+// (row-major A: 8 lanes read one 512-byte A row; transposed A: 64 lanes read 64 consecutive
+// elements).  The item's segment descriptors are staged in shared memory first, and two
+// segments are loaded per step (8 independent 16-byte streaming loads in flight per thread), so
+// the loop never waits on a descriptor load.  The 8 partial sums of a row are combined in a
+// fixed order (deterministic).
+constexpr int MV_THREADS = 512;
+constexpr int MV_SEGS = 256;  // descriptors staged per pass (8 KB)
+
+__device__ __forceinline__ double2 ld_na(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+
+__global__ void __launch_bounds__(MV_THREADS, 1) k_zgemv_grouped(const MmItem* __restrict__ items,
+                                                                 const MmSeg* __restrict__ segs,
+                                                                 MmBufs bf) {
+  __shared__ double2 red[8][MM_M];
+  __shared__ MmSeg ss[MV_SEGS];
   const MmItem it = items[blockIdx.x];
+  // all segments of an item share the A orientation (checked by h2b_plan_set_phase)
+  const bool trans = it.nseg > 0 && (segs[it.seg0].flags & SEG_TRANS);
+  const int i = trans ? (threadIdx.x & (MM_M - 1)) : (threadIdx.x >> 3);
+  const int g = trans ? (threadIdx.x >> 6) : (threadIdx.x & 7);
+  const int j0 = g * 4;
+  const bool row_ok = i < it.m;
   double2 acc = make_double2(0.0, 0.0);
-  for (int sgi = 0; sgi < it.nseg; ++sgi) {
-    const MmSeg s = segs[it.seg0 + sgi];
-    const double2* A = pick_a(bf, s.flags & 15) + s.a_off;
-    const double2* B = pick_b(bf, (s.flags >> 4) & 15);
-    const bool gather = s.flags & SEG_GATHER;
-    int i, g;
-    if (s.flags & SEG_TRANS) { i = threadIdx.x & (MM_M - 1); g = threadIdx.x >> 6; }
-    else { i = threadIdx.x >> 2; g = threadIdx.x & 3; }
-    if (i < it.m) {
-      const int j0 = g * 8, j1 = min(s.k, j0 + 8);
-      double2 av[8], xv[8];
+  for (int c0 = 0; c0 < it.nseg; c0 += MV_SEGS) {
+    const int n = min(MV_SEGS, it.nseg - c0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < n; e += MV_THREADS) ss[e] = segs[it.seg0 + c0 + e];
+    __syncthreads();
+    if (!row_ok) continue;
+    constexpr int SU = 4;  // segments per step: 16 streaming loads (256 B) in flight per thread
+    for (int s0 = 0; s0 < n; s0 += SU) {
+      double2 av[SU][4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int j = j0 + u;
-        if (j < j1) {
-          av[u] = (s.flags & SEG_TRANS) ? A[(int64_t)j * s.lda + i] : A[(int64_t)i * s.lda + j];
-          const int64_t row = gather ? (int64_t)__ldg(bf.gather + s.b_row + j) : s.b_row + j;
-          xv[u] = B[row];
-        }
+      for (int h = 0; h < SU; ++h) {
+        const bool live = s0 + h < n;
+        const MmSeg& sg = ss[live ? s0 + h : s0];
+        const double2* A = pick_a(bf, sg.flags & 15) + sg.a_off;
+        const int64_t step = trans ? sg.lda : 1;
+        const double2* Ap = A + (trans ? (int64_t)i : (int64_t)i * sg.lda) + (int64_t)j0 * step;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          av[h][u] = (live && j0 + u < sg.k) ? ld_na(Ap + u * step) : make_double2(0.0, 0.0);
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (j0 + u < j1) cfma(acc, av[u], xv[u]);
+      for (int h = 0; h < SU; ++h) {  // x / x̂ / ŷ rows: L1/L2 hits, read when the A stream lands
+        if (s0 + h >= n) break;
+        const MmSeg& sg = ss[s0 + h];
+        const double2* B = pick_b(bf, (sg.flags >> 4) & 15) + sg.b_row;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (j0 + u < sg.k) cfma(acc, av[h][u], __ldg(B + j0 + u));
+      }
     }
   }
-  // all segments of an item share the A orientation (checked by h2b_plan_set_phase), so the
-  // thread's (row, quarter) is the same for every segment
-  int i, g;
-  if (it.nseg > 0 && (segs[it.seg0].flags & SEG_TRANS)) { i = threadIdx.x & (MM_M - 1); g = threadIdx.x >> 6; }
-  else { i = threadIdx.x >> 2; g = threadIdx.x & 3; }
   red[g][i] = acc;
   __syncthreads();
   if (threadIdx.x < it.m) {
     const int r = threadIdx.x;
-    const double2 v = cadd(cadd(red[0][r], red[1][r]), cadd(red[2][r], red[3][r]));
+    double2 v = red[0][r];
+#pragma unroll
+    for (int gg = 1; gg < 8; ++gg) v = cadd(v, red[gg][r]);
     double2* o = pick_b(bf, it.flags & 15) + it.c_row + r;
     *o = (it.flags & ITEM_ACC) ? cadd(*o, v) : v;
   }

@@ -254,13 +254,28 @@ def plan_shard(pk, G: int, g: int, part: Partition | None = None) -> ShardPlan:
 
     Bd = _Builder()  # near-field + leaf back-transform of own leaves -> local y rows
     r0 = int(part.row0[g])
+    sample = None
+    if pk.dbuf.size == 0 and pk.n_near:  # near-field not on the host: sample this rank's rows
+        from .nearfield import assemble_block, geometry_arrays
+        geo = geometry_arrays(pk.meta["geometry"])
+        sample = lambda rows, cols: assemble_block(*geo, rows, cols)  # noqa: E731
     for t in np.nonzero(own & (lo_of < 0))[0]:
         nt = int(pk.c_size[t])
         blocks = []
+        if sample is not None:
+            rows = pk.perm[pk.c_start[t]:pk.c_start[t] + nt]
+            srcs = pk.d_col[pk.d_row_ptr[t]:pk.d_row_ptr[t + 1]]
+            panel = sample(rows, np.concatenate([pk.perm[pk.c_start[s]:pk.c_start[s] + pk.c_size[s]]
+                                                 for s in srcs]))
+        c0 = 0
         for b in range(pk.d_row_ptr[t], pk.d_row_ptr[t + 1]):
             s = int(pk.d_col[b])
             ns = int(pk.c_size[s])
-            D = pk.dbuf[pk.d_off[b]:pk.d_off[b] + nt * ns].reshape(nt, ns)
+            if sample is not None:
+                D = panel[:, c0:c0 + ns]
+                c0 += ns
+            else:
+                D = pk.dbuf[pk.d_off[b]:pk.d_off[b] + nt * ns].reshape(nt, ns)
             blocks.append((put(PAY_D, D), s, ns))
         voff = put(PAY_V, V(t)) if k[t] > 0 else -1
         for m0 in range(0, nt, MM_M):

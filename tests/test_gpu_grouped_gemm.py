@@ -55,11 +55,16 @@ def test_grouped_kernels_match_interpreter(q):
     Y0 = rng.standard_normal((n_rows, q)) + 1j * rng.standard_normal((n_rows, q))
     ref = [torch.from_numpy(a.copy()) for a in (X, YH, Y0)]
     NumpyPlanEngine(plan).run(4, ref[0], ref[1], ref[2], q)
-    dev = [torch.from_numpy(a.copy()).cuda() for a in (X, YH, Y0)]
     eng = CudaPlanEngine(plan, 0)
-    eng.run(4, dev[0], dev[1], dev[2], q)
-    torch.cuda.synchronize()
-    got = dev[2].cpu().numpy()
     exp = ref[2].numpy()
-    assert np.linalg.norm(got - exp) <= 1e-13 * np.linalg.norm(exp)
+    first = None
+    for rep in range(5):  # repeated launches: a scheduling race shows up as a rare wrong tile
+        dev = [torch.from_numpy(a.copy()).cuda() for a in (X, YH, Y0)]
+        eng.run(4, dev[0], dev[1], dev[2], q)
+        torch.cuda.synchronize()
+        got = dev[2].cpu().numpy()
+        assert np.linalg.norm(got - exp) <= 1e-13 * np.linalg.norm(exp), rep
+        if first is None:
+            first = got
+        assert np.array_equal(got, first)  # deterministic: fixed summation order
     eng.close()

@@ -28,11 +28,14 @@ eng = CudaPlanEngine(plan, 0)
 eng.run(4, dev[0], dev[1], dev[2], q)
 torch.cuda.synchronize()
 got, exp = dev[2].cpu().numpy(), ref[2].numpy()
+bad_any = False
 for n, it in enumerate(items):
     r0, m = int(it["c_row"]), int(it["m"])
     e = np.linalg.norm(got[r0:r0 + m] - exp[r0:r0 + m]) / max(np.linalg.norm(exp[r0:r0 + m]), 1e-300)
     sg = segs[it["seg0"]:it["seg0"] + it["nseg"]]
     bad_rows = np.nonzero(np.abs(got[r0:r0 + m] - exp[r0:r0 + m]).max(1) > 1e-10)[0]
     bad_cols = np.nonzero(np.abs(got[r0:r0 + m] - exp[r0:r0 + m]).max(0) > 1e-10)[0]
+    if e < 1e-12:
+        continue
     print(n, "acc", int(it["flags"]) >> 8, "m", m, "nseg", it["nseg"], "ks", [int(s["k"]) for s in sg], "trans", [int(s["flags"]) >> 8 & 1 for s in sg][:1],
           f"err {e:.2e}", "bad rows", bad_rows[:8].tolist(), "bad cols", bad_cols[:10].tolist())
