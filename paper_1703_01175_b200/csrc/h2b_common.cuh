@@ -206,6 +206,13 @@ struct GraphKey {
 
 struct MrhsPlan;  // h2b_mrhs.cu
 
+struct GmresKey {  // one captured Arnoldi step of h2b_gmres
+  const void* V;
+  int j, m;
+  int64_t n;
+  bool operator<(const GmresKey& o) const { return std::tie(V, j, m, n) < std::tie(o.V, o.j, o.m, o.n); }
+};
+
 struct h2b_ctx {
   int device = 0;
   int64_t n = 0;
@@ -296,6 +303,7 @@ struct h2b_ctx {
   cudaStream_t far_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::map<GraphKey, cudaGraphExec_t> graphs;
+  std::map<GmresKey, cudaGraphExec_t> gmres_graphs;  // per-step graphs of h2b_gmres
   int use_graphs = 1;
   int use_mega = 1;  // plan the persistent single-launch kernel for q = 1
   // krylov workspace
@@ -312,6 +320,8 @@ struct h2b_ctx {
 int h2b_prepare(h2b_ctx* h);
 int h2b_ensure_workspace(h2b_ctx* h, int q);
 int h2b_run_matvec(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st);
+// the launches of one matvec without graph replay (for capture into a larger graph)
+int h2b_enqueue_matvec(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st, int* nl);
 int h2b_run_phase(h2b_ctx* h, int phase, const double2* xp, double2* yp, int q, cudaStream_t st);
 int h2b_launch_gather(const int64_t* perm, int64_t n, const double2* in, double2* out, int q,
                       cudaStream_t st);

@@ -54,19 +54,20 @@ __global__ void __launch_bounds__(RT) k_dots_partial(DotPairs d, int64_t n, doub
   }
 }
 
-// multi-dot against the rows of a basis: partial[j*grid+blk] = Σ conj(V[j*ldv+i]) w[i]
+// multi-dot against the rows of a basis: partial[j*nb+blk] = Σ conj(V[j*ldv+i]) w[i]; one grid
+// row (blockIdx.y) per basis vector, so all j run in parallel (fixed per-block summation order)
 __global__ void __launch_bounds__(RT) k_basis_dots_partial(const double2* __restrict__ V, int64_t ldv,
                                                            int nv, const double2* __restrict__ w,
                                                            int64_t n, double2* partial) {
   __shared__ double2 sm[RT / 32];
-  for (int j = 0; j < nv; ++j) {
-    const double2* vj = V + j * ldv;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int64_t i = blockIdx.x * (int64_t)RT + threadIdx.x; i < n; i += (int64_t)gridDim.x * RT)
-      cfma_conj(acc, vj[i], w[i]);
-    double2 s = block_sum2(acc, sm);
-    if (threadIdx.x == 0) partial[j * gridDim.x + blockIdx.x] = s;
-  }
+  const int j = blockIdx.y;
+  if (j >= nv) return;
+  const double2* vj = V + j * ldv;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int64_t i = blockIdx.x * (int64_t)RT + threadIdx.x; i < n; i += (int64_t)gridDim.x * RT)
+    cfma_conj(acc, vj[i], w[i]);
+  double2 s = block_sum2(acc, sm);
+  if (threadIdx.x == 0) partial[j * gridDim.x + blockIdx.x] = s;
 }
 
 // out[j] = Σ_blk partial[j*nb + blk] in fixed order (one warp per j)
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(RT) k_lincomb(Lin3 L, double2* out, int64_t n,
 }
 
 int nblocks(int64_t n) {
-  int64_t b = (n + RT * 4 - 1) / (RT * 4);
+  int64_t b = (n + RT - 1) / RT;  // small n: one element per thread (latency-bound)
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, RB_MAX));
 }
 
@@ -216,6 +217,8 @@ struct KryWs {
 
 int krylov_ws(h2b_ctx* h, size_t bytes, double2** out) {
   if (h->kry_bytes < bytes) {
+    for (auto& kv : h->gmres_graphs) cudaGraphExecDestroy(kv.second);  // they point into kry
+    h->gmres_graphs.clear();
     if (h->kry) cudaFree(h->kry);
     h->device_bytes -= h->kry_bytes;
     h->kry = nullptr;
@@ -232,6 +235,70 @@ double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+
+// ---- GMRES: Givens rotations on the device --------------------------------------------------
+struct GivensState {
+  double2* H;       // (m+1) x m, row-major: H[i*m + j]
+  double2* g;       // m+1: rotated right-hand side
+  double2* cs_sn;   // m: {c_i, 0}
+  double2* res_hn;  // 2m: {res_j, 0}, {hn_j, 0}
+  double2* scale;   // 1: 1 / hn of the last step (0 on breakdown)
+};
+
+// Restates the host recurrence of oracle/krylov_oracle.py::gmres_solve for step j:
+// hc = h1 + h2 (CGS2), apply rotations 0..j-1, new rotation zeroing hn, update g.  The cosines
+// c_i live in cs_sn[i].x, the complex sines s_i in the spare last row of H (H[m*m + i]), which
+// never holds a Hessenberg entry (the sub-diagonal is rotated away, never stored).
+__global__ void k_givens_step(int j, int m, const double2* __restrict__ hv, GivensState S, double bnrm) {
+  if (threadIdx.x != 0) return;
+  double2 hc[64];
+  for (int i = 0; i <= j; ++i) hc[i] = make_double2(hv[i].x + hv[64 + i].x, hv[i].y + hv[64 + i].y);
+  const double hn = sqrt(hv[128].x);
+  double2* sn = S.H + (size_t)m * m;  // row m of H: the complex sines
+  for (int i = 0; i < j; ++i) {
+    const double c = S.cs_sn[i].x;
+    const double2 s = sn[i];
+    const double2 a = hc[i], bb = hc[i + 1];
+    // hc[i] = c a + s bb ; hc[i+1] = -conj(s) a + c bb
+    hc[i] = make_double2(c * a.x + (s.x * bb.x - s.y * bb.y), c * a.y + (s.x * bb.y + s.y * bb.x));
+    hc[i + 1] = make_double2(-(s.x * a.x + s.y * a.y) + c * bb.x, -(s.x * a.y - s.y * a.x) + c * bb.y);
+  }
+  double c;
+  double2 s, rr;
+  const double ahj = hypot(hc[j].x, hc[j].y);
+  if (hn == 0.0) {
+    c = 1.0; s = make_double2(0.0, 0.0); rr = hc[j];
+  } else if (ahj == 0.0) {
+    c = 0.0; s = make_double2(1.0, 0.0); rr = make_double2(hn, 0.0);
+  } else {
+    const double t = hypot(ahj, hn);
+    const double2 ph = make_double2(hc[j].x / ahj, hc[j].y / ahj);
+    c = ahj / t;
+    s = make_double2(ph.x * hn / t, ph.y * hn / t);
+    rr = make_double2(ph.x * t, ph.y * t);
+  }
+  S.cs_sn[j] = make_double2(c, 0.0);
+  sn[j] = s;
+  for (int i = 0; i <= j; ++i) S.H[(size_t)i * m + j] = hc[i];
+  S.H[(size_t)j * m + j] = rr;
+  const double2 gj = S.g[j];
+  S.g[j + 1] = make_double2(-(s.x * gj.x + s.y * gj.y), -(s.x * gj.y - s.y * gj.x));  // -conj(s) gj
+  S.g[j] = make_double2(c * gj.x, c * gj.y);
+  const double2 gn = S.g[j + 1];
+  S.res_hn[2 * j] = make_double2(hypot(gn.x, gn.y) / bnrm, 0.0);
+  S.res_hn[2 * j + 1] = make_double2(hn, 0.0);
+  S.scale[0] = make_double2(hn == 0.0 ? 0.0 : 1.0 / hn, 0.0);
+}
+
+// w *= scale[0] (a device scalar: the normalisation of the new basis vector)
+__global__ void __launch_bounds__(RT) k_scale_dev(double2* w, int64_t n, const double2* __restrict__ scale) {
+  const double f = scale[0].x;
+  for (int64_t i = blockIdx.x * (int64_t)RT + threadIdx.x; i < n; i += (int64_t)gridDim.x * RT) {
+    double2 v = w[i];
+    w[i] = make_double2(v.x * f, v.y * f);
+  }
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -246,7 +313,7 @@ extern "C" int h2b_zdotc_multi(const void* V, int64_t ldv, int nv, const void* w
   TRY(scratch_ready());
   cudaStream_t st = (cudaStream_t)stream;
   const int nb = nblocks(n);
-  k_basis_dots_partial<<<nb, RT, 0, st>>>((const double2*)V, ldv, nv, (const double2*)w, n,
+  k_basis_dots_partial<<<dim3(nb, nv), RT, 0, st>>>((const double2*)V, ldv, nv, (const double2*)w, n,
                                           g_scratch.partial);
   H2B_CHECK_LAUNCH();
   k_reduce_partials<<<nv, 32, 0, st>>>(g_scratch.partial, nb, nv, (double2*)out_dev);
@@ -309,16 +376,24 @@ extern "C" int h2b_gmres(h2b_handle h, const void* b_perm, void* x_perm, int res
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t n = h->n;
   const int m = restart;
+  // workspace: V (m+1) x n basis, r, tmp, then the device Givens state
+  const size_t gs_elems = (size_t)(m + 1) * m + (m + 1) + 3 * (size_t)m + 1;
   double2* ws = nullptr;
-  // V: (m+1) x n basis, r, tmp
-  TRY(krylov_ws(h, sizeof(double2) * (size_t)n * (m + 3), &ws));
+  TRY(krylov_ws(h, sizeof(double2) * ((size_t)n * (m + 3) + gs_elems), &ws));
   double2* V = ws;
   double2* r = ws + (size_t)n * (m + 1);
   double2* tmp = r + n;
+  GivensState S;
+  S.H = tmp + n;
+  S.g = S.H + (size_t)(m + 1) * m;
+  S.cs_sn = S.g + (m + 1);
+  S.res_hn = S.cs_sn + m;
+  S.scale = S.res_hn + m + m;
   const double2* b = (const double2*)b_perm;
   double2* x = (double2*)x_perm;
   Ops ops{st, n, nblocks(n), g_scratch.partial, g_scratch.vals, g_scratch.host};
-  double2* hvals = g_scratch.vals;  // device scalars
+  double2* hvals = g_scratch.vals;        // device scalars (CGS2 coefficients, ||w||^2)
+  double2* hres = g_scratch.host + 128;   // pinned: (res_j, hn_j) of step j
 
   *report = h2b_report{0, 0, 0, 0, 0.0};
   TRY(ops.dots({{b, b}}, true));
@@ -331,86 +406,113 @@ extern "C" int h2b_gmres(h2b_handle h, const void* b_perm, void* x_perm, int res
     return H2B_OK;
   }
   H2B_CUDA_TRY(cudaMemcpyAsync(r, b, sizeof(double2) * n, cudaMemcpyDeviceToDevice, st));
+  // one Arnoldi step j (matvec, CGS2, device Givens, normalisation, (res, hn) -> pinned host)
+  // as a CUDA graph, captured once per (basis, j) and replayed
+  auto step_graph = [&](int j, cudaGraphExec_t* out) -> int {
+    const GmresKey key{V, j, m, n};
+    auto it = h->gmres_graphs.find(key);
+    if (it != h->gmres_graphs.end()) {
+      *out = it->second;
+      return H2B_OK;
+    }
+    cudaStream_t cs = nullptr;
+    H2B_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    H2B_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    double2* w = V + (size_t)n * (j + 1);
+    int nl = 0;
+    int rc = h2b_enqueue_matvec(h, V + (size_t)n * j, w, 1, cs, &nl);
+    if (!rc) {
+      const int nb = ops.nb;
+      k_basis_dots_partial<<<dim3(nb, j + 1), RT, 0, cs>>>(V, n, j + 1, w, n, ops.partial);
+      k_reduce_partials<<<j + 1, 32, 0, cs>>>(ops.partial, nb, j + 1, hvals);
+      k_basis_sub<<<nb, RT, 0, cs>>>(V, n, j + 1, hvals, w, n, nullptr);
+      k_basis_dots_partial<<<dim3(nb, j + 1), RT, 0, cs>>>(V, n, j + 1, w, n, ops.partial);
+      k_reduce_partials<<<j + 1, 32, 0, cs>>>(ops.partial, nb, j + 1, hvals + 64);
+      k_basis_sub<<<nb, RT, 0, cs>>>(V, n, j + 1, hvals + 64, w, n, ops.partial);
+      k_reduce_partials<<<1, 32, 0, cs>>>(ops.partial, nb, 1, hvals + 128);
+      k_givens_step<<<1, 32, 0, cs>>>(j, m, hvals, S, bnrm);
+      k_scale_dev<<<nb, RT, 0, cs>>>(w, n, S.scale);
+      cudaMemcpyAsync(hres + 2 * j, S.res_hn + 2 * j, sizeof(double2) * 2, cudaMemcpyDeviceToHost, cs);
+    }
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cs, &g);
+    cudaStreamDestroy(cs);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) {
+      h2b_set_error(std::string("h2b_gmres: step capture: ") + cudaGetErrorString(e));
+      return H2B_ECUDA;
+    }
+    cudaGraphExec_t ex = nullptr;
+    e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+      h2b_set_error(std::string("h2b_gmres: step instantiate: ") + cudaGetErrorString(e));
+      return H2B_ECUDA;
+    }
+    h->gmres_graphs.emplace(key, ex);
+    *out = ex;
+    return H2B_OK;
+  };
+  TRY(h2b_prepare(h));
+  TRY(h2b_ensure_workspace(h, 1));
+  std::vector<cudaGraphExec_t> gx(m);
+  for (int j = 0; j < m; ++j) TRY(step_graph(j, &gx[j]));
+  cudaEvent_t ev[2];
+  H2B_CUDA_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  H2B_CUDA_TRY(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() { cudaEventDestroy(e[0]); cudaEventDestroy(e[1]); }
+  } guard{ev};
+
   int it = 0, matvecs = 0, nh = 0;
   bool converged = false;
-  std::vector<cplx> H((size_t)(m + 1) * m), g(m + 1), sn(m), y(m);
-  std::vector<double> cs(m);
+  std::vector<double2> Hh((size_t)(m + 1) * m), gh(m + 1);
+  std::vector<cplx> y(m);
   double beta = bnrm;
   while (it < max_iter) {
     if (it > 0) {
       TRY(ops.dots({{r, r}}, true));
       beta = sqrt(g_scratch.host[0].x);
     }
-    std::fill(H.begin(), H.end(), cplx(0));
-    std::fill(g.begin(), g.end(), cplx(0));
-    g[0] = beta;
+    gh.assign(m + 1, make_double2(0.0, 0.0));
+    gh[0] = make_double2(beta, 0.0);
+    H2B_CUDA_TRY(cudaMemcpyAsync(S.g, gh.data(), sizeof(double2) * (m + 1), cudaMemcpyHostToDevice, st));
     TRY(ops.lincomb(V, {{cplx(1.0 / beta), r}}, -1));
+    // steps run one ahead of the host's convergence check: step j+1 is queued before the host
+    // waits for step j's residual.  A speculative step only writes V[j+2], H[:, j+1], g[j+1..j+2]
+    // and rotation j+1, none of which the back substitution of a cycle ending at j reads.
+    const int it0 = it;
     int j_done = 0;
-  
+    H2B_CUDA_TRY(cudaGraphLaunch(gx[0], st));
+    H2B_CUDA_TRY(cudaEventRecord(ev[0], st));
     for (int j = 0; j < m; ++j) {
-      double2* w = V + (size_t)n * (j + 1);
-      TRY(h2b_run_matvec(h, V + (size_t)n * j, w, 1, st));
+      if (j + 1 < m && it0 + j + 1 < max_iter) {
+        H2B_CUDA_TRY(cudaGraphLaunch(gx[j + 1], st));
+        H2B_CUDA_TRY(cudaEventRecord(ev[(j + 1) & 1], st));
+        ++matvecs;
+      }
+      H2B_CUDA_TRY(cudaEventSynchronize(ev[j & 1]));
       ++it;
-      ++matvecs;
-      // CGS2: h1 = V^H w ; w -= V h1 ; h2 = V^H w ; w -= V h2 (+ ||w||^2)
-      k_basis_dots_partial<<<ops.nb, RT, 0, st>>>(V, n, j + 1, w, n, ops.partial);
-      k_reduce_partials<<<j + 1, 32, 0, st>>>(ops.partial, ops.nb, j + 1, hvals);
-      k_basis_sub<<<ops.nb, RT, 0, st>>>(V, n, j + 1, hvals, w, n, nullptr);
-      k_basis_dots_partial<<<ops.nb, RT, 0, st>>>(V, n, j + 1, w, n, ops.partial);
-      k_reduce_partials<<<j + 1, 32, 0, st>>>(ops.partial, ops.nb, j + 1, hvals + 64);
-      k_basis_sub<<<ops.nb, RT, 0, st>>>(V, n, j + 1, hvals + 64, w, n, ops.partial);
-      k_reduce_partials<<<1, 32, 0, st>>>(ops.partial, ops.nb, 1, hvals + 128);
-      H2B_CHECK_LAUNCH();
-      H2B_CUDA_TRY(cudaMemcpyAsync(g_scratch.host, hvals, sizeof(double2) * 129,
-                                   cudaMemcpyDeviceToHost, st));
-      H2B_CUDA_TRY(cudaStreamSynchronize(st));
-      std::vector<cplx> hc(j + 1);
-      for (int i = 0; i <= j; ++i)
-        hc[i] = cplx(g_scratch.host[i].x, g_scratch.host[i].y) +
-                cplx(g_scratch.host[64 + i].x, g_scratch.host[64 + i].y);
-      const double hn = sqrt(g_scratch.host[128].x);
-      for (int i = 0; i < j; ++i) {
-        const cplx a = hc[i], bb = hc[i + 1];
-        hc[i] = cs[i] * a + sn[i] * bb;
-        hc[i + 1] = -std::conj(sn[i]) * a + cs[i] * bb;
-      }
-      // Givens rotation zeroing hn below hc[j]
-      double c;
-      cplx s, rr;
-      if (hn == 0.0) {
-        c = 1.0; s = 0.0; rr = hc[j];
-      } else if (hc[j] == cplx(0)) {
-        c = 0.0; s = 1.0; rr = hn;
-      } else {
-        const double t = hypot(std::abs(hc[j]), hn);
-        const cplx ph = hc[j] / std::abs(hc[j]);
-        c = std::abs(hc[j]) / t;
-        s = ph * hn / t;
-        rr = ph * t;
-      }
-      cs[j] = c;
-      sn[j] = s;
-      for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = hc[i];
-      H[(size_t)j * m + j] = rr;
-      g[j + 1] = -std::conj(s) * g[j];
-      g[j] = c * g[j];
-      const double res = std::abs(g[j + 1]) / bnrm;
+      if (j == 0) ++matvecs;
+      const double res = hres[2 * j].x, hn = hres[2 * j + 1].x;
       if (history && nh < max_iter) history[nh] = res;
       ++nh;
       j_done = j + 1;
-      if (res <= tol) {
-
-        break;
-      }
-      if (it >= max_iter || hn == 0.0) break;
-      TRY(ops.lincomb(w, {{cplx(1.0 / hn), w}}, -1));
+      if (res <= tol || it >= max_iter || hn == 0.0) break;
     }
-
-    // back substitution, x += V y
+    // back substitution on the host (j_done <= 63), x += V y
+    H2B_CUDA_TRY(cudaMemcpyAsync(Hh.data(), S.H, sizeof(double2) * (size_t)(m + 1) * m, cudaMemcpyDeviceToHost, st));
+    H2B_CUDA_TRY(cudaMemcpyAsync(gh.data(), S.g, sizeof(double2) * (m + 1), cudaMemcpyDeviceToHost, st));
+    H2B_CUDA_TRY(cudaStreamSynchronize(st));
+    auto Hc = [&](int i, int l) { return cplx(Hh[(size_t)i * m + l].x, Hh[(size_t)i * m + l].y); };
     for (int i = j_done - 1; i >= 0; --i) {
-      cplx acc = g[i];
-      for (int l = i + 1; l < j_done; ++l) acc -= H[(size_t)i * m + l] * y[l];
-      y[i] = acc / H[(size_t)i * m + i];
+      cplx acc(gh[i].x, gh[i].y);
+      for (int l = i + 1; l < j_done; ++l) acc -= Hc(i, l) * y[l];
+      y[i] = acc / Hc(i, i);
     }
     for (int i = 0; i < j_done; ++i) g_scratch.host[i] = make_double2(-y[i].real(), -y[i].imag());
     H2B_CUDA_TRY(cudaMemcpyAsync(hvals, g_scratch.host, sizeof(double2) * j_done, cudaMemcpyHostToDevice, st));

@@ -122,6 +122,12 @@ int h2b_launch_scatter(const int64_t* perm, int64_t n, const double2* in, double
 void h2b_release_graphs(h2b_ctx* h) {
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
   h->graphs.clear();
+  for (auto& kv : h->gmres_graphs) cudaGraphExecDestroy(kv.second);
+  h->gmres_graphs.clear();
+}
+
+int h2b_enqueue_matvec(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st, int* nl) {
+  return enqueue_matvec(h, xp, yp, q, st, nl);
 }
 
 int h2b_ensure_workspace(h2b_ctx* h, int q) {

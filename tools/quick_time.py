@@ -1,6 +1,7 @@
 """Quick CUDA-event timing of the matvec on data/cfg<k>.npz (development aid)."""
 import sys, os, time, ctypes as C
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.chdir(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_1703_01175_b200 import as_operator, load_packed, _abi
 
@@ -20,7 +21,8 @@ def timeit(fn, reps, flush=None):
     return tot / reps
 
 for k in [int(a) for a in sys.argv[1:]] or [1, 2]:
-    pk, ex = load_packed(f"data/cfg{k}.npz", with_extra=True)
+    from bench import load
+    pk, ex = load(k)
     t = time.time(); op = as_operator(pk); _abi.check(_abi.lib().h2b_prepare_handle(op.handle)); torch.cuda.synchronize(); tu = time.time() - t
     x = torch.from_numpy(ex["x"][pk.perm, 0].copy()).cuda()
     y = torch.empty_like(x)
@@ -37,7 +39,7 @@ for k in [int(a) for a in sys.argv[1:]] or [1, 2]:
     op.matvec_perm(x, out=y)
     B = pk.algorithmic_bytes()
     yp = y.cpu().numpy(); yy = np.empty_like(yp); yy[pk.perm] = yp
-    err = np.linalg.norm(yy - ex["y"][:, 0]) / np.linalg.norm(ex["y"][:, 0])
+    err = np.linalg.norm(yy - ex["y"][:, 0]) / np.linalg.norm(ex["y"][:, 0]) if "y" in ex else float("nan")
     print(f"cfg{k}: N={pk.n} prep {tu:.2f}s span_mode={q(op,2)} ls={q(op,3)} top_staged={q(op,4)} launches={q(op,1)} | "
           f"warm {warm*1e3:.1f} us ({B/warm/1e6:.0f} GB/s) cold {cold*1e3:.1f} us ({B/cold/1e6:.0f} GB/s) | "
           f"near cold {near_c*1e3:.1f} us ({pk.near_bytes()/near_c/1e6:.0f} GB/s) far(no-graph) cold {far_c*1e3:.1f} us | relerr {err:.2e}", flush=True)
