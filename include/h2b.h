@@ -90,8 +90,8 @@ int h2b_device_ok(int device);
  * construction of the reference H2Matrix object as the matvec's input
  * (build.py:135-145). */
 int h2b_create(const h2b_layout* layout, int device, h2b_handle* out);
-/* Copy `bytes` of host payload into section `sec` at byte offset `offset`
- * (chunked uploads allowed).  All four sections must be covered before use. */
+/* Copy `bytes` of payload (host or device memory) into section `sec` at byte offset
+ * `offset` (chunked uploads allowed).  All four sections must be covered before use. */
 int h2b_upload(h2b_handle h, int sec, const void* src, size_t bytes, size_t offset);
 int h2b_destroy(h2b_handle h);
 /* Fill the near-field section on the device from the voxel geometry instead of uploading it

@@ -193,7 +193,8 @@ int h2b_upload(h2b_handle h, int sec, const void* src, size_t bytes, size_t offs
   if (bytes == 0) return H2B_OK;
   REQUIRE(src, H2B_EINVAL, "h2b_upload: null source");
   H2B_CUDA_TRY(cudaSetDevice(h->device));
-  H2B_CUDA_TRY(cudaMemcpy((char*)h->buf[sec] + offset, src, bytes, cudaMemcpyHostToDevice));
+  // host or device source (unified addressing): device-side fills need no host staging
+  H2B_CUDA_TRY(cudaMemcpy((char*)h->buf[sec] + offset, src, bytes, cudaMemcpyDefault));
   h->sec_uploaded[sec] = std::max<int64_t>(h->sec_uploaded[sec], (int64_t)((offset + bytes) / 16));
   return H2B_OK;
 }

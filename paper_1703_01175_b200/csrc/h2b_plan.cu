@@ -1314,6 +1314,7 @@ int h2b_prepare(h2b_ctx* h) {
       // the attribute is per kernel and process-wide: set the maximum, never a per-handle size
       H2B_TRY(h2b_near_stream_set_smem(mp.ns, mp.r, 232448 - near_static));
       h->near_grid = sms;
+      if (const char* e = getenv("H2B_NEAR_GRID")) h->near_grid = std::max(1, std::min(sms, atoi(e)));  // tuning aid
       h->mega = (per_sm > 0 && h->mega_grid <= per_sm * sms) ? 1 : 0;
       h->mega_est_us = mp.est_makespan;
     }

@@ -80,11 +80,17 @@ class H2Operator:
             setattr(lay, name, _ptr(arr(name, np.int64), C.c_int64))
         lay.n_coupling = pk.n_coupling
         lay.n_near = pk.n_near
-        lay.v_elems, lay.t_elems = int(pk.vbuf.size), int(pk.tbuf.size)
+        far_on_device = ("synthetic" in pk.meta and pk.sbuf.size == 0 and pk.vbuf.size == 0
+                         and pk.tbuf.size == 0)
+        if far_on_device:
+            ev, et, es = pk.far_elems_expected()
+        else:
+            ev, et, es = int(pk.vbuf.size), int(pk.tbuf.size), int(pk.sbuf.size)
+        lay.v_elems, lay.t_elems = ev, et
         near_on_device = pk.dbuf.size == 0 and pk.n_near > 0
         if near_on_device and "geometry" not in pk.meta:
             raise ValueError("operator has no near-field payload and no geometry to assemble it from")
-        lay.s_elems, lay.d_elems = int(pk.sbuf.size), int(pk.d_elems_expected())
+        lay.s_elems, lay.d_elems = es, int(pk.d_elems_expected())
         handle = C.c_void_p()
         _abi.check(L.h2b_create(C.byref(lay), self.device, C.byref(handle)), "h2b_create")
         self._h = handle
@@ -98,6 +104,9 @@ class H2Operator:
             _abi.check(L.h2b_assemble_near(handle, centers.ctypes.data, chi.ctypes.data, float(k0),
                                            float(vol), float(diag.real), float(diag.imag)),
                        "h2b_assemble_near")
+        if far_on_device:  # structure-exact operator: seeded V/T/S generated in HBM
+            from .synthetic import fill_far_field_on_device
+            fill_far_field_on_device(L, handle, pk, self.device, pk.meta["synthetic"].get("seed", 0))
         for sec, buf in ((_abi.SEC_V, pk.vbuf), (_abi.SEC_T, pk.tbuf), (_abi.SEC_S, pk.sbuf),
                          (_abi.SEC_D, pk.dbuf)):
             b = np.ascontiguousarray(buf, dtype=np.complex128).view(np.uint8)

@@ -71,6 +71,9 @@ def geometry_arrays(geom: dict):
     centers = lattice_centers(nx, ny, nz, h)
     n = centers.shape[0]
     eps = geom["eps_r"]
+    if isinstance(eps, dict):  # BASELINE cfg5: eps_r = lo + (hi - lo) * rng.random(N), seeded
+        lo, hi = eps["uniform"]
+        eps = lo + (hi - lo) * np.random.default_rng(int(eps.get("seed", 0))).random(n)
     chi = (np.full(n, complex(eps), dtype=np.complex128) - 1.0 if np.isscalar(eps)
            else np.asarray(eps, dtype=np.complex128) - 1.0)
     return centers, chi, float(geom["k0"]), h ** 3

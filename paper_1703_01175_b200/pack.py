@@ -121,9 +121,11 @@ class PackedH2:
 
     def element_counts(self):
         """E_V, E_T, E_S, E_D and K of SURVEY.md §8(d)."""
-        return dict(E_V=int(self.vbuf.size), E_T=int(self.tbuf.size),
-                    E_S=int(self.sbuf.size), E_D=self.d_elems_expected(),
-                    K=self.total_rank)
+        if self.sbuf.size or self.vbuf.size or self.tbuf.size:
+            ev, et, es = int(self.vbuf.size), int(self.tbuf.size), int(self.sbuf.size)
+        else:  # far field not materialised on the host (filled on the device)
+            ev, et, es = self.far_elems_expected()
+        return dict(E_V=ev, E_T=et, E_S=es, E_D=self.d_elems_expected(), K=self.total_rank)
 
     def storage_bytes(self):
         """Same total as H2Matrix.storage_bytes() (build.py:176-187)."""
@@ -139,6 +141,18 @@ class PackedH2:
         """Near-field elements implied by the tables: sum n_t * n_s over inadmissible pairs."""
         rows = np.repeat(np.arange(self.num_clusters), np.diff(self.d_row_ptr))
         return int(np.sum(self.c_size[rows].astype(np.int64) * self.c_size[self.d_col].astype(np.int64)))
+
+    def far_elems_expected(self):
+        """(E_V, E_T, E_S) implied by the tables (sizes of V, T, S even when not materialised)."""
+        rank, size = self.c_rank.astype(np.int64), self.c_size.astype(np.int64)
+        lo, hi = self.c_child_lo, self.c_child_hi
+        leaf = lo < 0
+        ev = int(np.sum(size[leaf] * rank[leaf]))
+        nl = ~leaf
+        et = int(np.sum((rank[lo[nl]] + rank[hi[nl]]) * rank[nl]))
+        rows = np.repeat(np.arange(self.num_clusters), np.diff(self.s_row_ptr))
+        es = int(np.sum(rank[rows] * rank[self.s_col]))
+        return ev, et, es
 
     def near_bytes(self, q=1):
         """Algorithmic bytes of the near-field phase alone: D once, x_s and y_t once."""
@@ -345,7 +359,7 @@ def _synthetic_far_field(kw, spec):
     return dict(vbuf=cplx(ev, 0.125), tbuf=cplx(et, 0.125), sbuf=cplx(es, 0.01))
 
 
-def load_packed(path, with_extra=False, near_on_host=True):
+def load_packed(path, with_extra=False, near_on_host=True, far_on_host=True):
     """Read a packed operator.  A compact file (no near-field payload, a geometry record) gets
     its near-field re-assembled on the host (nearfield.py) — or, with ``near_on_host=False``,
     left empty (``dbuf.size == 0``) for `H2Operator` to generate on the device."""
@@ -355,7 +369,11 @@ def load_packed(path, with_extra=False, near_on_host=True):
         raise ValueError(f"{path}: unsupported packed-H2 format {head.get('version')}")
     kw = {name: z[name] for name in _INT_TABLES + _PAYLOADS if name in z.files}
     if "synthetic" in head:
-        kw.update(_synthetic_far_field(kw, head["synthetic"]))
+        if far_on_host:
+            kw.update(_synthetic_far_field(kw, head["synthetic"]))
+        else:  # left empty: H2Operator fills V/T/S on the device (synthetic.py)
+            kw.update(vbuf=np.zeros(0, np.complex128), tbuf=np.zeros(0, np.complex128),
+                      sbuf=np.zeros(0, np.complex128))
     if "dbuf" not in kw:
         if "geometry" not in head:
             raise ValueError(f"{path}: no near-field payload and no geometry to rebuild it from")
