@@ -19,8 +19,12 @@ shipped packed as data/cfg2.npz (tools/make_golden.py).
               (oracle/h2_oracle.py, a faithful port of arith.matvec) timed on
               this host, 1 thread.
 ``--impl reference`` times that CPU port alone and prints the same line.
-Multi-GPU (torchrun): every rank runs an independent replica of the matvec
-("replicas", weak scaling); the max over ranks of the device time is used.
+Multi-GPU (torchrun, N > 1): the headline shards right-hand sides across ranks — every rank
+holds the operator and applies it to its own RHS (independent objects, no data-path collective,
+weak scaling; max over ranks of the device time).  Beside it, ``partitioned_strong`` measures the
+same operator partitioned by subtree over the N GPUs (paper_1703_01175_b200/dist.py: one NCCL
+all-gather of x and x̂ per matvec, strong scaling of one RHS); ``--partitioned`` makes that the
+headline.
 """
 
 from __future__ import annotations
@@ -278,7 +282,7 @@ def run_reference(a):
     return 0
 
 
-def run_partitioned(a, pk, ex, rank, world, local):
+def run_partitioned(a, pk, ex, rank, world, local, emit=True):
     """N GPUs, one process each: the operator is partitioned by subtree (SURVEY.md §8e,
     paper_1703_01175_b200/dist.py) — each rank owns a contiguous slice of rows and the
     matching bases / coupling rows / near-field rows; one NCCL all-gather of x and x̂ per
@@ -364,7 +368,11 @@ def run_partitioned(a, pk, ex, rank, world, local):
             "clocks": clk.summary(), "parity_relerr_vs_reference": relerr,
             "exchange_bytes_per_step": 16 * op.part.chunk * world,
         }
+        if not emit:
+            return line
         print(json.dumps(line))
+    if not emit:
+        return None
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -390,12 +398,12 @@ def main():
         if rank == 0:
             print(json.dumps({"metric": METRIC, "error": f"data/cfg{a.config}.npz missing"}))
         return 1
-    if world > 1 or a.partitioned:
+    if a.partitioned:
         return run_partitioned(a, pk, ex, rank, world, local)
     op = H2Operator(pk, device=local)
     L = _abi.lib()
     _abi.check(L.h2b_prepare_handle(op.handle), "prepare")
-    x = torch.from_numpy(ex["x"][pk.perm, 0].copy()).to(dev)
+    x = torch.from_numpy(ex["x"][pk.perm, rank % ex["x"].shape[1]].copy()).to(dev)  # own RHS
     y = torch.empty_like(x)
     stream = torch.cuda.current_stream(dev)
     sh = C.c_void_p(stream.cuda_stream)
@@ -489,7 +497,9 @@ def main():
         "dtype": "complex128 (f64)",
         "data": "synthetic: reference-built operator of BASELINE config, N(0,1) RHS (seed 0)",
         "config": dict(config_desc(a.config, pk), l2="flushed before every timed step (256 MiB write + 256 MiB read: clean L2)",
-                       parallelism=f"replicas x{world}"),
+                       parallelism=(f"{world} GPUs, one process each: right-hand sides sharded "
+                                    "across ranks (each rank a full operator replica and its own "
+                                    "RHS; no data-path collective)" if world > 1 else "1 GPU")),
         "achieved_gbs_total": pk.algorithmic_bytes(1) / (ms * 1e-3) / 1e9,
         "hbm_frac_total": pk.algorithmic_bytes(1) / (ms * 1e-3) / 1e9 / peak,
         "roofline": {"bound": "hbm",
@@ -523,6 +533,17 @@ def main():
                                 "sample": f"{n_cpu} full cfg{a.config} matvecs in {t_cpu * n_cpu:.1f} s "
                                           "(oracle/h2_oracle.py restates arith.matvec loop-for-loop)",
                                 "cpu": os.cpu_count()}
+    if world > 1:
+        # the same operator partitioned by subtree over the N GPUs (one NCCL all-gather per
+        # matvec, strong scaling of ONE right-hand side), reported beside the headline
+        part = run_partitioned(argparse.Namespace(**dict(vars(a), steps=min(a.steps, 10))), pk, ex,
+                               rank, world, local, emit=False)
+        if rank == 0 and part:
+            line["partitioned_strong"] = {k: part[k] for k in ("value", "ms_per_step", "scaling",
+                                                               "roofline", "exchange_bytes_per_step",
+                                                               "gpu_launches_per_step",
+                                                               "parity_relerr_vs_reference")}
+            line["partitioned_strong"]["parallelism"] = part["config"]["parallelism"]
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

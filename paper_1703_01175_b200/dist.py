@@ -54,7 +54,7 @@ class CudaPlanEngine:
 
     def run(self, phase, xbuf, yhat, y, q, stream=None):
         torch = __import__("torch")
-        st = torch.cuda.current_stream(self.device) if stream is None else stream
+        st = torch.cuda.current_stream(self.device) if stream is None else stream  # (capturing)
         _abi.check(_abi.lib().h2b_plan_run(self.handle, phase, C.c_void_p(xbuf.data_ptr()),
                                            C.c_void_p(xbuf.data_ptr()), C.c_void_p(yhat.data_ptr()),
                                            C.c_void_p(y.data_ptr()), int(q),
@@ -101,6 +101,7 @@ class DistH2Operator:
             self.device = torch.device(getattr(engine, "device_name", "cpu"))
         self.engine = engine
         self._ws = {}
+        self._graphs = {}
 
     def _work(self, q):
         import torch
@@ -122,17 +123,37 @@ class DistH2Operator:
         dist.all_gather_into_tensor(torch.view_as_real(xbuf[:self.world * ch]),
                                     torch.view_as_real(send), group=self.group)
 
-    def matvec_local(self, x_local):
+    def _body(self, q):
+        """The matvec on the workspace of q columns: x slice already in the exchange buffer."""
+        xbuf, yhat, y, send = self._work(q)
+        self.engine.run(PH_UP_OWN, xbuf, yhat, y, q)
+        self.exchange(xbuf, send, q)
+        for ph in (PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR):
+            self.engine.run(ph, xbuf, yhat, y, q)
+
+    def matvec_local(self, x_local, graph=True):
+        """This rank's rows of S x.  On CUDA the whole step — the plan launches of every phase
+        and the NCCL all-gather — is captured once per q into a CUDA graph and replayed."""
+        import torch
         squeeze = x_local.dim() == 1
         xl = x_local.reshape(self.nrows, -1)
         q = xl.shape[1]
         xbuf, yhat, y, send = self._work(q)
         g, ch = self.rank, self.part.chunk
         xbuf[g * ch:g * ch + self.nrows].copy_(xl)
-        self.engine.run(PH_UP_OWN, xbuf, yhat, y, q)
-        self.exchange(xbuf, send, q)
-        for ph in (PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR):
-            self.engine.run(ph, xbuf, yhat, y, q)
+        if graph and self.device.type == "cuda":
+            cg = self._graphs.get(q)
+            if cg is None:
+                self._body(q)  # warm-up outside capture (NCCL communicator, attributes)
+                torch.cuda.synchronize(self.device)
+                cg = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(cg):
+                    self._body(q)
+                self._graphs[q] = cg
+                xbuf[g * ch:g * ch + self.nrows].copy_(xl)
+            cg.replay()
+        else:
+            self._body(q)
         out = y.clone()
         return out[:, 0] if squeeze else out
 
