@@ -65,7 +65,21 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("H2B_BENCH_ONE_GPU"):  # functional test of the N > 1 flow on one GPU (gloo)
+        local = 0
     return rank, world, local
+
+
+def max_over_ranks(vals, dev):
+    """Element-wise max over ranks of a list of floats (device tensor under NCCL, host under gloo)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_initialized() and dist.get_world_size() > 1):
+        return list(vals)
+    on = dev if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor(list(vals), device=on, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.cpu()]
 
 
 def config_desc(k, pk):
@@ -331,10 +345,7 @@ def run_partitioned(a, pk, ex, rank, world, local, emit=True):
         yh = op.matvec_local(xh.to(dev, non_blocking=True)).cpu()
         t_e2e.append(time.perf_counter() - t0)
     e2e_s = float(np.mean(t_e2e))
-    t = torch.tensor([ms, e2e_s], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, e2e_s = float(t[0]), float(t[1])
+    ms, e2e_s = max_over_ranks([ms, e2e_s], dev)
     # parity: gather every rank's rows on rank 0
     yl = y.cpu().numpy()
     parts = [None] * world
@@ -388,7 +399,11 @@ def main():
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        backend = os.environ.get("H2B_BENCH_BACKEND", "nccl")  # gloo: functional tests only
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     from paper_1703_01175_b200 import H2Operator, _abi
@@ -437,10 +452,7 @@ def main():
         for _ in range(3):  # keep the device busy for a few more clock samples
             timed(mv, a.steps)
     torch.cuda.synchronize(dev)
-    if world > 1:
-        t = torch.tensor([ms, ms_warm], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms, ms_warm = float(t[0]), float(t[1])
+    ms, ms_warm = max_over_ranks([ms, ms_warm], dev)
     # parity guard on the measured output
     torch.cuda.synchronize(dev)
     yp = y.cpu().numpy()
@@ -464,10 +476,7 @@ def main():
         e2e_call()
         t_e2e.append(time.perf_counter() - t0)
     e2e_s = float(np.mean(t_e2e))
-    if world > 1:
-        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t[0])
+    e2e_s = max_over_ranks([e2e_s], dev)[0]
 
     nlaunch, mega = C.c_int64(), C.c_int64()
     _abi.check(L.h2b_query(op.handle, _abi.Q_LAUNCHES_Q1, C.byref(nlaunch)))

@@ -102,6 +102,9 @@ class DistH2Operator:
         self.engine = engine
         self._ws = {}
         self._graphs = {}
+        backend = dist.get_backend(group) if (dist.is_initialized() and self.world > 1) else "nccl"
+        self._host_staged = backend == "gloo" and self.device.type == "cuda"
+        self._graph_ok = self.device.type == "cuda" and (self.world == 1 or backend == "nccl")
 
     def _work(self, q):
         import torch
@@ -120,8 +123,27 @@ class DistH2Operator:
         if self.world == 1:
             return
         send.copy_(xbuf[g * ch:(g + 1) * ch])
+        if self._host_staged:  # gloo with device buffers (functional tests): stage on the host
+            out = torch.empty((self.world * ch,) + tuple(send.shape[1:]), dtype=send.dtype)
+            dist.all_gather_into_tensor(torch.view_as_real(out), torch.view_as_real(send.cpu()),
+                                        group=self.group)
+            xbuf[:self.world * ch].copy_(out)
+            return
         dist.all_gather_into_tensor(torch.view_as_real(xbuf[:self.world * ch]),
                                     torch.view_as_real(send), group=self.group)
+
+    def allreduce_(self, t):
+        """In-place sum over ranks of a real tensor (host-staged under gloo with CUDA tensors)."""
+        import torch.distributed as dist
+        if self.world == 1:
+            return t
+        if self._host_staged:
+            c = t.cpu()
+            dist.all_reduce(c, group=self.group)
+            t.copy_(c)
+        else:
+            dist.all_reduce(t, group=self.group)
+        return t
 
     def _body(self, q):
         """The matvec on the workspace of q columns: x slice already in the exchange buffer."""
@@ -141,7 +163,7 @@ class DistH2Operator:
         xbuf, yhat, y, send = self._work(q)
         g, ch = self.rank, self.part.chunk
         xbuf[g * ch:g * ch + self.nrows].copy_(xl)
-        if graph and self.device.type == "cuda":
+        if graph and self._graph_ok:
             cg = self._graphs.get(q)
             if cg is None:
                 self._body(q)  # warm-up outside capture (NCCL communicator, attributes)
@@ -162,8 +184,7 @@ class DistH2Operator:
         import torch
         import torch.distributed as dist
         s = (a.real * a.real + a.imag * a.imag).sum().reshape(1)
-        if self.world > 1:
-            dist.all_reduce(s, group=self.group)
+        self.allreduce_(s)
         return float(torch.sqrt(s)[0])
 
 
@@ -256,7 +277,5 @@ def _multi_dot(op, Vj, w):
     import torch.distributed as dist
     h = (Vj.conj() * w.unsqueeze(0)).sum(1)
     if op.world > 1:
-        r = torch.view_as_real(h).clone()
-        dist.all_reduce(r, group=op.group)
-        h = torch.view_as_complex(r)
+        h = torch.view_as_complex(op.allreduce_(torch.view_as_real(h).clone()))
     return h
