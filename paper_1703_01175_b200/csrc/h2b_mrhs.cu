@@ -40,11 +40,16 @@ constexpr int MM_N = 64;         // complex columns per tile
 constexpr int MM_K = 32;         // complex K per stage
 constexpr int MM_AST = 34;       // A row stride (complex): 68 doubles -> conflict-free fragments
 constexpr int MM_TST = 68;       // transposed-A row stride: 32 rows x 68 = the same 2176 elements
+constexpr int MM_CST = 65;       // epilogue tile row stride (rows 16 bytes apart in the banks)
+constexpr int MM_BST = 68;       // B row stride (complex): rows j, j+1 land 16 banks apart, so a
+                                 // half-warp's 64-bit fragment loads of two rows never collide
 constexpr int MM_STAGES = 3;
 constexpr int MM_A_ELEMS = MM_M * MM_AST;
-constexpr int MM_B_ELEMS = MM_K * MM_N;
+constexpr int MM_B_ELEMS = MM_K * MM_BST;
 constexpr int MM_STAGE_ELEMS = MM_A_ELEMS + MM_B_ELEMS;
-constexpr int MM_SMEM = 16 * MM_STAGES * MM_STAGE_ELEMS;  // 202752 bytes
+constexpr int MM_SMEM = 16 * MM_STAGES * MM_STAGE_ELEMS;
+static_assert(MM_M * MM_CST <= MM_STAGE_ELEMS, "epilogue tile must fit in stage 0");
+static_assert(MM_SMEM <= 227 * 1024, "shared memory budget");  // 202752 bytes
 
 enum : int32_t { A_V = 0, A_T, A_S, A_D, A_VT, A_TT, A_N };
 enum : int32_t { B_X = 0, B_XHAT, B_YHAT, B_N };
@@ -104,12 +109,12 @@ __device__ __forceinline__ void mm_arrive(uint64_t* bar) {
 // stage instead of thousands of 16-byte ones, so a single CTA per SM keeps enough bytes in flight.
 //   A row-major (non-trans): smem [i][j] stride MM_AST, row i = k elements of source row i
 //   A transposed (SEG_TRANS): smem [j][i] stride MM_TST, row j = m elements of source row j
-//   B: smem [r][c] stride MM_N, row r = qv elements of x / x̂ / ŷ row (contiguous or gathered)
+//   B: smem [r][c] stride MM_BST, row r = qv elements of x / x̂ / ŷ row (contiguous or gathered)
 // Shapes are not multiples of the MMA tiles, so the few pad elements the MMA reads (rows m..m4,
 // column / row k when k is odd, columns qv..q8) are zeroed by the consumer after the copies land
 // (they are disjoint from the copied bytes).
 __device__ __forceinline__ void issue_seg(const MmSeg& s, const MmBufs& bf, int m, int q, int col0, int qv,
-                                          double2* st, uint64_t* bar) {
+                                          double2* st, uint64_t* bar, int64_t brow) {
   const int lane = threadIdx.x & 31;
   const double2* A = pick_a(bf, s.flags & 15) + s.a_off;
   const double2* B = pick_b(bf, (s.flags >> 4) & 15);
@@ -125,10 +130,14 @@ __device__ __forceinline__ void issue_seg(const MmSeg& s, const MmBufs& bf, int 
   double2* Bs = st + MM_A_ELEMS;
   for (int r = lane; r < na; r += 32)
     bulk_g2s(As + r * (trans ? MM_TST : MM_AST), A + (int64_t)r * s.lda, 16u * la, bar);
-  for (int r = lane; r < s.k; r += 32) {
-    const int64_t row = (s.flags & SEG_GATHER) ? (int64_t)__ldg(bf.gather + s.b_row + r) : s.b_row + r;
-    bulk_g2s(Bs + r * MM_N, B + row * q + col0, 16u * qv, bar);
-  }
+  if (lane < s.k) bulk_g2s(Bs + lane * MM_BST, B + brow * q + col0, 16u * qv, bar);  // k <= 32
+}
+
+// B row of this lane for a segment (gather index or contiguous row), loaded by the producer
+// before it waits for the stage to drain, so the index latency overlaps the wait
+__device__ __forceinline__ int64_t seg_brow(const MmSeg& s, const MmBufs& bf, int lane) {
+  if (lane >= s.k) return 0;
+  return (s.flags & SEG_GATHER) ? (int64_t)__ldg(bf.gather + s.b_row + lane) : s.b_row + lane;
 }
 
 __device__ __forceinline__ void zero_pads(const MmSeg& s, int m, int qv, double2* st, int lane) {
@@ -147,10 +156,10 @@ __device__ __forceinline__ void zero_pads(const MmSeg& s, int m, int qv, double2
   // B: columns qv..q8 of rows < k2; row k (odd k) for columns < qv
   for (int e = lane; e < (q8 - qv) * k2; e += 32) {
     const int r = e / (q8 - qv), c = qv + e % (q8 - qv);
-    Bs[r * MM_N + c] = z;
+    Bs[r * MM_BST + c] = z;
   }
   if (k & 1)
-    for (int c = lane; c < qv; c += 32) Bs[k * MM_N + c] = z;
+    for (int c = lane; c < qv; c += 32) Bs[k * MM_BST + c] = z;
 }
 
 // One staged chunk: nks k4-steps of NU 8x8 tiles per warp (A fragment: B_rᵀ, shared by the NU
@@ -162,7 +171,7 @@ __device__ __forceinline__ void mma_chunk(double (&acc)[MM_TPW][2], const double
 #pragma unroll 2
   for (int ks = 0; ks < nks; ++ks) {
     const int j = ks * 2 + jo;
-    const double af = Bs[j * (2 * MM_N) + a_off];
+    const double af = Bs[j * (2 * MM_BST) + a_off];
     const double* bp = bq + j * sj;
     double bv[NU];
 #pragma unroll
@@ -225,15 +234,16 @@ __global__ void __launch_bounds__(MM_THREADS, 1) k_zgemm_grouped(const MmItem* _
     // producer: wait until the buffer's previous chunk is consumed, zero its pads, copy
     for (int s = 0; s < ns; ++s) {
       const int buf = s % MM_STAGES;
-      if (s >= MM_STAGES) mbar_wait(&empty[buf], (uint32_t)(s / MM_STAGES - 1) & 1u);
       const MmSeg sg = segs[it.seg0 + s];
+      const int64_t brow = seg_brow(sg, bf, lane);  // in flight while we wait for the stage
+      if (s >= MM_STAGES) mbar_wait(&empty[buf], (uint32_t)(s / MM_STAGES - 1) & 1u);
       double2* st = sm + buf * MM_STAGE_ELEMS;
       zero_pads(sg, it.m, qv, st, lane);
       __syncwarp();
       // order the generic-proxy pad stores (this chunk's and the buffer's earlier ones) before
       // the async-proxy TMA writes into the same buffer
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_seg(sg, bf, it.m, q, col0, qv, st, &full[buf]);  // lane 0 arrives (release) first
+      issue_seg(sg, bf, it.m, q, col0, qv, st, &full[buf], brow);  // lane 0 arrives first
     }
   } else {
     for (int s = 0; s < ns; ++s) {
@@ -268,7 +278,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) k_zgemm_grouped(const MmItem* _
 #pragma unroll
     for (int u = 0; u < MM_TPW; ++u) {
       if (u >= nu) break;
-      Cs[((ng + G * u) * 4 + kk) * MM_N + c] = make_double2(acc[u][0], acc[u][1]);
+      Cs[((ng + G * u) * 4 + kk) * MM_CST + c] = make_double2(acc[u][0], acc[u][1]);
     }
   }
   __syncthreads();
@@ -279,7 +289,7 @@ __global__ void __launch_bounds__(MM_THREADS, 1) k_zgemm_grouped(const MmItem* _
     const int i = e >> 6, c = e & (MM_N - 1);
     if (c >= qv) continue;
     double2* o = C + (it.c_row + i) * q + col0 + c;
-    const double2 v = Cs[i * MM_N + c];
+    const double2 v = Cs[i * MM_CST + c];
     *o = accum ? cadd(*o, v) : v;
   }
   // the next CTA on this SM fills the same shared memory with TMA: order this CTA's generic
