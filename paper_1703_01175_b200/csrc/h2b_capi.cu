@@ -46,6 +46,7 @@ void free_ctx(h2b_ctx* h) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->far_stream) cudaStreamDestroy(h->far_stream);
+  if (h->host_stream) cudaStreamDestroy(h->host_stream);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   delete h;
@@ -218,6 +219,17 @@ int h2b_matvec_perm(h2b_handle h, const void* x_perm, void* y_perm, int q, void*
   return h2b_run_matvec(h, (const double2*)x_perm, (double2*)y_perm, q, (cudaStream_t)stream);
 }
 
+namespace {
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+}  // namespace
+
 int h2b_matvec_host(h2b_handle h, const void* x, void* y, int q) {
   int rc = ready(h);
   if (rc) return rc;
@@ -226,6 +238,7 @@ int h2b_matvec_host(h2b_handle h, const void* x, void* y, int q) {
   H2B_CUDA_TRY(cudaSetDevice(h->device));
   const size_t bytes = (size_t)16 * h->n * q;
   if (h->hws_q < q) {
+    h2b_release_graphs(h);  // host-path graphs hold the staging pointers
     if (h->hxp) cudaFree(h->hxp);
     if (h->hyp) cudaFree(h->hyp);
     h->hxp = h->hyp = nullptr;
@@ -234,16 +247,55 @@ int h2b_matvec_host(h2b_handle h, const void* x, void* y, int q) {
     H2B_CUDA_TRY(cudaMalloc(&h->hyp, 2 * bytes));
     h->hws_q = q;
   }
+  if (!h->host_stream) H2B_CUDA_TRY(cudaStreamCreateWithFlags(&h->host_stream, cudaStreamNonBlocking));
   double2* dx = h->hxp;                  // original order
   double2* dxp = h->hxp + h->n * q;      // permuted
   double2* dyp = h->hyp;                 // permuted
   double2* dy = h->hyp + h->n * q;       // original order
-  cudaStream_t st = 0;
-  H2B_CUDA_TRY(cudaMemcpyAsync(dx, x, bytes, cudaMemcpyHostToDevice, st));
-  if ((rc = h2b_launch_gather(h->perm, h->n, dx, dxp, q, st))) return rc;
-  if ((rc = h2b_run_matvec(h, dxp, dyp, q, st))) return rc;
-  if ((rc = h2b_launch_scatter(h->perm, h->n, dyp, dy, q, st))) return rc;
-  H2B_CUDA_TRY(cudaMemcpyAsync(y, dy, bytes, cudaMemcpyDeviceToHost, st));
+  cudaStream_t st = h->host_stream;
+  auto enqueue = [&](cudaStream_t s, bool in_graph) -> int {
+    H2B_CUDA_TRY(cudaMemcpyAsync(dx, x, bytes, cudaMemcpyHostToDevice, s));
+    int r = h2b_launch_gather(h->perm, h->n, dx, dxp, q, s);
+    if (!r) {
+      int nl = 0;
+      r = in_graph ? h2b_enqueue_matvec(h, dxp, dyp, q, s, &nl) : h2b_run_matvec(h, dxp, dyp, q, s);
+    }
+    if (!r) r = h2b_launch_scatter(h->perm, h->n, dyp, dy, q, s);
+    if (r) return r;
+    H2B_CUDA_TRY(cudaMemcpyAsync(y, dy, bytes, cudaMemcpyDeviceToHost, s));
+    return H2B_OK;
+  };
+  if (h->use_graphs && is_pinned(x) && is_pinned(y)) {
+    // pinned host buffers: the whole call (H2D, gather, matvec, scatter, D2H) is one graph
+    H2B_TRY(h2b_prepare(h));
+    H2B_TRY(h2b_ensure_workspace(h, q));
+    if (q >= 2 && h->use_mrhs) H2B_TRY(h2b_mrhs_prepare(h));
+    const GraphKey key{x, y, -q};  // negative q: host-path graph
+    auto it = h->graphs.find(key);
+    if (it == h->graphs.end()) {
+      cudaStream_t cs = nullptr;
+      H2B_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      H2B_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      rc = enqueue(cs, true);
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamEndCapture(cs, &g);
+      cudaStreamDestroy(cs);
+      if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      REQUIRE(e == cudaSuccess, H2B_ECUDA, std::string("host-path capture: ") + cudaGetErrorString(e));
+      cudaGraphExec_t ex = nullptr;
+      e = cudaGraphInstantiate(&ex, g, 0);
+      cudaGraphDestroy(g);
+      REQUIRE(e == cudaSuccess, H2B_ECUDA, std::string("host-path instantiate: ") + cudaGetErrorString(e));
+      if (h->graphs.size() >= 64) h2b_release_graphs(h);
+      it = h->graphs.emplace(key, ex).first;
+    }
+    H2B_CUDA_TRY(cudaGraphLaunch(it->second, st));
+  } else {
+    H2B_TRY(enqueue(st, false));
+  }
   H2B_CUDA_TRY(cudaStreamSynchronize(st));
   return H2B_OK;
 }

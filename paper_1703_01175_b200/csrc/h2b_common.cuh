@@ -301,6 +301,7 @@ struct h2b_ctx {
   int64_t hws_q = 0;
   // streams / events / graphs
   cudaStream_t far_stream = nullptr;
+  cudaStream_t host_stream = nullptr;  // h2b_matvec_host
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   std::map<GmresKey, cudaGraphExec_t> gmres_graphs;  // per-step graphs of h2b_gmres
