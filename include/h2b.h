@@ -218,7 +218,7 @@ int h2b_zaxpby(int64_t n, double ar, double ai, const void* x, double br, double
  *   seg:  A = payload[a_src][a_off + i*lda + j] (i < m, j < k <= 32),
  *         B row j = (b_src buffer)[b_row + j]
  * flags: seg  = a_src | b_src << 4 (b_src 0 x, 1 xhat, 2 yhat)
- *        item = dst (0 x, 1 xhat, 2 yhat, 3 y) | 256 (accumulate)
+ *        item = dst (0 x, 1 xhat, 2 yhat, 3 y) | 256 (accumulate) | 512 (broadcast to peers)
  * --------------------------------------------------------------------- */
 typedef struct h2b_mm_item {
   int64_t c_row;
@@ -241,6 +241,25 @@ int h2b_plan_set_phase(h2b_plan_handle p, int phase, int n_launches, const int64
 int h2b_plan_run(h2b_plan_handle p, int phase, const void* x, const void* xhat, void* yhat, void* y,
                  int q, void* stream);
 int h2b_plan_destroy(h2b_plan_handle p);
+/* Fused exchange over peer memory (NVLink P2P stores): items flagged 512 (broadcast) store
+ * their rows into the local buffer AND into every peer's buffer at the same rows (the all-gather
+ * of x̂ fused into the kernel that produces it); h2b_plan_bcast_rows pushes this rank's x rows
+ * [row0, row0 + nrows) of `buf` the same way.  Peers are the other ranks' exchange buffers,
+ * mapped with h2b_ipc_open (or any device pointers this device can store to).  The caller
+ * orders the peers' next phase after these stores (e.g. a barrier collective). */
+int h2b_plan_set_peers(h2b_plan_handle p, void* const* peer_bufs, int npeers);
+int h2b_plan_bcast_rows(h2b_plan_handle p, const void* buf, int64_t row0, int64_t nrows, int q,
+                        void* stream);
+/* Element offset added to every peer pointer by subsequent runs / broadcasts (alternating
+ * exchange buffers inside one allocation). */
+int h2b_plan_set_peer_offset(h2b_plan_handle p, int64_t elems);
+/* Plain device allocations (exchange buffers to be shared with CUDA IPC), zero-filled. */
+int h2b_device_alloc(int device, size_t bytes, void** out);
+int h2b_device_free(void* ptr);
+/* CUDA IPC of a device buffer between the ranks' processes (64-byte handle). */
+int h2b_ipc_get_handle(const void* dev_ptr, void* handle_out);
+int h2b_ipc_open(const void* handle, void** dev_ptr_out);
+int h2b_ipc_close(void* dev_ptr);
 int64_t h2b_plan_device_bytes(h2b_plan_handle p);
 
 #ifdef __cplusplus

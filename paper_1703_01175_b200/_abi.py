@@ -22,7 +22,9 @@ EXPORTED = (
     "h2b_zdotc_multi", "h2b_zgemv_sub", "h2b_zaxpby", "h2b_matvec_phase",
     "h2b_prepare_handle", "h2b_set_option", "h2b_query", "h2b_get_trace",
     "h2b_plan_create", "h2b_plan_upload", "h2b_plan_set_phase", "h2b_plan_run",
-    "h2b_plan_destroy", "h2b_plan_device_bytes", "h2b_assemble_near",
+    "h2b_plan_destroy", "h2b_plan_device_bytes", "h2b_assemble_near", "h2b_plan_set_peers",
+    "h2b_plan_bcast_rows", "h2b_ipc_get_handle", "h2b_ipc_open", "h2b_ipc_close",
+    "h2b_plan_set_peer_offset", "h2b_device_alloc", "h2b_device_free",
 )
 OPT_GRAPHS, OPT_MEGA, OPT_TRACE, OPT_DEBUG, OPT_MRHS = 1, 2, 3, 4, 5
 Q_LAUNCHES_Q1, Q_SPAN_MODE, Q_SPLIT_LEVEL, Q_TOP_STAGED, Q_DEVICE_BYTES = 1, 2, 3, 4, 5
@@ -61,7 +63,7 @@ MM_ITEM = _np.dtype([("c_row", "<i8"), ("m", "<i4"), ("seg0", "<i4"), ("nseg", "
 MM_SEG = _np.dtype([("a_off", "<i8"), ("b_row", "<i8"), ("k", "<i4"), ("lda", "<i4"),
                     ("flags", "<i4"), ("pad", "<i4")])
 B_X, B_XHAT, B_YHAT, B_Y = 0, 1, 2, 3
-ITEM_ACC = 256
+ITEM_ACC, ITEM_BCAST = 256, 512
 
 
 class H2BError(RuntimeError):
@@ -115,6 +117,14 @@ def lib():
     L.h2b_plan_set_phase.argtypes = [vp, C.c_int, C.c_int, _i64p, vp, C.c_int64, vp, C.c_int64]
     L.h2b_plan_run.argtypes = [vp, C.c_int, vp, vp, vp, vp, C.c_int, vp]
     L.h2b_plan_destroy.argtypes = [vp]
+    L.h2b_plan_set_peers.argtypes = [vp, C.POINTER(vp), C.c_int]
+    L.h2b_plan_bcast_rows.argtypes = [vp, vp, C.c_int64, C.c_int64, C.c_int, vp]
+    L.h2b_ipc_get_handle.argtypes = [vp, vp]
+    L.h2b_ipc_open.argtypes = [vp, C.POINTER(vp)]
+    L.h2b_ipc_close.argtypes = [vp]
+    L.h2b_plan_set_peer_offset.argtypes = [vp, C.c_int64]
+    L.h2b_device_alloc.argtypes = [C.c_int, C.c_size_t, C.POINTER(vp)]
+    L.h2b_device_free.argtypes = [vp]
     L.h2b_plan_device_bytes.argtypes = [vp]
     L.h2b_plan_device_bytes.restype = C.c_int64
     _lib = L

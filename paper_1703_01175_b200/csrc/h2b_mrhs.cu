@@ -26,6 +26,7 @@
 // interleaved complex layout in shared memory; each lane's fragment load picks re/im and
 // flips the sign bit (lane-constant), so no real expansion is ever stored.
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 #include "h2b_common.cuh"
@@ -56,6 +57,8 @@ enum : int32_t { B_X = 0, B_XHAT, B_YHAT, B_N };
 constexpr int SEG_TRANS = 1 << 8;   // A[i][j] = src[a_off + j*lda + i]
 constexpr int SEG_GATHER = 1 << 9;  // B row r = gather[b_row + r]
 constexpr int ITEM_ACC = 1 << 8;
+constexpr int ITEM_BCAST = 1 << 9;  // also store the result into every peer's buffer (same rows)
+constexpr int MAX_PEERS = 8;
 
 struct MmSeg {
   int64_t a_off;   // element offset of A(0,0) in its source
@@ -76,7 +79,22 @@ struct MmBufs {
   double2* b[B_N];   // also the destinations (x̂, ŷ; y passed separately)
   double2* y;
   const int32_t* gather;
+  double2* peers[MAX_PEERS];  // other ranks' exchange buffers (P2P-mapped), for ITEM_BCAST
+  int npeers;
 };
+
+// the epilogue store of one output element: local (overwrite / accumulate) and, for
+// ITEM_BCAST items, the same element of every peer's exchange buffer (NVLink P2P stores: the
+// all-gather of x̂ fused into the producing kernel)
+__device__ __forceinline__ void store_out(const MmBufs& bf, double2* C, int flags, int64_t idx, double2 v) {
+  double2* o = C + idx;
+  const double2 r = (flags & ITEM_ACC) ? cadd(*o, v) : v;
+  *o = r;
+  if (flags & ITEM_BCAST) {
+#pragma unroll 1
+    for (int p = 0; p < bf.npeers; ++p) bf.peers[p][idx] = r;
+  }
+}
 
 // buffer selection by id without dynamic indexing of the parameter block (which would spill it
 // to local memory)
@@ -284,14 +302,12 @@ __global__ void __launch_bounds__(MM_THREADS, 1) k_zgemm_grouped(const MmItem* _
   __syncthreads();
   const int dst_id = it.flags & 15;
   double2* C = pick_b(bf, dst_id);
-  const bool accum = it.flags & ITEM_ACC;
   for (int e = threadIdx.x; e < it.m * MM_N; e += MM_THREADS) {
     const int i = e >> 6, c = e & (MM_N - 1);
     if (c >= qv) continue;
-    double2* o = C + (it.c_row + i) * q + col0 + c;
-    const double2 v = Cs[i * MM_CST + c];
-    *o = accum ? cadd(*o, v) : v;
+    store_out(bf, C, it.flags, (it.c_row + i) * q + col0 + c, Cs[i * MM_CST + c]);
   }
+  if (it.flags & ITEM_BCAST) __threadfence_system();
   // the next CTA on this SM fills the same shared memory with TMA: order this CTA's generic
   // stores (epilogue tile, pads) before any async-proxy write
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -364,8 +380,8 @@ __global__ void __launch_bounds__(MV_THREADS, 1) k_zgemv_grouped(const MmItem* _
     double2 v = red[0][r];
 #pragma unroll
     for (int gg = 1; gg < 8; ++gg) v = cadd(v, red[gg][r]);
-    double2* o = pick_b(bf, it.flags & 15) + it.c_row + r;
-    *o = (it.flags & ITEM_ACC) ? cadd(*o, v) : v;
+    store_out(bf, pick_b(bf, it.flags & 15), it.flags, it.c_row + r, v);
+    if (it.flags & ITEM_BCAST) __threadfence_system();
   }
 }
 
@@ -586,6 +602,10 @@ struct h2b_plan_ctx {
   };
   std::vector<Phase> phases;
   int64_t device_bytes = 0;
+  double2* peers[MAX_PEERS] = {};
+  double2** dpeers = nullptr;  // device copy of `peers`
+  int npeers = 0;
+  int64_t peer_off = 0;        // element offset added to every peer pointer (ping-pong buffers)
 };
 
 extern "C" int h2b_plan_create(int device, int n_payloads, const int64_t* payload_elems,
@@ -645,7 +665,7 @@ extern "C" int h2b_plan_set_phase(h2b_plan_handle p, int phase, int n_launches, 
   for (int64_t i = 0; i < n_items; ++i) {  // validate references (the kernel trusts them)
     const h2b_mm_item& it = items[i];
     if (it.m < 0 || it.m > MM_M || it.seg0 < 0 || it.nseg < 0 || it.seg0 + (int64_t)it.nseg > n_segs ||
-        (it.flags & 15) > B_N) {
+        (it.flags & 15) > B_N || (it.flags & ~(15 | ITEM_ACC | ITEM_BCAST))) {
       h2b_set_error("h2b_plan_set_phase: item " + std::to_string(i) + " out of range");
       return H2B_EINVAL;
     }
@@ -702,10 +722,107 @@ extern "C" int h2b_plan_run(h2b_plan_handle p, int phase, const void* x, const v
   bf.b[B_YHAT] = (double2*)yhat;
   bf.y = (double2*)y;
   bf.gather = nullptr;
+  for (int i = 0; i < p->npeers; ++i) bf.peers[i] = p->peers[i] + p->peer_off;
+  bf.npeers = p->npeers;
   const auto& ph = p->phases[phase];
   int nl = 0;
   for (const int2& L : ph.launches)
     H2B_TRY(run_grouped(ph.items + L.x, L.y, ph.segs, bf, q, (cudaStream_t)stream, &nl));
+  return H2B_OK;
+}
+
+namespace {
+// rows [r0, r0 + nrows) of `src` (q columns) into `dst` at the same rows, for every peer
+__global__ void k_bcast_rows(const double2* __restrict__ src, int64_t off, int64_t n,
+                             double2* const* __restrict__ peers, int np, int64_t peer_off) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = src[off + e];
+    for (int p = 0; p < np; ++p) peers[p][peer_off + off + e] = v;
+  }
+  __threadfence_system();
+}
+}  // namespace
+
+extern "C" int h2b_plan_set_peers(h2b_plan_handle p, void* const* peer_bufs, int npeers) {
+  if (!p || npeers < 0 || npeers > MAX_PEERS || (npeers && !peer_bufs)) {
+    h2b_set_error("h2b_plan_set_peers: bad arguments (at most 8 peers)");
+    return H2B_EINVAL;
+  }
+  H2B_CUDA_TRY(cudaSetDevice(p->device));
+  for (int i = 0; i < npeers; ++i) p->peers[i] = (double2*)peer_bufs[i];
+  p->npeers = npeers;
+  if (!p->dpeers) H2B_CUDA_TRY(cudaMalloc(&p->dpeers, sizeof(double2*) * MAX_PEERS));
+  if (npeers)  // device copy of the table for k_bcast_rows (set once, outside any capture)
+    H2B_CUDA_TRY(cudaMemcpy(p->dpeers, p->peers, sizeof(double2*) * npeers, cudaMemcpyHostToDevice));
+  return H2B_OK;
+}
+
+extern "C" int h2b_plan_bcast_rows(h2b_plan_handle p, const void* buf, int64_t row0, int64_t nrows, int q,
+                                   void* stream) {
+  if (!p || !buf || row0 < 0 || nrows < 0 || q < 1) {
+    h2b_set_error("h2b_plan_bcast_rows: bad arguments");
+    return H2B_EINVAL;
+  }
+  if (p->npeers == 0 || nrows == 0) return H2B_OK;
+  const int64_t n = nrows * q;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  k_bcast_rows<<<grid, 256, 0, (cudaStream_t)stream>>>((const double2*)buf, row0 * q, n, p->dpeers, p->npeers,
+                                                        p->peer_off);
+  H2B_CHECK_LAUNCH();
+  return H2B_OK;
+}
+
+extern "C" int h2b_plan_set_peer_offset(h2b_plan_handle p, int64_t elems) {
+  if (!p || elems < 0) {
+    h2b_set_error("h2b_plan_set_peer_offset: bad arguments");
+    return H2B_EINVAL;
+  }
+  p->peer_off = elems;
+  return H2B_OK;
+}
+
+// raw device allocations (exchange buffers that are shared with CUDA IPC)
+extern "C" int h2b_device_alloc(int device, size_t bytes, void** out) {
+  if (!out) {
+    h2b_set_error("h2b_device_alloc: null argument");
+    return H2B_EINVAL;
+  }
+  H2B_CUDA_TRY(cudaSetDevice(device));
+  H2B_CUDA_TRY(cudaMalloc(out, std::max<size_t>(bytes, 16)));
+  H2B_CUDA_TRY(cudaMemset(*out, 0, std::max<size_t>(bytes, 16)));
+  return H2B_OK;
+}
+
+extern "C" int h2b_device_free(void* ptr) {
+  if (ptr) H2B_CUDA_TRY(cudaFree(ptr));
+  return H2B_OK;
+}
+
+// CUDA IPC of an exchange buffer between the ranks' processes (one process per GPU)
+extern "C" int h2b_ipc_get_handle(const void* dev_ptr, void* handle_out /* 64 bytes */) {
+  if (!dev_ptr || !handle_out) {
+    h2b_set_error("h2b_ipc_get_handle: null argument");
+    return H2B_EINVAL;
+  }
+  cudaIpcMemHandle_t hd;
+  H2B_CUDA_TRY(cudaIpcGetMemHandle(&hd, const_cast<void*>(dev_ptr)));
+  memcpy(handle_out, &hd, sizeof(hd));
+  return H2B_OK;
+}
+
+extern "C" int h2b_ipc_open(const void* handle, void** dev_ptr_out) {
+  if (!handle || !dev_ptr_out) {
+    h2b_set_error("h2b_ipc_open: null argument");
+    return H2B_EINVAL;
+  }
+  cudaIpcMemHandle_t hd;
+  memcpy(&hd, handle, sizeof(hd));
+  H2B_CUDA_TRY(cudaIpcOpenMemHandle(dev_ptr_out, hd, cudaIpcMemLazyEnablePeerAccess));
+  return H2B_OK;
+}
+
+extern "C" int h2b_ipc_close(void* dev_ptr) {
+  if (dev_ptr) H2B_CUDA_TRY(cudaIpcCloseMemHandle(dev_ptr));
   return H2B_OK;
 }
 
@@ -717,6 +834,7 @@ extern "C" int h2b_plan_destroy(h2b_plan_handle p) {
     cudaFree(ph.segs);
   }
   for (int i = 0; i < p->n_payloads; ++i) cudaFree(p->pay[i]);
+  if (p->dpeers) cudaFree(p->dpeers);
   delete p;
   return H2B_OK;
 }

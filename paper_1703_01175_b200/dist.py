@@ -52,6 +52,17 @@ class CudaPlanEngine:
                                             items.ctypes.data, int(items.size), segs.ctypes.data,
                                             int(segs.size)), "h2b_plan_set_phase")
 
+    def set_peers(self, ptrs):
+        arr = (C.c_void_p * max(1, len(ptrs)))(*ptrs)
+        _abi.check(_abi.lib().h2b_plan_set_peers(self.handle, arr, len(ptrs)), "h2b_plan_set_peers")
+
+    def bcast_rows(self, buf, row0, nrows, q, stream=None):
+        torch = __import__("torch")
+        st = torch.cuda.current_stream(self.device) if stream is None else stream
+        _abi.check(_abi.lib().h2b_plan_bcast_rows(self.handle, C.c_void_p(buf.data_ptr()), int(row0),
+                                                  int(nrows), int(q), C.c_void_p(st.cuda_stream)),
+                   "h2b_plan_bcast_rows")
+
     def run(self, phase, xbuf, yhat, y, q, stream=None):
         torch = __import__("torch")
         st = torch.cuda.current_stream(self.device) if stream is None else stream  # (capturing)
@@ -77,9 +88,15 @@ class DistH2Operator:
     returns its rows of y = S x.  Collective: every rank must call it.
     """
 
-    def __init__(self, pk, group=None, device=None, engine=None, rank=None, world=None):
+    def __init__(self, pk, group=None, device=None, engine=None, rank=None, world=None,
+                 exchange="auto"):
         """``engine``: None (libh2b on ``device`` / the current CUDA device) or a factory
-        ``plan -> engine`` (the CPU tests pass the plan interpreter)."""
+        ``plan -> engine`` (the CPU tests pass the plan interpreter).
+
+        ``exchange``: "p2p" — the x̂ all-gather fused into the UP_OWN kernels, which store into
+        every rank's exchange buffer over NVLink (CUDA IPC mappings), then one barrier collective;
+        "allgather" — one NCCL all-gather of the exchange buffer; "auto" — p2p when every pair
+        of GPUs has peer access under NCCL, else allgather."""
         import torch
         import torch.distributed as dist
         self.group = group
@@ -89,7 +106,14 @@ class DistH2Operator:
             rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.rank, self.world = int(rank), int(world)
         self.part = partition(pk, self.world)
-        self.plan = plan_shard(pk, self.world, self.rank, self.part)
+        backend = dist.get_backend(group) if (dist.is_initialized() and self.world > 1) else "nccl"
+        want_p2p = (exchange in ("auto", "p2p") and engine is None and self.world > 1
+                    and backend == "nccl")
+        if want_p2p and exchange == "auto":
+            want_p2p = _peer_access_everywhere(group, torch.cuda.current_device() if device is None
+                                               else int(device), self.world)
+        self.exchange_mode = "p2p" if want_p2p else "allgather"
+        self.plan = plan_shard(pk, self.world, self.rank, self.part, bcast=want_p2p)
         self.n = int(pk.n)
         self.row0, self.nrows = self.plan.row0, self.plan.nrows
         if engine is None:
@@ -105,14 +129,47 @@ class DistH2Operator:
         backend = dist.get_backend(group) if (dist.is_initialized() and self.world > 1) else "nccl"
         self._host_staged = backend == "gloo" and self.device.type == "cuda"
         self._graph_ok = self.device.type == "cuda" and (self.world == 1 or backend == "nccl")
+        self._slot = 0
+        self._p2p = {}  # q -> (raw allocation, two exchange-buffer views, opened peer pointers)
 
     def _work(self, q):
         import torch
         if q not in self._ws:
             z = lambda r: torch.zeros((r, q), dtype=torch.complex128, device=self.device)  # noqa: E731
-            self._ws[q] = (z(self.part.xlen), z(self.part.xlen), z(self.nrows),
-                           z(self.part.chunk))
-        return self._ws[q]
+            xb = self._p2p_buffers(q)[self._slot] if self.exchange_mode == "p2p" else z(self.part.xlen)
+            self._ws[q] = (xb, z(self.part.xlen), z(self.nrows), z(self.part.chunk))
+        ws = self._ws[q]
+        if self.exchange_mode == "p2p":  # alternate exchange buffers between matvecs
+            ws = (self._p2p_buffers(q)[self._slot],) + ws[1:]
+        return ws
+
+    def _p2p_buffers(self, q):
+        """Two exchange buffers in one IPC-shared allocation; peers mapped once per q."""
+        if q not in self._p2p:
+            import torch
+            import torch.distributed as dist
+            L = _abi.lib()
+            elems = self.part.xlen * q
+            raw = C.c_void_p()
+            _abi.check(L.h2b_device_alloc(int(self.device.index), 32 * elems, C.byref(raw)),
+                       "h2b_device_alloc")
+            hd = (C.c_char * 64)()
+            _abi.check(L.h2b_ipc_get_handle(raw, hd), "h2b_ipc_get_handle")
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(hd), group=self.group)
+            peers = []
+            for r in range(self.world):
+                if r == self.rank:
+                    continue
+                ptr = C.c_void_p()
+                buf = (C.c_char * 64).from_buffer_copy(handles[r])
+                _abi.check(L.h2b_ipc_open(buf, C.byref(ptr)), "h2b_ipc_open")
+                peers.append(ptr.value)
+            self.engine.set_peers(peers)
+            views = [_device_view(raw.value + 16 * elems * b, (self.part.xlen, q), self.device)
+                     for b in range(2)]
+            self._p2p[q] = (raw, views, peers)
+        return self._p2p[q][1]
 
     def exchange(self, xbuf, send, q):
         """All-gather of every rank's chunk (x slice + own x̂) into the exchange buffer."""
@@ -148,8 +205,18 @@ class DistH2Operator:
     def _body(self, q):
         """The matvec on the workspace of q columns: x slice already in the exchange buffer."""
         xbuf, yhat, y, send = self._work(q)
-        self.engine.run(PH_UP_OWN, xbuf, yhat, y, q)
-        self.exchange(xbuf, send, q)
+        if self.exchange_mode == "p2p":
+            # fused exchange: x rows pushed to every peer, x̂ stored to every peer by the UP_OWN
+            # epilogues; one barrier collective orders the peers' next phase after the stores
+            _abi.check(_abi.lib().h2b_plan_set_peer_offset(self.engine.handle,
+                                                           self._slot * self.part.xlen * q),
+                       "h2b_plan_set_peer_offset")
+            self.engine.bcast_rows(xbuf, self.rank * self.part.chunk, self.nrows, q)
+            self.engine.run(PH_UP_OWN, xbuf, yhat, y, q)
+            self._barrier()
+        else:
+            self.engine.run(PH_UP_OWN, xbuf, yhat, y, q)
+            self.exchange(xbuf, send, q)
         for ph in (PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR):
             self.engine.run(ph, xbuf, yhat, y, q)
 
@@ -164,20 +231,31 @@ class DistH2Operator:
         g, ch = self.rank, self.part.chunk
         xbuf[g * ch:g * ch + self.nrows].copy_(xl)
         if graph and self._graph_ok:
-            cg = self._graphs.get(q)
+            key = (q, self._slot)
+            cg = self._graphs.get(key)
             if cg is None:
                 self._body(q)  # warm-up outside capture (NCCL communicator, attributes)
                 torch.cuda.synchronize(self.device)
                 cg = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(cg):
                     self._body(q)
-                self._graphs[q] = cg
+                self._graphs[key] = cg
                 xbuf[g * ch:g * ch + self.nrows].copy_(xl)
             cg.replay()
         else:
             self._body(q)
         out = y.clone()
+        if self.exchange_mode == "p2p":
+            self._slot ^= 1
         return out[:, 0] if squeeze else out
+
+    def _barrier(self):
+        """Stream-ordered barrier collective (NCCL all-reduce of one element)."""
+        import torch
+        import torch.distributed as dist
+        if not hasattr(self, "_bar"):
+            self._bar = torch.zeros(1, dtype=torch.float32, device=self.device)
+        dist.all_reduce(self._bar, group=self.group)
 
     # ---- Krylov helper: global 2-norm over the row slices -------------------------
     def norm(self, a):
@@ -186,6 +264,36 @@ class DistH2Operator:
         s = (a.real * a.real + a.imag * a.imag).sum().reshape(1)
         self.allreduce_(s)
         return float(torch.sqrt(s)[0])
+
+
+class _CudaArray:
+    """__cuda_array_interface__ wrapper so torch can view a raw libh2b allocation."""
+
+    def __init__(self, ptr, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape) + (2,), "typestr": "<f8",
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def _device_view(ptr, shape, device):
+    import torch
+    with torch.cuda.device(device):
+        t = torch.as_tensor(_CudaArray(ptr, shape), device=device)
+    return torch.view_as_complex(t)
+
+
+def _peer_access_everywhere(group, dev, world):
+    """True when this rank's GPU can store to every other rank's GPU (NVLink / NVSwitch)."""
+    import torch
+    import torch.distributed as dist
+    devs = [None] * world
+    props = torch.cuda.get_device_properties(dev)
+    dist.all_gather_object(devs, (str(getattr(props, "uuid", dev)), dev), group=group)
+    if len({d[0] for d in devs}) < world:
+        return False  # two ranks on one GPU: no IPC peer mapping
+    ok = all(torch.cuda.can_device_access_peer(dev, d[1]) for d in devs if d[1] != dev)
+    flags = [None] * world
+    dist.all_gather_object(flags, bool(ok), group=group)
+    return all(flags)
 
 
 def _givens(a, b):

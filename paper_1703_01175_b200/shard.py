@@ -39,7 +39,7 @@ PHASES = (PH_UP_OWN, PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR)
 PAY_VT, PAY_TT, PAY_T, PAY_S, PAY_D, PAY_V = 0, 1, 2, 3, 4, 5
 N_PAY = 6
 B_X, B_XHAT, B_YHAT, B_Y = 0, 1, 2, 3
-ITEM_ACC = 256
+ITEM_ACC, ITEM_BCAST = 256, 512
 
 
 @dataclass
@@ -149,8 +149,12 @@ class _Builder:
                 np.array(self.items, dtype=self._it), np.array(self.segs, dtype=self._sg))
 
 
-def plan_shard(pk, G: int, g: int, part: Partition | None = None) -> ShardPlan:
-    """Payloads and work lists of rank g of G (see the module docstring)."""
+def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = False) -> ShardPlan:
+    """Payloads and work lists of rank g of G (see the module docstring).
+
+    ``bcast``: the UP_OWN items also store their x̂ rows into every peer's exchange buffer
+    (P2P stores over NVLink, libh2b ITEM_BCAST) — the all-gather of x̂ fused into the kernel that
+    computes it; the x slice is pushed by ``h2b_plan_bcast_rows``."""
     part = part or partition(pk, G)
     if not 0 <= g < G:
         raise ValueError("rank out of range")
@@ -211,6 +215,8 @@ def plan_shard(pk, G: int, g: int, part: Partition | None = None) -> ShardPlan:
     Bd = _Builder()
     up(Bd, range(pk.depth - 1, part.p - 1, -1), own)
     phases[PH_UP_OWN] = Bd.done()
+    if bcast:
+        phases[PH_UP_OWN][1]["flags"] |= ITEM_BCAST
     Bd = _Builder()
     up(Bd, range(part.p - 1, -1, -1), top)
     phases[PH_UP_TOP] = Bd.done()

@@ -86,3 +86,69 @@ def test_dist_operator_single_rank_gmres():
     assert rel(op.matvec_local(xp).cpu().numpy(), ex["y"][pk.perm, 0]) <= 1e-10
     _, rep = dist_gmres_solve(op, xp, tol=1e-6, restart=30, max_iter=2000)
     assert rep.converged and abs(rep.iterations - int(ex["gmres_iters"])) <= 1
+
+
+def _run_sharded_p2p(pk, G, X):
+    """Fused exchange: every rank's UP_OWN kernel stores its x̂ rows straight into all ranks'
+    exchange buffers (ITEM_BCAST epilogue, P2P stores on a multi-GPU box; here the G ranks'
+    buffers live on one GPU) and h2b_plan_bcast_rows pushes its x slice — no all-gather."""
+    from paper_1703_01175_b200.dist import CudaPlanEngine
+    from paper_1703_01175_b200.shard import (PH_COUPLE, PH_DOWN, PH_NEAR, PH_UP_OWN, PH_UP_TOP,
+                                             partition, plan_shard)
+    part = partition(pk, G)
+    q = X.shape[1]
+    dev = torch.device("cuda:0")
+    Xd = torch.from_numpy(X).to(dev)
+    plans = [plan_shard(pk, G, g, part, bcast=True) for g in range(G)]
+    eng = [CudaPlanEngine(p, 0) for p in plans]
+    ch = part.chunk
+    bufs = [(torch.zeros((part.xlen, q), dtype=torch.complex128, device=dev),
+             torch.zeros((part.xlen, q), dtype=torch.complex128, device=dev),
+             torch.zeros((p.nrows, q), dtype=torch.complex128, device=dev)) for p in plans]
+    for g in range(G):
+        eng[g].set_peers([bufs[o][0].data_ptr() for o in range(G) if o != g])
+    for g, p in enumerate(plans):
+        bufs[g][0][g * ch:g * ch + p.nrows] = Xd[p.row0:p.row0 + p.nrows]
+        eng[g].bcast_rows(bufs[g][0], g * ch, p.nrows, q)
+        eng[g].run(PH_UP_OWN, *bufs[g], q)
+    torch.cuda.synchronize()  # stands in for the barrier collective after the exchange
+    Y = torch.empty_like(Xd)
+    for g, p in enumerate(plans):
+        for ph in (PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR):
+            eng[g].run(ph, *bufs[g], q)
+        Y[p.row0:p.row0 + p.nrows] = bufs[g][2]
+    torch.cuda.synchronize()
+    for e in eng:
+        e.close()
+    return Y.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", ["rod164", "cube8", "line2048", "plate32", "random137"])
+@pytest.mark.parametrize("q", [1, 64])
+def test_fused_p2p_exchange_matches_oracle(name, q):
+    from oracle import h2_oracle as ho
+    pk, _ = load_golden(name)
+    X = np.random.default_rng(q).standard_normal((pk.n, q)) * (1 - 0.5j)
+    ref = ho.matvec_perm(pk, X)
+    for G in _ranks(pk)[1:]:
+        assert rel(_run_sharded_p2p(pk, G, X), ref) <= 1e-12, G
+
+
+def test_ipc_exchange_buffer_view_roundtrip():
+    """The raw exchange allocation (h2b_device_alloc, shareable with CUDA IPC) seen as a torch
+    tensor, written by a plan broadcast into a 'peer' buffer on the same device."""
+    import ctypes
+    from paper_1703_01175_b200 import _abi
+    from paper_1703_01175_b200.dist import _device_view
+    L = _abi.lib()
+    raw = ctypes.c_void_p()
+    _abi.check(L.h2b_device_alloc(0, 16 * 2 * 100 * 3, ctypes.byref(raw)))
+    dev = torch.device("cuda:0")
+    a, b = (_device_view(raw.value + 16 * 300 * k, (100, 3), dev) for k in range(2))
+    assert a.dtype == torch.complex128 and a.shape == (100, 3) and not a.any()
+    a.copy_(torch.arange(300, dtype=torch.float64, device=dev).reshape(100, 3) * (1 + 1j))
+    assert torch.equal(a, torch.arange(300, dtype=torch.float64, device=dev).reshape(100, 3) * (1 + 1j))
+    assert not b.any()
+    hd = (ctypes.c_char * 64)()
+    _abi.check(L.h2b_ipc_get_handle(raw, hd))  # shareable (opened by the other ranks' processes)
+    _abi.check(L.h2b_device_free(raw))
