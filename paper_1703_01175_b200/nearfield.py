@@ -79,6 +79,23 @@ def geometry_arrays(geom: dict):
     return centers, chi, float(geom["k0"]), h ** 3
 
 
+def plane_wave_rhs(centers, k0, direction):
+    """Plane-wave excitation exp(-j k0 d.r) at the voxel centres (restates kernel.py:237-242,
+    the right-hand side of BASELINE configs 3 and 5); ValueError unless |d| = 1 (to 1e-12)."""
+    d = np.asarray(direction, dtype=np.float64)
+    if abs(np.linalg.norm(d) - 1.0) > 1e-12:
+        raise ValueError("direction must be a unit vector")
+    return np.exp(-1j * k0 * (np.asarray(centers, dtype=np.float64) @ d))
+
+
+def seeded_incidence(rng):
+    """Incidence direction drawn as in SURVEY.md §8d (cfg 3/5): theta = arccos(U(-1, 1)), then
+    phi = U(0, 2 pi), from a numpy Generator."""
+    th = np.arccos(rng.uniform(-1, 1))
+    ph = rng.uniform(0, 2 * np.pi)
+    return np.array([np.sin(th) * np.cos(ph), np.sin(th) * np.sin(ph), np.cos(th)])
+
+
 def assemble_near(pk, centers, chi, k0, volume):
     """dbuf for a packed operator whose near-field payload was not shipped."""
     out = np.empty(int(pk.d_elems_expected()), dtype=np.complex128)

@@ -37,3 +37,15 @@ def test_compact_fixture_reproduces_reference_matvec(k):
     full = os.path.join(ROOT, "data", f"cfg{k}.npz")
     if os.path.exists(full):
         assert np.array_equal(load_packed(full).dbuf, pk.dbuf)
+
+
+@pytest.mark.parametrize("name", ["cube8", "line2048", "plate32"])
+def test_plane_wave_rhs_matches_reference(name):
+    """plane_wave_rhs restates kernel.plane_wave_rhs (kernel.py:237-242): bit-identical to the
+    right-hand side the reference generated for the golden BiCGStab solves."""
+    from paper_1703_01175_b200.nearfield import plane_wave_rhs
+    _, ex = load_golden(name)
+    centers, _, k0, _ = geometry_arrays(LATTICE[name])
+    assert np.array_equal(plane_wave_rhs(centers, k0, [0, -1, 0]), ex["bicg_rhs"])
+    with pytest.raises(ValueError):
+        plane_wave_rhs(centers, k0, [1, 1, 0])
