@@ -24,7 +24,7 @@ EXPORTED = (
     "h2b_plan_create", "h2b_plan_upload", "h2b_plan_set_phase", "h2b_plan_run",
     "h2b_plan_destroy", "h2b_plan_device_bytes", "h2b_assemble_near", "h2b_plan_set_peers",
     "h2b_plan_bcast_rows", "h2b_ipc_get_handle", "h2b_ipc_open", "h2b_ipc_close",
-    "h2b_plan_set_peer_offset", "h2b_device_alloc", "h2b_device_free",
+    "h2b_plan_set_peer_offset", "h2b_device_alloc", "h2b_device_free", "h2b_plan_set_gather",
 )
 OPT_GRAPHS, OPT_MEGA, OPT_TRACE, OPT_DEBUG, OPT_MRHS = 1, 2, 3, 4, 5
 Q_LAUNCHES_Q1, Q_SPAN_MODE, Q_SPLIT_LEVEL, Q_TOP_STAGED, Q_DEVICE_BYTES = 1, 2, 3, 4, 5
@@ -123,6 +123,7 @@ def lib():
     L.h2b_ipc_open.argtypes = [vp, C.POINTER(vp)]
     L.h2b_ipc_close.argtypes = [vp]
     L.h2b_plan_set_peer_offset.argtypes = [vp, C.c_int64]
+    L.h2b_plan_set_gather.argtypes = [vp, C.POINTER(C.c_int32), C.c_int64]
     L.h2b_device_alloc.argtypes = [C.c_int, C.c_size_t, C.POINTER(vp)]
     L.h2b_device_free.argtypes = [vp]
     L.h2b_plan_device_bytes.argtypes = [vp]

@@ -329,6 +329,7 @@ __device__ __forceinline__ double2 ld_na(const double2* p) {
   return r;
 }
 
+template <bool GATHER>
 __global__ void __launch_bounds__(MV_THREADS, 1) k_zgemv_grouped(const MmItem* __restrict__ items,
                                                                  const MmSeg* __restrict__ segs,
                                                                  MmBufs bf) {
@@ -366,10 +367,15 @@ __global__ void __launch_bounds__(MV_THREADS, 1) k_zgemv_grouped(const MmItem* _
       for (int h = 0; h < SU; ++h) {  // x / x̂ / ŷ rows: L1/L2 hits, read when the A stream lands
         if (s0 + h >= n) break;
         const MmSeg& sg = ss[s0 + h];
-        const double2* B = pick_b(bf, (sg.flags >> 4) & 15) + sg.b_row;
+        const double2* B = pick_b(bf, (sg.flags >> 4) & 15);
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          if (j0 + u < sg.k) cfma(acc, av[h][u], __ldg(B + j0 + u));
+          if (j0 + u < sg.k) {
+            int64_t row = sg.b_row + j0 + u;
+            if constexpr (GATHER)
+              if (sg.flags & SEG_GATHER) row = (int64_t)__ldg(bf.gather + row);
+            cfma(acc, av[h][u], __ldg(B + row));
+          }
       }
     }
   }
@@ -386,12 +392,14 @@ __global__ void __launch_bounds__(MV_THREADS, 1) k_zgemv_grouped(const MmItem* _
 }
 
 int run_grouped(const MmItem* items, int n_items, const MmSeg* segs, const MmBufs& bf, int q,
-                cudaStream_t st, int* nl) {
+                cudaStream_t st, int* nl, bool gather = true) {
   const int nct = (q + MM_N - 1) / MM_N;
   for (int i0 = 0; i0 < n_items; i0 += 65535) {
     const int cnt = std::min(65535, n_items - i0);
-    if (q == 1)
-      k_zgemv_grouped<<<cnt, MV_THREADS, 0, st>>>(items + i0, segs, bf);
+    if (q == 1 && gather)
+      k_zgemv_grouped<true><<<cnt, MV_THREADS, 0, st>>>(items + i0, segs, bf);
+    else if (q == 1)
+      k_zgemv_grouped<false><<<cnt, MV_THREADS, 0, st>>>(items + i0, segs, bf);
     else
       k_zgemm_grouped<<<dim3(cnt, nct), MM_THREADS, MM_SMEM, st>>>(items + i0, segs, bf, q);
     H2B_CHECK_LAUNCH();
@@ -599,11 +607,14 @@ struct h2b_plan_ctx {
     std::vector<int2> launches;
     MmItem* items = nullptr;
     MmSeg* segs = nullptr;
+    bool gather = false;  // any SEG_GATHER segment (selects the GEMV instantiation)
   };
   std::vector<Phase> phases;
   int64_t device_bytes = 0;
   double2* peers[MAX_PEERS] = {};
   double2** dpeers = nullptr;  // device copy of `peers`
+  int32_t* gather = nullptr;   // B-row index table of SEG_GATHER segments
+  int64_t n_gather = 0;
   int npeers = 0;
   int64_t peer_off = 0;        // element offset added to every peer pointer (ping-pong buffers)
 };
@@ -678,7 +689,7 @@ extern "C" int h2b_plan_set_phase(h2b_plan_handle p, int phase, int n_launches, 
   for (int64_t i = 0; i < n_segs; ++i) {
     const h2b_mm_seg& sg = segs[i];
     if (sg.k < 0 || sg.k > MM_K || (sg.flags & 15) >= p->n_payloads || ((sg.flags >> 4) & 15) >= B_N ||
-        (sg.flags & SEG_GATHER)) {
+        ((sg.flags & SEG_GATHER) && (sg.b_row < 0 || sg.b_row + sg.k > p->n_gather))) {
       h2b_set_error("h2b_plan_set_phase: segment " + std::to_string(i) + " out of range");
       return H2B_EINVAL;
     }
@@ -695,6 +706,8 @@ extern "C" int h2b_plan_set_phase(h2b_plan_handle p, int phase, int n_launches, 
   H2B_CUDA_TRY(cudaMalloc(&ph.segs, sizeof(MmSeg) * std::max<int64_t>(n_segs, 1)));
   if (n_items) H2B_CUDA_TRY(cudaMemcpy(ph.items, items, sizeof(MmItem) * n_items, cudaMemcpyHostToDevice));
   if (n_segs) H2B_CUDA_TRY(cudaMemcpy(ph.segs, segs, sizeof(MmSeg) * n_segs, cudaMemcpyHostToDevice));
+  ph.gather = false;
+  for (int64_t i = 0; i < n_segs; ++i) ph.gather |= (segs[i].flags & SEG_GATHER) != 0;
   int64_t first = 0;
   for (int i = 0; i < n_launches; ++i) {
     ph.launches.push_back(int2{(int)first, (int)launch_items[i]});
@@ -721,13 +734,13 @@ extern "C" int h2b_plan_run(h2b_plan_handle p, int phase, const void* x, const v
   bf.b[B_XHAT] = const_cast<double2*>((const double2*)xhat);
   bf.b[B_YHAT] = (double2*)yhat;
   bf.y = (double2*)y;
-  bf.gather = nullptr;
+  bf.gather = p->gather;
   for (int i = 0; i < p->npeers; ++i) bf.peers[i] = p->peers[i] + p->peer_off;
   bf.npeers = p->npeers;
   const auto& ph = p->phases[phase];
   int nl = 0;
   for (const int2& L : ph.launches)
-    H2B_TRY(run_grouped(ph.items + L.x, L.y, ph.segs, bf, q, (cudaStream_t)stream, &nl));
+    H2B_TRY(run_grouped(ph.items + L.x, L.y, ph.segs, bf, q, (cudaStream_t)stream, &nl, ph.gather));
   return H2B_OK;
 }
 
@@ -769,6 +782,21 @@ extern "C" int h2b_plan_bcast_rows(h2b_plan_handle p, const void* buf, int64_t r
   k_bcast_rows<<<grid, 256, 0, (cudaStream_t)stream>>>((const double2*)buf, row0 * q, n, p->dpeers, p->npeers,
                                                         p->peer_off);
   H2B_CHECK_LAUNCH();
+  return H2B_OK;
+}
+
+extern "C" int h2b_plan_set_gather(h2b_plan_handle p, const int32_t* idx, int64_t n) {
+  if (!p || n < 0 || (n && !idx)) {
+    h2b_set_error("h2b_plan_set_gather: bad arguments");
+    return H2B_EINVAL;
+  }
+  H2B_CUDA_TRY(cudaSetDevice(p->device));
+  cudaFree(p->gather);
+  p->gather = nullptr;
+  H2B_CUDA_TRY(cudaMalloc(&p->gather, sizeof(int32_t) * std::max<int64_t>(n, 1)));
+  if (n) H2B_CUDA_TRY(cudaMemcpy(p->gather, idx, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  p->n_gather = n;
+  p->device_bytes += 4 * n;
   return H2B_OK;
 }
 
@@ -835,6 +863,7 @@ extern "C" int h2b_plan_destroy(h2b_plan_handle p) {
   }
   for (int i = 0; i < p->n_payloads; ++i) cudaFree(p->pay[i]);
   if (p->dpeers) cudaFree(p->dpeers);
+  if (p->gather) cudaFree(p->gather);
   delete p;
   return H2B_OK;
 }

@@ -45,6 +45,9 @@ class CudaPlanEngine:
             for off in range(0, b.size, _UPLOAD_CHUNK):
                 ch = b[off:off + _UPLOAD_CHUNK]
                 _abi.check(L.h2b_plan_upload(h, i, ch.ctypes.data, ch.size, off), "h2b_plan_upload")
+        g = np.ascontiguousarray(getattr(plan, "gather", np.zeros(0, np.int32)), dtype=np.int32)
+        _abi.check(L.h2b_plan_set_gather(h, g.ctypes.data_as(C.POINTER(C.c_int32)), int(g.size)),
+                   "h2b_plan_set_gather")
         for ph in PHASES:
             counts, items, segs = plan.phases[ph]
             _abi.check(L.h2b_plan_set_phase(h, ph, int(counts.size),

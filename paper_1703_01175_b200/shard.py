@@ -40,6 +40,7 @@ PAY_VT, PAY_TT, PAY_T, PAY_S, PAY_D, PAY_V = 0, 1, 2, 3, 4, 5
 N_PAY = 6
 B_X, B_XHAT, B_YHAT, B_Y = 0, 1, 2, 3
 ITEM_ACC, ITEM_BCAST = 256, 512
+SEG_GATHER = 512
 
 
 @dataclass
@@ -106,6 +107,7 @@ class ShardPlan:
     part: Partition
     payloads: list                          # N_PAY complex128 arrays
     phases: dict = field(default_factory=dict)  # phase -> (launch_counts, items, segs)
+    gather: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))  # gathered B rows
 
     @property
     def row0(self):
@@ -126,10 +128,10 @@ class _Builder:
         self.items, self.segs, self.counts = [], [], []
         self._first = 0
 
-    def seg(self, a_src, a_off, lda, m0, k, b_src, b_row):
+    def seg(self, a_src, a_off, lda, m0, k, b_src, b_row, gather=False):
         for k0 in range(0, k, MM_K):
             self.segs.append((a_off + m0 * lda + k0, b_row + k0, min(MM_K, k - k0), lda,
-                              a_src | (b_src << 4), 0))
+                              a_src | (b_src << 4) | (SEG_GATHER if gather else 0), 0))
 
     def begin(self):
         return len(self.segs)
@@ -149,12 +151,15 @@ class _Builder:
                 np.array(self.items, dtype=self._it), np.array(self.segs, dtype=self._sg))
 
 
-def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = False) -> ShardPlan:
+def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = False,
+               couple_panels: bool = False) -> ShardPlan:
     """Payloads and work lists of rank g of G (see the module docstring).
 
     ``bcast``: the UP_OWN items also store their x̂ rows into every peer's exchange buffer
     (P2P stores over NVLink, libh2b ITEM_BCAST) — the all-gather of x̂ fused into the kernel that
-    computes it; the x slice is pushed by ``h2b_plan_bcast_rows``."""
+    computes it; the x slice is pushed by ``h2b_plan_bcast_rows``.
+    ``couple_panels``: each coupling row as one panel against gathered x̂ rows (full K chunks,
+    for multi-RHS use) instead of one segment per source block."""
     part = part or partition(pk, G)
     if not 0 <= g < G:
         raise ValueError("rank out of range")
@@ -222,6 +227,7 @@ def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = 
     phases[PH_UP_TOP] = Bd.done()
 
     Bd = _Builder()  # coupling: every own/top target with k > 0 (zero when it has no block)
+    gat, n_gat = [], 0  # gathered x̂ rows (panel mode): the sources of a target, concatenated
     for t in np.nonzero(mine & (k > 0))[0]:
         kt = int(k[t])
         blocks = []
@@ -229,14 +235,28 @@ def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = 
             s = int(pk.s_col[b])
             if k[s] == 0:
                 continue
-            S = pk.sbuf[pk.s_off[b]:pk.s_off[b] + kt * k[s]].reshape(kt, int(k[s]))
-            blocks.append((put(PAY_S, S), s))
+            blocks.append((pk.sbuf[pk.s_off[b]:pk.s_off[b] + kt * k[s]].reshape(kt, int(k[s])), s))
+        R = sum(B.shape[1] for B, _ in blocks)
+        if couple_panels and R:
+            # one row-major panel [S_t,s1 | S_t,s2 | ...] (k_t x R) against gathered x̂ rows:
+            # full 32-wide K chunks (best for the DMMA path, q >= 2)
+            off = put(PAY_S, np.concatenate([B for B, _ in blocks], axis=1))
+            gat.extend(np.arange(hat[s], hat[s] + k[s]) for _, s in blocks)
+            for m0 in range(0, kt, MM_M):
+                s0 = Bd.begin()
+                Bd.seg(PAY_S, off, R, m0, R, B_XHAT, n_gat, gather=True)
+                Bd.end(s0, hat[t] + m0, min(MM_M, kt - m0), B_YHAT)
+            n_gat += R
+            continue
+        # one segment per source block, contiguous x̂ rows (best for the GEMV path, q = 1)
+        offs = [(put(PAY_S, B), s) for B, s in blocks]
         for m0 in range(0, kt, MM_M):
             s0 = Bd.begin()
-            for off, s in blocks:
+            for off, s in offs:
                 Bd.seg(PAY_S, off, int(k[s]), m0, int(k[s]), B_XHAT, hat[s])
             Bd.end(s0, hat[t] + m0, min(MM_M, kt - m0), B_YHAT)
     phases[PH_COUPLE] = Bd.done()
+    gather = (np.concatenate(gat).astype(np.int32) if gat else np.zeros(0, np.int32))
 
     Bd = _Builder()  # downward, root first: [ŷ_lo; ŷ_hi] += [T_lo; T_hi] ŷ_c
     for lvl in range(pk.depth - 1):
@@ -294,4 +314,4 @@ def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = 
     phases[PH_NEAR] = Bd.done()
 
     payloads = [np.concatenate(a) if a else np.zeros(0, np.complex128) for a in pays]
-    return ShardPlan(rank=g, part=part, payloads=payloads, phases=phases)
+    return ShardPlan(rank=g, part=part, payloads=payloads, phases=phases, gather=gather)

@@ -150,3 +150,22 @@ def test_gloo_distributed_matvec_and_gmres(name, world, tmp_path):
     assert len(its) == 1 and abs(its.pop() - ro.iterations) <= 1
     assert all(bool(z["conv"]) for z in parts)
     assert np.linalg.norm(ho.matvec_perm(pk, xs) - bp) / np.linalg.norm(bp) <= 1e-8
+
+
+@pytest.mark.parametrize("name", ["cube8", "plate32", "random137"])
+def test_shard_couple_panels_reproduce_oracle(name):
+    """Coupling rows as gathered panels (h2b SEG_GATHER) give the same matvec."""
+    from oracle import h2_oracle as ho
+    from oracle.plan_exec import NumpyPlanEngine
+    from paper_1703_01175_b200.shard import PH_COUPLE, PH_DOWN, PH_NEAR, PH_UP_OWN, PH_UP_TOP, plan_shard
+    pk, _ = load_golden(name)
+    X = _cvec(np.random.default_rng(2), (pk.n, 2))
+    plan = plan_shard(pk, 1, 0, couple_panels=True)
+    assert plan.gather.size > 0
+    eng = NumpyPlanEngine(plan)
+    xb = torch.zeros((plan.part.xlen, 2), dtype=torch.complex128)
+    xb[:pk.n] = torch.from_numpy(X)
+    yh, y = torch.zeros_like(xb), torch.zeros((pk.n, 2), dtype=torch.complex128)
+    for ph in (PH_UP_OWN, PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR):
+        eng.run(ph, xb, yh, y, 2)
+    assert rel(y.numpy(), ho.matvec_perm(pk, X)) <= 1e-13

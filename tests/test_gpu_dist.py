@@ -26,7 +26,7 @@ def _ranks(pk):
     return out
 
 
-def _run_sharded(pk, G, X):
+def _run_sharded(pk, G, X, **plan_kw):
     from paper_1703_01175_b200.dist import CudaPlanEngine
     from paper_1703_01175_b200.shard import (PH_COUPLE, PH_DOWN, PH_NEAR, PH_UP_OWN, PH_UP_TOP,
                                              partition, plan_shard)
@@ -34,7 +34,7 @@ def _run_sharded(pk, G, X):
     q = X.shape[1]
     dev = torch.device("cuda:0")
     Xd = torch.from_numpy(X).to(dev)
-    plans = [plan_shard(pk, G, g, part) for g in range(G)]
+    plans = [plan_shard(pk, G, g, part, **plan_kw) for g in range(G)]
     eng = [CudaPlanEngine(p, 0) for p in plans]
     ch = part.chunk
     bufs = []
@@ -152,3 +152,15 @@ def test_ipc_exchange_buffer_view_roundtrip():
     hd = (ctypes.c_char * 64)()
     _abi.check(L.h2b_ipc_get_handle(raw, hd))  # shareable (opened by the other ranks' processes)
     _abi.check(L.h2b_device_free(raw))
+
+
+@pytest.mark.parametrize("name", ["cube8", "plate32", "random137", "line2048"])
+@pytest.mark.parametrize("q", [1, 64])
+def test_shard_couple_panels_on_device(name, q):
+    """Coupling rows as gathered panels: GEMV (q = 1) and DMMA (q >= 2) gather paths."""
+    from oracle import h2_oracle as ho
+    pk, _ = load_golden(name)
+    X = np.random.default_rng(7).standard_normal((pk.n, q)) * (0.5 + 1j)
+    ref = ho.matvec_perm(pk, X)
+    for G in _ranks(pk):
+        assert rel(_run_sharded(pk, G, X, couple_panels=True), ref) <= 1e-12, G
