@@ -217,7 +217,9 @@ int h2b_zaxpby(int64_t n, double ar, double ai, const void* x, double br, double
  *   item: C[c_row + i, :] (+)= sum over its segments of A_seg[i, :] B_seg[:, :], i < m <= 64
  *   seg:  A = payload[a_src][a_off + i*lda + j] (i < m, j < k <= 32),
  *         B row j = (b_src buffer)[b_row + j]
- * flags: seg  = a_src | b_src << 4 (b_src 0 x, 1 xhat, 2 yhat)
+ * flags: seg  = a_src | b_src << 4 (b_src 0 x, 1 xhat, 2 yhat) | 256 (A transposed:
+ *               A[i][j] = payload[a_off + j*lda + i]) | 512 (B rows gathered: row j =
+ *               gather[b_row + j], table set by h2b_plan_set_gather)
  *        item = dst (0 x, 1 xhat, 2 yhat, 3 y) | 256 (accumulate) | 512 (broadcast to peers)
  * --------------------------------------------------------------------- */
 typedef struct h2b_mm_item {
@@ -240,6 +242,8 @@ int h2b_plan_set_phase(h2b_plan_handle p, int phase, int n_launches, const int64
                        int64_t n_segs);
 int h2b_plan_run(h2b_plan_handle p, int phase, const void* x, const void* xhat, void* yhat, void* y,
                  int q, void* stream);
+/* Row-index table of gathered segments (set before h2b_plan_set_phase validates them). */
+int h2b_plan_set_gather(h2b_plan_handle p, const int32_t* idx, int64_t n);
 int h2b_plan_destroy(h2b_plan_handle p);
 /* Fused exchange over peer memory (NVLink P2P stores): items flagged 512 (broadcast) store
  * their rows into the local buffer AND into every peer's buffer at the same rows (the all-gather

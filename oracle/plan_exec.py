@@ -39,7 +39,11 @@ class NumpyPlanEngine:
                 else:
                     idx = off + np.arange(m)[:, None] * lda + np.arange(k)[None, :]
                 A = pays[a_src][idx]
-                Bm = bufs[b_src][int(sg["b_row"]):int(sg["b_row"]) + k]
+                if int(sg["flags"]) & 512:  # SEG_GATHER: B row j = gather[b_row + j]
+                    g = self.plan.gather[int(sg["b_row"]):int(sg["b_row"]) + k]
+                    Bm = bufs[b_src][g]
+                else:
+                    Bm = bufs[b_src][int(sg["b_row"]):int(sg["b_row"]) + k]
                 acc += A @ Bm
             dst = bufs[int(it["flags"]) & 15]
             r0 = int(it["c_row"])
