@@ -8,7 +8,7 @@ import numpy as np, torch
 from paper_1703_01175_b200 import H2Operator, load_packed, _abi
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 dbg = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-pk, ex = load_packed(f"data/cfg{k}.npz", with_extra=True)
+sys.path.insert(0, "."); from bench import load; pk, ex = load(k)
 op = H2Operator(pk)
 L = _abi.lib()
 _abi.check(L.h2b_prepare_handle(op.handle))
