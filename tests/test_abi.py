@@ -69,3 +69,14 @@ def test_create_rejects_without_device_with_status():
     rc = _abi.lib().h2b_create(C.byref(lay), 0, C.byref(h))
     assert rc == _abi.H2B_ENODEV
     assert b"no CPU fallback" in _abi.lib().h2b_last_error()
+
+
+def test_plan_create_without_device_fails_loudly():
+    import ctypes as C
+    import torch
+    from paper_1703_01175_b200 import _abi
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    h = C.c_void_p()
+    elems = (C.c_int64 * 1)(4)
+    assert _abi.lib().h2b_plan_create(0, 1, elems, C.byref(h)) == _abi.H2B_ENODEV

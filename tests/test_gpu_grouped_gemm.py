@@ -68,3 +68,31 @@ def test_grouped_kernels_match_interpreter(q):
             first = got
         assert np.array_equal(got, first)  # deterministic: fixed summation order
     eng.close()
+
+
+def test_plan_set_phase_validates_work_lists():
+    """Malformed items/segments are rejected at upload (the kernels trust the lists)."""
+    import ctypes as C
+    from paper_1703_01175_b200 import _abi
+    L = _abi.lib()
+    h = C.c_void_p()
+    elems = (C.c_int64 * 2)(4096, 4096)
+    _abi.check(L.h2b_plan_create(0, 2, elems, C.byref(h)))
+
+    def phase(items, segs, counts=None):
+        it = np.array(items, dtype=_abi.MM_ITEM)
+        sg = np.array(segs, dtype=_abi.MM_SEG)
+        cnt = np.array(counts if counts is not None else [it.size], dtype=np.int64)
+        return L.h2b_plan_set_phase(h, 0, int(cnt.size), cnt.ctypes.data_as(C.POINTER(C.c_int64)),
+                                    it.ctypes.data, int(it.size), sg.ctypes.data, int(sg.size))
+
+    ok_seg = (0, 0, 8, 8, 0, 0)
+    assert phase([(0, 8, 0, 1, 3, 0)], [ok_seg]) == _abi.H2B_OK
+    assert phase([(0, 65, 0, 1, 3, 0)], [ok_seg]) == _abi.H2B_EINVAL        # m > 64
+    assert phase([(0, 8, 0, 2, 3, 0)], [ok_seg]) == _abi.H2B_EINVAL         # segments out of range
+    assert phase([(0, 8, 0, 1, 3, 0)], [(0, 0, 33, 40, 0, 0)]) == _abi.H2B_EINVAL  # k > 32
+    assert phase([(0, 8, 0, 1, 3, 0)], [(0, 0, 8, 8, 7, 0)]) == _abi.H2B_EINVAL    # no payload 7
+    assert phase([(0, 8, 0, 2, 3, 0)], [ok_seg, (0, 0, 8, 8, 256, 0)]) == _abi.H2B_EINVAL  # mixed A
+    assert phase([(0, 8, 0, 1, 3, 0)], [(0, 0, 8, 8, 512, 0)]) == _abi.H2B_EINVAL  # gather, no table
+    assert phase([(0, 8, 0, 1, 3, 0)], [ok_seg], counts=[2]) == _abi.H2B_EINVAL     # counts mismatch
+    _abi.check(L.h2b_plan_destroy(h))
