@@ -252,6 +252,19 @@ class DistH2Operator:
             self._slot ^= 1
         return out[:, 0] if squeeze else out
 
+    def close(self):
+        """Release the device resources: IPC mappings, exchange allocations, the plan handle."""
+        L = _abi.lib()
+        for raw, _views, peers in self._p2p.values():
+            for ptr in peers:
+                L.h2b_ipc_close(C.c_void_p(ptr))
+            L.h2b_device_free(raw)
+        self._p2p.clear()
+        self._graphs.clear()
+        self._ws.clear()
+        if hasattr(self.engine, "close"):
+            self.engine.close()
+
     def _barrier(self):
         """Stream-ordered barrier collective (NCCL all-reduce of one element)."""
         import torch
