@@ -44,3 +44,32 @@ def test_validate_rejects_broken_tiling():
     bad.d_col = pk.d_col[:-1]
     with pytest.raises(ValueError):
         validate(bad)
+
+
+@pytest.mark.parametrize("name", GOLDEN_NAMES)
+def test_payload_sizes_implied_by_tables(name):
+    """E_V, E_T, E_S, E_D recomputed from the index tables equal the payload sizes (the sizes the
+    device allocates for operators whose payloads are generated on the device)."""
+    pk, _ = load_golden(name)
+    assert pk.far_elems_expected() == (pk.vbuf.size, pk.tbuf.size, pk.sbuf.size)
+    assert pk.d_elems_expected() == pk.dbuf.size
+
+
+def test_structure_file_roundtrip(tmp_path):
+    """save_structure keeps every table and the geometry; load_packed fills seeded payloads of the
+    reference shapes (host) or leaves them for the device."""
+    from paper_1703_01175_b200.pack import save_structure
+    pk, _ = load_golden("cube8")
+    geom = dict(kind="lattice", dims=[8, 8, 8], h=1 / 16, eps_r=4.0, k0=2 * np.pi)
+    path = tmp_path / "s.npz"
+    save_structure(pk, path, geom, seed=3)
+    a = load_packed(path)
+    b = load_packed(path)
+    for t in ("c_start", "c_rank", "s_col", "s_off", "d_col", "d_off", "perm"):
+        assert np.array_equal(getattr(a, t), getattr(pk, t))
+    assert (a.vbuf.size, a.tbuf.size, a.sbuf.size) == (pk.vbuf.size, pk.tbuf.size, pk.sbuf.size)
+    assert np.array_equal(a.sbuf, b.sbuf)                      # seeded: reproducible
+    assert np.max(np.abs(a.dbuf - pk.dbuf)) <= 1e-14 * np.max(np.abs(pk.dbuf))  # near-field exact
+    c = load_packed(path, near_on_host=False, far_on_host=False)
+    assert c.sbuf.size == 0 and c.dbuf.size == 0 and "synthetic" in c.meta and "geometry" in c.meta
+    assert c.algorithmic_bytes() == pk.algorithmic_bytes()
