@@ -269,7 +269,7 @@ int h2b_matvec_host(h2b_handle h, const void* x, void* y, int q) {
     // pinned host buffers: the whole call (H2D, gather, matvec, scatter, D2H) is one graph
     H2B_TRY(h2b_prepare(h));
     H2B_TRY(h2b_ensure_workspace(h, q));
-    if (q >= 2 && h->use_mrhs) H2B_TRY(h2b_mrhs_prepare(h));
+    if (q >= 2 && h->use_mrhs) H2B_TRY(h2b_mrhs_workspace(h, q));
     const GraphKey key{x, y, -q};  // negative q: host-path graph
     auto it = h->graphs.find(key);
     if (it == h->graphs.end()) {

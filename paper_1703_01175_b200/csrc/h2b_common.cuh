@@ -333,6 +333,7 @@ void h2b_release_graphs(h2b_ctx* h);
 int h2b_mrhs_prepare(h2b_ctx* h);
 void h2b_mrhs_free(h2b_ctx* h);
 int h2b_mrhs_launches(const h2b_ctx* h);
+int h2b_mrhs_workspace(h2b_ctx* h, int q);
 int h2b_launch_mrhs(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st, int* nl);
 
 // ---------------------------------------------------------------------------

@@ -149,7 +149,7 @@ int h2b_ensure_workspace(h2b_ctx* h, int q) {
 int h2b_run_matvec(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st) {
   H2B_TRY(h2b_prepare(h));
   H2B_TRY(h2b_ensure_workspace(h, q));
-  if (q >= 2 && h->use_mrhs) H2B_TRY(h2b_mrhs_prepare(h));  // allocates: never inside a capture
+  if (q >= 2 && h->use_mrhs) H2B_TRY(h2b_mrhs_workspace(h, q));  // allocates: never inside a capture
   int nl = 0;
   if (!h->use_graphs) {
     H2B_TRY(enqueue_matvec(h, xp, yp, q, st, &nl));

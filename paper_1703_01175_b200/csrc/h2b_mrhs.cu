@@ -54,6 +54,7 @@ static_assert(MM_SMEM <= 227 * 1024, "shared memory budget");  // 202752 bytes
 
 enum : int32_t { A_V = 0, A_T, A_S, A_D, A_VT, A_TT, A_N };
 enum : int32_t { B_X = 0, B_XHAT, B_YHAT, B_N };
+constexpr int B_SCR = B_N + 1;  // destination id of split-K parts (single-GPU multi-RHS plan)
 constexpr int SEG_TRANS = 1 << 8;   // A[i][j] = src[a_off + j*lda + i]
 constexpr int SEG_GATHER = 1 << 9;  // B row r = gather[b_row + r]
 constexpr int ITEM_ACC = 1 << 8;
@@ -81,6 +82,7 @@ struct MmBufs {
   const int32_t* gather;
   double2* peers[MAX_PEERS];  // other ranks' exchange buffers (P2P-mapped), for ITEM_BCAST
   int npeers;
+  double2* scratch;           // split-K partial planes (dst id B_SCR)
 };
 
 // the epilogue store of one output element: local (overwrite / accumulate) and, for
@@ -108,7 +110,17 @@ __device__ __forceinline__ double2* pick_b(const MmBufs& bf, int id) {
   double2* p = bf.b[0];
 #pragma unroll
   for (int i = 1; i < B_N; ++i) p = id == i ? bf.b[i] : p;
+  p = id == B_SCR ? bf.scratch : p;
   return id == B_N ? bf.y : p;
+}
+
+// y[e] = sum over the split-K planes, in plane order (deterministic)
+__global__ void k_sum_parts(const double2* __restrict__ scr, int parts, int64_t plane, double2* __restrict__ y) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < plane; e += (int64_t)gridDim.x * blockDim.x) {
+    double2 a = scr[e];
+    for (int p = 1; p < parts; ++p) a = cadd(a, scr[p * plane + e]);
+    y[e] = a;
+  }
 }
 
 
@@ -415,6 +427,9 @@ int run_grouped(const MmItem* items, int n_items, const MmSeg* segs, const MmBuf
 // ---------------------------------------------------------------------------
 struct MrhsPlan {
   std::vector<int2> launches;  // {item_first, n_items} in execution order
+  int split = 1;               // split-K parts of the near-field launch (1: none)
+  double2* scratch = nullptr;  // split planes: split x N x q
+  int64_t scratch_q = 0;
   MmItem* items = nullptr;
   MmSeg* segs = nullptr;
   int64_t flops_q1 = 0;        // useful real flops per column (for reporting)
@@ -523,24 +538,48 @@ int h2b_mrhs_prepare(h2b_ctx* h) {
     }
     B.end_launch();
   }
-  // near-field + leaf back-transform, one item per (leaf, 64-row chunk): y overwritten
+  // near-field + leaf back-transform, one item per (leaf, 64-row chunk): y overwritten.  Small
+  // operators (fewer items than two per SM) split every item's segment list into `split` parts
+  // writing partial planes, summed in a fixed order afterwards (deterministic split-K).
+  int n_near_items = 0, max_segs = 0;
+  for (int t : h->h_leaves) {
+    n_near_items += (h->c_size[t] + MM_M - 1) / MM_M;
+    max_segs = std::max<int>(max_segs, (int)(h->d_row_ptr[t + 1] - h->d_row_ptr[t]) + 1);
+  }
+  int split = 1;
+  if (n_near_items > 0 && n_near_items < 2 * 148)
+    split = std::max(1, std::min({8, (2 * 148 + n_near_items - 1) / n_near_items, max_segs / 4}));
   for (int t : h->h_leaves) {
     const int nt = h->c_size[t];
     for (int m0 = 0; m0 < nt; m0 += MM_M) {
-      const int s0 = B.begin_item();
-      for (int64_t b = h->d_row_ptr[t]; b < h->d_row_ptr[t + 1]; ++b) {
-        const int s = h->d_col[b];
-        B.seg(A_D, h->d_off[b], h->c_size[s], false, m0, h->c_size[s], B_X, h->c_start[s], false);
+      std::vector<int> bl;  // logical segments: partner blocks, then the leaf basis (-1)
+      for (int64_t b = h->d_row_ptr[t]; b < h->d_row_ptr[t + 1]; ++b) bl.push_back((int)(b - h->d_row_ptr[t]));
+      if (h->c_rank[t] > 0) bl.push_back(-1);
+      const int parts = split;
+      for (int pt = 0; pt < parts; ++pt) {
+        const size_t lo = bl.size() * pt / parts, hi = bl.size() * (pt + 1) / parts;
+        const int s0 = B.begin_item();
+        for (size_t u = lo; u < hi; ++u) {
+          if (bl[u] < 0) {
+            B.seg(A_V, h->c_voff[t], h->c_rank[t], false, m0, h->c_rank[t], B_YHAT, h->c_xoff[t], false);
+          } else {
+            const int64_t b = h->d_row_ptr[t] + bl[u];
+            const int s = h->d_col[b];
+            B.seg(A_D, h->d_off[b], h->c_size[s], false, m0, h->c_size[s], B_X, h->c_start[s], false);
+          }
+        }
+        if (split == 1)
+          B.end_item(s0, h->c_start[t] + m0, std::min(MM_M, nt - m0), B_N, false);
+        else
+          B.end_item(s0, (int64_t)pt * h->n + h->c_start[t] + m0, std::min(MM_M, nt - m0), B_SCR, false);
       }
-      if (h->c_rank[t] > 0)
-        B.seg(A_V, h->c_voff[t], h->c_rank[t], false, m0, h->c_rank[t], B_YHAT, h->c_xoff[t], false);
-      B.end_item(s0, h->c_start[t] + m0, std::min(MM_M, nt - m0), B_N, false);
     }
   }
   B.end_launch();
 
   auto* plan = new MrhsPlan();
   plan->launches = B.launches;
+  plan->split = split;
   int64_t acc = 0;
   const size_t bi = sizeof(MmItem) * std::max<size_t>(B.items.size(), 1);
   const size_t bs = sizeof(MmSeg) * std::max<size_t>(B.segs.size(), 1);
@@ -566,6 +605,7 @@ void h2b_mrhs_free(h2b_ctx* h) {
   if (!h->mrhs) return;
   cudaFree(h->mrhs->items);
   cudaFree(h->mrhs->segs);
+  cudaFree(h->mrhs->scratch);
   delete h->mrhs;
   h->mrhs = nullptr;
 }
@@ -586,8 +626,30 @@ int h2b_launch_mrhs(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStrea
   bf.b[B_YHAT] = h->yhat;
   bf.y = yp;
   bf.gather = h->s_xcol;
+  bf.scratch = h->mrhs->scratch;
   for (const int2& L : h->mrhs->launches)
     H2B_TRY(run_grouped(h->mrhs->items + L.x, L.y, h->mrhs->segs, bf, q, st, nl));
+  if (h->mrhs->split > 1) {
+    const int64_t plane = h->n * q;
+    k_sum_parts<<<(int)std::min<int64_t>((plane + 255) / 256, 148 * 8), 256, 0, st>>>(h->mrhs->scratch, h->mrhs->split,
+                                                                                      plane, yp);
+    H2B_CHECK_LAUNCH();
+    ++*nl;
+  }
+  return H2B_OK;
+}
+
+// split-K planes for q columns (allocated before any graph capture)
+int h2b_mrhs_workspace(h2b_ctx* h, int q) {
+  H2B_TRY(h2b_mrhs_prepare(h));
+  MrhsPlan* p = h->mrhs;
+  if (p->split <= 1 || p->scratch_q >= q) return H2B_OK;
+  h2b_release_graphs(h);  // captured graphs hold the old planes
+  cudaFree(p->scratch);
+  p->scratch = nullptr;
+  p->scratch_q = 0;
+  H2B_CUDA_TRY(cudaMalloc(&p->scratch, sizeof(double2) * (size_t)p->split * h->n * q));
+  p->scratch_q = q;
   return H2B_OK;
 }
 
