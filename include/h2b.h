@@ -242,6 +242,12 @@ int h2b_plan_set_phase(h2b_plan_handle p, int phase, int n_launches, const int64
                        int64_t n_segs);
 int h2b_plan_run(h2b_plan_handle p, int phase, const void* x, const void* xhat, void* yhat, void* y,
                  int q, void* stream);
+/* q = 1 near-field of a plan on the streaming near-field kernel: items {int64 y_row; int32
+ * b_first, nb; int32 row0, pad} (rows_per_thread * 128 / (ns/2) rows of a ns-point leaf each),
+ * blocks {int64 d_off (in payload 4), int64 x_row}.  When set, h2b_plan_run(phase 4, q = 1)
+ * overwrites y with the near-field and then runs phase 5 (the leaf back-transform items). */
+int h2b_plan_set_near_fast(h2b_plan_handle p, const void* items, int64_t n_items, const void* blks,
+                           int64_t n_blks, int ns, int rows_per_thread);
 /* Row-index table of gathered segments (set before h2b_plan_set_phase validates them). */
 int h2b_plan_set_gather(h2b_plan_handle p, const int32_t* idx, int64_t n);
 int h2b_plan_destroy(h2b_plan_handle p);

@@ -25,6 +25,7 @@ EXPORTED = (
     "h2b_plan_destroy", "h2b_plan_device_bytes", "h2b_assemble_near", "h2b_plan_set_peers",
     "h2b_plan_bcast_rows", "h2b_ipc_get_handle", "h2b_ipc_open", "h2b_ipc_close",
     "h2b_plan_set_peer_offset", "h2b_device_alloc", "h2b_device_free", "h2b_plan_set_gather",
+    "h2b_plan_set_near_fast",
 )
 OPT_GRAPHS, OPT_MEGA, OPT_TRACE, OPT_DEBUG, OPT_MRHS = 1, 2, 3, 4, 5
 Q_LAUNCHES_Q1, Q_SPAN_MODE, Q_SPLIT_LEVEL, Q_TOP_STAGED, Q_DEVICE_BYTES = 1, 2, 3, 4, 5
@@ -62,6 +63,9 @@ MM_ITEM = _np.dtype([("c_row", "<i8"), ("m", "<i4"), ("seg0", "<i4"), ("nseg", "
                      ("flags", "<i4"), ("pad", "<i8")])
 MM_SEG = _np.dtype([("a_off", "<i8"), ("b_row", "<i8"), ("k", "<i4"), ("lda", "<i4"),
                     ("flags", "<i4"), ("pad", "<i4")])
+NEAR_ITEM = _np.dtype([("y_off", "<i8"), ("b_first", "<i4"), ("nb", "<i4"), ("row0", "<i4"),
+                      ("pad", "<i4")])
+NEAR_BLK = _np.dtype([("d_off", "<i8"), ("x_off", "<i8")])
 B_X, B_XHAT, B_YHAT, B_Y = 0, 1, 2, 3
 ITEM_ACC, ITEM_BCAST = 256, 512
 
@@ -124,6 +128,7 @@ def lib():
     L.h2b_ipc_close.argtypes = [vp]
     L.h2b_plan_set_peer_offset.argtypes = [vp, C.c_int64]
     L.h2b_plan_set_gather.argtypes = [vp, C.POINTER(C.c_int32), C.c_int64]
+    L.h2b_plan_set_near_fast.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, C.c_int, C.c_int]
     L.h2b_device_alloc.argtypes = [C.c_int, C.c_size_t, C.POINTER(vp)]
     L.h2b_device_free.argtypes = [vp]
     L.h2b_plan_device_bytes.argtypes = [vp]

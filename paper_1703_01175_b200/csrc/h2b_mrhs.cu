@@ -31,6 +31,11 @@
 
 #include "h2b_common.cuh"
 
+// h2b_near.cu: the q = 1 near-field streaming kernel on explicit work lists
+int h2b_launch_near_list(const NearItem* items, int n_items, const NearBlk* blks, const double2* dbuf,
+                         const double2* x, double2* y, int ns, int R, cudaStream_t st);
+int h2b_near_rows_per_item(int ns, int r);
+
 namespace {
 
 constexpr int MM_WARPS = 16;                  // MMA warps (4 per SM sub-partition)
@@ -679,6 +684,11 @@ struct h2b_plan_ctx {
   int64_t n_gather = 0;
   int npeers = 0;
   int64_t peer_off = 0;        // element offset added to every peer pointer (ping-pong buffers)
+  // q = 1 near-field on the streaming kernel (h2b_plan_set_near_fast): y overwritten from
+  // payload 4 (D) and the exchange buffer, then phase 5 (leaf back, accumulating) instead of 4
+  NearItem* nf_items = nullptr;
+  NearBlk* nf_blks = nullptr;
+  int nf_n = 0, nf_ns = 0, nf_r = 0;
 };
 
 extern "C" int h2b_plan_create(int device, int n_payloads, const int64_t* payload_elems,
@@ -799,8 +809,14 @@ extern "C" int h2b_plan_run(h2b_plan_handle p, int phase, const void* x, const v
   bf.gather = p->gather;
   for (int i = 0; i < p->npeers; ++i) bf.peers[i] = p->peers[i] + p->peer_off;
   bf.npeers = p->npeers;
-  const auto& ph = p->phases[phase];
   int nl = 0;
+  if (phase == 4 && q == 1 && p->nf_n > 0) {
+    H2B_TRY(h2b_launch_near_list(p->nf_items, p->nf_n, p->nf_blks, p->pay[4], bf.b[B_X], bf.y, p->nf_ns,
+                                 p->nf_r, (cudaStream_t)stream));
+    phase = 5;  // then the leaf back-transform items (accumulate)
+    if (phase >= (int)p->phases.size()) return H2B_OK;
+  }
+  const auto& ph = p->phases[phase];
   for (const int2& L : ph.launches)
     H2B_TRY(run_grouped(ph.items + L.x, L.y, ph.segs, bf, q, (cudaStream_t)stream, &nl, ph.gather));
   return H2B_OK;
@@ -844,6 +860,44 @@ extern "C" int h2b_plan_bcast_rows(h2b_plan_handle p, const void* buf, int64_t r
   k_bcast_rows<<<grid, 256, 0, (cudaStream_t)stream>>>((const double2*)buf, row0 * q, n, p->dpeers, p->npeers,
                                                         p->peer_off);
   H2B_CHECK_LAUNCH();
+  return H2B_OK;
+}
+
+extern "C" int h2b_plan_set_near_fast(h2b_plan_handle p, const void* items, int64_t n_items, const void* blks,
+                                      int64_t n_blks, int ns, int rows_per_thread) {
+  if (!p || n_items < 0 || n_blks < 0 || (n_items && (!items || !blks)) || p->n_payloads < 5 ||
+      h2b_near_rows_per_item(ns, rows_per_thread) == 0 || n_items > (1 << 30)) {
+    h2b_set_error("h2b_plan_set_near_fast: bad arguments (leaf size 32/64, rows per thread 1/2/4, "
+                  "payload 4 = near-field)");
+    return H2B_EINVAL;
+  }
+  const NearItem* it = (const NearItem*)items;
+  const NearBlk* bl = (const NearBlk*)blks;
+  const int64_t rb = h2b_near_rows_per_item(ns, rows_per_thread);
+  for (int64_t i = 0; i < n_items; ++i)  // the kernel trusts the lists
+    if (it[i].b_first < 0 || it[i].nb < 0 || it[i].b_first + (int64_t)it[i].nb > n_blks || it[i].row0 < 0 ||
+        it[i].row0 + rb > ns) {
+      h2b_set_error("h2b_plan_set_near_fast: item " + std::to_string(i) + " out of range");
+      return H2B_EINVAL;
+    }
+  for (int64_t b = 0; b < n_blks; ++b)
+    if (bl[b].d_off < 0 || bl[b].d_off + (int64_t)ns * ns > p->pay_elems[4]) {
+      h2b_set_error("h2b_plan_set_near_fast: block " + std::to_string(b) + " outside the near-field payload");
+      return H2B_EINVAL;
+    }
+  H2B_CUDA_TRY(cudaSetDevice(p->device));
+  cudaFree(p->nf_items);
+  cudaFree(p->nf_blks);
+  p->nf_items = nullptr;
+  p->nf_blks = nullptr;
+  p->nf_n = 0;
+  H2B_CUDA_TRY(cudaMalloc(&p->nf_items, sizeof(NearItem) * std::max<int64_t>(n_items, 1)));
+  H2B_CUDA_TRY(cudaMalloc(&p->nf_blks, sizeof(NearBlk) * std::max<int64_t>(n_blks, 1)));
+  if (n_items) H2B_CUDA_TRY(cudaMemcpy(p->nf_items, items, sizeof(NearItem) * n_items, cudaMemcpyHostToDevice));
+  if (n_blks) H2B_CUDA_TRY(cudaMemcpy(p->nf_blks, blks, sizeof(NearBlk) * n_blks, cudaMemcpyHostToDevice));
+  p->nf_n = (int)n_items;
+  p->nf_ns = ns;
+  p->nf_r = rows_per_thread;
   return H2B_OK;
 }
 
@@ -926,6 +980,8 @@ extern "C" int h2b_plan_destroy(h2b_plan_handle p) {
   for (int i = 0; i < p->n_payloads; ++i) cudaFree(p->pay[i]);
   if (p->dpeers) cudaFree(p->dpeers);
   if (p->gather) cudaFree(p->gather);
+  cudaFree(p->nf_items);
+  cudaFree(p->nf_blks);
   delete p;
   return H2B_OK;
 }

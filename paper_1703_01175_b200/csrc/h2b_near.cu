@@ -127,6 +127,23 @@ void launch_q1(const h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st
 // rows per CTA of the q=1 kernel for a leaf size (0 = not supported)
 int h2b_near_rows_per_item(int ns, int r) { return (ns == 32 || ns == 64) ? r * NEAR_NT / (ns / 2) : 0; }
 
+// the q=1 streaming kernel on explicit work lists (plan handles: one rank's near-field rows,
+// x columns in the exchange buffer); y rows overwritten
+int h2b_launch_near_list(const NearItem* items, int n_items, const NearBlk* blks, const double2* dbuf,
+                         const double2* x, double2* y, int ns, int R, cudaStream_t st) {
+  if (n_items <= 0) return H2B_OK;
+#define NL(A, B)                                                                           \
+  if (ns == A && R == B) k_near_q1<A, B><<<n_items, NEAR_NT, 0, st>>>(items, blks, dbuf, x, y); \
+  else
+  NL(32, 1) NL(32, 2) NL(32, 4) NL(64, 1) NL(64, 2) NL(64, 4) {
+    h2b_set_error("h2b_launch_near_list: unsupported leaf size / rows per thread");
+    return H2B_EINVAL;
+  }
+#undef NL
+  H2B_CHECK_LAUNCH();
+  return H2B_OK;
+}
+
 int h2b_launch_near(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st) {
   if (q == 1 && h->near_rb > 0) {
     const int ns = h->uniform_leaf, R = h->near_rb * (ns / 2) / NEAR_NT;

@@ -48,12 +48,17 @@ class CudaPlanEngine:
         g = np.ascontiguousarray(getattr(plan, "gather", np.zeros(0, np.int32)), dtype=np.int32)
         _abi.check(L.h2b_plan_set_gather(h, g.ctypes.data_as(C.POINTER(C.c_int32)), int(g.size)),
                    "h2b_plan_set_gather")
-        for ph in PHASES:
+        for ph in sorted(plan.phases):
             counts, items, segs = plan.phases[ph]
             _abi.check(L.h2b_plan_set_phase(h, ph, int(counts.size),
                                             counts.ctypes.data_as(C.POINTER(C.c_int64)),
                                             items.ctypes.data, int(items.size), segs.ctypes.data,
                                             int(segs.size)), "h2b_plan_set_phase")
+        nf = getattr(plan, "near_fast", None)
+        if nf is not None and nf["items"].size:  # q = 1 near-field on the streaming kernel
+            _abi.check(L.h2b_plan_set_near_fast(h, nf["items"].ctypes.data, int(nf["items"].size),
+                                                nf["blks"].ctypes.data, int(nf["blks"].size),
+                                                int(nf["ns"]), int(nf["R"])), "h2b_plan_set_near_fast")
 
     def set_peers(self, ptrs):
         arr = (C.c_void_p * max(1, len(ptrs)))(*ptrs)

@@ -35,6 +35,7 @@ import numpy as np
 
 MM_M, MM_K = 64, 32
 PH_UP_OWN, PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR = 0, 1, 2, 3, 4
+PH_LEAFBACK = 5  # leaf back-transform alone (accumulating), after the fast q=1 near-field
 PHASES = (PH_UP_OWN, PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR)
 PAY_VT, PAY_TT, PAY_T, PAY_S, PAY_D, PAY_V = 0, 1, 2, 3, 4, 5
 N_PAY = 6
@@ -88,7 +89,9 @@ def partition(pk, G: int) -> Partition:
             local[c] = kown[owner[c]]
             kown[owner[c]] += pk.c_rank[c]
     nmax = int(nrows.max())
+    nmax += nmax & 1  # even: x rows of every leaf stay 32-byte aligned (256-bit loads)
     chunk = nmax + int(kown.max())
+    chunk += chunk & 1
     hat = np.full(P, -1, dtype=np.int64)
     own = local >= 0
     hat[own] = owner[own] * chunk + nmax + local[own]
@@ -108,6 +111,7 @@ class ShardPlan:
     payloads: list                          # N_PAY complex128 arrays
     phases: dict = field(default_factory=dict)  # phase -> (launch_counts, items, segs)
     gather: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))  # gathered B rows
+    near_fast: dict | None = None  # q=1 near-field work lists for the streaming kernel
 
     @property
     def row0(self):
@@ -280,6 +284,7 @@ def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = 
 
     Bd = _Builder()  # near-field + leaf back-transform of own leaves -> local y rows
     r0 = int(part.row0[g])
+    near_blocks, v_offs = {}, {}
     sample = None
     if pk.dbuf.size == 0 and pk.n_near:  # near-field not on the host: sample this rank's rows
         from .nearfield import assemble_block, geometry_arrays
@@ -303,7 +308,9 @@ def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = 
             else:
                 D = pk.dbuf[pk.d_off[b]:pk.d_off[b] + nt * ns].reshape(nt, ns)
             blocks.append((put(PAY_D, D), s, ns))
+        near_blocks[t] = [(off, xrow_leaf(s)) for off, s, _ in blocks]
         voff = put(PAY_V, V(t)) if k[t] > 0 else -1
+        v_offs[t] = voff
         for m0 in range(0, nt, MM_M):
             s0 = Bd.begin()
             for off, s, ns in blocks:
@@ -313,5 +320,39 @@ def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = 
             Bd.end(s0, int(pk.c_start[t]) - r0 + m0, min(MM_M, nt - m0), B_Y)
     phases[PH_NEAR] = Bd.done()
 
+    # q = 1: the same near-field on the streaming kernel (uniform 32/64-point leaves), the leaf
+    # back-transform as its own accumulating phase
+    own_leaves = np.nonzero(own & (lo_of < 0))[0]
+    sizes = {int(pk.c_size[t]) for t in own_leaves}
+    for t in own_leaves:
+        sizes.update(int(pk.c_size[s]) for s in pk.d_col[pk.d_row_ptr[t]:pk.d_row_ptr[t + 1]])
+    near_fast = None
+    Bd = _Builder()
+    for t in own_leaves:
+        if k[t] > 0:
+            nt = int(pk.c_size[t])
+            for m0 in range(0, nt, MM_M):
+                s0 = Bd.begin()
+                Bd.seg(PAY_V, v_offs[t], int(k[t]), m0, int(k[t]), B_YHAT, hat[t])
+                Bd.end(s0, int(pk.c_start[t]) - r0 + m0, min(MM_M, nt - m0), B_Y, acc=True)
+    phases[PH_LEAFBACK] = Bd.done()
+    if len(sizes) == 1 and sizes.pop() in (32, 64) and len(own_leaves):
+        from ._abi import NEAR_BLK, NEAR_ITEM
+        ns = int(pk.c_size[own_leaves[0]])
+        avg = np.mean([len(near_blocks[t]) for t in own_leaves])
+        R = 1
+        while R < 4 and R * 128 // (ns // 2) * ns * 16.0 * avg < 24e3:
+            R *= 2
+        rb = R * 128 // (ns // 2)
+        items, blks = [], []
+        for t in own_leaves:
+            first = len(blks)
+            blks.extend(near_blocks[t])
+            for row0 in range(0, ns, rb):
+                items.append((int(pk.c_start[t]) - r0 + row0, first, len(near_blocks[t]), row0, 0))
+        near_fast = dict(items=np.array(items, dtype=NEAR_ITEM), blks=np.array(blks, dtype=NEAR_BLK),
+                         ns=ns, R=R)
+
     payloads = [np.concatenate(a) if a else np.zeros(0, np.complex128) for a in pays]
-    return ShardPlan(rank=g, part=part, payloads=payloads, phases=phases, gather=gather)
+    return ShardPlan(rank=g, part=part, payloads=payloads, phases=phases, gather=gather,
+                     near_fast=near_fast)
