@@ -248,6 +248,12 @@ int h2b_plan_run(h2b_plan_handle p, int phase, const void* x, const void* xhat, 
  * overwrites y with the near-field and then runs phase 5 (the leaf back-transform items). */
 int h2b_plan_set_near_fast(h2b_plan_handle p, const void* items, int64_t n_items, const void* blks,
                            int64_t n_blks, int ns, int rows_per_thread);
+/* q = 1 coupling of a plan on the panel kernels: payload 3 holds, per target, the stacked Sᵀ
+ * panel (Σ k_s) x k_t; items {int64 panel, xcol, out; int32 R, w} (out = x̂/ŷ row of the
+ * target), xcol = the gathered x̂ row of every panel row.  When set, h2b_plan_run(phase 2, q = 1)
+ * runs them instead of the phase's items. */
+int h2b_plan_set_couple_fast(h2b_plan_handle p, const void* items, int64_t n_items, const int32_t* xcol,
+                             int64_t n_xcol);
 /* Row-index table of gathered segments (set before h2b_plan_set_phase validates them). */
 int h2b_plan_set_gather(h2b_plan_handle p, const int32_t* idx, int64_t n);
 int h2b_plan_destroy(h2b_plan_handle p);

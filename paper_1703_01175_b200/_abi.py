@@ -25,7 +25,7 @@ EXPORTED = (
     "h2b_plan_destroy", "h2b_plan_device_bytes", "h2b_assemble_near", "h2b_plan_set_peers",
     "h2b_plan_bcast_rows", "h2b_ipc_get_handle", "h2b_ipc_open", "h2b_ipc_close",
     "h2b_plan_set_peer_offset", "h2b_device_alloc", "h2b_device_free", "h2b_plan_set_gather",
-    "h2b_plan_set_near_fast",
+    "h2b_plan_set_near_fast", "h2b_plan_set_couple_fast",
 )
 OPT_GRAPHS, OPT_MEGA, OPT_TRACE, OPT_DEBUG, OPT_MRHS = 1, 2, 3, 4, 5
 Q_LAUNCHES_Q1, Q_SPAN_MODE, Q_SPLIT_LEVEL, Q_TOP_STAGED, Q_DEVICE_BYTES = 1, 2, 3, 4, 5
@@ -66,6 +66,7 @@ MM_SEG = _np.dtype([("a_off", "<i8"), ("b_row", "<i8"), ("k", "<i4"), ("lda", "<
 NEAR_ITEM = _np.dtype([("y_off", "<i8"), ("b_first", "<i4"), ("nb", "<i4"), ("row0", "<i4"),
                       ("pad", "<i4")])
 NEAR_BLK = _np.dtype([("d_off", "<i8"), ("x_off", "<i8")])
+COUPLE_ITEM = _np.dtype([("panel", "<i8"), ("xcol", "<i8"), ("out", "<i8"), ("R", "<i4"), ("w", "<i4")])
 B_X, B_XHAT, B_YHAT, B_Y = 0, 1, 2, 3
 ITEM_ACC, ITEM_BCAST = 256, 512
 
@@ -128,6 +129,7 @@ def lib():
     L.h2b_ipc_close.argtypes = [vp]
     L.h2b_plan_set_peer_offset.argtypes = [vp, C.c_int64]
     L.h2b_plan_set_gather.argtypes = [vp, C.POINTER(C.c_int32), C.c_int64]
+    L.h2b_plan_set_couple_fast.argtypes = [vp, vp, C.c_int64, C.POINTER(C.c_int32), C.c_int64]
     L.h2b_plan_set_near_fast.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, C.c_int, C.c_int]
     L.h2b_device_alloc.argtypes = [C.c_int, C.c_size_t, C.POINTER(vp)]
     L.h2b_device_free.argtypes = [vp]

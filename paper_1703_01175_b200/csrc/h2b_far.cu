@@ -207,6 +207,18 @@ int h2b_launch_span(h2b_ctx* h, const SpanLaunch& L, bool up, const double2* xp,
   return H2B_OK;
 }
 
+// q = 1 coupling on explicit work lists (plan handles): Sᵀ panels in `sbuf`, gathered x̂ rows
+int h2b_launch_couple_list(const CoupleItem* items, int n, const double2* sbuf, const int32_t* xcol,
+                           const double2* xhat, double2* yhat, int warp_mode, cudaStream_t st) {
+  if (n <= 0) return H2B_OK;
+  if (warp_mode)
+    k_couple_warp<<<(n + NT / 32 - 1) / (NT / 32), NT, 0, st>>>(items, n, sbuf, xcol, xhat, yhat);
+  else
+    k_couple_cta<<<n, NT, 0, st>>>(items, sbuf, xcol, xhat, yhat);
+  H2B_CHECK_LAUNCH();
+  return H2B_OK;
+}
+
 int h2b_launch_coupling(h2b_ctx* h, int q, cudaStream_t st) {
   const double2* sbuf = h->buf[H2B_SEC_S];
   if (q == 1) {

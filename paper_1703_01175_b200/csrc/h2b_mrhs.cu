@@ -35,6 +35,9 @@
 int h2b_launch_near_list(const NearItem* items, int n_items, const NearBlk* blks, const double2* dbuf,
                          const double2* x, double2* y, int ns, int R, cudaStream_t st);
 int h2b_near_rows_per_item(int ns, int r);
+// h2b_far.cu: the q = 1 coupling kernels on explicit work lists
+int h2b_launch_couple_list(const CoupleItem* items, int n, const double2* sbuf, const int32_t* xcol,
+                           const double2* xhat, double2* yhat, int warp_mode, cudaStream_t st);
 
 namespace {
 
@@ -689,6 +692,10 @@ struct h2b_plan_ctx {
   NearItem* nf_items = nullptr;
   NearBlk* nf_blks = nullptr;
   int nf_n = 0, nf_ns = 0, nf_r = 0;
+  // q = 1 coupling on the panel kernels (h2b_plan_set_couple_fast): payload 3 holds Sᵀ panels
+  CoupleItem* cf_items = nullptr;
+  int32_t* cf_xcol = nullptr;
+  int cf_n = 0, cf_warp = 0;
 };
 
 extern "C" int h2b_plan_create(int device, int n_payloads, const int64_t* payload_elems,
@@ -810,6 +817,9 @@ extern "C" int h2b_plan_run(h2b_plan_handle p, int phase, const void* x, const v
   for (int i = 0; i < p->npeers; ++i) bf.peers[i] = p->peers[i] + p->peer_off;
   bf.npeers = p->npeers;
   int nl = 0;
+  if (phase == 2 && q == 1 && p->cf_n > 0)
+    return h2b_launch_couple_list(p->cf_items, p->cf_n, p->pay[3], p->cf_xcol, bf.b[B_XHAT], bf.b[B_YHAT],
+                                  p->cf_warp, (cudaStream_t)stream);
   if (phase == 4 && q == 1 && p->nf_n > 0) {
     H2B_TRY(h2b_launch_near_list(p->nf_items, p->nf_n, p->nf_blks, p->pay[4], bf.b[B_X], bf.y, p->nf_ns,
                                  p->nf_r, (cudaStream_t)stream));
@@ -901,6 +911,38 @@ extern "C" int h2b_plan_set_near_fast(h2b_plan_handle p, const void* items, int6
   return H2B_OK;
 }
 
+extern "C" int h2b_plan_set_couple_fast(h2b_plan_handle p, const void* items, int64_t n_items,
+                                        const int32_t* xcol, int64_t n_xcol) {
+  if (!p || n_items < 0 || n_xcol < 0 || (n_items && !items) || (n_xcol && !xcol) || p->n_payloads < 4 ||
+      n_items > (1 << 30)) {
+    h2b_set_error("h2b_plan_set_couple_fast: bad arguments (payload 3 = coupling panels)");
+    return H2B_EINVAL;
+  }
+  const CoupleItem* it = (const CoupleItem*)items;
+  int64_t elems = 0;
+  for (int64_t i = 0; i < n_items; ++i) {  // the kernels trust the lists
+    if (it[i].R < 0 || it[i].w < 0 || it[i].xcol < 0 || it[i].xcol + it[i].R > n_xcol || it[i].panel < 0 ||
+        it[i].panel + (int64_t)it[i].R * it[i].w > p->pay_elems[3] || it[i].out < 0) {
+      h2b_set_error("h2b_plan_set_couple_fast: item " + std::to_string(i) + " out of range");
+      return H2B_EINVAL;
+    }
+    elems += (int64_t)it[i].R * it[i].w;
+  }
+  H2B_CUDA_TRY(cudaSetDevice(p->device));
+  cudaFree(p->cf_items);
+  cudaFree(p->cf_xcol);
+  p->cf_items = nullptr;
+  p->cf_xcol = nullptr;
+  p->cf_n = 0;
+  H2B_CUDA_TRY(cudaMalloc(&p->cf_items, sizeof(CoupleItem) * std::max<int64_t>(n_items, 1)));
+  H2B_CUDA_TRY(cudaMalloc(&p->cf_xcol, sizeof(int32_t) * std::max<int64_t>(n_xcol, 1)));
+  if (n_items) H2B_CUDA_TRY(cudaMemcpy(p->cf_items, items, sizeof(CoupleItem) * n_items, cudaMemcpyHostToDevice));
+  if (n_xcol) H2B_CUDA_TRY(cudaMemcpy(p->cf_xcol, xcol, sizeof(int32_t) * n_xcol, cudaMemcpyHostToDevice));
+  p->cf_n = (int)n_items;
+  p->cf_warp = (n_items > 0 && elems / n_items < 4096) ? 1 : 0;  // as the single-GPU planner
+  return H2B_OK;
+}
+
 extern "C" int h2b_plan_set_gather(h2b_plan_handle p, const int32_t* idx, int64_t n) {
   if (!p || n < 0 || (n && !idx)) {
     h2b_set_error("h2b_plan_set_gather: bad arguments");
@@ -982,6 +1024,8 @@ extern "C" int h2b_plan_destroy(h2b_plan_handle p) {
   if (p->gather) cudaFree(p->gather);
   cudaFree(p->nf_items);
   cudaFree(p->nf_blks);
+  cudaFree(p->cf_items);
+  cudaFree(p->cf_xcol);
   delete p;
   return H2B_OK;
 }

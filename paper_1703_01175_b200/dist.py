@@ -54,6 +54,11 @@ class CudaPlanEngine:
                                             counts.ctypes.data_as(C.POINTER(C.c_int64)),
                                             items.ctypes.data, int(items.size), segs.ctypes.data,
                                             int(segs.size)), "h2b_plan_set_phase")
+        cf = getattr(plan, "couple_fast", None)
+        if cf is not None and cf["items"].size:  # q = 1 coupling on the panel kernels
+            _abi.check(L.h2b_plan_set_couple_fast(h, cf["items"].ctypes.data, int(cf["items"].size),
+                                                  cf["xcol"].ctypes.data_as(C.POINTER(C.c_int32)),
+                                                  int(cf["xcol"].size)), "h2b_plan_set_couple_fast")
         nf = getattr(plan, "near_fast", None)
         if nf is not None and nf["items"].size:  # q = 1 near-field on the streaming kernel
             _abi.check(L.h2b_plan_set_near_fast(h, nf["items"].ctypes.data, int(nf["items"].size),

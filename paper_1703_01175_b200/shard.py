@@ -41,7 +41,7 @@ PAY_VT, PAY_TT, PAY_T, PAY_S, PAY_D, PAY_V = 0, 1, 2, 3, 4, 5
 N_PAY = 6
 B_X, B_XHAT, B_YHAT, B_Y = 0, 1, 2, 3
 ITEM_ACC, ITEM_BCAST = 256, 512
-SEG_GATHER = 512
+SEG_TRANS, SEG_GATHER = 256, 512
 
 
 @dataclass
@@ -112,6 +112,7 @@ class ShardPlan:
     phases: dict = field(default_factory=dict)  # phase -> (launch_counts, items, segs)
     gather: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))  # gathered B rows
     near_fast: dict | None = None  # q=1 near-field work lists for the streaming kernel
+    couple_fast: dict | None = None  # q=1 coupling work lists for the panel kernels
 
     @property
     def row0(self):
@@ -132,10 +133,14 @@ class _Builder:
         self.items, self.segs, self.counts = [], [], []
         self._first = 0
 
-    def seg(self, a_src, a_off, lda, m0, k, b_src, b_row, gather=False):
+    def seg(self, a_src, a_off, lda, m0, k, b_src, b_row, gather=False, trans=False):
+        """K-chunks of one A block: row-major A[i][j] = p[a_off + (m0+i)*lda + j], or transposed
+        (A[i][j] = p[a_off + j*lda + m0 + i])."""
         for k0 in range(0, k, MM_K):
-            self.segs.append((a_off + m0 * lda + k0, b_row + k0, min(MM_K, k - k0), lda,
-                              a_src | (b_src << 4) | (SEG_GATHER if gather else 0), 0))
+            off = a_off + (k0 * lda + m0 if trans else m0 * lda + k0)
+            self.segs.append((off, b_row + k0, min(MM_K, k - k0), lda,
+                              a_src | (b_src << 4) | (SEG_GATHER if gather else 0)
+                              | (SEG_TRANS if trans else 0), 0))
 
     def begin(self):
         return len(self.segs)
@@ -231,7 +236,11 @@ def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = 
     phases[PH_UP_TOP] = Bd.done()
 
     Bd = _Builder()  # coupling: every own/top target with k > 0 (zero when it has no block)
-    gat, n_gat = [], 0  # gathered x̂ rows (panel mode): the sources of a target, concatenated
+    # payload 3 holds, per target, the stacked transposed panel [S_t,s1ᵀ; S_t,s2ᵀ; ...]
+    # ((Σ k_s) x k_t, the single-GPU layout): the q = 1 panel kernels read it with gathered x̂
+    # rows, the grouped kernels as transposed segments (one per source, or one gathered panel)
+    gat, n_gat = [], 0            # gathered x̂ rows (panel mode)
+    cf_items, cf_xcol, n_xcol = [], [], 0
     for t in np.nonzero(mine & (k > 0))[0]:
         kt = int(k[t])
         blocks = []
@@ -241,26 +250,31 @@ def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = 
                 continue
             blocks.append((pk.sbuf[pk.s_off[b]:pk.s_off[b] + kt * k[s]].reshape(kt, int(k[s])), s))
         R = sum(B.shape[1] for B, _ in blocks)
-        if couple_panels and R:
-            # one row-major panel [S_t,s1 | S_t,s2 | ...] (k_t x R) against gathered x̂ rows:
-            # full 32-wide K chunks (best for the DMMA path, q >= 2)
-            off = put(PAY_S, np.concatenate([B for B, _ in blocks], axis=1))
-            gat.extend(np.arange(hat[s], hat[s] + k[s]) for _, s in blocks)
-            for m0 in range(0, kt, MM_M):
-                s0 = Bd.begin()
-                Bd.seg(PAY_S, off, R, m0, R, B_XHAT, n_gat, gather=True)
-                Bd.end(s0, hat[t] + m0, min(MM_M, kt - m0), B_YHAT)
-            n_gat += R
-            continue
-        # one segment per source block, contiguous x̂ rows (best for the GEMV path, q = 1)
-        offs = [(put(PAY_S, B), s) for B, s in blocks]
+        panel = put(PAY_S, np.concatenate([B.T for B, _ in blocks], axis=0)) if R else 0
+        rows = [np.arange(hat[s], hat[s] + k[s]) for _, s in blocks]
+        cf_items.append((panel, n_xcol, int(hat[t]), R, kt))
+        cf_xcol.extend(rows)
+        n_xcol += R
         for m0 in range(0, kt, MM_M):
             s0 = Bd.begin()
-            for off, s in offs:
-                Bd.seg(PAY_S, off, int(k[s]), m0, int(k[s]), B_XHAT, hat[s])
+            if couple_panels and R:
+                Bd.seg(PAY_S, panel, kt, m0, R, B_XHAT, n_gat, gather=True, trans=True)
+            else:
+                r = 0
+                for B, s in blocks:
+                    ks = int(k[s])
+                    Bd.seg(PAY_S, panel + r * kt, kt, m0, ks, B_XHAT, hat[s], trans=True)
+                    r += ks
             Bd.end(s0, hat[t] + m0, min(MM_M, kt - m0), B_YHAT)
+        if couple_panels and R:
+            gat.extend(rows)
+            n_gat += R
     phases[PH_COUPLE] = Bd.done()
     gather = (np.concatenate(gat).astype(np.int32) if gat else np.zeros(0, np.int32))
+    from ._abi import COUPLE_ITEM
+    couple_fast = dict(items=np.array(cf_items, dtype=COUPLE_ITEM),
+                       xcol=(np.concatenate(cf_xcol).astype(np.int32) if cf_xcol
+                             else np.zeros(0, np.int32)))
 
     Bd = _Builder()  # downward, root first: [ŷ_lo; ŷ_hi] += [T_lo; T_hi] ŷ_c
     for lvl in range(pk.depth - 1):
@@ -355,4 +369,4 @@ def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = 
 
     payloads = [np.concatenate(a) if a else np.zeros(0, np.complex128) for a in pays]
     return ShardPlan(rank=g, part=part, payloads=payloads, phases=phases, gather=gather,
-                     near_fast=near_fast)
+                     near_fast=near_fast, couple_fast=couple_fast)
