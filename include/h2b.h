@@ -272,6 +272,20 @@ int h2b_plan_set_peer_offset(h2b_plan_handle p, int64_t elems);
 /* Plain device allocations (exchange buffers to be shared with CUDA IPC), zero-filled. */
 int h2b_device_alloc(int device, size_t bytes, void** out);
 int h2b_device_free(void* ptr);
+/* Structure-exact operators (benchmarks): seeded synthetic payload values from a counter-based
+ * generator value(seed, section, global index) — identical wherever a block is materialised.
+ * Raw: dev_ptr[e] = value(section, global_off + e).  Plan: descriptors {plan_off, global_off,
+ * rows, cols, transposed, section} (n x 6 int64, host), each writing a rows x cols global block
+ * as-is or transposed at plan_off of `payload`. */
+int h2b_fill_synthetic_raw(void* dev_ptr, int64_t n, int64_t global_off, int section, uint64_t seed,
+                           double scale);
+int h2b_plan_fill_synthetic(h2b_plan_handle p, int payload, const int64_t* desc, int64_t n_desc,
+                            uint64_t seed, double scale);
+/* Near-field blocks of a plan sampled on the device: descriptors {plan_off, t_start, nt,
+ * s_start, ns} (permuted index space, host), perm / centers / chi as in h2b_assemble_near. */
+int h2b_plan_fill_near(h2b_plan_handle p, int payload, const int64_t* desc, int64_t n_desc,
+                       const int64_t* perm, int64_t n, const double* centers, const double* chi,
+                       double k0, double volume, double diag_re, double diag_im);
 /* CUDA IPC of a device buffer between the ranks' processes (64-byte handle). */
 int h2b_ipc_get_handle(const void* dev_ptr, void* handle_out);
 int h2b_ipc_open(const void* handle, void** dev_ptr_out);

@@ -25,7 +25,8 @@ EXPORTED = (
     "h2b_plan_destroy", "h2b_plan_device_bytes", "h2b_assemble_near", "h2b_plan_set_peers",
     "h2b_plan_bcast_rows", "h2b_ipc_get_handle", "h2b_ipc_open", "h2b_ipc_close",
     "h2b_plan_set_peer_offset", "h2b_device_alloc", "h2b_device_free", "h2b_plan_set_gather",
-    "h2b_plan_set_near_fast", "h2b_plan_set_couple_fast",
+    "h2b_plan_set_near_fast", "h2b_plan_set_couple_fast", "h2b_fill_synthetic_raw",
+    "h2b_plan_fill_synthetic", "h2b_plan_fill_near",
 )
 OPT_GRAPHS, OPT_MEGA, OPT_TRACE, OPT_DEBUG, OPT_MRHS = 1, 2, 3, 4, 5
 Q_LAUNCHES_Q1, Q_SPAN_MODE, Q_SPLIT_LEVEL, Q_TOP_STAGED, Q_DEVICE_BYTES = 1, 2, 3, 4, 5
@@ -129,6 +130,10 @@ def lib():
     L.h2b_ipc_close.argtypes = [vp]
     L.h2b_plan_set_peer_offset.argtypes = [vp, C.c_int64]
     L.h2b_plan_set_gather.argtypes = [vp, C.POINTER(C.c_int32), C.c_int64]
+    L.h2b_fill_synthetic_raw.argtypes = [vp, C.c_int64, C.c_int64, C.c_int, C.c_uint64, C.c_double]
+    L.h2b_plan_fill_synthetic.argtypes = [vp, C.c_int, vp, C.c_int64, C.c_uint64, C.c_double]
+    L.h2b_plan_fill_near.argtypes = [vp, C.c_int, vp, C.c_int64, vp, C.c_int64, vp, vp, C.c_double,
+                                     C.c_double, C.c_double, C.c_double]
     L.h2b_plan_set_couple_fast.argtypes = [vp, vp, C.c_int64, C.POINTER(C.c_int32), C.c_int64]
     L.h2b_plan_set_near_fast.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, C.c_int, C.c_int]
     L.h2b_device_alloc.argtypes = [C.c_int, C.c_size_t, C.POINTER(vp)]

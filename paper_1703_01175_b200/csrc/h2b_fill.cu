@@ -1,0 +1,197 @@
+// Device-side payload generation for structure-exact operators and shard plans.
+//
+// * Seeded far-field values: a counter-based generator — value(seed, section, global index) —
+//   so that a payload block gets the same values wherever it is materialised: in the single-GPU
+//   handle's V/T/S sections (identity layout) or, copied / transposed, in any rank's shard plan
+//   payload.  A partitioned operator then equals the single-GPU one element for element.
+//   value = scale * (u1 - 1/2, u2 - 1/2) * 2, (u1, u2) the two 32-bit halves of
+//   splitmix64(seed ^ section << 56 ^ index * golden) / 2^32  (exact in double: numpy restates it
+//   bit for bit in paper_1703_01175_b200/synthetic.py).
+// * Near-field blocks of a shard plan sampled from the geometry (the h2b_assemble_near formula,
+//   restating the reference sampler _kernel_core.pyx:13-47), written at plan offsets.
+#include "h2b_common.cuh"
+
+namespace {
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ double2 synth_value(uint64_t seed, int sec, uint64_t idx, double scale) {
+  const uint64_t h = splitmix64(seed ^ ((uint64_t)sec << 56) ^ (idx * 0x9E3779B97F4A7C15ull));
+  const double u1 = (double)(uint32_t)(h >> 32) * (1.0 / 4294967296.0);
+  const double u2 = (double)(uint32_t)h * (1.0 / 4294967296.0);
+  return make_double2((u1 - 0.5) * 2.0 * scale, (u2 - 0.5) * 2.0 * scale);
+}
+
+// identity layout: out[e] = value(sec, goff + e)
+__global__ void k_fill_raw(double2* out, int64_t n, uint64_t goff, int sec, uint64_t seed, double scale) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = synth_value(seed, sec, goff + e, scale);
+}
+
+// block descriptors {plan_off, global_off, rows, cols, trans, sec}: global block G (rows x cols,
+// row-major at global_off of section sec) stored as-is or transposed at plan_off
+__global__ void k_fill_blocks(double2* out, const int64_t* __restrict__ desc, uint64_t seed, double scale) {
+  const int64_t* d = desc + 6 * blockIdx.x;
+  const int64_t p0 = d[0], g0 = d[1], r = d[2], c = d[3];
+  const bool tr = d[4] != 0;
+  const int sec = (int)d[5];
+  for (int64_t e = threadIdx.x; e < r * c; e += blockDim.x) {
+    const int64_t i = e / c, j = e - i * c;
+    out[tr ? p0 + j * r + i : p0 + e] = synth_value(seed, sec, (uint64_t)(g0 + e), scale);
+  }
+}
+
+// near-field descriptors {plan_off, t_start, nt, s_start, ns} (permuted index space)
+__global__ void k_fill_near(double2* out, const int64_t* __restrict__ desc, const int64_t* __restrict__ perm,
+                            const double* __restrict__ centers, const double2* __restrict__ chi, double k0,
+                            double coef, double2 diag, unsigned long long* bad) {
+  const int64_t* d = desc + 5 * blockIdx.x;
+  const int64_t p0 = d[0], t0 = d[1], nt = d[2], s0 = d[3], ns = d[4];
+  for (int64_t e = threadIdx.x; e < nt * ns; e += blockDim.x) {
+    const int64_t i = e / ns, j = e - i * ns;
+    const int64_t m = perm[t0 + i], n = perm[s0 + j];
+    const double2 cn = chi[n];
+    double2 v;
+    if (m == n) {
+      v = make_double2(1.0 - (cn.x * diag.x - cn.y * diag.y), -(cn.x * diag.y + cn.y * diag.x));
+    } else {
+      const double dx = centers[3 * m] - centers[3 * n];
+      const double dy = centers[3 * m + 1] - centers[3 * n + 1];
+      const double dz = centers[3 * m + 2] - centers[3 * n + 2];
+      const double rr = sqrt(dx * dx + dy * dy + dz * dz);
+      if (rr == 0.0) {
+        atomicMin(bad, (unsigned long long)blockIdx.x);
+        v = make_double2(0.0, 0.0);
+      } else {
+        const double amp = coef / rr;
+        double sn, cs;
+        sincos(k0 * rr, &sn, &cs);
+        const double ar = amp * cs, ai = -(amp * sn);
+        v = make_double2(-(cn.x * ar - cn.y * ai), -(cn.x * ai + cn.y * ar));
+      }
+    }
+    out[p0 + e] = v;
+  }
+}
+
+template <class T>
+int to_dev(T** d, const T* h, int64_t n) {
+  H2B_CUDA_TRY(cudaMalloc(d, sizeof(T) * std::max<int64_t>(n, 1)));
+  if (n) H2B_CUDA_TRY(cudaMemcpy(*d, h, sizeof(T) * n, cudaMemcpyHostToDevice));
+  return H2B_OK;
+}
+
+}  // namespace
+
+extern "C" int h2b_fill_synthetic_raw(void* dev_ptr, int64_t n, int64_t global_off, int section, uint64_t seed,
+                                      double scale) {
+  if (!dev_ptr || n < 0 || global_off < 0) {
+    h2b_set_error("h2b_fill_synthetic_raw: bad arguments");
+    return H2B_EINVAL;
+  }
+  if (n == 0) return H2B_OK;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  k_fill_raw<<<grid, 256>>>((double2*)dev_ptr, n, (uint64_t)global_off, section, seed, scale);
+  H2B_CHECK_LAUNCH();
+  H2B_CUDA_TRY(cudaDeviceSynchronize());
+  return H2B_OK;
+}
+
+// implemented in h2b_mrhs.cu (plan internals)
+double2* h2b_plan_payload(h2b_plan_handle p, int payload, int64_t* elems, int* device);
+
+extern "C" int h2b_plan_fill_synthetic(h2b_plan_handle p, int payload, const int64_t* desc, int64_t n_desc,
+                                       uint64_t seed, double scale) {
+  int64_t elems = 0;
+  int dev = 0;
+  double2* out = h2b_plan_payload(p, payload, &elems, &dev);
+  if (!out || n_desc < 0 || (n_desc && !desc)) {
+    h2b_set_error("h2b_plan_fill_synthetic: bad arguments");
+    return H2B_EINVAL;
+  }
+  for (int64_t i = 0; i < n_desc; ++i) {
+    const int64_t* d = desc + 6 * i;
+    if (d[0] < 0 || d[1] < 0 || d[2] < 0 || d[3] < 0 || d[0] + d[2] * d[3] > elems) {
+      h2b_set_error("h2b_plan_fill_synthetic: descriptor " + std::to_string(i) + " out of range");
+      return H2B_EINVAL;
+    }
+  }
+  if (n_desc == 0) return H2B_OK;
+  H2B_CUDA_TRY(cudaSetDevice(dev));
+  int64_t* dd = nullptr;
+  for (int64_t i0 = 0; i0 < n_desc; i0 += 65535) {
+    const int64_t cnt = std::min<int64_t>(65535, n_desc - i0);
+    H2B_TRY(to_dev(&dd, desc + 6 * i0, 6 * cnt));
+    k_fill_blocks<<<(int)cnt, 256>>>(out, dd, seed, scale);
+    cudaError_t e = cudaGetLastError();
+    cudaFree(dd);
+    if (e != cudaSuccess) {
+      h2b_set_error(std::string("h2b_plan_fill_synthetic: ") + cudaGetErrorString(e));
+      return H2B_ECUDA;
+    }
+  }
+  H2B_CUDA_TRY(cudaDeviceSynchronize());
+  return H2B_OK;
+}
+
+extern "C" int h2b_plan_fill_near(h2b_plan_handle p, int payload, const int64_t* desc, int64_t n_desc,
+                                  const int64_t* perm, int64_t n, const double* centers, const double* chi,
+                                  double k0, double volume, double diag_re, double diag_im) {
+  int64_t elems = 0;
+  int dev = 0;
+  double2* out = h2b_plan_payload(p, payload, &elems, &dev);
+  if (!out || n_desc < 0 || (n_desc && !desc) || !perm || !centers || !chi || n <= 0 || !(volume > 0)) {
+    h2b_set_error("h2b_plan_fill_near: bad arguments");
+    return H2B_EINVAL;
+  }
+  for (int64_t i = 0; i < n_desc; ++i) {
+    const int64_t* d = desc + 5 * i;
+    if (d[0] < 0 || d[1] < 0 || d[3] < 0 || d[1] + d[2] > n || d[3] + d[4] > n || d[0] + d[2] * d[4] > elems) {
+      h2b_set_error("h2b_plan_fill_near: descriptor " + std::to_string(i) + " out of range");
+      return H2B_EINVAL;
+    }
+  }
+  if (n_desc == 0) return H2B_OK;
+  H2B_CUDA_TRY(cudaSetDevice(dev));
+  int64_t *dperm = nullptr, *dd = nullptr;
+  double* dc = nullptr;
+  double2* dchi = nullptr;
+  unsigned long long* bad = nullptr;
+  const unsigned long long none = ~0ull;
+  H2B_TRY(to_dev(&dperm, perm, n));
+  H2B_TRY(to_dev(&dc, centers, 3 * n));
+  H2B_TRY(to_dev(&dchi, (const double2*)chi, n));
+  H2B_TRY(to_dev(&bad, &none, 1));
+  const double coef = k0 * k0 * volume / 12.566370614359172953850573533118;
+  int rc = H2B_OK;
+  for (int64_t i0 = 0; i0 < n_desc && !rc; i0 += 65535) {
+    const int64_t cnt = std::min<int64_t>(65535, n_desc - i0);
+    rc = to_dev(&dd, desc + 5 * i0, 5 * cnt);
+    if (rc) break;
+    k_fill_near<<<(int)cnt, 256>>>(out, dd, dperm, dc, dchi, k0, coef, make_double2(diag_re, diag_im), bad);
+    cudaError_t e = cudaGetLastError();
+    cudaDeviceSynchronize();
+    cudaFree(dd);
+    if (e != cudaSuccess) {
+      h2b_set_error(std::string("h2b_plan_fill_near: ") + cudaGetErrorString(e));
+      rc = H2B_ECUDA;
+    }
+  }
+  unsigned long long first = none;
+  if (!rc) cudaMemcpy(&first, bad, sizeof(first), cudaMemcpyDeviceToHost);
+  cudaFree(dperm);
+  cudaFree(dc);
+  cudaFree(dchi);
+  cudaFree(bad);
+  if (rc) return rc;
+  if (first != none) {
+    h2b_set_error("h2b_plan_fill_near: coincident voxel centres (kernel singular)");
+    return H2B_EINVAL;
+  }
+  return H2B_OK;
+}

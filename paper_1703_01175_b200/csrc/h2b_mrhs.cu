@@ -873,6 +873,14 @@ extern "C" int h2b_plan_bcast_rows(h2b_plan_handle p, const void* buf, int64_t r
   return H2B_OK;
 }
 
+// payload access for the fill kernels (h2b_fill.cu)
+double2* h2b_plan_payload(h2b_plan_handle p, int payload, int64_t* elems, int* device) {
+  if (!p || payload < 0 || payload >= p->n_payloads) return nullptr;
+  *elems = p->pay_elems[payload];
+  *device = p->device;
+  return p->pay[payload];
+}
+
 extern "C" int h2b_plan_set_near_fast(h2b_plan_handle p, const void* items, int64_t n_items, const void* blks,
                                       int64_t n_blks, int ns, int rows_per_thread) {
   if (!p || n_items < 0 || n_blks < 0 || (n_items && (!items || !blks)) || p->n_payloads < 5 ||

@@ -36,7 +36,8 @@ class CudaPlanEngine:
     def __init__(self, plan, device):
         L = _abi.lib()
         self.device = int(device)
-        elems = (C.c_int64 * N_PAY)(*[int(a.size) for a in plan.payloads])
+        sizes = plan.payload_sizes() if hasattr(plan, "payload_sizes") else [int(a.size) for a in plan.payloads]
+        elems = (C.c_int64 * N_PAY)(*sizes)
         h = C.c_void_p()
         _abi.check(L.h2b_plan_create(self.device, N_PAY, elems, C.byref(h)), "h2b_plan_create")
         self.handle = h
@@ -45,6 +46,28 @@ class CudaPlanEngine:
             for off in range(0, b.size, _UPLOAD_CHUNK):
                 ch = b[off:off + _UPLOAD_CHUNK]
                 _abi.check(L.h2b_plan_upload(h, i, ch.ctypes.data, ch.size, off), "h2b_plan_upload")
+        fills = getattr(plan, "fills", None)
+        if fills is not None:  # structure-exact payloads generated on this device
+            from .synthetic import SCALES
+            for i, d in enumerate(fills["synth"]):
+                if d.size:
+                    d = np.ascontiguousarray(d)
+                    sec = int(d[0, 5])
+                    _abi.check(L.h2b_plan_fill_synthetic(h, i, d.ctypes.data, int(d.shape[0]),
+                                                         int(fills["seed"]), SCALES[sec]),
+                               "h2b_plan_fill_synthetic")
+            if fills["near"].size:
+                from .nearfield import geometry_arrays, self_term
+                centers, chi, k0, vol = geometry_arrays(fills["geometry"])
+                diag = k0 ** 2 * self_term(vol, k0)
+                d = np.ascontiguousarray(fills["near"])
+                perm = np.ascontiguousarray(fills["perm"], dtype=np.int64)
+                centers = np.ascontiguousarray(centers, dtype=np.float64)
+                chi = np.ascontiguousarray(chi, dtype=np.complex128)
+                _abi.check(L.h2b_plan_fill_near(h, 4, d.ctypes.data, int(d.shape[0]), perm.ctypes.data,
+                                                int(perm.size), centers.ctypes.data, chi.ctypes.data,
+                                                float(k0), float(vol), float(diag.real), float(diag.imag)),
+                           "h2b_plan_fill_near")
         g = np.ascontiguousarray(getattr(plan, "gather", np.zeros(0, np.int32)), dtype=np.int32)
         _abi.check(L.h2b_plan_set_gather(h, g.ctypes.data_as(C.POINTER(C.c_int32)), int(g.size)),
                    "h2b_plan_set_gather")
@@ -126,7 +149,8 @@ class DistH2Operator:
             want_p2p = _peer_access_everywhere(group, torch.cuda.current_device() if device is None
                                                else int(device), self.world)
         self.exchange_mode = "p2p" if want_p2p else "allgather"
-        self.plan = plan_shard(pk, self.world, self.rank, self.part, bcast=want_p2p)
+        self.plan = plan_shard(pk, self.world, self.rank, self.part, bcast=want_p2p,
+                               device_payloads=engine is None)
         self.n = int(pk.n)
         self.row0, self.nrows = self.plan.row0, self.plan.nrows
         if engine is None:

@@ -337,8 +337,10 @@ def save_structure(pk: PackedH2, path, geometry, seed=0, note=""):
 
 
 def _synthetic_far_field(kw, spec):
-    """Seeded far-field payloads with the shapes implied by the tables (see save_structure)."""
-    rng = np.random.default_rng(int(spec.get("seed", 0)))
+    """Seeded far-field payloads with the shapes implied by the tables (see save_structure and
+    synthetic.py: the same values the device generates)."""
+    from .synthetic import SCALES, synth_values
+    seed = int(spec.get("seed", 0))
     rank, size, lo, hi = kw["c_rank"].astype(np.int64), kw["c_size"].astype(np.int64), \
         kw["c_child_lo"], kw["c_child_hi"]
     leaf = lo < 0
@@ -348,15 +350,8 @@ def _synthetic_far_field(kw, spec):
     P = rank.size
     rows = np.repeat(np.arange(P), np.diff(kw["s_row_ptr"]))
     es = int(np.sum(rank[rows] * rank[kw["s_col"]]))
-
-    def cplx(n, scale):
-        out = np.empty(n, dtype=np.complex128)
-        f = out.view(np.float64)
-        rng.standard_normal(out=f)
-        f *= scale
-        return out
-
-    return dict(vbuf=cplx(ev, 0.125), tbuf=cplx(et, 0.125), sbuf=cplx(es, 0.01))
+    return dict(vbuf=synth_values(seed, 0, 0, ev, SCALES[0]), tbuf=synth_values(seed, 1, 0, et, SCALES[1]),
+                sbuf=synth_values(seed, 2, 0, es, SCALES[2]))
 
 
 def load_packed(path, with_extra=False, near_on_host=True, far_on_host=True):

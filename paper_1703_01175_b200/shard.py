@@ -65,6 +65,11 @@ class Partition:
         return g * self.chunk + (i - int(self.row0[g]))
 
 
+def _with_far(pk, far):
+    import dataclasses
+    return dataclasses.replace(pk, **far)
+
+
 def partition(pk, G: int) -> Partition:
     if G < 1 or (G & (G - 1)):
         raise ValueError("the subtree partition needs a power-of-two number of ranks")
@@ -113,6 +118,7 @@ class ShardPlan:
     gather: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))  # gathered B rows
     near_fast: dict | None = None  # q=1 near-field work lists for the streaming kernel
     couple_fast: dict | None = None  # q=1 coupling work lists for the panel kernels
+    fills: dict | None = None  # device-generated payloads (sizes + block descriptors)
 
     @property
     def row0(self):
@@ -122,8 +128,14 @@ class ShardPlan:
     def nrows(self):
         return int(self.part.nrows[self.rank])
 
+    def payload_sizes(self):
+        """Complex elements of each payload (described blocks included)."""
+        if self.fills is not None:
+            return list(self.fills["sizes"])
+        return [int(a.size) for a in self.payloads]
+
     def payload_bytes(self):
-        return int(sum(a.nbytes for a in self.payloads))
+        return 16 * int(sum(self.payload_sizes()))
 
 
 class _Builder:
@@ -160,15 +172,45 @@ class _Builder:
                 np.array(self.items, dtype=self._it), np.array(self.segs, dtype=self._sg))
 
 
+class _GBlock:
+    """A payload block not materialised on the host: rows x cols of global section `sec` at
+    element `g0` (row-major), to be written as-is or transposed by the device generator."""
+
+    def __init__(self, sec, g0, rows, cols, trans=False):
+        self.sec, self.g0, self.rows, self.cols, self.trans = sec, int(g0), int(rows), int(cols), trans
+
+    @property
+    def T(self):
+        return _GBlock(self.sec, self.g0, self.rows, self.cols, not self.trans)
+
+    @property
+    def size(self):
+        return self.rows * self.cols
+
+
+class _NBlock:
+    """A near-field block sampled on the device: rows of leaf t, columns of leaf s."""
+
+    def __init__(self, t0, nt, s0, ns):
+        self.t0, self.nt, self.s0, self.ns = int(t0), int(nt), int(s0), int(ns)
+        self.size = self.nt * self.ns
+
+
+SEC_V, SEC_T, SEC_S = 0, 1, 2  # global sections of the synthetic generator (= libh2b H2B_SEC_*)
+
+
 def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = False,
-               couple_panels: bool = False) -> ShardPlan:
+               couple_panels: bool = False, device_payloads: bool = False) -> ShardPlan:
     """Payloads and work lists of rank g of G (see the module docstring).
 
     ``bcast``: the UP_OWN items also store their x̂ rows into every peer's exchange buffer
     (P2P stores over NVLink, libh2b ITEM_BCAST) — the all-gather of x̂ fused into the kernel that
     computes it; the x slice is pushed by ``h2b_plan_bcast_rows``.
     ``couple_panels``: each coupling row as one panel against gathered x̂ rows (full K chunks,
-    for multi-RHS use) instead of one segment per source block."""
+    for multi-RHS use) instead of one segment per source block.
+    ``device_payloads``: payloads the host does not hold (structure-exact operators: seeded far
+    field, near-field from geometry) are described, not materialised — the rank's device fills
+    them (libh2b h2b_plan_fill_synthetic / _near) with the values the single-GPU operator has."""
     part = part or partition(pk, G)
     if not 0 <= g < G:
         raise ValueError("rank out of range")
@@ -180,10 +222,22 @@ def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = 
     hat = part.hat
     pays = [[] for _ in range(N_PAY)]
     size = [0] * N_PAY
+    synth_fills = [[] for _ in range(N_PAY)]  # {plan_off, global_off, rows, cols, trans, sec}
+    near_fills = []                          # {plan_off, t_start, nt, s_start, ns}
+    far_dev = device_payloads and pk.sbuf.size == 0 and pk.vbuf.size == 0 and "synthetic" in pk.meta
+    near_dev = device_payloads and pk.dbuf.size == 0 and "geometry" in pk.meta
+    if not far_dev and pk.sbuf.size == 0 and pk.vbuf.size == 0 and "synthetic" in pk.meta:
+        from .synthetic import host_far_field  # CPU engines: the same values, on the host
+        pk = _with_far(pk, host_far_field(pk))
 
     def put(which, mat):
         off = size[which]
-        pays[which].append(np.ascontiguousarray(mat, dtype=np.complex128).ravel())
+        if isinstance(mat, _GBlock):
+            synth_fills[which].append((off, mat.g0, mat.rows, mat.cols, int(mat.trans), mat.sec))
+        elif isinstance(mat, _NBlock):
+            near_fills.append((off, mat.t0, mat.nt, mat.s0, mat.ns))
+        else:
+            pays[which].append(np.ascontiguousarray(mat, dtype=np.complex128).ravel())
         size[which] += mat.size
         return off
 
@@ -193,11 +247,20 @@ def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = 
 
     def V(c):
         n, kc = int(pk.c_size[c]), int(k[c])
+        if far_dev:
+            return _GBlock(SEC_V, pk.c_v_off[c], n, kc)
         return pk.vbuf[pk.c_v_off[c]:pk.c_v_off[c] + n * kc].reshape(n, kc)
 
     def T(c):
         m = int(k[lo_of[c]] + k[hi_of[c]])
+        if far_dev:
+            return _GBlock(SEC_T, pk.c_t_off[c], m, int(k[c]))
         return pk.tbuf[pk.c_t_off[c]:pk.c_t_off[c] + m * k[c]].reshape(m, int(k[c]))
+
+    def S(b, kt, ks):
+        if far_dev:
+            return _GBlock(SEC_S, pk.s_off[b], kt, ks)
+        return pk.sbuf[pk.s_off[b]:pk.s_off[b] + kt * ks].reshape(kt, ks)
 
     def up(Bd, levels, sel):
         for lvl in levels:
@@ -248,9 +311,11 @@ def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = 
             s = int(pk.s_col[b])
             if k[s] == 0:
                 continue
-            blocks.append((pk.sbuf[pk.s_off[b]:pk.s_off[b] + kt * k[s]].reshape(kt, int(k[s])), s))
-        R = sum(B.shape[1] for B, _ in blocks)
-        panel = put(PAY_S, np.concatenate([B.T for B, _ in blocks], axis=0)) if R else 0
+            blocks.append((S(b, kt, int(k[s])), s))
+        R = int(sum(k[s] for _, s in blocks))
+        panel = size[PAY_S]
+        for B, _ in blocks:  # contiguous: the stacked panel [S_t,s1ᵀ; S_t,s2ᵀ; ...]
+            put(PAY_S, B.T)
         rows = [np.arange(hat[s], hat[s] + k[s]) for _, s in blocks]
         cf_items.append((panel, n_xcol, int(hat[t]), R, kt))
         cf_xcol.extend(rows)
@@ -300,7 +365,7 @@ def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = 
     r0 = int(part.row0[g])
     near_blocks, v_offs = {}, {}
     sample = None
-    if pk.dbuf.size == 0 and pk.n_near:  # near-field not on the host: sample this rank's rows
+    if pk.dbuf.size == 0 and pk.n_near and not near_dev:  # not on the host: sample this rank's rows
         from .nearfield import assemble_block, geometry_arrays
         geo = geometry_arrays(pk.meta["geometry"])
         sample = lambda rows, cols: assemble_block(*geo, rows, cols)  # noqa: E731
@@ -316,7 +381,9 @@ def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = 
         for b in range(pk.d_row_ptr[t], pk.d_row_ptr[t + 1]):
             s = int(pk.d_col[b])
             ns = int(pk.c_size[s])
-            if sample is not None:
+            if near_dev:
+                D = _NBlock(pk.c_start[t], nt, pk.c_start[s], ns)
+            elif sample is not None:
                 D = panel[:, c0:c0 + ns]
                 c0 += ns
             else:
@@ -368,5 +435,15 @@ def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = 
                          ns=ns, R=R)
 
     payloads = [np.concatenate(a) if a else np.zeros(0, np.complex128) for a in pays]
+    deferred = any(synth_fills) or bool(near_fills)
+    if deferred:  # sizes only; the device fills the described blocks
+        payloads = [np.zeros(0, np.complex128) for _ in range(N_PAY)]
+    fills = None
+    if deferred:
+        fills = dict(sizes=list(size),
+                     synth=[np.array(f, dtype=np.int64).reshape(-1, 6) for f in synth_fills],
+                     near=np.array(near_fills, dtype=np.int64).reshape(-1, 5),
+                     seed=int(pk.meta.get("synthetic", {}).get("seed", 0)),
+                     geometry=pk.meta.get("geometry"), perm=pk.perm if near_fills else None)
     return ShardPlan(rank=g, part=part, payloads=payloads, phases=phases, gather=gather,
-                     near_fast=near_fast, couple_fast=couple_fast)
+                     near_fast=near_fast, couple_fast=couple_fast, fills=fills)
