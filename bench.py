@@ -510,6 +510,22 @@ def main():
     relerr = (float(np.linalg.norm(yy - ex["y"][:, 0]) / np.linalg.norm(ex["y"][:, 0]))
               if "y" in ex else None)  # structure-exact operator: no reference output
 
+    # the byte-dominant kernel alone: the same step with the far-field launch switched off
+    # (H2B_OPT_DEBUG bit 1: timing only, y is then wrong and is not used)
+    dominant = None
+    mega_on = C.c_int64()
+    _abi.check(L.h2b_query(op.handle, _abi.Q_MEGA, C.byref(mega_on)))
+    if mega_on.value:
+        _abi.check(L.h2b_set_option(op.handle, _abi.OPT_DEBUG, 2))
+        for _ in range(3):
+            mv()
+        ms_near = max_over_ranks([timed(mv, a.steps)], dev)[0]
+        _abi.check(L.h2b_set_option(op.handle, _abi.OPT_DEBUG, 0))
+        nb = pk.near_bytes(1)
+        dominant = {"kernel": "k_near_stream (near-field, alone: the step without its far-field launch)",
+                    "alg_bytes_per_launch": nb, "ms_per_launch": ms_near,
+                    "achieved": nb / (ms_near * 1e-3) / 1e9}
+
     # end-to-end through the host-buffer C-ABI call (pinned host memory)
     xh = torch.from_numpy(ex["x"][:, 0].copy()).pin_memory()
     yh = torch.empty_like(xh).pin_memory()
@@ -574,6 +590,8 @@ def main():
                      "warm_l2_achieved": alg_bytes / (ms_warm * 1e-3) / 1e9,
                      "cold_read_same_bytes_ms": ms_read,
                      "frac_of_cold_read": ms_read / ms},
+        "dominant_kernel": (dict(dominant, peak=peaks()[0], unit="GB/s",
+                                 frac=dominant["achieved"] / peaks()[0]) if dominant else None),
         "e2e": {"value": world * unknowns / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * pk.n,
                 "d2h_bytes_per_step": 16 * pk.n, "ms_per_call": e2e_s * 1e3},
         "gpu_launches": int(nlaunch.value) * a.steps,
