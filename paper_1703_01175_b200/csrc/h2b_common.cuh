@@ -284,6 +284,7 @@ struct h2b_ctx {
   int4* near_recs = nullptr;           // near task records
   int2* near_idx = nullptr;            // per near task {first slot, slots}
   int n_near_tasks = 0, near_rec_max = 0, near_nst = 0, near_smem = 0, near_grid = 0;
+  uint32_t near_delay_ns = 0;  // tuning aid (H2B_DEBUG_NEAR_DELAY_NS)
   // flattened bottom tier (0 = off): W buffer and the deep spans' y_deep
   int mega_flat = 0;
   double2* wbuf = nullptr;

@@ -33,14 +33,11 @@ __device__ __forceinline__ uint32_t smid() {
   asm volatile("mov.u32 %0, %smid;" : "=r"(s));
   return s;
 }
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+// no memory clobber: a sweep's loads may all be in flight before the first compare (the
+// sweep ends with __all_sync and, once complete, an acquire fence)
+__device__ __forceinline__ uint32_t ld_relaxed_nc(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
@@ -84,6 +81,7 @@ struct NearArgs {
   const int64_t *d_row_ptr, *d_off;
   int nst;        // ring stages
   int rec_slots;  // slots of each of the two record buffers
+  uint32_t delay_ns;  // tuning aid: the producer starts this late (0 = at once)
 };
 
 // One CTA streams a sequence of near-field tasks as ONE continuous sequence of D blocks:
@@ -165,6 +163,10 @@ __global__ void __launch_bounds__(NEAR_THREADS, 1) k_near_stream(NearArgs A) {
     // ---------------- producer (one lane) ----------------
     if (threadIdx.x == MNT) {
       const uint64_t pol = policy_evict_first();
+      if (A.delay_ns) {
+        const uint64_t t0 = gtimer();
+        while (gtimer() - t0 < A.delay_ns) __nanosleep(256);
+      }
       int claimed = 0;  // records 0 .. claimed-1 claimed
       bool end = false;
       // claim record `claimed` into buffer claimed % NRB, given the counter value c (fetched
@@ -318,8 +320,11 @@ struct MegaArgs {
 // shared memory meanwhile.  A single big panel (cta_mode) streams from HBM.
 // ---------------------------------------------------------------------------
 // static part (before the dependencies are met): the panels' bulk copy
+// The gather indices are static too: each thread loads the (up to XPRE) indices it will
+// gather into registers here, so that after the wait only the x̂ loads remain.
+constexpr int XPRE = 2;
 __device__ __forceinline__ void couple_stage_static(const MegaArgs& A, const int4* rec, double2* sm,
-                                                    uint64_t* bar) {
+                                                    uint64_t* bar, int (&xi)[XPRE]) {
   const int n_items = rec[0].x, cta_mode = rec[0].y;
   const CoupleItem* items = reinterpret_cast<const CoupleItem*>(rec + 1);
   const CoupleItem first = items[0], last = items[n_items - 1];
@@ -329,10 +334,16 @@ __device__ __forceinline__ void couple_stage_static(const MegaArgs& A, const int
     mbar_arrive_expect_tx(bar, 16u * (uint32_t)pe);
     bulk_g2s(sm, A.sbuf + p0, 16u * (uint32_t)pe, bar);
   }
+  const int64_t x0 = first.xcol, xe = last.xcol + last.R - x0;
+#pragma unroll
+  for (int j = 0; j < XPRE; ++j) {
+    const int64_t e = threadIdx.x + (int64_t)j * MNT;
+    xi[j] = e < xe ? __ldg(A.xcol + x0 + e) : 0;
+  }
 }
 
 __device__ __forceinline__ void couple_task(const MegaArgs& A, const int4* rec, double2* red,
-                                            double2* sm, uint64_t* bar, uint32_t& phase) {
+                                            double2* sm, uint64_t* bar, uint32_t& phase, const int (&xi)[XPRE]) {
   const int n_items = rec[0].x, cta_mode = rec[0].y;
   const CoupleItem* items = reinterpret_cast<const CoupleItem*>(rec + 1);
   const CoupleItem first = items[0], last = items[n_items - 1];
@@ -340,7 +351,12 @@ __device__ __forceinline__ void couple_task(const MegaArgs& A, const int4* rec, 
   const int64_t pe = cta_mode ? 0 : (last.panel + (int64_t)last.R * last.w - p0);
   const int64_t xe = last.xcol + last.R - x0;
   double2* sx = sm + pe;  // gathered x̂ after the staged panels
-  for (int64_t e = threadIdx.x; e < xe; e += MNT) sx[e] = __ldcg(A.xhat + A.xcol[x0 + e]);
+#pragma unroll
+  for (int j = 0; j < XPRE; ++j) {
+    const int64_t e = threadIdx.x + (int64_t)j * MNT;
+    if (e < xe) sx[e] = __ldcg(A.xhat + xi[j]);
+  }
+  for (int64_t e = threadIdx.x + (int64_t)XPRE * MNT; e < xe; e += MNT) sx[e] = __ldcg(A.xhat + A.xcol[x0 + e]);
   if (pe > 0) {
     mbar_wait(bar, phase);
     phase ^= 1u;
@@ -473,28 +489,57 @@ __global__ void __launch_bounds__(MNT, 2) k_mega(MegaArgs A) {
     phase = 0;
     // static operands stream in while the dependencies are still outstanding
     const FlatRec& fr = *reinterpret_cast<const FlatRec*>(rec);
+    int xi[XPRE] = {};
     if (!skip && type == T_SPAN)
       span_stage_static<MNT>(hd, cps, A.B, sm, &bar);
     else if (!skip && type == T_COUPLE)
-      couple_stage_static(A, rec, sm, &bar);
+      couple_stage_static(A, rec, sm, &bar, xi);
     else if (!skip)
       flat_stage_static(A, fr, type == T_FLAT_UP, sm, &bar);
     // dependencies: warp 0 polls (lanes share the flags) with a short backoff; the other warps
-    // wait at the barrier.  A lane re-reads only the flag it is waiting for.
-    if (threadIdx.x < 32)
+    // wait at the barrier.  Each sweep issues relaxed loads of every outstanding flag back to
+    // back (one L2 round trip per sweep however many ranges there are: acquire loads would
+    // serialise, one round trip per flag), and one acquire fence follows the last sweep.
+    if (threadIdx.x < 32 && n_dep) {
+      // lane L takes the flattened dependencies L, L+32, ... (up to four in registers; longer
+      // lists sweep the ranges)
+      const int lane = threadIdx.x;
+      int f0 = -1, f1 = -1, f2 = -1, f3 = -1, cnt = 0, base = 0;
       for (int i = 0; i < n_dep; ++i) {
         const int2 rg = deps[i];
-        for (int d = rg.x + threadIdx.x; d < rg.y; d += 32) {
-          long spins = 0;
-          while (ld_acquire(A.flags + d) != done) {
-            if (++spins > (1l << 24)) {  // never expected: report instead of hanging the GPU
-              atomicExch(&A.ctrl->error, 1u);
-              break;
-            }
-            __nanosleep(64);
+        for (int d = rg.x + ((lane - base) & 31); d < rg.y; d += 32, ++cnt) {
+          if (cnt == 0) f0 = d;
+          else if (cnt == 1) f1 = d;
+          else if (cnt == 2) f2 = d;
+          else if (cnt == 3) f3 = d;
+        }
+        base += rg.y - rg.x;
+      }
+      const bool small = __all_sync(0xffffffffu, cnt <= 4);
+      long spins = 0;
+      for (;;) {
+        bool ok = true;
+        if (small) {
+          const uint32_t v0 = f0 >= 0 ? ld_relaxed_nc(A.flags + f0) : done;
+          const uint32_t v1 = f1 >= 0 ? ld_relaxed_nc(A.flags + f1) : done;
+          const uint32_t v2 = f2 >= 0 ? ld_relaxed_nc(A.flags + f2) : done;
+          const uint32_t v3 = f3 >= 0 ? ld_relaxed_nc(A.flags + f3) : done;
+          ok = v0 == done && v1 == done && v2 == done && v3 == done;
+        } else {
+          for (int i = 0; i < n_dep; ++i) {
+            const int2 rg = deps[i];
+            for (int d = rg.x + lane; d < rg.y; d += 32) ok &= ld_relaxed_nc(A.flags + d) == done;
           }
         }
+        if (__all_sync(0xffffffffu, ok)) break;
+        if (++spins > (1l << 24)) {  // never expected: report instead of hanging the GPU
+          atomicExch(&A.ctrl->error, 1u);
+          break;
+        }
+        __nanosleep(32);
       }
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
     __syncthreads();
     // order the acquires (made visible to every thread by the barrier) before the async-proxy
     // (TMA) reads of the produced data: the fence follows the barrier in the issuing thread
@@ -505,7 +550,7 @@ __global__ void __launch_bounds__(MNT, 2) k_mega(MegaArgs A) {
     } else if (type == T_SPAN) {
       span_finish<MNT>(hd, cps, A.B, sm, &bar, phase, A.trace ? A.trace + 8 * t + 2 : nullptr, 3);
     } else if (type == T_COUPLE) {
-      couple_task(A, rec, red, sm, &bar, phase);
+      couple_task(A, rec, red, sm, &bar, phase, xi);
     } else if (type == T_FLAT_UP) {
       flat_up(A, fr, sm, &bar, red);
     } else {
@@ -662,6 +707,7 @@ int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st)
     N.d_off = h->d_off_d;
     N.nst = std::max(1, h->near_nst);
     N.rec_slots = std::max(1, h->near_rec_max);  // NRB buffers of this size follow the ring
+    N.delay_ns = h->near_delay_ns;
     const int ns = h->mega_ns, r = h->mega_r;
     bool launched = false;
 #define X(a, b)                                                                            \

@@ -445,6 +445,7 @@ bool plan_with_split(const h2b_ctx* h, int ls, Plan& pl) {
 
 // ------------------------- persistent-kernel task graph -------------------------
 constexpr int MEGA_BUDGET = 5800;  // double2 elements (92.8 KB): largest work area of a far CTA
+constexpr int MEGA_BUDGET_MAX = 12000;  // tuning override ceiling (the near ring shrinks to fit)
 constexpr int MEGA_BLOB_MAX = 1024;  // 16-byte slots (16 KB) of per-CTA task blob
 constexpr double NEAR_TASK_BYTES = 64e3;  // target D bytes per near-field task
 
@@ -501,7 +502,9 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
     if (h->c_child_lo[p] < 0) min_leaf = std::min(min_leaf, level_of(h, p));
   // ---- tiers: bottom split ls, then upper splits up to the root -----------------
   int ls = -1;
-  for (int l = 0; l <= min_leaf && ls < 0; ++l)
+  int ls_min = 0;
+  if (const char* e = getenv("H2B_DEBUG_LS")) ls_min = std::max(0, atoi(e));  // tuning aid
+  for (int l = ls_min; l <= min_leaf && ls < 0; ++l)
     if (tier_fits(h, l, L - l, false, budget)) ls = l;
   if (ls < 0) return false;
   std::vector<int> splits = {ls};  // bottom-up list of tier roots
@@ -1196,7 +1199,7 @@ int h2b_prepare(h2b_ctx* h) {
     int far_per_sm = 1;
     if (const char* e = getenv("H2B_FAR_PER_SM")) far_per_sm = std::max(1, std::min(2, atoi(e)));
     int budget = far_per_sm == 1 ? MEGA_BUDGET : 3900;
-    if (const char* e = getenv("H2B_MEGA_BUDGET")) budget = std::max(1000, std::min(MEGA_BUDGET, atoi(e)));
+    if (const char* e = getenv("H2B_MEGA_BUDGET")) budget = std::max(1000, std::min(MEGA_BUDGET_MAX, atoi(e)));
     if (plan_mega(h, citems, targets, far_per_sm * sms_est, budget, mp)) {
       H2B_TRY(to_device(&h->span_heads, mp.prog.heads, &acc));
       H2B_TRY(to_device(&h->span_copies, mp.prog.copies, &acc));
@@ -1297,7 +1300,7 @@ int h2b_prepare(h2b_ctx* h) {
       h->mega_smem = std::max(mp.smem, 16);
       h->mega_grid = (int)mp.cta_lists.size();
       const int far_bytes = h->mega_smem + 16 * h->mega_blob_slots;
-      H2B_TRY(h2b_mega_set_smem(0, 0, 16 * (MEGA_BUDGET + MEGA_BLOB_MAX)));
+      H2B_TRY(h2b_mega_set_smem(0, 0, 16 * (std::max(budget, MEGA_BUDGET) + MEGA_BLOB_MAX)));
       int per_sm = 1;
       if (h->mega_grid > 0) H2B_TRY(h2b_mega_occupancy(0, 0, far_bytes, &per_sm));
       // near-field stream: one CTA per SM beside the far-field CTA, ring in the shared memory left
@@ -1308,12 +1311,14 @@ int h2b_prepare(h2b_ctx* h) {
       const int rec_bytes = 3 * 16 * std::max(1, mp.near_rec_max);  // NRB record buffers
       const int stg = mp.ns > 0 ? 16 * (mp.r * (256 / (mp.ns / 2)) * mp.ns + mp.ns) : 0;
       int nst = stg > 0 ? std::min(8, (sm_total - far_total - near_static - rec_bytes) / stg) : 0;
+      if (const char* e = getenv("H2B_DEBUG_NEAR_NST")) nst = std::min(nst, std::max(2, atoi(e)));  // tuning aid
       if (mp.ns > 0 && nst < 2) nst = 2;  // still correct; the two kernels then share SMs less well
       h->near_nst = nst;
       h->near_smem = nst * stg + rec_bytes;
       // the attribute is per kernel and process-wide: set the maximum, never a per-handle size
       H2B_TRY(h2b_near_stream_set_smem(mp.ns, mp.r, 232448 - near_static));
       h->near_grid = sms;
+      if (const char* e = getenv("H2B_DEBUG_NEAR_DELAY_NS")) h->near_delay_ns = (uint32_t)std::max(0, atoi(e));  // tuning aid
       if (const char* e = getenv("H2B_NEAR_GRID")) h->near_grid = std::max(1, std::min(sms, atoi(e)));  // tuning aid
       h->mega = (per_sm > 0 && h->mega_grid <= per_sm * sms) ? 1 : 0;
       h->mega_est_us = mp.est_makespan;

@@ -5,7 +5,7 @@ import torch
 from paper_1703_01175_b200 import H2Operator, load_packed, _abi
 L = _abi.lib()
 for k in [int(a) for a in sys.argv[1:]] or [1, 2]:
-    pk, ex = load_packed(f"data/cfg{k}.npz", with_extra=True)
+    sys.path.insert(0, "."); from bench import load; pk, ex = load(k)
     op = H2Operator(pk)
     _abi.check(L.h2b_prepare_handle(op.handle))
     x = torch.from_numpy(ex["x"][pk.perm, 0].copy()).cuda(); y = torch.empty_like(x)

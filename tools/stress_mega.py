@@ -9,7 +9,7 @@ k = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 graphs = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 400
 dbg = int(sys.argv[4]) if len(sys.argv) > 4 else 0
-pk, ex = load_packed(f"data/cfg{k}.npz", with_extra=True)
+sys.path.insert(0, "."); from bench import load; pk, ex = load(k)
 a = H2Operator(pk); b = H2Operator(pk)
 _abi.check(L.h2b_set_option(a.handle, _abi.OPT_GRAPHS, graphs))
 _abi.check(L.h2b_set_option(a.handle, 4, dbg))
