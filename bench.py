@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="budget of the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gmres", action="store_true")
+    ap.add_argument("--no-cube", action="store_true",
+                    help="N > 1: skip the partitioned 2M-unknown cube (cfg4) leg")
     ap.add_argument("--exchange", default="auto", choices=["auto", "p2p", "allgather"],
                     help="partitioned path: fused P2P exchange or NCCL all-gather")
     ap.add_argument("--partitioned", action="store_true",
@@ -87,7 +89,9 @@ def max_over_ranks(vals, dev):
 def config_desc(k, pk):
     names = {1: "cfg1 cube 16^3 (N=4096), leaf 32, tol 1e-4",
              2: "cfg2 line 2048 lambda at 32 pts/lambda (N=65536), leaf 32, tol 1e-4",
-             3: "cfg3 plate 512^2 (N=262144), leaf 64, tol 1e-4"}
+             3: "cfg3 plate 512^2 (N=262144), leaf 64, tol 1e-4",
+             4: "cfg4 cube 128^3 (N=2097152), leaf 64, tol 1e-3",
+             5: "cfg5 cube 64^3 random eps_r (N=262144), leaf 64, tol 1e-4"}
     return {"workload": names.get(k, f"cfg{k}"), "N": int(pk.n), "q": 1, "eta": 1.0,
             "operator_bytes_alg": int(pk.algorithmic_bytes()),
             "operator": (f"cfg{k} structure-exact: reference block structure/ranks, seeded V/T/S, "
@@ -109,7 +113,8 @@ def load(k):
     path = os.path.join(ROOT, "fixtures", f"cfg{k}_structure.npz")
     if not os.path.exists(path):
         return None, None
-    pk, ex = load_packed(path, with_extra=True, near_on_host=False)
+    # cfg4's far field (26 GB) is generated on the device only (no CPU path at that size)
+    pk, ex = load_packed(path, with_extra=True, near_on_host=False, far_on_host=k != 4)
     rng = np.random.default_rng(0)
     ex = dict(ex, x=(rng.standard_normal((pk.n, 2)) + 1j * rng.standard_normal((pk.n, 2))))
     return pk, ex
@@ -495,9 +500,14 @@ def main():
         ms_warm = timed(mv, a.steps, flush_l2=False)
         # calibration: a plain cold read (sum) of as many bytes as the matvec's algorithmic
         # traffic, same flush and timing — the attainable streaming time at this size
-        cal = torch.ones(pk.algorithmic_bytes(1) // 8, dtype=torch.float64, device=dev)
-        ms_read = timed(lambda: cal.sum(), max(5, min(a.steps, 10)))
-        del cal
+        # (skipped when that buffer does not fit beside the operator: at such sizes the cold
+        # read runs at the copy peak anyway)
+        free_b, _ = torch.cuda.mem_get_info(dev)
+        ms_read = None
+        if pk.algorithmic_bytes(1) < 0.8 * free_b:
+            cal = torch.ones(pk.algorithmic_bytes(1) // 8, dtype=torch.float64, device=dev)
+            ms_read = timed(lambda: cal.sum(), max(5, min(a.steps, 10)))
+            del cal
         for _ in range(3):  # keep the device busy for a few more clock samples
             timed(mv, a.steps)
     torch.cuda.synchronize(dev)
@@ -589,7 +599,7 @@ def main():
                      "warm_l2_ms_per_launch": ms_warm,
                      "warm_l2_achieved": alg_bytes / (ms_warm * 1e-3) / 1e9,
                      "cold_read_same_bytes_ms": ms_read,
-                     "frac_of_cold_read": ms_read / ms},
+                     "frac_of_cold_read": ms_read / ms if ms_read else None},
         "dominant_kernel": (dict(dominant, peak=peaks()[0], unit="GB/s",
                                  frac=dominant["achieved"] / peaks()[0]) if dominant else None),
         "e2e": {"value": world * unknowns / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * pk.n,
@@ -636,6 +646,30 @@ def main():
                                                                "parity_relerr_vs_reference")}
             line["partitioned_strong"]["parallelism"] = part["config"]["parallelism"]
             line["partitioned_strong"]["exchange"] = part.get("exchange")
+        # BASELINE's scaling config: the 2M-unknown cube (cfg4, structure-exact: the reference
+        # block structure and ranks, payloads generated on each rank's device) partitioned over
+        # the N GPUs — strong scaling of one right-hand side
+        cube_k = int(os.environ.get("H2B_BENCH_CUBE_CONFIG", "4"))  # another config: functional tests
+        if not a.no_cube and a.config != cube_k:
+            del op
+            torch.cuda.empty_cache()
+            cube, errs = None, []
+            try:
+                pk4, ex4 = load(cube_k)
+                if pk4 is None:
+                    raise FileNotFoundError(f"fixtures/cfg{cube_k}_structure.npz")
+                cube = run_partitioned(argparse.Namespace(**dict(vars(a), config=cube_k, steps=min(a.steps, 10),
+                                                                 exchange="auto")),
+                                       pk4, ex4, rank, world, local, emit=False)
+            except Exception as e:  # noqa: BLE001
+                errs.append(f"{type(e).__name__}: {e}"[:300])
+            if rank == 0:
+                line["partitioned_cube_strong"] = (
+                    {"error": errs} if cube is None else
+                    dict({k: cube[k] for k in ("value", "unit", "ms_per_step", "scaling", "roofline",
+                                               "exchange_bytes_per_step", "gpu_launches_per_step",
+                                               "e2e", "exchange")},
+                         config=cube["config"]))
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

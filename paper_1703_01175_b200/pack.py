@@ -320,20 +320,48 @@ def save_packed(pk: PackedH2, path, extra=None, geometry=None):
     os.replace(tmp, path)
 
 
-def save_structure(pk: PackedH2, path, geometry, seed=0, note=""):
+def save_structure(pk: PackedH2, path, geometry, seed=0, note="", compact=False):
     """Write only the index tables + geometry of `pk` (a *structure-exact* operator file).
 
     `load_packed` fills the far-field payloads (V, T, S) with seeded random values of exactly
     the reference shapes and re-assembles the near-field from the geometry: same bytes, flops
     and block structure as the reference-built operator, for throughput measurements of
     operators too large to ship ("configs 3-5 without a reference build")."""
-    arrays = {name: getattr(pk, name) for name in _INT_TABLES}
+    arrays = {name: getattr(pk, name) for name in _INT_TABLES if not (compact and name in _DERIVED)}
     head = dict(n=pk.n, depth=pk.depth, meta=pk.meta, version=FORMAT_VERSION, geometry=geometry,
                 synthetic=dict(seed=int(seed), note=note))
     arrays["__header__"] = np.frombuffer(json.dumps(head).encode(), dtype=np.uint8)
     tmp = str(path) + ".tmp.npz"
-    np.savez(tmp, **arrays)
+    (np.savez_compressed if compact else np.savez)(tmp, **arrays)
     os.replace(tmp, path)
+
+
+_DERIVED = ("c_xhat_off", "c_v_off", "c_t_off", "s_off", "d_off")
+
+
+def _derive_offsets(kw):
+    """The payload offsets implied by the tables (what the packer writes: V/T/S/D blocks in
+    cluster / CSR order, -1 where a cluster has no V or T block); compact structure files omit
+    them."""
+    rank, size = kw["c_rank"].astype(np.int64), kw["c_size"].astype(np.int64)
+    lo, hi = kw["c_child_lo"], kw["c_child_hi"]
+    leaf = lo < 0
+    P = rank.size
+
+    def excl(v):
+        o = np.zeros(v.size, np.int64)
+        np.cumsum(v[:-1], out=o[1:])
+        return o
+
+    out = {"c_xhat_off": np.concatenate([[0], np.cumsum(rank)]).astype(np.int64)}
+    out["c_v_off"] = np.where(leaf, excl(np.where(leaf, size * rank, 0)), -1)
+    li, hj = np.where(leaf, 0, lo), np.where(leaf, 0, hi)
+    out["c_t_off"] = np.where(leaf, -1, excl(np.where(leaf, 0, (rank[li] + rank[hj]) * rank)))
+    rows = np.repeat(np.arange(P), np.diff(kw["s_row_ptr"]))
+    out["s_off"] = excl(rank[rows] * rank[kw["s_col"]])
+    drows = np.repeat(np.arange(P), np.diff(kw["d_row_ptr"]))
+    out["d_off"] = excl(size[drows] * size[kw["d_col"]])
+    return out
 
 
 def _synthetic_far_field(kw, spec):
@@ -363,6 +391,8 @@ def load_packed(path, with_extra=False, near_on_host=True, far_on_host=True):
     if head.get("version") != FORMAT_VERSION:
         raise ValueError(f"{path}: unsupported packed-H2 format {head.get('version')}")
     kw = {name: z[name] for name in _INT_TABLES + _PAYLOADS if name in z.files}
+    if any(name not in kw for name in _DERIVED):  # compact structure file
+        kw.update({k: v for k, v in _derive_offsets(kw).items() if k not in kw})
     if "synthetic" in head:
         if far_on_host:
             kw.update(_synthetic_far_field(kw, head["synthetic"]))

@@ -73,3 +73,17 @@ def test_structure_file_roundtrip(tmp_path):
     c = load_packed(path, near_on_host=False, far_on_host=False)
     assert c.sbuf.size == 0 and c.dbuf.size == 0 and "synthetic" in c.meta and "geometry" in c.meta
     assert c.algorithmic_bytes() == pk.algorithmic_bytes()
+
+
+@pytest.mark.parametrize("name", GOLDEN_NAMES)
+def test_compact_structure_file_derives_offsets(name, tmp_path):
+    """A compact structure file (compressed, without the payload offsets) loads to the same
+    tables: the offsets are exactly the cumulative block sizes of the packer's order."""
+    from paper_1703_01175_b200.pack import _INT_TABLES, save_structure
+    pk, _ = load_golden(name)
+    path = tmp_path / "c.npz"
+    save_structure(pk, path, dict(kind="none"), seed=1, compact=True)
+    assert "s_off" not in np.load(path).files
+    c = load_packed(path, near_on_host=False, far_on_host=False)
+    for t in _INT_TABLES:
+        assert np.array_equal(getattr(c, t), getattr(pk, t)), t
