@@ -16,6 +16,8 @@
 #include <complex>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "h2b_common.cuh"
 
 namespace {
@@ -243,14 +245,14 @@ struct GivensState {
   double2* cs_sn;   // m: {c_i, 0}
   double2* res_hn;  // 2m: {res_j, 0}, {hn_j, 0}
   double2* scale;   // 1: 1 / hn of the last step (0 on breakdown)
+  double2* host_res = nullptr;  // optional: mapped pinned copy of res_hn (stored by the kernel itself)
 };
 
 // Restates the host recurrence of oracle/krylov_oracle.py::gmres_solve for step j:
 // hc = h1 + h2 (CGS2), apply rotations 0..j-1, new rotation zeroing hn, update g.  The cosines
 // c_i live in cs_sn[i].x, the complex sines s_i in the spare last row of H (H[m*m + i]), which
 // never holds a Hessenberg entry (the sub-diagonal is rotated away, never stored).
-__global__ void k_givens_step(int j, int m, const double2* __restrict__ hv, GivensState S, double bnrm) {
-  if (threadIdx.x != 0) return;
+__device__ __noinline__ void givens_update(int j, int m, const double2* hv, GivensState S, double bnrm) {
   double2 hc[64];
   for (int i = 0; i <= j; ++i) hc[i] = make_double2(hv[i].x + hv[64 + i].x, hv[i].y + hv[64 + i].y);
   const double hn = sqrt(hv[128].x);
@@ -287,7 +289,155 @@ __global__ void k_givens_step(int j, int m, const double2* __restrict__ hv, Give
   const double2 gn = S.g[j + 1];
   S.res_hn[2 * j] = make_double2(hypot(gn.x, gn.y) / bnrm, 0.0);
   S.res_hn[2 * j + 1] = make_double2(hn, 0.0);
+  if (S.host_res) {  // straight into the host's pinned buffer (no copy node in the step graph)
+    S.host_res[2 * j] = S.res_hn[2 * j];
+    S.host_res[2 * j + 1] = S.res_hn[2 * j + 1];
+    __threadfence_system();
+  }
   S.scale[0] = make_double2(hn == 0.0 ? 0.0 : 1.0 / hn, 0.0);
+}
+
+__global__ void k_givens_step(int j, int m, const double2* __restrict__ hv, GivensState S, double bnrm) {
+  if (threadIdx.x == 0) givens_update(j, m, hv, S, bnrm);
+}
+
+// ---------------------------------------------------------------------------
+// One Arnoldi step after the matvec (CGS2 against V[0..nv), normalisation, Givens update) in
+// ONE launch of one thread-block cluster, for small n: CTA c owns rows [cR, cR + R) and keeps
+// its rows of the basis and of w in shared memory (the basis is read once per step instead of
+// four times); the per-CTA partial dot products meet through distributed shared memory, summed
+// in CTA order by every CTA (deterministic, the same bits in all CTAs), at three cluster
+// barriers.  Replaces nine launches of the multi-kernel step (dots / reduce / subtract twice,
+// norm, Givens, scale), whose launch latencies dominate at these sizes.
+// ---------------------------------------------------------------------------
+constexpr int AC_T = 256;
+struct ArnoldiArgs {
+  const double2* V;
+  int64_t n;
+  int nv, R;
+  double2* w;
+  double2* hv;  // [0, nv): pass-1 coefficients, [64, 64 + nv): pass 2, [128]: ||w||^2
+  GivensState S;
+  double bnrm;
+  int j, m;
+};
+
+__global__ void __launch_bounds__(AC_T) k_arnoldi_cluster(ArnoldiArgs A) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int c = (int)cl.block_rank(), ncl = (int)cl.num_blocks();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int NW = AC_T / 32;
+  extern __shared__ __align__(16) double2 dsm[];
+  __shared__ double2 part[3][64];  // this CTA's partials: pass-1 dots, pass-2 dots, ||w||^2
+  __shared__ double2 hs[64];
+  __shared__ double2 red[NW];
+  __shared__ double s_hn2;
+  const int R = A.R, nv = A.nv;
+  const int64_t row0 = (int64_t)c * R;
+  const int64_t left = A.n - row0;
+  const int rows = left <= 0 ? 0 : (left < R ? (int)left : R);
+  double2* Vs = dsm;                // nv x R (vector-major)
+  double2* ws = dsm + (size_t)nv * R;
+  for (int idx = tid; idx < nv * R; idx += AC_T) {
+    const int i = idx / R, r = idx - i * R;
+    Vs[idx] = r < rows ? A.V[(int64_t)i * A.n + row0 + r] : make_double2(0.0, 0.0);
+  }
+  for (int r = tid; r < R; r += AC_T) ws[r] = r < rows ? A.w[row0 + r] : make_double2(0.0, 0.0);
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int i = warp; i < nv; i += NW) {  // this CTA's part of <V_i, w>, fixed order
+      double2 acc = make_double2(0.0, 0.0);
+      for (int r = lane; r < R; r += 32) cfma_conj(acc, Vs[(size_t)i * R + r], ws[r]);
+      acc = warp_sum2(acc);
+      if (lane == 0) part[pass][i] = acc;
+    }
+    cl.sync();  // every CTA's partials visible cluster-wide
+    if (tid < nv) {
+      double2 sum = make_double2(0.0, 0.0);
+      for (int q = 0; q < ncl; ++q) sum = cadd(sum, cl.map_shared_rank(&part[pass][0], q)[tid]);
+      hs[tid] = sum;
+      if (c == 0) A.hv[64 * pass + tid] = sum;
+    }
+    __syncthreads();
+    double2 nrm = make_double2(0.0, 0.0);
+    for (int r = tid; r < R; r += AC_T) {  // w -= V h (CGS), then ||w||^2 on the second pass
+      double2 acc = make_double2(0.0, 0.0);
+      for (int i = 0; i < nv; ++i) cfma(acc, Vs[(size_t)i * R + r], hs[i]);
+      double2 wi = ws[r];
+      wi.x -= acc.x;
+      wi.y -= acc.y;
+      ws[r] = wi;
+      nrm.x = fma(wi.x, wi.x, nrm.x);
+      nrm.x = fma(wi.y, wi.y, nrm.x);
+    }
+    if (pass == 1) {
+      nrm = warp_sum2(nrm);
+      if (lane == 0) red[warp] = nrm;
+      __syncthreads();
+      if (tid == 0) {
+        double2 t = make_double2(0.0, 0.0);
+        for (int q = 0; q < NW; ++q) t = cadd(t, red[q]);
+        part[2][0] = t;
+      }
+    }
+    __syncthreads();
+  }
+  cl.sync();
+  if (tid == 0) {
+    double2 sum = make_double2(0.0, 0.0);
+    for (int q = 0; q < ncl; ++q) sum = cadd(sum, cl.map_shared_rank(&part[2][0], q)[0]);
+    s_hn2 = sum.x;
+    if (c == 0) A.hv[128] = sum;
+  }
+  cl.sync();  // every remote read done: no CTA's shared memory is read after this point
+  const double hn = sqrt(s_hn2), f = hn == 0.0 ? 0.0 : 1.0 / hn;  // = givens_update's scale
+  for (int r = tid; r < rows; r += AC_T) A.w[row0 + r] = make_double2(ws[r].x * f, ws[r].y * f);
+  if (c == 0 && tid == 0) givens_update(A.j, A.m, A.hv, A.S, A.bnrm);  // reads CTA 0's hv writes
+}
+
+// Fused Arnoldi step configuration for (n, m): cluster size and rows per CTA, or cl = 0 (the
+// multi-kernel step) when the basis rows of a CTA do not fit its shared memory or no cluster of
+// that size can be resident.  H2B_NO_FUSED_ARNOLDI forces the multi-kernel step (A/B timing).
+struct FusedArnoldi {
+  int cl = 0, R = 0;
+};
+FusedArnoldi fused_arnoldi_config(int64_t n, int m) {
+  FusedArnoldi f;
+  if (getenv("H2B_NO_FUSED_ARNOLDI") || n <= 0) return f;
+  constexpr int DYN_MAX = 200 * 1024;
+  if (cudaFuncSetAttribute(k_arnoldi_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+      cudaFuncSetAttribute(k_arnoldi_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, DYN_MAX) != cudaSuccess) {
+    cudaGetLastError();
+    return f;
+  }
+  for (int cl : {16, 8}) {
+    const int64_t R = (n + cl - 1) / cl;
+    const int64_t bytes = (int64_t)sizeof(double2) * (m + 1) * R;  // nv <= m basis rows + w
+    if (bytes > DYN_MAX) continue;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cl);
+    cfg.blockDim = dim3(AC_T);
+    cfg.dynamicSmemBytes = (size_t)bytes;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, k_arnoldi_cluster, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (nclusters >= 1) {
+      f.cl = cl;
+      f.R = (int)R;
+      return f;
+    }
+  }
+  return f;
 }
 
 // w *= scale[0] (a device scalar: the normalisation of the new basis vector)
@@ -394,6 +544,11 @@ extern "C" int h2b_gmres(h2b_handle h, const void* b_perm, void* x_perm, int res
   Ops ops{st, n, nblocks(n), g_scratch.partial, g_scratch.vals, g_scratch.host};
   double2* hvals = g_scratch.vals;        // device scalars (CGS2 coefficients, ||w||^2)
   double2* hres = g_scratch.host + 128;   // pinned: (res_j, hn_j) of step j
+  S.host_res = nullptr;
+  if (!getenv("H2B_GMRES_COPY_RES") && cudaHostGetDevicePointer((void**)&S.host_res, hres, 0) != cudaSuccess) {
+    cudaGetLastError();
+    S.host_res = nullptr;
+  }
 
   *report = h2b_report{0, 0, 0, 0, 0.0};
   TRY(ops.dots({{b, b}}, true));
@@ -406,6 +561,7 @@ extern "C" int h2b_gmres(h2b_handle h, const void* b_perm, void* x_perm, int res
     return H2B_OK;
   }
   H2B_CUDA_TRY(cudaMemcpyAsync(r, b, sizeof(double2) * n, cudaMemcpyDeviceToDevice, st));
+  const FusedArnoldi fa = fused_arnoldi_config(n, m);
   // one Arnoldi step j (matvec, CGS2, device Givens, normalisation, (res, hn) -> pinned host)
   // as a CUDA graph, captured once per (basis, j) and replayed
   auto step_graph = [&](int j, cudaGraphExec_t* out) -> int {
@@ -423,6 +579,26 @@ extern "C" int h2b_gmres(h2b_handle h, const void* b_perm, void* x_perm, int res
     int rc = h2b_enqueue_matvec(h, V + (size_t)n * j, w, 1, cs, &nl);
     if (!rc) {
       const int nb = ops.nb;
+      if (fa.cl > 0) {  // the whole post-matvec step as one cluster launch
+        ArnoldiArgs aa{V, n, j + 1, fa.R, w, hvals, S, bnrm, j, m};
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(fa.cl);
+        cfg.blockDim = dim3(AC_T);
+        cfg.dynamicSmemBytes = sizeof(double2) * (size_t)(j + 2) * fa.R;
+        cfg.stream = cs;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = fa.cl;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaError_t le = cudaLaunchKernelEx(&cfg, k_arnoldi_cluster, aa);
+        if (le != cudaSuccess) {
+          h2b_set_error(std::string("h2b_gmres: fused Arnoldi step: ") + cudaGetErrorString(le));
+          rc = H2B_ECUDA;
+        }
+      } else {
       k_basis_dots_partial<<<dim3(nb, j + 1), RT, 0, cs>>>(V, n, j + 1, w, n, ops.partial);
       k_reduce_partials<<<j + 1, 32, 0, cs>>>(ops.partial, nb, j + 1, hvals);
       k_basis_sub<<<nb, RT, 0, cs>>>(V, n, j + 1, hvals, w, n, nullptr);
@@ -432,7 +608,9 @@ extern "C" int h2b_gmres(h2b_handle h, const void* b_perm, void* x_perm, int res
       k_reduce_partials<<<1, 32, 0, cs>>>(ops.partial, nb, 1, hvals + 128);
       k_givens_step<<<1, 32, 0, cs>>>(j, m, hvals, S, bnrm);
       k_scale_dev<<<nb, RT, 0, cs>>>(w, n, S.scale);
-      cudaMemcpyAsync(hres + 2 * j, S.res_hn + 2 * j, sizeof(double2) * 2, cudaMemcpyDeviceToHost, cs);
+      }
+      if (!S.host_res)
+        cudaMemcpyAsync(hres + 2 * j, S.res_hn + 2 * j, sizeof(double2) * 2, cudaMemcpyDeviceToHost, cs);
     }
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(cs, &g);
