@@ -449,6 +449,173 @@ __global__ void __launch_bounds__(RT) k_scale_dev(double2* w, int64_t n, const d
   }
 }
 
+// ---------------------------------------------------------------------------
+// Graph-driven BiCGStab: one CUDA graph per iteration, every scalar of the recurrence computed
+// and tested on the device (the host's only per-iteration work is reading a record that the
+// last kernel stores into mapped pinned memory, one iteration behind the GPU).  A status word
+// stops the recurrence: once it is non-zero every later kernel of the iteration — and of a
+// speculatively queued next iteration — leaves the vectors alone.
+// ---------------------------------------------------------------------------
+enum BiStatus : int {
+  BI_RUN = 0,
+  BI_CONV_S = 1,       // converged on ||s|| (x += alpha p pending)
+  BI_CONV_R = 2,       // converged on ||r||
+  BI_RHO_BREAK = 3,    // rho breakdown: the host restarts with the noise vector or stops
+  BI_DENOM_ZERO = 4,   // <rh, v> = 0 (one matvec done)
+  BI_CONV_S_DONE = 5,  // BI_CONV_S with its x update applied
+  BI_NONFINITE = 6,    // ||r|| not finite (its history entry is recorded)
+  BI_OMEGA_ZERO = 7,   // <t, t> = 0 or omega = 0 (two matvecs done)
+};
+struct BiSc {
+  double2 rho, alpha, omega, rho_new;
+  double2 cp[3], cs[2], cx[3], cr[2];
+  double hist_s, hist_r;
+  int status, p_zero, run, pad;
+};
+
+// complex128 scalar arithmetic as numpy evaluates it (the reference's scalars are numpy
+// complex128): Smith's division, products without fused multiply-adds
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {  // a / b
+  const double abr = fabs(b.x), abi = fabs(b.y);
+  if (abr >= abi) {
+    if (abr == 0.0 && abi == 0.0) return make_double2(a.x / abr, a.y / abr);
+    const double rat = b.y / b.x;
+    const double scl = 1.0 / __dadd_rn(b.x, __dmul_rn(b.y, rat));
+    return make_double2(__dmul_rn(__dadd_rn(a.x, __dmul_rn(a.y, rat)), scl),
+                        __dmul_rn(__dsub_rn(a.y, __dmul_rn(a.x, rat)), scl));
+  }
+  const double rat = b.x / b.y;
+  const double scl = 1.0 / __dadd_rn(b.y, __dmul_rn(b.x, rat));
+  return make_double2(__dmul_rn(__dadd_rn(__dmul_rn(a.x, rat), a.y), scl),
+                      __dmul_rn(__dsub_rn(__dmul_rn(a.y, rat), a.x), scl));
+}
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
+                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+}
+
+// out = Σ_k coef[k] x_k while the status equals `want` (optional ||out||^2 partials)
+__global__ void __launch_bounds__(RT) k_lincomb_dev(const BiSc* __restrict__ sc, int want,
+                                                    const double2* coef, int nx, const double2* x0,
+                                                    const double2* x1, const double2* x2, double2* out,
+                                                    int64_t n, double2* nrm_partial) {
+  __shared__ double2 sm[RT / 32];
+  if (sc->status != want) return;  // uniform over the grid
+  const double2 c0 = coef[0], c1 = nx > 1 ? coef[1] : make_double2(0.0, 0.0),
+                c2 = nx > 2 ? coef[2] : make_double2(0.0, 0.0);
+  double2 nrm = make_double2(0.0, 0.0);
+  for (int64_t i = blockIdx.x * (int64_t)RT + threadIdx.x; i < n; i += (int64_t)gridDim.x * RT) {
+    double2 acc = make_double2(0.0, 0.0);
+    cfma(acc, c0, x0[i]);
+    if (nx > 1) cfma(acc, c1, x1[i]);
+    if (nx > 2) cfma(acc, c2, x2[i]);
+    out[i] = acc;
+    nrm.x = fma(acc.x, acc.x, nrm.x);
+    nrm.x = fma(acc.y, acc.y, nrm.x);
+  }
+  if (nrm_partial) {
+    double2 t = block_sum2(nrm, sm);
+    if (threadIdx.x == 0) nrm_partial[blockIdx.x] = t;
+  }
+}
+
+// rho_new = <rh, r>: breakdown test, then the coefficients of p = r + beta (p - omega v)
+__global__ void k_bi_rho(BiSc* sc, const double2* vals, double thr) {
+  ++sc->run;
+  if (sc->status) return;
+  const double2 rn = vals[0];
+  if (hypot(rn.x, rn.y) < thr) {
+    sc->status = BI_RHO_BREAK;
+    return;
+  }
+  if (sc->p_zero) {
+    sc->cp[0] = make_double2(1.0, 0.0);
+    sc->cp[1] = sc->cp[2] = make_double2(0.0, 0.0);
+    sc->p_zero = 0;
+  } else {
+    const double2 beta = cmul(cdiv(rn, sc->rho), cdiv(sc->alpha, sc->omega));
+    const double2 bo = cmul(beta, sc->omega);
+    sc->cp[0] = make_double2(1.0, 0.0);
+    sc->cp[1] = beta;
+    sc->cp[2] = make_double2(-bo.x, -bo.y);
+  }
+  sc->rho_new = rn;
+}
+
+// alpha = rho_new / <rh, v>; s = r - alpha v
+__global__ void k_bi_alpha(BiSc* sc, const double2* vals) {
+  if (sc->status) return;
+  const double2 d = vals[0];
+  if (d.x == 0.0 && d.y == 0.0) {
+    sc->status = BI_DENOM_ZERO;
+    return;
+  }
+  sc->alpha = cdiv(sc->rho_new, d);
+  sc->cs[0] = make_double2(1.0, 0.0);
+  sc->cs[1] = make_double2(-sc->alpha.x, -sc->alpha.y);
+}
+
+// ||s|| test: converged -> x += alpha p (by the BI_CONV_S-gated combination that follows)
+__global__ void k_bi_snorm(BiSc* sc, const double2* vals, double bnrm, double tol) {
+  if (sc->status) return;
+  const double rel = sqrt(vals[0].x) / bnrm;
+  sc->hist_s = rel;
+  if (rel <= tol) {
+    sc->cx[0] = make_double2(1.0, 0.0);
+    sc->cx[1] = sc->alpha;
+    sc->status = BI_CONV_S;
+  }
+}
+
+__global__ void k_bi_mark(BiSc* sc, int from, int to) {
+  if (sc->status == from) sc->status = to;
+}
+
+// omega = <t, s> / <t, t>; x += alpha p + omega s; r = s - omega t
+__global__ void k_bi_omega(BiSc* sc, const double2* vals) {
+  if (sc->status) return;
+  const double tt = vals[0].x;
+  if (tt == 0.0) {
+    sc->status = BI_OMEGA_ZERO;
+    return;
+  }
+  const double2 om = cdiv(vals[1], make_double2(tt, 0.0));  // numpy: vdot(t, s) / vdot(t, t)
+  if (om.x == 0.0 && om.y == 0.0) {
+    sc->status = BI_OMEGA_ZERO;
+    return;
+  }
+  sc->omega = om;
+  sc->cx[0] = make_double2(1.0, 0.0);
+  sc->cx[1] = sc->alpha;
+  sc->cx[2] = om;
+  sc->cr[0] = make_double2(1.0, 0.0);
+  sc->cr[1] = make_double2(-om.x, -om.y);
+}
+
+// restart with a re-seeded shadow residual: scalars back to 1, p = v = 0 (the run counter stays)
+__global__ void k_bi_restart(BiSc* sc) {
+  sc->rho = sc->alpha = sc->omega = make_double2(1.0, 0.0);
+  sc->p_zero = 1;
+  sc->status = BI_RUN;
+}
+
+// ||r|| test and the iteration's record {status, run}, {hist_s, hist_r} into mapped pinned memory
+__global__ void k_bi_final(BiSc* sc, const double2* vals, double bnrm, double tol, double2* rec) {
+  if (sc->status == BI_RUN) {
+    const double rel = sqrt(vals[0].x) / bnrm;
+    sc->hist_r = rel;
+    sc->rho = sc->rho_new;
+    if (rel <= tol)
+      sc->status = BI_CONV_R;
+    else if (!isfinite(rel))
+      sc->status = BI_NONFINITE;
+  }
+  double2* slot = rec + 2 * (sc->run & 1);
+  slot[1] = make_double2(sc->hist_s, sc->hist_r);
+  slot[0] = make_double2((double)sc->status, (double)sc->run);
+  __threadfence_system();
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -718,6 +885,174 @@ extern "C" int h2b_gmres(h2b_handle h, const void* b_perm, void* x_perm, int res
 // ===========================================================================
 // BiCGStab (arith.py:605-689)
 // ===========================================================================
+// Graph-driven loop: one iteration (two matvecs, three dot launches, the vector updates and
+// the scalar kernels above) is ONE CUDA graph; the host queues iteration i+1 before it reads
+// iteration i's record, so the GPU never waits for the host.  A speculative iteration after a
+// terminal status is a no-op on the vectors (the status is sticky).  Same recurrence, tests and
+// order of operations as the host-driven loop below; scalars are numpy-style complex128.
+int bicgstab_graph(h2b_ctx* h, const double2* b, double2* x, double2* r, double2* rh, double2* p,
+                   double2* v, double2* s, double2* t, BiSc* sc, double bnrm, double tol, int max_iter,
+                   const double2* noise, double* history, h2b_report* report, cudaStream_t st,
+                   double t0) {
+  const int64_t n = h->n;
+  const int nb = nblocks(n);
+  double2* partial = g_scratch.partial;
+  double2* vals = g_scratch.vals;
+  double2* rec_h = g_scratch.host + 200;  // pinned, mapped: two records of two double2
+  double2* rec = nullptr;
+  H2B_CUDA_TRY(cudaHostGetDevicePointer((void**)&rec, rec_h, 0));
+  {
+    BiSc init{};
+    init.rho = init.alpha = init.omega = make_double2(1.0, 0.0);
+    init.p_zero = 1;
+    H2B_CUDA_TRY(cudaMemcpyAsync(sc, &init, sizeof(BiSc), cudaMemcpyHostToDevice, st));
+    H2B_CUDA_TRY(cudaStreamSynchronize(st));  // `init` leaves scope
+  }
+  const double eps = 2.220446049250313e-16;
+  const double thr = eps * eps * std::max(1.0, bnrm * bnrm);
+  TRY(h2b_prepare(h));  // streams, events and the matvec workspace exist before the capture
+  TRY(h2b_ensure_workspace(h, 1));
+  // ---- capture one iteration ----
+  cudaStream_t cs = nullptr;
+  H2B_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  H2B_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  auto dots = [&](std::initializer_list<std::pair<const double2*, const double2*>> pairs) {
+    DotPairs d;
+    d.np = 0;
+    for (auto& pr : pairs) {
+      d.a[d.np] = pr.first;
+      d.b[d.np] = pr.second;
+      ++d.np;
+    }
+    k_dots_partial<<<nb, RT, 0, cs>>>(d, n, partial);
+    k_reduce_partials<<<d.np, 32, 0, cs>>>(partial, nb, d.np, vals);
+  };
+  int nl = 0;
+  dots({{rh, r}});                                                             // rho_new
+  k_bi_rho<<<1, 1, 0, cs>>>(sc, vals, thr);
+  k_lincomb_dev<<<nb, RT, 0, cs>>>(sc, BI_RUN, sc->cp, 3, r, p, v, p, n, nullptr);  // p
+  int rc = h2b_enqueue_matvec(h, p, v, 1, cs, &nl);                            // v = A p
+  if (!rc) {
+    dots({{rh, v}});
+    k_bi_alpha<<<1, 1, 0, cs>>>(sc, vals);
+    k_lincomb_dev<<<nb, RT, 0, cs>>>(sc, BI_RUN, sc->cs, 2, r, v, nullptr, s, n, partial);  // s
+    k_reduce_partials<<<1, 32, 0, cs>>>(partial, nb, 1, vals);
+    k_bi_snorm<<<1, 1, 0, cs>>>(sc, vals, bnrm, tol);
+    k_lincomb_dev<<<nb, RT, 0, cs>>>(sc, BI_CONV_S, sc->cx, 2, x, p, nullptr, x, n, nullptr);
+    k_bi_mark<<<1, 1, 0, cs>>>(sc, BI_CONV_S, BI_CONV_S_DONE);
+    rc = h2b_enqueue_matvec(h, s, t, 1, cs, &nl);                              // t = A s
+  }
+  if (!rc) {
+    dots({{t, t}, {t, s}});
+    k_bi_omega<<<1, 1, 0, cs>>>(sc, vals);
+    k_lincomb_dev<<<nb, RT, 0, cs>>>(sc, BI_RUN, sc->cx, 3, x, p, s, x, n, nullptr);    // x
+    k_lincomb_dev<<<nb, RT, 0, cs>>>(sc, BI_RUN, sc->cr, 2, s, t, nullptr, r, n, partial);  // r
+    k_reduce_partials<<<1, 32, 0, cs>>>(partial, nb, 1, vals);
+    k_bi_final<<<1, 1, 0, cs>>>(sc, vals, bnrm, tol, rec);
+  }
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(cs, &g);
+  cudaStreamDestroy(cs);
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess) {
+    h2b_set_error(std::string("h2b_bicgstab: capture: ") + cudaGetErrorString(e));
+    return H2B_ECUDA;
+  }
+  cudaGraphExec_t gx = nullptr;
+  e = cudaGraphInstantiate(&gx, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    h2b_set_error(std::string("h2b_bicgstab: instantiate: ") + cudaGetErrorString(e));
+    return H2B_ECUDA;
+  }
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  struct Guard {
+    cudaGraphExec_t g;
+    cudaEvent_t* e;
+    ~Guard() {
+      cudaGraphExecDestroy(g);
+      if (e[0]) cudaEventDestroy(e[0]);
+      if (e[1]) cudaEventDestroy(e[1]);
+    }
+  } guard{gx, ev};
+  H2B_CUDA_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  H2B_CUDA_TRY(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  // ---- the loop ----
+  int launches = 0;
+  auto launch = [&]() -> int {
+    H2B_CUDA_TRY(cudaGraphLaunch(gx, st));
+    H2B_CUDA_TRY(cudaEventRecord(ev[launches & 1], st));
+    ++launches;
+    return H2B_OK;
+  };
+  int it = 0, matvecs = 0, nh = 0;
+  bool converged = false, restarted = false;
+  TRY(launch());
+  int obs = 0;  // launch index of the iteration observed next
+  while (true) {
+    ++it;
+    if (it < max_iter) TRY(launch());  // speculative next iteration
+    H2B_CUDA_TRY(cudaEventSynchronize(ev[obs & 1]));
+    const double2* slot = rec_h + 2 * ((obs + 1) & 1);
+    const int status = (int)slot[0].x;
+    if ((int)slot[0].y != obs + 1) {
+      h2b_set_error("h2b_bicgstab: iteration record out of sequence");
+      return H2B_ECUDA;
+    }
+    const double hs = slot[1].x, hr = slot[1].y;
+    auto push = [&](double val) {
+      if (history && nh < max_iter) history[nh] = val;
+      ++nh;
+    };
+    bool stop = true;
+    if (status == BI_RUN) {
+      push(hr);
+      matvecs += 2;
+      stop = it >= max_iter;
+      obs += 1;
+    } else if (status == BI_CONV_R) {
+      push(hr);
+      matvecs += 2;
+      converged = true;
+    } else if (status == BI_CONV_S || status == BI_CONV_S_DONE) {
+      push(hs);
+      matvecs += 1;
+      converged = true;
+    } else if (status == BI_NONFINITE) {
+      push(hr);
+      matvecs += 2;
+    } else if (status == BI_DENOM_ZERO) {
+      matvecs += 1;
+    } else if (status == BI_OMEGA_ZERO) {
+      matvecs += 2;
+    } else if (status == BI_RHO_BREAK && !restarted && noise) {
+      // restart once (the reference re-seeds the shadow residual) and redo this iteration
+      Ops ops{st, n, nb, partial, vals, g_scratch.host};
+      TRY(ops.lincomb(rh, {{cplx(1.0), r}, {cplx(1.0), noise}}, -1));
+      H2B_CUDA_TRY(cudaMemsetAsync(v, 0, sizeof(double2) * n, st));
+      H2B_CUDA_TRY(cudaMemsetAsync(p, 0, sizeof(double2) * n, st));
+      k_bi_restart<<<1, 1, 0, st>>>(sc);
+      H2B_CHECK_LAUNCH();
+      restarted = true;
+      --it;
+      TRY(launch());
+      obs = launches - 1;
+      stop = false;
+    }
+    if (stop) break;
+  }
+  H2B_CUDA_TRY(cudaStreamSynchronize(st));
+  report->iterations = it;
+  report->converged = converged ? 1 : 0;
+  report->n_history = nh < max_iter ? nh : max_iter;
+  report->matvecs = matvecs;
+  report->wall_time = now_s() - t0;
+  return H2B_OK;
+}
+
 extern "C" int h2b_bicgstab(h2b_handle h, const void* b_perm, void* x_perm, double tol, int max_iter,
                             const void* shadow_perm, const void* restart_noise_perm, double* history,
                             h2b_report* report, void* stream) {
@@ -738,8 +1073,9 @@ extern "C" int h2b_bicgstab(h2b_handle h, const void* b_perm, void* x_perm, doub
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t n = h->n;
   double2* ws = nullptr;
-  TRY(krylov_ws(h, sizeof(double2) * (size_t)n * 6, &ws));
+  TRY(krylov_ws(h, sizeof(double2) * (size_t)n * 6 + sizeof(BiSc), &ws));
   double2 *r = ws, *rh = ws + n, *p = ws + 2 * n, *v = ws + 3 * n, *s = ws + 4 * n, *t = ws + 5 * n;
+  BiSc* sc = reinterpret_cast<BiSc*>(ws + 6 * n);
   const double2* b = (const double2*)b_perm;
   double2* x = (double2*)x_perm;
   Ops ops{st, n, nblocks(n), g_scratch.partial, g_scratch.vals, g_scratch.host};
@@ -760,6 +1096,9 @@ extern "C" int h2b_bicgstab(h2b_handle h, const void* b_perm, void* x_perm, doub
                                cudaMemcpyDeviceToDevice, st));
   H2B_CUDA_TRY(cudaMemsetAsync(v, 0, sizeof(double2) * n, st));
   H2B_CUDA_TRY(cudaMemsetAsync(p, 0, sizeof(double2) * n, st));
+  if (!getenv("H2B_BICG_HOST"))  // H2B_BICG_HOST: the host-driven loop below (A/B timing)
+    return bicgstab_graph(h, b, x, r, rh, p, v, s, t, sc, bnrm, tol, max_iter,
+                          (const double2*)restart_noise_perm, history, report, st, t0);
   cplx rho = 1.0, alpha = 1.0, omega = 1.0;
   bool converged = false, restarted = false, p_zero = true;
   int it = 0, matvecs = 0, nh = 0;
