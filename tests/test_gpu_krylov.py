@@ -70,3 +70,46 @@ def test_gmres_config1_iteration_count():
     assert rel(x, ex["gmres_x"]) <= 1e-5
     op = as_operator(pk)
     assert np.linalg.norm(op.matvec(x) - b) / np.linalg.norm(b) <= 1e-6
+
+
+@pytest.mark.parametrize("name,restart", [("rod164", 30), ("cube2", 10), ("line2048", 30)])
+def test_gmres_fused_arnoldi_step_matches_multi_kernel_step(name, restart, monkeypatch):
+    """The single-cluster Arnoldi step (k_arnoldi_cluster, DSMEM reductions) and the nine-launch
+    step reach the same solution in the same number of iterations (±1: summation orders differ)."""
+    from paper_1703_01175_b200 import gmres_solve
+    pk, ex = load_golden(name)
+    b = ex["x"][:, 0]
+    xf, rf = gmres_solve(pk, b, tol=1e-8, restart=restart, max_iter=2000)
+    monkeypatch.setenv("H2B_NO_FUSED_ARNOLDI", "1")
+    xm, rm = gmres_solve(pk, b, tol=1e-8, restart=restart, max_iter=2000)
+    assert rf.converged and rm.converged
+    assert abs(rf.iterations - rm.iterations) <= 1
+    assert rel(xf, xm) <= 1e-7
+    k = min(10, len(rf.residual_history))
+    assert np.allclose(rf.residual_history[:k], rm.residual_history[:k], rtol=1e-8)
+
+
+@pytest.mark.parametrize("name", ["rod164", "cube2"])
+def test_bicgstab_graph_loop_matches_host_loop(name, monkeypatch):
+    """The graph-driven BiCGStab (device scalars, sticky status, records read one iteration
+    behind) and the host-driven loop give the same iterations (±1) and solution."""
+    from paper_1703_01175_b200 import bicgstab_solve
+    pk, ex = load_golden(name)
+    xg, rg = bicgstab_solve(pk, ex["bicg_rhs"], tol=1e-6, max_iter=400)
+    monkeypatch.setenv("H2B_BICG_HOST", "1")
+    xh, rh = bicgstab_solve(pk, ex["bicg_rhs"], tol=1e-6, max_iter=400)
+    assert rg.converged == rh.converged
+    assert abs(rg.iterations - rh.iterations) <= 1
+    assert rel(xg, xh) <= 1e-6
+    assert len(rg.residual_history) == rg.iterations
+
+
+def test_bicgstab_graph_loop_iteration_cap():
+    """max_iter stops the graph-driven loop exactly (the speculative iteration is never queued
+    past the cap) and the history holds one entry per iteration."""
+    from paper_1703_01175_b200 import bicgstab_solve
+    pk, ex = load_golden("rod164")
+    for cap in (1, 2, 5):
+        _, rep = bicgstab_solve(pk, ex["bicg_rhs"], tol=1e-14, max_iter=cap)
+        assert rep.iterations == cap and not rep.converged
+        assert len(rep.residual_history) == cap
