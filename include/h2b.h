@@ -245,7 +245,10 @@ int h2b_plan_run(h2b_plan_handle p, int phase, const void* x, const void* xhat, 
 /* q = 1 near-field of a plan on the streaming near-field kernel: items {int64 y_row; int32
  * b_first, nb; int32 row0, pad} (rows_per_thread * 128 / (ns/2) rows of a ns-point leaf each),
  * blocks {int64 d_off (in payload 4), int64 x_row}.  When set, h2b_plan_run(phase 4, q = 1)
- * overwrites y with the near-field and then runs phase 5 (the leaf back-transform items). */
+ * overwrites y with the near-field and then runs phase 5 (the leaf back-transform items);
+ * h2b_plan_run(H2B_PLAN_PHASE_NEAR_FAST, q = 1) runs the near-field alone (it reads only x, so
+ * it may run on a second stream beside phases 1-3, with phase 5 after both). */
+#define H2B_PLAN_PHASE_NEAR_FAST 6
 int h2b_plan_set_near_fast(h2b_plan_handle p, const void* items, int64_t n_items, const void* blks,
                            int64_t n_blks, int ns, int rows_per_thread);
 /* q = 1 coupling of a plan on the panel kernels: payload 3 holds, per target, the stacked Sᵀ

@@ -70,6 +70,7 @@ NEAR_BLK = _np.dtype([("d_off", "<i8"), ("x_off", "<i8")])
 COUPLE_ITEM = _np.dtype([("panel", "<i8"), ("xcol", "<i8"), ("out", "<i8"), ("R", "<i4"), ("w", "<i4")])
 B_X, B_XHAT, B_YHAT, B_Y = 0, 1, 2, 3
 ITEM_ACC, ITEM_BCAST = 256, 512
+PLAN_PHASE_NEAR_FAST = 6  # h2b.h H2B_PLAN_PHASE_NEAR_FAST
 
 
 class H2BError(RuntimeError):

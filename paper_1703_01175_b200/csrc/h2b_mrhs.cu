@@ -798,6 +798,14 @@ extern "C" int h2b_plan_set_phase(h2b_plan_handle p, int phase, int n_launches, 
 
 extern "C" int h2b_plan_run(h2b_plan_handle p, int phase, const void* x, const void* xhat, void* yhat,
                             void* y, int q, void* stream) {
+  if (p && phase == H2B_PLAN_PHASE_NEAR_FAST) {  // the q = 1 streaming near-field alone
+    if (q != 1 || p->nf_n == 0) {
+      h2b_set_error("h2b_plan_run: the near-field-only phase needs q = 1 and h2b_plan_set_near_fast");
+      return H2B_EINVAL;
+    }
+    return h2b_launch_near_list(p->nf_items, p->nf_n, p->nf_blks, p->pay[4], (const double2*)x, (double2*)y,
+                                p->nf_ns, p->nf_r, (cudaStream_t)stream);
+  }
   if (!p || phase < 0 || phase >= (int)p->phases.size() || q < 1) {
     h2b_set_error("h2b_plan_run: bad arguments");
     return H2B_EINVAL;

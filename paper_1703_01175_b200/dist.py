@@ -24,8 +24,8 @@ import numpy as np
 
 from . import _abi
 from .krylov import SolveReport
-from .shard import (N_PAY, PH_COUPLE, PH_DOWN, PH_NEAR, PH_UP_OWN, PH_UP_TOP, PHASES, partition,
-                    plan_shard)
+from .shard import (N_PAY, PH_COUPLE, PH_DOWN, PH_LEAFBACK, PH_NEAR, PH_UP_OWN, PH_UP_TOP, PHASES,
+                    partition, plan_shard)
 
 _UPLOAD_CHUNK = 1 << 30
 
@@ -83,7 +83,9 @@ class CudaPlanEngine:
                                                   cf["xcol"].ctypes.data_as(C.POINTER(C.c_int32)),
                                                   int(cf["xcol"].size)), "h2b_plan_set_couple_fast")
         nf = getattr(plan, "near_fast", None)
-        if nf is not None and nf["items"].size:  # q = 1 near-field on the streaming kernel
+        self.has_near_fast = bool(nf is not None and nf["items"].size)
+        self._side = self._ev = None
+        if self.has_near_fast:  # q = 1 near-field on the streaming kernel
             _abi.check(L.h2b_plan_set_near_fast(h, nf["items"].ctypes.data, int(nf["items"].size),
                                                 nf["blks"].ctypes.data, int(nf["blks"].size),
                                                 int(nf["ns"]), int(nf["R"])), "h2b_plan_set_near_fast")
@@ -106,6 +108,30 @@ class CudaPlanEngine:
                                            C.c_void_p(xbuf.data_ptr()), C.c_void_p(yhat.data_ptr()),
                                            C.c_void_p(y.data_ptr()), int(q),
                                            C.c_void_p(st.cuda_stream)), "h2b_plan_run")
+
+    def run_tail(self, xbuf, yhat, y, q):
+        """The phases after the exchange: UP_TOP → COUPLE → DOWN (the far field), and NEAR.  At
+        q = 1 with the streaming near-field, the near-field (it reads only x) runs on a second
+        stream beside the latency-bound far-field chain, and the leaf back-transform (it needs
+        both) after the join — capturable into the caller's CUDA graph."""
+        torch = __import__("torch")
+        if not (q == 1 and self.has_near_fast):
+            for ph in (PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR):
+                self.run(ph, xbuf, yhat, y, q)
+            return
+        main = torch.cuda.current_stream(self.device)
+        if self._side is None:  # high priority: the chain's CTAs go ahead of the near-field's
+            self._side = torch.cuda.Stream(self.device, priority=-1)
+            self._ev = (torch.cuda.Event(), torch.cuda.Event())
+        fork, join = self._ev
+        fork.record(main)
+        self._side.wait_event(fork)
+        for ph in (PH_UP_TOP, PH_COUPLE, PH_DOWN):
+            self.run(ph, xbuf, yhat, y, 1, stream=self._side)
+        self.run(_abi.PLAN_PHASE_NEAR_FAST, xbuf, yhat, y, 1, stream=main)
+        join.record(self._side)
+        main.wait_event(join)
+        self.run(PH_LEAFBACK, xbuf, yhat, y, 1, stream=main)
 
     def device_bytes(self):
         return int(_abi.lib().h2b_plan_device_bytes(self.handle))
@@ -254,8 +280,12 @@ class DistH2Operator:
         else:
             self.engine.run(PH_UP_OWN, xbuf, yhat, y, q)
             self.exchange(xbuf, send, q)
-        for ph in (PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR):
-            self.engine.run(ph, xbuf, yhat, y, q)
+        tail = getattr(self.engine, "run_tail", None)  # the CPU plan interpreter has none
+        if tail is not None:
+            tail(xbuf, yhat, y, q)
+        else:
+            for ph in (PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR):
+                self.engine.run(ph, xbuf, yhat, y, q)
 
     def matvec_local(self, x_local, graph=True):
         """This rank's rows of S x.  On CUDA the whole step — the plan launches of every phase

@@ -26,7 +26,7 @@ def _ranks(pk):
     return out
 
 
-def _run_sharded(pk, G, X, **plan_kw):
+def _run_sharded(pk, G, X, tail=False, **plan_kw):
     from paper_1703_01175_b200.dist import CudaPlanEngine
     from paper_1703_01175_b200.shard import (PH_COUPLE, PH_DOWN, PH_NEAR, PH_UP_OWN, PH_UP_TOP,
                                              partition, plan_shard)
@@ -48,8 +48,11 @@ def _run_sharded(pk, G, X, **plan_kw):
     Y = torch.empty_like(Xd)
     for g, p in enumerate(plans):
         bufs[g][0][:G * ch] = gathered
-        for ph in (PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR):
-            eng[g].run(ph, *bufs[g], q)
+        if tail:  # the dist operator's tail: near-field on a second stream beside the far field
+            eng[g].run_tail(*bufs[g], q)
+        else:
+            for ph in (PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR):
+                eng[g].run(ph, *bufs[g], q)
         Y[p.row0:p.row0 + p.nrows] = bufs[g][2]
     torch.cuda.synchronize()
     for e in eng:
@@ -75,6 +78,7 @@ def test_shard_plans_on_device_baseline_configs(k):
     yp = ex["y"][pk.perm][:, :1]
     for G in (1, 2, 4, 8):
         assert rel(_run_sharded(pk, G, xp), yp) <= 1e-10, G
+        assert rel(_run_sharded(pk, G, xp, tail=True), yp) <= 1e-10, G
 
 
 def test_dist_operator_single_rank_gmres():

@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--ranks", default="")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--phases", action="store_true", help="also time each phase (events between launches)")
+    ap.add_argument("--sequential", action="store_true", help="phases one after another (no concurrent near-field)")
     a = ap.parse_args()
     from paper_1703_01175_b200.dist import CudaPlanEngine
     from paper_1703_01175_b200.pack import load_packed
@@ -79,9 +81,13 @@ def main():
         st = torch.cuda.Stream(dev)
         st.wait_stream(torch.cuda.current_stream())
 
-        def step():
-            for ph in (PH_UP_OWN, PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR):
-                eng.run(ph, xb, xh, y, 1)
+        def step():  # as DistH2Operator._body after the exchange
+            eng.run(PH_UP_OWN, xb, xh, y, 1)
+            if a.sequential:
+                for ph in (PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR):
+                    eng.run(ph, xb, xh, y, 1)
+            else:
+                eng.run_tail(xb, xh, y, 1)
 
         with torch.cuda.stream(st):
             step()  # warm (lazy preparation outside the capture)
@@ -100,9 +106,23 @@ def main():
             torch.cuda.synchronize()
             times.append(s.elapsed_time(e))
         ms = float(np.median(times))
+        phase_ms = None
+        if a.phases:  # per phase, outside the graph (launch overheads included), L2 flushed per step
+            names = ("UP_OWN", "UP_TOP", "COUPLE", "DOWN", "NEAR")
+            acc = np.zeros(5)
+            for _ in range(a.reps):
+                flush.flush()
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+                ev[0].record()
+                for i, ph in enumerate((PH_UP_OWN, PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR)):
+                    eng.run(ph, xb, xh, y, 1)
+                    ev[i + 1].record()
+                torch.cuda.synchronize()
+                acc += [ev[i].elapsed_time(ev[i + 1]) for i in range(5)]
+            phase_ms = dict(zip(names, (acc / a.reps).round(4).tolist()))
         rec = {"rank": g, "G": G, "rows": int(p.nrows), "ms": ms, "payload_bytes": p.payload_bytes(),
                "payload_gbs": p.payload_bytes() / (ms * 1e-3) / 1e9, "plan_s": round(t_plan, 2),
-               "fill_s": round(t_fill, 2)}
+               "fill_s": round(t_fill, 2), "phase_ms": phase_ms}
         out.append(rec)
         print(json.dumps(rec), flush=True)
         if a.check:
