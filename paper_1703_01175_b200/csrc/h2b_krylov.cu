@@ -592,6 +592,207 @@ __global__ void k_bi_omega(BiSc* sc, const double2* vals) {
   sc->cr[1] = make_double2(-om.x, -om.y);
 }
 
+// ---------------------------------------------------------------------------
+// Small n: each of the three vector segments of a BiCGStab iteration (dots -> scalar tests ->
+// vector updates -> norm -> tests) as ONE launch of a 16-CTA thread-block cluster instead of
+// five to seven launches.  Every CTA computes the same scalars from the same cluster sums
+// (CTA-order summation over distributed shared memory: deterministic), CTA 0 alone writes the
+// state back.  Segment 0: rho / p.  1: alpha / s / ||s|| test / x on convergence.  2: omega /
+// x / r / ||r|| test / record.
+// ---------------------------------------------------------------------------
+struct BiSegArgs {
+  BiSc* sc;
+  const double2 *rh;
+  double2 *r, *p, *v, *s, *t, *x;
+  int64_t n;
+  int R;  // rows per CTA
+  double thr, bnrm, tol;
+  double2* rec;
+};
+
+template <int NP>
+__device__ __forceinline__ void cl_sums(cooperative_groups::cluster_group& cl, double2 (&v)[NP],
+                                        double2* part, double2* red, double2* bcast) {
+  // v: this thread's partials -> the cluster totals (valid in every thread of every CTA)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int NW = AC_T / 32;
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    const double2 w = warp_sum2(v[i]);
+    if (lane == 0) red[i * NW + warp] = w;
+  }
+  __syncthreads();
+  if (tid < NP) {
+    double2 a = make_double2(0.0, 0.0);
+    for (int q = 0; q < NW; ++q) a = cadd(a, red[tid * NW + q]);
+    part[tid] = a;
+  }
+  cl.sync();
+  if (tid < NP) {
+    double2 a = make_double2(0.0, 0.0);
+    for (int q = 0; q < (int)cl.num_blocks(); ++q) a = cadd(a, cl.map_shared_rank(part, q)[tid]);
+    bcast[tid] = a;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NP; ++i) v[i] = bcast[i];
+}
+
+__global__ void __launch_bounds__(AC_T) k_bicg_segment(BiSegArgs A, int seg) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ double2 part0[4], part1[4], red[4 * (AC_T / 32)], bc[4];
+  __shared__ BiSc S;  // this CTA's copy of the state
+  const int tid = threadIdx.x, c = (int)cl.block_rank();
+  const int64_t row0 = (int64_t)c * A.R;
+  const int64_t row1 = row0 + A.R < A.n ? row0 + A.R : A.n;
+  if (tid == 0) S = *A.sc;
+  __syncthreads();
+  const int status0 = S.status;
+  if (seg == 0) {
+    if (tid == 0) ++S.run;
+    if (status0 == BI_RUN) {
+      double2 d[1] = {make_double2(0.0, 0.0)};
+      for (int64_t i = row0 + tid; i < row1; i += AC_T) cfma_conj(d[0], A.rh[i], A.r[i]);
+      cl_sums<1>(cl, d, part0, red, bc);
+      if (tid == 0) {
+        const double2 rn = d[0];
+        if (hypot(rn.x, rn.y) < A.thr) {
+          S.status = BI_RHO_BREAK;
+        } else if (S.p_zero) {
+          S.cp[0] = make_double2(1.0, 0.0);
+          S.cp[1] = S.cp[2] = make_double2(0.0, 0.0);
+          S.p_zero = 0;
+          S.rho_new = rn;
+        } else {
+          const double2 beta = cmul(cdiv(rn, S.rho), cdiv(S.alpha, S.omega));
+          const double2 bo = cmul(beta, S.omega);
+          S.cp[0] = make_double2(1.0, 0.0);
+          S.cp[1] = beta;
+          S.cp[2] = make_double2(-bo.x, -bo.y);
+          S.rho_new = rn;
+        }
+      }
+      __syncthreads();
+      if (S.status == BI_RUN)
+        for (int64_t i = row0 + tid; i < row1; i += AC_T) {
+          double2 acc = make_double2(0.0, 0.0);
+          cfma(acc, S.cp[0], A.r[i]);
+          cfma(acc, S.cp[1], A.p[i]);
+          cfma(acc, S.cp[2], A.v[i]);
+          A.p[i] = acc;
+        }
+    }
+  } else if (seg == 1 && status0 == BI_RUN) {
+    double2 d[1] = {make_double2(0.0, 0.0)};
+    for (int64_t i = row0 + tid; i < row1; i += AC_T) cfma_conj(d[0], A.rh[i], A.v[i]);
+    cl_sums<1>(cl, d, part0, red, bc);
+    if (tid == 0) {
+      if (d[0].x == 0.0 && d[0].y == 0.0) {
+        S.status = BI_DENOM_ZERO;
+      } else {
+        S.alpha = cdiv(S.rho_new, d[0]);
+        S.cs[0] = make_double2(1.0, 0.0);
+        S.cs[1] = make_double2(-S.alpha.x, -S.alpha.y);
+      }
+    }
+    __syncthreads();
+    if (S.status == BI_RUN) {
+      double2 nr[1] = {make_double2(0.0, 0.0)};
+      for (int64_t i = row0 + tid; i < row1; i += AC_T) {
+        double2 acc = make_double2(0.0, 0.0);
+        cfma(acc, S.cs[0], A.r[i]);
+        cfma(acc, S.cs[1], A.v[i]);
+        A.s[i] = acc;
+        nr[0].x = fma(acc.x, acc.x, nr[0].x);
+        nr[0].x = fma(acc.y, acc.y, nr[0].x);
+      }
+      cl_sums<1>(cl, nr, part1, red, bc);
+      if (tid == 0) {
+        const double rel = sqrt(nr[0].x) / A.bnrm;
+        S.hist_s = rel;
+        if (rel <= A.tol) {
+          S.cx[0] = make_double2(1.0, 0.0);
+          S.cx[1] = S.alpha;
+          S.status = BI_CONV_S_DONE;  // x updated right below
+        }
+      }
+      __syncthreads();
+      if (S.status == BI_CONV_S_DONE)
+        for (int64_t i = row0 + tid; i < row1; i += AC_T) {
+          double2 acc = make_double2(0.0, 0.0);
+          cfma(acc, S.cx[0], A.x[i]);
+          cfma(acc, S.cx[1], A.p[i]);
+          A.x[i] = acc;
+        }
+    }
+  } else if (seg == 2) {
+    if (status0 == BI_RUN) {
+      double2 d[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+      for (int64_t i = row0 + tid; i < row1; i += AC_T) {
+        cfma_conj(d[0], A.t[i], A.t[i]);
+        cfma_conj(d[1], A.t[i], A.s[i]);
+      }
+      cl_sums<2>(cl, d, part0, red, bc);
+      if (tid == 0) {
+        const double tt = d[0].x;
+        if (tt == 0.0) {
+          S.status = BI_OMEGA_ZERO;
+        } else {
+          const double2 om = cdiv(d[1], make_double2(tt, 0.0));
+          if (om.x == 0.0 && om.y == 0.0) {
+            S.status = BI_OMEGA_ZERO;
+          } else {
+            S.omega = om;
+            S.cx[0] = make_double2(1.0, 0.0);
+            S.cx[1] = S.alpha;
+            S.cx[2] = om;
+            S.cr[0] = make_double2(1.0, 0.0);
+            S.cr[1] = make_double2(-om.x, -om.y);
+          }
+        }
+      }
+      __syncthreads();
+      if (S.status == BI_RUN) {
+        double2 nr[1] = {make_double2(0.0, 0.0)};
+        for (int64_t i = row0 + tid; i < row1; i += AC_T) {
+          double2 acc = make_double2(0.0, 0.0);
+          cfma(acc, S.cx[0], A.x[i]);
+          cfma(acc, S.cx[1], A.p[i]);
+          cfma(acc, S.cx[2], A.s[i]);
+          A.x[i] = acc;
+          double2 rr = make_double2(0.0, 0.0);
+          cfma(rr, S.cr[0], A.s[i]);
+          cfma(rr, S.cr[1], A.t[i]);
+          A.r[i] = rr;
+          nr[0].x = fma(rr.x, rr.x, nr[0].x);
+          nr[0].x = fma(rr.y, rr.y, nr[0].x);
+        }
+        cl_sums<1>(cl, nr, part1, red, bc);
+        if (tid == 0) {
+          const double rel = sqrt(nr[0].x) / A.bnrm;
+          S.hist_r = rel;
+          S.rho = S.rho_new;
+          if (rel <= A.tol)
+            S.status = BI_CONV_R;
+          else if (!isfinite(rel))
+            S.status = BI_NONFINITE;
+        }
+      }
+    }
+    if (c == 0 && tid == 0) {  // the iteration's record (every iteration, whatever the status)
+      double2* slot = A.rec + 2 * (S.run & 1);
+      slot[1] = make_double2(S.hist_s, S.hist_r);
+      slot[0] = make_double2((double)S.status, (double)S.run);
+    }
+  }
+  if (c == 0 && tid == 0) {
+    *A.sc = S;
+    __threadfence_system();
+  }
+  cl.sync();  // no CTA's shared memory is read after its exit
+}
+
 // restart with a re-seeded shadow residual: scalars back to 1, p = v = 0 (the run counter stays)
 __global__ void k_bi_restart(BiSc* sc) {
   sc->rho = sc->alpha = sc->omega = make_double2(1.0, 0.0);
@@ -890,79 +1091,17 @@ extern "C" int h2b_gmres(h2b_handle h, const void* b_perm, void* x_perm, int res
 // iteration i's record, so the GPU never waits for the host.  A speculative iteration after a
 // terminal status is a no-op on the vectors (the status is sticky).  Same recurrence, tests and
 // order of operations as the host-driven loop below; scalars are numpy-style complex128.
-int bicgstab_graph(h2b_ctx* h, const double2* b, double2* x, double2* r, double2* rh, double2* p,
-                   double2* v, double2* s, double2* t, BiSc* sc, double bnrm, double tol, int max_iter,
-                   const double2* noise, double* history, h2b_report* report, cudaStream_t st,
-                   double t0) {
-  const int64_t n = h->n;
+// the host side of the graph-driven loop: one launch of the captured iteration per step, the
+// record read one iteration behind
+int bicgstab_loop(h2b_ctx* h, cudaGraph_t g, double2* r, double2* rh, double2* p, double2* v, BiSc* sc,
+                  int64_t n, int max_iter, const double2* noise, double* history, h2b_report* report,
+                  cudaStream_t st, double t0, double2* rec_h) {
+  (void)h;
   const int nb = nblocks(n);
   double2* partial = g_scratch.partial;
   double2* vals = g_scratch.vals;
-  double2* rec_h = g_scratch.host + 200;  // pinned, mapped: two records of two double2
-  double2* rec = nullptr;
-  H2B_CUDA_TRY(cudaHostGetDevicePointer((void**)&rec, rec_h, 0));
-  {
-    BiSc init{};
-    init.rho = init.alpha = init.omega = make_double2(1.0, 0.0);
-    init.p_zero = 1;
-    H2B_CUDA_TRY(cudaMemcpyAsync(sc, &init, sizeof(BiSc), cudaMemcpyHostToDevice, st));
-    H2B_CUDA_TRY(cudaStreamSynchronize(st));  // `init` leaves scope
-  }
-  const double eps = 2.220446049250313e-16;
-  const double thr = eps * eps * std::max(1.0, bnrm * bnrm);
-  TRY(h2b_prepare(h));  // streams, events and the matvec workspace exist before the capture
-  TRY(h2b_ensure_workspace(h, 1));
-  // ---- capture one iteration ----
-  cudaStream_t cs = nullptr;
-  H2B_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-  H2B_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-  auto dots = [&](std::initializer_list<std::pair<const double2*, const double2*>> pairs) {
-    DotPairs d;
-    d.np = 0;
-    for (auto& pr : pairs) {
-      d.a[d.np] = pr.first;
-      d.b[d.np] = pr.second;
-      ++d.np;
-    }
-    k_dots_partial<<<nb, RT, 0, cs>>>(d, n, partial);
-    k_reduce_partials<<<d.np, 32, 0, cs>>>(partial, nb, d.np, vals);
-  };
-  int nl = 0;
-  dots({{rh, r}});                                                             // rho_new
-  k_bi_rho<<<1, 1, 0, cs>>>(sc, vals, thr);
-  k_lincomb_dev<<<nb, RT, 0, cs>>>(sc, BI_RUN, sc->cp, 3, r, p, v, p, n, nullptr);  // p
-  int rc = h2b_enqueue_matvec(h, p, v, 1, cs, &nl);                            // v = A p
-  if (!rc) {
-    dots({{rh, v}});
-    k_bi_alpha<<<1, 1, 0, cs>>>(sc, vals);
-    k_lincomb_dev<<<nb, RT, 0, cs>>>(sc, BI_RUN, sc->cs, 2, r, v, nullptr, s, n, partial);  // s
-    k_reduce_partials<<<1, 32, 0, cs>>>(partial, nb, 1, vals);
-    k_bi_snorm<<<1, 1, 0, cs>>>(sc, vals, bnrm, tol);
-    k_lincomb_dev<<<nb, RT, 0, cs>>>(sc, BI_CONV_S, sc->cx, 2, x, p, nullptr, x, n, nullptr);
-    k_bi_mark<<<1, 1, 0, cs>>>(sc, BI_CONV_S, BI_CONV_S_DONE);
-    rc = h2b_enqueue_matvec(h, s, t, 1, cs, &nl);                              // t = A s
-  }
-  if (!rc) {
-    dots({{t, t}, {t, s}});
-    k_bi_omega<<<1, 1, 0, cs>>>(sc, vals);
-    k_lincomb_dev<<<nb, RT, 0, cs>>>(sc, BI_RUN, sc->cx, 3, x, p, s, x, n, nullptr);    // x
-    k_lincomb_dev<<<nb, RT, 0, cs>>>(sc, BI_RUN, sc->cr, 2, s, t, nullptr, r, n, partial);  // r
-    k_reduce_partials<<<1, 32, 0, cs>>>(partial, nb, 1, vals);
-    k_bi_final<<<1, 1, 0, cs>>>(sc, vals, bnrm, tol, rec);
-  }
-  cudaGraph_t g = nullptr;
-  cudaError_t e = cudaStreamEndCapture(cs, &g);
-  cudaStreamDestroy(cs);
-  if (rc) {
-    if (g) cudaGraphDestroy(g);
-    return rc;
-  }
-  if (e != cudaSuccess) {
-    h2b_set_error(std::string("h2b_bicgstab: capture: ") + cudaGetErrorString(e));
-    return H2B_ECUDA;
-  }
   cudaGraphExec_t gx = nullptr;
-  e = cudaGraphInstantiate(&gx, g, 0);
+  cudaError_t e = cudaGraphInstantiate(&gx, g, 0);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) {
     h2b_set_error(std::string("h2b_bicgstab: instantiate: ") + cudaGetErrorString(e));
@@ -1051,6 +1190,137 @@ int bicgstab_graph(h2b_ctx* h, const double2* b, double2* x, double2* r, double2
   report->matvecs = matvecs;
   report->wall_time = now_s() - t0;
   return H2B_OK;
+}
+
+int bicgstab_graph(h2b_ctx* h, const double2* b, double2* x, double2* r, double2* rh, double2* p,
+                   double2* v, double2* s, double2* t, BiSc* sc, double bnrm, double tol, int max_iter,
+                   const double2* noise, double* history, h2b_report* report, cudaStream_t st,
+                   double t0) {
+  const int64_t n = h->n;
+  const int nb = nblocks(n);
+  double2* partial = g_scratch.partial;
+  double2* vals = g_scratch.vals;
+  double2* rec_h = g_scratch.host + 200;  // pinned, mapped: two records of two double2
+  double2* rec = nullptr;
+  H2B_CUDA_TRY(cudaHostGetDevicePointer((void**)&rec, rec_h, 0));
+  {
+    BiSc init{};
+    init.rho = init.alpha = init.omega = make_double2(1.0, 0.0);
+    init.p_zero = 1;
+    H2B_CUDA_TRY(cudaMemcpyAsync(sc, &init, sizeof(BiSc), cudaMemcpyHostToDevice, st));
+    H2B_CUDA_TRY(cudaStreamSynchronize(st));  // `init` leaves scope
+  }
+  const double eps = 2.220446049250313e-16;
+  const double thr = eps * eps * std::max(1.0, bnrm * bnrm);
+  TRY(h2b_prepare(h));  // streams, events and the matvec workspace exist before the capture
+  TRY(h2b_ensure_workspace(h, 1));
+  // ---- capture one iteration ----
+  cudaStream_t cs = nullptr;
+  H2B_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  H2B_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  auto dots = [&](std::initializer_list<std::pair<const double2*, const double2*>> pairs) {
+    DotPairs d;
+    d.np = 0;
+    for (auto& pr : pairs) {
+      d.a[d.np] = pr.first;
+      d.b[d.np] = pr.second;
+      ++d.np;
+    }
+    k_dots_partial<<<nb, RT, 0, cs>>>(d, n, partial);
+    k_reduce_partials<<<d.np, 32, 0, cs>>>(partial, nb, d.np, vals);
+  };
+  int nl = 0;
+  // small n: the three vector segments as single cluster launches (k_bicg_segment)
+  int seg_cl = 0;
+  if (!getenv("H2B_BICG_UNFUSED") && n <= 16384) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(16);
+    cfg.blockDim = dim3(AC_T);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 16;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaFuncSetAttribute(k_bicg_segment, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+        cudaOccupancyMaxActiveClusters(&ncl, k_bicg_segment, &cfg) == cudaSuccess && ncl >= 1)
+      seg_cl = 16;
+    cudaGetLastError();
+  }
+  if (seg_cl) {
+    BiSegArgs sa{sc, rh, r, p, v, s, t, x, n, (int)((n + seg_cl - 1) / seg_cl), thr, bnrm, tol, rec};
+    auto seg = [&](int k) -> int {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(seg_cl);
+      cfg.blockDim = dim3(AC_T);
+      cfg.stream = cs;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = seg_cl;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      if (cudaLaunchKernelEx(&cfg, k_bicg_segment, sa, k) != cudaSuccess) {
+        h2b_set_error("h2b_bicgstab: fused segment launch failed");
+        return H2B_ECUDA;
+      }
+      return H2B_OK;
+    };
+    int rc = seg(0);
+    if (!rc) rc = h2b_enqueue_matvec(h, p, v, 1, cs, &nl);
+    if (!rc) rc = seg(1);
+    if (!rc) rc = h2b_enqueue_matvec(h, s, t, 1, cs, &nl);
+    if (!rc) rc = seg(2);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cs, &g);
+    cudaStreamDestroy(cs);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) {
+      h2b_set_error(std::string("h2b_bicgstab: capture: ") + cudaGetErrorString(e));
+      return H2B_ECUDA;
+    }
+    return bicgstab_loop(h, g, r, rh, p, v, sc, n, max_iter, noise, history, report, st, t0, rec_h);
+  }
+  dots({{rh, r}});                                                             // rho_new
+  k_bi_rho<<<1, 1, 0, cs>>>(sc, vals, thr);
+  k_lincomb_dev<<<nb, RT, 0, cs>>>(sc, BI_RUN, sc->cp, 3, r, p, v, p, n, nullptr);  // p
+  int rc = h2b_enqueue_matvec(h, p, v, 1, cs, &nl);                            // v = A p
+  if (!rc) {
+    dots({{rh, v}});
+    k_bi_alpha<<<1, 1, 0, cs>>>(sc, vals);
+    k_lincomb_dev<<<nb, RT, 0, cs>>>(sc, BI_RUN, sc->cs, 2, r, v, nullptr, s, n, partial);  // s
+    k_reduce_partials<<<1, 32, 0, cs>>>(partial, nb, 1, vals);
+    k_bi_snorm<<<1, 1, 0, cs>>>(sc, vals, bnrm, tol);
+    k_lincomb_dev<<<nb, RT, 0, cs>>>(sc, BI_CONV_S, sc->cx, 2, x, p, nullptr, x, n, nullptr);
+    k_bi_mark<<<1, 1, 0, cs>>>(sc, BI_CONV_S, BI_CONV_S_DONE);
+    rc = h2b_enqueue_matvec(h, s, t, 1, cs, &nl);                              // t = A s
+  }
+  if (!rc) {
+    dots({{t, t}, {t, s}});
+    k_bi_omega<<<1, 1, 0, cs>>>(sc, vals);
+    k_lincomb_dev<<<nb, RT, 0, cs>>>(sc, BI_RUN, sc->cx, 3, x, p, s, x, n, nullptr);    // x
+    k_lincomb_dev<<<nb, RT, 0, cs>>>(sc, BI_RUN, sc->cr, 2, s, t, nullptr, r, n, partial);  // r
+    k_reduce_partials<<<1, 32, 0, cs>>>(partial, nb, 1, vals);
+    k_bi_final<<<1, 1, 0, cs>>>(sc, vals, bnrm, tol, rec);
+  }
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(cs, &g);
+  cudaStreamDestroy(cs);
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess) {
+    h2b_set_error(std::string("h2b_bicgstab: capture: ") + cudaGetErrorString(e));
+    return H2B_ECUDA;
+  }
+  return bicgstab_loop(h, g, r, rh, p, v, sc, n, max_iter, noise, history, report, st, t0, rec_h);
 }
 
 extern "C" int h2b_bicgstab(h2b_handle h, const void* b_perm, void* x_perm, double tol, int max_iter,
