@@ -90,11 +90,15 @@ def test_gmres_fused_arnoldi_step_matches_multi_kernel_step(name, restart, monke
 
 
 @pytest.mark.parametrize("name", ["rod164", "cube2"])
-def test_bicgstab_graph_loop_matches_host_loop(name, monkeypatch):
+@pytest.mark.parametrize("unfused", [False, True])
+def test_bicgstab_graph_loop_matches_host_loop(name, unfused, monkeypatch):
     """The graph-driven BiCGStab (device scalars, sticky status, records read one iteration
-    behind) and the host-driven loop give the same iterations (±1) and solution."""
+    behind; fused cluster segments or separate launches) and the host-driven loop give the same
+    iterations (±1) and solution."""
     from paper_1703_01175_b200 import bicgstab_solve
     pk, ex = load_golden(name)
+    if unfused:
+        monkeypatch.setenv("H2B_BICG_UNFUSED", "1")
     xg, rg = bicgstab_solve(pk, ex["bicg_rhs"], tol=1e-6, max_iter=400)
     monkeypatch.setenv("H2B_BICG_HOST", "1")
     xh, rh = bicgstab_solve(pk, ex["bicg_rhs"], tol=1e-6, max_iter=400)
