@@ -339,11 +339,23 @@ __global__ void __launch_bounds__(AC_T) k_arnoldi_cluster(ArnoldiArgs A) {
   const int rows = left <= 0 ? 0 : (left < R ? (int)left : R);
   double2* Vs = dsm;                // nv x R (vector-major)
   double2* ws = dsm + (size_t)nv * R;
-  for (int idx = tid; idx < nv * R; idx += AC_T) {
-    const int i = idx / R, r = idx - i * R;
-    Vs[idx] = r < rows ? A.V[(int64_t)i * A.n + row0 + r] : make_double2(0.0, 0.0);
+  // this CTA's rows of the nv basis vectors and of w: one bulk copy per vector (a thread-strided
+  // copy loop would serialise its global loads), rows past n zeroed
+  __shared__ __align__(8) uint64_t bar;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_expect_tx(&bar, 16u * (uint32_t)(nv + 1) * (uint32_t)rows);
   }
-  for (int r = tid; r < R; r += AC_T) ws[r] = r < rows ? A.w[row0 + r] : make_double2(0.0, 0.0);
+  __syncthreads();
+  if (tid <= nv && rows > 0)
+    bulk_g2s(tid < nv ? Vs + (size_t)tid * R : ws, tid < nv ? A.V + (int64_t)tid * A.n + row0 : A.w + row0,
+             16u * (uint32_t)rows, &bar);
+  for (int idx = tid; idx < (nv + 1) * (R - rows); idx += AC_T) {
+    const int i = idx / (R - rows), r = rows + (idx - i * (R - rows));
+    (i < nv ? Vs + (size_t)i * R : ws)[r] = make_double2(0.0, 0.0);
+  }
+  mbar_wait(&bar, 0);
   __syncthreads();
   for (int pass = 0; pass < 2; ++pass) {
     for (int i = warp; i < nv; i += NW) {  // this CTA's part of <V_i, w>, fixed order
