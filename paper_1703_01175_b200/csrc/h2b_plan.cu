@@ -444,7 +444,8 @@ bool plan_with_split(const h2b_ctx* h, int ls, Plan& pl) {
 }
 
 // ------------------------- persistent-kernel task graph -------------------------
-constexpr int MEGA_BUDGET = 5800;  // double2 elements (92.8 KB): largest work area of a far CTA
+constexpr int MEGA_BUDGET = 7000;  // double2 elements (112 KB): largest work area of a far CTA
+                                   // (5800 / 8200 measured 2-3 us slower at cfg2: profiles/r01_budget_ab.txt)
 constexpr int MEGA_BUDGET_MAX = 12000;  // tuning override ceiling (the near ring shrinks to fit)
 constexpr int MEGA_BLOB_MAX = 1024;  // 16-byte slots (16 KB) of per-CTA task blob
 constexpr double NEAR_TASK_BYTES = 64e3;  // target D bytes per near-field task
