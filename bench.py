@@ -12,9 +12,12 @@ shipped packed as data/cfg2.npz (tools/make_golden.py).
 * ``e2e``     the same metric through the reference-facing call with HOST
               buffers (h2b_matvec_host: pinned H2D, gather, matvec, scatter,
               D2H), wall clock per call.
-* ``roofline`` the near-field kernel (the byte-dominant one): algorithmic bytes
-              (16·E_D + 32·N) / its average event-timed duration, against the
-              measured HBM copy bandwidth in MEASURED_PEAKS.json.
+* ``roofline`` the whole matvec step (the near-field stream and the far-field
+              task graph run concurrently, so the step is the unit one launch
+              pair processes): algorithmic bytes B_alg = 16(E_V+E_T+E_S+E_D) +
+              32(N+K) / the average event-timed step, against the measured HBM
+              copy bandwidth in MEASURED_PEAKS.json; ``dominant_kernel`` times
+              the near-field kernel alone the same way.
 * ``cpu_baseline`` the reference algorithm restated on the CPU
               (oracle/h2_oracle.py, a faithful port of arith.matvec) timed on
               this host, 1 thread.

@@ -39,6 +39,8 @@ def block_gmres_solve(apply_block, rhs, tol=1e-6, restart=30, max_iter=1000):
     if max_iter < 1 or restart < 1:
         raise ValueError("max_iter and restart must be >= 1")
     op = _operator_of(apply_block)
+    if op is None:
+        raise TypeError("block_gmres_solve needs the operator (H2Operator / H2Matrix / PackedH2)")
     B_h = np.asarray(rhs, dtype=np.complex128)
     if B_h.ndim != 2 or B_h.shape[0] != op.n:
         raise ValueError(f"rhs must be ({op.n}, q)")

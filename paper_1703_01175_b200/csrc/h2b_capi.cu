@@ -3,6 +3,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <iterator>
 #include <string>
 
 #include "h2b_common.cuh"
@@ -42,13 +43,17 @@ void free_ctx(h2b_ctx* h) {
                   h->couple_targets, h->span_heads, h->span_copies, h->span_outs,
                   h->span_ops, h->near_items, h->near_blks, h->couple_items, h->tasks, h->deps,
                   h->near_tasks, h->leaf_items, h->couple_groups, h->ctrl, h->flags, h->trace,
-                  h->rec_pool, h->l2_prefetch, h->cta_lists, h->task_list, h->near_recs, h->near_idx, h->wbuf, h->ydeep};
+                  h->rec_pool, h->l2_prefetch, h->cta_lists, h->task_list, h->near_recs, h->near_idx, h->wbuf, h->ydeep,
+                  h->ks_partial, h->ks_vals};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->far_stream) cudaStreamDestroy(h->far_stream);
   if (h->host_stream) cudaStreamDestroy(h->host_stream);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->ev_done) cudaEventDestroy(h->ev_done);
+  if (h->ks_host) cudaFreeHost(h->ks_host);
+  if (h->hpin) cudaFreeHost(h->hpin);
   delete h;
 }
 
@@ -196,7 +201,21 @@ int h2b_upload(h2b_handle h, int sec, const void* src, size_t bytes, size_t offs
   H2B_CUDA_TRY(cudaSetDevice(h->device));
   // host or device source (unified addressing): device-side fills need no host staging
   H2B_CUDA_TRY(cudaMemcpy((char*)h->buf[sec] + offset, src, bytes, cudaMemcpyDefault));
-  h->sec_uploaded[sec] = std::max<int64_t>(h->sec_uploaded[sec], (int64_t)((offset + bytes) / 16));
+  // record the chunk as a range and merge it with the ones it touches: ready() passes only
+  // when the merged ranges cover the whole section (any chunk order, overlaps allowed)
+  int64_t b = (int64_t)(offset / 16), e = (int64_t)((offset + bytes) / 16);
+  auto& iv = h->sec_iv[sec];
+  auto it = iv.upper_bound(b);
+  if (it != iv.begin() && std::prev(it)->second >= b) --it;
+  while (it != iv.end() && it->first <= e) {
+    b = std::min(b, it->first);
+    e = std::max(e, it->second);
+    it = iv.erase(it);
+  }
+  iv.emplace(b, e);
+  int64_t covered = 0;
+  for (const auto& kv : iv) covered += kv.second - kv.first;
+  h->sec_uploaded[sec] = covered;
   return H2B_OK;
 }
 
@@ -253,8 +272,34 @@ int h2b_matvec_host(h2b_handle h, const void* x, void* y, int q) {
   double2* dyp = h->hyp;                 // permuted
   double2* dy = h->hyp + h->n * q;       // original order
   cudaStream_t st = h->host_stream;
+  H2B_TRY(h2b_order_begin(h, st));
+  // pageable caller buffers (numpy arrays: the reference-facing drop-in) are staged through the
+  // handle's own pinned buffers so the call still runs as one graph with one DMA per direction;
+  // H2B_HOST_STAGING=driver leaves pageable copies to the CUDA driver instead (A/B timing)
+  const bool x_pinned = is_pinned(x), y_pinned = is_pinned(y);
+  static const bool driver_staging = [] {
+    const char* e = getenv("H2B_HOST_STAGING");
+    return e && !strcmp(e, "driver");
+  }();
+  const void* xs = x;
+  void* ys = y;
+  if (h->use_graphs && !driver_staging && (!x_pinned || !y_pinned)) {
+    if (h->hpin_bytes < 2 * bytes) {
+      h2b_release_graphs(h);  // host-path graphs hold the old staging pointers
+      if (h->hpin) cudaFreeHost(h->hpin);
+      h->hpin = nullptr;
+      h->hpin_bytes = 0;
+      H2B_CUDA_TRY(cudaMallocHost(&h->hpin, 2 * bytes));
+      h->hpin_bytes = 2 * bytes;
+    }
+    if (!x_pinned) {
+      memcpy(h->hpin, x, bytes);
+      xs = h->hpin;
+    }
+    if (!y_pinned) ys = (char*)h->hpin + bytes;
+  }
   auto enqueue = [&](cudaStream_t s, bool in_graph) -> int {
-    H2B_CUDA_TRY(cudaMemcpyAsync(dx, x, bytes, cudaMemcpyHostToDevice, s));
+    H2B_CUDA_TRY(cudaMemcpyAsync(dx, xs, bytes, cudaMemcpyHostToDevice, s));
     int r = h2b_launch_gather(h->perm, h->n, dx, dxp, q, s);
     if (!r) {
       int nl = 0;
@@ -262,15 +307,15 @@ int h2b_matvec_host(h2b_handle h, const void* x, void* y, int q) {
     }
     if (!r) r = h2b_launch_scatter(h->perm, h->n, dyp, dy, q, s);
     if (r) return r;
-    H2B_CUDA_TRY(cudaMemcpyAsync(y, dy, bytes, cudaMemcpyDeviceToHost, s));
+    H2B_CUDA_TRY(cudaMemcpyAsync(ys, dy, bytes, cudaMemcpyDeviceToHost, s));
     return H2B_OK;
   };
-  if (h->use_graphs && is_pinned(x) && is_pinned(y)) {
+  if (h->use_graphs && is_pinned(xs) && is_pinned(ys)) {
     // pinned host buffers: the whole call (H2D, gather, matvec, scatter, D2H) is one graph
     H2B_TRY(h2b_prepare(h));
     H2B_TRY(h2b_ensure_workspace(h, q));
     if (q >= 2 && h->use_mrhs) H2B_TRY(h2b_mrhs_workspace(h, q));
-    const GraphKey key{x, y, -q};  // negative q: host-path graph
+    const GraphKey key{xs, ys, -q};  // negative q: host-path graph
     auto it = h->graphs.find(key);
     if (it == h->graphs.end()) {
       cudaStream_t cs = nullptr;
@@ -296,7 +341,9 @@ int h2b_matvec_host(h2b_handle h, const void* x, void* y, int q) {
   } else {
     H2B_TRY(enqueue(st, false));
   }
+  H2B_TRY(h2b_order_end(h, st));
   H2B_CUDA_TRY(cudaStreamSynchronize(st));
+  if (ys != y) memcpy(y, ys, bytes);
   return H2B_OK;
 }
 

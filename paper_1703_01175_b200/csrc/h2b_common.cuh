@@ -221,7 +221,8 @@ struct h2b_ctx {
   int64_t K = 0;
   int64_t n_coupling = 0, n_near = 0;
   int64_t sec_elems[4] = {0, 0, 0, 0};
-  int64_t sec_uploaded[4] = {0, 0, 0, 0};
+  int64_t sec_uploaded[4] = {0, 0, 0, 0};  // elements covered by the uploaded chunks
+  std::map<int64_t, int64_t> sec_iv[4];     // merged [begin, end) element ranges uploaded
   bool prepared = false;  // device-side transposes / tables done
   int uniform_leaf = 0;   // leaf size if all leaves share it, else 0
 
@@ -299,6 +300,8 @@ struct h2b_ctx {
   double2 *xhat = nullptr, *yhat = nullptr;
   int64_t ws_q = 0;
   double2 *hxp = nullptr, *hyp = nullptr;  // host-path staging
+  void* hpin = nullptr;                     // pinned host staging of pageable x / y
+  size_t hpin_bytes = 0;
   int64_t hws_q = 0;
   // streams / events / graphs
   cudaStream_t far_stream = nullptr;
@@ -310,6 +313,14 @@ struct h2b_ctx {
   int use_mega = 1;  // plan the persistent single-launch kernel for q = 1
   // krylov workspace
   void* kry = nullptr;
+  // per-handle Krylov scratch on this handle's device (h2b_krylov.cu): reduction partials,
+  // device scalars and mapped pinned host records (GMRES residuals / BiCGStab records in
+  // separate slots)
+  double2 *ks_partial = nullptr, *ks_vals = nullptr, *ks_host = nullptr;
+  // device-side ordering of this handle's work across caller streams: every matvec / solve
+  // waits for the previous one (whatever stream it ran on) and records ev_done after itself,
+  // because the captured graphs share x̂/ŷ, control flags and workspaces
+  cudaEvent_t ev_done = nullptr;
   size_t kry_bytes = 0;
   int64_t device_bytes = 0;
   int launches_q1 = 0;  // kernels per q=1 matvec (reported to the bench)
@@ -324,6 +335,9 @@ int h2b_ensure_workspace(h2b_ctx* h, int q);
 int h2b_run_matvec(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st);
 // the launches of one matvec without graph replay (for capture into a larger graph)
 int h2b_enqueue_matvec(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st, int* nl);
+// cross-stream ordering of the handle's device work (see h2b_ctx::ev_done)
+int h2b_order_begin(h2b_ctx* h, cudaStream_t st);
+int h2b_order_end(h2b_ctx* h, cudaStream_t st);
 int h2b_run_phase(h2b_ctx* h, int phase, const double2* xp, double2* yp, int q, cudaStream_t st);
 int h2b_launch_gather(const int64_t* perm, int64_t n, const double2* in, double2* out, int q,
                       cudaStream_t st);

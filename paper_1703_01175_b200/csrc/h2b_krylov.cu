@@ -7,13 +7,16 @@
 //
 // Vector work is done by fused reduction kernels with a deterministic
 // two-stage (per-CTA partial, then fixed-order final sum) reduction, so the
-// same inputs always produce the same bits.  The tiny (m+1)xm Hessenberg /
-// Givens algebra runs on the host from scalars copied back once per step.
+// same inputs always produce the same bits.  The Givens rotations of each
+// Arnoldi step run on the device (givens_update); the host reads each step's
+// residual from mapped pinned memory one step behind the GPU and does the
+// cycle's (<= 63 x 63) back substitution.
 #include <math.h>
 
 #include <algorithm>
 #include <chrono>
 #include <complex>
+#include <map>
 #include <vector>
 
 #include <cooperative_groups.h>
@@ -139,23 +142,57 @@ int nblocks(int64_t n) {
 
 typedef std::complex<double> cplx;
 
-// scratch shared by the exported vector kernels (per process, single device)
+// Scratch of the reductions: partials (RB_MAX * 64), device scalars (256) and pinned, mapped
+// host scalars (SCR_HOST).  Solvers use the scratch of their handle (allocated on the handle's
+// device, never reallocated, so captured step graphs stay valid); the handle-less exported
+// vector kernels use one scratch per (thread, device).  Host slots: [0, 128) general (fetched
+// dot products, back-substitution coefficients), [128, 256) GMRES (res_j, hn_j) records,
+// [256, 260) BiCGStab iteration records.
+constexpr int SCR_HOST = 512, SCR_GMRES = 128, SCR_BICG = 256;
 struct Scratch {
-  double2* partial = nullptr;  // RB_MAX * 64
-  double2* vals = nullptr;     // 256 device scalars
-  double2* host = nullptr;     // 256 pinned host scalars
-  int device = -1;
+  double2* partial = nullptr;
+  double2* vals = nullptr;
+  double2* host = nullptr;
 };
-Scratch g_scratch;
 
-int scratch_ready() {
+int scratch_alloc(Scratch* s) {
+  H2B_CUDA_TRY(cudaMalloc(&s->partial, sizeof(double2) * RB_MAX * 64));
+  H2B_CUDA_TRY(cudaMalloc(&s->vals, sizeof(double2) * 256));
+  H2B_CUDA_TRY(cudaHostAlloc(&s->host, sizeof(double2) * SCR_HOST, cudaHostAllocMapped));
+  return H2B_OK;
+}
+
+int handle_scratch(h2b_ctx* h, Scratch* out) {
+  H2B_CUDA_TRY(cudaSetDevice(h->device));
+  if (!h->ks_partial) {
+    Scratch s;
+    const int rc = scratch_alloc(&s);
+    if (rc) {
+      if (s.partial) cudaFree(s.partial);
+      if (s.vals) cudaFree(s.vals);
+      return rc;
+    }
+    h->ks_partial = s.partial;
+    h->ks_vals = s.vals;
+    h->ks_host = s.host;
+  }
+  out->partial = h->ks_partial;
+  out->vals = h->ks_vals;
+  out->host = h->ks_host;
+  return H2B_OK;
+}
+
+int thread_scratch(Scratch* out) {
+  static thread_local std::map<int, Scratch> per_device;
   int dev = 0;
   H2B_CUDA_TRY(cudaGetDevice(&dev));
-  if (g_scratch.partial && g_scratch.device == dev) return H2B_OK;
-  H2B_CUDA_TRY(cudaMalloc(&g_scratch.partial, sizeof(double2) * RB_MAX * 64));
-  H2B_CUDA_TRY(cudaMalloc(&g_scratch.vals, sizeof(double2) * 256));
-  H2B_CUDA_TRY(cudaMallocHost(&g_scratch.host, sizeof(double2) * 256));
-  g_scratch.device = dev;
+  auto it = per_device.find(dev);
+  if (it == per_device.end()) {
+    Scratch s;
+    H2B_TRY(scratch_alloc(&s));
+    it = per_device.emplace(dev, s).first;
+  }
+  *out = it->second;
   return H2B_OK;
 }
 
@@ -245,6 +282,7 @@ struct GivensState {
   double2* cs_sn;   // m: {c_i, 0}
   double2* res_hn;  // 2m: {res_j, 0}, {hn_j, 0}
   double2* scale;   // 1: 1 / hn of the last step (0 on breakdown)
+  double2* bnrm;    // 1: {||b||, 0} of the current solve (written per solve, read by the graphs)
   double2* host_res = nullptr;  // optional: mapped pinned copy of res_hn (stored by the kernel itself)
 };
 
@@ -252,7 +290,8 @@ struct GivensState {
 // hc = h1 + h2 (CGS2), apply rotations 0..j-1, new rotation zeroing hn, update g.  The cosines
 // c_i live in cs_sn[i].x, the complex sines s_i in the spare last row of H (H[m*m + i]), which
 // never holds a Hessenberg entry (the sub-diagonal is rotated away, never stored).
-__device__ __noinline__ void givens_update(int j, int m, const double2* hv, GivensState S, double bnrm) {
+__device__ __noinline__ void givens_update(int j, int m, const double2* hv, GivensState S) {
+  const double bnrm = S.bnrm[0].x;
   double2 hc[64];
   for (int i = 0; i <= j; ++i) hc[i] = make_double2(hv[i].x + hv[64 + i].x, hv[i].y + hv[64 + i].y);
   const double hn = sqrt(hv[128].x);
@@ -297,8 +336,13 @@ __device__ __noinline__ void givens_update(int j, int m, const double2* hv, Give
   S.scale[0] = make_double2(hn == 0.0 ? 0.0 : 1.0 / hn, 0.0);
 }
 
-__global__ void k_givens_step(int j, int m, const double2* __restrict__ hv, GivensState S, double bnrm) {
-  if (threadIdx.x == 0) givens_update(j, m, hv, S, bnrm);
+__global__ void k_givens_step(int j, int m, const double2* __restrict__ hv, GivensState S) {
+  if (threadIdx.x == 0) givens_update(j, m, hv, S);
+}
+
+// out = {sqrt(v[0].x), 0}: a norm from a reduced squared norm
+__global__ void k_set_norm(const double2* __restrict__ v, double2* out) {
+  out[0] = make_double2(sqrt(v[0].x), 0.0);
 }
 
 // ---------------------------------------------------------------------------
@@ -318,7 +362,6 @@ struct ArnoldiArgs {
   double2* w;
   double2* hv;  // [0, nv): pass-1 coefficients, [64, 64 + nv): pass 2, [128]: ||w||^2
   GivensState S;
-  double bnrm;
   int j, m;
 };
 
@@ -405,7 +448,7 @@ __global__ void __launch_bounds__(AC_T) k_arnoldi_cluster(ArnoldiArgs A) {
   cl.sync();  // every remote read done: no CTA's shared memory is read after this point
   const double hn = sqrt(s_hn2), f = hn == 0.0 ? 0.0 : 1.0 / hn;  // = givens_update's scale
   for (int r = tid; r < rows; r += AC_T) A.w[row0 + r] = make_double2(ws[r].x * f, ws[r].y * f);
-  if (c == 0 && tid == 0) givens_update(A.j, A.m, A.hv, A.S, A.bnrm);  // reads CTA 0's hv writes
+  if (c == 0 && tid == 0) givens_update(A.j, A.m, A.hv, A.S);  // reads CTA 0's hv writes
 }
 
 // Fused Arnoldi step configuration for (n, m): cluster size and rows per CTA, or cl = 0 (the
@@ -840,13 +883,14 @@ extern "C" int h2b_zdotc_multi(const void* V, int64_t ldv, int nv, const void* w
     h2b_set_error("h2b_zdotc_multi: bad arguments (need 1 <= nv <= 64)");
     return H2B_EINVAL;
   }
-  TRY(scratch_ready());
+  Scratch sc;
+  TRY(thread_scratch(&sc));
   cudaStream_t st = (cudaStream_t)stream;
   const int nb = nblocks(n);
   k_basis_dots_partial<<<dim3(nb, nv), RT, 0, st>>>((const double2*)V, ldv, nv, (const double2*)w, n,
-                                          g_scratch.partial);
+                                          sc.partial);
   H2B_CHECK_LAUNCH();
-  k_reduce_partials<<<nv, 32, 0, st>>>(g_scratch.partial, nb, nv, (double2*)out_dev);
+  k_reduce_partials<<<nv, 32, 0, st>>>(sc.partial, nb, nv, (double2*)out_dev);
   H2B_CHECK_LAUNCH();
   return H2B_OK;
 }
@@ -857,16 +901,17 @@ extern "C" int h2b_zgemv_sub(const void* V, int64_t ldv, int nv, const void* h_d
     h2b_set_error("h2b_zgemv_sub: bad arguments (need 0 <= nv <= 64)");
     return H2B_EINVAL;
   }
-  TRY(scratch_ready());
+  Scratch sc;
+  TRY(thread_scratch(&sc));
   cudaStream_t st = (cudaStream_t)stream;
   const int nb = nblocks(n);
   k_basis_sub<<<nb, RT, 0, st>>>((const double2*)V, ldv, nv, (const double2*)h_dev, (double2*)w, n,
-                                 nrm2_out_dev ? g_scratch.partial : nullptr);
+                                 nrm2_out_dev ? sc.partial : nullptr);
   H2B_CHECK_LAUNCH();
   if (nrm2_out_dev) {
-    k_reduce_partials<<<1, 32, 0, st>>>(g_scratch.partial, nb, 1, g_scratch.vals);
+    k_reduce_partials<<<1, 32, 0, st>>>(sc.partial, nb, 1, sc.vals);
     H2B_CHECK_LAUNCH();
-    H2B_CUDA_TRY(cudaMemcpyAsync(nrm2_out_dev, g_scratch.vals, sizeof(double), cudaMemcpyDeviceToDevice, st));
+    H2B_CUDA_TRY(cudaMemcpyAsync(nrm2_out_dev, sc.vals, sizeof(double), cudaMemcpyDeviceToDevice, st));
   }
   return H2B_OK;
 }
@@ -902,12 +947,19 @@ extern "C" int h2b_gmres(h2b_handle h, const void* b_perm, void* x_perm, int res
     return H2B_EINVAL;
   }
   const double t0 = now_s();
-  TRY(scratch_ready());
+  Scratch g_scratch;
+  TRY(handle_scratch(h, &g_scratch));
   cudaStream_t st = (cudaStream_t)stream;
+  TRY(h2b_order_begin(h, st));
+  struct OrderEnd {  // the solve's last work on `st` orders the handle's next call
+    h2b_ctx* h;
+    cudaStream_t st;
+    ~OrderEnd() { h2b_order_end(h, st); }
+  } order_end{h, st};
   const int64_t n = h->n;
   const int m = restart;
   // workspace: V (m+1) x n basis, r, tmp, then the device Givens state
-  const size_t gs_elems = (size_t)(m + 1) * m + (m + 1) + 3 * (size_t)m + 1;
+  const size_t gs_elems = (size_t)(m + 1) * m + (m + 1) + 3 * (size_t)m + 2;
   double2* ws = nullptr;
   TRY(krylov_ws(h, sizeof(double2) * ((size_t)n * (m + 3) + gs_elems), &ws));
   double2* V = ws;
@@ -919,11 +971,12 @@ extern "C" int h2b_gmres(h2b_handle h, const void* b_perm, void* x_perm, int res
   S.cs_sn = S.g + (m + 1);
   S.res_hn = S.cs_sn + m;
   S.scale = S.res_hn + m + m;
+  S.bnrm = S.scale + 1;
   const double2* b = (const double2*)b_perm;
   double2* x = (double2*)x_perm;
   Ops ops{st, n, nblocks(n), g_scratch.partial, g_scratch.vals, g_scratch.host};
   double2* hvals = g_scratch.vals;        // device scalars (CGS2 coefficients, ||w||^2)
-  double2* hres = g_scratch.host + 128;   // pinned: (res_j, hn_j) of step j
+  double2* hres = g_scratch.host + SCR_GMRES;  // pinned: (res_j, hn_j) of step j
   S.host_res = nullptr;
   if (!getenv("H2B_GMRES_COPY_RES") && cudaHostGetDevicePointer((void**)&S.host_res, hres, 0) != cudaSuccess) {
     cudaGetLastError();
@@ -941,6 +994,10 @@ extern "C" int h2b_gmres(h2b_handle h, const void* b_perm, void* x_perm, int res
     return H2B_OK;
   }
   H2B_CUDA_TRY(cudaMemcpyAsync(r, b, sizeof(double2) * n, cudaMemcpyDeviceToDevice, st));
+  // ||b|| lives in device memory: the cached step graphs read it there, so a later solve with
+  // another right-hand side on the same handle scales its residuals by its own norm
+  k_set_norm<<<1, 1, 0, st>>>(g_scratch.vals, S.bnrm);
+  H2B_CHECK_LAUNCH();
   const FusedArnoldi fa = fused_arnoldi_config(n, m);
   // one Arnoldi step j (matvec, CGS2, device Givens, normalisation, (res, hn) -> pinned host)
   // as a CUDA graph, captured once per (basis, j) and replayed
@@ -960,7 +1017,7 @@ extern "C" int h2b_gmres(h2b_handle h, const void* b_perm, void* x_perm, int res
     if (!rc) {
       const int nb = ops.nb;
       if (fa.cl > 0) {  // the whole post-matvec step as one cluster launch
-        ArnoldiArgs aa{V, n, j + 1, fa.R, w, hvals, S, bnrm, j, m};
+        ArnoldiArgs aa{V, n, j + 1, fa.R, w, hvals, S, j, m};
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(fa.cl);
         cfg.blockDim = dim3(AC_T);
@@ -986,7 +1043,7 @@ extern "C" int h2b_gmres(h2b_handle h, const void* b_perm, void* x_perm, int res
       k_reduce_partials<<<j + 1, 32, 0, cs>>>(ops.partial, nb, j + 1, hvals + 64);
       k_basis_sub<<<nb, RT, 0, cs>>>(V, n, j + 1, hvals + 64, w, n, ops.partial);
       k_reduce_partials<<<1, 32, 0, cs>>>(ops.partial, nb, 1, hvals + 128);
-      k_givens_step<<<1, 32, 0, cs>>>(j, m, hvals, S, bnrm);
+      k_givens_step<<<1, 32, 0, cs>>>(j, m, hvals, S);
       k_scale_dev<<<nb, RT, 0, cs>>>(w, n, S.scale);
       }
       if (!S.host_res)
@@ -1107,7 +1164,7 @@ extern "C" int h2b_gmres(h2b_handle h, const void* b_perm, void* x_perm, int res
 // record read one iteration behind
 int bicgstab_loop(h2b_ctx* h, cudaGraph_t g, double2* r, double2* rh, double2* p, double2* v, BiSc* sc,
                   int64_t n, int max_iter, const double2* noise, double* history, h2b_report* report,
-                  cudaStream_t st, double t0, double2* rec_h) {
+                  cudaStream_t st, double t0, double2* rec_h, const Scratch& g_scratch) {
   (void)h;
   const int nb = nblocks(n);
   double2* partial = g_scratch.partial;
@@ -1204,7 +1261,7 @@ int bicgstab_loop(h2b_ctx* h, cudaGraph_t g, double2* r, double2* rh, double2* p
   return H2B_OK;
 }
 
-int bicgstab_graph(h2b_ctx* h, const double2* b, double2* x, double2* r, double2* rh, double2* p,
+int bicgstab_graph(h2b_ctx* h, const Scratch& g_scratch, const double2* b, double2* x, double2* r, double2* rh, double2* p,
                    double2* v, double2* s, double2* t, BiSc* sc, double bnrm, double tol, int max_iter,
                    const double2* noise, double* history, h2b_report* report, cudaStream_t st,
                    double t0) {
@@ -1212,7 +1269,7 @@ int bicgstab_graph(h2b_ctx* h, const double2* b, double2* x, double2* r, double2
   const int nb = nblocks(n);
   double2* partial = g_scratch.partial;
   double2* vals = g_scratch.vals;
-  double2* rec_h = g_scratch.host + 200;  // pinned, mapped: two records of two double2
+  double2* rec_h = g_scratch.host + SCR_BICG;  // pinned, mapped: two records of two double2
   double2* rec = nullptr;
   H2B_CUDA_TRY(cudaHostGetDevicePointer((void**)&rec, rec_h, 0));
   {
@@ -1297,7 +1354,7 @@ int bicgstab_graph(h2b_ctx* h, const double2* b, double2* x, double2* r, double2
       h2b_set_error(std::string("h2b_bicgstab: capture: ") + cudaGetErrorString(e));
       return H2B_ECUDA;
     }
-    return bicgstab_loop(h, g, r, rh, p, v, sc, n, max_iter, noise, history, report, st, t0, rec_h);
+    return bicgstab_loop(h, g, r, rh, p, v, sc, n, max_iter, noise, history, report, st, t0, rec_h, g_scratch);
   }
   dots({{rh, r}});                                                             // rho_new
   k_bi_rho<<<1, 1, 0, cs>>>(sc, vals, thr);
@@ -1332,7 +1389,7 @@ int bicgstab_graph(h2b_ctx* h, const double2* b, double2* x, double2* r, double2
     h2b_set_error(std::string("h2b_bicgstab: capture: ") + cudaGetErrorString(e));
     return H2B_ECUDA;
   }
-  return bicgstab_loop(h, g, r, rh, p, v, sc, n, max_iter, noise, history, report, st, t0, rec_h);
+  return bicgstab_loop(h, g, r, rh, p, v, sc, n, max_iter, noise, history, report, st, t0, rec_h, g_scratch);
 }
 
 extern "C" int h2b_bicgstab(h2b_handle h, const void* b_perm, void* x_perm, double tol, int max_iter,
@@ -1351,8 +1408,15 @@ extern "C" int h2b_bicgstab(h2b_handle h, const void* b_perm, void* x_perm, doub
     return H2B_EINVAL;
   }
   const double t0 = now_s();
-  TRY(scratch_ready());
+  Scratch g_scratch;
+  TRY(handle_scratch(h, &g_scratch));
   cudaStream_t st = (cudaStream_t)stream;
+  TRY(h2b_order_begin(h, st));
+  struct OrderEnd {
+    h2b_ctx* h;
+    cudaStream_t st;
+    ~OrderEnd() { h2b_order_end(h, st); }
+  } order_end{h, st};
   const int64_t n = h->n;
   double2* ws = nullptr;
   TRY(krylov_ws(h, sizeof(double2) * (size_t)n * 6 + sizeof(BiSc), &ws));
@@ -1379,7 +1443,7 @@ extern "C" int h2b_bicgstab(h2b_handle h, const void* b_perm, void* x_perm, doub
   H2B_CUDA_TRY(cudaMemsetAsync(v, 0, sizeof(double2) * n, st));
   H2B_CUDA_TRY(cudaMemsetAsync(p, 0, sizeof(double2) * n, st));
   if (!getenv("H2B_BICG_HOST"))  // H2B_BICG_HOST: the host-driven loop below (A/B timing)
-    return bicgstab_graph(h, b, x, r, rh, p, v, s, t, sc, bnrm, tol, max_iter,
+    return bicgstab_graph(h, g_scratch, b, x, r, rh, p, v, s, t, sc, bnrm, tol, max_iter,
                           (const double2*)restart_noise_perm, history, report, st, t0);
   cplx rho = 1.0, alpha = 1.0, omega = 1.0;
   bool converged = false, restarted = false, p_zero = true;

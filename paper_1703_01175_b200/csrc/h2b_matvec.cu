@@ -146,7 +146,31 @@ int h2b_ensure_workspace(h2b_ctx* h, int q) {
   return H2B_OK;
 }
 
+int h2b_order_begin(h2b_ctx* h, cudaStream_t st) {
+  if (!h->ev_done) H2B_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_done, cudaEventDisableTiming));
+  H2B_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_done, 0));  // never recorded yet: a no-op
+  return H2B_OK;
+}
+
+int h2b_order_end(h2b_ctx* h, cudaStream_t st) {
+  H2B_CUDA_TRY(cudaEventRecord(h->ev_done, st));
+  return H2B_OK;
+}
+
+namespace {
+int run_matvec(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st);
+}
+
+// one matvec on `st`, ordered after the handle's previous work on any stream (the graphs of one
+// handle share its x̂/ŷ workspace and control flags, so two matvecs must not overlap on the device)
 int h2b_run_matvec(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st) {
+  H2B_TRY(h2b_order_begin(h, st));
+  H2B_TRY(run_matvec(h, xp, yp, q, st));
+  return h2b_order_end(h, st);
+}
+
+namespace {
+int run_matvec(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st) {
   H2B_TRY(h2b_prepare(h));
   H2B_TRY(h2b_ensure_workspace(h, q));
   if (q >= 2 && h->use_mrhs) H2B_TRY(h2b_mrhs_workspace(h, q));  // allocates: never inside a capture
@@ -188,6 +212,7 @@ int h2b_run_matvec(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream
   H2B_CUDA_TRY(cudaGraphLaunch(it->second, st));
   return H2B_OK;
 }
+}  // namespace
 
 // phase 0: near-field only (y overwritten); phase 1: far field only (y accumulated);
 // both serialised on `st` so they can be timed one by one.

@@ -96,6 +96,8 @@ int h2b_assemble_near(h2b_handle h, const double* centers, const double* chi, do
                   std::to_string(first >> 20) + " (kernel singular; reference raises CoincidentCentersError)");
     return H2B_EINVAL;
   }
+  h->sec_iv[H2B_SEC_D].clear();
+  h->sec_iv[H2B_SEC_D].emplace(0, h->sec_elems[H2B_SEC_D]);
   h->sec_uploaded[H2B_SEC_D] = h->sec_elems[H2B_SEC_D];
   return H2B_OK;
 }

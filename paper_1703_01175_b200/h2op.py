@@ -52,13 +52,13 @@ class H2Operator:
     return numpy arrays in the original order (the drop-in surface).
     """
 
-    def __init__(self, h2, device=0):
+    def __init__(self, h2, device=0, _upload=True):
         pk = h2 if isinstance(h2, PackedH2) else pack_h2(h2)
         L = _abi.lib()
         if not L.h2b_device_ok(int(device)):
             raise RuntimeError("no sm_100 (B200) CUDA device visible; the H2 hot path has no CPU "
                                "fallback")
-        self.packed = pk
+        self.perm = np.asarray(pk.perm)  # not the PackedH2 itself: the cache must not keep it alive
         self.n = pk.n
         self.device = int(device)
         keep = {}
@@ -107,6 +107,10 @@ class H2Operator:
         if far_on_device:  # structure-exact operator: seeded V/T/S generated in HBM
             from .synthetic import fill_far_field_on_device
             fill_far_field_on_device(L, handle, pk, self.device, pk.meta["synthetic"].get("seed", 0))
+        self._lock = threading.Lock()
+        self._perm_t = None
+        if not _upload:  # tests of the C-ABI's upload bookkeeping upload the payloads themselves
+            return
         for sec, buf in ((_abi.SEC_V, pk.vbuf), (_abi.SEC_T, pk.tbuf), (_abi.SEC_S, pk.sbuf),
                          (_abi.SEC_D, pk.dbuf)):
             b = np.ascontiguousarray(buf, dtype=np.complex128).view(np.uint8)
@@ -114,7 +118,9 @@ class H2Operator:
                 chunk = b[off:off + _UPLOAD_CHUNK]
                 _abi.check(L.h2b_upload(handle, sec, chunk.ctypes.data, chunk.size, off),
                            "h2b_upload")
-        self._lock = threading.Lock()  # the handle's workspace is single-stream
+        # serialises the host-side enqueue (graph cache, workspace growth); on the device the
+        # library orders every call after the handle's previous one, whatever the stream
+        self._lock = threading.Lock()
         self._perm_t = None
 
     # ------------------------------------------------------------------
@@ -135,7 +141,7 @@ class H2Operator:
     def perm_tensor(self):
         torch = _torch()
         if self._perm_t is None:
-            self._perm_t = torch.from_numpy(self.packed.perm).to(f"cuda:{self.device}")
+            self._perm_t = torch.from_numpy(self.perm).to(f"cuda:{self.device}")
         return self._perm_t
 
     # ---- device-side (permuted order) --------------------------------
