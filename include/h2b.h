@@ -131,6 +131,9 @@ int h2b_prepare_handle(h2b_handle h);
 #define H2B_OPT_TRACE 3       /* 1: record a per-task timeline of the persistent kernel */
 #define H2B_OPT_DEBUG 4       /* profiling only, results are WRONG: bit 0 skips far-field task
                                  bodies, bit 1 near-field task bodies of the persistent kernel */
+#define H2B_OPT_TREE 6        /* 1 (default): the q=1 far field of a complete binary tree runs as
+                                 subtree programs (one CTA per subtree, payload staged once);
+                                 0: the task-graph kernel.  Set before the first matvec. */
 #define H2B_OPT_MRHS 5        /* 1 (default): q >= 2 runs every phase as a grouped complex GEMM on
                                  the FP64 tensor pipe (DMMA); 0: per-phase CUDA-core kernels */
 int h2b_set_option(h2b_handle h, int option, int value);
@@ -140,6 +143,10 @@ int h2b_set_option(h2b_handle h, int option, int value);
  * t_staged, t_level0, t_level1, t_computed (spans only; else 0), t_done
  * (ns, %globaltimer), smid | cta << 32}. */
 int h2b_get_trace(h2b_handle h, int64_t* out, int64_t max_tasks);
+/* development aid: per-program timeline of the q=1 tree far field (env H2B_TREE_TRACE at prepare):
+   out[32 i + j] = globaltimer stamp j of program i (SM clock64 at out[32 i + 16 + j]) (start, staged, external x̂ ready, x̂ published,
+   coupling inputs ready, before / after the parent wait, down pass done, end). */
+int h2b_tree_trace(h2b_handle h, int64_t* out, int64_t max_progs);
 
 #define H2B_Q_LAUNCHES_Q1 1   /* kernels per single-RHS matvec */
 #define H2B_Q_SPAN_MODE 2     /* 1 if the q=1 far field uses staged subtree spans */
@@ -157,6 +164,7 @@ int h2b_get_trace(h2b_handle h, int64_t* out, int64_t max_tasks);
 #define H2B_Q_MEGA_SMEM 14    /* dynamic shared memory of the far-field task-graph kernel (bytes) */
 #define H2B_Q_NEAR_VARIANT 15 /* 100 * leaf size + rows per thread of the near kernel (0: generic) */
 #define H2B_Q_MRHS_LAUNCHES 16 /* kernel launches of one multi-RHS (q >= 2) matvec */
+#define H2B_Q_TREE 17         /* q=1 far field as subtree programs: programs | split level << 16 | top level << 24 (0: off) */
 int h2b_query(h2b_handle h, int what, int64_t* out);
 
 /* Permutation helpers on device buffers: out[i,:] = in[perm[i],:] (gather,

@@ -26,13 +26,13 @@ EXPORTED = (
     "h2b_plan_bcast_rows", "h2b_ipc_get_handle", "h2b_ipc_open", "h2b_ipc_close",
     "h2b_plan_set_peer_offset", "h2b_device_alloc", "h2b_device_free", "h2b_plan_set_gather",
     "h2b_plan_set_near_fast", "h2b_plan_set_couple_fast", "h2b_fill_synthetic_raw",
-    "h2b_plan_fill_synthetic", "h2b_plan_fill_near",
+    "h2b_plan_fill_synthetic", "h2b_plan_fill_near", "h2b_tree_trace",
 )
-OPT_GRAPHS, OPT_MEGA, OPT_TRACE, OPT_DEBUG, OPT_MRHS = 1, 2, 3, 4, 5
+OPT_GRAPHS, OPT_MEGA, OPT_TRACE, OPT_DEBUG, OPT_MRHS, OPT_TREE = 1, 2, 3, 4, 5, 6
 Q_LAUNCHES_Q1, Q_SPAN_MODE, Q_SPLIT_LEVEL, Q_TOP_STAGED, Q_DEVICE_BYTES = 1, 2, 3, 4, 5
 Q_MEGA, Q_MEGA_TASKS, Q_MEGA_GRID, Q_MEGA_TIERS, Q_DEVICE_ERROR = 6, 7, 8, 9, 10
 Q_NEAR_TASKS, Q_NEAR_STAGES, Q_NEAR_SMEM, Q_MEGA_SMEM, Q_NEAR_VARIANT = 11, 12, 13, 14, 15
-Q_MRHS_LAUNCHES = 16
+Q_MRHS_LAUNCHES, Q_TREE = 16, 17
 
 _i32p = C.POINTER(C.c_int32)
 _i64p = C.POINTER(C.c_int64)

@@ -31,8 +31,15 @@ int upload_table(T** dst, const T* src, int64_t count, int64_t* acc) {
   return H2B_OK;
 }
 
+}  // namespace
+void h2b_tree_free(TreeDev* d);
+int h2b_tree_error(const TreeDev* d, uint32_t* err);
+namespace {
+
 void free_ctx(h2b_ctx* h) {
   h2b_release_graphs(h);
+  h2b_tree_free(h->tree);
+  h->tree = nullptr;
   h2b_mrhs_free(h);
   void* ptrs[] = {h->c_start_d, h->c_size_d, h->c_rank_d, h->c_lo,      h->c_hi,
                   h->c_parent,  h->c_xoff_d, h->c_voff_d, h->c_toff_d,  h->s_row_ptr_d,
@@ -392,6 +399,11 @@ int h2b_set_option(h2b_handle h, int option, int value) {
     h2b_release_graphs(h);
     return H2B_OK;
   }
+  if (option == H2B_OPT_TREE) {
+    REQUIRE(!h->prepared, H2B_ESTATE, "h2b_set_option(H2B_OPT_TREE): set before the first matvec");
+    h->use_tree = value ? 1 : 0;
+    return H2B_OK;
+  }
   if (option == H2B_OPT_MEGA) {
     REQUIRE(!h->prepared, H2B_ESTATE, "h2b_set_option(H2B_OPT_MEGA): set before the first matvec");
     h->use_mega = value ? 1 : 0;
@@ -422,9 +434,12 @@ int h2b_query(h2b_handle h, int what, int64_t* out) {
     case H2B_Q_DEVICE_ERROR: {
       MegaCtrl c{};
       if (h->ctrl) H2B_CUDA_TRY(cudaMemcpy(&c, h->ctrl, sizeof(c), cudaMemcpyDeviceToHost));
-      *out = c.error;
+      uint32_t te = 0;
+      if (h->tree) H2B_TRY(h2b_tree_error(h->tree, &te));
+      *out = c.error | te;
       return H2B_OK;
     }
+    case H2B_Q_TREE: *out = h->tree ? (int64_t)h->tree_progs | ((int64_t)h->tree_ls << 16) | ((int64_t)h->tree_lt << 24) : 0; return H2B_OK;
     default: break;
   }
   h2b_set_error("h2b_query: unknown key");

@@ -205,6 +205,7 @@ struct GraphKey {
 };
 
 struct MrhsPlan;  // h2b_mrhs.cu
+struct TreeDev;   // h2b_tree.cu
 
 struct GmresKey {  // one captured Arnoldi step of h2b_gmres
   const void* V;
@@ -286,6 +287,10 @@ struct h2b_ctx {
   int2* near_idx = nullptr;            // per near task {first slot, slots}
   int n_near_tasks = 0, near_rec_max = 0, near_nst = 0, near_smem = 0, near_grid = 0;
   uint32_t near_delay_ns = 0;  // tuning aid (H2B_DEBUG_NEAR_DELAY_NS)
+  // far field as subtree programs (h2b_tree.cu): replaces k_mega beside k_near_stream when set
+  TreeDev* tree = nullptr;
+  int use_tree = 1;  // H2B_OPT_TREE
+  int tree_ls = 0, tree_lt = 0, tree_progs = 0, tree_smem = 0;
   // flattened bottom tier (0 = off): W buffer and the deep spans' y_deep
   int mega_flat = 0;
   double2* wbuf = nullptr;

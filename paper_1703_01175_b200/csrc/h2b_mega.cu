@@ -637,12 +637,19 @@ int h2b_near_stream_set_smem(int ns, int r, int bytes) {
   return H2B_OK;
 }
 
-// y = 0; then k_near_stream on st and k_mega on h->far_stream, concurrently (fork / join)
+int h2b_launch_tree(h2b_ctx* h, const TreeDev* d, const double2* xp, double2* yp, cudaStream_t st);
+
+// y = 0; then k_near_stream on st and k_mega (or the tree programs) on h->far_stream,
+// concurrently (fork / join)
 int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st) {
   if (!(h->mega_debug & 8)) H2B_CUDA_TRY(cudaMemsetAsync(yp, 0, sizeof(double2) * h->n, st));
   const bool run_far = h->mega_grid > 0 && !(h->mega_debug & 2);
   const bool run_near = h->n_near_tasks > 0 && !(h->mega_debug & 4);
-  if (run_far) {
+  if (run_far && h->tree) {  // subtree programs (h2b_tree.cu) in k_mega's place
+    H2B_CUDA_TRY(cudaEventRecord(h->ev_fork, st));
+    H2B_CUDA_TRY(cudaStreamWaitEvent(h->far_stream, h->ev_fork, 0));
+    H2B_TRY(h2b_launch_tree(h, h->tree, xp, yp, h->far_stream));
+  } else if (run_far) {
     H2B_CUDA_TRY(cudaEventRecord(h->ev_fork, st));
     H2B_CUDA_TRY(cudaStreamWaitEvent(h->far_stream, h->ev_fork, 0));
     MegaArgs A;

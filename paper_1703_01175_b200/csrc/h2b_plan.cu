@@ -21,6 +21,9 @@ int h2b_mega_static_smem();
 int h2b_near_stream_static_smem(int ns, int r, int* bytes);
 int h2b_near_stream_set_smem(int ns, int r, int bytes);
 int h2b_near_rows_per_item(int ns, int r);
+int h2b_tree_prepare(h2b_ctx* h, int max_ctas, int budget_bytes, int64_t* bytes, int* planned);
+int h2b_tree_static_smem();
+constexpr int TREE_BUDGET = 168 * 1024;  // shared memory of one subtree program (bytes)
 
 namespace {
 
@@ -1323,6 +1326,20 @@ int h2b_prepare(h2b_ctx* h) {
       if (const char* e = getenv("H2B_NEAR_GRID")) h->near_grid = std::max(1, std::min(sms, atoi(e)));  // tuning aid
       h->mega = (per_sm > 0 && h->mega_grid <= per_sm * sms) ? 1 : 0;
       h->mega_est_us = mp.est_makespan;
+      // far field as subtree programs (h2b_tree.cu) when the tree qualifies: it takes k_mega's
+      // place beside the near-field stream, whose ring gets the shared memory left over
+      int planned = 0;
+      int64_t tb = 0;
+      if (h->mega && h->use_tree) H2B_TRY(h2b_tree_prepare(h, sms, TREE_BUDGET, &tb, &planned));
+      if (planned) {
+        acc += tb;
+        const int tree_total = h->tree_smem + h2b_tree_static_smem() + 1024;
+        int tnst = stg > 0 ? std::min(8, (sm_total - tree_total - near_static - rec_bytes) / stg) : 0;
+        if (const char* e = getenv("H2B_DEBUG_NEAR_NST")) tnst = std::min(tnst, std::max(2, atoi(e)));
+        if (mp.ns > 0 && tnst < 2) tnst = 2;
+        h->near_nst = tnst;
+        h->near_smem = tnst * stg + rec_bytes;
+      }
     }
   }
   if (h->mega) {  // the multi-kernel programs below are still planned for phase timing

@@ -1,0 +1,835 @@
+// Far field of the single-RHS H² matvec as ONE persistent launch of subtree programs (sm_100a).
+//
+// Restates the far-field part of the reference `_apply_perm` (/root/reference/pkg/src/h2vie/
+// arith.py:58-99): x̂ = Vᵀx at the leaves, x̂_t = T_loᵀx̂_lo + T_hiᵀx̂_hi upward, ŷ_t = Σ S^{t,s}x̂_s
+// over the admissible pairs, ŷ_child += T_child ŷ_t downward and y += V ŷ at the leaves.
+//
+// For complete binary cluster trees (every leaf on the deepest level, leaves of one size, the
+// packed children of ordinal i at ordinals 2i and 2i+1 of the next level; all BASELINE configs)
+// the tree is cut at a split level ls into
+//   * bottom programs: one per level-ls cluster, its whole subtree down to the leaves, and
+//   * top programs:    one per cluster of the topmost level lt with any non-zero rank, its
+//                      subtree down to level ls-1 (the level-ls clusters are its external
+//                      children, computed by the bottom programs).
+// Each program is ONE CTA for the whole launch.  It stages its operator payload (x, V, T and the
+// transposed coupling panels Sᵀ of its targets, plus its node table and gather list) with TMA
+// bulk copies once at launch and keeps it in shared memory: V and T serve both the upward and
+// the downward pass, so every payload element is read from HBM exactly once per matvec (the
+// minimal-traffic B_alg convention of SURVEY.md §8d).  The critical path is three inter-CTA
+// hand-offs (epoch-stamped flags in global memory):
+//   bottom up  -> [flag up] -> top up, top couplings (after the other top programs' flags),
+//   top down -> [flag down] -> bottom down; bottom couplings wait only for the neighbouring
+//   bottom programs' x̂ and run while the top works.
+// The near field runs concurrently in k_near_stream (h2b_mega.cu); both add into a zeroed y.
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <set>
+#include <vector>
+
+#include "h2b_panel.cuh"
+
+namespace {
+
+constexpr int TNT = 256;  // threads per program CTA
+constexpr int TREE_MAXLEV = 24;
+
+// node of a program (64 bytes, staged into shared memory; offsets in double2 elements).  Every
+// operand offset is precomputed on the host so that a level step is one record load per node.
+struct TNode {
+  int32_t k, kind;    // rank; kind: 0 leaf, 1 internal, 2 external child (x̂ / ŷ via global)
+  int32_t xh;         // x̂ of the node in smem (ŷ at xh + yoff)
+  int32_t pay;        // V (leaf, n x k) or T ((k_lo + k_hi) x k, rows lo then hi)
+  int32_t R;          // rows of pay (leaf: points n; internal: k_lo + k_hi)
+  int32_t in;         // up: input of the rows (leaf: x segment; internal: [x̂_lo; x̂_hi])
+  int32_t sh;         // log2 of k rounded up to a power of two
+  int32_t s_pay;      // coupling panel Sᵀ (s_rows x k): global element offset in sbuf (high half in pad)
+  int32_t s_rows;     // 0: no couplings
+  int32_t xg;         // first gathered x̂ row of the panel (x̂g area / gather index list)
+  int32_t gx_lo, gx_hi;  // global x̂ / ŷ offset of the node
+  int32_t gy_lo, gy_hi;  // leaf: global y offset; internal with external children: their global ŷ
+  int32_t ext, pad;      // internal: 1 if the children are external; pad: s_pay >> 32
+};
+static_assert(sizeof(TNode) == 64, "TNode layout");
+
+struct TCopy {  // global -> smem bulk copy
+  int64_t src;  // element offset in the source buffer
+  int32_t kind, elems, smem, pad;
+};
+enum TSrc : int32_t { TS_X = 0, TS_V, TS_T, TS_S, TS_NODES, TS_GIDX, TS_N };
+
+struct TProg {
+  int32_t n_nodes, nlev, n_copy, copy_first;
+  int32_t stage_bytes, smem_elems, yoff, xg_smem;
+  int32_t n_xg, gidx_smem, n_wait_up, wait_up_first;
+  int32_t wait_down, n_ext_wait, ext_wait_first, bottom;
+  int32_t lev_first[TREE_MAXLEV + 1];
+  int32_t pad[3];
+};
+
+struct TreeArgs {
+  const TProg* progs;
+  const TCopy* copies;
+  const int32_t* waits;  // program ids
+  const void* src[TS_N];
+  double2* xhat;
+  double2* yhat;
+  double2* y;
+  uint32_t* flags_up;
+  uint32_t* flags_down;
+  MegaCtrl* ctrl;
+  uint64_t* trace;  // optional (H2B_TREE_TRACE): 16 timestamps per program
+  int trace_levels;  // H2B_TREE_TRACE=2: also one stamp per level of the upward pass
+};
+
+__device__ __forceinline__ void tmark(const TreeArgs& A, int i) {
+  if (A.trace && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    A.trace[32 * blockIdx.x + i] = t;
+    A.trace[32 * blockIdx.x + 16 + i] = clock64();
+  }
+}
+
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_rel(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// warp 0 waits until flags[ids[i]] == want for every i: the ids are loaded once (up to four per
+// lane in registers), then relaxed sweeps, then one acquire fence; the caller follows with
+// __syncthreads
+__device__ __forceinline__ void wait_flags(const uint32_t* flags, const int32_t* ids, int n, uint32_t want,
+                                           MegaCtrl* ctrl) {
+  if (threadIdx.x >= 32 || n == 0) return;
+  const int lane = threadIdx.x;
+  int f[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) f[u] = lane + 32 * u < n ? ids[lane + 32 * u] : -1;
+  for (long spins = 0;; ++spins) {
+    bool ok = true;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) ok &= f[u] < 0 || ld_relaxed(flags + f[u]) == want;
+    for (int i = lane + 128; i < n; i += 32) ok &= ld_relaxed(flags + ids[i]) == want;
+    if (__all_sync(0xffffffffu, ok)) break;
+    if (spins > (1l << 24)) {  // never expected: report instead of hanging the GPU
+      atomicExch(&ctrl->error, 2u);
+      break;
+    }
+    __nanosleep(20);
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
+// out[c] = Σ_r P[r*w + c] in[r] for c < w (one warp).  Lane (g, c): column c of row group g,
+// rows g, g + G, ... ; every chunk issues its loads before its FMAs (the ops are small: latency,
+// not throughput, decides), then the G partial sums meet through xor shuffles.
+__device__ __forceinline__ double2 colsum_sum(const double2* P, int R, int w, int sh, const double2* in) {
+  const int lane = threadIdx.x & 31;
+  const int wp = 1 << sh, G = 32 >> sh;
+  const int g = lane >> sh, c = lane & (wp - 1);
+  double2 a = make_double2(0.0, 0.0), b = a;
+  if (w <= 32) {
+    for (int r0 = g; r0 < R; r0 += 4 * G) {
+      double2 pv[4], xv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = r0 + i * G;
+        const bool ok = c < w && r < R;
+        pv[i] = ok ? P[r * w + c] : make_double2(0.0, 0.0);
+        xv[i] = ok ? in[r] : make_double2(0.0, 0.0);
+      }
+      cfma(a, pv[0], xv[0]);
+      cfma(b, pv[1], xv[1]);
+      cfma(a, pv[2], xv[2]);
+      cfma(b, pv[3], xv[3]);
+    }
+    a = cadd(a, b);
+    for (int m = wp; m < 32; m <<= 1) a = cadd(a, shfl_xor2(a, m));
+  }
+  return a;
+}
+
+__device__ __forceinline__ void colsum(const double2* P, int R, int w, int sh, const double2* in, double2* out) {
+  const int lane = threadIdx.x & 31;
+  if (w <= 32) {
+    const double2 s = colsum_sum(P, R, w, sh, in);
+    if (lane < w) out[lane] = s;
+  } else {
+    for (int c = lane; c < w; c += 32) {
+      double2 a0 = make_double2(0.0, 0.0), a1 = a0;
+      int r = 0;
+      for (; r + 1 < R; r += 2) {
+        cfma(a0, P[r * w + c], in[r]);
+        cfma(a1, P[(r + 1) * w + c], in[r + 1]);
+      }
+      if (r < R) cfma(a0, P[r * w + c], in[r]);
+      out[c] = cadd(a0, a1);
+    }
+  }
+}
+
+// Σ_j P[r*w + j] v[j] for one row r (a lane's dot product), loads before FMAs in chunks of 4
+__device__ __forceinline__ double2 rowdot(const double2* P, int r, int w, const double2* v) {
+  double2 a = make_double2(0.0, 0.0), b = a;
+  const double2* p = P + r * w;
+  for (int j0 = 0; j0 < w; j0 += 4) {
+    double2 pv[4], vv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool ok = j0 + i < w;
+      pv[i] = ok ? p[j0 + i] : make_double2(0.0, 0.0);
+      vv[i] = ok ? v[j0 + i] : make_double2(0.0, 0.0);
+    }
+    cfma(a, pv[0], vv[0]);
+    cfma(b, pv[1], vv[1]);
+    cfma(a, pv[2], vv[2]);
+    cfma(b, pv[3], vv[3]);
+  }
+  return cadd(a, b);
+}
+
+__global__ void __launch_bounds__(TNT, 1) k_far_tree(TreeArgs A) {
+  extern __shared__ __align__(16) double2 sm[];
+  __shared__ __align__(8) uint64_t bar[2];  // [0]: nodes, gather list, x, V, T  [1]: staged S panels
+  __shared__ uint32_t s_epoch;
+  __shared__ TProg P;  // the program header (global loads would recur after every fence)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int NW = TNT / 32;
+  tmark(A, 0);
+  const TProg* gP = A.progs + blockIdx.x;
+  if (tid == 0) {
+    s_epoch = *(volatile uint32_t*)&A.ctrl->epoch;
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+  }
+  for (int i = tid; i < (int)(sizeof(TProg) / 4); i += TNT)
+    reinterpret_cast<int32_t*>(&P)[i] = reinterpret_cast<const int32_t*>(gP)[i];
+  // this thread's bulk copies (up-pass operands complete on bar[0], coupling panels on bar[1])
+  const int n_copy = gP->n_copy, c0 = gP->copy_first;
+  TCopy cp0 = tid < n_copy ? A.copies[c0 + tid] : TCopy{};
+  __syncthreads();
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&bar[0], (uint32_t)P.stage_bytes);
+    mbar_arrive_expect_tx(&bar[1], (uint32_t)P.pad[0]);  // staged coupling panels (0: from L2)
+  }
+  for (int i = tid; i < n_copy; i += TNT) {
+    const TCopy c = i == tid ? cp0 : A.copies[c0 + i];
+    if (c.kind == TS_S && c.smem < 0) {  // coupling panels read from L2 by the couplings: warm them
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const double2*)A.src[TS_S] + c.src),
+                   "r"(16u * (uint32_t)c.elems) : "memory");
+      continue;
+    }
+    const void* base = c.kind == TS_X ? A.src[TS_X] : c.kind == TS_V ? A.src[TS_V] : c.kind == TS_T ? A.src[TS_T]
+                     : c.kind == TS_S ? A.src[TS_S] : c.kind == TS_NODES ? A.src[TS_NODES] : A.src[TS_GIDX];
+    bulk_g2s(sm + c.smem, (const double2*)base + c.src, 16u * (uint32_t)c.elems, &bar[c.kind == TS_S ? 1 : 0]);
+  }
+  const uint32_t want = s_epoch + 1;
+  mbar_wait(&bar[0], 0);
+  tmark(A, 1);
+  const TNode* nodes = reinterpret_cast<const TNode*>(sm);
+  const int32_t* gidx = reinterpret_cast<const int32_t*>(sm + P.gidx_smem);
+  const int yoff = P.yoff;
+  const int nlev = P.nlev;
+  // ---- top programs: the external children's x̂ (bottom programs' roots) ----
+  if (P.n_ext_wait) {
+    wait_flags(A.flags_up, A.waits + P.ext_wait_first, P.n_ext_wait, want, A.ctrl);
+    __syncthreads();
+    tmark(A, 2);
+    const int e0 = P.lev_first[nlev - 1], e1 = P.lev_first[nlev];
+    for (int i = e0 + warp; i < e1; i += NW) {
+      const TNode nd = nodes[i];
+      const int64_t gx = (int64_t)(uint32_t)nd.gx_lo | ((int64_t)nd.gx_hi << 32);
+      for (int j = lane; j < nd.k; j += 32) sm[nd.xh + j] = __ldcg(A.xhat + gx + j);
+    }
+    __syncthreads();
+  }
+  // ---- upward pass, deepest level first ----
+  for (int lv = nlev - 1; lv >= 0; --lv) {
+    const int a = P.lev_first[lv], b = P.lev_first[lv + 1];
+    for (int i = a + warp; i < b; i += NW) {
+      const TNode nd = nodes[i];
+      if (nd.kind != 2 && nd.k > 0) colsum(sm + nd.pay, nd.R, nd.k, nd.sh, sm + nd.in, sm + nd.xh);
+    }
+    __syncthreads();
+    if (lv >= nlev - 6 && (A.trace_levels)) tmark(A, 9 + (nlev - 1 - lv));
+  }
+  // ---- publish x̂ of the program's own nodes ----
+  {
+    const int e = P.bottom ? P.lev_first[nlev] : P.lev_first[nlev - 1];
+    for (int i = warp; i < e; i += NW) {
+      const TNode nd = nodes[i];
+      const int64_t gx = (int64_t)(uint32_t)nd.gx_lo | ((int64_t)nd.gx_hi << 32);
+      for (int j = lane; j < nd.k; j += 32) A.xhat[gx + j] = sm[nd.xh + j];
+    }
+    __syncthreads();  // the CTA's x̂ stores happen before thread 0's (cumulative) release
+    if (tid == 0) st_rel(A.flags_up + blockIdx.x, want);
+    tmark(A, 3);
+  }
+  // ---- couplings: gather x̂ of the sources (own smem or other programs' published x̂) ----
+  wait_flags(A.flags_up, A.waits + P.wait_up_first, P.n_wait_up, want, A.ctrl);
+  if (P.pad[0]) mbar_wait(&bar[1], 0);
+  __syncthreads();
+  tmark(A, 4);
+  double2* xg = sm + P.xg_smem;
+  for (int i = tid; i < P.n_xg; i += TNT) {
+    const int g = gidx[i];
+    xg[i] = g >= 0 ? __ldcg(A.xhat + g) : sm[~g];
+  }
+  __syncthreads();
+  {
+    const int e = P.bottom ? P.lev_first[nlev] : P.lev_first[nlev - 1];
+    for (int i = warp; i < e; i += NW) {
+      const TNode nd = nodes[i];
+      if (nd.k == 0) continue;
+      if (nd.s_rows > 0) {
+        const int64_t so = (int64_t)(uint32_t)nd.s_pay | ((int64_t)nd.pad << 32);
+        const double2* sp = P.pad[0] ? sm + so : (const double2*)A.src[TS_S] + so;  // staged or L2
+        colsum(sp, nd.s_rows, nd.k, nd.sh, xg + nd.xg, sm + nd.xh + yoff);
+      } else {
+        for (int j = lane; j < nd.k; j += 32) sm[nd.xh + yoff + j] = make_double2(0.0, 0.0);
+      }
+    }
+  }
+  // ---- the root's contribution from the program above (bottom programs under a top) ----
+  if (P.wait_down >= 0) {
+    const int32_t wd = P.wait_down;
+    tmark(A, 5);
+    wait_flags(A.flags_down, &wd, 1, want, A.ctrl);
+    __syncthreads();  // also orders the coupling writes above
+    tmark(A, 6);
+    if (warp == 0) {
+      const TNode nd = nodes[0];
+      const int64_t gx = (int64_t)(uint32_t)nd.gx_lo | ((int64_t)nd.gx_hi << 32);
+      for (int j = lane; j < nd.k; j += 32) {
+        const double2 v = __ldcg(A.yhat + gx + j);
+        double2& o = sm[nd.xh + yoff + j];
+        o = cadd(o, v);
+      }
+    }
+  }
+  __syncthreads();
+  // ---- downward pass, root level first: children ŷ += T ŷ_parent; leaves: y += V ŷ ----
+  for (int lv = 0; lv < nlev; ++lv) {
+    const int a = P.lev_first[lv], b = P.lev_first[lv + 1];
+    for (int i = a + warp; i < b; i += NW) {
+      const TNode nd = nodes[i];
+      if (nd.k == 0 || nd.kind == 2) continue;
+      const double2* yp = sm + nd.xh + yoff;
+      const int64_t g = (int64_t)(uint32_t)nd.gy_lo | ((int64_t)nd.gy_hi << 32);
+      for (int r = lane; r < nd.R; r += 32) {
+        const double2 v = rowdot(sm + nd.pay, r, nd.k, yp);
+        if (nd.kind == 0) {  // leaf back-transform into y (k_near_stream adds concurrently)
+          atomicAdd(&A.y[g + r].x, v.x);
+          atomicAdd(&A.y[g + r].y, v.y);
+        } else if (nd.ext) {  // external children: their parent contribution to global ŷ
+          A.yhat[g + r] = v;
+        } else {  // [ŷ_lo; ŷ_hi] are adjacent, right behind [x̂_lo; x̂_hi]
+          double2& o = sm[nd.in + yoff + r];
+          o = cadd(o, v);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  tmark(A, 7);
+  if (!P.bottom) {  // hand the external children's ŷ to the bottom programs (cumulative release)
+    if (tid == 0) st_rel(A.flags_down + blockIdx.x, want);
+  }
+  tmark(A, 8);
+  if (tid == 0) {
+    if (atomicAdd(&A.ctrl->exited, 1u) == gridDim.x - 1) {  // last CTA out advances the epoch
+      A.ctrl->exited = 0;
+      __threadfence();
+      A.ctrl->epoch = want;
+    }
+  }
+}
+
+}  // namespace
+
+// ===========================================================================
+// host: the plan
+// ===========================================================================
+struct TreePlan {
+  std::vector<TProg> progs;
+  std::vector<TCopy> copies;
+  std::vector<int32_t> waits;
+  std::vector<TNode> nodes_all;   // staged from a device copy (TS_NODES)
+  std::vector<int32_t> gidx_all;  // staged from a device copy (TS_GIDX), 4 per 16-byte element
+  int smem_max = 0;               // bytes
+  int ls = 0, lt = 0, n_bottom = 0, n_top = 0;
+};
+
+namespace {
+
+int level_of_p(const h2b_ctx* h, int p) {
+  int l = 0;
+  while (l + 1 <= h->depth && h->level_ptr[l + 1] <= p) ++l;
+  return l;
+}
+
+// the tree qualifies when it is complete in packed order with uniform leaves on the last level
+// and only same-level couplings
+bool tree_shape_ok(const h2b_ctx* h) {
+  const int L = h->depth;
+  if (L < 2 || h->uniform_leaf <= 0) return false;
+  for (int l = 0; l < L; ++l)
+    if (h->level_ptr[l + 1] - h->level_ptr[l] != (1 << l)) return false;
+  for (int l = 0; l + 1 < L; ++l)
+    for (int p = h->level_ptr[l]; p < h->level_ptr[l + 1]; ++p) {
+      const int i = p - h->level_ptr[l];
+      if (h->c_child_lo[p] != h->level_ptr[l + 1] + 2 * i || h->c_child_hi[p] != h->level_ptr[l + 1] + 2 * i + 1)
+        return false;
+    }
+  for (int p = h->level_ptr[L - 1]; p < h->P; ++p)
+    if (h->c_child_lo[p] >= 0 || h->c_size[p] != h->uniform_leaf) return false;
+  for (int l = 0; l < L; ++l)
+    for (int t = h->level_ptr[l]; t < h->level_ptr[l + 1]; ++t)
+      for (int64_t b = h->s_row_ptr[t]; b < h->s_row_ptr[t + 1]; ++b) {
+        const int s = h->s_col[b];
+        if (s < h->level_ptr[l] || s >= h->level_ptr[l + 1]) return false;
+      }
+  return true;
+}
+
+struct Builder {
+  const h2b_ctx* h;
+  TreePlan& tp;
+  // one program: the subtree of cluster `root` over levels [root level, last] (last inclusive);
+  // ext: the level below `last` is external (x̂ from / ŷ to global)
+  bool build(int root, int last, bool bottom, int budget_elems) {
+    const int L = h->depth;
+    const int rl = level_of_p(h, root);
+    TProg P{};
+    P.bottom = bottom ? 1 : 0;
+    P.wait_down = -1;
+    // nodes by level (packed order inside a level)
+    std::vector<int> nd_p;
+    std::vector<int> lev_first;
+    const int nl = last - rl + 1 + (bottom ? 0 : 1);
+    if (nl > TREE_MAXLEV) return false;
+    const int i0 = root - h->level_ptr[rl];
+    for (int d = 0; d < nl; ++d) {
+      lev_first.push_back((int)nd_p.size());
+      const int l = rl + d;
+      const int a = h->level_ptr[l] + (i0 << d), cnt = 1 << d;
+      for (int p = a; p < a + cnt; ++p) nd_p.push_back(p);
+    }
+    lev_first.push_back((int)nd_p.size());
+    (void)L;
+    const int nn = (int)nd_p.size();
+    std::map<int, int> idx_of;
+    for (int i = 0; i < nn; ++i) idx_of[nd_p[i]] = i;
+    // smem layout (double2 elements): nodes | gather idx | x | V | T | S | x̂ | ŷ | x̂g
+    int off = 4 * nn;  // 64-byte nodes
+    std::vector<TNode> nodes(nn);
+    std::vector<int32_t> gl;  // gather list (global x̂ index, or ~smem offset for own nodes)
+    // coupling rows first (their count sizes the gather list)
+    std::vector<int> xh_of(nn, 0);
+    int xh_total = 0;
+    for (int i = 0; i < nn; ++i) {
+      xh_of[i] = xh_total;
+      xh_total += h->c_rank[nd_p[i]];
+    }
+    const int own_end = bottom ? nn : lev_first[nl - 1];  // nodes the program computes
+    int n_rows = 0;
+    for (int i = 0; i < own_end; ++i) {
+      const int t = nd_p[i];
+      if (h->c_rank[t] == 0) continue;
+      for (int64_t b = h->s_row_ptr[t]; b < h->s_row_ptr[t + 1]; ++b) n_rows += h->c_rank[h->s_col[b]];
+    }
+    const int gidx_smem = off;
+    off += (n_rows + 3) / 4;
+    int x_smem = -1, v_smem = -1;
+    auto push_copy = [&](int kind, int64_t src, int elems, int smem) {
+      if (elems <= 0) return;
+      if (!tp.copies.empty() && (int)tp.copies.size() > P.copy_first) {
+        TCopy& c = tp.copies.back();
+        if (c.kind == kind && c.src + c.elems == src && c.smem + c.elems == smem && c.elems + elems <= 65536) {
+          c.elems += elems;
+          return;
+        }
+      }
+      tp.copies.push_back(TCopy{src, kind, elems, smem, 0});
+    };
+    P.copy_first = (int)tp.copies.size();
+    push_copy(TS_NODES, (int64_t)tp.nodes_all.size() * 4, 4 * nn, 0);
+    if (bottom) {  // x of the subtree's points
+      x_smem = off;
+      push_copy(TS_X, h->c_start[root], h->c_size[root], off);
+      off += h->c_size[root];
+      v_smem = off;
+    }
+    // payloads
+    std::vector<int> lo_idx(nn, -1);
+    auto shpow = [](int w) { int sh = 0; while ((1 << sh) < w) ++sh; return sh; };
+    for (int i = 0; i < own_end; ++i) {
+      const int p = nd_p[i];
+      TNode& n = nodes[i];
+      n.k = h->c_rank[p];
+      n.sh = shpow(n.k);
+      const bool leaf = h->c_child_lo[p] < 0;
+      n.kind = leaf ? 0 : 1;
+      if (leaf) {
+        n.R = h->c_size[p];
+        n.in = x_smem + (int)(h->c_start[p] - h->c_start[root]);
+        n.gy_lo = (int32_t)(uint32_t)(int64_t)h->c_start[p];
+        n.gy_hi = (int32_t)((int64_t)h->c_start[p] >> 32);
+        const int e = n.R * n.k;
+        n.pay = off;
+        push_copy(TS_V, h->c_voff[p], e, off);
+        off += e;
+      } else {
+        const int lo = h->c_child_lo[p];
+        if (!idx_of.count(lo)) return false;
+        lo_idx[i] = idx_of[lo];
+        n.R = h->c_rank[lo] + h->c_rank[h->c_child_hi[p]];
+        n.ext = lo_idx[i] >= own_end ? 1 : 0;
+        if (n.ext) {  // the children's global ŷ (written by the down pass)
+          n.gy_lo = (int32_t)(uint32_t)h->c_xoff[lo];
+          n.gy_hi = (int32_t)(h->c_xoff[lo] >> 32);
+        }
+        const int e = n.R * n.k;
+        n.pay = off;
+        push_copy(TS_T, h->c_toff[p], e, off);
+        off += e;
+      }
+    }
+    for (int i = own_end; i < nn; ++i) {  // external children (top programs)
+      TNode& n = nodes[i];
+      n.k = h->c_rank[nd_p[i]];
+      n.kind = 2;
+    }
+    // coupling panels (Sᵀ, stacked per target) and the gather list.  The panels are staged in
+    // shared memory when they fit the budget (H2B_TREE_S_L2: never), else read from L2 after a
+    // prefetch at launch.
+    int64_t s_total = 0;
+    for (int i = 0; i < own_end; ++i) {
+      const int t = nd_p[i];
+      if (h->c_rank[t] == 0) continue;
+      for (int64_t b = h->s_row_ptr[t]; b < h->s_row_ptr[t + 1]; ++b)
+        s_total += (int64_t)h->c_rank[h->s_col[b]] * h->c_rank[t];
+    }
+    const bool stage_s = !getenv("H2B_TREE_S_L2") && off + s_total + 2 * xh_total + n_rows <= budget_elems;
+    int xg_rows = 0;
+    for (int i = 0; i < own_end; ++i) {
+      const int t = nd_p[i];
+      TNode& n = nodes[i];
+      n.s_rows = 0;
+      if (n.k == 0) continue;
+      const int64_t b0 = h->s_row_ptr[t], b1 = h->s_row_ptr[t + 1];
+      int rows = 0;
+      for (int64_t b = b0; b < b1; ++b) rows += h->c_rank[h->s_col[b]];
+      if (rows == 0) continue;
+      n.s_rows = rows;
+      n.xg = xg_rows;
+      const int64_t so = stage_s ? off : h->s_off[b0];  // smem offset (staged) or sbuf offset (L2)
+      n.s_pay = (int32_t)(uint32_t)so;
+      n.pad = (int32_t)(so >> 32);
+      if (stage_s) {
+        tp.copies.push_back(TCopy{h->s_off[b0], TS_S, rows * n.k, off, 0});
+        off += rows * n.k;
+      } else {  // L2 prefetch range (merged with the previous target's when contiguous)
+        TCopy pc{h->s_off[b0], TS_S, rows * n.k, -1, 0};
+        if ((int)tp.copies.size() > P.copy_first && tp.copies.back().kind == TS_S &&
+            tp.copies.back().src + tp.copies.back().elems == pc.src && tp.copies.back().elems + pc.elems <= 65536)
+          tp.copies.back().elems += pc.elems;
+        else
+          tp.copies.push_back(pc);
+      }
+      for (int64_t b = b0; b < b1; ++b) {
+        const int s = h->s_col[b];
+        auto it = idx_of.find(s);
+        const bool local = it != idx_of.end() && it->second < own_end;
+        // own source: placeholder -2 - (node << 8 | j), resolved to ~smem offset below;
+        // other program's source: the global x̂ index
+        for (int j = 0; j < h->c_rank[s]; ++j)
+          gl.push_back(local ? -2 - (int32_t)((it->second << 8) | j) : (int32_t)(h->c_xoff[s] + j));
+        xg_rows += h->c_rank[s];
+      }
+    }
+    // x̂ and ŷ areas, x̂g
+    const int xh_base = off;
+    for (int i = 0; i < nn; ++i) nodes[i].xh = xh_base + xh_of[i];
+    for (int i = 0; i < own_end; ++i)  // internal nodes read [x̂_lo; x̂_hi] (adjacent)
+      if (nodes[i].kind == 1) nodes[i].in = nodes[lo_idx[i]].xh;
+    off += xh_total;
+    P.yoff = xh_total;
+    off += xh_total;
+    P.xg_smem = off;
+    off += xg_rows;
+    P.n_xg = xg_rows;
+    for (int32_t& g : gl)
+      if (g <= -2) {
+        const int v = -2 - g;
+        g = ~(nodes[v >> 8].xh + (v & 255));
+      }
+    for (int i = 0; i < nn; ++i) {
+      const int64_t gx = h->c_xoff[nd_p[i]];
+      nodes[i].gx_lo = (int32_t)(uint32_t)gx;
+      nodes[i].gx_hi = (int32_t)(gx >> 32);
+    }
+    if (off > budget_elems) return false;
+    // gather list: staged as 16-byte elements (4 indices each)
+    P.gidx_smem = gidx_smem;
+    if (!gl.empty()) {
+      while (tp.gidx_all.size() % 4) tp.gidx_all.push_back(0);
+      const int64_t first = (int64_t)tp.gidx_all.size() / 4;
+      tp.gidx_all.insert(tp.gidx_all.end(), gl.begin(), gl.end());
+      while (tp.gidx_all.size() % 4) tp.gidx_all.push_back(0);
+      push_copy(TS_GIDX, first, (int)((gl.size() + 3) / 4), gidx_smem);
+    }
+    P.n_copy = (int)tp.copies.size() - P.copy_first;
+    int64_t bytes = 0, sbytes = 0;
+    for (int c = P.copy_first; c < (int)tp.copies.size(); ++c)
+      if (tp.copies[c].kind != TS_S || tp.copies[c].smem >= 0)
+        (tp.copies[c].kind == TS_S ? sbytes : bytes) += 16 * (int64_t)tp.copies[c].elems;
+    if (sbytes >= (1 << 20)) return false;
+    if (bytes >= (1 << 20)) return false;  // one mbarrier transaction count
+    P.stage_bytes = (int32_t)bytes;
+    P.pad[0] = (int32_t)sbytes;
+    P.smem_elems = off;
+    P.n_nodes = nn;
+    P.nlev = nl;
+    for (int d = 0; d <= nl; ++d) P.lev_first[d] = lev_first[d];
+    P.gidx_smem = gidx_smem;
+    tp.nodes_all.insert(tp.nodes_all.end(), nodes.begin(), nodes.end());
+    tp.smem_max = std::max(tp.smem_max, 16 * off);
+    tp.progs.push_back(P);
+    return true;
+  }
+};
+
+}  // namespace
+
+// Plan the tree far field for handle h (q = 1).  Returns false when the tree does not qualify or
+// the programs do not fit (the caller keeps the task-graph kernel).
+bool h2b_plan_tree(const h2b_ctx* h, int max_ctas, int budget_bytes, TreePlan& tp) {
+  if (getenv("H2B_NO_TREE") || h->K == 0 || !tree_shape_ok(h)) return false;
+  const int L = h->depth;
+  int lt = -1;
+  for (int l = 0; l < L && lt < 0; ++l)
+    for (int p = h->level_ptr[l]; p < h->level_ptr[l + 1]; ++p)
+      if (h->c_rank[p] > 0) {
+        lt = l;
+        break;
+      }
+  if (lt < 0) return false;
+  const int budget = budget_bytes / 16;
+  for (int ls = L - 1; ls >= lt; --ls) {  // the deepest split whose programs fit the grid
+    const int nb = 1 << ls, nt = ls > lt ? (1 << lt) : 0;
+    if (nb + nt > max_ctas) continue;
+    TreePlan cand;
+    Builder B{h, cand};
+    bool ok = true;
+    for (int i = 0; i < nb && ok; ++i) ok = B.build(h->level_ptr[ls] + i, L - 1, true, budget);
+    for (int i = 0; i < nt && ok; ++i) ok = B.build(h->level_ptr[lt] + i, ls - 1, false, budget);
+    if (!ok) continue;
+    // dependencies: program of each cluster (bottom: level >= ls; top: lt <= level < ls)
+    std::vector<int> prog_of(h->P, -1);
+    for (int i = 0; i < nb; ++i) {
+      const int r = h->level_ptr[ls] + i;
+      for (int d = 0; ls + d < L; ++d)
+        for (int j = 0; j < (1 << d); ++j) prog_of[h->level_ptr[ls + d] + (i << d) + j] = i;
+    }
+    for (int i = 0; i < nt; ++i)
+      for (int d = 0; lt + d < ls; ++d)
+        for (int j = 0; j < (1 << d); ++j) prog_of[h->level_ptr[lt + d] + (i << d) + j] = nb + i;
+    for (int pi = 0; pi < nb + nt; ++pi) {
+      TProg& P = cand.progs[pi];
+      const bool bottom = pi < nb;
+      const int root = bottom ? h->level_ptr[ls] + pi : h->level_ptr[lt] + (pi - nb);
+      const int rl = bottom ? ls : lt;
+      const int last = bottom ? L - 1 : ls - 1;
+      std::set<int> up;
+      for (int d = 0; rl + d <= last; ++d)
+        for (int j = 0; j < (1 << d); ++j) {
+          const int t = h->level_ptr[rl + d] + ((root - h->level_ptr[rl]) << d) + j;
+          if (h->c_rank[t] == 0) continue;
+          for (int64_t b = h->s_row_ptr[t]; b < h->s_row_ptr[t + 1]; ++b) {
+            const int s = h->s_col[b];
+            if (h->c_rank[s] > 0 && prog_of[s] != pi) up.insert(prog_of[s]);
+          }
+        }
+      P.wait_up_first = (int)cand.waits.size();
+      P.n_wait_up = (int)up.size();
+      cand.waits.insert(cand.waits.end(), up.begin(), up.end());
+      if (!bottom) {  // external children: the bottom programs under this top program
+        P.ext_wait_first = (int)cand.waits.size();
+        const int d = ls - lt;
+        const int first = (root - h->level_ptr[lt]) << d;
+        P.n_ext_wait = 1 << d;
+        for (int j = 0; j < (1 << d); ++j) cand.waits.push_back(first + j);
+      } else if (ls > lt) {
+        const int parent_top = nb + (pi >> (ls - lt));
+        // only when the parent carries rank (otherwise the top writes nothing for this root)
+        int par = h->level_ptr[ls - 1] + (pi >> 1);
+        P.wait_down = h->c_rank[par] > 0 ? parent_top : -1;
+      }
+    }
+    cand.ls = ls;
+    cand.lt = lt;
+    cand.n_bottom = nb;
+    cand.n_top = nt;
+    tp = std::move(cand);
+    return true;
+  }
+  return false;
+}
+
+// device state of the tree far field
+struct TreeDev {
+  TProg* progs = nullptr;
+  TCopy* copies = nullptr;
+  int32_t* waits = nullptr;
+  TNode* nodes = nullptr;
+  int32_t* gidx = nullptr;
+  uint32_t* flags = nullptr;  // up [n], down [n]
+  MegaCtrl* ctrl = nullptr;
+  uint64_t* trace = nullptr;
+  int n_progs = 0, smem = 0;
+};
+
+namespace {
+template <typename T>
+int upload_vec(T** dst, const std::vector<T>& v) {
+  const size_t bytes = sizeof(T) * std::max<size_t>(v.size(), 1);
+  H2B_CUDA_TRY(cudaMalloc((void**)dst, bytes));
+  if (!v.empty()) H2B_CUDA_TRY(cudaMemcpy(*dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  return H2B_OK;
+}
+}  // namespace
+
+int h2b_tree_upload(const TreePlan& tp, TreeDev** out, int64_t* bytes) {
+  TreeDev* d = new TreeDev();
+  int rc = upload_vec(&d->progs, tp.progs);
+  if (!rc) rc = upload_vec(&d->copies, tp.copies);
+  if (!rc) rc = upload_vec(&d->waits, tp.waits);
+  if (!rc) rc = upload_vec(&d->nodes, tp.nodes_all);
+  if (!rc) rc = upload_vec(&d->gidx, tp.gidx_all);
+  d->n_progs = (int)tp.progs.size();
+  if (!rc) {
+    const cudaError_t e1 = cudaMalloc(&d->flags, sizeof(uint32_t) * 2 * std::max(d->n_progs, 1));
+    const cudaError_t e2 = cudaMalloc(&d->ctrl, sizeof(MegaCtrl));
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+      h2b_set_error("h2b_tree_upload: allocation failed");
+      rc = H2B_ENOMEM;
+    } else {
+      cudaMemset(d->flags, 0, sizeof(uint32_t) * 2 * std::max(d->n_progs, 1));
+      cudaMemset(d->ctrl, 0, sizeof(MegaCtrl));
+    }
+  }
+  d->smem = tp.smem_max;
+  if (!rc && getenv("H2B_TREE_TRACE")) {
+    cudaMalloc(&d->trace, sizeof(uint64_t) * 32 * std::max(d->n_progs, 1));
+    cudaMemset(d->trace, 0, sizeof(uint64_t) * 32 * std::max(d->n_progs, 1));
+  }
+  if (!rc) {
+    const cudaError_t e = cudaFuncSetAttribute(k_far_tree, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 13800);
+    cudaFuncSetAttribute(k_far_tree, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) {
+      h2b_set_error(std::string("k_far_tree attributes: ") + cudaGetErrorString(e));
+      rc = H2B_ECUDA;
+    }
+  }
+  *bytes = (int64_t)(sizeof(TProg) * tp.progs.size() + sizeof(TCopy) * tp.copies.size() +
+                     sizeof(TNode) * tp.nodes_all.size() + 4 * tp.gidx_all.size());
+  *out = d;
+  return rc;
+}
+
+void h2b_tree_free(TreeDev* d) {
+  if (!d) return;
+  void* ptrs[] = {d->progs, d->copies, d->waits, d->nodes, d->gidx, d->flags, d->ctrl, d->trace};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete d;
+}
+
+int h2b_tree_static_smem() {
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, k_far_tree) != cudaSuccess) {
+    cudaGetLastError();
+    return 1024;
+  }
+  return (int)fa.sharedSizeBytes;
+}
+
+int h2b_tree_error(const TreeDev* d, uint32_t* err) {
+  MegaCtrl c{};
+  H2B_CUDA_TRY(cudaMemcpy(&c, d->ctrl, sizeof(c), cudaMemcpyDeviceToHost));
+  *err = c.error;
+  return H2B_OK;
+}
+
+// plan + upload for handle h; *planned = 0 when the tree does not qualify (k_mega stays)
+int h2b_tree_prepare(h2b_ctx* h, int max_ctas, int budget_bytes, int64_t* bytes, int* planned) {
+  *planned = 0;
+  *bytes = 0;
+  TreePlan tp;
+  if (!h2b_plan_tree(h, max_ctas, budget_bytes, tp)) return H2B_OK;
+  H2B_TRY(h2b_tree_upload(tp, &h->tree, bytes));
+  h->tree_ls = tp.ls;
+  h->tree_lt = tp.lt;
+  h->tree_progs = (int)tp.progs.size();
+  h->tree_smem = tp.smem_max;
+  *planned = 1;
+  return H2B_OK;
+}
+
+// one launch of the far field on `st` (cooperative: the programs wait on one another)
+int h2b_launch_tree(h2b_ctx* h, const TreeDev* d, const double2* xp, double2* yp, cudaStream_t st) {
+  TreeArgs A;
+  A.progs = d->progs;
+  A.copies = d->copies;
+  A.waits = d->waits;
+  A.src[TS_X] = xp;
+  A.src[TS_V] = h->buf[H2B_SEC_V];
+  A.src[TS_T] = h->buf[H2B_SEC_T];
+  A.src[TS_S] = h->buf[H2B_SEC_S];
+  A.src[TS_NODES] = d->nodes;
+  A.src[TS_GIDX] = d->gidx;
+  A.xhat = h->xhat;
+  A.yhat = h->yhat;
+  A.y = yp;
+  A.flags_up = d->flags;
+  A.flags_down = d->flags + d->n_progs;
+  A.ctrl = d->ctrl;
+  A.trace = d->trace;
+  {
+    const char* e = getenv("H2B_TREE_TRACE");
+    A.trace_levels = e && atoi(e) == 2;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(d->n_progs);
+  cfg.blockDim = dim3(TNT);
+  cfg.dynamicSmemBytes = d->smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  H2B_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_far_tree, A));
+  return H2B_OK;
+}
+
+// development aid: the per-program timeline of the last launch (H2B_TREE_TRACE set at prepare):
+// out[32 * i + j] = timestamp j of program i (ns, globaltimer; 0 = not reached; SM clock64 at
+// out[32 * i + 16 + j]), programs
+// [0, n_bottom) bottom, then top
+extern "C" int h2b_tree_trace(h2b_handle h, int64_t* out, int64_t max_progs) {
+  if (!h || !out || !h->tree || !h->tree->trace) {
+    h2b_set_error("h2b_tree_trace: no tree trace (set H2B_TREE_TRACE before the first matvec)");
+    return H2B_ESTATE;
+  }
+  const int64_t n = std::min<int64_t>(max_progs, h->tree->n_progs);
+  H2B_CUDA_TRY(cudaDeviceSynchronize());
+  H2B_CUDA_TRY(cudaMemcpy(out, h->tree->trace, sizeof(uint64_t) * 32 * n, cudaMemcpyDeviceToHost));
+  return H2B_OK;
+}

@@ -162,11 +162,24 @@ def make_config(k, seed=0):
         xs, rep = arith.bicgstab_solve(lambda v: arith.matvec(h2, v), x, tol=1e-6, max_iter=1000)
         extra.update(bicg_iters=np.int64(rep.iterations), bicg_hist=np.asarray(rep.residual_history))
     if k == 3:
-        # plane wave with seeded incidence (SURVEY.md §8d cfg 3)
-        th = np.arccos(rng.uniform(-1, 1))
-        ph = rng.uniform(0, 2 * np.pi)
+        # plane wave with seeded incidence (SURVEY.md §8d cfg 3): a FRESH default_rng(0), theta
+        # first, then phi; then GMRES(50) to 1e-6 on it with the reference matvec (the oracle
+        # restatement; the reference has no GMRES) and scipy's count beside it
+        rng3 = np.random.default_rng(0)
+        th = np.arccos(rng3.uniform(-1, 1))
+        ph = rng3.uniform(0, 2 * np.pi)
         d = np.array([np.sin(th) * np.cos(ph), np.sin(th) * np.sin(ph), np.cos(th)])
-        extra["rhs_plane_wave"] = kernel.plane_wave_rhs(g, K0, d)
+        b = kernel.plane_wave_rhs(g, K0, d)
+        extra["rhs_plane_wave"] = b
+        extra["incidence"] = d
+        if os.environ.get("H2B_CFG3_GMRES"):
+            from oracle.krylov_oracle import gmres_solve
+            t = time.time()
+            xs, rep = gmres_solve(lambda v: arith.matvec(h2, v), b, tol=1e-6, restart=50, max_iter=3000)
+            extra.update(gmres_iters=np.int64(rep.iterations), gmres_hist=np.asarray(rep.residual_history),
+                         gmres_s=np.float64(time.time() - t))
+            print(f"cfg3 oracle GMRES(50): {rep.iterations} it, converged {rep.converged}, "
+                  f"{time.time() - t:.0f} s", flush=True)
     os.makedirs(os.path.join(ROOT, "data"), exist_ok=True)
     out = os.path.join(ROOT, "data", f"cfg{k}.npz")
     save_packed(pk, out, extra=extra)
