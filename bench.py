@@ -369,8 +369,9 @@ def run_partitioned(a, pk, ex, rank, world, local, emit=True):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
+    yl_buf = torch.empty_like(xl)
     for _ in range(max(3, a.warmup)):
-        op.matvec_local(xl)
+        op.matvec_local(xl, out=yl_buf)
     barrier()
     with ClockSampler(local) as clk:
         time.sleep(0.25)
@@ -381,7 +382,7 @@ def run_partitioned(a, pk, ex, rank, world, local, emit=True):
             if world > 1:
                 dist.barrier()  # all ranks start the step together (the all-gather couples them)
             s.record(stream)
-            y = op.matvec_local(xl)
+            y = op.matvec_local(xl, out=yl_buf)
             e.record(stream)
         barrier()
     ms = sum(s.elapsed_time(e) for s, e in ev) / a.steps
@@ -394,7 +395,8 @@ def run_partitioned(a, pk, ex, rank, world, local, emit=True):
         yh = op.matvec_local(xh.to(dev, non_blocking=True)).cpu()
         t_e2e.append(time.perf_counter() - t0)
     e2e_s = float(np.median(t_e2e))  # wall clock per call: median (host jitter)
-    ms, e2e_s = max_over_ranks([ms, e2e_s], dev)
+    exch_ms = op.exchange_ms(reps=10)
+    ms, e2e_s, exch_ms = max_over_ranks([ms, e2e_s, exch_ms], dev)
     # parity: gather every rank's rows on rank 0
     yl = y.cpu().numpy()
     parts = [None] * world
@@ -414,11 +416,12 @@ def run_partitioned(a, pk, ex, rank, world, local, emit=True):
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "complex128 (f64)",
             "data": "synthetic: reference-built operator of BASELINE config, N(0,1) RHS (seed 0)",
-            "config": dict(config_desc(a.config, pk), parallelism=f"subtree partition x{world} "
-                           "(level-log2(N) clusters); exchange of x and x-hat per matvec: "
-                           + ("fused into the upward-pass kernels as NVLink P2P stores + one barrier"
-                              if op.exchange_mode == "p2p" else "one NCCL all-gather"),
-                           l2="flushed before every timed step"),
+            "config": config_desc(a.config, pk),
+            "parallelism": f"subtree partition x{world} (level-log2(N) clusters); exchange of x and "
+                           "x-hat per matvec: " + ("fused into the upward-pass kernels as NVLink P2P "
+                                                   "stores + one barrier" if op.exchange_mode == "p2p"
+                                                   else "one NCCL all-gather"),
+            "l2": "flushed before every timed step",
             "roofline": {"bound": "hbm", "kernel": "whole partitioned matvec step (grouped GEMV "
                          "plan kernels per rank, max over ranks)", "achieved": alg / (ms * 1e-3) / 1e9,
                          "peak": peak * world, "unit": "GB/s",
@@ -429,6 +432,7 @@ def run_partitioned(a, pk, ex, rank, world, local, emit=True):
             "gpu_launches": launches * a.steps, "gpu_launches_per_step": launches,
             "clocks": clk.summary(), "parity_relerr_vs_reference": relerr,
             "exchange_bytes_per_step": 16 * op.part.chunk * world,
+            "exchange_ms": exch_ms,
             "exchange": op.exchange_mode,
         }
         if not emit:
@@ -441,32 +445,13 @@ def run_partitioned(a, pk, ex, rank, world, local, emit=True):
     return 0
 
 
-def main():
-    a = parse()
-    if a.impl == "reference":
-        return run_reference(a)
+def run_single(a, pk, ex, rank, world, local, steps=None, extras=True):
+    """One GPU: the whole operator on this device, q = 1; L2 flushed before every timed step."""
     import ctypes as C
     import torch
-    rank, world, local = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        backend = os.environ.get("H2B_BENCH_BACKEND", "nccl")  # gloo: functional tests only
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-        else:
-            dist.init_process_group(backend)
+    from paper_1703_01175_b200 import H2Operator, _abi, matvec as h2_matvec
+    steps = steps or a.steps
     dev = torch.device(f"cuda:{local}")
-    torch.cuda.set_device(dev)
-    from paper_1703_01175_b200 import H2Operator, _abi
-
-    pk, ex = load(a.config)
-    if pk is None:
-        if rank == 0:
-            print(json.dumps({"metric": METRIC, "error": f"data/cfg{a.config}.npz missing"}))
-        return 1
-    if a.partitioned:
-        return run_partitioned(a, pk, ex, rank, world, local)
     op = H2Operator(pk, device=local)
     L = _abi.lib()
     _abi.check(L.h2b_prepare_handle(op.handle), "prepare")
@@ -499,8 +484,8 @@ def main():
     torch.cuda.synchronize(dev)
     with ClockSampler(local) as clk:
         time.sleep(0.25)  # let the sampler start
-        ms = timed(mv, a.steps)
-        ms_warm = timed(mv, a.steps, flush_l2=False)
+        ms = timed(mv, steps)
+        ms_warm = timed(mv, steps, flush_l2=False)
         # calibration: a plain cold read (sum) of as many bytes as the matvec's algorithmic
         # traffic, same flush and timing — the attainable streaming time at this size
         # (skipped when that buffer does not fit beside the operator: at such sizes the cold
@@ -509,10 +494,10 @@ def main():
         ms_read = None
         if pk.algorithmic_bytes(1) < 0.8 * free_b:
             cal = torch.ones(pk.algorithmic_bytes(1) // 8, dtype=torch.float64, device=dev)
-            ms_read = timed(lambda: cal.sum(), max(5, min(a.steps, 10)))
+            ms_read = timed(lambda: cal.sum(), max(5, min(steps, 10)))
             del cal
         for _ in range(3):  # keep the device busy for a few more clock samples
-            timed(mv, a.steps)
+            timed(mv, steps)
     torch.cuda.synchronize(dev)
     ms, ms_warm = max_over_ranks([ms, ms_warm], dev)
     # parity guard on the measured output
@@ -532,14 +517,28 @@ def main():
         _abi.check(L.h2b_set_option(op.handle, _abi.OPT_DEBUG, 2))
         for _ in range(3):
             mv()
-        ms_near = max_over_ranks([timed(mv, a.steps)], dev)[0]
+        ms_near = max_over_ranks([timed(mv, steps)], dev)[0]
         _abi.check(L.h2b_set_option(op.handle, _abi.OPT_DEBUG, 0))
         nb = pk.near_bytes(1)
         dominant = {"kernel": "k_near_stream (near-field, alone: the step without its far-field launch)",
                     "alg_bytes_per_launch": nb, "ms_per_launch": ms_near,
                     "achieved": nb / (ms_near * 1e-3) / 1e9}
 
-    # end-to-end through the host-buffer C-ABI call (pinned host memory)
+    # end to end through the reference-facing drop-in: matvec(h2, x) with a numpy (pageable)
+    # x in, a fresh numpy y out (arith.py:108-117) — h2b_matvec_host stages the pageable buffers
+    # through its own pinned ones; beside it the same C-ABI call on pinned caller buffers
+    xn = ex["x"][:, 0].copy()
+    for _ in range(3):
+        h2_matvec(op, xn)
+    t_e2e = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        yn = h2_matvec(op, xn)
+        t_e2e.append(time.perf_counter() - t0)
+    e2e_s = float(np.median(t_e2e))  # wall clock per call: median (host jitter)
+    e2e_s = max_over_ranks([e2e_s], dev)[0]
+    e2e_relerr = (float(np.linalg.norm(yn - ex["y"][:, 0]) / np.linalg.norm(ex["y"][:, 0]))
+                  if "y" in ex else None)
     xh = torch.from_numpy(ex["x"][:, 0].copy()).pin_memory()
     yh = torch.empty_like(xh).pin_memory()
 
@@ -548,16 +547,17 @@ def main():
 
     for _ in range(3):
         e2e_call()
-    t_e2e = []
-    for _ in range(a.steps):
+    t_pin = []
+    for _ in range(steps):
         t0 = time.perf_counter()
         e2e_call()
-        t_e2e.append(time.perf_counter() - t0)
-    e2e_s = float(np.median(t_e2e))  # wall clock per call: median (host jitter)
-    e2e_s = max_over_ranks([e2e_s], dev)[0]
+        t_pin.append(time.perf_counter() - t0)
+    e2e_pinned_s = float(np.median(t_pin))
 
-    nlaunch, mega = C.c_int64(), C.c_int64()
+    nlaunch, mega, tree_q = C.c_int64(), C.c_int64(), C.c_int64()
     _abi.check(L.h2b_query(op.handle, _abi.Q_LAUNCHES_Q1, C.byref(nlaunch)))
+    _abi.check(L.h2b_query(op.handle, _abi.Q_TREE, C.byref(tree_q)))
+    tree_on = tree_q.value != 0
     _abi.check(L.h2b_query(op.handle, _abi.Q_MEGA, C.byref(mega)))
     peak, peak_src = peaks()
     alg_bytes = pk.algorithmic_bytes(1)
@@ -575,7 +575,7 @@ def main():
         "value": world * unknowns / (ms * 1e-3),
         "unit": UNIT,
         "n_gpus": world,
-        "steps": a.steps,
+        "steps": steps,
         "warmup": a.warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
@@ -583,16 +583,16 @@ def main():
         "vs_baseline": None,
         "dtype": "complex128 (f64)",
         "data": "synthetic: reference-built operator of BASELINE config, N(0,1) RHS (seed 0)",
-        "config": dict(config_desc(a.config, pk), l2="flushed before every timed step (256 MiB write + 256 MiB read: clean L2)",
-                       parallelism=(f"{world} GPUs, one process each: right-hand sides sharded "
-                                    "across ranks (each rank a full operator replica and its own "
-                                    "RHS; no data-path collective)" if world > 1 else "1 GPU")),
+        "config": config_desc(a.config, pk),
+        "l2": "flushed before every timed step (256 MiB write + 256 MiB read: clean L2)",
+        "parallelism": "1 GPU (the whole operator)",
         "achieved_gbs_total": pk.algorithmic_bytes(1) / (ms * 1e-3) / 1e9,
         "hbm_frac_total": pk.algorithmic_bytes(1) / (ms * 1e-3) / 1e9 / peak,
         "roofline": {"bound": "hbm",
                      "kernel": ("whole matvec step: k_near_stream (near-field, ~83% of B_alg) "
-                                "concurrent with k_mega (far-field task graph); B_alg = "
-                                "16(E_V+E_T+E_S+E_D) + 32(N+K) bytes per step"
+                                "concurrent with " + ("k_far_tree (far field as subtree programs)"
+                                                      if tree_on else "k_mega (far-field task graph)") +
+                                "; B_alg = 16(E_V+E_T+E_S+E_D) + 32(N+K) bytes per step"
                                 if int(nlaunch.value) == 2 and int(mega.value) else
                                 f"whole matvec step ({int(nlaunch.value)} launches); B_alg = "
                                 "16(E_V+E_T+E_S+E_D) + 32(N+K) bytes per step"),
@@ -606,73 +606,103 @@ def main():
         "dominant_kernel": (dict(dominant, peak=peaks()[0], unit="GB/s",
                                  frac=dominant["achieved"] / peaks()[0]) if dominant else None),
         "e2e": {"value": world * unknowns / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * pk.n,
-                "d2h_bytes_per_step": 16 * pk.n, "ms_per_call": e2e_s * 1e3},
-        "gpu_launches": int(nlaunch.value) * a.steps,
+                "d2h_bytes_per_step": 16 * pk.n, "ms_per_call": e2e_s * 1e3,
+                "call": "paper_1703_01175_b200.matvec(h2, x): numpy x in, fresh numpy y out",
+                "parity_relerr_vs_reference": e2e_relerr},
+        "e2e_pinned": {"value": world * unknowns / e2e_pinned_s, "unit": UNIT,
+                       "ms_per_call": e2e_pinned_s * 1e3,
+                       "call": "h2b_matvec_host on pinned caller buffers (one CUDA graph per call)"},
+        "gpu_launches": int(nlaunch.value) * steps,
         "gpu_launches_per_step": int(nlaunch.value),
         "clocks": clk.summary(),
         "parity_relerr_vs_reference": relerr,
     }
-    gm = gmres_bench(rank, world, local) if not a.no_gmres else None
-    if gm:
-        line["gmres"] = gm
-    bc = bicgstab_bench(rank, local) if not a.no_gmres else None
-    if bc:
-        line["bicgstab"] = bc
-    mr = mrhs_bench(rank, local) if not a.no_gmres else None
-    if mr:
-        line["multi_rhs"] = mr
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        t_cpu, n_cpu = cpu_port_time(pk, ex["x"][:, 0], a.cpu_seconds)
-        line["cpu_baseline"] = {"value": pk.n / t_cpu, "unit": UNIT, "cores": 1, "kind": "port",
-                                "sample": f"{n_cpu} full cfg{a.config} matvecs in {t_cpu * n_cpu:.1f} s "
-                                          "(oracle/h2_oracle.py restates arith.matvec loop-for-loop)",
-                                "cpu": os.cpu_count()}
+    op.close()
+    return line
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    import ctypes as C
+    import torch
+    rank, world, local = dist_env()
     if world > 1:
-        # the same operator partitioned by subtree over the N GPUs (fused P2P exchange, else one
-        # NCCL all-gather per matvec; strong scaling of ONE right-hand side), reported beside the
-        # headline — a failure here must not cost the headline line
-        part, errs = None, []
-        for mode in ("auto", "allgather"):
-            try:
-                part = run_partitioned(argparse.Namespace(**dict(vars(a), steps=min(a.steps, 10),
-                                                                 exchange=mode)),
-                                       pk, ex, rank, world, local, emit=False)
-                break
-            except Exception as e:  # noqa: BLE001
-                errs.append(f"{mode}: {type(e).__name__}: {e}"[:300])
-        if rank == 0 and part is None:
-            line["partitioned_strong"] = {"error": errs}
-        if rank == 0 and part:
-            line["partitioned_strong"] = {k: part[k] for k in ("value", "ms_per_step", "scaling",
-                                                               "roofline", "exchange_bytes_per_step",
-                                                               "gpu_launches_per_step",
-                                                               "parity_relerr_vs_reference")}
-            line["partitioned_strong"]["parallelism"] = part["config"]["parallelism"]
-            line["partitioned_strong"]["exchange"] = part.get("exchange")
-        # BASELINE's scaling config: the 2M-unknown cube (cfg4, structure-exact: the reference
-        # block structure and ranks, payloads generated on each rank's device) partitioned over
-        # the N GPUs — strong scaling of one right-hand side
-        cube_k = int(os.environ.get("H2B_BENCH_CUBE_CONFIG", "4"))  # another config: functional tests
-        if not a.no_cube and a.config != cube_k:
-            del op
-            torch.cuda.empty_cache()
-            cube, errs = None, []
-            try:
-                pk4, ex4 = load(cube_k)
-                if pk4 is None:
-                    raise FileNotFoundError(f"fixtures/cfg{cube_k}_structure.npz")
-                cube = run_partitioned(argparse.Namespace(**dict(vars(a), config=cube_k, steps=min(a.steps, 10),
-                                                                 exchange="auto")),
-                                       pk4, ex4, rank, world, local, emit=False)
-            except Exception as e:  # noqa: BLE001
-                errs.append(f"{type(e).__name__}: {e}"[:300])
-            if rank == 0:
-                line["partitioned_cube_strong"] = (
-                    {"error": errs} if cube is None else
-                    dict({k: cube[k] for k in ("value", "unit", "ms_per_step", "scaling", "roofline",
-                                               "exchange_bytes_per_step", "gpu_launches_per_step",
-                                               "e2e", "exchange")},
-                         config=cube["config"]))
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        backend = os.environ.get("H2B_BENCH_BACKEND", "nccl")  # gloo: functional tests only
+        # NCCL's init log (one line per rank and channel setup) on stderr: the rank count and the
+        # NVLink / NVLS transport are visible in the run's log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    from paper_1703_01175_b200 import H2Operator, _abi
+
+    pk, ex = load(a.config)
+    if pk is None:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "error": f"data/cfg{a.config}.npz missing"}))
+        return 1
+    if world > 1 or a.partitioned:
+        # N GPUs: the operator partitioned by subtree: strong scaling of one RHS
+        line = run_partitioned(a, pk, ex, rank, world, local, emit=False)
+        if rank == 0 and line is None:
+            return 1
+    else:
+        line = run_single(a, pk, ex, rank, world, local)
+    if world == 1:
+        gm = gmres_bench(rank, world, local) if not a.no_gmres else None
+        if gm:
+            line["gmres"] = gm
+        bc = bicgstab_bench(rank, local) if not a.no_gmres else None
+        if bc:
+            line["bicgstab"] = bc
+        mr = mrhs_bench(rank, local) if not a.no_gmres else None
+        if mr:
+            line["multi_rhs"] = mr
+        if rank == 0 and not a.no_cpu_baseline:
+            t_cpu, n_cpu = cpu_port_time(pk, ex["x"][:, 0], a.cpu_seconds)
+            line["cpu_baseline"] = {"value": pk.n / t_cpu, "unit": UNIT, "cores": 1, "kind": "port",
+                                    "sample": f"{n_cpu} full cfg{a.config} matvecs in {t_cpu * n_cpu:.1f} s "
+                                              "(oracle/h2_oracle.py restates arith.matvec loop-for-loop)",
+                                    "cpu": os.cpu_count()}
+    # BASELINE's scaling config at every N: the 2M-unknown cube (cfg4, structure-exact: the
+    # reference block structure and ranks, payloads generated on each device) — one GPU holds the
+    # whole 140 GB operator at N = 1, N > 1 partitions it by subtree (strong scaling of one RHS).
+    # A failure here must not cost the headline line.
+    cube_k = int(os.environ.get("H2B_BENCH_CUBE_CONFIG", "4"))  # another config: functional tests
+    if not a.no_cube and a.config != cube_k:
+        import gc
+        gc.collect()
+        torch.cuda.empty_cache()
+        cube, errs = None, []
+        try:
+            pk4, ex4 = load(cube_k)
+            if pk4 is None:
+                raise FileNotFoundError(f"fixtures/cfg{cube_k}_structure.npz")
+            sub = argparse.Namespace(**dict(vars(a), config=cube_k, steps=min(a.steps, 5), warmup=3,
+                                            exchange="auto"))
+            if world > 1:
+                cube = run_partitioned(sub, pk4, ex4, rank, world, local, emit=False)
+            else:
+                cube = run_single(sub, pk4, ex4, rank, world, local, steps=sub.steps)
+        except Exception as e:  # noqa: BLE001
+            errs.append(f"{type(e).__name__}: {e}"[:300])
+        if rank == 0:
+            line["cube_strong"] = (
+                {"error": errs} if cube is None else
+                dict({k: cube[k] for k in ("value", "unit", "ms_per_step", "scaling", "roofline", "e2e",
+                                           "gpu_launches_per_step", "parallelism", "n_gpus")
+                      if k in cube},
+                     config=cube["config"],
+                     **{k: cube[k] for k in ("exchange_bytes_per_step", "exchange_ms", "exchange")
+                        if k in cube}))
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

@@ -515,7 +515,11 @@ struct Builder {
       for (int64_t b = h->s_row_ptr[t]; b < h->s_row_ptr[t + 1]; ++b)
         s_total += (int64_t)h->c_rank[h->s_col[b]] * h->c_rank[t];
     }
-    const bool stage_s = !getenv("H2B_TREE_S_L2") && off + s_total + 2 * xh_total + n_rows <= budget_elems;
+    const bool s_l2 = getenv("H2B_TREE_S_L2") != nullptr;  // experiment: panels from L2 always
+    const bool stage_s = !s_l2 && off + s_total + 2 * xh_total + n_rows <= budget_elems;
+    // reading the panels from L2 was measured 3x slower than the task-graph kernel at cfg1
+    // (warp-per-target GEMVs on L2 latency): the tree plan is only taken with staged panels
+    if (!stage_s && !s_l2) return false;
     int xg_rows = 0;
     for (int i = 0; i < own_end; ++i) {
       const int t = nd_p[i];

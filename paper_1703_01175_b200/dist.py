@@ -287,9 +287,36 @@ class DistH2Operator:
             for ph in (PH_UP_TOP, PH_COUPLE, PH_DOWN, PH_NEAR):
                 self.engine.run(ph, xbuf, yhat, y, q)
 
-    def matvec_local(self, x_local, graph=True):
+    def exchange_ms(self, reps=10, q=1):
+        """Device time (ms, CUDA events, mean of ``reps``) of this rank's exchange step alone: the
+        NCCL all-gather of the exchange buffer, or (p2p) the x-slice broadcast over NVLink plus the
+        barrier collective — the x̂ stores of the p2p mode are fused into the upward-pass kernels
+        and are not separable.  Collective: every rank must call it."""
+        import torch
+        xbuf, yhat, y, send = self._work(q)
+        if self.world == 1 or self.device.type != "cuda":
+            return 0.0
+
+        def step():
+            if self.exchange_mode == "p2p":
+                self.engine.bcast_rows(xbuf, self.rank * self.part.chunk, self.nrows, q)
+                self._barrier()
+            else:
+                self.exchange(xbuf, send, q)
+        step()
+        torch.cuda.synchronize(self.device)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            step()
+        e.record()
+        torch.cuda.synchronize(self.device)
+        return s.elapsed_time(e) / reps
+
+    def matvec_local(self, x_local, graph=True, out=None):
         """This rank's rows of S x.  On CUDA the whole step — the plan launches of every phase
-        and the NCCL all-gather — is captured once per q into a CUDA graph and replayed."""
+        and the NCCL all-gather — is captured once per q into a CUDA graph and replayed.
+        ``out``: a caller-owned (nrows,) / (nrows, q) tensor to write into (no allocation)."""
         import torch
         squeeze = x_local.dim() == 1
         xl = x_local.reshape(self.nrows, -1)
@@ -311,10 +338,15 @@ class DistH2Operator:
             cg.replay()
         else:
             self._body(q)
-        out = y.clone()
+        if out is None:
+            out = y.clone()
+            res = out[:, 0] if squeeze else out
+        else:
+            out.reshape(self.nrows, -1).copy_(y)
+            res = out
         if self.exchange_mode == "p2p":
             self._slot ^= 1
-        return out[:, 0] if squeeze else out
+        return res
 
     def close(self):
         """Release the device resources: IPC mappings, exchange allocations, the plan handle."""
