@@ -214,6 +214,15 @@ int h2b_zgemv_sub(const void* V, int64_t ldv, int nv, const void* h_dev, void* w
 /* y = a*x + b*y with complex scalars given by value (re, im) */
 int h2b_zaxpby(int64_t n, double ar, double ai, const void* x, double br, double bi, void* y,
                void* stream);
+/* Row-distributed GMRES building blocks (paper_1703_01175_b200/dist.py): the device Givens
+ * recurrence of h2b_gmres on a caller-owned state of h2b_gmres_state_elems(m) complex128 values
+ * (H (m+1) x m | g (m+1) | cosines (m) | residual records (2m) | 1/hn | {||b||, 0}), reading
+ * step j's CGS2 coefficients from hvals_dev ([0, j], [64, 64 + j]: the two passes, [128].x:
+ * ||w||^2, all already summed over ranks); host_res (mapped pinned, or NULL) receives
+ * {res_j, hn_j}.  h2b_zscale_dev: w *= scale_dev[0].x (the normalisation). */
+int64_t h2b_gmres_state_elems(int m);
+int h2b_gmres_givens(void* state, int m, int j, const void* hvals_dev, double* host_res, void* stream);
+int h2b_zscale_dev(void* w, int64_t n, const void* scale_dev, void* stream);
 
 /* ---------------------------------------------------------------------
  * Plan handles: a set of device payloads plus per-phase lists of grouped

@@ -1517,3 +1517,51 @@ extern "C" int h2b_bicgstab(h2b_handle h, const void* b_perm, void* x_perm, doub
   report->wall_time = now_s() - t0;
   return H2B_OK;
 }
+
+// ===========================================================================
+// building blocks of the row-distributed GMRES (paper_1703_01175_b200/dist.py): the same device
+// Givens recurrence as h2b_gmres, on a caller-owned state, plus the normalisation by a device
+// scalar — the host never reads a vector element between steps
+// ===========================================================================
+extern "C" int64_t h2b_gmres_state_elems(int m) {
+  return (int64_t)(m + 1) * m + (m + 1) + 3 * (int64_t)m + 2;
+}
+
+extern "C" int h2b_gmres_givens(void* state, int m, int j, const void* hvals_dev, double* host_res,
+                                void* stream) {
+  if (!state || !hvals_dev || m < 1 || m > 63 || j < 0 || j >= m) {
+    h2b_set_error("h2b_gmres_givens: bad arguments (need 1 <= m <= 63, 0 <= j < m)");
+    return H2B_EINVAL;
+  }
+  double2* base = (double2*)state;
+  GivensState S;
+  S.H = base;
+  S.g = S.H + (size_t)(m + 1) * m;
+  S.cs_sn = S.g + (m + 1);
+  S.res_hn = S.cs_sn + m;
+  S.scale = S.res_hn + m + m;
+  S.bnrm = S.scale + 1;
+  S.host_res = nullptr;
+  if (host_res) {
+    double2* d = nullptr;
+    if (cudaHostGetDevicePointer((void**)&d, host_res, 0) != cudaSuccess) {
+      cudaGetLastError();
+      h2b_set_error("h2b_gmres_givens: host_res is not mapped pinned memory");
+      return H2B_EINVAL;
+    }
+    S.host_res = d;  // records {res_j, 0}, {hn_j, 0} at 2j, 2j + 1
+  }
+  k_givens_step<<<1, 32, 0, (cudaStream_t)stream>>>(j, m, (const double2*)hvals_dev, S);
+  H2B_CHECK_LAUNCH();
+  return H2B_OK;
+}
+
+extern "C" int h2b_zscale_dev(void* w, int64_t n, const void* scale_dev, void* stream) {
+  if (!w || !scale_dev || n < 0) {
+    h2b_set_error("h2b_zscale_dev: bad arguments");
+    return H2B_EINVAL;
+  }
+  k_scale_dev<<<nblocks(n), RT, 0, (cudaStream_t)stream>>>((double2*)w, n, (const double2*)scale_dev);
+  H2B_CHECK_LAUNCH();
+  return H2B_OK;
+}

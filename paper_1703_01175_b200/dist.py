@@ -371,9 +371,19 @@ class DistH2Operator:
 
     # ---- Krylov helper: global 2-norm over the row slices -------------------------
     def norm(self, a):
+        """||a|| over all ranks: the rank's partial (libh2b reduction on CUDA), one all-reduce."""
         import torch
-        import torch.distributed as dist
-        s = (a.real * a.real + a.imag * a.imag).sum().reshape(1)
+        if a.is_cuda:
+            a = a.contiguous()
+            s = torch.empty(1, dtype=torch.complex128, device=a.device)
+            _abi.check(_abi.lib().h2b_zdotc_multi(C.c_void_p(a.data_ptr()), a.numel(), 1,
+                                                  C.c_void_p(a.data_ptr()), a.numel(),
+                                                  C.c_void_p(s.data_ptr()),
+                                                  C.c_void_p(torch.cuda.current_stream(a.device).cuda_stream)),
+                       "h2b_zdotc_multi")
+            s = s.real.clone()
+        else:
+            s = (a.real * a.real + a.imag * a.imag).sum().reshape(1)
         self.allreduce_(s)
         return float(torch.sqrt(s)[0])
 
@@ -421,16 +431,117 @@ def _givens(a, b):
 def dist_gmres_solve(op: DistH2Operator, b_local, tol=1e-6, restart=30, max_iter=1000):
     """Restarted GMRES(m), CGS2 Arnoldi, x0 = 0, on row-distributed vectors (collective).
 
-    Same recurrence and stopping rule as the single-GPU ``gmres_solve`` and the CPU
-    restatement (oracle/krylov_oracle.py::gmres_solve); the Arnoldi basis lives in
-    device memory as an (m+1, nrows) slice per rank; every inner product is a
-    per-rank partial summed by one all-reduce.
+    Same recurrence and stopping rule as the single-GPU ``gmres_solve`` (h2b_krylov.cu:
+    h2b_gmres) and the CPU restatement (oracle/krylov_oracle.py::gmres_solve).  Each rank keeps
+    its rows of the Arnoldi basis in device memory; one step is the partitioned matvec, two CGS
+    passes (libh2b multi-dot → ONE all-reduce of the j+1 coefficients per pass → basis update,
+    the second fused with ||w||^2 → one all-reduce), the device Givens recurrence
+    (h2b_gmres_givens, which writes the step's residual into mapped pinned memory) and the
+    normalisation by a device scalar.  Nothing is read back per step: the host checks the
+    residual of step j while step j+1 is already queued, and syncs only at the end of a cycle
+    (back substitution).  With the CPU plan interpreter (tests) the same recurrence runs on
+    torch CPU tensors.
     """
     import torch
     if not (0.0 < tol < 1.0):
         raise ValueError("tol must be in (0, 1)")
     if max_iter < 1 or restart < 1:
         raise ValueError("max_iter and restart must be >= 1")
+    if restart > 63:
+        raise ValueError("restart must be <= 63")
+    if op.device.type != "cuda":
+        return _dist_gmres_host(op, b_local, tol, restart, max_iter)
+    t0 = time.perf_counter()
+    L = _abi.lib()
+    dev = op.device
+    stream = torch.cuda.current_stream(dev)
+    sh = C.c_void_p(stream.cuda_stream)
+    b = b_local.to(dev, torch.complex128).contiguous()
+    bnrm = op.norm(b)
+    if bnrm == 0.0:
+        return torch.zeros_like(b), SolveReport(0, [], True, time.perf_counter() - t0)
+    m, n = int(restart), op.nrows
+    x = torch.zeros_like(b)
+    r = b.clone()
+    V = torch.zeros((m + 1, n), dtype=torch.complex128, device=dev)
+    hv = torch.zeros(256, dtype=torch.complex128, device=dev)       # CGS coefficients, ||w||^2
+    st = torch.zeros(int(L.h2b_gmres_state_elems(m)), dtype=torch.complex128, device=dev)
+    o_g = (m + 1) * m
+    o_scale = o_g + (m + 1) + 3 * m
+    st[o_scale + 1] = bnrm                                           # {||b||, 0}
+    # mapped pinned records written by the Givens kernel: {res_j, 0}, {hn_j, 0} per step j
+    host_res = torch.zeros(4 * m, dtype=torch.float64).pin_memory()
+    tmp = torch.empty_like(b)
+
+    def ptr(t, off=0):
+        return C.c_void_p(t.data_ptr() + 16 * off)
+
+    def allreduce(t):
+        if op.world > 1:
+            op.allreduce_(torch.view_as_real(t))
+
+    def step(j):
+        w = V[j + 1]
+        op.matvec_local(V[j], out=w)
+        _abi.check(L.h2b_zdotc_multi(ptr(V), n, j + 1, ptr(w), n, ptr(hv), sh), "h2b_zdotc_multi")
+        allreduce(hv[:j + 1])
+        _abi.check(L.h2b_zgemv_sub(ptr(V), n, j + 1, ptr(hv), ptr(w), n, None, sh), "h2b_zgemv_sub")
+        _abi.check(L.h2b_zdotc_multi(ptr(V), n, j + 1, ptr(w), n, ptr(hv, 64), sh), "h2b_zdotc_multi")
+        allreduce(hv[64:65 + j])
+        _abi.check(L.h2b_zgemv_sub(ptr(V), n, j + 1, ptr(hv, 64), ptr(w), n, ptr(hv, 128), sh),
+                   "h2b_zgemv_sub")
+        allreduce(hv[128:129])
+        _abi.check(L.h2b_gmres_givens(ptr(st), m, j, ptr(hv), C.c_void_p(host_res.data_ptr()), sh),
+                   "h2b_gmres_givens")
+        _abi.check(L.h2b_zscale_dev(ptr(w), n, ptr(st, o_scale), sh), "h2b_zscale_dev")
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        return ev
+
+    it, history, converged = 0, [], False
+    beta = bnrm
+    while it < max_iter:
+        if it > 0:
+            beta = op.norm(r)
+        st[o_g:o_g + m + 1] = 0
+        st[o_g] = beta
+        _abi.check(L.h2b_zaxpby(n, 1.0 / beta, 0.0, ptr(r), 0.0, 0.0, ptr(V[0]), sh), "h2b_zaxpby")
+        # step j+1 is queued before the host reads step j's residual (h2b_gmres's scheme: a
+        # speculative step writes only V[j+2], column j+1 of H and g[j+1..j+2], none of which the
+        # back substitution of a cycle ending at j reads)
+        it0, j_done = it, 0
+        evs = [step(0)]
+        for j in range(m):
+            if j + 1 < m and it0 + j + 1 < max_iter:
+                evs.append(step(j + 1))
+            evs[j].synchronize()
+            it += 1
+            res, hn = float(host_res[4 * j]), float(host_res[4 * j + 2])
+            history.append(res)
+            j_done = j + 1
+            if res <= tol or it >= max_iter or hn == 0.0:
+                break
+        torch.cuda.synchronize(dev)
+        Hh = st[:o_g].view(m + 1, m).cpu().numpy()
+        gh = st[o_g:o_g + m + 1].cpu().numpy()
+        y = np.zeros(j_done, dtype=np.complex128)
+        for i in range(j_done - 1, -1, -1):
+            y[i] = (gh[i] - Hh[i, i + 1:j_done] @ y[i + 1:j_done]) / Hh[i, i]
+        hv[:j_done] = torch.from_numpy(-y)
+        _abi.check(L.h2b_zgemv_sub(ptr(V), n, j_done, ptr(hv), ptr(x), n, None, sh), "h2b_zgemv_sub")
+        op.matvec_local(x, out=tmp)
+        r.copy_(b)
+        _abi.check(L.h2b_zaxpby(n, -1.0, 0.0, ptr(tmp), 1.0, 0.0, ptr(r), sh), "h2b_zaxpby")  # r = b - A x
+        true_res = op.norm(r) / bnrm
+        if true_res <= tol:
+            converged = True
+            break
+    return x, SolveReport(it, history, converged, time.perf_counter() - t0)
+
+
+def _dist_gmres_host(op, b_local, tol, restart, max_iter):
+    """The same recurrence on torch CPU tensors, for the CPU plan interpreter of the tests."""
+    import torch
     t0 = time.perf_counter()
     b = b_local.to(op.device, torch.complex128)
     bnrm = op.norm(b)
@@ -494,7 +605,6 @@ def dist_gmres_solve(op: DistH2Operator, b_local, tol=1e-6, restart=30, max_iter
 def _multi_dot(op, Vj, w):
     """h_i = Σ conj(V_i) w over all ranks, one all-reduce for all i."""
     import torch
-    import torch.distributed as dist
     h = (Vj.conj() * w.unsqueeze(0)).sum(1)
     if op.world > 1:
         h = torch.view_as_complex(op.allreduce_(torch.view_as_real(h).clone()))

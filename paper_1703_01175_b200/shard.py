@@ -436,8 +436,15 @@ def plan_shard(pk, G: int, g: int, part: Partition | None = None, bcast: bool = 
 
     payloads = [np.concatenate(a) if a else np.zeros(0, np.complex128) for a in pays]
     deferred = any(synth_fills) or bool(near_fills)
-    if deferred:  # sizes only; the device fills the described blocks
-        payloads = [np.zeros(0, np.complex128) for _ in range(N_PAY)]
+    if deferred:
+        # sections the device fills carry sizes only; sections built from host arrays (e.g. the
+        # reference-built far field of an operator whose near-field is sampled on the device)
+        # keep their data — a section is never mixed (far / near payloads are all-or-nothing)
+        for i in range(N_PAY):
+            dev_filled = bool(synth_fills[i]) or (i == PAY_D and bool(near_fills))
+            if dev_filled:
+                assert not pays[i], "payload section mixes host data and device fills"
+                payloads[i] = np.zeros(0, np.complex128)
     fills = None
     if deferred:
         fills = dict(sizes=list(size),
