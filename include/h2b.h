@@ -191,6 +191,16 @@ typedef struct h2b_report {
 int h2b_gmres(h2b_handle h, const void* b_perm, void* x_perm, int restart, double tol,
               int max_iter, double* history, h2b_report* report, void* stream);
 
+/* Block GMRES(restart) for q <= 64 right-hand sides (BASELINE config 5), all on device: the q-column
+ * matvec, block CGS2 (tall-skinny V^H W / W - V C kernels), CholQR2 of every block, the small
+ * least-squares problem orthonormalised incrementally in the (restart+1)q-dimensional space (no
+ * host work per step: the residual is read from mapped pinned memory one step behind).  B_perm,
+ * X_perm: N x q row-major complex128 device arrays in the permuted order.  Converged when every
+ * column's true relative residual is <= tol at the end of a cycle (oracle/krylov_oracle.py::
+ * block_gmres_solve); history: max over columns of the least-squares residual per block step. */
+int h2b_block_gmres(h2b_handle h, const void* B_perm, void* X_perm, int q, int restart, double tol,
+                    int max_iter, double* history, h2b_report* report, void* stream);
+
 /* BiCGStab, a line-by-line restatement of arith.bicgstab_solve
  * (arith.py:605-689) incl. the single rho-breakdown restart; the restart's
  * random perturbation (numpy default_rng(seed)) cannot be drawn on device,

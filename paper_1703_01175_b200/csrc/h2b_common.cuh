@@ -340,6 +340,8 @@ int h2b_ensure_workspace(h2b_ctx* h, int q);
 int h2b_run_matvec(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st);
 // the launches of one matvec without graph replay (for capture into a larger graph)
 int h2b_enqueue_matvec(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStream_t st, int* nl);
+// the handle's Krylov workspace (h2b_krylov.cu), shared by the solvers of one handle
+int h2b_krylov_workspace(h2b_ctx* h, size_t bytes, double2** out);
 // cross-stream ordering of the handle's device work (see h2b_ctx::ev_done)
 int h2b_order_begin(h2b_ctx* h, cudaStream_t st);
 int h2b_order_end(h2b_ctx* h, cudaStream_t st);

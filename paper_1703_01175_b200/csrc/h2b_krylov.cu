@@ -275,6 +275,13 @@ double now_s() {
 }
 
 
+}  // namespace
+
+// the handle's Krylov workspace (grown on demand; the cached GMRES step graphs point into it)
+int h2b_krylov_workspace(h2b_ctx* h, size_t bytes, double2** out) { return krylov_ws(h, bytes, out); }
+
+namespace {
+
 // ---- GMRES: Givens rotations on the device --------------------------------------------------
 struct GivensState {
   double2* H;       // (m+1) x m, row-major: H[i*m + j]
