@@ -177,6 +177,7 @@ struct Task {
 //   span:   SpanHead (9 slots) | n_copy x SpanCopy (2 slots each)
 //   couple: {n_items, cta_mode, 0, 0} | n_items x CoupleItem (2 slots each)
 constexpr int REC_SLOTS = 256;  // 4 KB per record buffer
+constexpr int NEAR_NRB = 8;     // near-field stream: record buffers (the task in use + NRB - 1 claimed ahead)
 constexpr int NEAR_REC_MAXB = 160;
 struct DepRange {
   int32_t lo, hi;           // task ids [lo, hi) that must be complete
@@ -287,6 +288,8 @@ struct h2b_ctx {
   int2* near_idx = nullptr;            // per near task {first slot, slots}
   int n_near_tasks = 0, near_rec_max = 0, near_nst = 0, near_smem = 0, near_grid = 0;
   uint32_t near_delay_ns = 0;  // tuning aid (H2B_DEBUG_NEAR_DELAY_NS)
+  int near_static = 0;         // near tasks split statically over the CTAs (H2B_NEAR_STATIC)
+  int near_dbg = 0;            // profiling only (H2B_NEAR_DBG): see NearArgs::dbg
   // far field as subtree programs (h2b_tree.cu): replaces k_mega beside k_near_stream when set
   TreeDev* tree = nullptr;
   int use_tree = 1;  // H2B_OPT_TREE

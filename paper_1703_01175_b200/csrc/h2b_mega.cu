@@ -82,6 +82,8 @@ struct NearArgs {
   int nst;        // ring stages
   int rec_slots;  // slots of each of the two record buffers
   uint32_t delay_ns;  // tuning aid: the producer starts this late (0 = at once)
+  int static_split;   // 1: CTA c streams tasks [c T / G, (c+1) T / G) in order (no claims)
+  int dbg;            // profiling only (results wrong): 1 no consumer math, 2 no x copies
 };
 
 // One CTA streams a sequence of near-field tasks as ONE continuous sequence of D blocks:
@@ -90,7 +92,7 @@ struct NearArgs {
 // blocks in the same order.  A record buffer is refilled with a newly claimed task as soon as
 // its task is consumed, so the stream never drains at task boundaries however small the
 // tasks are.
-constexpr int NRB = 3;  // record buffers: the consumer's task and up to two claimed ahead
+constexpr int NRB = NEAR_NRB;  // record buffers: the consumer's task and up to NRB - 1 claimed ahead
 
 template <int NS, int R>
 __device__ __forceinline__ void issue_block(const NearArgs& A, const int64_t* bl, int i, double2* st,
@@ -186,13 +188,26 @@ __global__ void __launch_bounds__(NEAR_THREADS, 1) k_near_stream(NearArgs A) {
         }
         ++claimed;
       };
-      for (int i = 0; i < NRB - 1; ++i) finish_claim((int)atomicAdd(&A.ctrl->near_next, 1u));
+      // claims: the next task from the global counter (dynamic balance), or this CTA's next task
+      // of a static contiguous split (no atomics on the producer's path)
+      const int s_first = (int)((int64_t)blockIdx.x * A.n_tasks / gridDim.x);
+      const int s_end = (int)((int64_t)(blockIdx.x + 1) * A.n_tasks / gridDim.x);
+      int s_next = s_first;
+      auto claim = [&]() -> int {
+        if (A.static_split) {
+          const int c = s_next < s_end ? s_next : A.n_tasks;
+          ++s_next;
+          return c;
+        }
+        return (int)atomicAdd(&A.ctrl->near_next, 1u);
+      };
+      for (int i = 0; i < NRB - 1; ++i) finish_claim(claim());
       int issued = 0;
       for (int q = 0;; ++q) {
         // keep NRB - 1 records claimed beyond q: fetch the counter now, complete the claim after
         // this record's blocks are issued
         const bool want = claimed < q + NRB && !end;
-        const int pending = want ? (int)atomicAdd(&A.ctrl->near_next, 1u) : 0;
+        const int pending = want ? claim() : 0;
         const int b = q % NRB;
         mbar_wait(&rbar[b], (q / NRB) & 1u);
         if (s_task[b] >= A.n_tasks) {
@@ -207,9 +222,9 @@ __global__ void __launch_bounds__(NEAR_THREADS, 1) k_near_stream(NearArgs A) {
             const int st = issued % nst;
             if (issued >= nst) mbar_wait(&ebar[st], ((issued / nst) - 1) & 1u);
             double2* sp = sm + (size_t)st * STG;
-            mbar_arrive_expect_tx(&fbar[st], 16u * (RB * NS + NS));
+            mbar_arrive_expect_tx(&fbar[st], 16u * (RB * NS + ((A.dbg & 2) ? 0 : NS)));
             bulk_g2s_hint(sp, A.dbuf + bl[2 * j], 16u * RB * NS, &fbar[st], pol);
-            bulk_g2s(sp + RB * NS, A.x + bl[2 * j + 1], 16u * NS, &fbar[st]);
+            if (!(A.dbg & 2)) bulk_g2s(sp + RB * NS, A.x + bl[2 * j + 1], 16u * NS, &fbar[st]);
           }
         }
         if (want) finish_claim(pending);
@@ -257,12 +272,14 @@ __global__ void __launch_bounds__(NEAR_THREADS, 1) k_near_stream(NearArgs A) {
         const int st = consumed % nst;
         mbar_wait(&fbar[st], (consumed / nst) & 1u);
         const double2* sp = sm + (size_t)st * STG;
-        const double2 xa = sp[RB * NS + col], xb = sp[RB * NS + col + 1];
+        if (!(A.dbg & 1)) {
+          const double2 xa = sp[RB * NS + col], xb = sp[RB * NS + col + 1];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const double2* d = sp + (r0 + r * RPP) * NS + col;
-          cfma(acc[r][0], d[0], xa);
-          cfma(acc[r][1], d[1], xb);
+          for (int r = 0; r < R; ++r) {
+            const double2* d = sp + (r0 + r * RPP) * NS + col;
+            cfma(acc[r][0], d[0], xa);
+            cfma(acc[r][1], d[1], xb);
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&ebar[st]);  // this warp is done with the stage
@@ -715,6 +732,8 @@ int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st)
     N.nst = std::max(1, h->near_nst);
     N.rec_slots = std::max(1, h->near_rec_max);  // NRB buffers of this size follow the ring
     N.delay_ns = h->near_delay_ns;
+    N.static_split = h->near_static;
+    N.dbg = h->near_dbg;
     const int ns = h->mega_ns, r = h->mega_r;
     bool launched = false;
 #define X(a, b)                                                                            \

@@ -195,7 +195,8 @@ __device__ __forceinline__ double2 rowdot(const double2* P, int r, int w, const 
 
 __global__ void __launch_bounds__(TNT, 1) k_far_tree(TreeArgs A) {
   extern __shared__ __align__(16) double2 sm[];
-  __shared__ __align__(8) uint64_t bar[2];  // [0]: nodes, gather list, x, V, T  [1]: staged S panels
+  // [0]: nodes, gather list, x, V (the leaf level)  [1]: staged S panels  [2]: T (internal levels)
+  __shared__ __align__(8) uint64_t bar[3];
   __shared__ uint32_t s_epoch;
   __shared__ TProg P;  // the program header (global loads would recur after every fence)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -206,6 +207,7 @@ __global__ void __launch_bounds__(TNT, 1) k_far_tree(TreeArgs A) {
     s_epoch = *(volatile uint32_t*)&A.ctrl->epoch;
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
   }
   for (int i = tid; i < (int)(sizeof(TProg) / 4); i += TNT)
     reinterpret_cast<int32_t*>(&P)[i] = reinterpret_cast<const int32_t*>(gP)[i];
@@ -216,6 +218,7 @@ __global__ void __launch_bounds__(TNT, 1) k_far_tree(TreeArgs A) {
   if (tid == 0) {
     mbar_arrive_expect_tx(&bar[0], (uint32_t)P.stage_bytes);
     mbar_arrive_expect_tx(&bar[1], (uint32_t)P.pad[0]);  // staged coupling panels (0: from L2)
+    mbar_arrive_expect_tx(&bar[2], (uint32_t)P.pad[1]);  // transfer matrices
   }
   for (int i = tid; i < n_copy; i += TNT) {
     const TCopy c = i == tid ? cp0 : A.copies[c0 + i];
@@ -226,7 +229,8 @@ __global__ void __launch_bounds__(TNT, 1) k_far_tree(TreeArgs A) {
     }
     const void* base = c.kind == TS_X ? A.src[TS_X] : c.kind == TS_V ? A.src[TS_V] : c.kind == TS_T ? A.src[TS_T]
                      : c.kind == TS_S ? A.src[TS_S] : c.kind == TS_NODES ? A.src[TS_NODES] : A.src[TS_GIDX];
-    bulk_g2s(sm + c.smem, (const double2*)base + c.src, 16u * (uint32_t)c.elems, &bar[c.kind == TS_S ? 1 : 0]);
+    bulk_g2s(sm + c.smem, (const double2*)base + c.src, 16u * (uint32_t)c.elems,
+             &bar[c.kind == TS_S ? 1 : c.kind == TS_T ? 2 : 0]);
   }
   const uint32_t want = s_epoch + 1;
   mbar_wait(&bar[0], 0);
@@ -248,9 +252,14 @@ __global__ void __launch_bounds__(TNT, 1) k_far_tree(TreeArgs A) {
     }
     __syncthreads();
   }
-  // ---- upward pass, deepest level first ----
+  // ---- upward pass, deepest level first (the transfer matrices land during the leaf level) ----
+  bool t_ready = false;
   for (int lv = nlev - 1; lv >= 0; --lv) {
     const int a = P.lev_first[lv], b = P.lev_first[lv + 1];
+    if (!t_ready && (!P.bottom || lv < nlev - 1)) {
+      mbar_wait(&bar[2], 0);
+      t_ready = true;
+    }
     for (int i = a + warp; i < b; i += NW) {
       const TNode nd = nodes[i];
       if (nd.kind != 2 && nd.k > 0) colsum(sm + nd.pay, nd.R, nd.k, nd.sh, sm + nd.in, sm + nd.xh);
@@ -273,6 +282,7 @@ __global__ void __launch_bounds__(TNT, 1) k_far_tree(TreeArgs A) {
   // ---- couplings: gather x̂ of the sources (own smem or other programs' published x̂) ----
   wait_flags(A.flags_up, A.waits + P.wait_up_first, P.n_wait_up, want, A.ctrl);
   if (P.pad[0]) mbar_wait(&bar[1], 0);
+  if (!t_ready) mbar_wait(&bar[2], 0);
   __syncthreads();
   tmark(A, 4);
   double2* xg = sm + P.xg_smem;
@@ -589,11 +599,13 @@ struct Builder {
       push_copy(TS_GIDX, first, (int)((gl.size() + 3) / 4), gidx_smem);
     }
     P.n_copy = (int)tp.copies.size() - P.copy_first;
-    int64_t bytes = 0, sbytes = 0;
+    int64_t bytes = 0, sbytes = 0, tbytes = 0;
     for (int c = P.copy_first; c < (int)tp.copies.size(); ++c)
       if (tp.copies[c].kind != TS_S || tp.copies[c].smem >= 0)
-        (tp.copies[c].kind == TS_S ? sbytes : bytes) += 16 * (int64_t)tp.copies[c].elems;
-    if (sbytes >= (1 << 20)) return false;
+        (tp.copies[c].kind == TS_S ? sbytes : tp.copies[c].kind == TS_T ? tbytes : bytes) +=
+            16 * (int64_t)tp.copies[c].elems;
+    if (sbytes >= (1 << 20) || tbytes >= (1 << 20)) return false;
+    P.pad[1] = (int32_t)tbytes;
     if (bytes >= (1 << 20)) return false;  // one mbarrier transaction count
     P.stage_bytes = (int32_t)bytes;
     P.pad[0] = (int32_t)sbytes;
