@@ -562,11 +562,14 @@ def run_single(a, pk, ex, rank, world, local, steps=None, extras=True):
     peak, peak_src = peaks()
     alg_bytes = pk.algorithmic_bytes(1)
     achieved = alg_bytes / (ms * 1e-3) / 1e9
+    # DRAM bytes per step (read + write of both kernels) from the committed ncu launch list of
+    # this configuration and far-field variant (profiles/step_traffic.json)
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "mega_traffic.json")
+    prof = os.path.join(ROOT, "profiles", "step_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(f"cfg{a.config}")
+            ent = json.load(open(prof)).get(f"cfg{a.config}", {}).get("tree" if tree_on else "mega")
+            traffic = ent["bytes"] if ent else None
         except Exception:
             traffic = None
     unknowns = pk.n * 1
