@@ -470,6 +470,10 @@ def run_single(a, pk, ex, rank, world, local, steps=None, extras=True):
         for s, e in ev:
             if flush_l2:
                 flush.flush()  # evict L2 (126 MB) before every timed step; not timed
+            # a 20 us device spin before the start event: the host-side launch of the step
+            # overlaps it, so the event pair brackets the device work (as in a solver loop,
+            # where launches are queued ahead of the GPU)
+            _abi.check(L.h2b_spin_ns(20000, sh))
             s.record(stream)
             fn()
             e.record(stream)
@@ -486,15 +490,20 @@ def run_single(a, pk, ex, rank, world, local, steps=None, extras=True):
         time.sleep(0.25)  # let the sampler start
         ms = timed(mv, steps)
         ms_warm = timed(mv, steps, flush_l2=False)
-        # calibration: a plain cold read (sum) of as many bytes as the matvec's algorithmic
-        # traffic, same flush and timing — the attainable streaming time at this size
-        # (skipped when that buffer does not fit beside the operator: at such sizes the cold
-        # read runs at the copy peak anyway)
+        # calibration: a plain cold read of as many bytes as the matvec's algorithmic traffic
+        # through libh2b's TMA bulk-copy ring (h2b_stream_read: the near-field kernel's access
+        # pattern without math), same flush and timing — the attainable streaming time at this
+        # size (skipped when that buffer does not fit beside the operator: at such sizes the
+        # cold read runs at the copy peak anyway)
         free_b, _ = torch.cuda.mem_get_info(dev)
         ms_read = None
         if pk.algorithmic_bytes(1) < 0.8 * free_b:
-            cal = torch.ones(pk.algorithmic_bytes(1) // 8, dtype=torch.float64, device=dev)
-            ms_read = timed(lambda: cal.sum(), max(5, min(steps, 10)))
+            nb = int(pk.algorithmic_bytes(1)) // 16 * 16
+            cal = torch.ones(nb // 8, dtype=torch.float64, device=dev)
+            sink = torch.zeros(1, dtype=torch.float64, device=dev)
+            ms_read = timed(lambda: _abi.check(L.h2b_stream_read(C.c_void_p(cal.data_ptr()), nb,
+                                                                 C.c_void_p(sink.data_ptr()), sh)),
+                            max(5, min(steps, 10)))
             del cal
         for _ in range(3):  # keep the device busy for a few more clock samples
             timed(mv, steps)

@@ -230,6 +230,12 @@ int h2b_zaxpby(int64_t n, double ar, double ai, const void* x, double br, double
  * step j's CGS2 coefficients from hvals_dev ([0, j], [64, 64 + j]: the two passes, [128].x:
  * ||w||^2, all already summed over ranks); host_res (mapped pinned, or NULL) receives
  * {res_j, hn_j}.  h2b_zscale_dev: w *= scale_dev[0].x (the normalisation). */
+/* Streaming-read calibration: reads `bytes` of device memory through a TMA bulk-copy ring (the
+ * near-field kernel's access pattern, no math) — the attainable cold read of that many bytes. */
+int h2b_stream_read(const void* src, size_t bytes, void* sink_dev, void* stream);
+/* Keeps `stream` busy for `ns` nanoseconds (one thread polling %globaltimer): enqueued before a
+ * timed region's start event so that host-side launch latency does not count as device time. */
+int h2b_spin_ns(uint64_t ns, void* stream);
 int64_t h2b_gmres_state_elems(int m);
 int h2b_gmres_givens(void* state, int m, int j, const void* hvals_dev, double* host_res, void* stream);
 int h2b_zscale_dev(void* w, int64_t n, const void* scale_dev, void* stream);

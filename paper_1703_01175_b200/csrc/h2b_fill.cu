@@ -195,3 +195,77 @@ extern "C" int h2b_plan_fill_near(h2b_plan_handle p, int payload, const int64_t*
   }
   return H2B_OK;
 }
+
+// ===========================================================================
+// Streaming-read calibration (bench.py: the attainable cold read of as many bytes as a matvec's
+// algorithmic traffic, for `frac_of_cold_read`): every CTA streams a contiguous slab of `bytes`
+// through a TMA bulk-copy ring of 16 KB stages (the access pattern of k_near_stream), one CTA
+// per SM x 2, no math; a checksum word keeps the reads live.
+// ===========================================================================
+namespace {
+constexpr int SR_STAGE = 16384, SR_NST = 4, SR_THREADS = 128;
+
+__global__ void __launch_bounds__(SR_THREADS) k_stream_read(const char* __restrict__ src, size_t bytes,
+                                                           double* sink) {
+  extern __shared__ __align__(128) char srs[];
+  __shared__ __align__(8) uint64_t bars[SR_NST];
+  const size_t per = (bytes / gridDim.x) & ~size_t(15);
+  const char* base = src + per * blockIdx.x;
+  const size_t mine = blockIdx.x + 1 == gridDim.x ? bytes - per * blockIdx.x : per;
+  const int n = (int)((mine + SR_STAGE - 1) / SR_STAGE);
+  if (threadIdx.x == 0)
+    for (int i = 0; i < SR_NST; ++i) mbar_init(&bars[i], 1);
+  __syncthreads();
+  auto issue = [&](int i) {
+    const int s = i % SR_NST;
+    const size_t left = mine - (size_t)i * SR_STAGE;
+    const uint32_t len = (uint32_t)(left < (size_t)SR_STAGE ? left : (size_t)SR_STAGE) & ~15u;
+    mbar_arrive_expect_tx(&bars[s], len);
+    if (len) bulk_g2s(srs + s * SR_STAGE, base + (size_t)i * SR_STAGE, len, &bars[s]);
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < SR_NST && i < n; ++i) issue(i);
+  double acc = 0.0;
+  for (int i = 0; i < n; ++i) {
+    mbar_wait(&bars[i % SR_NST], (i / SR_NST) & 1u);
+    acc += reinterpret_cast<const double*>(srs + (i % SR_NST) * SR_STAGE)[threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x == 0 && i + SR_NST < n) issue(i + SR_NST);
+  }
+  if (acc == 1.2345e300) sink[0] = acc;  // never true for the calibration data; keeps the loads
+}
+}  // namespace
+
+extern "C" int h2b_stream_read(const void* src, size_t bytes, void* sink_dev, void* stream) {
+  if (!src || !sink_dev || bytes < 16) {
+    h2b_set_error("h2b_stream_read: bad arguments");
+    return H2B_EINVAL;
+  }
+  int dev = 0, sms = 148;
+  H2B_CUDA_TRY(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  H2B_CUDA_TRY(cudaFuncSetAttribute(k_stream_read, cudaFuncAttributeMaxDynamicSharedMemorySize, SR_STAGE * SR_NST));
+  k_stream_read<<<2 * sms, SR_THREADS, SR_STAGE * SR_NST, (cudaStream_t)stream>>>((const char*)src, bytes,
+                                                                                  (double*)sink_dev);
+  H2B_CHECK_LAUNCH();
+  return H2B_OK;
+}
+
+// A one-thread kernel that keeps `stream` busy for `ns` nanoseconds (globaltimer): bench.py
+// enqueues it before a timed step's start event so that the host-side launch latency of the
+// step overlaps it and the event pair brackets the device work alone.
+namespace {
+__global__ void k_spin_ns(uint64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+}  // namespace
+
+extern "C" int h2b_spin_ns(uint64_t ns, void* stream) {
+  k_spin_ns<<<1, 1, 0, (cudaStream_t)stream>>>(ns);
+  H2B_CHECK_LAUNCH();
+  return H2B_OK;
+}
