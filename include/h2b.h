@@ -236,6 +236,21 @@ int h2b_stream_read(const void* src, size_t bytes, void* sink_dev, void* stream)
 /* Keeps `stream` busy for `ns` nanoseconds (one thread polling %globaltimer): enqueued before a
  * timed region's start event so that host-side launch latency does not count as device time. */
 int h2b_spin_ns(uint64_t ns, void* stream);
+/* Stage II of the H² builder on the device: nested bases, transfers and
+ * couplings from the Stage-I grouped factors (the reference's build_all_cluster_ab output) of a
+ * packed block structure.  Results stay on the device until fetched: h2b_builder_ranks (k per
+ * cluster), h2b_builder_fetch (0: leaf bases, 1: transfers, 2: couplings, concatenated in packed
+ * / CSR order).  Gram matrices up to 80 x 80 (leaf size, k_lo + k_hi). */
+int h2b_builder_create(int P, int depth, const int32_t* level_ptr, const int32_t* c_start,
+                       const int32_t* c_size, const int32_t* c_child_lo, const int32_t* c_child_hi,
+                       const int32_t* c_parent, const int32_t* s1_rank, const int64_t* s1_a_off,
+                       const void* s1_a, const int64_t* s1_m_off, const void* s1_m,
+                       const int64_t* s1_b_off, const void* s1_b, const int64_t* s1_part_ptr,
+                       const int32_t* s1_partner, const int64_t* s1_prow, const int64_t* s_row_ptr,
+                       const int32_t* s_col, double eps_acc, int device, void** builder);
+int h2b_builder_ranks(void* builder, int32_t* ranks);
+int h2b_builder_fetch(void* builder, int what, const int32_t* c_child_lo, void* dst);
+int h2b_builder_destroy(void* builder);
 int64_t h2b_gmres_state_elems(int m);
 int h2b_gmres_givens(void* state, int m, int j, const void* hvals_dev, double* host_res, void* stream);
 int h2b_zscale_dev(void* w, int64_t n, const void* scale_dev, void* stream);

@@ -1,0 +1,594 @@
+// Stage II of the H² builder on the device (first step): nested cluster bases,
+// transfer matrices and couplings from the Stage-I grouped factors.
+//
+// Restates the reference's build_bases / build_coupling (/root/reference/pkg/src/h2vie/
+// build.py:228-309) with linalg.trunc_eig_hermitian (linalg.py:207-231):
+//   * cluster c's Gram matrix G_c = Σ_j X_j M_j X_j^H over the Stage-I factors j of c and of its
+//     ancestors (build.py:_gram_terms), X_j = A_j restricted to c's rows for a leaf, and the
+//     children-projected [V_lo^H A_j|lo ; V_hi^H A_j|hi] for a non-leaf (basis.apply_vh), M_j =
+//     B_j^T conj(B_j); G_c <- (G_c + G_c^H) / 2;
+//   * its accuracy-truncated eigendecomposition: the k leading eigenvectors with
+//     sqrt(lambda / lambda_1) > eps_acc — the leaf basis V_c, or the transfers [T_lo; T_hi];
+//   * couplings S_{t,s} = (V_t^H A_t)(V_s^H B_t|s)^T (build.py:build_coupling).
+// The Hermitian eigenproblem is a parallel cyclic Jacobi in one CTA (tournament ordering: all
+// m/2 rotations of a round at once; complex rotations reduced to real ones by a phase),
+// matrix and eigenvectors in shared memory (m <= 80).  The flattened bases V_c (n_c x k_c,
+// V_c = [V_lo T_lo ; V_hi T_hi]) are kept in HBM, so every projection is one small product.
+// Eigenvectors are unique only up to phase (and rotations inside degenerate eigenspaces), so the
+// bases differ from the reference's by unitary factors; the operator V_t S V_s^T is the same up
+// to the truncation tolerance, which is what the tests check (dense operator, reference matvec).
+#include <math.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "h2b_common.cuh"
+
+namespace {
+
+constexpr int BT = 256;     // threads per builder CTA
+constexpr int JMAX = 80;    // largest Gram matrix (leaf size or k_lo + k_hi)
+constexpr int JSMEM = 2 * JMAX * (JMAX + 1) * 16 + 8 * JMAX * 16;
+
+struct BTerm {             // one Stage-I factor feeding a cluster's Gram matrix
+  int64_t a_off;           // element offset of A_j's first row restricted to the cluster
+  int64_t m_off;           // element offset of M_j = B_j^T conj(B_j) (r x r)
+  int32_t r, pad;          // rank of the factor
+};
+struct BClu {              // one cluster of a level step
+  int32_t c, m, n, leaf;   // packed index, Gram size, points, leaf flag
+  int32_t t_first, nt;     // terms
+  int32_t lo, hi;          // children (packed) or -1
+  int32_t klo, khi, pad0, pad1;
+  int64_t x_off;           // scratch (m x rmax) for X and Y
+  int64_t out_off;         // result slot (m x m): eigenvectors, sorted, leading k columns used
+};
+
+// G (m x m) in smem <- Σ_terms X M X^H, X computed into global scratch
+__device__ void gram(const BClu& C, const BTerm* terms, const double2* __restrict__ A, const double2* __restrict__ Mb,
+                     const double2* __restrict__ Vf, const int64_t* __restrict__ vf_off, const int32_t* c_size,
+                     double2* scratch, double2 (*G)[JMAX + 1], int lda_unused) {
+  (void)lda_unused;
+  const int tid = threadIdx.x, m = C.m;
+  for (int e = tid; e < m * m; e += BT) G[e / m][e % m] = make_double2(0.0, 0.0);
+  __syncthreads();
+  for (int ti = 0; ti < C.nt; ++ti) {
+    const BTerm T = terms[C.t_first + ti];
+    const int r = T.r;
+    const double2* Aj = A + T.a_off;  // rows of the cluster, r columns (row-major, ld r)
+    double2* X = scratch + C.x_off;     // m x r
+    double2* Y = X + (int64_t)m * r;    // m x r
+    if (C.leaf) {
+      for (int e = tid; e < m * r; e += BT) X[e] = Aj[e];
+    } else {
+      // X = [Vf_lo^H A|lo ; Vf_hi^H A|hi]
+      const int nlo = c_size[C.lo];
+      for (int e = tid; e < m * r; e += BT) {
+        const int i = e / r, j = e % r;
+        const bool lo = i < C.klo;
+        const int ch = lo ? C.lo : C.hi, ii = lo ? i : i - C.klo, kk = lo ? C.klo : C.khi;
+        const int nch = c_size[ch], r0 = lo ? 0 : nlo;
+        const double2* V = Vf + vf_off[ch];  // nch x kk
+        double2 s = make_double2(0.0, 0.0);
+        for (int p = 0; p < nch; ++p) cfma_conj(s, V[(int64_t)p * kk + ii], Aj[(int64_t)(r0 + p) * r + j]);
+        X[e] = s;
+      }
+    }
+    __syncthreads();
+    // Y = X M
+    const double2* Mj = Mb + T.m_off;
+    for (int e = tid; e < m * r; e += BT) {
+      const int i = e / r, j = e % r;
+      double2 s = make_double2(0.0, 0.0);
+      for (int l = 0; l < r; ++l) cfma(s, X[(int64_t)i * r + l], Mj[(int64_t)l * r + j]);
+      Y[e] = s;
+    }
+    __syncthreads();
+    // G += Y X^H
+    for (int e = tid; e < m * m; e += BT) {
+      const int i = e / m, j = e % m;
+      double2 s = make_double2(0.0, 0.0);
+      for (int l = 0; l < r; ++l) cfma_conj(s, X[(int64_t)j * r + l], Y[(int64_t)i * r + l]);  // Y[i,l] conj(X[j,l])
+      G[i][j] = cadd(G[i][j], s);
+    }
+    __syncthreads();
+  }
+  // symmetrise: G <- (G + G^H) / 2
+  for (int e = tid; e < m * m; e += BT) {
+    const int i = e / m, j = e % m;
+    if (i < j) {
+      const double2 a = G[i][j], b = G[j][i];
+      const double2 h = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+      G[i][j] = h;
+      G[j][i] = make_double2(h.x, -h.y);
+    } else if (i == j) {
+      G[i][i].y = 0.0;
+    }
+  }
+  __syncthreads();
+}
+
+// one level step: Gram, Jacobi eigendecomposition, sorted eigenvectors and rank
+__global__ void __launch_bounds__(BT, 1) k_stage2_level(const BClu* __restrict__ clus, const BTerm* __restrict__ terms,
+                                                        const double2* __restrict__ A, const double2* __restrict__ Mb,
+                                                        const double2* __restrict__ Vf, const int64_t* __restrict__ vf_off,
+                                                        const int32_t* __restrict__ c_size, double2* scratch,
+                                                        double2* out, int32_t* rank_out, double eps_acc) {
+  extern __shared__ __align__(16) double2 bsm[];
+  auto G = reinterpret_cast<double2(*)[JMAX + 1]>(bsm);
+  auto E = reinterpret_cast<double2(*)[JMAX + 1]>(bsm + JMAX * (JMAX + 1));  // eigenvectors
+  double2* rot = bsm + 2 * JMAX * (JMAX + 1);  // per pair: {c, s}, {e^{-i phi}}
+  __shared__ int pp[JMAX / 2], qq[JMAX / 2];
+  __shared__ double lam[JMAX];
+  __shared__ int order[JMAX];
+  __shared__ double offn, totn;
+  const BClu C = clus[blockIdx.x];
+  const int tid = threadIdx.x, m = C.m;
+  if (C.nt == 0 || m == 0) {
+    if (tid == 0) rank_out[C.c] = 0;
+    return;
+  }
+  gram(C, terms, A, Mb, Vf, vf_off, c_size, scratch, G, 0);
+  for (int e = tid; e < m * m; e += BT) E[e / m][e % m] = make_double2(e / m == e % m ? 1.0 : 0.0, 0.0);
+  const int me = m + (m & 1);  // even tournament size (a dummy index pairs with the odd one out)
+  __syncthreads();
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    // convergence: off-diagonal norm vs total
+    if (tid == 0) {
+      offn = 0.0;
+      totn = 0.0;
+    }
+    __syncthreads();
+    double o = 0.0, t = 0.0;
+    for (int e = tid; e < m * m; e += BT) {
+      const double2 v = G[e / m][e % m];
+      const double a2 = v.x * v.x + v.y * v.y;
+      t += a2;
+      if (e / m != e % m) o += a2;
+    }
+    atomicAdd(&offn, o);
+    atomicAdd(&totn, t);
+    __syncthreads();
+    if (!(offn > 1e-32 * totn)) break;
+    for (int round = 0; round < me - 1; ++round) {
+      // tournament pairs: position 0 fixed, the others rotate
+      if (tid < me / 2) {
+        auto at = [&](int pos) { return pos == 0 ? 0 : 1 + (pos - 1 + round) % (me - 1); };
+        int p = at(tid), q = at(me - 1 - tid);
+        if (p > q) { const int w = p; p = q; q = w; }
+        pp[tid] = p;
+        qq[tid] = q;
+        double c = 1.0, s = 0.0, er = 1.0, ei = 0.0;
+        if (q < m) {
+          const double2 b = G[p][q];
+          const double ab = hypot(b.x, b.y);
+          if (ab > 1e-300) {
+            const double a = G[p][p].x, d = G[q][q].x;
+            const double tau = (d - a) / (2.0 * ab);
+            const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            c = 1.0 / sqrt(1.0 + tt * tt);
+            s = tt * c;
+            er = b.x / ab;   // e^{-i phi} = conj(b) / |b|
+            ei = -b.y / ab;
+          }
+        }
+        rot[2 * tid] = make_double2(c, s);
+        rot[2 * tid + 1] = make_double2(er, ei);
+      }
+      __syncthreads();
+      // columns: G <- G J, E <- E J with J = [[c, s], [-s e, c e]], e = e^{-i phi}
+      for (int w = tid; w < (me / 2) * m; w += BT) {
+        const int i = w / m, r = w % m;
+        const int p = pp[i], q = qq[i];
+        if (q >= m) continue;
+        const double c = rot[2 * i].x, s = rot[2 * i].y;
+        const double2 e = rot[2 * i + 1];
+        const double2 j10 = make_double2(-s * e.x, -s * e.y), j11 = make_double2(c * e.x, c * e.y);
+#pragma unroll
+        for (int mat = 0; mat < 2; ++mat) {
+          double2 (*Mx)[JMAX + 1] = mat == 0 ? G : E;
+          const double2 gp = Mx[r][p], gq = Mx[r][q];
+          double2 np_ = make_double2(c * gp.x, c * gp.y), nq = make_double2(s * gp.x, s * gp.y);
+          cfma(np_, gq, j10);
+          cfma(nq, gq, j11);
+          Mx[r][p] = np_;
+          Mx[r][q] = nq;
+        }
+      }
+      __syncthreads();
+      // rows: G <- J^H G
+      for (int w = tid; w < (me / 2) * m; w += BT) {
+        const int i = w / m, col = w % m;
+        const int p = pp[i], q = qq[i];
+        if (q >= m) continue;
+        const double c = rot[2 * i].x, s = rot[2 * i].y;
+        const double2 e = rot[2 * i + 1];
+        const double2 cj10 = make_double2(-s * e.x, s * e.y), cj11 = make_double2(c * e.x, -c * e.y);  // conj
+        const double2 gp = G[p][col], gq = G[q][col];
+        double2 np_ = make_double2(c * gp.x, c * gp.y), nq = make_double2(s * gp.x, s * gp.y);
+        cfma(np_, cj10, gq);
+        cfma(nq, cj11, gq);
+        G[p][col] = np_;
+        G[q][col] = nq;
+      }
+      __syncthreads();
+    }
+  }
+  // eigenvalues, descending order, truncation rank
+  for (int i = tid; i < m; i += BT) lam[i] = fmax(G[i][i].x, 0.0);
+  __syncthreads();
+  for (int i = tid; i < m; i += BT) {
+    int rk = 0;
+    for (int j = 0; j < m; ++j) rk += (lam[j] > lam[i]) || (lam[j] == lam[i] && j < i);
+    order[rk] = i;
+  }
+  __syncthreads();
+  __shared__ int s_k;
+  if (tid == 0) {
+    const double l1 = lam[order[0]];
+    int k = 0;
+    if (l1 > 0.0)
+      for (int i = 0; i < m; ++i) k += sqrt(lam[order[i]] / l1) > eps_acc;
+    s_k = k;
+    rank_out[C.c] = k;
+  }
+  __syncthreads();
+  // the leading k eigenvectors, row-major m x k
+  const int k = s_k;
+  double2* o = out + C.out_off;
+  for (int e = tid; e < m * k; e += BT) o[e] = E[e / k][order[e % k]];
+}
+
+// flattened bases of one level: leaf V_c = p; non-leaf V_c = [Vf_lo T_lo ; Vf_hi T_hi]
+__global__ void k_stage2_flatten(const BClu* __restrict__ clus, const double2* __restrict__ out,
+                                 const int32_t* __restrict__ rank, const int32_t* __restrict__ c_size,
+                                 double2* Vf, const int64_t* __restrict__ vf_off) {
+  const BClu C = clus[blockIdx.x];
+  const int k = rank[C.c];
+  if (k == 0 || C.nt == 0) return;
+  const double2* p = out + C.out_off;  // m x k
+  double2* V = Vf + vf_off[C.c];       // n x k
+  if (C.leaf) {
+    for (int e = threadIdx.x; e < C.n * k; e += blockDim.x) V[e] = p[e];
+    return;
+  }
+  const int nlo = c_size[C.lo];
+  for (int e = threadIdx.x; e < C.n * k; e += blockDim.x) {
+    const int row = e / k, j = e % k;
+    const bool lo = row < nlo;
+    const int ch = lo ? C.lo : C.hi, kk = lo ? C.klo : C.khi, r0 = lo ? 0 : C.klo;
+    const int rr = lo ? row : row - nlo;
+    const double2* Vc = Vf + vf_off[ch];
+    double2 s = make_double2(0.0, 0.0);
+    for (int l = 0; l < kk; ++l) cfma(s, Vc[(int64_t)rr * kk + l], p[(int64_t)(r0 + l) * k + j]);
+    V[e] = s;
+  }
+}
+
+struct SBlk {               // one admissible block (t, s)
+  int32_t t, s, kt, ks;
+  int32_t r, nt_, ns, pad;
+  int64_t a_off;            // A_t (n_t x r)
+  int64_t b_off;            // B_t rows of s (n_s x r)
+  int64_t out_off;          // S (kt x ks)
+};
+
+// S = (Vf_t^H A_t)(Vf_s^H B_t|s)^T; one CTA per block, P and Q in shared memory
+__global__ void k_stage2_couple(const SBlk* __restrict__ blks, const double2* __restrict__ A,
+                                const double2* __restrict__ B, const double2* __restrict__ Vf,
+                                const int64_t* __restrict__ vf_off, double2* S) {
+  extern __shared__ __align__(16) double2 csm[];
+  const SBlk b = blks[blockIdx.x];
+  const int kt = b.kt, ks = b.ks, r = b.r;
+  if (kt == 0 || ks == 0) return;
+  double2* P = csm;              // kt x r
+  double2* Q = csm + kt * r;     // ks x r
+  const double2* Vt = Vf + vf_off[b.t];
+  const double2* Vs = Vf + vf_off[b.s];
+  for (int e = threadIdx.x; e < kt * r; e += blockDim.x) {
+    const int i = e / r, j = e % r;
+    double2 s = make_double2(0.0, 0.0);
+    for (int p = 0; p < b.nt_; ++p) cfma_conj(s, Vt[(int64_t)p * kt + i], A[b.a_off + (int64_t)p * r + j]);
+    P[e] = s;
+  }
+  for (int e = threadIdx.x; e < ks * r; e += blockDim.x) {
+    const int i = e / r, j = e % r;
+    double2 s = make_double2(0.0, 0.0);
+    for (int p = 0; p < b.ns; ++p) cfma_conj(s, Vs[(int64_t)p * ks + i], B[b.b_off + (int64_t)p * r + j]);
+    Q[e] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kt * ks; e += blockDim.x) {
+    const int i = e / ks, j = e % ks;
+    double2 s = make_double2(0.0, 0.0);
+    for (int l = 0; l < r; ++l) cfma(s, P[i * r + l], Q[j * r + l]);
+    S[b.out_off + e] = s;
+  }
+}
+
+template <typename T>
+int up(T** d, const T* h, size_t n) {
+  H2B_CUDA_TRY(cudaMalloc((void**)d, sizeof(T) * std::max<size_t>(n, 1)));
+  if (n) H2B_CUDA_TRY(cudaMemcpy(*d, h, sizeof(T) * n, cudaMemcpyHostToDevice));
+  return H2B_OK;
+}
+
+}  // namespace
+
+struct h2b_builder_ctx {
+  int P = 0, device = 0;
+  std::vector<int32_t> rank;
+  std::vector<int64_t> res_off;   // per cluster: result slot (V for leaves, T for non-leaves)
+  std::vector<int64_t> s_off;     // per admissible block
+  double2 *res = nullptr, *S = nullptr;
+  std::vector<int32_t> m_of;      // Gram size per cluster
+};
+
+// Stage II on the device.  Inputs (host, packed order): the tree tables, the Stage-I factors
+// (A_c, M_c = B_c^T conj(B_c), B_c with its partners' row offsets) and the admissible blocks in
+// CSR by target (s_row_ptr / s_col).  Outputs stay on the device until fetched.
+extern "C" int h2b_builder_create(int P, int depth, const int32_t* level_ptr, const int32_t* c_start,
+                                  const int32_t* c_size, const int32_t* c_child_lo, const int32_t* c_child_hi,
+                                  const int32_t* c_parent, const int32_t* s1_rank, const int64_t* s1_a_off,
+                                  const void* s1_a, const int64_t* s1_m_off, const void* s1_m,
+                                  const int64_t* s1_b_off, const void* s1_b, const int64_t* s1_part_ptr,
+                                  const int32_t* s1_partner, const int64_t* s1_prow, const int64_t* s_row_ptr,
+                                  const int32_t* s_col, double eps_acc, int device, void** out) {
+  if (!level_ptr || !c_start || !c_size || !c_child_lo || !c_child_hi || !c_parent || !s1_rank || !out || P < 1) {
+    h2b_set_error("h2b_builder_create: null argument");
+    return H2B_EINVAL;
+  }
+  *out = nullptr;
+  H2B_CUDA_TRY(cudaSetDevice(device));
+  h2b_builder_ctx* B = new h2b_builder_ctx();
+  B->P = P;
+  B->device = device;
+  B->rank.assign(P, 0);
+  B->m_of.assign(P, 0);
+  B->res_off.assign(P + 1, 0);
+  // device copies of the Stage-I factors and tables
+  const int64_t na = s1_a_off[P], nm = s1_m_off[P], nb = s1_b_off[P];
+  double2 *dA = nullptr, *dM = nullptr, *dB = nullptr, *Vf = nullptr, *scratch = nullptr;
+  int32_t *dsize = nullptr, *drank = nullptr;
+  int64_t* dvf = nullptr;
+  int rc = up(&dA, (const double2*)s1_a, (size_t)na);
+  if (!rc) rc = up(&dM, (const double2*)s1_m, (size_t)nm);
+  if (!rc) rc = up(&dB, (const double2*)s1_b, (size_t)nb);
+  if (!rc) rc = up(&dsize, c_size, (size_t)P);
+  if (!rc) rc = up(&drank, B->rank.data(), (size_t)P);
+  std::vector<int64_t> vf_off(P + 1, 0);
+  // flattened bases: sized per level as ranks become known (upper bound: n_c x m_c)
+  int64_t vf_cap = 0;
+  for (int p = 0; p < P; ++p) vf_cap += (int64_t)c_size[p] * std::min<int64_t>(c_size[p], JMAX);
+  if (!rc) {
+    const cudaError_t e = cudaMalloc(&Vf, sizeof(double2) * std::max<int64_t>(vf_cap, 1));
+    if (e != cudaSuccess) rc = H2B_ENOMEM;
+  }
+  if (!rc) rc = up(&dvf, vf_off.data(), (size_t)P + 1);
+  int64_t res_total = 0;
+  if (!rc) H2B_CUDA_TRY(cudaFuncSetAttribute(k_stage2_level, cudaFuncAttributeMaxDynamicSharedMemorySize, JSMEM));
+  // level by level, bottom-up
+  int64_t vf_used = 0;
+  std::vector<double2*> res_parts;
+  for (int l = depth - 1; l >= 0 && !rc; --l) {
+    std::vector<BClu> clus;
+    std::vector<BTerm> terms;
+    int64_t x_total = 0, o_total = 0;
+    for (int c = level_ptr[l]; c < level_ptr[l + 1]; ++c) {
+      BClu C{};
+      C.c = c;
+      C.n = c_size[c];
+      C.leaf = c_child_lo[c] < 0;
+      C.lo = c_child_lo[c];
+      C.hi = c_child_hi[c];
+      C.klo = C.leaf ? 0 : B->rank[C.lo];
+      C.khi = C.leaf ? 0 : B->rank[C.hi];
+      C.m = C.leaf ? C.n : C.klo + C.khi;
+      if (C.m > JMAX) {
+        h2b_set_error("h2b_builder_create: a Gram matrix exceeds " + std::to_string(JMAX) +
+                      " (leaf size or k_lo + k_hi): not supported by the device Stage II yet");
+        rc = H2B_EINVAL;
+        break;
+      }
+      C.t_first = (int)terms.size();
+      int rmax = 0;
+      for (int j = c; j >= 0; j = c_parent[j]) {  // the cluster itself, then its ancestors
+        if (s1_rank[j] <= 0) continue;
+        BTerm T{};
+        T.r = s1_rank[j];
+        T.a_off = s1_a_off[j] + (int64_t)(c_start[c] - c_start[j]) * T.r;
+        T.m_off = s1_m_off[j];
+        terms.push_back(T);
+        rmax = std::max(rmax, T.r);
+      }
+      C.nt = (int)terms.size() - C.t_first;
+      if (C.m == 0) C.nt = 0;
+      C.x_off = x_total;
+      x_total += 2 * (int64_t)C.m * rmax;
+      C.out_off = o_total;
+      o_total += (int64_t)C.m * C.m;
+      B->m_of[c] = C.m;
+      clus.push_back(C);
+    }
+    if (rc) break;
+    BClu* dclus = nullptr;
+    BTerm* dterms = nullptr;
+    double2* res = nullptr;
+    rc = up(&dclus, clus.data(), clus.size());
+    if (!rc) rc = up(&dterms, terms.data(), terms.size());
+    if (!rc) {
+      cudaError_t e1 = cudaMalloc(&scratch, sizeof(double2) * std::max<int64_t>(x_total, 1));
+      cudaError_t e2 = cudaMalloc(&res, sizeof(double2) * std::max<int64_t>(o_total, 1));
+      if (e1 != cudaSuccess || e2 != cudaSuccess) rc = H2B_ENOMEM;
+    }
+    if (!rc) {
+      k_stage2_level<<<(int)clus.size(), BT, JSMEM>>>(dclus, dterms, dA, dM, Vf, dvf, dsize, scratch, res, drank,
+                                                      eps_acc);
+      cudaError_t e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) {
+        h2b_set_error(std::string("h2b_builder_create: level kernel: ") + cudaGetErrorString(e));
+        rc = H2B_ECUDA;
+      }
+    }
+    if (!rc) {
+      H2B_CUDA_TRY(cudaMemcpy(B->rank.data(), drank, sizeof(int32_t) * P, cudaMemcpyDeviceToHost));
+      for (const BClu& C : clus) {
+        vf_off[C.c] = vf_used;
+        vf_used += (int64_t)C.n * B->rank[C.c];
+      }
+      if (vf_used > vf_cap) {
+        h2b_set_error("h2b_builder_create: flattened bases exceed their allocation");
+        rc = H2B_EINVAL;
+      }
+    }
+    if (!rc) {
+      H2B_CUDA_TRY(cudaMemcpy(dvf, vf_off.data(), sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice));
+      k_stage2_flatten<<<(int)clus.size(), 256>>>(dclus, res, drank, dsize, Vf, dvf);
+      cudaError_t e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) {
+        h2b_set_error(std::string("h2b_builder_create: flatten: ") + cudaGetErrorString(e));
+        rc = H2B_ECUDA;
+      }
+    }
+    // keep this level's results (eigenvector slots, m x m each) for the fetch
+    if (!rc) {
+      for (const BClu& C : clus) B->res_off[C.c] = res_total + C.out_off;
+      res_total += o_total;
+      res_parts.push_back(res);
+    } else if (res) {
+      cudaFree(res);
+    }
+    if (scratch) cudaFree(scratch);
+    scratch = nullptr;
+    if (dclus) cudaFree(dclus);
+    if (dterms) cudaFree(dterms);
+  }
+  // gather the per-level result slots into one buffer (offsets in res_off)
+  if (!rc) {
+    H2B_CUDA_TRY(cudaMalloc(&B->res, sizeof(double2) * std::max<int64_t>(res_total, 1)));
+    int64_t o = 0;
+    int li = 0;
+    for (int l = depth - 1; l >= 0 && li < (int)res_parts.size(); --l, ++li) {
+      int64_t sz = 0;
+      for (int c = level_ptr[l]; c < level_ptr[l + 1]; ++c) sz += (int64_t)B->m_of[c] * B->m_of[c];
+      H2B_CUDA_TRY(cudaMemcpy(B->res + o, res_parts[li], sizeof(double2) * sz, cudaMemcpyDeviceToDevice));
+      o += sz;
+    }
+  }
+  for (double2* p : res_parts) cudaFree(p);
+  // couplings
+  if (!rc) {
+    std::vector<SBlk> blks;
+    B->s_off.assign((size_t)s_row_ptr[P] + 1, 0);
+    int64_t st = 0;
+    int smax = 16;
+    for (int t = 0; t < P; ++t)
+      for (int64_t b = s_row_ptr[t]; b < s_row_ptr[t + 1]; ++b) {
+        const int s = s_col[b];
+        SBlk K{};
+        K.t = t;
+        K.s = s;
+        K.kt = B->rank[t];
+        K.ks = B->rank[s];
+        K.r = s1_rank[t];
+        K.nt_ = c_size[t];
+        K.ns = c_size[s];
+        K.a_off = s1_a_off[t];
+        int64_t prow = -1;
+        for (int64_t j = s1_part_ptr[t]; j < s1_part_ptr[t + 1]; ++j)
+          if (s1_partner[j] == s) prow = s1_prow[j];
+        if (prow < 0 && K.kt > 0 && K.ks > 0) {
+          h2b_set_error("h2b_builder_create: admissible block without its Stage-I partner");
+          rc = H2B_EINVAL;
+        }
+        K.b_off = s1_b_off[t] + std::max<int64_t>(prow, 0) * K.r;
+        K.out_off = st;
+        B->s_off[(size_t)b] = st;
+        st += (int64_t)K.kt * K.ks;
+        smax = std::max(smax, 16 * (K.kt + K.ks) * std::max(K.r, 1));
+        blks.push_back(K);
+      }
+    B->s_off[(size_t)s_row_ptr[P]] = st;
+    SBlk* dblk = nullptr;
+    if (!rc) rc = up(&dblk, blks.data(), blks.size());
+    if (!rc) {
+      H2B_CUDA_TRY(cudaMalloc(&B->S, sizeof(double2) * std::max<int64_t>(st, 1)));
+      if (!blks.empty()) {
+        H2B_CUDA_TRY(cudaFuncSetAttribute(k_stage2_couple, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          std::min(smax, 200 * 1024)));
+        if (smax > 200 * 1024) {
+          h2b_set_error("h2b_builder_create: coupling factors exceed shared memory");
+          rc = H2B_EINVAL;
+        } else {
+          k_stage2_couple<<<(int)blks.size(), 256, smax>>>(dblk, dA, dB, Vf, dvf, B->S);
+          cudaError_t e = cudaGetLastError();
+          if (e == cudaSuccess) e = cudaDeviceSynchronize();
+          if (e != cudaSuccess) {
+            h2b_set_error(std::string("h2b_builder_create: couplings: ") + cudaGetErrorString(e));
+            rc = H2B_ECUDA;
+          }
+        }
+      }
+    }
+    if (dblk) cudaFree(dblk);
+  }
+  void* ptrs[] = {dA, dM, dB, dsize, drank, dvf, Vf};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (rc) {
+    if (B->res) cudaFree(B->res);
+    if (B->S) cudaFree(B->S);
+    delete B;
+    return rc;
+  }
+  *out = B;
+  return H2B_OK;
+}
+
+extern "C" int h2b_builder_ranks(void* b, int32_t* k) {
+  h2b_builder_ctx* B = (h2b_builder_ctx*)b;
+  if (!B || !k) {
+    h2b_set_error("h2b_builder_ranks: null argument");
+    return H2B_EINVAL;
+  }
+  std::copy(B->rank.begin(), B->rank.end(), k);
+  return H2B_OK;
+}
+
+// what 0: leaf bases V_c (n_c x k_c) for every leaf, in packed order, concatenated;
+//      1: transfers [T_lo; T_hi] ((k_lo + k_hi) x k_c) for every non-leaf, concatenated;
+//      2: couplings S (k_t x k_s) in the CSR order of the admissible blocks.
+// dst: host buffer of the concatenated size (complex128); c_child_lo: leaf test.
+extern "C" int h2b_builder_fetch(void* b, int what, const int32_t* c_child_lo, void* dst) {
+  h2b_builder_ctx* B = (h2b_builder_ctx*)b;
+  if (!B || !dst || (what != 2 && !c_child_lo)) {
+    h2b_set_error("h2b_builder_fetch: null argument");
+    return H2B_EINVAL;
+  }
+  H2B_CUDA_TRY(cudaSetDevice(B->device));
+  double2* o = (double2*)dst;
+  if (what == 2) {
+    H2B_CUDA_TRY(cudaMemcpy(o, B->S, sizeof(double2) * B->s_off.back(), cudaMemcpyDeviceToHost));
+    return H2B_OK;
+  }
+  for (int c = 0; c < B->P; ++c) {
+    const bool leaf = c_child_lo[c] < 0;
+    if ((what == 0) != leaf) continue;
+    const int64_t e = (int64_t)B->m_of[c] * B->rank[c];
+    if (e) H2B_CUDA_TRY(cudaMemcpy(o, B->res + B->res_off[c], sizeof(double2) * e, cudaMemcpyDeviceToHost));
+    o += e;
+  }
+  return H2B_OK;
+}
+
+extern "C" int h2b_builder_destroy(void* b) {
+  h2b_builder_ctx* B = (h2b_builder_ctx*)b;
+  if (!B) return H2B_OK;
+  cudaSetDevice(B->device);
+  if (B->res) cudaFree(B->res);
+  if (B->S) cudaFree(B->S);
+  delete B;
+  return H2B_OK;
+}
