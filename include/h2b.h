@@ -251,6 +251,16 @@ int h2b_builder_create(int P, int depth, const int32_t* level_ptr, const int32_t
 int h2b_builder_ranks(void* builder, int32_t* ranks);
 int h2b_builder_fetch(void* builder, int what, const int32_t* c_child_lo, void* dst);
 int h2b_builder_destroy(void* builder);
+/* Stage I on the device: partially pivoted ACA of every cluster's grouped admissible block row
+ * (the reference's aca_factorize, entries sampled from the voxel geometry), one CTA per cluster;
+ * outputs the factor offsets and partner lists, h2b_stage1_fetch copies A / B / B^T conj(B). */
+int h2b_stage1_run(int P, const int32_t* c_start, const int32_t* c_size, const int64_t* perm, int64_t n,
+                   const int64_t* s_row_ptr, const int32_t* s_col, const double* centers, const void* chi,
+                   double k0, double volume, double eps_aca, int max_rank, int device, int32_t* rank_out,
+                   int64_t* a_off, int64_t* b_off, int64_t* m_off, int64_t* part_ptr, int32_t* partner,
+                   int64_t* prow, void** stage1);
+int h2b_stage1_fetch(void* stage1, void* a, void* b, void* m);
+int h2b_stage1_destroy(void* stage1);
 int64_t h2b_gmres_state_elems(int m);
 int h2b_gmres_givens(void* state, int m, int j, const void* hvals_dev, double* host_res, void* stream);
 int h2b_zscale_dev(void* w, int64_t n, const void* scale_dev, void* stream);

@@ -89,3 +89,47 @@ def build_stage2(pk: PackedH2, stage1: dict, eps_acc: float, device: int = 0) ->
     meta = dict(pk.meta, built_on_device=True, eps_acc=float(eps_acc))
     return dataclasses.replace(pk, c_rank=k.astype(pk.c_rank.dtype), c_xhat_off=xoff, c_v_off=c_v_off,
                                c_t_off=c_t_off, s_off=s_off, vbuf=vbuf, tbuf=tbuf, sbuf=sbuf, meta=meta)
+
+
+def stage1_device(pk: PackedH2, centers, chi, k0: float, volume: float, eps_aca: float, max_rank: int = 200,
+                  device: int = 0) -> dict:
+    """Stage I on the device: the ACA factors of every cluster's grouped admissible block row
+    (csrc/h2b_build.cu: ``h2b_stage1_run``, restating linalg.aca_factorize), as the dict
+    `build_stage2` takes.  ``centers`` (N x 3) and ``chi`` (N) in the original point order."""
+    L = _abi.lib()
+    if not L.h2b_device_ok(int(device)):
+        raise RuntimeError("no sm_100 (B200) CUDA device visible; the builder has no CPU fallback")
+    P = pk.num_clusters
+    nb = int(pk.s_row_ptr[-1])
+    keep = dict(c_start=np.ascontiguousarray(pk.c_start, np.int32), c_size=np.ascontiguousarray(pk.c_size, np.int32),
+                perm=np.ascontiguousarray(pk.perm, np.int64), s_row_ptr=np.ascontiguousarray(pk.s_row_ptr, np.int64),
+                s_col=np.ascontiguousarray(pk.s_col, np.int32),
+                centers=np.ascontiguousarray(centers, np.float64), chi=np.ascontiguousarray(chi, np.complex128),
+                rank=np.zeros(P, np.int32), a_off=np.zeros(P + 1, np.int64), b_off=np.zeros(P + 1, np.int64),
+                m_off=np.zeros(P + 1, np.int64), part_ptr=np.zeros(P + 1, np.int64),
+                partner=np.zeros(max(nb, 1), np.int32), prow=np.zeros(max(nb, 1), np.int64))
+    p = {k: v.ctypes.data for k, v in keep.items()}
+    h = C.c_void_p()
+    _abi.check(L.h2b_stage1_run(P, p["c_start"], p["c_size"], p["perm"], int(pk.n), p["s_row_ptr"], p["s_col"],
+                                p["centers"], p["chi"], float(k0), float(volume), float(eps_aca), int(max_rank),
+                                int(device), p["rank"], p["a_off"], p["b_off"], p["m_off"], p["part_ptr"],
+                                p["partner"], p["prow"], C.byref(h)), "h2b_stage1_run")
+    try:
+        A = np.empty(int(keep["a_off"][-1]), np.complex128)
+        B = np.empty(int(keep["b_off"][-1]), np.complex128)
+        M = np.empty(int(keep["m_off"][-1]), np.complex128)
+        _abi.check(L.h2b_stage1_fetch(h, A.ctypes.data, B.ctypes.data, M.ctypes.data), "h2b_stage1_fetch")
+    finally:
+        L.h2b_stage1_destroy(h)
+    return dict(s1_rank=keep["rank"], s1_a=A, s1_a_off=keep["a_off"], s1_b=B, s1_b_off=keep["b_off"], s1_m=M,
+                s1_m_off=keep["m_off"], s1_part_ptr=keep["part_ptr"], s1_partner=keep["partner"][:nb],
+                s1_prow=keep["prow"][:nb])
+
+
+def build_device(pk: PackedH2, centers, chi, k0: float, volume: float, eps_aca: float, eps_acc: float,
+                 max_rank: int = 200, device: int = 0) -> PackedH2:
+    """The far field of ``pk``'s block structure built on the device: Stage I (ACA) then Stage II
+    (bases, transfers, couplings).  The near-field payload of ``pk`` is kept (or, when it is empty,
+    sampled from the geometry on the device by `H2Operator`)."""
+    s1 = stage1_device(pk, centers, chi, k0, volume, eps_aca, max_rank, device)
+    return build_stage2(pk, s1, eps_acc, device)

@@ -592,3 +592,410 @@ extern "C" int h2b_builder_destroy(void* b) {
   delete B;
   return H2B_OK;
 }
+
+// =================================================================================================
+// Stage I on the device: partially pivoted adaptive cross approximation of every cluster's
+// grouped admissible block row (the cluster's points x all its partners' points), restating
+// linalg.aca_factorize (/root/reference/pkg/src/h2vie/linalg.py:87-178) with the reference's
+// pivoting, Frobenius estimate and stopping rule; entries sampled on the fly from the geometry
+// (kernel.py:190-210: S[m, n] = -chi_n (k0^2 V / 4 pi r) e^{-j k0 r}, admissible blocks never
+// hold the diagonal).  One CTA per cluster.  The SVD trim of the reference (recompress_lowrank)
+// is skipped: the Gram matrices and couplings of Stage II depend on the block A B^T only, and
+// Stage II's truncated eigendecomposition trims at eps_acc.
+// =================================================================================================
+namespace {
+
+constexpr int AT = 256;
+
+struct ACAClu {
+  int32_t c, nr, ncols, cap;
+  int64_t cols_off;   // into the column index list (original point indices, partners in CSR order)
+  int64_t ws_a, ws_b; // workspace: a (nr x cap), b (ncols x cap), row-major
+  int64_t ws_f;       // flags: used rows (nr) then used cols (ncols), one byte each
+};
+
+__device__ __forceinline__ double2 sys_entry(int64_t m, int64_t n, const double* __restrict__ ctr,
+                                             const double2* __restrict__ chi, double k0, double coef) {
+  const double dx = ctr[3 * m] - ctr[3 * n], dy = ctr[3 * m + 1] - ctr[3 * n + 1], dz = ctr[3 * m + 2] - ctr[3 * n + 2];
+  const double r = sqrt(dx * dx + dy * dy + dz * dz);
+  const double amp = coef / r;
+  double sn, cs;
+  sincos(k0 * r, &sn, &cs);
+  const double ar = amp * cs, ai = -(amp * sn);
+  const double2 cn = chi[n];
+  return make_double2(-(cn.x * ar - cn.y * ai), -(cn.x * ai + cn.y * ar));
+}
+
+// block-wide argmax of v (value, index), ties to the lowest index (np.argmax)
+__device__ void bmax(double v, int i, double* sv, int* si, double* out_v, int* out_i) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_down_sync(0xffffffffu, v, o);
+    const int i2 = __shfl_down_sync(0xffffffffu, i, o);
+    if (v2 > v || (v2 == v && i2 < i)) { v = v2; i = i2; }
+  }
+  if (lane == 0) { sv[w] = v; si[w] = i; }
+  __syncthreads();
+  if (tid == 0) {
+    double bv = sv[0];
+    int bi = si[0];
+    for (int k = 1; k < AT / 32; ++k)
+      if (sv[k] > bv || (sv[k] == bv && si[k] < bi)) { bv = sv[k]; bi = si[k]; }
+    *out_v = bv;
+    *out_i = bi;
+  }
+  __syncthreads();
+}
+
+__device__ double bsum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < AT / 32; ++k) s += red[k];
+    red[AT / 32] = s;
+  }
+  __syncthreads();
+  s = red[AT / 32];
+  __syncthreads();
+  return s;
+}
+
+__global__ void __launch_bounds__(AT) k_aca(const ACAClu* __restrict__ clus, const int32_t* __restrict__ c_start,
+                                            const int64_t* __restrict__ perm, const int64_t* __restrict__ cols_all,
+                                            const double* __restrict__ ctr, const double2* __restrict__ chi, double k0,
+                                            double coef, double eps_aca, double2* ws, unsigned char* flags,
+                                            int32_t* rank_out, int32_t* err) {
+  __shared__ double sv[AT / 32 + 1];
+  __shared__ int si[AT / 32];
+  __shared__ double s_v;
+  __shared__ int s_i, s_next, s_stop;
+  __shared__ double2 s_piv;
+  __shared__ double2 dots[2][128];
+  const ACAClu C = clus[blockIdx.x];
+  const int tid = threadIdx.x, nr = C.nr, nc = C.ncols, cap = C.cap;
+  const int64_t r0 = c_start[C.c];
+  const int64_t* cols = cols_all + C.cols_off;
+  double2* a = ws + C.ws_a;
+  double2* b = ws + C.ws_b;
+  unsigned char* ur = flags + C.ws_f;
+  unsigned char* uc = ur + nr;
+  for (int i = tid; i < nr; i += AT) ur[i] = 0;
+  for (int j = tid; j < nc; j += AT) uc[j] = 0;
+  if (tid == 0) { s_next = 0; s_stop = 0; }
+  __syncthreads();
+  const int full = min(nr, nc);
+  double fro2 = 0.0;
+  int k = 0;
+  for (;;) {
+    // residual row at the pivot row, skipping rows that are already resolved
+    bool found = false;
+    while (s_next >= 0) {
+      const int i = s_next;
+      if (tid == 0) ur[i] = 1;
+      const int64_t m = perm[r0 + i];
+      double best = -1.0;
+      int bj = 0x7fffffff;
+      for (int j = tid; j < nc; j += AT) {
+        double2 r = make_double2(0.0, 0.0);
+        if (!uc[j]) {
+          r = sys_entry(m, cols[j], ctr, chi, k0, coef);
+          for (int l = 0; l < k; ++l) {  // r -= a_l[i] b_l[j]
+            const double2 al = a[(int64_t)i * cap + l], bl = b[(int64_t)j * cap + l];
+            r.x -= al.x * bl.x - al.y * bl.y;
+            r.y -= al.x * bl.y + al.y * bl.x;
+          }
+        }
+        b[(int64_t)j * cap + k] = r;  // the candidate row, scaled below
+        const double ab = hypot(r.x, r.y);
+        if (ab > best) { best = ab; bj = j; }
+      }
+      bmax(best, bj, sv, si, &s_v, &s_i);
+      if (s_v > 0.0) { found = true; break; }
+      if (tid == 0) {  // first free row, or none
+        int nx = -1;
+        for (int q = 0; q < nr; ++q)
+          if (!ur[q]) { nx = q; break; }
+        s_next = nx;
+      }
+      __syncthreads();
+    }
+    if (!found) break;
+    const int i = s_next, j = s_i;
+    if (tid == 0) { s_piv = b[(int64_t)j * cap + k]; uc[j] = 1; }
+    __syncthreads();
+    const double2 pv = s_piv;
+    const double pn = pv.x * pv.x + pv.y * pv.y;
+    double nb2 = 0.0;
+    for (int q = tid; q < nc; q += AT) {  // b_new = row / pivot
+      const double2 r = b[(int64_t)q * cap + k];
+      const double2 v = make_double2((r.x * pv.x + r.y * pv.y) / pn, (r.y * pv.x - r.x * pv.y) / pn);
+      b[(int64_t)q * cap + k] = v;
+      nb2 += v.x * v.x + v.y * v.y;
+    }
+    const int64_t nj = cols[j];
+    double na2 = 0.0;
+    for (int q = tid; q < nr; q += AT) {  // a_new = column j - sum b_l[j] a_l
+      double2 c = sys_entry(perm[r0 + q], nj, ctr, chi, k0, coef);
+      for (int l = 0; l < k; ++l) {
+        const double2 bl = b[(int64_t)j * cap + l], al = a[(int64_t)q * cap + l];
+        c.x -= bl.x * al.x - bl.y * al.y;
+        c.y -= bl.x * al.y + bl.y * al.x;
+      }
+      a[(int64_t)q * cap + k] = c;
+      na2 += c.x * c.x + c.y * c.y;
+    }
+    __syncthreads();
+    nb2 = bsum(nb2, sv);
+    na2 = bsum(na2, sv);
+    // cross = sum_l Re(<a_l, a_new> <b_l, b_new>), l = 0 .. k-1 (k < cap <= 128)
+    for (int l = tid; l < k; l += AT) {
+      double2 da = make_double2(0.0, 0.0), db = da;
+      for (int q = 0; q < nr; ++q) cfma_conj(da, a[(int64_t)q * cap + l], a[(int64_t)q * cap + k]);
+      for (int q = 0; q < nc; ++q) cfma_conj(db, b[(int64_t)q * cap + l], b[(int64_t)q * cap + k]);
+      dots[0][l] = da;
+      dots[1][l] = db;
+    }
+    __syncthreads();
+    double cross = 0.0;
+    if (tid == 0) {
+      for (int l = 0; l < k; ++l) {
+        const double2 da = dots[0][l], db = dots[1][l];
+        cross += da.x * db.x - da.y * db.y;
+      }
+      double f2 = fro2 + na2 * nb2 + 2.0 * cross;
+      f2 = f2 > 0.0 ? f2 : 0.0;
+      if (na2 * nb2 <= eps_aca * eps_aca * f2) {
+        s_stop = 1;  // converged: the terminating cross is dropped
+      } else {
+        fro2 = f2;
+        s_stop = 0;
+      }
+    }
+    __syncthreads();
+    if (s_stop) break;
+    ++k;
+    if (k >= full) break;
+    if (k >= cap) {
+      if (tid == 0) atomicExch(err, C.c + 1);
+      break;
+    }
+    // next pivot row: the largest |a_new| over unused rows, else the first free row
+    double best = -1.0;
+    int bi = 0x7fffffff;
+    for (int q = tid; q < nr; q += AT) {
+      const double2 v = a[(int64_t)q * cap + k - 1];
+      const double ab = ur[q] ? 0.0 : hypot(v.x, v.y);
+      if (ab > best || (ab == best && q < bi)) { best = ab; bi = q; }
+    }
+    bmax(best, bi, sv, si, &s_v, &s_i);
+    if (tid == 0) {
+      if (s_v > 0.0) {
+        s_next = s_i;
+      } else {
+        int nx = -1;
+        for (int q = 0; q < nr; ++q)
+          if (!ur[q]) { nx = q; break; }
+        s_next = nx;
+      }
+    }
+    __syncthreads();
+    if (s_next < 0) break;
+  }
+  if (tid == 0) rank_out[C.c] = k;
+}
+
+}  // namespace
+
+namespace {
+// compacted Stage-I factors of one cluster: A (nr x r), B (ncols x r), M = B^T conj(B) (r x r)
+__global__ void k_stage1_pack(const ACAClu* __restrict__ clus, const int32_t* __restrict__ rank,
+                              const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off,
+                              const int64_t* __restrict__ m_off, const double2* __restrict__ ws, double2* A,
+                              double2* B, double2* M) {
+  const ACAClu C = clus[blockIdx.x];
+  const int r = rank[C.c], cap = C.cap;
+  if (r == 0) return;
+  const double2* a = ws + C.ws_a;
+  const double2* b = ws + C.ws_b;
+  for (int e = threadIdx.x; e < C.nr * r; e += blockDim.x) A[a_off[C.c] + e] = a[(int64_t)(e / r) * cap + e % r];
+  for (int e = threadIdx.x; e < C.ncols * r; e += blockDim.x) B[b_off[C.c] + e] = b[(int64_t)(e / r) * cap + e % r];
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+    const int i = e / r, j = e % r;
+    double2 s = make_double2(0.0, 0.0);
+    for (int q = 0; q < C.ncols; ++q) cfma_conj(s, b[(int64_t)q * cap + j], b[(int64_t)q * cap + i]);  // B[q,i] conj(B[q,j])
+    M[m_off[C.c] + e] = s;
+  }
+}
+}  // namespace
+
+struct h2b_stage1_ctx {
+  int P = 0, device = 0;
+  double2 *A = nullptr, *B = nullptr, *M = nullptr;
+  int64_t na = 0, nb = 0, nm = 0;
+};
+
+// Stage I on the device for the admissible block structure (s_row_ptr / s_col, packed CSR) of a
+// cluster tree (c_start / c_size, perm) over a voxel geometry.  Outputs: per-cluster ACA rank,
+// the offsets of the compacted factors (a_off / b_off / m_off, P + 1 each), the partner lists in
+// CSR order with each partner's first row in B (part_ptr P + 1, partner / prow one per block);
+// the factors themselves via h2b_stage1_fetch.
+extern "C" int h2b_stage1_run(int P, const int32_t* c_start, const int32_t* c_size, const int64_t* perm, int64_t n,
+                              const int64_t* s_row_ptr, const int32_t* s_col, const double* centers, const void* chi,
+                              double k0, double volume, double eps_aca, int max_rank, int device, int32_t* rank_out,
+                              int64_t* a_off, int64_t* b_off, int64_t* m_off, int64_t* part_ptr, int32_t* partner,
+                              int64_t* prow, void** out) {
+  if (!c_start || !c_size || !perm || !s_row_ptr || !centers || !chi || !rank_out || !out || P < 1) {
+    h2b_set_error("h2b_stage1_run: null argument");
+    return H2B_EINVAL;
+  }
+  *out = nullptr;
+  H2B_CUDA_TRY(cudaSetDevice(device));
+  std::vector<ACAClu> clus;
+  std::vector<int64_t> cols;
+  int64_t ws = 0, fl = 0;
+  part_ptr[0] = 0;
+  for (int c = 0; c < P; ++c) {
+    int64_t nc = 0;
+    for (int64_t b = s_row_ptr[c]; b < s_row_ptr[c + 1]; ++b) {
+      const int s = s_col[b];
+      partner[b] = s;
+      prow[b] = nc;
+      nc += c_size[s];
+    }
+    part_ptr[c + 1] = s_row_ptr[c + 1];
+    if (nc == 0) continue;
+    ACAClu C{};
+    C.c = c;
+    C.nr = c_size[c];
+    C.ncols = (int32_t)nc;
+    C.cap = (int32_t)std::min<int64_t>(std::min<int64_t>(max_rank, 128), std::min<int64_t>(C.nr, nc));
+    C.cols_off = (int64_t)cols.size();
+    for (int64_t b = s_row_ptr[c]; b < s_row_ptr[c + 1]; ++b) {
+      const int s = s_col[b];
+      for (int q = 0; q < c_size[s]; ++q) cols.push_back(perm[c_start[s] + q]);
+    }
+    C.ws_a = ws;
+    ws += (int64_t)C.nr * C.cap;
+    C.ws_b = ws;
+    ws += nc * C.cap;
+    C.ws_f = fl;
+    fl += C.nr + nc;
+    clus.push_back(C);
+  }
+  h2b_stage1_ctx* S = new h2b_stage1_ctx();
+  S->P = P;
+  S->device = device;
+  ACAClu* dclus = nullptr;
+  int32_t *dstart = nullptr, *drank = nullptr, *derr = nullptr;
+  int64_t *dperm = nullptr, *dcols = nullptr, *dao = nullptr, *dbo = nullptr, *dmo = nullptr;
+  double* dctr = nullptr;
+  double2 *dchi = nullptr, *dws = nullptr;
+  unsigned char* dfl = nullptr;
+  std::vector<int32_t> zeros(P, 0);
+  int rc = up(&dclus, clus.data(), clus.size());
+  if (!rc) rc = up(&dstart, c_start, (size_t)P);
+  if (!rc) rc = up(&dperm, perm, (size_t)n);
+  if (!rc) rc = up(&dcols, cols.data(), cols.size());
+  if (!rc) rc = up(&dctr, centers, (size_t)(3 * n));
+  if (!rc) rc = up(&dchi, (const double2*)chi, (size_t)n);
+  if (!rc) rc = up(&drank, zeros.data(), (size_t)P);
+  if (!rc) rc = up(&derr, zeros.data(), 1);
+  if (!rc) {
+    cudaError_t e1 = cudaMalloc(&dws, sizeof(double2) * std::max<int64_t>(ws, 1));
+    cudaError_t e2 = cudaMalloc(&dfl, std::max<int64_t>(fl, 1));
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+      h2b_set_error("h2b_stage1_run: workspace allocation failed");
+      rc = H2B_ENOMEM;
+    }
+  }
+  if (!rc && !clus.empty()) {
+    const double coef = k0 * k0 * volume / (4.0 * 3.14159265358979323846);
+    k_aca<<<(int)clus.size(), AT>>>(dclus, dstart, dperm, dcols, dctr, dchi, k0, coef, eps_aca, dws, dfl, drank, derr);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      h2b_set_error(std::string("h2b_stage1_run: ACA kernel: ") + cudaGetErrorString(e));
+      rc = H2B_ECUDA;
+    }
+  }
+  if (!rc) {
+    int32_t err = 0;
+    H2B_CUDA_TRY(cudaMemcpy(rank_out, drank, sizeof(int32_t) * P, cudaMemcpyDeviceToHost));
+    H2B_CUDA_TRY(cudaMemcpy(&err, derr, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (err) {
+      h2b_set_error("h2b_stage1_run: ACA reached its rank cap at cluster " + std::to_string(err - 1) +
+                    " (the reference raises ClusterCompressionError)");
+      rc = H2B_EINVAL;
+    }
+  }
+  if (!rc) {
+    a_off[0] = b_off[0] = m_off[0] = 0;
+    std::vector<int64_t> ncols(P, 0);
+    for (const ACAClu& C : clus) ncols[C.c] = C.ncols;
+    for (int c = 0; c < P; ++c) {
+      const int64_t r = rank_out[c];
+      a_off[c + 1] = a_off[c] + (int64_t)c_size[c] * r;
+      b_off[c + 1] = b_off[c] + ncols[c] * r;
+      m_off[c + 1] = m_off[c] + r * r;
+    }
+    S->na = a_off[P];
+    S->nb = b_off[P];
+    S->nm = m_off[P];
+    rc = up(&dao, a_off, (size_t)P + 1);
+    if (!rc) rc = up(&dbo, b_off, (size_t)P + 1);
+    if (!rc) rc = up(&dmo, m_off, (size_t)P + 1);
+    if (!rc) {
+      cudaError_t e1 = cudaMalloc(&S->A, sizeof(double2) * std::max<int64_t>(S->na, 1));
+      cudaError_t e2 = cudaMalloc(&S->B, sizeof(double2) * std::max<int64_t>(S->nb, 1));
+      cudaError_t e3 = cudaMalloc(&S->M, sizeof(double2) * std::max<int64_t>(S->nm, 1));
+      if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) rc = H2B_ENOMEM;
+    }
+    if (!rc && !clus.empty()) {
+      k_stage1_pack<<<(int)clus.size(), 256>>>(dclus, drank, dao, dbo, dmo, dws, S->A, S->B, S->M);
+      cudaError_t e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) {
+        h2b_set_error(std::string("h2b_stage1_run: pack: ") + cudaGetErrorString(e));
+        rc = H2B_ECUDA;
+      }
+    }
+  }
+  void* ptrs[] = {dclus, dstart, drank, derr, dperm, dcols, dao, dbo, dmo, dctr, dchi, dws, dfl};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (rc) {
+    if (S->A) cudaFree(S->A);
+    if (S->B) cudaFree(S->B);
+    if (S->M) cudaFree(S->M);
+    delete S;
+    return rc;
+  }
+  *out = S;
+  return H2B_OK;
+}
+
+extern "C" int h2b_stage1_fetch(void* h, void* a, void* b, void* m) {
+  h2b_stage1_ctx* S = (h2b_stage1_ctx*)h;
+  if (!S) {
+    h2b_set_error("h2b_stage1_fetch: null handle");
+    return H2B_EINVAL;
+  }
+  H2B_CUDA_TRY(cudaSetDevice(S->device));
+  if (a && S->na) H2B_CUDA_TRY(cudaMemcpy(a, S->A, sizeof(double2) * S->na, cudaMemcpyDeviceToHost));
+  if (b && S->nb) H2B_CUDA_TRY(cudaMemcpy(b, S->B, sizeof(double2) * S->nb, cudaMemcpyDeviceToHost));
+  if (m && S->nm) H2B_CUDA_TRY(cudaMemcpy(m, S->M, sizeof(double2) * S->nm, cudaMemcpyDeviceToHost));
+  return H2B_OK;
+}
+
+extern "C" int h2b_stage1_destroy(void* h) {
+  h2b_stage1_ctx* S = (h2b_stage1_ctx*)h;
+  if (!S) return H2B_OK;
+  cudaSetDevice(S->device);
+  if (S->A) cudaFree(S->A);
+  if (S->B) cudaFree(S->B);
+  if (S->M) cudaFree(S->M);
+  delete S;
+  return H2B_OK;
+}

@@ -1,0 +1,36 @@
+"""Build the far field of a BASELINE operator's block structure on the B200 (Stage I ACA + Stage II)
+from the voxel geometry, and compare its matvec with the reference-built operator's stored
+outputs.  Usage: python tools/build_device.py cfg2 [cfg1 ...]"""
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1703_01175_b200 import H2Operator  # noqa: E402
+from paper_1703_01175_b200.builder import build_stage2, stage1_device  # noqa: E402
+from paper_1703_01175_b200.nearfield import geometry_arrays  # noqa: E402
+from paper_1703_01175_b200.pack import load_packed  # noqa: E402
+
+for name in sys.argv[1:] or ["cfg2"]:
+    pk, ex = load_packed(os.path.join(ROOT, "fixtures", name + ".npz"), with_extra=True, near_on_host=False)
+    centers, chi, k0, vol = geometry_arrays(pk.meta["geometry"])
+    eps = 1e-4
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s1 = stage1_device(pk, centers, chi, k0, vol, eps)
+    t1 = time.perf_counter()
+    pkd = build_stage2(pk, s1, eps)
+    t2 = time.perf_counter()
+    op = H2Operator(pkd, device=0)
+    errs = [float(np.linalg.norm(op.matvec(ex["x"][:, j]) - ex["y"][:, j]) / np.linalg.norm(ex["y"][:, j]))
+            for j in range(ex["x"].shape[1])]
+    dk = np.abs(pkd.c_rank.astype(int) - pk.c_rank.astype(int))
+    print(f"{name}: N={pk.n} Stage I {t1 - t0:.2f} s (ACA ranks max {int(s1['s1_rank'].max())}), Stage II "
+          f"{t2 - t1:.2f} s; ranks vs reference: {int(np.count_nonzero(dk))} of {pk.num_clusters} differ "
+          f"(max {int(dk.max())}); K {int(pkd.c_rank.sum())} vs {int(pk.c_rank.sum())}; matvec vs the "
+          f"reference-built operator {max(errs):.2e} (eps_acc {eps:g})", flush=True)
+    op.close()

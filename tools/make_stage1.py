@@ -1,4 +1,4 @@
-"""Stage-I factors of the reference builder for the device Stage II — test fixtures.
+"""Stage-I factors of the reference builder (and the geometry) for the device Stage II — test fixtures.
 
 Runs only in the build container (imports the reference).  For each small fixture it rebuilds
 the operator exactly as tools/make_golden.py does and stores, next to the packed reference
@@ -60,7 +60,12 @@ def dump(name, geom, kp, n_min, tol=1e-4):
                  s1_b=np.concatenate(B), s1_b_off=b_off, s1_m=np.concatenate(M), s1_m_off=m_off,
                  s1_part_ptr=part_ptr, s1_partner=np.asarray(partners, np.int32),
                  s1_prow=np.asarray(prow, np.int64), s1_eps_acc=np.float64(cparams.eps_acc),
-                 ref_rank=pk.c_rank.copy(), ref_rep_error=np.float64(np.nan))
+                 ref_rank=pk.c_rank.copy(), s1_eps_aca=np.float64(cparams.eps_aca),
+                 s1_max_rank=np.int64(cparams.max_rank),
+                 # the geometry the entries come from (kernel.py:190-210): a device Stage I samples it
+                 geom_centers=np.ascontiguousarray(geom.centers, np.float64),
+                 geom_chi=np.ascontiguousarray(np.broadcast_to(kp.eps_r, (pk.n,)) - 1.0, np.complex128),
+                 geom_k0=np.float64(kp.k0), geom_volume=np.float64(geom.voxel_volume))
     out = os.path.join(ROOT, "tests", "golden", f"stage1_{name}.npz")
     save_packed(pk, out, extra=extra)
     print(f"{name}: N={pk.n} P={P} Stage-I ranks max {r.max()} -> {out} {os.path.getsize(out) / 1e6:.2f} MB")
