@@ -261,6 +261,9 @@ int h2b_stage1_run(int P, const int32_t* c_start, const int32_t* c_size, const i
                    int64_t* prow, void** stage1);
 int h2b_stage1_fetch(void* stage1, void* a, void* b, void* m);
 int h2b_stage1_destroy(void* stage1);
+/* device pointers of the Stage-I factors A / B / B^T conj(B) (input of h2b_builder_create, which
+ * accepts host or device pointers). */
+int h2b_stage1_device_ptrs(void* stage1, void** a, void** b, void** m);
 int64_t h2b_gmres_state_elems(int m);
 int h2b_gmres_givens(void* state, int m, int j, const void* hvals_dev, double* host_res, void* stream);
 int h2b_zscale_dev(void* w, int64_t n, const void* scale_dev, void* stream);

@@ -41,16 +41,21 @@ def build_stage2(pk: PackedH2, stage1: dict, eps_acc: float, device: int = 0) ->
     def a(name, dtype):
         return np.ascontiguousarray(stage1[name], dtype=dtype)
 
+    dev = stage1.get("s1_device")  # (A, B, M) device pointers of a device Stage I: no host round trip
+    empty = np.zeros(1, np.complex128)
     keep = dict(
         level_ptr=np.ascontiguousarray(pk.level_ptr, np.int32), c_start=np.ascontiguousarray(pk.c_start, np.int32),
         c_size=np.ascontiguousarray(pk.c_size, np.int32), c_lo=np.ascontiguousarray(pk.c_child_lo, np.int32),
         c_hi=np.ascontiguousarray(pk.c_child_hi, np.int32), c_par=np.ascontiguousarray(pk.c_parent, np.int32),
-        r=a("s1_rank", np.int32), a_off=a("s1_a_off", np.int64), A=a("s1_a", np.complex128),
-        m_off=a("s1_m_off", np.int64), M=a("s1_m", np.complex128), b_off=a("s1_b_off", np.int64),
-        B=a("s1_b", np.complex128), pp=a("s1_part_ptr", np.int64), partner=a("s1_partner", np.int32),
+        r=a("s1_rank", np.int32), a_off=a("s1_a_off", np.int64),
+        A=empty if dev else a("s1_a", np.complex128),
+        m_off=a("s1_m_off", np.int64), M=empty if dev else a("s1_m", np.complex128), b_off=a("s1_b_off", np.int64),
+        B=empty if dev else a("s1_b", np.complex128), pp=a("s1_part_ptr", np.int64), partner=a("s1_partner", np.int32),
         prow=a("s1_prow", np.int64), s_row_ptr=np.ascontiguousarray(pk.s_row_ptr, np.int64),
         s_col=np.ascontiguousarray(pk.s_col, np.int32))
     p = {k: v.ctypes.data for k, v in keep.items()}
+    if dev:
+        p["A"], p["B"], p["M"] = dev
     h = C.c_void_p()
     _abi.check(L.h2b_builder_create(P, int(pk.depth), p["level_ptr"], p["c_start"], p["c_size"], p["c_lo"],
                                     p["c_hi"], p["c_par"], p["r"], p["a_off"], p["A"], p["m_off"], p["M"],
@@ -86,13 +91,14 @@ def build_stage2(pk: PackedH2, stage1: dict, eps_acc: float, device: int = 0) ->
         L.h2b_builder_destroy(h)
     xoff = np.zeros(P + 1, np.int64)
     np.cumsum(k, out=xoff[1:])
-    meta = dict(pk.meta, built_on_device=True, eps_acc=float(eps_acc))
+    meta = {k: v for k, v in pk.meta.items() if k != "synthetic"}  # real payloads now
+    meta.update(built_on_device=True, eps_acc=float(eps_acc))
     return dataclasses.replace(pk, c_rank=k.astype(pk.c_rank.dtype), c_xhat_off=xoff, c_v_off=c_v_off,
                                c_t_off=c_t_off, s_off=s_off, vbuf=vbuf, tbuf=tbuf, sbuf=sbuf, meta=meta)
 
 
 def stage1_device(pk: PackedH2, centers, chi, k0: float, volume: float, eps_aca: float, max_rank: int = 200,
-                  device: int = 0) -> dict:
+                  device: int = 0, keep_on_device: bool = False) -> dict:
     """Stage I on the device: the ACA factors of every cluster's grouped admissible block row
     (csrc/h2b_build.cu: ``h2b_stage1_run``, restating linalg.aca_factorize), as the dict
     `build_stage2` takes.  ``centers`` (N x 3) and ``chi`` (N) in the original point order."""
@@ -114,6 +120,13 @@ def stage1_device(pk: PackedH2, centers, chi, k0: float, volume: float, eps_aca:
                                 p["centers"], p["chi"], float(k0), float(volume), float(eps_aca), int(max_rank),
                                 int(device), p["rank"], p["a_off"], p["b_off"], p["m_off"], p["part_ptr"],
                                 p["partner"], p["prow"], C.byref(h)), "h2b_stage1_run")
+    out = dict(s1_rank=keep["rank"], s1_a_off=keep["a_off"], s1_b_off=keep["b_off"], s1_m_off=keep["m_off"],
+               s1_part_ptr=keep["part_ptr"], s1_partner=keep["partner"][:nb], s1_prow=keep["prow"][:nb])
+    if keep_on_device:  # the caller releases the factors with h2b_stage1_destroy(out["s1_handle"])
+        pa, pb, pm = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _abi.check(L.h2b_stage1_device_ptrs(h, C.byref(pa), C.byref(pb), C.byref(pm)), "h2b_stage1_device_ptrs")
+        out.update(s1_device=(pa.value, pb.value, pm.value), s1_handle=h)
+        return out
     try:
         A = np.empty(int(keep["a_off"][-1]), np.complex128)
         B = np.empty(int(keep["b_off"][-1]), np.complex128)
@@ -121,9 +134,8 @@ def stage1_device(pk: PackedH2, centers, chi, k0: float, volume: float, eps_aca:
         _abi.check(L.h2b_stage1_fetch(h, A.ctypes.data, B.ctypes.data, M.ctypes.data), "h2b_stage1_fetch")
     finally:
         L.h2b_stage1_destroy(h)
-    return dict(s1_rank=keep["rank"], s1_a=A, s1_a_off=keep["a_off"], s1_b=B, s1_b_off=keep["b_off"], s1_m=M,
-                s1_m_off=keep["m_off"], s1_part_ptr=keep["part_ptr"], s1_partner=keep["partner"][:nb],
-                s1_prow=keep["prow"][:nb])
+    out.update(s1_a=A, s1_b=B, s1_m=M)
+    return out
 
 
 def build_device(pk: PackedH2, centers, chi, k0: float, volume: float, eps_aca: float, eps_acc: float,
@@ -131,5 +143,8 @@ def build_device(pk: PackedH2, centers, chi, k0: float, volume: float, eps_aca: 
     """The far field of ``pk``'s block structure built on the device: Stage I (ACA) then Stage II
     (bases, transfers, couplings).  The near-field payload of ``pk`` is kept (or, when it is empty,
     sampled from the geometry on the device by `H2Operator`)."""
-    s1 = stage1_device(pk, centers, chi, k0, volume, eps_aca, max_rank, device)
-    return build_stage2(pk, s1, eps_acc, device)
+    s1 = stage1_device(pk, centers, chi, k0, volume, eps_aca, max_rank, device, keep_on_device=True)
+    try:
+        return build_stage2(pk, s1, eps_acc, device)
+    finally:
+        _abi.lib().h2b_stage1_destroy(s1["s1_handle"])

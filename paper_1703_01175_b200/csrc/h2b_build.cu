@@ -30,6 +30,14 @@ constexpr int BT = 256;     // threads per builder CTA
 constexpr int JMAX = 80;    // largest Gram matrix (leaf size or k_lo + k_hi)
 constexpr int JSMEM = 2 * JMAX * (JMAX + 1) * 16 + 8 * JMAX * 16;
 
+constexpr int JBIG = 256;   // largest Gram matrix at all (beyond JMAX: G and eigenvectors in HBM)
+
+struct Mat {               // a matrix in shared or global memory, row stride ld
+  double2* p;
+  int ld;
+  __device__ __forceinline__ double2& operator()(int i, int j) const { return p[(int64_t)i * ld + j]; }
+};
+
 struct BTerm {             // one Stage-I factor feeding a cluster's Gram matrix
   int64_t a_off;           // element offset of A_j's first row restricted to the cluster
   int64_t m_off;           // element offset of M_j = B_j^T conj(B_j) (r x r)
@@ -42,15 +50,15 @@ struct BClu {              // one cluster of a level step
   int32_t klo, khi, pad0, pad1;
   int64_t x_off;           // scratch (m x rmax) for X and Y
   int64_t out_off;         // result slot (m x m): eigenvectors, sorted, leading k columns used
+  int64_t j_off;           // m > JMAX: G and the eigenvectors in HBM (2 m^2 elements), else -1
 };
 
 // G (m x m) in smem <- Σ_terms X M X^H, X computed into global scratch
 __device__ void gram(const BClu& C, const BTerm* terms, const double2* __restrict__ A, const double2* __restrict__ Mb,
                      const double2* __restrict__ Vf, const int64_t* __restrict__ vf_off, const int32_t* c_size,
-                     double2* scratch, double2 (*G)[JMAX + 1], int lda_unused) {
-  (void)lda_unused;
+                     double2* scratch, Mat G) {
   const int tid = threadIdx.x, m = C.m;
-  for (int e = tid; e < m * m; e += BT) G[e / m][e % m] = make_double2(0.0, 0.0);
+  for (int e = tid; e < m * m; e += BT) G(e / m, e % m) = make_double2(0.0, 0.0);
   __syncthreads();
   for (int ti = 0; ti < C.nt; ++ti) {
     const BTerm T = terms[C.t_first + ti];
@@ -89,7 +97,7 @@ __device__ void gram(const BClu& C, const BTerm* terms, const double2* __restric
       const int i = e / m, j = e % m;
       double2 s = make_double2(0.0, 0.0);
       for (int l = 0; l < r; ++l) cfma_conj(s, X[(int64_t)j * r + l], Y[(int64_t)i * r + l]);  // Y[i,l] conj(X[j,l])
-      G[i][j] = cadd(G[i][j], s);
+      G(i, j) = cadd(G(i, j), s);
     }
     __syncthreads();
   }
@@ -97,12 +105,12 @@ __device__ void gram(const BClu& C, const BTerm* terms, const double2* __restric
   for (int e = tid; e < m * m; e += BT) {
     const int i = e / m, j = e % m;
     if (i < j) {
-      const double2 a = G[i][j], b = G[j][i];
+      const double2 a = G(i, j), b = G(j, i);
       const double2 h = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
-      G[i][j] = h;
-      G[j][i] = make_double2(h.x, -h.y);
+      G(i, j) = h;
+      G(j, i) = make_double2(h.x, -h.y);
     } else if (i == j) {
-      G[i][i].y = 0.0;
+      G(i, i).y = 0.0;
     }
   }
   __syncthreads();
@@ -113,23 +121,25 @@ __global__ void __launch_bounds__(BT, 1) k_stage2_level(const BClu* __restrict__
                                                         const double2* __restrict__ A, const double2* __restrict__ Mb,
                                                         const double2* __restrict__ Vf, const int64_t* __restrict__ vf_off,
                                                         const int32_t* __restrict__ c_size, double2* scratch,
-                                                        double2* out, int32_t* rank_out, double eps_acc) {
+                                                        double2* out, int32_t* rank_out, double eps_acc,
+                                                        double2* jwork) {
   extern __shared__ __align__(16) double2 bsm[];
-  auto G = reinterpret_cast<double2(*)[JMAX + 1]>(bsm);
-  auto E = reinterpret_cast<double2(*)[JMAX + 1]>(bsm + JMAX * (JMAX + 1));  // eigenvectors
-  double2* rot = bsm + 2 * JMAX * (JMAX + 1);  // per pair: {c, s}, {e^{-i phi}}
-  __shared__ int pp[JMAX / 2], qq[JMAX / 2];
-  __shared__ double lam[JMAX];
-  __shared__ int order[JMAX];
+  __shared__ double2 rot[JBIG];  // per pair: {c, s}, {e^{-i phi}}
+  __shared__ int pp[JBIG / 2], qq[JBIG / 2];
+  __shared__ double lam[JBIG];
+  __shared__ int order[JBIG];
   __shared__ double offn, totn;
   const BClu C = clus[blockIdx.x];
   const int tid = threadIdx.x, m = C.m;
+  // G and its eigenvectors E: shared memory up to JMAX, else this cluster's HBM slot
+  const Mat G = C.j_off < 0 ? Mat{bsm, JMAX + 1} : Mat{jwork + C.j_off, m};
+  const Mat E = C.j_off < 0 ? Mat{bsm + JMAX * (JMAX + 1), JMAX + 1} : Mat{jwork + C.j_off + (int64_t)m * m, m};
   if (C.nt == 0 || m == 0) {
     if (tid == 0) rank_out[C.c] = 0;
     return;
   }
-  gram(C, terms, A, Mb, Vf, vf_off, c_size, scratch, G, 0);
-  for (int e = tid; e < m * m; e += BT) E[e / m][e % m] = make_double2(e / m == e % m ? 1.0 : 0.0, 0.0);
+  gram(C, terms, A, Mb, Vf, vf_off, c_size, scratch, G);
+  for (int e = tid; e < m * m; e += BT) E(e / m, e % m) = make_double2(e / m == e % m ? 1.0 : 0.0, 0.0);
   const int me = m + (m & 1);  // even tournament size (a dummy index pairs with the odd one out)
   __syncthreads();
   for (int sweep = 0; sweep < 30; ++sweep) {
@@ -141,7 +151,7 @@ __global__ void __launch_bounds__(BT, 1) k_stage2_level(const BClu* __restrict__
     __syncthreads();
     double o = 0.0, t = 0.0;
     for (int e = tid; e < m * m; e += BT) {
-      const double2 v = G[e / m][e % m];
+      const double2 v = G(e / m, e % m);
       const double a2 = v.x * v.x + v.y * v.y;
       t += a2;
       if (e / m != e % m) o += a2;
@@ -160,10 +170,10 @@ __global__ void __launch_bounds__(BT, 1) k_stage2_level(const BClu* __restrict__
         qq[tid] = q;
         double c = 1.0, s = 0.0, er = 1.0, ei = 0.0;
         if (q < m) {
-          const double2 b = G[p][q];
+          const double2 b = G(p, q);
           const double ab = hypot(b.x, b.y);
           if (ab > 1e-300) {
-            const double a = G[p][p].x, d = G[q][q].x;
+            const double a = G(p, p).x, d = G(q, q).x;
             const double tau = (d - a) / (2.0 * ab);
             const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
             c = 1.0 / sqrt(1.0 + tt * tt);
@@ -186,13 +196,13 @@ __global__ void __launch_bounds__(BT, 1) k_stage2_level(const BClu* __restrict__
         const double2 j10 = make_double2(-s * e.x, -s * e.y), j11 = make_double2(c * e.x, c * e.y);
 #pragma unroll
         for (int mat = 0; mat < 2; ++mat) {
-          double2 (*Mx)[JMAX + 1] = mat == 0 ? G : E;
-          const double2 gp = Mx[r][p], gq = Mx[r][q];
+          const Mat Mx = mat == 0 ? G : E;
+          const double2 gp = Mx(r, p), gq = Mx(r, q);
           double2 np_ = make_double2(c * gp.x, c * gp.y), nq = make_double2(s * gp.x, s * gp.y);
           cfma(np_, gq, j10);
           cfma(nq, gq, j11);
-          Mx[r][p] = np_;
-          Mx[r][q] = nq;
+          Mx(r, p) = np_;
+          Mx(r, q) = nq;
         }
       }
       __syncthreads();
@@ -204,18 +214,18 @@ __global__ void __launch_bounds__(BT, 1) k_stage2_level(const BClu* __restrict__
         const double c = rot[2 * i].x, s = rot[2 * i].y;
         const double2 e = rot[2 * i + 1];
         const double2 cj10 = make_double2(-s * e.x, s * e.y), cj11 = make_double2(c * e.x, -c * e.y);  // conj
-        const double2 gp = G[p][col], gq = G[q][col];
+        const double2 gp = G(p, col), gq = G(q, col);
         double2 np_ = make_double2(c * gp.x, c * gp.y), nq = make_double2(s * gp.x, s * gp.y);
         cfma(np_, cj10, gq);
         cfma(nq, cj11, gq);
-        G[p][col] = np_;
-        G[q][col] = nq;
+        G(p, col) = np_;
+        G(q, col) = nq;
       }
       __syncthreads();
     }
   }
   // eigenvalues, descending order, truncation rank
-  for (int i = tid; i < m; i += BT) lam[i] = fmax(G[i][i].x, 0.0);
+  for (int i = tid; i < m; i += BT) lam[i] = fmax(G(i, i).x, 0.0);
   __syncthreads();
   for (int i = tid; i < m; i += BT) {
     int rk = 0;
@@ -236,7 +246,7 @@ __global__ void __launch_bounds__(BT, 1) k_stage2_level(const BClu* __restrict__
   // the leading k eigenvectors, row-major m x k
   const int k = s_k;
   double2* o = out + C.out_off;
-  for (int e = tid; e < m * k; e += BT) o[e] = E[e / k][order[e % k]];
+  for (int e = tid; e < m * k; e += BT) o[e] = E(e / k, order[e % k]);
 }
 
 // flattened bases of one level: leaf V_c = p; non-leaf V_c = [Vf_lo T_lo ; Vf_hi T_hi]
@@ -268,48 +278,65 @@ __global__ void k_stage2_flatten(const BClu* __restrict__ clus, const double2* _
 struct SBlk {               // one admissible block (t, s)
   int32_t t, s, kt, ks;
   int32_t r, nt_, ns, pad;
-  int64_t a_off;            // A_t (n_t x r)
+  int64_t p_off;            // P_t = Vf_t^H A_t (kt x r), shared by t's blocks
   int64_t b_off;            // B_t rows of s (n_s x r)
   int64_t out_off;          // S (kt x ks)
 };
+struct PTgt {              // one target: P_t = Vf_t^H A_t
+  int32_t t, kt, r, nt_;
+  int64_t a_off, p_off;
+};
 
-// S = (Vf_t^H A_t)(Vf_s^H B_t|s)^T; one CTA per block, P and Q in shared memory
-__global__ void k_stage2_couple(const SBlk* __restrict__ blks, const double2* __restrict__ A,
+// P_t = Vf_t^H A_t (kt x r) for every target with couplings
+__global__ void k_stage2_proj(const PTgt* __restrict__ tg, const double2* __restrict__ A, const double2* __restrict__ Vf,
+                              const int64_t* __restrict__ vf_off, double2* Pbuf) {
+  const PTgt T = tg[blockIdx.x];
+  const double2* Vt = Vf + vf_off[T.t];
+  for (int e = threadIdx.x; e < T.kt * T.r; e += blockDim.x) {
+    const int i = e / T.r, j = e % T.r;
+    double2 s = make_double2(0.0, 0.0);
+    for (int p = 0; p < T.nt_; ++p) cfma_conj(s, Vt[(int64_t)p * T.kt + i], A[T.a_off + (int64_t)p * T.r + j]);
+    Pbuf[T.p_off + e] = s;
+  }
+}
+
+// S = P_t (Vf_s^H B_t|s)^T, the inner dimension r in chunks of 32: Q chunk (ks x 32) in shared
+// memory, S accumulated in global memory (each thread owns fixed elements)
+constexpr int QCH = 8;
+__global__ void k_stage2_couple(const SBlk* __restrict__ blks, const double2* __restrict__ Pbuf,
                                 const double2* __restrict__ B, const double2* __restrict__ Vf,
                                 const int64_t* __restrict__ vf_off, double2* S) {
-  extern __shared__ __align__(16) double2 csm[];
+  __shared__ double2 Q[JBIG * QCH];
   const SBlk b = blks[blockIdx.x];
   const int kt = b.kt, ks = b.ks, r = b.r;
   if (kt == 0 || ks == 0) return;
-  double2* P = csm;              // kt x r
-  double2* Q = csm + kt * r;     // ks x r
-  const double2* Vt = Vf + vf_off[b.t];
   const double2* Vs = Vf + vf_off[b.s];
-  for (int e = threadIdx.x; e < kt * r; e += blockDim.x) {
-    const int i = e / r, j = e % r;
-    double2 s = make_double2(0.0, 0.0);
-    for (int p = 0; p < b.nt_; ++p) cfma_conj(s, Vt[(int64_t)p * kt + i], A[b.a_off + (int64_t)p * r + j]);
-    P[e] = s;
-  }
-  for (int e = threadIdx.x; e < ks * r; e += blockDim.x) {
-    const int i = e / r, j = e % r;
-    double2 s = make_double2(0.0, 0.0);
-    for (int p = 0; p < b.ns; ++p) cfma_conj(s, Vs[(int64_t)p * ks + i], B[b.b_off + (int64_t)p * r + j]);
-    Q[e] = s;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < kt * ks; e += blockDim.x) {
-    const int i = e / ks, j = e % ks;
-    double2 s = make_double2(0.0, 0.0);
-    for (int l = 0; l < r; ++l) cfma(s, P[i * r + l], Q[j * r + l]);
-    S[b.out_off + e] = s;
+  const double2* P = Pbuf + b.p_off;
+  double2* So = S + b.out_off;
+  for (int e = threadIdx.x; e < kt * ks; e += blockDim.x) So[e] = make_double2(0.0, 0.0);
+  for (int l0 = 0; l0 < r; l0 += QCH) {
+    const int lc = min(QCH, r - l0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < ks * lc; e += blockDim.x) {
+      const int j = e / lc, l = e % lc;
+      double2 s = make_double2(0.0, 0.0);
+      for (int p = 0; p < b.ns; ++p) cfma_conj(s, Vs[(int64_t)p * ks + j], B[b.b_off + (int64_t)p * r + l0 + l]);
+      Q[j * QCH + l] = s;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kt * ks; e += blockDim.x) {
+      const int i = e / ks, j = e % ks;
+      double2 s = So[e];
+      for (int l = 0; l < lc; ++l) cfma(s, P[(int64_t)i * r + l0 + l], Q[j * QCH + l]);
+      So[e] = s;
+    }
   }
 }
 
 template <typename T>
-int up(T** d, const T* h, size_t n) {
+int up(T** d, const T* h, size_t n) {  // h: host or device memory (unified addressing)
   H2B_CUDA_TRY(cudaMalloc((void**)d, sizeof(T) * std::max<size_t>(n, 1)));
-  if (n) H2B_CUDA_TRY(cudaMemcpy(*d, h, sizeof(T) * n, cudaMemcpyHostToDevice));
+  if (n) H2B_CUDA_TRY(cudaMemcpy(*d, h, sizeof(T) * n, cudaMemcpyDefault));
   return H2B_OK;
 }
 
@@ -359,7 +386,7 @@ extern "C" int h2b_builder_create(int P, int depth, const int32_t* level_ptr, co
   std::vector<int64_t> vf_off(P + 1, 0);
   // flattened bases: sized per level as ranks become known (upper bound: n_c x m_c)
   int64_t vf_cap = 0;
-  for (int p = 0; p < P; ++p) vf_cap += (int64_t)c_size[p] * std::min<int64_t>(c_size[p], JMAX);
+  for (int p = 0; p < P; ++p) vf_cap += (int64_t)c_size[p] * std::min<int64_t>(c_size[p], JBIG);
   if (!rc) {
     const cudaError_t e = cudaMalloc(&Vf, sizeof(double2) * std::max<int64_t>(vf_cap, 1));
     if (e != cudaSuccess) rc = H2B_ENOMEM;
@@ -373,7 +400,8 @@ extern "C" int h2b_builder_create(int P, int depth, const int32_t* level_ptr, co
   for (int l = depth - 1; l >= 0 && !rc; --l) {
     std::vector<BClu> clus;
     std::vector<BTerm> terms;
-    int64_t x_total = 0, o_total = 0;
+    int64_t x_total = 0, o_total = 0, j_total = 0;
+    double2* jwork = nullptr;
     for (int c = level_ptr[l]; c < level_ptr[l + 1]; ++c) {
       BClu C{};
       C.c = c;
@@ -384,11 +412,16 @@ extern "C" int h2b_builder_create(int P, int depth, const int32_t* level_ptr, co
       C.klo = C.leaf ? 0 : B->rank[C.lo];
       C.khi = C.leaf ? 0 : B->rank[C.hi];
       C.m = C.leaf ? C.n : C.klo + C.khi;
-      if (C.m > JMAX) {
-        h2b_set_error("h2b_builder_create: a Gram matrix exceeds " + std::to_string(JMAX) +
-                      " (leaf size or k_lo + k_hi): not supported by the device Stage II yet");
+      if (C.m > JBIG) {
+        h2b_set_error("h2b_builder_create: a Gram matrix exceeds " + std::to_string(JBIG) +
+                      " (leaf size or k_lo + k_hi): not supported by the device Stage II");
         rc = H2B_EINVAL;
         break;
+      }
+      C.j_off = -1;
+      if (C.m > JMAX) {
+        C.j_off = j_total;
+        j_total += 2 * (int64_t)C.m * C.m;
       }
       C.t_first = (int)terms.size();
       int rmax = 0;
@@ -419,11 +452,12 @@ extern "C" int h2b_builder_create(int P, int depth, const int32_t* level_ptr, co
     if (!rc) {
       cudaError_t e1 = cudaMalloc(&scratch, sizeof(double2) * std::max<int64_t>(x_total, 1));
       cudaError_t e2 = cudaMalloc(&res, sizeof(double2) * std::max<int64_t>(o_total, 1));
-      if (e1 != cudaSuccess || e2 != cudaSuccess) rc = H2B_ENOMEM;
+      cudaError_t e3 = cudaMalloc(&jwork, sizeof(double2) * std::max<int64_t>(j_total, 1));
+      if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) rc = H2B_ENOMEM;
     }
     if (!rc) {
       k_stage2_level<<<(int)clus.size(), BT, JSMEM>>>(dclus, dterms, dA, dM, Vf, dvf, dsize, scratch, res, drank,
-                                                      eps_acc);
+                                                      eps_acc, jwork);
       cudaError_t e = cudaGetLastError();
       if (e == cudaSuccess) e = cudaDeviceSynchronize();
       if (e != cudaSuccess) {
@@ -462,6 +496,7 @@ extern "C" int h2b_builder_create(int P, int depth, const int32_t* level_ptr, co
     }
     if (scratch) cudaFree(scratch);
     scratch = nullptr;
+    if (jwork) cudaFree(jwork);
     if (dclus) cudaFree(dclus);
     if (dterms) cudaFree(dterms);
   }
@@ -478,12 +513,21 @@ extern "C" int h2b_builder_create(int P, int depth, const int32_t* level_ptr, co
     }
   }
   for (double2* p : res_parts) cudaFree(p);
-  // couplings
+  // couplings: P_t once per target, then one CTA per block
   if (!rc) {
     std::vector<SBlk> blks;
+    std::vector<PTgt> tgs;
+    std::vector<int64_t> p_of(P, -1);
+    int64_t ptot = 0;
+    for (int t = 0; t < P; ++t) {
+      if (s_row_ptr[t + 1] == s_row_ptr[t] || B->rank[t] == 0 || s1_rank[t] == 0) continue;
+      PTgt T{t, B->rank[t], s1_rank[t], c_size[t], s1_a_off[t], ptot};
+      p_of[t] = ptot;
+      ptot += (int64_t)T.kt * T.r;
+      tgs.push_back(T);
+    }
     B->s_off.assign((size_t)s_row_ptr[P] + 1, 0);
     int64_t st = 0;
-    int smax = 16;
     for (int t = 0; t < P; ++t)
       for (int64_t b = s_row_ptr[t]; b < s_row_ptr[t + 1]; ++b) {
         const int s = s_col[b];
@@ -495,11 +539,11 @@ extern "C" int h2b_builder_create(int P, int depth, const int32_t* level_ptr, co
         K.r = s1_rank[t];
         K.nt_ = c_size[t];
         K.ns = c_size[s];
-        K.a_off = s1_a_off[t];
+        K.p_off = std::max<int64_t>(p_of[t], 0);
         int64_t prow = -1;
         for (int64_t j = s1_part_ptr[t]; j < s1_part_ptr[t + 1]; ++j)
           if (s1_partner[j] == s) prow = s1_prow[j];
-        if (prow < 0 && K.kt > 0 && K.ks > 0) {
+        if (prow < 0 && K.kt > 0 && K.ks > 0 && K.r > 0) {
           h2b_set_error("h2b_builder_create: admissible block without its Stage-I partner");
           rc = H2B_EINVAL;
         }
@@ -507,32 +551,50 @@ extern "C" int h2b_builder_create(int P, int depth, const int32_t* level_ptr, co
         K.out_off = st;
         B->s_off[(size_t)b] = st;
         st += (int64_t)K.kt * K.ks;
-        smax = std::max(smax, 16 * (K.kt + K.ks) * std::max(K.r, 1));
         blks.push_back(K);
       }
     B->s_off[(size_t)s_row_ptr[P]] = st;
     SBlk* dblk = nullptr;
+    PTgt* dtg = nullptr;
+    double2* dP = nullptr;
     if (!rc) rc = up(&dblk, blks.data(), blks.size());
+    if (!rc) rc = up(&dtg, tgs.data(), tgs.size());
     if (!rc) {
-      H2B_CUDA_TRY(cudaMalloc(&B->S, sizeof(double2) * std::max<int64_t>(st, 1)));
-      if (!blks.empty()) {
-        H2B_CUDA_TRY(cudaFuncSetAttribute(k_stage2_couple, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          std::min(smax, 200 * 1024)));
-        if (smax > 200 * 1024) {
-          h2b_set_error("h2b_builder_create: coupling factors exceed shared memory");
-          rc = H2B_EINVAL;
-        } else {
-          k_stage2_couple<<<(int)blks.size(), 256, smax>>>(dblk, dA, dB, Vf, dvf, B->S);
-          cudaError_t e = cudaGetLastError();
-          if (e == cudaSuccess) e = cudaDeviceSynchronize();
-          if (e != cudaSuccess) {
-            h2b_set_error(std::string("h2b_builder_create: couplings: ") + cudaGetErrorString(e));
-            rc = H2B_ECUDA;
-          }
+      cudaError_t e1 = cudaMalloc(&B->S, sizeof(double2) * std::max<int64_t>(st, 1));
+      cudaError_t e2 = cudaMalloc(&dP, sizeof(double2) * std::max<int64_t>(ptot, 1));
+      if (e1 != cudaSuccess || e2 != cudaSuccess) rc = H2B_ENOMEM;
+    }
+    if (!rc) H2B_CUDA_TRY(cudaMemset(B->S, 0, sizeof(double2) * std::max<int64_t>(st, 1)));
+    if (!rc && !tgs.empty()) {
+      k_stage2_proj<<<(int)tgs.size(), 256>>>(dtg, dA, Vf, dvf, dP);
+      cudaError_t e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) {
+        h2b_set_error(std::string("h2b_builder_create: projections: ") + cudaGetErrorString(e));
+        rc = H2B_ECUDA;
+      }
+    }
+    // blocks whose target has no Stage-I factor keep S = 0 (the reference's zero coupling)
+    if (!rc) {
+      std::vector<SBlk> live;
+      for (const SBlk& K : blks)
+        if (K.r > 0 && p_of[K.t] >= 0 && K.kt > 0 && K.ks > 0) live.push_back(K);
+      if (dblk) cudaFree(dblk);
+      dblk = nullptr;
+      rc = up(&dblk, live.data(), live.size());
+      if (!rc && !live.empty()) {
+        k_stage2_couple<<<(int)live.size(), 256>>>(dblk, dP, dB, Vf, dvf, B->S);
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) {
+          h2b_set_error(std::string("h2b_builder_create: couplings: ") + cudaGetErrorString(e));
+          rc = H2B_ECUDA;
         }
       }
     }
     if (dblk) cudaFree(dblk);
+    if (dtg) cudaFree(dtg);
+    if (dP) cudaFree(dP);
   }
   void* ptrs[] = {dA, dM, dB, dsize, drank, dvf, Vf};
   for (void* p : ptrs)
@@ -672,7 +734,7 @@ __global__ void __launch_bounds__(AT) k_aca(const ACAClu* __restrict__ clus, con
   __shared__ double s_v;
   __shared__ int s_i, s_next, s_stop;
   __shared__ double2 s_piv;
-  __shared__ double2 dots[2][128];
+  __shared__ double2 dots[2][200];
   const ACAClu C = clus[blockIdx.x];
   const int tid = threadIdx.x, nr = C.nr, nc = C.ncols, cap = C.cap;
   const int64_t r0 = c_start[C.c];
@@ -722,7 +784,7 @@ __global__ void __launch_bounds__(AT) k_aca(const ACAClu* __restrict__ clus, con
       __syncthreads();
     }
     if (!found) break;
-    const int i = s_next, j = s_i;
+    const int j = s_i;
     if (tid == 0) { s_piv = b[(int64_t)j * cap + k]; uc[j] = 1; }
     __syncthreads();
     const double2 pv = s_piv;
@@ -749,7 +811,7 @@ __global__ void __launch_bounds__(AT) k_aca(const ACAClu* __restrict__ clus, con
     __syncthreads();
     nb2 = bsum(nb2, sv);
     na2 = bsum(na2, sv);
-    // cross = sum_l Re(<a_l, a_new> <b_l, b_new>), l = 0 .. k-1 (k < cap <= 128)
+    // cross = sum_l Re(<a_l, a_new> <b_l, b_new>), l = 0 .. k-1 (k < cap <= 200)
     for (int l = tid; l < k; l += AT) {
       double2 da = make_double2(0.0, 0.0), db = da;
       for (int q = 0; q < nr; ++q) cfma_conj(da, a[(int64_t)q * cap + l], a[(int64_t)q * cap + k]);
@@ -852,117 +914,173 @@ extern "C" int h2b_stage1_run(int P, const int32_t* c_start, const int32_t* c_si
   }
   *out = nullptr;
   H2B_CUDA_TRY(cudaSetDevice(device));
-  std::vector<ACAClu> clus;
-  std::vector<int64_t> cols;
-  int64_t ws = 0, fl = 0;
+  // partner lists (CSR order) and each partner's first row in the grouped B
+  std::vector<int64_t> ncols(P, 0);
   part_ptr[0] = 0;
   for (int c = 0; c < P; ++c) {
     int64_t nc = 0;
     for (int64_t b = s_row_ptr[c]; b < s_row_ptr[c + 1]; ++b) {
-      const int s = s_col[b];
-      partner[b] = s;
+      partner[b] = s_col[b];
       prow[b] = nc;
-      nc += c_size[s];
+      nc += c_size[s_col[b]];
     }
+    ncols[c] = nc;
     part_ptr[c + 1] = s_row_ptr[c + 1];
-    if (nc == 0) continue;
-    ACAClu C{};
-    C.c = c;
-    C.nr = c_size[c];
-    C.ncols = (int32_t)nc;
-    C.cap = (int32_t)std::min<int64_t>(std::min<int64_t>(max_rank, 128), std::min<int64_t>(C.nr, nc));
-    C.cols_off = (int64_t)cols.size();
-    for (int64_t b = s_row_ptr[c]; b < s_row_ptr[c + 1]; ++b) {
-      const int s = s_col[b];
-      for (int q = 0; q < c_size[s]; ++q) cols.push_back(perm[c_start[s] + q]);
-    }
-    C.ws_a = ws;
-    ws += (int64_t)C.nr * C.cap;
-    C.ws_b = ws;
-    ws += nc * C.cap;
-    C.ws_f = fl;
-    fl += C.nr + nc;
-    clus.push_back(C);
   }
   h2b_stage1_ctx* S = new h2b_stage1_ctx();
   S->P = P;
   S->device = device;
-  ACAClu* dclus = nullptr;
   int32_t *dstart = nullptr, *drank = nullptr, *derr = nullptr;
-  int64_t *dperm = nullptr, *dcols = nullptr, *dao = nullptr, *dbo = nullptr, *dmo = nullptr;
+  int64_t* dperm = nullptr;
   double* dctr = nullptr;
-  double2 *dchi = nullptr, *dws = nullptr;
-  unsigned char* dfl = nullptr;
+  double2* dchi = nullptr;
   std::vector<int32_t> zeros(P, 0);
-  int rc = up(&dclus, clus.data(), clus.size());
-  if (!rc) rc = up(&dstart, c_start, (size_t)P);
+  int rc = up(&dstart, c_start, (size_t)P);
   if (!rc) rc = up(&dperm, perm, (size_t)n);
-  if (!rc) rc = up(&dcols, cols.data(), cols.size());
   if (!rc) rc = up(&dctr, centers, (size_t)(3 * n));
   if (!rc) rc = up(&dchi, (const double2*)chi, (size_t)n);
   if (!rc) rc = up(&drank, zeros.data(), (size_t)P);
   if (!rc) rc = up(&derr, zeros.data(), 1);
-  if (!rc) {
-    cudaError_t e1 = cudaMalloc(&dws, sizeof(double2) * std::max<int64_t>(ws, 1));
-    cudaError_t e2 = cudaMalloc(&dfl, std::max<int64_t>(fl, 1));
-    if (e1 != cudaSuccess || e2 != cudaSuccess) {
-      h2b_set_error("h2b_stage1_run: workspace allocation failed");
-      rc = H2B_ENOMEM;
+  const double coef = k0 * k0 * volume / (4.0 * 3.14159265358979323846);
+  // clusters in batches of bounded ACA workspace (packed order, so the compacted factors come out
+  // in packed order): the workspace holds cap columns per cluster, the factors only their rank
+  struct Part {
+    double2 *A = nullptr, *B = nullptr, *M = nullptr;
+    int64_t na = 0, nb = 0, nm = 0;
+  };
+  std::vector<Part> parts;
+  a_off[0] = b_off[0] = m_off[0] = 0;
+  const int64_t WS_MAX = (int64_t)1 << 31;  // complex elements of ACA workspace per batch (32 GB)
+  int c0 = 0;
+  while (c0 < P && !rc) {
+    std::vector<ACAClu> clus;
+    std::vector<int64_t> cols;
+    int64_t ws = 0, fl = 0;
+    int c1 = c0;
+    for (; c1 < P; ++c1) {
+      const int64_t nc = ncols[c1];
+      if (nc == 0) continue;
+      ACAClu C{};
+      C.c = c1;
+      C.nr = c_size[c1];
+      C.ncols = (int32_t)nc;
+      C.cap = (int32_t)std::min<int64_t>(std::min<int64_t>(max_rank, 200), std::min<int64_t>(C.nr, nc));
+      const int64_t need = ((int64_t)C.nr + nc) * C.cap;
+      if (!clus.empty() && ws + need > WS_MAX) break;
+      C.cols_off = (int64_t)cols.size();
+      for (int64_t b = s_row_ptr[c1]; b < s_row_ptr[c1 + 1]; ++b) {
+        const int s = s_col[b];
+        for (int q = 0; q < c_size[s]; ++q) cols.push_back(perm[c_start[s] + q]);
+      }
+      C.ws_a = ws;
+      ws += (int64_t)C.nr * C.cap;
+      C.ws_b = ws;
+      ws += nc * C.cap;
+      C.ws_f = fl;
+      fl += C.nr + nc;
+      clus.push_back(C);
     }
-  }
-  if (!rc && !clus.empty()) {
-    const double coef = k0 * k0 * volume / (4.0 * 3.14159265358979323846);
-    k_aca<<<(int)clus.size(), AT>>>(dclus, dstart, dperm, dcols, dctr, dchi, k0, coef, eps_aca, dws, dfl, drank, derr);
-    cudaError_t e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaDeviceSynchronize();
-    if (e != cudaSuccess) {
-      h2b_set_error(std::string("h2b_stage1_run: ACA kernel: ") + cudaGetErrorString(e));
-      rc = H2B_ECUDA;
-    }
-  }
-  if (!rc) {
-    int32_t err = 0;
-    H2B_CUDA_TRY(cudaMemcpy(rank_out, drank, sizeof(int32_t) * P, cudaMemcpyDeviceToHost));
-    H2B_CUDA_TRY(cudaMemcpy(&err, derr, sizeof(int32_t), cudaMemcpyDeviceToHost));
-    if (err) {
-      h2b_set_error("h2b_stage1_run: ACA reached its rank cap at cluster " + std::to_string(err - 1) +
-                    " (the reference raises ClusterCompressionError)");
-      rc = H2B_EINVAL;
-    }
-  }
-  if (!rc) {
-    a_off[0] = b_off[0] = m_off[0] = 0;
-    std::vector<int64_t> ncols(P, 0);
-    for (const ACAClu& C : clus) ncols[C.c] = C.ncols;
-    for (int c = 0; c < P; ++c) {
-      const int64_t r = rank_out[c];
-      a_off[c + 1] = a_off[c] + (int64_t)c_size[c] * r;
-      b_off[c + 1] = b_off[c] + ncols[c] * r;
-      m_off[c + 1] = m_off[c] + r * r;
-    }
-    S->na = a_off[P];
-    S->nb = b_off[P];
-    S->nm = m_off[P];
-    rc = up(&dao, a_off, (size_t)P + 1);
-    if (!rc) rc = up(&dbo, b_off, (size_t)P + 1);
-    if (!rc) rc = up(&dmo, m_off, (size_t)P + 1);
+    ACAClu* dclus = nullptr;
+    int64_t *dcols = nullptr, *dao = nullptr, *dbo = nullptr, *dmo = nullptr;
+    double2* dws = nullptr;
+    unsigned char* dfl = nullptr;
+    Part pt;
+    rc = up(&dclus, clus.data(), clus.size());
+    if (!rc) rc = up(&dcols, cols.data(), cols.size());
     if (!rc) {
-      cudaError_t e1 = cudaMalloc(&S->A, sizeof(double2) * std::max<int64_t>(S->na, 1));
-      cudaError_t e2 = cudaMalloc(&S->B, sizeof(double2) * std::max<int64_t>(S->nb, 1));
-      cudaError_t e3 = cudaMalloc(&S->M, sizeof(double2) * std::max<int64_t>(S->nm, 1));
-      if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) rc = H2B_ENOMEM;
+      cudaError_t e1 = cudaMalloc(&dws, sizeof(double2) * std::max<int64_t>(ws, 1));
+      cudaError_t e2 = cudaMalloc(&dfl, std::max<int64_t>(fl, 1));
+      if (e1 != cudaSuccess || e2 != cudaSuccess) {
+        h2b_set_error("h2b_stage1_run: ACA workspace allocation failed");
+        rc = H2B_ENOMEM;
+      }
     }
     if (!rc && !clus.empty()) {
-      k_stage1_pack<<<(int)clus.size(), 256>>>(dclus, drank, dao, dbo, dmo, dws, S->A, S->B, S->M);
+      k_aca<<<(int)clus.size(), AT>>>(dclus, dstart, dperm, dcols, dctr, dchi, k0, coef, eps_aca, dws, dfl, drank,
+                                      derr);
       cudaError_t e = cudaGetLastError();
       if (e == cudaSuccess) e = cudaDeviceSynchronize();
       if (e != cudaSuccess) {
-        h2b_set_error(std::string("h2b_stage1_run: pack: ") + cudaGetErrorString(e));
+        h2b_set_error(std::string("h2b_stage1_run: ACA kernel: ") + cudaGetErrorString(e));
         rc = H2B_ECUDA;
       }
     }
+    if (!rc) {
+      int32_t err = 0;
+      H2B_CUDA_TRY(cudaMemcpy(rank_out, drank, sizeof(int32_t) * P, cudaMemcpyDeviceToHost));
+      H2B_CUDA_TRY(cudaMemcpy(&err, derr, sizeof(int32_t), cudaMemcpyDeviceToHost));
+      if (err) {
+        h2b_set_error("h2b_stage1_run: ACA reached its rank cap at cluster " + std::to_string(err - 1) +
+                      " (the reference raises ClusterCompressionError)");
+        rc = H2B_EINVAL;
+      }
+    }
+    if (!rc) {
+      // batch-local offsets for clusters c0 .. c1-1, then the global ones
+      std::vector<int64_t> la(P + 1, 0), lb(P + 1, 0), lm(P + 1, 0);
+      for (int c = c0; c < c1; ++c) {
+        const int64_t r = rank_out[c];
+        la[c + 1] = la[c] + (int64_t)c_size[c] * r;
+        lb[c + 1] = lb[c] + ncols[c] * r;
+        lm[c + 1] = lm[c] + r * r;
+        a_off[c + 1] = a_off[c] + (int64_t)c_size[c] * r;
+        b_off[c + 1] = b_off[c] + ncols[c] * r;
+        m_off[c + 1] = m_off[c] + r * r;
+      }
+      pt.na = la[c1];
+      pt.nb = lb[c1];
+      pt.nm = lm[c1];
+      rc = up(&dao, la.data(), (size_t)P + 1);
+      if (!rc) rc = up(&dbo, lb.data(), (size_t)P + 1);
+      if (!rc) rc = up(&dmo, lm.data(), (size_t)P + 1);
+      if (!rc) {
+        cudaError_t e1 = cudaMalloc(&pt.A, sizeof(double2) * std::max<int64_t>(pt.na, 1));
+        cudaError_t e2 = cudaMalloc(&pt.B, sizeof(double2) * std::max<int64_t>(pt.nb, 1));
+        cudaError_t e3 = cudaMalloc(&pt.M, sizeof(double2) * std::max<int64_t>(pt.nm, 1));
+        if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) rc = H2B_ENOMEM;
+      }
+      if (!rc && !clus.empty()) {
+        k_stage1_pack<<<(int)clus.size(), 256>>>(dclus, drank, dao, dbo, dmo, dws, pt.A, pt.B, pt.M);
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) {
+          h2b_set_error(std::string("h2b_stage1_run: pack: ") + cudaGetErrorString(e));
+          rc = H2B_ECUDA;
+        }
+      }
+      parts.push_back(pt);
+    }
+    void* ptrs[] = {dclus, dcols, dao, dbo, dmo, dws, dfl};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    c0 = c1;
   }
-  void* ptrs[] = {dclus, dstart, drank, derr, dperm, dcols, dao, dbo, dmo, dctr, dchi, dws, dfl};
+  // one buffer per factor kind, batches in order (packed order)
+  if (!rc) {
+    S->na = a_off[P];
+    S->nb = b_off[P];
+    S->nm = m_off[P];
+    cudaError_t e1 = cudaMalloc(&S->A, sizeof(double2) * std::max<int64_t>(S->na, 1));
+    cudaError_t e2 = cudaMalloc(&S->B, sizeof(double2) * std::max<int64_t>(S->nb, 1));
+    cudaError_t e3 = cudaMalloc(&S->M, sizeof(double2) * std::max<int64_t>(S->nm, 1));
+    if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) rc = H2B_ENOMEM;
+    int64_t oa = 0, ob = 0, om = 0;
+    for (const Part& pt : parts) {
+      if (rc) break;
+      if (pt.na) H2B_CUDA_TRY(cudaMemcpy(S->A + oa, pt.A, sizeof(double2) * pt.na, cudaMemcpyDeviceToDevice));
+      if (pt.nb) H2B_CUDA_TRY(cudaMemcpy(S->B + ob, pt.B, sizeof(double2) * pt.nb, cudaMemcpyDeviceToDevice));
+      if (pt.nm) H2B_CUDA_TRY(cudaMemcpy(S->M + om, pt.M, sizeof(double2) * pt.nm, cudaMemcpyDeviceToDevice));
+      oa += pt.na;
+      ob += pt.nb;
+      om += pt.nm;
+    }
+  }
+  for (const Part& pt : parts) {
+    if (pt.A) cudaFree(pt.A);
+    if (pt.B) cudaFree(pt.B);
+    if (pt.M) cudaFree(pt.M);
+  }
+  void* ptrs[] = {dstart, drank, derr, dperm, dctr, dchi};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (rc) {
@@ -973,6 +1091,19 @@ extern "C" int h2b_stage1_run(int P, const int32_t* c_start, const int32_t* c_si
     return rc;
   }
   *out = S;
+  return H2B_OK;
+}
+
+// device pointers of the Stage-I factors (for h2b_builder_create without a host round trip)
+extern "C" int h2b_stage1_device_ptrs(void* h, void** a, void** b, void** m) {
+  h2b_stage1_ctx* S = (h2b_stage1_ctx*)h;
+  if (!S || !a || !b || !m) {
+    h2b_set_error("h2b_stage1_device_ptrs: null argument");
+    return H2B_EINVAL;
+  }
+  *a = S->A;
+  *b = S->B;
+  *m = S->M;
   return H2B_OK;
 }
 

@@ -16,7 +16,12 @@ from paper_1703_01175_b200.nearfield import geometry_arrays  # noqa: E402
 from paper_1703_01175_b200.pack import load_packed  # noqa: E402
 
 for name in sys.argv[1:] or ["cfg2"]:
-    pk, ex = load_packed(os.path.join(ROOT, "fixtures", name + ".npz"), with_extra=True, near_on_host=False)
+    if name == "cfg3":  # the reference block structure + the reference's own matvec outputs
+        pk, _ = load_packed(os.path.join(ROOT, "fixtures", "cfg3_structure.npz"), with_extra=True,
+                            near_on_host=False, far_on_host=False)
+        ex = dict(np.load(os.path.join(ROOT, "fixtures", "cfg3_ref_outputs.npz")))
+    else:
+        pk, ex = load_packed(os.path.join(ROOT, "fixtures", name + ".npz"), with_extra=True, near_on_host=False)
     centers, chi, k0, vol = geometry_arrays(pk.meta["geometry"])
     eps = 1e-4
     torch.cuda.synchronize()
@@ -29,8 +34,14 @@ for name in sys.argv[1:] or ["cfg2"]:
     errs = [float(np.linalg.norm(op.matvec(ex["x"][:, j]) - ex["y"][:, j]) / np.linalg.norm(ex["y"][:, j]))
             for j in range(ex["x"].shape[1])]
     dk = np.abs(pkd.c_rank.astype(int) - pk.c_rank.astype(int))
+    gm = ""
+    if "rhs_plane_wave" in ex:  # GMRES(50) on the BASELINE cfg3 plane wave (SURVEY 8d draw)
+        from paper_1703_01175_b200 import gmres_solve
+        xg, rep = gmres_solve(op, ex["rhs_plane_wave"], tol=1e-6, restart=50, max_iter=3000)
+        gm = (f"; GMRES(50) to 1e-6: {rep.iterations} it (reference operator, oracle: "
+              f"{int(ex['gmres_iters'])}), {rep.wall_time:.3f} s, converged {rep.converged}")
     print(f"{name}: N={pk.n} Stage I {t1 - t0:.2f} s (ACA ranks max {int(s1['s1_rank'].max())}), Stage II "
           f"{t2 - t1:.2f} s; ranks vs reference: {int(np.count_nonzero(dk))} of {pk.num_clusters} differ "
           f"(max {int(dk.max())}); K {int(pkd.c_rank.sum())} vs {int(pk.c_rank.sum())}; matvec vs the "
-          f"reference-built operator {max(errs):.2e} (eps_acc {eps:g})", flush=True)
+          f"reference-built operator {max(errs):.2e} (eps_acc {eps:g})" + gm, flush=True)
     op.close()
