@@ -264,6 +264,11 @@ int h2b_stage1_destroy(void* stage1);
 /* device pointers of the Stage-I factors A / B / B^T conj(B) (input of h2b_builder_create, which
  * accepts host or device pointers). */
 int h2b_stage1_device_ptrs(void* stage1, void** a, void** b, void** m);
+/* out[i] = Σ_j S[rows[i], j] x[j]: exact rows of the system matrix (entries from the geometry, self
+ * term diag = k0^2 self_term), summed directly over all N columns (original point order; host
+ * arrays) — the reference for device-built operators the reference builder cannot produce. */
+int h2b_exact_rows(const int64_t* rows, int nrows, int64_t n, const double* centers, const void* chi, double k0,
+                   double volume, double diag_re, double diag_im, const void* x, void* out, int device);
 int64_t h2b_gmres_state_elems(int m);
 int h2b_gmres_givens(void* state, int m, int j, const void* hvals_dev, double* host_res, void* stream);
 int h2b_zscale_dev(void* w, int64_t n, const void* scale_dev, void* stream);

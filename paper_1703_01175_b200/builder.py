@@ -148,3 +148,20 @@ def build_device(pk: PackedH2, centers, chi, k0: float, volume: float, eps_aca: 
         return build_stage2(pk, s1, eps_acc, device)
     finally:
         _abi.lib().h2b_stage1_destroy(s1["s1_handle"])
+
+
+def exact_rows(rows, x, centers, chi, k0: float, volume: float, device: int = 0):
+    """(S x)[rows] of the exact system matrix (kernel.py:190-210 entries incl. the self term,
+    summed over all N columns on the device): the dense reference for sampled rows."""
+    from .nearfield import self_term
+    L = _abi.lib()
+    rows = np.ascontiguousarray(rows, np.int64)
+    x = np.ascontiguousarray(x, np.complex128)
+    centers = np.ascontiguousarray(centers, np.float64)
+    chi = np.ascontiguousarray(chi, np.complex128)
+    diag = k0 ** 2 * self_term(volume, k0)
+    out = np.empty(rows.size, np.complex128)
+    _abi.check(L.h2b_exact_rows(rows.ctypes.data, int(rows.size), int(x.size), centers.ctypes.data, chi.ctypes.data,
+                                float(k0), float(volume), float(diag.real), float(diag.imag), x.ctypes.data,
+                                out.ctypes.data, int(device)), "h2b_exact_rows")
+    return out

@@ -101,3 +101,84 @@ int h2b_assemble_near(h2b_handle h, const double* centers, const double* chi, do
   h->sec_uploaded[H2B_SEC_D] = h->sec_elems[H2B_SEC_D];
   return H2B_OK;
 }
+
+// ===========================================================================
+// Exact rows of the system matrix times a vector, summed directly over all N columns (entries
+// sampled from the geometry as above, self term included): the reference for the device-built
+// operators that the reference builder cannot produce (BASELINE cfg4/cfg5).  One CTA per row.
+// ===========================================================================
+namespace {
+__global__ void __launch_bounds__(256) k_exact_rows(const int64_t* __restrict__ rows, int64_t n,
+                                                    const double* __restrict__ centers,
+                                                    const double2* __restrict__ chi, double k0, double coef,
+                                                    double2 diag, const double2* __restrict__ x,
+                                                    double2* __restrict__ out) {
+  __shared__ double2 red[256];
+  const int64_t m = rows[blockIdx.x];
+  const double mx = centers[3 * m], my = centers[3 * m + 1], mz = centers[3 * m + 2];
+  double2 acc = make_double2(0.0, 0.0);
+  for (int64_t j = threadIdx.x; j < n; j += 256) {
+    const double2 cn = chi[j];
+    double2 v;
+    if (j == m) {
+      v = make_double2(1.0 - (cn.x * diag.x - cn.y * diag.y), -(cn.x * diag.y + cn.y * diag.x));
+    } else {
+      const double dx = mx - centers[3 * j], dy = my - centers[3 * j + 1], dz = mz - centers[3 * j + 2];
+      const double r = sqrt(dx * dx + dy * dy + dz * dz);
+      const double amp = coef / r;
+      double sn, cs;
+      sincos(k0 * r, &sn, &cs);
+      const double ar = amp * cs, ai = -(amp * sn);
+      v = make_double2(-(cn.x * ar - cn.y * ai), -(cn.x * ai + cn.y * ar));
+    }
+    cfma(acc, v, x[j]);
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = cadd(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = red[0];
+}
+}  // namespace
+
+// out[i] = Σ_j S[rows[i], j] x[j] (original point order, host arrays in and out)
+extern "C" int h2b_exact_rows(const int64_t* rows, int nrows, int64_t n, const double* centers, const void* chi,
+                              double k0, double volume, double diag_re, double diag_im, const void* x, void* out,
+                              int device) {
+  if (!rows || !centers || !chi || !x || !out || nrows < 1 || n < 1) {
+    h2b_set_error("h2b_exact_rows: bad arguments");
+    return H2B_EINVAL;
+  }
+  H2B_CUDA_TRY(cudaSetDevice(device));
+  int64_t* dr = nullptr;
+  double* dc = nullptr;
+  double2 *dchi = nullptr, *dx = nullptr, *dout = nullptr;
+  auto fin = [&](int rc) {
+    void* ptrs[] = {dr, dc, dchi, dx, dout};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    return rc;
+  };
+  if (cudaMalloc(&dr, 8 * (size_t)nrows) != cudaSuccess || cudaMalloc(&dc, 24 * (size_t)n) != cudaSuccess ||
+      cudaMalloc(&dchi, 16 * (size_t)n) != cudaSuccess || cudaMalloc(&dx, 16 * (size_t)n) != cudaSuccess ||
+      cudaMalloc(&dout, 16 * (size_t)nrows) != cudaSuccess) {
+    cudaGetLastError();
+    h2b_set_error("h2b_exact_rows: allocation failed");
+    return fin(H2B_ENOMEM);
+  }
+  cudaMemcpy(dr, rows, 8 * (size_t)nrows, cudaMemcpyHostToDevice);
+  cudaMemcpy(dc, centers, 24 * (size_t)n, cudaMemcpyHostToDevice);
+  cudaMemcpy(dchi, chi, 16 * (size_t)n, cudaMemcpyHostToDevice);
+  cudaMemcpy(dx, x, 16 * (size_t)n, cudaMemcpyHostToDevice);
+  const double coef = k0 * k0 * volume / (4.0 * 3.14159265358979323846);
+  k_exact_rows<<<nrows, 256>>>(dr, n, dc, dchi, k0, coef, make_double2(diag_re, diag_im), dx, dout);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpy(out, dout, 16 * (size_t)nrows, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) {
+    h2b_set_error(std::string("h2b_exact_rows: ") + cudaGetErrorString(e));
+    return fin(H2B_ECUDA);
+  }
+  return fin(H2B_OK);
+}
