@@ -65,6 +65,7 @@ struct TProg {
   int32_t wait_down, n_ext_wait, ext_wait_first, bottom;
   int32_t lev_first[TREE_MAXLEV + 1];
   int32_t pad[3];
+  int32_t f_base, f_stride;  // bottom: per-node slots for F_c = T-chain from the root (-1: none)
 };
 
 struct TreeArgs {
@@ -305,8 +306,12 @@ __global__ void __launch_bounds__(TNT, 1) k_far_tree(TreeArgs A) {
       }
     }
   }
-  // ---- the root's contribution from the program above (bottom programs under a top) ----
-  if (P.wait_down >= 0) {
+  // The root's contribution from the program above arrives last.  A bottom program with room for
+  // its transfer chains (f_base >= 0) does all the rest before waiting for it: the local down pass
+  // (children's couplings only) into y, and F_c = (T-chain from the root to c), so that after the
+  // flag only y_leaf += V_leaf (F_leaf ŷ_par) remains — two short steps instead of the whole pass.
+  const bool split = P.bottom && P.wait_down >= 0 && P.f_base >= 0;
+  if (P.wait_down >= 0 && !split) {
     const int32_t wd = P.wait_down;
     tmark(A, 5);
     wait_flags(A.flags_down, &wd, 1, want, A.ctrl);
@@ -329,6 +334,7 @@ __global__ void __launch_bounds__(TNT, 1) k_far_tree(TreeArgs A) {
     for (int i = a + warp; i < b; i += NW) {
       const TNode nd = nodes[i];
       if (nd.k == 0 || nd.kind == 2) continue;
+      if (split && nd.kind == 0) continue;  // leaves wait for the root's contribution (below)
       const double2* yp = sm + nd.xh + yoff;
       const int64_t g = (int64_t)(uint32_t)nd.gy_lo | ((int64_t)nd.gy_hi << 32);
       for (int r = lane; r < nd.R; r += 32) {
@@ -342,6 +348,70 @@ __global__ void __launch_bounds__(TNT, 1) k_far_tree(TreeArgs A) {
           double2& o = sm[nd.in + yoff + r];
           o = cadd(o, v);
         }
+      }
+    }
+    __syncthreads();
+  }
+  if (split) {
+    // F_root = I; F_c = T_parent[rows of c] F_parent (k_c x k_root), level by level
+    const int kr = nodes[0].k, fs = P.f_stride;
+    double2* F = sm + P.f_base;
+    for (int lv = 0; lv < nlev; ++lv) {
+      const int a = P.lev_first[lv], b = P.lev_first[lv + 1];
+      for (int i = a + warp; i < b; i += NW) {
+        const int kc = nodes[i].k;
+        double2* Fi = F + (int64_t)i * fs;
+        if (lv == 0) {
+          for (int e = lane; e < kc * kr; e += 32) Fi[e] = make_double2(e / kr == e % kr ? 1.0 : 0.0, 0.0);
+          continue;
+        }
+        const int pi = P.lev_first[lv - 1] + (i - a) / 2, hi = (i - a) & 1;
+        const TNode pn = nodes[pi];
+        const int kp = pn.k, r0 = hi ? nodes[a + 2 * (pi - P.lev_first[lv - 1])].k : 0;
+        const double2* Fp = F + (int64_t)pi * fs;
+        for (int e = lane; e < kc * kr; e += 32) {
+          const int r = e / kr, c = e % kr;
+          double2 s = make_double2(0.0, 0.0);
+          for (int j = 0; j < kp; ++j) cfma(s, sm[pn.pay + (r0 + r) * kp + j], Fp[j * kr + c]);
+          Fi[e] = s;
+        }
+      }
+      __syncthreads();
+    }
+    const int32_t wd = P.wait_down;
+    tmark(A, 5);
+    wait_flags(A.flags_down, &wd, 1, want, A.ctrl);
+    __syncthreads();
+    tmark(A, 6);
+    // g = the root's parent contribution (k_root <= 32 in split mode; the root's own ŷ slot may be
+    // a leaf's, still needed)
+    __shared__ double2 gsh[32];
+    double2* gv = gsh;
+    if (warp == 0) {
+      const TNode nd = nodes[0];
+      const int64_t gx = (int64_t)(uint32_t)nd.gx_lo | ((int64_t)nd.gx_hi << 32);
+      for (int j = lane; j < nd.k; j += 32) gv[j] = __ldcg(A.yhat + gx + j);
+    }
+    __syncthreads();
+    // leaves: u = ŷ_leaf (local part) + F_leaf g, then y += V u — one contribution per element
+    // of y from the far field, as without the split (two addends in y: deterministic)
+    const int a = P.lev_first[nlev - 1], b = P.lev_first[nlev];
+    for (int i = a + warp; i < b; i += NW) {
+      const TNode nd = nodes[i];
+      if (nd.k == 0) continue;
+      double2* u = sm + nd.xh + yoff;
+      const double2* Fi = F + (int64_t)i * fs;
+      if (lane < nd.k) {
+        double2 s = u[lane];
+        for (int c = 0; c < kr; ++c) cfma(s, Fi[lane * kr + c], gv[c]);
+        u[lane] = s;
+      }
+      __syncwarp();
+      const int64_t g = (int64_t)(uint32_t)nd.gy_lo | ((int64_t)nd.gy_hi << 32);
+      for (int r = lane; r < nd.R; r += 32) {
+        const double2 v = rowdot(sm + nd.pay, r, nd.k, u);
+        atomicAdd(&A.y[g + r].x, v.x);
+        atomicAdd(&A.y[g + r].y, v.y);
       }
     }
     __syncthreads();
@@ -526,6 +596,7 @@ struct Builder {
         s_total += (int64_t)h->c_rank[h->s_col[b]] * h->c_rank[t];
     }
     const bool s_l2 = getenv("H2B_TREE_S_L2") != nullptr;  // experiment: panels from L2 always
+    const int s_first = off;  // the staged panels start here
     const bool stage_s = !s_l2 && off + s_total + 2 * xh_total + n_rows <= budget_elems;
     // reading the panels from L2 was measured 3x slower than the task-graph kernel at cfg1
     // (warp-per-target GEMVs on L2 latency): the tree plan is only taken with staged panels
@@ -612,6 +683,19 @@ struct Builder {
     P.smem_elems = off;
     P.n_nodes = nn;
     P.nlev = nl;
+    // transfer chains of a bottom program (see k_far_tree): in the staged coupling panels' region
+    // (dead once the couplings are done) when it is large enough, else none
+    P.f_base = -1;
+    P.f_stride = 0;
+    if (bottom && stage_s && s_total > 0 && !getenv("H2B_TREE_NO_SPLIT")) {
+      int kmax = 0;
+      for (int i = 0; i < nn; ++i) kmax = std::max(kmax, nodes[i].k);
+      const int64_t need = (int64_t)nn * kmax * nodes[0].k;
+      if (need > 0 && need <= s_total && nodes[0].k > 0 && kmax <= 32) {
+        P.f_base = s_first;
+        P.f_stride = kmax * nodes[0].k;
+      }
+    }
     for (int d = 0; d <= nl; ++d) P.lev_first[d] = lev_first[d];
     P.gidx_smem = gidx_smem;
     tp.nodes_all.insert(tp.nodes_all.end(), nodes.begin(), nodes.end());
