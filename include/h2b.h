@@ -147,6 +147,13 @@ int h2b_get_trace(h2b_handle h, int64_t* out, int64_t max_tasks);
    out[32 i + j] = globaltimer stamp j of program i (SM clock64 at out[32 i + 16 + j]) (start, staged, external x̂ ready, x̂ published,
    coupling inputs ready, before / after the parent wait, down pass done, end). */
 int h2b_tree_trace(h2b_handle h, int64_t* out, int64_t max_progs);
+/* Development aid: per-CTA timeline of the last near-field launch (H2B_NEAR_TRACE set before
+ * the first matvec): out[24 c + j], globaltimer ns: 0 entry, 1 first record in, 2 last block
+ * issued, 3 first block landed, 4 last block consumed, 5 producer exit; 6 blocks, 7 SM id;
+ * SM cycles: producer waits 8 stage free, 9 record landed, 10 record buffer free, 11 index
+ * load; consumer (thread 0) waits 12 block landed, 13 record landed; 14 consumer total;
+ * 16 block math to stage release, 17 leaf ends. */
+int h2b_near_trace(h2b_handle h, int64_t* out, int64_t max_ctas);
 
 #define H2B_Q_LAUNCHES_Q1 1   /* kernels per single-RHS matvec */
 #define H2B_Q_SPAN_MODE 2     /* 1 if the q=1 far field uses staged subtree spans */

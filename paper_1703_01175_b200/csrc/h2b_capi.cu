@@ -58,7 +58,7 @@ void free_ctx(h2b_ctx* h) {
                   h->span_ops, h->near_items, h->near_blks, h->couple_items, h->tasks, h->deps,
                   h->near_tasks, h->leaf_items, h->couple_groups, h->ctrl, h->flags, h->trace,
                   h->rec_pool, h->l2_prefetch, h->cta_lists, h->task_list, h->near_recs, h->near_idx, h->wbuf, h->ydeep,
-                  h->ks_partial, h->ks_vals};
+                  h->ks_partial, h->ks_vals, h->near_trace};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->far_stream) cudaStreamDestroy(h->far_stream);

@@ -286,6 +286,7 @@ struct h2b_ctx {
   // near-field stream kernel (runs beside the far-field task graph; both add into a zeroed y)
   int4* near_recs = nullptr;           // near task records
   int2* near_idx = nullptr;            // per near task {first slot, slots}
+  uint64_t* near_trace = nullptr;  // H2B_NEAR_TRACE: 8 stamps per near CTA
   int n_near_tasks = 0, near_rec_max = 0, near_nst = 0, near_smem = 0, near_grid = 0;
   uint32_t near_delay_ns = 0;  // tuning aid (H2B_DEBUG_NEAR_DELAY_NS)
   int near_static = 0;         // near tasks split statically over the CTAs (H2B_NEAR_STATIC)

@@ -84,6 +84,7 @@ struct NearArgs {
   uint32_t delay_ns;  // tuning aid: the producer starts this late (0 = at once)
   int static_split;   // 1: CTA c streams tasks [c T / G, (c+1) T / G) in order (no claims)
   int dbg;            // profiling only (results wrong): 1 no consumer math, 2 no x copies
+  uint64_t* trace;    // optional (H2B_NEAR_TRACE): 8 stamps per CTA, see h2b_near_trace
 };
 
 // One CTA streams a sequence of near-field tasks as ONE continuous sequence of D blocks:
@@ -137,8 +138,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+
+// at most 80 registers: its 9 warps sit beside the far kernel's 8 (<= 128 registers) within each
+// scheduler's 16K-register share (warp i runs on scheduler i % 4: scheduler 0 holds 3 near
+// warps).  Over budget, most near CTAs wait for the far kernel to exit (measured: step 82 us)
 template <int NS, int R>
-__global__ void __launch_bounds__(NEAR_THREADS, 1) k_near_stream(NearArgs A) {
+__global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
   // dynamic shared memory: [ring: nst stages][NRB record buffers]
   extern __shared__ __align__(16) double2 sm[];
   __shared__ uint64_t fbar[NST_MAX], ebar[NST_MAX], rbar[NRB], rfree[NRB];
@@ -150,7 +155,13 @@ __global__ void __launch_bounds__(NEAR_THREADS, 1) k_near_stream(NearArgs A) {
   const int nst = NS > 0 ? A.nst : 0;
   int4* rbuf0 = reinterpret_cast<int4*>(sm + (size_t)nst * STG);
   auto rbuf = [&](int b) { return rbuf0 + (size_t)b * A.rec_slots; };
+  uint64_t* tr = A.trace ? A.trace + 24 * blockIdx.x : nullptr;
+  uint64_t cw[4] = {0, 0, 0, 0};  // trace: wait cycles (see h2b_near_trace)
   if (threadIdx.x == 0) {
+    if (tr) {
+      tr[0] = gtimer();
+      tr[7] = smid();
+    }
     for (int i = 0; i < NST_MAX; ++i) {
       mbar_init(&fbar[i], 1);
       mbar_init(&ebar[i], MNT / 32);
@@ -175,12 +186,16 @@ __global__ void __launch_bounds__(NEAR_THREADS, 1) k_near_stream(NearArgs A) {
       // early: the atomic's round trip overlaps the block issues of the record before)
       auto finish_claim = [&](int c) {
         const int b = claimed % NRB;
+        uint64_t c0 = tr ? clock64() : 0;
         if (claimed >= NRB) mbar_wait(&rfree[b], ((claimed / NRB) - 1) & 1u);  // consumers done with it
+        if (tr) cw[2] += clock64() - c0;
         if (end) c = A.n_tasks;
         s_task[b] = c;
         if (c < A.n_tasks) {
+          if (tr) c0 = clock64();
           const int2 ix = A.idx[c];
           mbar_arrive_expect_tx(&rbar[b], 16u * ix.y);
+          if (tr) cw[3] += clock64() - c0;
           bulk_g2s(rbuf(b), A.recs + ix.x, 16u * ix.y, &rbar[b]);
         } else {
           end = true;
@@ -203,13 +218,19 @@ __global__ void __launch_bounds__(NEAR_THREADS, 1) k_near_stream(NearArgs A) {
       };
       for (int i = 0; i < NRB - 1; ++i) finish_claim(claim());
       int issued = 0;
+      int pst = 0;       // ring stage of the next block (no divisions on the issue path)
+      uint32_t pph = 0;  // its phase parity
+      const int dbg = A.dbg;
       for (int q = 0;; ++q) {
         // keep NRB - 1 records claimed beyond q: fetch the counter now, complete the claim after
         // this record's blocks are issued
         const bool want = claimed < q + NRB && !end;
         const int pending = want ? claim() : 0;
         const int b = q % NRB;
+        uint64_t c1 = tr ? clock64() : 0;
         mbar_wait(&rbar[b], (q / NRB) & 1u);
+        if (tr) cw[1] += clock64() - c1;
+        if (tr && q == 0) tr[1] = gtimer();
         if (s_task[b] >= A.n_tasks) {
           if (want) finish_claim(pending);  // (an unused claim past the end is harmless)
           break;
@@ -219,20 +240,30 @@ __global__ void __launch_bounds__(NEAR_THREADS, 1) k_near_stream(NearArgs A) {
           const int nb = r[0].x;
           const int64_t* bl = reinterpret_cast<const int64_t*>(r + 1 + r[0].y);
           for (int j = 0; j < nb; ++j, ++issued) {
-            const int st = issued % nst;
-            if (issued >= nst) mbar_wait(&ebar[st], ((issued / nst) - 1) & 1u);
-            double2* sp = sm + (size_t)st * STG;
-            mbar_arrive_expect_tx(&fbar[st], 16u * (RB * NS + ((A.dbg & 2) ? 0 : NS)));
-            bulk_g2s_hint(sp, A.dbuf + bl[2 * j], 16u * RB * NS, &fbar[st], pol);
-            if (!(A.dbg & 2)) bulk_g2s(sp + RB * NS, A.x + bl[2 * j + 1], 16u * NS, &fbar[st]);
+            uint64_t c2 = tr ? clock64() : 0;
+            if (issued >= nst) mbar_wait(&ebar[pst], pph ^ 1u);  // freed by round issued / nst - 1
+            if (tr) cw[0] += clock64() - c2;
+            double2* sp = sm + (size_t)pst * STG;
+            mbar_arrive_expect_tx(&fbar[pst], 16u * (RB * NS + ((dbg & 2) ? 0 : NS)));
+            bulk_g2s_hint(sp, A.dbuf + bl[2 * j], 16u * RB * NS, &fbar[pst], pol);
+            if (!(dbg & 2)) bulk_g2s(sp + RB * NS, A.x + bl[2 * j + 1], 16u * NS, &fbar[pst]);
+            if (++pst == nst) {
+              pst = 0;
+              pph ^= 1u;
+            }
           }
         }
         if (want) finish_claim(pending);
       }
+      if (tr) tr[2] = gtimer();
       // every claimed record has been consumed or marked as the end; wait for the consumers to
       // release the last buffers so no bulk copy is in flight at exit
       for (int q = (claimed > NRB ? claimed - NRB : 0); q < claimed; ++q)
         if (s_task[q % NRB] < A.n_tasks) mbar_wait(&rfree[q % NRB], (q / NRB) & 1u);
+      if (tr) {
+        tr[5] = gtimer();
+        for (int i = 0; i < 4; ++i) tr[8 + i] = cw[i];
+      }
       if (atomicAdd(&A.ctrl->near_exited, 1u) == gridDim.x - 1) {
         A.ctrl->near_exited = 0;  // last CTA out resets the claim counter for the next launch
         A.ctrl->near_next = 0;
@@ -253,51 +284,95 @@ __global__ void __launch_bounds__(NEAR_THREADS, 1) k_near_stream(NearArgs A) {
       if (lane == 0) mbar_arrive(&rfree[b]);
     }
   } else {
-    const int r0 = threadIdx.x / LPR;
-    const int col = (threadIdx.x % LPR) * 2;
+    // consumer mapping: each thread owns CPL interleaved columns (c0 + j LPRC: conflict-free
+    // 16-byte loads) of RR rows of the block slice; a leaf's row sums then need log2(LPRC)
+    // shuffle levels (3 for 32-wide leaves)
+    constexpr int EPT = NS > 0 ? RB * NS / MNT : 1;  // slice elements per thread
+    constexpr int CPL = EPT < 4 ? EPT : 4;
+    constexpr int LPRC = NS > 0 ? NS / CPL : 1;
+    constexpr int RPPC = MNT / LPRC;
+    constexpr int RR = EPT / CPL;
+    static_assert(NS == 0 || (RR * RPPC == RB && CPL * LPRC == NS), "near consumer mapping");
+    const int r0 = threadIdx.x / LPRC;
+    const int c0 = threadIdx.x % LPRC;
     int consumed = 0;
+    int st = 0;       // ring stage of the next block and its phase parity: the per-block path
+    uint32_t ph = 0;  // has no divisions (it is latency-bound: 2 consumer warps per scheduler)
+    const bool math = !(A.dbg & 1);
+    const uint64_t cstart = tr ? clock64() : 0;
     for (int q = 0;; ++q) {
       const int b = q % NRB;
+      uint64_t c4 = tr ? clock64() : 0;
       mbar_wait(&rbar[b], (q / NRB) & 1u);
+      if (tr) cw[1] += clock64() - c4;
       if (s_task[b] >= A.n_tasks) break;
       const int4* rec = rbuf(b);
       const int nb = rec[0].x, nl = rec[0].y, row0 = rec[0].z;
       const int64_t* lv = reinterpret_cast<const int64_t*>(rec + 1);  // {y_off, nb} per leaf
       int li = 0;
       int leaf_end = (int)lv[1];
-      double2 acc[R][2];
+      constexpr int NACC = CPL < 2 ? 1 : 2;  // accumulators per row (even / odd columns)
+      double2 acc[RR][NACC];
 #pragma unroll
-      for (int r = 0; r < R; ++r) acc[r][0] = acc[r][1] = make_double2(0.0, 0.0);
+      for (int r = 0; r < RR; ++r)
+#pragma unroll
+        for (int j = 0; j < NACC; ++j) acc[r][j] = make_double2(0.0, 0.0);
       for (int i = 0; i < nb; ++i, ++consumed) {
-        const int st = consumed % nst;
-        mbar_wait(&fbar[st], (consumed / nst) & 1u);
+        uint64_t c3 = tr ? clock64() : 0;
+        mbar_wait(&fbar[st], ph);
+        if (tr) cw[0] += clock64() - c3;
+        if (tr && consumed == 0 && threadIdx.x == 0) tr[3] = gtimer();
         const double2* sp = sm + (size_t)st * STG;
-        if (!(A.dbg & 1)) {
-          const double2 xa = sp[RB * NS + col], xb = sp[RB * NS + col + 1];
+        const uint64_t c5 = tr ? clock64() : 0;
+        if (math) {
+          double2 xv[CPL];  // a row's loads before its FMAs
 #pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const double2* d = sp + (r0 + r * RPP) * NS + col;
-            cfma(acc[r][0], d[0], xa);
-            cfma(acc[r][1], d[1], xb);
+          for (int j = 0; j < CPL; ++j) xv[j] = sp[RB * NS + c0 + j * LPRC];
+#pragma unroll
+          for (int r = 0; r < RR; ++r) {
+            double2 dv[CPL];
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) dv[j] = sp[(r0 + r * RPPC) * NS + c0 + j * LPRC];
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) cfma(acc[r][j % NACC], dv[j], xv[j]);
           }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&ebar[st]);  // this warp is done with the stage
+        if (++st == nst) {
+          st = 0;
+          ph ^= 1u;
+        }
+        const uint64_t c6 = tr ? clock64() : 0;
+        if (tr) cw[2] += c6 - c5;
         if (i + 1 == leaf_end) {  // last partner of this leaf: reduce and add its rows
           const int64_t y_off = lv[2 * li];
 #pragma unroll
-          for (int r = 0; r < R; ++r) {
-            double2 a = cadd(acc[r][0], acc[r][1]);
+          for (int r = 0; r < RR; ++r) {
+            double2 a = acc[r][0];
 #pragma unroll
-            for (int m = LPR / 2; m > 0; m >>= 1) a = cadd(a, shfl_xor2(a, m));
-            if ((threadIdx.x % LPR) == 0) atomic_add2(A.y + y_off + row0 + r0 + r * RPP, a);
-            acc[r][0] = acc[r][1] = make_double2(0.0, 0.0);
+            for (int j = 1; j < NACC; ++j) a = cadd(a, acc[r][j]);
+#pragma unroll
+            for (int m = LPRC / 2; m > 0; m >>= 1) a = cadd(a, shfl_xor2(a, m));
+            if (c0 == 0) atomic_add2(A.y + y_off + row0 + r0 + r * RPPC, a);
+#pragma unroll
+            for (int j = 0; j < NACC; ++j) acc[r][j] = make_double2(0.0, 0.0);
           }
           if (++li < nl) leaf_end += (int)lv[2 * li + 1];
         }
+        if (tr) cw[3] += clock64() - c6;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&rfree[b]);  // this warp is done with the record
+    }
+    if (tr && threadIdx.x == 0) {
+      tr[4] = gtimer();
+      tr[6] = consumed;
+      tr[12] = cw[0];
+      tr[13] = cw[1];
+      tr[14] = clock64() - cstart;
+      tr[16] = cw[2];
+      tr[17] = cw[3];
     }
   }
 }
@@ -734,6 +809,7 @@ int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st)
     N.delay_ns = h->near_delay_ns;
     N.static_split = h->near_static;
     N.dbg = h->near_dbg;
+    N.trace = h->near_trace;
     const int ns = h->mega_ns, r = h->mega_r;
     bool launched = false;
 #define X(a, b)                                                                            \
@@ -750,5 +826,22 @@ int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st)
     H2B_CUDA_TRY(cudaEventRecord(h->ev_join, h->far_stream));
     H2B_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_join, 0));
   }
+  return H2B_OK;
+}
+
+// development aid: the per-CTA timeline of the last near-field launch (H2B_NEAR_TRACE set at
+// prepare): out[24 * c + j] for CTA c, globaltimer ns: 0 entry, 1 first record in, 2 last block
+// issued, 3 first block landed, 4 last block consumed, 5 producer exit; 6 blocks, 7 SM id;
+// SM cycles: producer waits 8 stage free, 9 record landed, 10 record buffer free, 11 index
+// load; consumer (thread 0) waits 12 block landed, 13 record landed; 14 consumer total; 16 block
+// math to stage release, 17 leaf ends
+extern "C" int h2b_near_trace(h2b_handle h, int64_t* out, int64_t max_ctas) {
+  if (!h || !out || !h->near_trace) {
+    h2b_set_error("h2b_near_trace: no near trace (set H2B_NEAR_TRACE before the first matvec)");
+    return H2B_ESTATE;
+  }
+  const int64_t n = std::min<int64_t>(max_ctas, h->near_grid);
+  H2B_CUDA_TRY(cudaDeviceSynchronize());
+  H2B_CUDA_TRY(cudaMemcpy(out, h->near_trace, sizeof(uint64_t) * 24 * n, cudaMemcpyDeviceToHost));
   return H2B_OK;
 }

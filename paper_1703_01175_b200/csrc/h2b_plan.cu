@@ -1331,6 +1331,10 @@ int h2b_prepare(h2b_ctx* h) {
       if (const char* e = getenv("H2B_NEAR_STATIC")) h->near_static = atoi(e) ? 1 : 0;  // tuning aid
       if (const char* e = getenv("H2B_NEAR_DBG")) h->near_dbg = atoi(e);  // profiling only
       if (const char* e = getenv("H2B_NEAR_GRID")) h->near_grid = std::max(1, std::min(sms, atoi(e)));  // tuning aid
+      if (getenv("H2B_NEAR_TRACE") && !h->near_trace) {  // development aid (h2b_near_trace)
+        H2B_CUDA_TRY(cudaMalloc(&h->near_trace, sizeof(uint64_t) * 24 * sms));
+        H2B_CUDA_TRY(cudaMemset(h->near_trace, 0, sizeof(uint64_t) * 24 * sms));
+      }
       h->mega = (per_sm > 0 && h->mega_grid <= per_sm * sms) ? 1 : 0;
       h->mega_est_us = mp.est_makespan;
       // far field as subtree programs (h2b_tree.cu) when the tree qualifies: it takes k_mega's

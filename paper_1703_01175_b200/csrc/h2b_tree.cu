@@ -80,7 +80,7 @@ struct TreeArgs {
   uint32_t* flags_down;
   MegaCtrl* ctrl;
   uint64_t* trace;  // optional (H2B_TREE_TRACE): 16 timestamps per program
-  int trace_levels;  // H2B_TREE_TRACE=2: also one stamp per level of the upward pass
+  int trace_levels;  // H2B_TREE_TRACE=2: stamps 9-14 per level of the upward pass; 3: of the downward pass
 };
 
 __device__ __forceinline__ void tmark(const TreeArgs& A, int i) {
@@ -194,7 +194,9 @@ __device__ __forceinline__ double2 rowdot(const double2* P, int r, int w, const 
   return cadd(a, b);
 }
 
-__global__ void __launch_bounds__(TNT, 1) k_far_tree(TreeArgs A) {
+// at most 128 registers: 2 warps per scheduler (8192 registers) leave the near-field stream's 3
+// warps on scheduler 0 their 80 each within the scheduler's 16K (both kernels co-resident)
+__global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
   extern __shared__ __align__(16) double2 sm[];
   // [0]: nodes, gather list, x, V (the leaf level)  [1]: staged S panels  [2]: T (internal levels)
   __shared__ __align__(8) uint64_t bar[3];
@@ -245,11 +247,30 @@ __global__ void __launch_bounds__(TNT, 1) k_far_tree(TreeArgs A) {
     wait_flags(A.flags_up, A.waits + P.ext_wait_first, P.n_ext_wait, want, A.ctrl);
     __syncthreads();
     tmark(A, 2);
+    // one L2 round trip, not one per node: a warp issues the loads of U nodes before any store
+    // (the stores to shared memory would otherwise order each next load behind them)
     const int e0 = P.lev_first[nlev - 1], e1 = P.lev_first[nlev];
-    for (int i = e0 + warp; i < e1; i += NW) {
-      const TNode nd = nodes[i];
-      const int64_t gx = (int64_t)(uint32_t)nd.gx_lo | ((int64_t)nd.gx_hi << 32);
-      for (int j = lane; j < nd.k; j += 32) sm[nd.xh + j] = __ldcg(A.xhat + gx + j);
+    constexpr int U = 4;
+    for (int i0 = e0 + warp; i0 < e1; i0 += NW * U) {
+      double2 v[U];
+      int dst[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * NW;
+        dst[u] = -1;
+        if (i < e1) {
+          const TNode nd = nodes[i];
+          const int64_t gx = (int64_t)(uint32_t)nd.gx_lo | ((int64_t)nd.gx_hi << 32);
+          if (lane < nd.k) {
+            v[u] = __ldcg(A.xhat + gx + lane);
+            dst[u] = nd.xh + lane;
+          }
+          for (int j = lane + 32; j < nd.k; j += 32) sm[nd.xh + j] = __ldcg(A.xhat + gx + j);  // k > 32
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (dst[u] >= 0) sm[dst[u]] = v[u];
     }
     __syncthreads();
   }
@@ -266,7 +287,7 @@ __global__ void __launch_bounds__(TNT, 1) k_far_tree(TreeArgs A) {
       if (nd.kind != 2 && nd.k > 0) colsum(sm + nd.pay, nd.R, nd.k, nd.sh, sm + nd.in, sm + nd.xh);
     }
     __syncthreads();
-    if (lv >= nlev - 6 && (A.trace_levels)) tmark(A, 9 + (nlev - 1 - lv));
+    if (lv >= nlev - 6 && A.trace_levels == 2) tmark(A, 9 + (nlev - 1 - lv));
   }
   // ---- publish x̂ of the program's own nodes ----
   {
@@ -287,11 +308,25 @@ __global__ void __launch_bounds__(TNT, 1) k_far_tree(TreeArgs A) {
   __syncthreads();
   tmark(A, 4);
   double2* xg = sm + P.xg_smem;
-  for (int i = tid; i < P.n_xg; i += TNT) {
-    const int g = gidx[i];
-    xg[i] = g >= 0 ? __ldcg(A.xhat + g) : sm[~g];
+  {
+    constexpr int U = 4;  // loads of U elements in flight per thread before their stores
+    for (int i0 = tid; i0 < P.n_xg; i0 += TNT * U) {
+      double2 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * TNT;
+        if (i < P.n_xg) {
+          const int g = gidx[i];
+          v[u] = g >= 0 ? __ldcg(A.xhat + g) : sm[~g];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (i0 + u * TNT < P.n_xg) xg[i0 + u * TNT] = v[u];
+    }
   }
   __syncthreads();
+  if (A.trace_levels == 3) tmark(A, 9);
   {
     const int e = P.bottom ? P.lev_first[nlev] : P.lev_first[nlev - 1];
     for (int i = warp; i < e; i += NW) {
@@ -300,7 +335,13 @@ __global__ void __launch_bounds__(TNT, 1) k_far_tree(TreeArgs A) {
       if (nd.s_rows > 0) {
         const int64_t so = (int64_t)(uint32_t)nd.s_pay | ((int64_t)nd.pad << 32);
         const double2* sp = P.pad[0] ? sm + so : (const double2*)A.src[TS_S] + so;  // staged or L2
+        if (A.trace_levels == 4 && i == warp) colsum(sp, nd.s_rows, nd.k, nd.sh, xg + nd.xg, sm + nd.xh + yoff);
+        const long long ck0 = clock64();
         colsum(sp, nd.s_rows, nd.k, nd.sh, xg + nd.xg, sm + nd.xh + yoff);
+        if (A.trace_levels >= 3 && A.trace && tid == 0 && i == 0) {
+          A.trace[32 * blockIdx.x + 15] = clock64() - ck0;
+          A.trace[32 * blockIdx.x + 31] = ((int64_t)nd.s_rows << 16) | ((int64_t)nd.k << 8) | nd.sh;
+        }
       } else {
         for (int j = lane; j < nd.k; j += 32) sm[nd.xh + yoff + j] = make_double2(0.0, 0.0);
       }
@@ -310,6 +351,10 @@ __global__ void __launch_bounds__(TNT, 1) k_far_tree(TreeArgs A) {
   // its transfer chains (f_base >= 0) does all the rest before waiting for it: the local down pass
   // (children's couplings only) into y, and F_c = (T-chain from the root to c), so that after the
   // flag only y_leaf += V_leaf (F_leaf ŷ_par) remains — two short steps instead of the whole pass.
+  if (A.trace_levels == 3) {
+    __syncthreads();
+    tmark(A, 10);
+  }
   const bool split = P.bottom && P.wait_down >= 0 && P.f_base >= 0;
   if (P.wait_down >= 0 && !split) {
     const int32_t wd = P.wait_down;
@@ -351,6 +396,7 @@ __global__ void __launch_bounds__(TNT, 1) k_far_tree(TreeArgs A) {
       }
     }
     __syncthreads();
+    if (A.trace_levels == 3 && lv < 4) tmark(A, 11 + lv);
   }
   if (split) {
     // F_root = I; F_c = T_parent[rows of c] F_parent (k_c x k_root), level by level
@@ -903,7 +949,7 @@ int h2b_launch_tree(h2b_ctx* h, const TreeDev* d, const double2* xp, double2* yp
   A.trace = d->trace;
   {
     const char* e = getenv("H2B_TREE_TRACE");
-    A.trace_levels = e && atoi(e) == 2;
+    A.trace_levels = e ? atoi(e) : 0;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(d->n_progs);

@@ -1,0 +1,67 @@
+// One-shot vs repeated latency of the tree kernel's colsum (h2b_tree.cu), 1 or 8 warps per CTA.
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "../../paper_1703_01175_b200/csrc/h2b_common.cuh"
+
+__device__ __forceinline__ double2 colsum_sum(const double2* P, int R, int w, int sh, const double2* in) {
+  const int lane = threadIdx.x & 31;
+  const int wp = 1 << sh, G = 32 >> sh;
+  const int g = lane >> sh, c = lane & (wp - 1);
+  double2 a = make_double2(0.0, 0.0), b = a;
+  for (int r0 = g; r0 < R; r0 += 4 * G) {
+    double2 pv[4], xv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = r0 + i * G;
+      const bool ok = c < w && r < R;
+      pv[i] = ok ? P[r * w + c] : make_double2(0.0, 0.0);
+      xv[i] = ok ? in[r] : make_double2(0.0, 0.0);
+    }
+    cfma(a, pv[0], xv[0]);
+    cfma(b, pv[1], xv[1]);
+    cfma(a, pv[2], xv[2]);
+    cfma(b, pv[3], xv[3]);
+  }
+  a = cadd(a, b);
+  for (int m = wp; m < 32; m <<= 1) a = cadd(a, shfl_xor2(a, m));
+  return a;
+}
+
+__global__ void k(int R, int w, int sh, long long* out, double2* sink) {
+  extern __shared__ double2 sm[];
+  double2* P = sm + (threadIdx.x >> 5) * 1024;
+  double2* xin = sm + 8 * 1024 + (threadIdx.x >> 5) * 64;
+  double2* o = sm + 8 * 1024 + 8 * 64 + (threadIdx.x >> 5) * 32;
+  for (int i = threadIdx.x & 31; i < 1024; i += 32) P[i] = make_double2(1e-3 * i, 1.0);
+  for (int i = threadIdx.x & 31; i < 64; i += 32) xin[i] = make_double2(1.0, 1e-3 * i);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  long long t[4];
+  for (int it = 0; it < 4; ++it) {
+    __syncwarp();
+    const long long t0 = clock64();
+    const double2 s = colsum_sum(P, R, w, sh, xin);
+    if (lane < w) o[lane] = s;
+    t[it] = clock64() - t0;
+  }
+  if (lane == 0 && threadIdx.x == 0)
+    for (int i = 0; i < 4; ++i) out[i] = t[i];
+  sink[threadIdx.x] = o[lane];
+}
+
+int main() {
+  long long* d;
+  double2* sink;
+  cudaMalloc(&d, 64);
+  cudaMalloc(&sink, 256 * 16);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  long long h[4];
+  int cases[][3] = {{4, 3, 2}, {24, 8, 3}, {21, 7, 3}, {48, 8, 3}};
+  for (auto& c : cases)
+    for (int nt : {32, 256}) {
+      k<<<1, nt, (8 * 1024 + 8 * 64 + 8 * 32) * 16>>>(c[0], c[1], c[2], d, sink);
+      cudaMemcpy(h, d, 32, cudaMemcpyDeviceToHost);
+      printf("R %2d w %d threads %3d: calls %lld %lld %lld %lld cycles\n", c[0], c[1], nt, h[0], h[1], h[2], h[3]);
+    }
+  return 0;
+}
