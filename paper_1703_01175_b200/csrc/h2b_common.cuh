@@ -177,7 +177,8 @@ struct Task {
 //   span:   SpanHead (9 slots) | n_copy x SpanCopy (2 slots each)
 //   couple: {n_items, cta_mode, 0, 0} | n_items x CoupleItem (2 slots each)
 constexpr int REC_SLOTS = 256;  // 4 KB per record buffer
-constexpr int NEAR_NRB = 8;     // near-field stream: record buffers (the task in use + NRB - 1 claimed ahead)
+constexpr int NEAR_NRB = 8;      // near-field stream: record buffers (the task in use + NRB - 1 claimed ahead)
+constexpr int NEAR_MAXG = 152;  // CTAs of the near stream with kernel-parameter first copies
 constexpr int NEAR_REC_MAXB = 160;
 struct DepRange {
   int32_t lo, hi;           // task ids [lo, hi) that must be complete
@@ -286,7 +287,10 @@ struct h2b_ctx {
   // near-field stream kernel (runs beside the far-field task graph; both add into a zeroed y)
   int4* near_recs = nullptr;           // near task records
   int2* near_idx = nullptr;            // per near task {first slot, slots}
-  uint64_t* near_trace = nullptr;  // H2B_NEAR_TRACE: 8 stamps per near CTA
+  uint64_t* near_trace = nullptr;  // H2B_NEAR_TRACE: stamps per near CTA
+  int near_early = 0;               // first record / block per CTA known at plan time
+  std::vector<int2> near_first_rec;
+  std::vector<longlong2> near_first_blk;
   int n_near_tasks = 0, near_rec_max = 0, near_nst = 0, near_smem = 0, near_grid = 0;
   uint32_t near_delay_ns = 0;  // tuning aid (H2B_DEBUG_NEAR_DELAY_NS)
   int near_static = 0;         // near tasks split statically over the CTAs (H2B_NEAR_STATIC)

@@ -85,6 +85,12 @@ struct NearArgs {
   int static_split;   // 1: CTA c streams tasks [c T / G, (c+1) T / G) in order (no claims)
   int dbg;            // profiling only (results wrong): 1 no consumer math, 2 no x copies
   uint64_t* trace;    // optional (H2B_NEAR_TRACE): 8 stamps per CTA, see h2b_near_trace
+  // static split: each CTA's first record {slot, slots} and first block {D, x} offsets, so the
+  // kernel's first two copies need no index or record load (one memory round trip to the first
+  // block instead of three: at kernel start the far kernel's staging burst makes each ~2 us)
+  int early;
+  int2 first_rec[NEAR_MAXG];
+  longlong2 first_blk[NEAR_MAXG];
 };
 
 // One CTA streams a sequence of near-field tasks as ONE continuous sequence of D blocks:
@@ -182,6 +188,18 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
       }
       int claimed = 0;  // records 0 .. claimed-1 claimed
       bool end = false;
+      // static split: the index entries of this CTA's first NRB tasks, loaded together (one
+      // round trip, not NRB sequential ones before the ring fills); the first from the params
+      const int s_first = (int)((int64_t)blockIdx.x * A.n_tasks / gridDim.x);
+      const int s_end = (int)((int64_t)(blockIdx.x + 1) * A.n_tasks / gridDim.x);
+      const bool pre_ok = A.static_split != 0;
+      int2 pre[NRB];
+      if (pre_ok) {
+#pragma unroll
+        for (int i = 0; i < NRB; ++i)
+          pre[i] = (i == 0 && A.early) ? A.first_rec[blockIdx.x]
+                   : s_first + i < s_end ? __ldg(A.idx + s_first + i) : make_int2(0, 0);
+      }
       // claim record `claimed` into buffer claimed % NRB, given the counter value c (fetched
       // early: the atomic's round trip overlaps the block issues of the record before)
       auto finish_claim = [&](int c) {
@@ -193,7 +211,7 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
         s_task[b] = c;
         if (c < A.n_tasks) {
           if (tr) c0 = clock64();
-          const int2 ix = A.idx[c];
+          const int2 ix = claimed < NRB && pre_ok ? pre[claimed] : A.idx[c];
           mbar_arrive_expect_tx(&rbar[b], 16u * ix.y);
           if (tr) cw[3] += clock64() - c0;
           bulk_g2s(rbuf(b), A.recs + ix.x, 16u * ix.y, &rbar[b]);
@@ -205,8 +223,6 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
       };
       // claims: the next task from the global counter (dynamic balance), or this CTA's next task
       // of a static contiguous split (no atomics on the producer's path)
-      const int s_first = (int)((int64_t)blockIdx.x * A.n_tasks / gridDim.x);
-      const int s_end = (int)((int64_t)(blockIdx.x + 1) * A.n_tasks / gridDim.x);
       int s_next = s_first;
       auto claim = [&]() -> int {
         if (A.static_split) {
@@ -216,11 +232,21 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
         }
         return (int)atomicAdd(&A.ctrl->near_next, 1u);
       };
-      for (int i = 0; i < NRB - 1; ++i) finish_claim(claim());
+      const int dbg = A.dbg;
       int issued = 0;
       int pst = 0;       // ring stage of the next block (no divisions on the issue path)
       uint32_t pph = 0;  // its phase parity
-      const int dbg = A.dbg;
+      const bool early = A.early && s_first < s_end && NS > 0;
+      if (early) {  // the first block before any record (its offsets are kernel parameters)
+        const longlong2 fb = A.first_blk[blockIdx.x];
+        mbar_arrive_expect_tx(&fbar[0], 16u * (RB * NS + ((dbg & 2) ? 0 : NS)));
+        bulk_g2s_hint(sm, A.dbuf + fb.x, 16u * RB * NS, &fbar[0], pol);
+        if (!(dbg & 2)) bulk_g2s(sm + RB * NS, A.x + fb.y, 16u * NS, &fbar[0]);
+        issued = 1;
+        pst = nst == 1 ? 0 : 1;
+        pph = nst == 1 ? 1u : 0u;
+      }
+      for (int i = 0; i < NRB - 1; ++i) finish_claim(claim());
       for (int q = 0;; ++q) {
         // keep NRB - 1 records claimed beyond q: fetch the counter now, complete the claim after
         // this record's blocks are issued
@@ -239,7 +265,7 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
           const int4* r = rbuf(b);
           const int nb = r[0].x;
           const int64_t* bl = reinterpret_cast<const int64_t*>(r + 1 + r[0].y);
-          for (int j = 0; j < nb; ++j, ++issued) {
+          for (int j = (q == 0 && early) ? 1 : 0; j < nb; ++j, ++issued) {
             uint64_t c2 = tr ? clock64() : 0;
             if (issued >= nst) mbar_wait(&ebar[pst], pph ^ 1u);  // freed by round issued / nst - 1
             if (tr) cw[0] += clock64() - c2;
@@ -677,6 +703,15 @@ int h2b_mega_static_smem() {
   return (int)fa.sharedSizeBytes;
 }
 
+int h2b_mega_regs() {
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, k_mega) != cudaSuccess) {
+    cudaGetLastError();
+    return 255;
+  }
+  return fa.numRegs;
+}
+
 int h2b_mega_occupancy(int, int, int smem_bytes, int* blocks_per_sm) {
   const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_mega, MNT, smem_bytes);
   if (e != cudaSuccess) {
@@ -712,6 +747,21 @@ int h2b_near_stream_static_smem(int ns, int r, int* bytes) {
   }
   *bytes = (int)fa.sharedSizeBytes;
   return H2B_OK;
+}
+
+int h2b_near_stream_regs(int ns, int r) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaErrorInvalidValue;
+#define X(a, b) \
+  if (ns == a && r == b) e = cudaFuncGetAttributes(&fa, k_near_stream<a, b>);
+  NEAR_VARIANTS(X)
+#undef X
+  if (ns != 32 && ns != 64) e = cudaFuncGetAttributes(&fa, k_near_stream<0, 1>);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return 255;
+  }
+  return fa.numRegs;
 }
 
 int h2b_near_stream_set_smem(int ns, int r, int bytes) {
@@ -810,6 +860,12 @@ int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st)
     N.static_split = h->near_static;
     N.dbg = h->near_dbg;
     N.trace = h->near_trace;
+    N.early = h->near_static && h->near_early && h->near_grid <= NEAR_MAXG;
+    if (N.early)
+      for (int c = 0; c < h->near_grid; ++c) {
+        N.first_rec[c] = h->near_first_rec[c];
+        N.first_blk[c] = h->near_first_blk[c];
+      }
     const int ns = h->mega_ns, r = h->mega_r;
     bool launched = false;
 #define X(a, b)                                                                            \

@@ -17,6 +17,9 @@
 int h2b_far_init_attributes(int smem_cap_bytes);
 int h2b_mega_set_smem(int ns, int r, int bytes);
 int h2b_mega_occupancy(int ns, int r, int smem_bytes, int* blocks_per_sm);
+int h2b_mega_regs();
+int h2b_tree_regs();
+int h2b_near_stream_regs(int ns, int r);
 int h2b_mega_static_smem();
 int h2b_near_stream_static_smem(int ns, int r, int* bytes);
 int h2b_near_stream_set_smem(int ns, int r, int bytes);
@@ -1331,6 +1334,24 @@ int h2b_prepare(h2b_ctx* h) {
       if (const char* e = getenv("H2B_NEAR_STATIC")) h->near_static = atoi(e) ? 1 : 0;  // tuning aid
       if (const char* e = getenv("H2B_NEAR_DBG")) h->near_dbg = atoi(e);  // profiling only
       if (const char* e = getenv("H2B_NEAR_GRID")) h->near_grid = std::max(1, std::min(sms, atoi(e)));  // tuning aid
+      // each CTA's first record and first block (static split): kernel parameters
+      h->near_early = 0;
+      h->near_first_rec.assign(h->near_grid, int2{0, 0});
+      h->near_first_blk.assign(h->near_grid, longlong2{0, 0});
+      if (mp.ns > 0 && h->near_grid <= NEAR_MAXG && !getenv("H2B_NEAR_NO_EARLY")) {
+        const int nt = (int)mp.near_idx.size();
+        for (int c = 0; c < h->near_grid; ++c) {
+          const int t = (int)((int64_t)c * nt / h->near_grid);
+          if (t >= (int)((int64_t)(c + 1) * nt / h->near_grid)) continue;  // no task
+          const int2 ix = mp.near_idx[t];
+          const int4 head = mp.near_recs[ix.x];
+          const int4 b0 = mp.near_recs[ix.x + 1 + head.y];  // {D offset, x offset} as two int64
+          h->near_first_rec[c] = ix;
+          h->near_first_blk[c] = longlong2{(long long)(uint32_t)b0.x | ((long long)b0.y << 32),
+                                           (long long)(uint32_t)b0.z | ((long long)b0.w << 32)};
+        }
+        h->near_early = 1;
+      }
       if (getenv("H2B_NEAR_TRACE") && !h->near_trace) {  // development aid (h2b_near_trace)
         H2B_CUDA_TRY(cudaMalloc(&h->near_trace, sizeof(uint64_t) * 24 * sms));
         H2B_CUDA_TRY(cudaMemset(h->near_trace, 0, sizeof(uint64_t) * 24 * sms));
@@ -1350,6 +1371,21 @@ int h2b_prepare(h2b_ctx* h) {
         if (mp.ns > 0 && tnst < 2) tnst = 2;
         h->near_nst = tnst;
         h->near_smem = tnst * stg + rec_bytes;
+      }
+      // both kernels must fit one SM's register file per scheduler (warp w runs on scheduler
+      // w % 4: 3 of the near kernel's 9 warps share scheduler 0 with 2 far warps); otherwise
+      // the near CTAs wait for the far kernel to exit (correct, but the step nearly doubles)
+      if (h->near_grid > 0) {
+        auto warp_regs = [](int regs) { return ((regs + 7) / 8 * 8) * 32; };
+        const int far_regs = planned ? h2b_tree_regs() : h2b_mega_regs();
+        const int need = 3 * warp_regs(h2b_near_stream_regs(mp.ns, mp.r)) + 2 * warp_regs(far_regs);
+        if (need > 16384) {
+          static bool warned = false;
+          if (!warned)
+            fprintf(stderr, "h2b: near-field and far-field kernels exceed a scheduler's registers (%d > 16384): "
+                            "they will not run concurrently\n", need);
+          warned = true;
+        }
       }
     }
   }

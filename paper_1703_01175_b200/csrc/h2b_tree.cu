@@ -194,6 +194,95 @@ __device__ __forceinline__ double2 rowdot(const double2* P, int r, int w, const 
   return cadd(a, b);
 }
 
+// ---- CTA-wide level operations --------------------------------------------------------------
+// A level's nodes are small (ranks 3..30, a few dozen rows): warp-per-node loops left most of a
+// warp idle and chained shared-memory loads, shuffles and node after node (measured ~700 cycles
+// for a 4 x 3 coupling panel).  Here all nodes of a level are processed at once, each by a
+// group of 2^shk x G threads (column c, row group g); a thread's loads are issued together
+// (unconditional, from clamped rows) before its FMAs, and G <= 4 row groups meet in log2 G
+// shuffle levels.
+
+// Σ over rows r = g, g + G, ... < R of M[r w + c] in[r] (c < w, R >= 1)
+__device__ __forceinline__ double2 col_dot(const double2* M, int R, int w, int c, const double2* in, int g, int G) {
+  double2 a0 = make_double2(0.0, 0.0), a1 = a0;
+  int r = g;
+  for (; r + 3 * G < R; r += 4 * G) {
+    const double2 p0 = M[r * w + c], p1 = M[(r + G) * w + c], p2 = M[(r + 2 * G) * w + c],
+                  p3 = M[(r + 3 * G) * w + c];
+    const double2 x0 = in[r], x1 = in[r + G], x2 = in[r + 2 * G], x3 = in[r + 3 * G];
+    cfma(a0, p0, x0);
+    cfma(a1, p1, x1);
+    cfma(a0, p2, x2);
+    cfma(a1, p3, x3);
+  }
+  for (; r < R; r += G) cfma(a0, M[r * w + c], in[r]);
+  return cadd(a0, a1);
+}
+
+// Σ_j M[r w + j] v[j] for one row (loads of 4 columns before their FMAs)
+__device__ __forceinline__ double2 row_dot(const double2* M, int r, int w, const double2* v) {
+  double2 a0 = make_double2(0.0, 0.0), a1 = a0;
+  const double2* m = M + r * w;
+  int j = 0;
+  for (; j + 4 <= w; j += 4) {
+    const double2 p0 = m[j], p1 = m[j + 1], p2 = m[j + 2], p3 = m[j + 3];
+    const double2 x0 = v[j], x1 = v[j + 1], x2 = v[j + 2], x3 = v[j + 3];
+    cfma(a0, p0, x0);
+    cfma(a1, p1, x1);
+    cfma(a0, p2, x2);
+    cfma(a1, p3, x3);
+  }
+  for (; j < w; ++j) cfma(a0, m[j], v[j]);
+  return cadd(a0, a1);
+}
+
+// out_i[c] = Σ_r M_i[r w_i + c] in_i[r] (c < w_i) for the nodes i in [a, b) that get() accepts;
+// get(nd, M, R, w, in, out) -> bool.  shk: log2 of the columns slot per node (w_i <= 2^shk).
+// A node accepted with R = 0 gets out = 0.
+template <class Get>
+__device__ __forceinline__ void cta_colsum(const TNode* nodes, int a, int b, int shk, Get get) {
+  const int n = b - a;
+  if (n <= 0) return;
+  int shg = 0;  // row groups G = 2^shg: as many as the CTA has threads for, at most 4
+  while (shg < 2 && shk + shg < 5 && (n << (shk + shg + 1)) <= TNT) ++shg;
+  const int sht = shk + shg, G = 1 << shg;
+  const int items = n << sht;
+  const int bound = (items + 31) & ~31;  // warp-uniform trip count (the shuffles below)
+  for (int it = threadIdx.x; it < bound; it += TNT) {
+    const int l = it & ((1 << sht) - 1);
+    const int c = l & ((1 << shk) - 1), g = l >> shk;
+    double2 s = make_double2(0.0, 0.0);
+    double2* out = nullptr;
+    bool ok = false;
+    if (it < items) {
+      const TNode nd = nodes[a + (it >> sht)];
+      const double2 *M, *in;
+      int R, w;
+      if (get(nd, M, R, w, in, out) && c < w) {
+        ok = true;
+        if (g < R) s = col_dot(M, R, w, c, in, g, G);
+      }
+    }
+    for (int m = 1 << shk; m < (1 << sht); m <<= 1) s = cadd(s, shfl_xor2(s, m));
+    if (ok && g == 0) out[c] = s;
+  }
+}
+
+// for the nodes i in [a, b) that get() accepts, each row r < R_i: emit(nd, r, Σ_j M_i[r w_i + j]
+// v_i[j]); get(i, nd, M, R, w, v) -> bool.  2^shr threads per node (rows r = l, l + 2^shr, ...).
+template <class Get, class Emit>
+__device__ __forceinline__ void cta_rowdot(const TNode* nodes, int a, int b, int shr, Get get, Emit emit) {
+  const int items = (b - a) << shr;
+  for (int it = threadIdx.x; it < items; it += TNT) {
+    const int i = a + (it >> shr);
+    const TNode nd = nodes[i];
+    const double2 *M, *v;
+    int R, w;
+    if (!get(i, nd, M, R, w, v)) continue;
+    for (int r = it & ((1 << shr) - 1); r < R; r += 1 << shr) emit(nd, r, row_dot(M, r, w, v));
+  }
+}
+
 // at most 128 registers: 2 warps per scheduler (8192 registers) leave the near-field stream's 3
 // warps on scheduler 0 their 80 each within the scheduler's 16K (both kernels co-resident)
 __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
@@ -242,6 +331,7 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
   const int32_t* gidx = reinterpret_cast<const int32_t*>(sm + P.gidx_smem);
   const int yoff = P.yoff;
   const int nlev = P.nlev;
+  const int shk = P.pad[2] & 255, shr = (P.pad[2] >> 8) & 255;  // threads per node: 2^shk (columns), 2^shr (rows)
   // ---- top programs: the external children's x̂ (bottom programs' roots) ----
   if (P.n_ext_wait) {
     wait_flags(A.flags_up, A.waits + P.ext_wait_first, P.n_ext_wait, want, A.ctrl);
@@ -327,30 +417,17 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
   }
   __syncthreads();
   if (A.trace_levels == 3) tmark(A, 9);
-  {
-    const int e = P.bottom ? P.lev_first[nlev] : P.lev_first[nlev - 1];
-    for (int i = warp; i < e; i += NW) {
-      const TNode nd = nodes[i];
-      if (nd.k == 0) continue;
-      if (nd.s_rows > 0) {
-        const int64_t so = (int64_t)(uint32_t)nd.s_pay | ((int64_t)nd.pad << 32);
-        const double2* sp = P.pad[0] ? sm + so : (const double2*)A.src[TS_S] + so;  // staged or L2
-        if (A.trace_levels == 4 && i == warp) colsum(sp, nd.s_rows, nd.k, nd.sh, xg + nd.xg, sm + nd.xh + yoff);
-        const long long ck0 = clock64();
-        colsum(sp, nd.s_rows, nd.k, nd.sh, xg + nd.xg, sm + nd.xh + yoff);
-        if (A.trace_levels >= 3 && A.trace && tid == 0 && i == 0) {
-          A.trace[32 * blockIdx.x + 15] = clock64() - ck0;
-          A.trace[32 * blockIdx.x + 31] = ((int64_t)nd.s_rows << 16) | ((int64_t)nd.k << 8) | nd.sh;
-        }
-      } else {
-        for (int j = lane; j < nd.k; j += 32) sm[nd.xh + yoff + j] = make_double2(0.0, 0.0);
-      }
-    }
-  }
-  // The root's contribution from the program above arrives last.  A bottom program with room for
-  // its transfer chains (f_base >= 0) does all the rest before waiting for it: the local down pass
-  // (children's couplings only) into y, and F_c = (T-chain from the root to c), so that after the
-  // flag only y_leaf += V_leaf (F_leaf ŷ_par) remains — two short steps instead of the whole pass.
+  cta_colsum(nodes, 0, P.bottom ? P.lev_first[nlev] : P.lev_first[nlev - 1], shk,
+             [&](const TNode& nd, const double2*& M, int& R, int& w, const double2*& in, double2*& out) {
+               if (nd.k == 0) return false;
+               const int64_t so = (int64_t)(uint32_t)nd.s_pay | ((int64_t)nd.pad << 32);
+               M = P.pad[0] ? sm + so : (const double2*)A.src[TS_S] + so;  // staged or L2
+               R = nd.s_rows;  // 0: no couplings (ŷ = 0)
+               w = nd.k;
+               in = xg + nd.xg;
+               out = sm + nd.xh + yoff;
+               return true;
+             });
   if (A.trace_levels == 3) {
     __syncthreads();
     tmark(A, 10);
@@ -726,6 +803,17 @@ struct Builder {
     if (bytes >= (1 << 20)) return false;  // one mbarrier transaction count
     P.stage_bytes = (int32_t)bytes;
     P.pad[0] = (int32_t)sbytes;
+    {  // threads per node of the CTA-wide level operations: 2^shk >= every rank (column ops),
+       // 2^shr >= every row count up to 32 (row ops loop over the rest)
+      int kmax = 1, rmax = 1;
+      for (int i = 0; i < nn; ++i) kmax = std::max(kmax, nodes[i].k);
+      for (int i = 0; i < own_end; ++i) rmax = std::max(rmax, nodes[i].R);
+      int shk = 0, shr = 0;
+      while ((1 << shk) < kmax) ++shk;
+      while ((1 << shr) < rmax && shr < 5) ++shr;
+      if (shk > 5) return false;  // ranks above 32: not for this kernel
+      P.pad[2] = shk | (shr << 8);
+    }
     P.smem_elems = off;
     P.n_nodes = nn;
     P.nlev = nl;
@@ -904,6 +992,15 @@ int h2b_tree_static_smem() {
     return 1024;
   }
   return (int)fa.sharedSizeBytes;
+}
+
+int h2b_tree_regs() {
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, k_far_tree) != cudaSuccess) {
+    cudaGetLastError();
+    return 255;
+  }
+  return fa.numRegs;
 }
 
 int h2b_tree_error(const TreeDev* d, uint32_t* err) {
