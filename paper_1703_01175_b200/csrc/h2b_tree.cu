@@ -66,6 +66,10 @@ struct TProg {
   int32_t lev_first[TREE_MAXLEV + 1];
   int32_t pad[3];
   int32_t f_base, f_stride;  // bottom: per-node slots for F_c = T-chain from the root (-1: none)
+  // bottom: the far field of the subtree's y rows is assembled in shared memory (the staged x
+  // area, dead after the upward pass) and added to y by ONE bulk reduce-add (instead of an
+  // atomic per element): y_n rows from smem y_smem to global row y_g
+  int32_t y_smem, y_n, y_g_lo, y_g_hi;
 };
 
 struct TreeArgs {
@@ -80,16 +84,21 @@ struct TreeArgs {
   uint32_t* flags_down;
   MegaCtrl* ctrl;
   uint64_t* trace;  // optional (H2B_TREE_TRACE): 16 timestamps per program
+  int defer_s;       // request the staged coupling panels after the up-pass operands
   int trace_levels;  // H2B_TREE_TRACE=2: stamps 9-14 per level of the upward pass; 3: of the downward pass
 };
 
+// Code size matters here: every phase of k_far_tree runs once per launch, so its instructions
+// are fetched cold (measured: the bottom programs' last step 2.8 us on first execution, 1.7 us
+// when repeated).  Rare paths are kept out of line and not unrolled.
+__device__ __noinline__ void tmark_impl(uint64_t* trace, int i) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  trace[32 * blockIdx.x + i] = t;
+  trace[32 * blockIdx.x + 16 + i] = clock64();
+}
 __device__ __forceinline__ void tmark(const TreeArgs& A, int i) {
-  if (A.trace && threadIdx.x == 0) {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    A.trace[32 * blockIdx.x + i] = t;
-    A.trace[32 * blockIdx.x + 16 + i] = clock64();
-  }
+  if (A.trace && threadIdx.x == 0) tmark_impl(A.trace, i);
 }
 
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
@@ -104,8 +113,8 @@ __device__ __forceinline__ void st_rel(uint32_t* p, uint32_t v) {
 // warp 0 waits until flags[ids[i]] == want for every i: the ids are loaded once (up to four per
 // lane in registers), then relaxed sweeps, then one acquire fence; the caller follows with
 // __syncthreads
-__device__ __forceinline__ void wait_flags(const uint32_t* flags, const int32_t* ids, int n, uint32_t want,
-                                           MegaCtrl* ctrl) {
+__device__ __noinline__ void wait_flags(const uint32_t* flags, const int32_t* ids, int n, uint32_t want,
+                                        MegaCtrl* ctrl) {
   if (threadIdx.x >= 32 || n == 0) return;
   const int lane = threadIdx.x;
   int f[4];
@@ -115,6 +124,7 @@ __device__ __forceinline__ void wait_flags(const uint32_t* flags, const int32_t*
     bool ok = true;
 #pragma unroll
     for (int u = 0; u < 4; ++u) ok &= f[u] < 0 || ld_relaxed(flags + f[u]) == want;
+#pragma unroll 1
     for (int i = lane + 128; i < n; i += 32) ok &= ld_relaxed(flags + ids[i]) == want;
     if (__all_sync(0xffffffffu, ok)) break;
     if (spins > (1l << 24)) {  // never expected: report instead of hanging the GPU
@@ -164,6 +174,7 @@ __device__ __forceinline__ void colsum(const double2* P, int R, int w, int sh, c
     for (int c = lane; c < w; c += 32) {
       double2 a0 = make_double2(0.0, 0.0), a1 = a0;
       int r = 0;
+#pragma unroll 1
       for (; r + 1 < R; r += 2) {
         cfma(a0, P[r * w + c], in[r]);
         cfma(a1, P[(r + 1) * w + c], in[r + 1]);
@@ -312,8 +323,13 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
     mbar_arrive_expect_tx(&bar[1], (uint32_t)P.pad[0]);  // staged coupling panels (0: from L2)
     mbar_arrive_expect_tx(&bar[2], (uint32_t)P.pad[1]);  // transfer matrices
   }
+  // coupling panels (about half of the staged bytes at cfg2) are needed last: with A.defer_s
+  // they are requested once the up-pass operands have landed, so that the launch burst (the
+  // near-field stream starts at the same time) is smaller
+  const bool defer_s = A.defer_s && P.pad[0] > 0;
   for (int i = tid; i < n_copy; i += TNT) {
     const TCopy c = i == tid ? cp0 : A.copies[c0 + i];
+    if (defer_s && c.kind == TS_S) continue;
     if (c.kind == TS_S && c.smem < 0) {  // coupling panels read from L2 by the couplings: warm them
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const double2*)A.src[TS_S] + c.src),
                    "r"(16u * (uint32_t)c.elems) : "memory");
@@ -327,6 +343,12 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
   const uint32_t want = s_epoch + 1;
   mbar_wait(&bar[0], 0);
   tmark(A, 1);
+  if (defer_s)
+#pragma unroll 1
+    for (int i = tid; i < n_copy; i += TNT) {
+      const TCopy c = i == tid ? cp0 : A.copies[c0 + i];
+      if (c.kind == TS_S) bulk_g2s(sm + c.smem, (const double2*)A.src[TS_S] + c.src, 16u * (uint32_t)c.elems, &bar[1]);
+    }
   const TNode* nodes = reinterpret_cast<const TNode*>(sm);
   const int32_t* gidx = reinterpret_cast<const int32_t*>(sm + P.gidx_smem);
   const int yoff = P.yoff;
@@ -355,6 +377,7 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
             v[u] = __ldcg(A.xhat + gx + lane);
             dst[u] = nd.xh + lane;
           }
+#pragma unroll 1
           for (int j = lane + 32; j < nd.k; j += 32) sm[nd.xh + j] = __ldcg(A.xhat + gx + j);  // k > 32
         }
       }
@@ -385,6 +408,7 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
     for (int i = warp; i < e; i += NW) {
       const TNode nd = nodes[i];
       const int64_t gx = (int64_t)(uint32_t)nd.gx_lo | ((int64_t)nd.gx_hi << 32);
+#pragma unroll 1
       for (int j = lane; j < nd.k; j += 32) A.xhat[gx + j] = sm[nd.xh + j];
     }
     __syncthreads();  // the CTA's x̂ stores happen before thread 0's (cumulative) release
@@ -428,6 +452,8 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
                out = sm + nd.xh + yoff;
                return true;
              });
+#pragma unroll 1
+  for (int i = tid; i < P.y_n; i += TNT) sm[P.y_smem + i] = make_double2(0.0, 0.0);  // x is dead
   if (A.trace_levels == 3) {
     __syncthreads();
     tmark(A, 10);
@@ -462,8 +488,12 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
       for (int r = lane; r < nd.R; r += 32) {
         const double2 v = rowdot(sm + nd.pay, r, nd.k, yp);
         if (nd.kind == 0) {  // leaf back-transform into y (k_near_stream adds concurrently)
-          atomicAdd(&A.y[g + r].x, v.x);
-          atomicAdd(&A.y[g + r].y, v.y);
+          if (P.y_n > 0) {
+            sm[nd.in + r] = v;  // the program's y rows (bulk-added below)
+          } else {
+            atomicAdd(&A.y[g + r].x, v.x);
+            atomicAdd(&A.y[g + r].y, v.y);
+          }
         } else if (nd.ext) {  // external children: their parent contribution to global ŷ
           A.yhat[g + r] = v;
         } else {  // [ŷ_lo; ŷ_hi] are adjacent, right behind [x̂_lo; x̂_hi]
@@ -485,6 +515,7 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
         const int kc = nodes[i].k;
         double2* Fi = F + (int64_t)i * fs;
         if (lv == 0) {
+#pragma unroll 1
           for (int e = lane; e < kc * kr; e += 32) Fi[e] = make_double2(e / kr == e % kr ? 1.0 : 0.0, 0.0);
           continue;
         }
@@ -495,6 +526,7 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
         for (int e = lane; e < kc * kr; e += 32) {
           const int r = e / kr, c = e % kr;
           double2 s = make_double2(0.0, 0.0);
+#pragma unroll 1
           for (int j = 0; j < kp; ++j) cfma(s, sm[pn.pay + (r0 + r) * kp + j], Fp[j * kr + c]);
           Fi[e] = s;
         }
@@ -516,9 +548,11 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
       for (int j = lane; j < nd.k; j += 32) gv[j] = __ldcg(A.yhat + gx + j);
     }
     __syncthreads();
+    if (A.trace_levels >= 4) tmark(A, 11);
     // leaves: u = ŷ_leaf (local part) + F_leaf g, then y += V u — one contribution per element
     // of y from the far field, as without the split (two addends in y: deterministic)
     const int a = P.lev_first[nlev - 1], b = P.lev_first[nlev];
+    for (int rep = 0; rep < (A.trace_levels == 5 ? 2 : 1); ++rep) {  // 5: profiling (results wrong)
     for (int i = a + warp; i < b; i += NW) {
       const TNode nd = nodes[i];
       if (nd.k == 0) continue;
@@ -533,11 +567,27 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
       const int64_t g = (int64_t)(uint32_t)nd.gy_lo | ((int64_t)nd.gy_hi << 32);
       for (int r = lane; r < nd.R; r += 32) {
         const double2 v = rowdot(sm + nd.pay, r, nd.k, u);
-        atomicAdd(&A.y[g + r].x, v.x);
-        atomicAdd(&A.y[g + r].y, v.y);
+        if (P.y_n > 0) {
+          sm[nd.in + r] = v;
+        } else {
+          atomicAdd(&A.y[g + r].x, v.x);
+          atomicAdd(&A.y[g + r].y, v.y);
+        }
       }
     }
     __syncthreads();
+    if (rep == 0 && A.trace_levels == 5) tmark(A, 13);
+    }
+  }
+  if (A.trace_levels >= 4) tmark(A, 12);
+  if (P.y_n > 0 && tid == 0) {  // y[rows] += the assembled far field: one bulk reduce-add
+    const int64_t yg = (int64_t)(uint32_t)P.y_g_lo | ((int64_t)P.y_g_hi << 32);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the generic-proxy stores above
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(A.y + yg),
+                 "r"(smem_u32(sm + P.y_smem)), "r"(16u * (uint32_t)P.y_n)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem stays valid until read
   }
   tmark(A, 7);
   if (!P.bottom) {  // hand the external children's ŷ to the bottom programs (cumulative release)
@@ -821,6 +871,15 @@ struct Builder {
     // (dead once the couplings are done) when it is large enough, else none
     P.f_base = -1;
     P.f_stride = 0;
+    P.y_smem = 0;
+    P.y_n = 0;
+    P.y_g_lo = P.y_g_hi = 0;
+    if (bottom && x_smem >= 0 && !getenv("H2B_TREE_Y_ATOMIC")) {
+      P.y_smem = x_smem;
+      P.y_n = h->c_size[root];
+      P.y_g_lo = (int32_t)(uint32_t)(int64_t)h->c_start[root];
+      P.y_g_hi = (int32_t)((int64_t)h->c_start[root] >> 32);
+    }
     if (bottom && stage_s && s_total > 0 && !getenv("H2B_TREE_NO_SPLIT")) {
       int kmax = 0;
       for (int i = 0; i < nn; ++i) kmax = std::max(kmax, nodes[i].k);
@@ -1047,6 +1106,8 @@ int h2b_launch_tree(h2b_ctx* h, const TreeDev* d, const double2* xp, double2* yp
   {
     const char* e = getenv("H2B_TREE_TRACE");
     A.trace_levels = e ? atoi(e) : 0;
+    const char* d = getenv("H2B_TREE_DEFER_S");  // A/B aid
+    A.defer_s = d ? atoi(d) : 1;  // measured: step 40.3 vs 41.0 us at cfg2
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(d->n_progs);

@@ -32,6 +32,8 @@ L.h2b_tree_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
 names = ["start", "staged", "ext", "pub_up", "cpl_wait", "dn_wait0", "dn_wait1", "down_end", "end", "up0", "up1", "up2", "up3", "up4", "up5"]
 if os.environ.get("H2B_TREE_TRACE") == "3":  # stamps 9-14 of the downward pass instead
     names[9:15] = ["xg", "couple", "dn0", "dn1", "dn2", "dn3"]
+if os.environ.get("H2B_TREE_TRACE") in ("4", "5"):  # the bottom programs' last step (5: run twice)
+    names[9:15] = ["-", "-", "g_in", "leaves", "leaves1", "-"]
 acc = []
 for rep in range(10):
     if not warm:
@@ -54,7 +56,7 @@ for label, sel in (("bottom", slice(0, nb)), ("top", slice(nb, n))):
     if r.size == 0:
         continue
     print(f"  {label}: " + "  ".join(f"{names[j]} {np.nanmin(r[:, j]):.1f}/{np.nanmedian(r[:, j]):.1f}/{np.nanmax(r[:, j]):.1f}"
-                                    for j in ((0, 1, 2, 3, 4, 9, 10, 5, 6, 11, 12, 13, 14, 7, 8) if os.environ.get("H2B_TREE_TRACE") == "3" else (0, 1, 2, 9, 10, 11, 12, 13, 14, 3, 4, 5, 6, 7, 8)) if np.isfinite(r[:, j]).any()))
+                                    for j in ((0, 1, 2, 3, 4, 9, 10, 5, 6, 11, 12, 13, 14, 7, 8) if os.environ.get("H2B_TREE_TRACE") in ("3", "4", "5") else (0, 1, 2, 9, 10, 11, 12, 13, 14, 3, 4, 5, 6, 7, 8)) if np.isfinite(r[:, j]).any()))
 if os.environ.get("H2B_TREE_TRACE") in ("3", "4"):  # slot 15: SM cycles of warp 0's first coupling colsum
     meta = tr2[:, 31]
     cyc = tr2[:, 15]
