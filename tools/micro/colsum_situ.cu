@@ -116,6 +116,43 @@ __device__ __forceinline__ double2 v5(const double2* P, int R, int w, int sh, co
   for (int m = 1; m < 32; m <<= 1) if (m >= wp) a = cadd(a, shfl_xor2(a, m));
   return a;
 }
+// V6: column-serial (lane c < w sums its column over all rows; no shuffles), 4-row chunks
+__device__ __forceinline__ double2 v6(const double2* P, int R, int w, int sh, const double2* in) {
+  const int c = threadIdx.x & 31;
+  double2 a0 = make_double2(0.0, 0.0), a1 = a0;
+  if (c < w) {
+    int r = 0;
+    for (; r + 4 <= R; r += 4) {
+      const double2 p0 = P[r * w + c], p1 = P[(r + 1) * w + c], p2 = P[(r + 2) * w + c], p3 = P[(r + 3) * w + c];
+      const double2 x0 = in[r], x1 = in[r + 1], x2 = in[r + 2], x3 = in[r + 3];
+      cfma(a0, p0, x0); cfma(a1, p1, x1); cfma(a0, p2, x2); cfma(a1, p3, x3);
+    }
+    for (; r < R; ++r) cfma(a0, P[r * w + c], in[r]);
+  }
+  return cadd(a0, a1);
+}
+// V7: column-serial, 8-row chunks, 4 accumulators
+__device__ __forceinline__ double2 v7(const double2* P, int R, int w, int sh, const double2* in) {
+  const int c = threadIdx.x & 31;
+  double2 a0 = make_double2(0.0, 0.0), a1 = a0, a2 = a0, a3 = a0;
+  if (c < w) {
+    int r = 0;
+    for (; r + 8 <= R; r += 8) {
+      double2 p[8], x[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { p[i] = P[(r + i) * w + c]; x[i] = in[r + i]; }
+      cfma(a0, p[0], x[0]); cfma(a1, p[1], x[1]); cfma(a2, p[2], x[2]); cfma(a3, p[3], x[3]);
+      cfma(a0, p[4], x[4]); cfma(a1, p[5], x[5]); cfma(a2, p[6], x[6]); cfma(a3, p[7], x[7]);
+    }
+    for (; r + 4 <= R; r += 4) {
+      const double2 p0 = P[r * w + c], p1 = P[(r + 1) * w + c], p2 = P[(r + 2) * w + c], p3 = P[(r + 3) * w + c];
+      const double2 x0 = in[r], x1 = in[r + 1], x2 = in[r + 2], x3 = in[r + 3];
+      cfma(a0, p0, x0); cfma(a1, p1, x1); cfma(a2, p2, x2); cfma(a3, p3, x3);
+    }
+    for (; r < R; ++r) cfma(a0, P[r * w + c], in[r]);
+  }
+  return cadd(cadd(a0, a1), cadd(a2, a3));
+}
 template <int V>
 __global__ void k(int R, int w, int sh, long long* out, double2* sink) {
   extern __shared__ double2 sm[];
@@ -130,7 +167,7 @@ __global__ void k(int R, int w, int sh, long long* out, double2* sink) {
   for (int it = 0; it < 4; ++it) {
     __syncwarp();
     const long long t0 = clock64();
-    const double2 s = V == 1 ? colsum_sum(P, R, w, sh, xin) : V == 2 ? colsum_v2(P, R, w, sh, xin) : V == 3 ? colsum_v3(P, R, w, sh, xin) : V == 4 ? v4(P, R, w, sh, xin) : v5(P, R, w, sh, xin);
+    const double2 s = V == 1 ? colsum_sum(P, R, w, sh, xin) : V == 2 ? colsum_v2(P, R, w, sh, xin) : V == 3 ? colsum_v3(P, R, w, sh, xin) : V == 4 ? v4(P, R, w, sh, xin) : V == 5 ? v5(P, R, w, sh, xin) : V == 6 ? v6(P, R, w, sh, xin) : v7(P, R, w, sh, xin);
     if (lane < w) o[lane] = s;
     t[it] = clock64() - t0;
   }
@@ -149,15 +186,20 @@ int main() {
   cudaFuncSetAttribute(k<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   long long h[4];
-  int cases[][3] = {{4, 3, 2}, {24, 8, 3}, {21, 7, 3}, {48, 8, 3}};
+  int cases[][3] = {{4, 3, 2}, {14, 7, 3}, {24, 8, 3}, {32, 6, 3}, {48, 8, 3}};
   for (auto& c : cases)
-    for (int v = 1; v <= 5; ++v) {
+    for (int v = 1; v <= 7; ++v) {
+      if (v == 4 || v == 5) continue;
       const int nt = 256;
       if (v == 1) k<1><<<1, nt, (8 * 1024 + 8 * 64 + 8 * 32) * 16>>>(c[0], c[1], c[2], d, sink);
       if (v == 2) k<2><<<1, nt, (8 * 1024 + 8 * 64 + 8 * 32) * 16>>>(c[0], c[1], c[2], d, sink);
       if (v == 4) k<4><<<1, nt, (8 * 1024 + 8 * 64 + 8 * 32) * 16>>>(c[0], c[1], c[2], d, sink);
       if (v == 5) k<5><<<1, nt, (8 * 1024 + 8 * 64 + 8 * 32) * 16>>>(c[0], c[1], c[2], d, sink);
+      if (v == 6) k<6><<<1, nt, (8 * 1024 + 8 * 64 + 8 * 32) * 16>>>(c[0], c[1], c[2], d, sink);
+      if (v == 7) k<7><<<1, nt, (8 * 1024 + 8 * 64 + 8 * 32) * 16>>>(c[0], c[1], c[2], d, sink);
       if (v == 3) k<3><<<1, nt, (8 * 1024 + 8 * 64 + 8 * 32) * 16>>>(c[0], c[1], c[2], d, sink);
       cudaMemcpy(h, d, 32, cudaMemcpyDeviceToHost);
       printf("R %2d w %d v%d: calls %lld %lld %lld %lld cycles\n", c[0], c[1], v, h[0], h[1], h[2], h[3]);
