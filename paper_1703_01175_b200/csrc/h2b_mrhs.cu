@@ -436,7 +436,10 @@ int run_grouped(const MmItem* items, int n_items, const MmSeg* segs, const MmBuf
 struct MrhsPlan {
   std::vector<int2> launches;  // {item_first, n_items} in execution order
   int split = 1;               // split-K parts of the near-field launch (1: none)
-  double2* scratch = nullptr;  // split planes: split x N x q
+  int csplit = 1;              // split-K parts of the coupling launch (1: none)
+  int couple_launch = -1;      // index of the coupling launch in `launches`
+  int64_t scratch_rows = 0;    // rows of the split planes: max(split x N, csplit x K)
+  double2* scratch = nullptr;  // split planes (near: split x N x q; coupling: csplit x K x q)
   int64_t scratch_q = 0;
   MmItem* items = nullptr;
   MmSeg* segs = nullptr;
@@ -518,18 +521,41 @@ int h2b_mrhs_prepare(h2b_ctx* h) {
     }
     prow_h[P] = r;
   }
+  // small operators (fewer coupling items than two per SM): every item's K-chunks are split into
+  // csplit parts writing partial planes (K x q each), summed into ŷ in a fixed order (as the
+  // near field below; measured at cfg1 q = 64: the coupling launch was the longest phase)
+  int n_couple_items = 0, max_cchunks = 0;
   for (int t = 0; t < P; ++t) {
     const int kt = h->c_rank[t];
     if (kt == 0) continue;
-    const int64_t b0 = h->s_row_ptr[t], b1 = h->s_row_ptr[t + 1];
     const int R = (int)(prow_h[t + 1] - prow_h[t]);
-    for (int m0 = 0; m0 < kt; m0 += MM_M) {
-      const int s0 = B.begin_item();
-      if (R > 0) B.seg(A_S, h->s_off[b0], kt, true, m0, R, B_XHAT, prow_h[t], true);
-      B.end_item(s0, h->c_xoff[t] + m0, std::min(MM_M, kt - m0), B_YHAT, false);
-    }
-    (void)b1;
+    n_couple_items += (kt + MM_M - 1) / MM_M;
+    max_cchunks = std::max(max_cchunks, (R + MM_K - 1) / MM_K);
   }
+  int csplit = 1;
+  if (n_couple_items > 0 && n_couple_items < 2 * 148 && !getenv("H2B_MRHS_NO_CSPLIT"))
+    csplit = std::max(1, std::min({8, (2 * 148 + n_couple_items - 1) / n_couple_items, max_cchunks / 4}));
+  for (int t = 0; t < P; ++t) {
+    const int kt = h->c_rank[t];
+    if (kt == 0) continue;
+    const int64_t b0 = h->s_row_ptr[t];
+    const int R = (int)(prow_h[t + 1] - prow_h[t]);
+    const int nch = (R + MM_K - 1) / MM_K;
+    for (int m0 = 0; m0 < kt; m0 += MM_M) {
+      for (int pt = 0; pt < csplit; ++pt) {
+        const int c_lo = nch * pt / csplit, c_hi = nch * (pt + 1) / csplit;
+        const int r_lo = c_lo * MM_K, r_hi = std::min(R, c_hi * MM_K);
+        const int s0 = B.begin_item();
+        if (r_hi > r_lo)
+          B.seg(A_S, h->s_off[b0] + (int64_t)r_lo * kt, kt, true, m0, r_hi - r_lo, B_XHAT, prow_h[t] + r_lo, true);
+        if (csplit == 1)
+          B.end_item(s0, h->c_xoff[t] + m0, std::min(MM_M, kt - m0), B_YHAT, false);
+        else
+          B.end_item(s0, (int64_t)pt * h->K + h->c_xoff[t] + m0, std::min(MM_M, kt - m0), B_SCR, false);
+      }
+    }
+  }
+  const int couple_launch = (int)B.launches.size();
   B.end_launch();
   // down: root first, children rows [lo; hi] += T ŷ_t
   for (int l : h->down_levels) {
@@ -588,6 +614,9 @@ int h2b_mrhs_prepare(h2b_ctx* h) {
   auto* plan = new MrhsPlan();
   plan->launches = B.launches;
   plan->split = split;
+  plan->csplit = csplit;
+  plan->couple_launch = (int)plan->launches.size() > couple_launch ? couple_launch : -1;
+  plan->scratch_rows = std::max<int64_t>(split > 1 ? (int64_t)split * h->n : 0, csplit > 1 ? (int64_t)csplit * h->K : 0);
   int64_t acc = 0;
   const size_t bi = sizeof(MmItem) * std::max<size_t>(B.items.size(), 1);
   const size_t bs = sizeof(MmSeg) * std::max<size_t>(B.segs.size(), 1);
@@ -635,8 +664,17 @@ int h2b_launch_mrhs(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStrea
   bf.y = yp;
   bf.gather = h->s_xcol;
   bf.scratch = h->mrhs->scratch;
-  for (const int2& L : h->mrhs->launches)
+  for (size_t li = 0; li < h->mrhs->launches.size(); ++li) {
+    const int2& L = h->mrhs->launches[li];
     H2B_TRY(run_grouped(h->mrhs->items + L.x, L.y, h->mrhs->segs, bf, q, st, nl));
+    if ((int)li == h->mrhs->couple_launch && h->mrhs->csplit > 1) {  // ŷ = Σ coupling parts
+      const int64_t plane = h->K * q;
+      k_sum_parts<<<(int)std::min<int64_t>((plane + 255) / 256, 148 * 8), 256, 0, st>>>(
+          h->mrhs->scratch, h->mrhs->csplit, plane, h->yhat);
+      H2B_CHECK_LAUNCH();
+      ++*nl;
+    }
+  }
   if (h->mrhs->split > 1) {
     const int64_t plane = h->n * q;
     k_sum_parts<<<(int)std::min<int64_t>((plane + 255) / 256, 148 * 8), 256, 0, st>>>(h->mrhs->scratch, h->mrhs->split,
@@ -651,12 +689,12 @@ int h2b_launch_mrhs(h2b_ctx* h, const double2* xp, double2* yp, int q, cudaStrea
 int h2b_mrhs_workspace(h2b_ctx* h, int q) {
   H2B_TRY(h2b_mrhs_prepare(h));
   MrhsPlan* p = h->mrhs;
-  if (p->split <= 1 || p->scratch_q >= q) return H2B_OK;
+  if (p->scratch_rows == 0 || p->scratch_q >= q) return H2B_OK;
   h2b_release_graphs(h);  // captured graphs hold the old planes
   cudaFree(p->scratch);
   p->scratch = nullptr;
   p->scratch_q = 0;
-  H2B_CUDA_TRY(cudaMalloc(&p->scratch, sizeof(double2) * (size_t)p->split * h->n * q));
+  H2B_CUDA_TRY(cudaMalloc(&p->scratch, sizeof(double2) * (size_t)p->scratch_rows * q));
   p->scratch_q = q;
   return H2B_OK;
 }
