@@ -58,7 +58,7 @@ void free_ctx(h2b_ctx* h) {
                   h->span_ops, h->near_items, h->near_blks, h->couple_items, h->tasks, h->deps,
                   h->near_tasks, h->leaf_items, h->couple_groups, h->ctrl, h->flags, h->trace,
                   h->rec_pool, h->l2_prefetch, h->cta_lists, h->task_list, h->near_recs, h->near_idx, h->wbuf, h->ydeep,
-                  h->ks_partial, h->ks_vals, h->near_trace};
+                  h->ks_partial, h->ks_vals, h->near_trace, h->iperm};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->far_stream) cudaStreamDestroy(h->far_stream);
@@ -407,14 +407,34 @@ int h2b_matvec_host(h2b_handle h, const void* x, void* y, int q) {
     }
     if (!y_pinned) ys = (char*)h->hpin + bytes;
   }
+  // pinned buffers are read / written by the permutation kernels themselves over PCIe (zero
+  // copy: one kernel per direction instead of a DMA node plus a gather / scatter kernel);
+  // H2B_HOST_ZC=0 keeps the DMA path (A/B timing)
+  static const bool zc_env = [] {
+    const char* e = getenv("H2B_HOST_ZC");
+    return !(e && !strcmp(e, "0"));
+  }();
+  void* xs_dev = nullptr;
+  void* ys_dev = nullptr;
+  bool zc = zc_env && is_pinned(xs) && is_pinned(ys) && cudaHostGetDevicePointer(&xs_dev, const_cast<void*>(xs), 0) == cudaSuccess &&
+            cudaHostGetDevicePointer(&ys_dev, ys, 0) == cudaSuccess;
+  if (!zc) cudaGetLastError();
+  if (zc) H2B_TRY(h2b_ensure_iperm(h));
   auto enqueue = [&](cudaStream_t s, bool in_graph) -> int {
-    H2B_CUDA_TRY(cudaMemcpyAsync(dx, xs, bytes, cudaMemcpyHostToDevice, s));
-    int r = h2b_launch_gather(h->perm, h->n, dx, dxp, q, s);
+    int r = H2B_OK;
+    if (zc) {
+      r = h2b_launch_host_in((const double2*)xs_dev, h->iperm, h->n, dxp, q, s);
+    } else {
+      H2B_CUDA_TRY(cudaMemcpyAsync(dx, xs, bytes, cudaMemcpyHostToDevice, s));
+      r = h2b_launch_gather(h->perm, h->n, dx, dxp, q, s);
+    }
     if (!r) {
       int nl = 0;
       r = in_graph ? h2b_enqueue_matvec(h, dxp, dyp, q, s, &nl) : h2b_run_matvec(h, dxp, dyp, q, s);
     }
-    if (!r) r = h2b_launch_scatter(h->perm, h->n, dyp, dy, q, s);
+    if (r) return r;
+    if (zc) return h2b_launch_host_out(dyp, h->iperm, h->n, (double2*)ys_dev, q, s);
+    r = h2b_launch_scatter(h->perm, h->n, dyp, dy, q, s);
     if (r) return r;
     H2B_CUDA_TRY(cudaMemcpyAsync(ys, dy, bytes, cudaMemcpyDeviceToHost, s));
     return H2B_OK;

@@ -287,6 +287,7 @@ struct h2b_ctx {
   // near-field stream kernel (runs beside the far-field task graph; both add into a zeroed y)
   int4* near_recs = nullptr;           // near task records
   int2* near_idx = nullptr;            // per near task {first slot, slots}
+  int64_t* iperm = nullptr;         // inverse of perm (original index -> packed), host path
   uint64_t* near_trace = nullptr;  // H2B_NEAR_TRACE: stamps per near CTA
   int near_early = 0;               // first record / block per CTA known at plan time
   std::vector<int2> near_first_rec;
@@ -356,6 +357,9 @@ int h2b_order_end(h2b_ctx* h, cudaStream_t st);
 int h2b_run_phase(h2b_ctx* h, int phase, const double2* xp, double2* yp, int q, cudaStream_t st);
 int h2b_launch_gather(const int64_t* perm, int64_t n, const double2* in, double2* out, int q,
                       cudaStream_t st);
+int h2b_launch_host_in(const double2* xh, const int64_t* iperm, int64_t n, double2* out, int q, cudaStream_t st);
+int h2b_launch_host_out(const double2* in, const int64_t* iperm, int64_t n, double2* yh, int q, cudaStream_t st);
+int h2b_ensure_iperm(h2b_ctx* h);
 int h2b_launch_scatter(const int64_t* perm, int64_t n, const double2* in, double2* out, int q,
                        cudaStream_t st);
 void h2b_release_graphs(h2b_ctx* h);

@@ -41,6 +41,34 @@ __global__ void k_scatter(const int64_t* __restrict__ perm, int64_t n, const dou
   }
 }
 
+// host <-> device through mapped pinned memory (zero copy): x read over PCIe in the original
+// order (contiguous, coalesced) and written to its packed position, y written over PCIe in the
+// original order; replaces a DMA node plus a gather / scatter kernel on the host path
+__global__ void k_host_in(const double2* __restrict__ xh, const int64_t* __restrict__ iperm, int64_t n,
+                          double2* __restrict__ out, int q) {
+  const int64_t tot = n * q;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = e / q, c = e - o * q;
+    out[iperm[o] * q + c] = xh[e];
+  }
+}
+
+__global__ void k_host_out(const double2* __restrict__ in, const int64_t* __restrict__ iperm, int64_t n,
+                           double2* __restrict__ yh, int q) {
+  const int64_t tot = n * q;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = e / q, c = e - o * q;
+    yh[e] = in[iperm[o] * q + c];
+  }
+}
+
+__global__ void k_invert_perm(const int64_t* __restrict__ perm, int64_t n, int64_t* __restrict__ iperm) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    iperm[perm[i]] = i;
+}
+
 int grid_for(int64_t tot) {
   int64_t g = (tot + 255) / 256;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
@@ -116,6 +144,28 @@ int h2b_launch_scatter(const int64_t* perm, int64_t n, const double2* in, double
                        cudaStream_t st) {
   k_scatter<<<grid_for(n * q), 256, 0, st>>>(perm, n, in, out, q);
   H2B_CHECK_LAUNCH();
+  return H2B_OK;
+}
+
+int h2b_launch_host_in(const double2* xh, const int64_t* iperm, int64_t n, double2* out, int q, cudaStream_t st) {
+  k_host_in<<<grid_for(n * q), 256, 0, st>>>(xh, iperm, n, out, q);
+  H2B_CHECK_LAUNCH();
+  return H2B_OK;
+}
+
+int h2b_launch_host_out(const double2* in, const int64_t* iperm, int64_t n, double2* yh, int q, cudaStream_t st) {
+  k_host_out<<<grid_for(n * q), 256, 0, st>>>(in, iperm, n, yh, q);
+  H2B_CHECK_LAUNCH();
+  return H2B_OK;
+}
+
+int h2b_ensure_iperm(h2b_ctx* h) {
+  if (h->iperm) return H2B_OK;
+  H2B_CUDA_TRY(cudaMalloc(&h->iperm, sizeof(int64_t) * std::max<int64_t>(h->n, 1)));
+  k_invert_perm<<<grid_for(h->n), 256>>>(h->perm, h->n, h->iperm);
+  H2B_CHECK_LAUNCH();
+  H2B_CUDA_TRY(cudaDeviceSynchronize());
+  h->device_bytes += sizeof(int64_t) * h->n;
   return H2B_OK;
 }
 

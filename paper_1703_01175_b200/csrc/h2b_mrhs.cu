@@ -535,6 +535,7 @@ int h2b_mrhs_prepare(h2b_ctx* h) {
   int csplit = 1;
   if (n_couple_items > 0 && n_couple_items < 2 * 148 && !getenv("H2B_MRHS_NO_CSPLIT"))
     csplit = std::max(1, std::min({8, (2 * 148 + n_couple_items - 1) / n_couple_items, max_cchunks / 4}));
+  if (const char* e = getenv("H2B_MRHS_CSPLIT")) csplit = std::max(1, std::min(16, atoi(e)));  // tuning aid
   for (int t = 0; t < P; ++t) {
     const int kt = h->c_rank[t];
     if (kt == 0) continue;
@@ -583,6 +584,7 @@ int h2b_mrhs_prepare(h2b_ctx* h) {
   int split = 1;
   if (n_near_items > 0 && n_near_items < 2 * 148)
     split = std::max(1, std::min({8, (2 * 148 + n_near_items - 1) / n_near_items, max_segs / 4}));
+  if (const char* e = getenv("H2B_MRHS_SPLIT")) split = std::max(1, std::min(16, atoi(e)));  // tuning aid
   for (int t : h->h_leaves) {
     const int nt = h->c_size[t];
     for (int m0 = 0; m0 < nt; m0 += MM_M) {
