@@ -662,10 +662,13 @@ bool plan_mega(const h2b_ctx* h, const std::vector<CoupleItem>& citems_all,
     const double row_bytes = ns * 16.0 * avg_nb;
     const int rpp = 256 / (ns / 2);  // rows per pass of a 256-thread CTA
     int R = 1;
-    // tasks of ~NEAR_TASK_BYTES: claimed dynamically, so small tasks keep the tail short
+    // tasks of ~NEAR_TASK_BYTES: small tasks keep the tail of the static split short.  (Choosing
+    // the slice height by an estimated near-field makespan made cfg1's near field 37 -> 25 us
+    // but its step 43 -> 46 us: the faster stream slows the concurrent far field more.)
     double task_bytes = NEAR_TASK_BYTES;
     if (const char* e = getenv("H2B_NEAR_TASK_BYTES")) task_bytes = std::max(4e3, atof(e));  // tuning aid
     while (R * 2 * rpp <= ns && R * 2 <= (ns == 32 ? 2 : 8) && R * 2 * rpp * row_bytes <= task_bytes) R *= 2;
+    if (const char* e = getenv("H2B_NEAR_R")) R = std::max(1, std::min(ns == 32 ? 2 : 8, atoi(e)));  // tuning aid
     mp.ns = ns;
     mp.r = R;
     const int rb = R * rpp;
