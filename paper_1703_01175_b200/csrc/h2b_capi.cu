@@ -311,11 +311,13 @@ struct CopyPool {
     clock_gettime(CLOCK_MONOTONIC, &ts);
     return ts.tv_sec * 1e6 + ts.tv_nsec * 1e-3;
   }
+  std::mutex job_mu;  // one job at a time (handles used from several threads share the pool)
   void copy(void* d, const void* s_, size_t n) {
     if (nw == 0 || n < (256u << 10)) {
       memcpy(d, s_, n);
       return;
     }
+    std::lock_guard<std::mutex> job(job_mu);
     dst = (char*)d;
     src = (const char*)s_;
     bytes = n;
