@@ -34,7 +34,7 @@ constexpr int BQ = 64;        // max right-hand sides per block
 constexpr int GT = 256;       // threads of the GEMM kernels
 constexpr int KR = 16;        // rows per smem tile of k_bgram / k-slice of k_bupdate
 constexpr int MROWS = 32;     // output rows per CTA of k_bupdate
-constexpr int CHOL_SMEM = 2 * BQ * (BQ + 1) * 16;  // k_chol_small: G / R and R^-1
+constexpr int CHOL_SMEM = 3 * BQ * (BQ + 1) * 16;  // k_chol_small: G (updated), R and R^-1
 
 // ---------------------------------------------------------------------------------------------
 // k_bgram: partial[(blk * nchunk + c)] (q x q) = Σ_{r in chunk c} conj(A_blk[r][a]) B[r][b]
@@ -200,45 +200,49 @@ __global__ void __launch_bounds__(GT) k_chol_small(const double2* __restrict__ G
     thr = 1e-28 * mx;
   }
   __syncthreads();
+  // One barrier per step: row k is scaled into R (a separate array) while the trailing update
+  // reads the unscaled row (S[i][j] -= conj(S[k][i]) S[k][j] / d^2), so no thread writes what
+  // another reads within a step; 1/d from one reciprocal square root (no per-element divides).
+  auto Rm = reinterpret_cast<double2(*)[BQ + 1]>(chol_sm + 2 * BQ * (BQ + 1));
   for (int k = 0; k < q; ++k) {
     const double d2 = S[k][k].x;
     if (tid == 0 && !(d2 == d2)) bad = 1;  // NaN
     const bool dk = !(d2 > thr);
-    const double d = dk ? 1.0 : sqrt(d2);
+    const double inv_d = dk ? 1.0 : rsqrt(d2);
+    const double inv_d2 = inv_d * inv_d;
     if (tid == 0) defl[k] = dk;
-    __syncthreads();
-    for (int j = k + tid; j < q; j += GT) {
+    for (int j = tid; j < q; j += GT) {
       const double2 v = S[k][j];
-      S[k][j] = dk ? make_double2(j == k ? 1.0 : 0.0, 0.0)
-                   : (j == k ? make_double2(d, 0.0) : make_double2(v.x / d, v.y / d));
+      Rm[k][j] = j < k ? make_double2(0.0, 0.0)
+                 : dk  ? make_double2(j == k ? 1.0 : 0.0, 0.0)
+                       : (j == k ? make_double2(d2 * inv_d, 0.0) : make_double2(v.x * inv_d, v.y * inv_d));
     }
-    __syncthreads();
     // trailing update on a 16 x 16 thread grid (no integer division per element)
-    for (int i = k + 1 + (tid >> 4); i < q; i += 16) {
-      const double2 a = S[k][i];
-      for (int j = i + ((tid & 15) - i % 16 + 16) % 16; j < q; j += 16) {
-        const double2 b = S[k][j];
-        // S[i][j] -= conj(a) b
-        S[i][j].x -= a.x * b.x + a.y * b.y;
-        S[i][j].y -= a.x * b.y - a.y * b.x;
+    if (!dk)
+      for (int i = k + 1 + (tid >> 4); i < q; i += 16) {
+        const double2 a = S[k][i];
+        for (int j = i + ((tid & 15) - i % 16 + 16) % 16; j < q; j += 16) {
+          const double2 b = S[k][j];
+          // S[i][j] -= conj(a) b / d^2
+          S[i][j].x -= (a.x * b.x + a.y * b.y) * inv_d2;
+          S[i][j].y -= (a.x * b.y - a.y * b.x) * inv_d2;
+        }
       }
-    }
     __syncthreads();
   }
-  // zero the strict lower part; X = I; then Gauss-Jordan on [R | X] from the last row up:
-  // row i /= R[i][i], then row r -= R[r][i] row i for r < i (all elements in parallel)
+  // X = R^-1 by Gauss-Jordan from the last row up, one barrier per step: rows r < i take
+  // X[r] -= (R[r][i] / R[i][i]) X[i] with row i left unscaled until the end (row i is not
+  // written in its own step)
   for (int e = tid; e < q * q; e += GT) {
     const int i = e / q, j = e % q;
-    if (i > j) S[i][j] = make_double2(0.0, 0.0);
     X[i][j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
   }
   __syncthreads();
   for (int i = q - 1; i >= 0; --i) {
-    const double rr = S[i][i].x;  // 1 for a deflated pivot
-    for (int c = i + tid; c < q; c += GT) X[i][c] = make_double2(X[i][c].x / rr, X[i][c].y / rr);
-    __syncthreads();
+    const double irr = 1.0 / Rm[i][i].x;  // 1 for a deflated pivot
     for (int r = tid >> 4; r < i; r += 16) {
-      const double2 f = S[r][i];
+      const double2 f0 = Rm[r][i];
+      const double2 f = make_double2(f0.x * irr, f0.y * irr);
       for (int c = i + (tid & 15); c < q; c += 16) {
         const double2 x = X[i][c];
         X[r][c].x -= f.x * x.x - f.y * x.y;
@@ -248,8 +252,14 @@ __global__ void __launch_bounds__(GT) k_chol_small(const double2* __restrict__ G
     __syncthreads();
   }
   for (int e = tid; e < q * q; e += GT) {
+    const int i = e / q;
+    const double irr = 1.0 / Rm[i][i].x;
+    X[i][e % q] = make_double2(X[i][e % q].x * irr, X[i][e % q].y * irr);
+  }
+  __syncthreads();
+  for (int e = tid; e < q * q; e += GT) {
     const int i = e / q, j = e % q;
-    Rout[e] = defl[i] ? make_double2(0.0, 0.0) : S[i][j];  // deflated rows of R are zero
+    Rout[e] = defl[i] ? make_double2(0.0, 0.0) : Rm[i][j];  // deflated rows of R are zero
     RinvOut[e] = X[i][j];
   }
   if (tid == 0 && bad && status) status[0] = 1;
