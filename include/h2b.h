@@ -112,8 +112,9 @@ int h2b_matvec_perm(h2b_handle h, const void* x_perm, void* y_perm, int q, void*
 
 /* y = S x with HOST buffers in the ORIGINAL ordering, (N, q) row-major:
  * the drop-in for arith.matvec / arith.matmat_apply (arith.py:108-130).
- * Includes host->device copy, the permutation gather, the matvec, the
- * scatter and device->host copy; synchronous. */
+ * Synchronous; one CUDA graph per call: pinned buffers are read and written
+ * over PCIe by the permutation kernels themselves (zero copy), pageable ones
+ * (numpy) are staged through the handle's pinned buffers by host threads. */
 int h2b_matvec_host(h2b_handle h, const void* x, void* y, int q);
 
 /* Profiling split of h2b_matvec_perm: phase 0 = near-field only (y overwritten,
