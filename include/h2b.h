@@ -244,6 +244,8 @@ int h2b_stream_read(const void* src, size_t bytes, void* sink_dev, void* stream)
 /* Keeps `stream` busy for `ns` nanoseconds (one thread polling %globaltimer): enqueued before a
  * timed region's start event so that host-side launch latency does not count as device time. */
 int h2b_spin_ns(uint64_t ns, void* stream);
+/* Development aid: a one-thread kernel on `stream` writes %globaltimer (ns) to dst_dev[0]. */
+int h2b_stamp_ns(uint64_t* dst_dev, void* stream);
 /* Stage II of the H² builder on the device: nested bases, transfers and
  * couplings from the Stage-I grouped factors (the reference's build_all_cluster_ab output) of a
  * packed block structure.  Results stay on the device until fetched: h2b_builder_ranks (k per

@@ -26,7 +26,7 @@ EXPORTED = (
     "h2b_plan_bcast_rows", "h2b_ipc_get_handle", "h2b_ipc_open", "h2b_ipc_close",
     "h2b_plan_set_peer_offset", "h2b_device_alloc", "h2b_device_free", "h2b_plan_set_gather",
     "h2b_plan_set_near_fast", "h2b_plan_set_couple_fast", "h2b_fill_synthetic_raw",
-    "h2b_plan_fill_synthetic", "h2b_plan_fill_near", "h2b_tree_trace", "h2b_near_trace", "h2b_gmres_state_elems", "h2b_gmres_givens", "h2b_zscale_dev", "h2b_block_gmres", "h2b_stream_read", "h2b_spin_ns", "h2b_builder_create", "h2b_builder_ranks", "h2b_builder_fetch", "h2b_builder_destroy", "h2b_stage1_run", "h2b_stage1_fetch", "h2b_stage1_destroy", "h2b_stage1_device_ptrs", "h2b_exact_rows",
+    "h2b_plan_fill_synthetic", "h2b_plan_fill_near", "h2b_tree_trace", "h2b_near_trace", "h2b_gmres_state_elems", "h2b_gmres_givens", "h2b_zscale_dev", "h2b_block_gmres", "h2b_stream_read", "h2b_spin_ns", "h2b_stamp_ns", "h2b_builder_create", "h2b_builder_ranks", "h2b_builder_fetch", "h2b_builder_destroy", "h2b_stage1_run", "h2b_stage1_fetch", "h2b_stage1_destroy", "h2b_stage1_device_ptrs", "h2b_exact_rows",
 )
 OPT_GRAPHS, OPT_MEGA, OPT_TRACE, OPT_DEBUG, OPT_MRHS, OPT_TREE = 1, 2, 3, 4, 5, 6
 Q_LAUNCHES_Q1, Q_SPAN_MODE, Q_SPLIT_LEVEL, Q_TOP_STAGED, Q_DEVICE_BYTES = 1, 2, 3, 4, 5

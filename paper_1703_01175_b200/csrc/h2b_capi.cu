@@ -570,7 +570,7 @@ int h2b_query(h2b_handle h, int what, int64_t* out) {
       *out = c.error | te;
       return H2B_OK;
     }
-    case H2B_Q_TREE: *out = h->tree ? (int64_t)h->tree_progs | ((int64_t)h->tree_ls << 16) | ((int64_t)h->tree_lt << 24) : 0; return H2B_OK;
+    case H2B_Q_TREE: *out = h->tree ? (int64_t)h->tree_progs | ((int64_t)h->tree_ls << 16) | ((int64_t)h->tree_lt << 24) | ((int64_t)h->tree_flat << 30) | ((int64_t)h->tree_smem << 32) : 0; return H2B_OK;
     default: break;
   }
   h2b_set_error("h2b_query: unknown key");

@@ -292,6 +292,10 @@ struct h2b_ctx {
   int near_early = 0;               // first record / block per CTA known at plan time
   std::vector<int2> near_first_rec;
   std::vector<longlong2> near_first_blk;
+  // static split: CTA c's rows of y {first, count} (each row belongs to exactly one CTA) and
+  // whether they tile [0, n) — then the near kernel zeroes y itself (no memset node)
+  std::vector<int2> near_zero_row;
+  int near_zero_ok = 0;
   int n_near_tasks = 0, near_rec_max = 0, near_nst = 0, near_smem = 0, near_grid = 0;
   uint32_t near_delay_ns = 0;  // tuning aid (H2B_DEBUG_NEAR_DELAY_NS)
   int near_static = 0;         // near tasks split statically over the CTAs (H2B_NEAR_STATIC)
@@ -299,7 +303,7 @@ struct h2b_ctx {
   // far field as subtree programs (h2b_tree.cu): replaces k_mega beside k_near_stream when set
   TreeDev* tree = nullptr;
   int use_tree = 1;  // H2B_OPT_TREE
-  int tree_ls = 0, tree_lt = 0, tree_progs = 0, tree_smem = 0;
+  int tree_ls = 0, tree_lt = 0, tree_progs = 0, tree_smem = 0, tree_flat = 0;
   // flattened bottom tier (0 = off): W buffer and the deep spans' y_deep
   int mega_flat = 0;
   double2* wbuf = nullptr;

@@ -269,3 +269,19 @@ extern "C" int h2b_spin_ns(uint64_t ns, void* stream) {
   H2B_CHECK_LAUNCH();
   return H2B_OK;
 }
+
+// Development aid: writes %globaltimer (ns) to dst_dev[0] from a one-thread kernel on `stream`
+// (tools/step_trace.py brackets a step with two of them to place the kernels' own stamps).
+namespace {
+__global__ void k_stamp_ns(uint64_t* dst) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  *dst = t;
+}
+}  // namespace
+
+extern "C" int h2b_stamp_ns(uint64_t* dst_dev, void* stream) {
+  k_stamp_ns<<<1, 1, 0, (cudaStream_t)stream>>>(dst_dev);
+  H2B_CHECK_LAUNCH();
+  return H2B_OK;
+}

@@ -89,7 +89,12 @@ struct NearArgs {
   // kernel's first two copies need no index or record load (one memory round trip to the first
   // block instead of three: at kernel start the far kernel's staging burst makes each ~2 us)
   int early;
+  // no memset of y before the step (r02): with the static split every row of y is updated by
+  // exactly one CTA, which zeroes its rows [zero_row[c].x, + zero_row[c].y) first and then counts
+  // itself in *zeroed (release); the far-field kernel adds into y only after all CTAs counted
+  uint32_t* zeroed;  // nullptr: y is zeroed by the caller
   int2 first_rec[NEAR_MAXG];
+  int2 zero_row[NEAR_MAXG];
   longlong2 first_blk[NEAR_MAXG];
 };
 
@@ -178,6 +183,19 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
     }
   }
   __syncthreads();
+  if (A.zeroed && threadIdx.x < MNT) {
+    // the consumers zero the CTA's rows while the producer fills the ring (their first update of
+    // y comes after the first block has landed and been summed); the count follows a consumer-only
+    // barrier, so every zero store of the CTA is ordered before it
+    const int2 zr = A.zero_row[blockIdx.x];
+    for (int i = threadIdx.x; i < zr.y; i += MNT) A.y[zr.x + i] = make_double2(0.0, 0.0);
+    __threadfence();
+    asm volatile("bar.sync 1, %0;" ::"n"(MNT) : "memory");
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(A.zeroed, 1u);
+    }
+  }
   if (threadIdx.x >= MNT) {
     // ---------------- producer (one lane) ----------------
     if (threadIdx.x == MNT) {
@@ -779,18 +797,25 @@ int h2b_near_stream_set_smem(int ns, int r, int bytes) {
   return H2B_OK;
 }
 
-int h2b_launch_tree(h2b_ctx* h, const TreeDev* d, const double2* xp, double2* yp, cudaStream_t st);
+int h2b_launch_tree(h2b_ctx* h, const TreeDev* d, const double2* xp, double2* yp, cudaStream_t st, int wait_zeroed);
+uint32_t* h2b_tree_zeroed_counter(const TreeDev* d);
 
 // y = 0; then k_near_stream on st and k_mega (or the tree programs) on h->far_stream,
 // concurrently (fork / join)
 int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st) {
-  if (!(h->mega_debug & 8)) H2B_CUDA_TRY(cudaMemsetAsync(yp, 0, sizeof(double2) * h->n, st));
   const bool run_far = h->mega_grid > 0 && !(h->mega_debug & 2);
   const bool run_near = h->n_near_tasks > 0 && !(h->mega_debug & 4);
+  // No memset node (r02): when every row of y belongs to exactly one near CTA (static split),
+  // the near kernel zeroes its own rows and the tree kernel's bulk adds wait for all near CTAs'
+  // counts (k_near_stream / k_far_tree); the near kernel never waits on the tree kernel, so the
+  // two can start in any order.
+  static const bool nozero_off = getenv("H2B_Y_MEMSET") != nullptr;
+  uint32_t* zeroed = run_far && run_near && h->tree && h->near_zero_ok && !nozero_off ? h2b_tree_zeroed_counter(h->tree) : nullptr;
+  if (!zeroed && !(h->mega_debug & 8)) H2B_CUDA_TRY(cudaMemsetAsync(yp, 0, sizeof(double2) * h->n, st));
   if (run_far && h->tree) {  // subtree programs (h2b_tree.cu) in k_mega's place
     H2B_CUDA_TRY(cudaEventRecord(h->ev_fork, st));
     H2B_CUDA_TRY(cudaStreamWaitEvent(h->far_stream, h->ev_fork, 0));
-    H2B_TRY(h2b_launch_tree(h, h->tree, xp, yp, h->far_stream));
+    H2B_TRY(h2b_launch_tree(h, h->tree, xp, yp, h->far_stream, zeroed ? h->near_grid : 0));
   } else if (run_far) {
     H2B_CUDA_TRY(cudaEventRecord(h->ev_fork, st));
     H2B_CUDA_TRY(cudaStreamWaitEvent(h->far_stream, h->ev_fork, 0));
@@ -861,6 +886,9 @@ int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st)
     N.dbg = h->near_dbg;
     N.trace = h->near_trace;
     N.early = h->near_static && h->near_early && h->near_grid <= NEAR_MAXG;
+    N.zeroed = zeroed;
+    if (zeroed)
+      for (int c = 0; c < h->near_grid; ++c) N.zero_row[c] = h->near_zero_row[c];
     if (N.early)
       for (int c = 0; c < h->near_grid; ++c) {
         N.first_rec[c] = h->near_first_rec[c];

@@ -1339,6 +1339,7 @@ int h2b_prepare(h2b_ctx* h) {
       if (const char* e = getenv("H2B_NEAR_GRID")) h->near_grid = std::max(1, std::min(sms, atoi(e)));  // tuning aid
       // each CTA's first record and first block (static split): kernel parameters
       h->near_early = 0;
+      auto leaf_has_near = [&](int t) { return h->d_row_ptr[t + 1] > h->d_row_ptr[t]; };
       h->near_first_rec.assign(h->near_grid, int2{0, 0});
       h->near_first_blk.assign(h->near_grid, longlong2{0, 0});
       if (mp.ns > 0 && h->near_grid <= NEAR_MAXG && !getenv("H2B_NEAR_NO_EARLY")) {
@@ -1354,6 +1355,34 @@ int h2b_prepare(h2b_ctx* h) {
                                            (long long)(uint32_t)b0.z | ((long long)b0.w << 32)};
         }
         h->near_early = 1;
+      }
+      // rows of y per CTA of the static split (tasks are in row order: whole leaves, or row
+      // slices of one leaf): valid when the ranges tile [0, n)
+      h->near_zero_ok = 0;
+      h->near_zero_row.assign(h->near_grid, int2{0, 0});
+      if (h->near_static && mp.ns > 0 && h->near_grid <= NEAR_MAXG && h->n < (int64_t)1 << 31 &&
+          mp.near_tasks.size() == mp.near_idx.size()) {
+        const int nt = (int)mp.near_tasks.size();
+        const int rb = mp.r * (256 / (mp.ns / 2));
+        int64_t next = 0;
+        bool ok = true;
+        for (int c = 0; c < h->near_grid && ok; ++c) {
+          const int t0 = (int)((int64_t)c * nt / h->near_grid), t1 = (int)((int64_t)(c + 1) * nt / h->near_grid);
+          int64_t first = next;
+          for (int t = t0; t < t1 && ok; ++t) {
+            const NearTask& k = mp.near_tasks[t];
+            for (int i = 0; i < k.n_leaves && ok; ++i) {
+              const int leaf = h->h_leaves[k.leaf_first + i];
+              const bool sliced = rb < mp.ns;
+              const int64_t a = h->c_start[leaf] + (sliced ? k.row0 : 0);
+              const int64_t b = sliced ? a + rb : a + h->c_size[leaf];
+              ok = a == next && leaf_has_near(leaf);
+              next = b;
+            }
+          }
+          h->near_zero_row[c] = int2{(int)first, (int)(next - first)};
+        }
+        h->near_zero_ok = ok && next == h->n ? 1 : 0;
       }
       if (getenv("H2B_NEAR_TRACE") && !h->near_trace) {  // development aid (h2b_near_trace)
         H2B_CUDA_TRY(cudaMalloc(&h->near_trace, sizeof(uint64_t) * 24 * sms));

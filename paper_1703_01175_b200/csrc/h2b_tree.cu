@@ -32,6 +32,7 @@
 namespace {
 
 constexpr int TNT = 256;  // threads per program CTA
+constexpr int TREE_FLAT_EXTRA = 6 * 1024;  // shared memory a flat-top program may use beyond the budget
 constexpr int TREE_MAXLEV = 24;
 
 // node of a program (64 bytes, staged into shared memory; offsets in double2 elements).  Every
@@ -56,7 +57,12 @@ struct TCopy {  // global -> smem bulk copy
   int64_t src;  // element offset in the source buffer
   int32_t kind, elems, smem, pad;
 };
-enum TSrc : int32_t { TS_X = 0, TS_V, TS_T, TS_S, TS_NODES, TS_GIDX, TS_N };
+enum TSrc : int32_t { TS_X = 0, TS_V, TS_T, TS_S, TS_NODES, TS_GIDX, TS_FM, TS_FH, TS_FF, TS_N };
+// TS_FM / TS_FH / TS_FF: the flattened top tier of a bottom program (chains M up to its
+// ancestors, the panels H = Sᵀ Mᵀ of the ancestors, the chains F from its root down to its
+// leaves; see "flat top" below).  M is staged with the transfers; H and F are requested late,
+// into the place of the coupling panels.
+__host__ __device__ inline bool ts_late(int kind) { return kind >= TS_FH; }
 
 struct TProg {
   int32_t n_nodes, nlev, n_copy, copy_first;
@@ -70,6 +76,13 @@ struct TProg {
   // area, dead after the upward pass) and added to y by ONE bulk reduce-add (instead of an
   // atomic per element): y_n rows from smem y_smem to global row y_g
   int32_t y_smem, y_n, y_g_lo, y_g_hi;
+  // flat top (bottom programs, no top programs): n_flat pseudo nodes (one per ancestor above the
+  // split level) at nodes[flat_first ..]; gather rows of the ancestors' sources: n_frow headers
+  // {log2 partials per entry, first entry, valid entries, first x̂g row} at smem element frow_smem,
+  // the entries' first partial (index into px) as int32 at smem element ebase_smem
+  int32_t n_flat, flat_first, n_frow, frow_smem;
+  int32_t ebase_smem, px_stride, fh_bytes, split_mode;  // split_mode: 0 none, 1 F chains formed here, 2 staged
+  int32_t n_wait_far, wait_far_first, fpad2, fpad3;  // flat top: the programs whose partials are read
 };
 
 struct TreeArgs {
@@ -80,11 +93,14 @@ struct TreeArgs {
   double2* xhat;
   double2* yhat;
   double2* y;
+  double2* px;  // flat top: partial x̂ of every ancestor level from every bottom program
   uint32_t* flags_up;
   uint32_t* flags_down;
   MegaCtrl* ctrl;
   uint64_t* trace;  // optional (H2B_TREE_TRACE): 16 timestamps per program
+  int wait_zeroed;   // > 0: y is zeroed by the near-field kernel's CTAs; bulk adds wait for this many counts
   int defer_s;       // request the staged coupling panels after the up-pass operands
+  int dbg;           // profiling only (H2B_TREE_DBG, results wrong): 1 exit once staged, 2 idle 25 us then exit
   int trace_levels;  // H2B_TREE_TRACE=2: stamps 9-14 per level of the upward pass; 3: of the downward pass
 };
 
@@ -299,7 +315,7 @@ __device__ __forceinline__ void cta_rowdot(const TNode* nodes, int a, int b, int
 __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
   extern __shared__ __align__(16) double2 sm[];
   // [0]: nodes, gather list, x, V (the leaf level)  [1]: staged S panels  [2]: T (internal levels)
-  __shared__ __align__(8) uint64_t bar[3];
+  __shared__ __align__(8) uint64_t bar[4];
   __shared__ uint32_t s_epoch;
   __shared__ TProg P;  // the program header (global loads would recur after every fence)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -311,6 +327,7 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     mbar_init(&bar[2], 1);
+    mbar_init(&bar[3], 1);
   }
   for (int i = tid; i < (int)(sizeof(TProg) / 4); i += TNT)
     reinterpret_cast<int32_t*>(&P)[i] = reinterpret_cast<const int32_t*>(gP)[i];
@@ -329,6 +346,11 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
   const bool defer_s = A.defer_s && P.pad[0] > 0;
   for (int i = tid; i < n_copy; i += TNT) {
     const TCopy c = i == tid ? cp0 : A.copies[c0 + i];
+    if (ts_late(c.kind)) {  // requested later, into the coupling panels' place
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const double2*)A.src[TS_FH] + c.src),
+                   "r"(16u * (uint32_t)c.elems) : "memory");
+      continue;
+    }
     if (defer_s && c.kind == TS_S) continue;
     if (c.kind == TS_S && c.smem < 0) {  // coupling panels read from L2 by the couplings: warm them
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const double2*)A.src[TS_S] + c.src),
@@ -336,9 +358,10 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
       continue;
     }
     const void* base = c.kind == TS_X ? A.src[TS_X] : c.kind == TS_V ? A.src[TS_V] : c.kind == TS_T ? A.src[TS_T]
-                     : c.kind == TS_S ? A.src[TS_S] : c.kind == TS_NODES ? A.src[TS_NODES] : A.src[TS_GIDX];
+                     : c.kind == TS_S ? A.src[TS_S] : c.kind == TS_NODES ? A.src[TS_NODES]
+                     : c.kind == TS_GIDX ? A.src[TS_GIDX] : A.src[TS_FM];
     bulk_g2s(sm + c.smem, (const double2*)base + c.src, 16u * (uint32_t)c.elems,
-             &bar[c.kind == TS_S ? 1 : c.kind == TS_T ? 2 : 0]);
+             &bar[c.kind == TS_S ? 1 : (c.kind == TS_T || c.kind == TS_FM) ? 2 : 0]);
   }
   const uint32_t want = s_epoch + 1;
   mbar_wait(&bar[0], 0);
@@ -349,6 +372,28 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
       const TCopy c = i == tid ? cp0 : A.copies[c0 + i];
       if (c.kind == TS_S) bulk_g2s(sm + c.smem, (const double2*)A.src[TS_S] + c.src, 16u * (uint32_t)c.elems, &bar[1]);
     }
+  if (A.dbg) {  // profiling: how much the resident (idle) programs alone slow the near-field stream
+    if (P.pad[0]) mbar_wait(&bar[1], 0);
+    mbar_wait(&bar[2], 0);
+    if (A.dbg == 2 && tid == 0) {
+      uint64_t t0, t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+      do {
+        __nanosleep(200);
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      } while (t - t0 < 22000);
+    }
+    __syncthreads();
+    tmark(A, 7);
+    tmark(A, 8);
+    if (tid == 0 && atomicAdd(&A.ctrl->exited, 1u) == gridDim.x - 1) {
+      A.ctrl->exited = 0;
+      A.ctrl->pad[0] = 0;
+      __threadfence();
+      A.ctrl->epoch = want;
+    }
+    return;
+  }
   const TNode* nodes = reinterpret_cast<const TNode*>(sm);
   const int32_t* gidx = reinterpret_cast<const int32_t*>(sm + P.gidx_smem);
   const int yoff = P.yoff;
@@ -401,6 +446,19 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
     }
     __syncthreads();
     if (lv >= nlev - 6 && A.trace_levels == 2) tmark(A, 9 + (nlev - 1 - lv));
+  }
+  // ---- flat top: this program's share of every ancestor's x̂ (M_dᵀ x̂_root), one warp each ----
+  if (P.n_flat) {
+    if (!t_ready) {
+      mbar_wait(&bar[2], 0);
+      t_ready = true;
+    }
+    const TNode rt = nodes[0];
+    for (int j = warp; j < P.n_flat; j += NW) {
+      const TNode nd = nodes[P.flat_first + j];
+      const int64_t gx = (int64_t)(uint32_t)nd.gx_lo | ((int64_t)nd.gx_hi << 32);
+      colsum(sm + nd.pay, rt.k, nd.R, nd.sh, sm + rt.xh, A.px + gx);
+    }
   }
   // ---- publish x̂ of the program's own nodes ----
   {
@@ -458,7 +516,22 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
     __syncthreads();
     tmark(A, 10);
   }
-  const bool split = P.bottom && P.wait_down >= 0 && P.f_base >= 0;
+  const bool split = P.bottom && (P.wait_down >= 0 || P.n_flat) && P.split_mode > 0;
+  if (P.fh_bytes) {
+    // flat top: the H panels take the place of the staged coupling panels (dead once every
+    // thread is past the couplings above); they were prefetched to L2 at launch
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect_tx(&bar[3], (uint32_t)P.fh_bytes);
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int i = tid; i < n_copy; i += TNT) {
+      const TCopy c = i == tid ? cp0 : A.copies[c0 + i];
+      if (ts_late(c.kind)) bulk_g2s(sm + c.smem, (const double2*)A.src[TS_FH] + c.src, 16u * (uint32_t)c.elems, &bar[3]);
+    }
+  }
   if (P.wait_down >= 0 && !split) {
     const int32_t wd = P.wait_down;
     tmark(A, 5);
@@ -509,7 +582,7 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
     // F_root = I; F_c = T_parent[rows of c] F_parent (k_c x k_root), level by level
     const int kr = nodes[0].k, fs = P.f_stride;
     double2* F = sm + P.f_base;
-    for (int lv = 0; lv < nlev; ++lv) {
+    for (int lv = 0; lv < (P.split_mode == 1 ? nlev : 0); ++lv) {
       const int a = P.lev_first[lv], b = P.lev_first[lv + 1];
       for (int i = a + warp; i < b; i += NW) {
         const int kc = nodes[i].k;
@@ -533,19 +606,74 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
       }
       __syncthreads();
     }
-    const int32_t wd = P.wait_down;
-    tmark(A, 5);
-    wait_flags(A.flags_down, &wd, 1, want, A.ctrl);
-    __syncthreads();
-    tmark(A, 6);
     // g = the root's parent contribution (k_root <= 32 in split mode; the root's own ŷ slot may be
     // a leaf's, still needed)
     __shared__ double2 gsh[32];
     double2* gv = gsh;
-    if (warp == 0) {
-      const TNode nd = nodes[0];
-      const int64_t gx = (int64_t)(uint32_t)nd.gx_lo | ((int64_t)nd.gx_hi << 32);
-      for (int j = lane; j < nd.k; j += 32) gv[j] = __ldcg(A.yhat + gx + j);
+    tmark(A, 5);
+    if (P.n_flat) {
+      // flat top: the partials of the programs below every source of every ancestor, then the
+      // ancestors' couplings and the way down to this root in one panel product per ancestor
+      wait_flags(A.flags_up, A.waits + P.wait_far_first, P.n_wait_far, want, A.ctrl);
+      __syncthreads();
+      tmark(A, 6);
+    if (P.n_frow) {
+      // x̂ of the ancestors' sources: the sum of the partials of the bottom programs below each
+      // source, 2^d partials per entry on adjacent lanes (butterfly: a fixed summation order)
+      const int4* fr = reinterpret_cast<const int4*>(sm + P.frow_smem);
+      const int32_t* eb = reinterpret_cast<const int32_t*>(sm + P.ebase_smem);
+      constexpr int U = 4;
+      for (int r0 = warp; r0 < P.n_frow; r0 += NW * U) {
+        double2 v[U];
+        int4 hd[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int r = r0 + u * NW;
+          v[u] = make_double2(0.0, 0.0);
+          hd[u] = make_int4(0, 0, 0, 0);
+          if (r < P.n_frow) {
+            hd[u] = fr[r];
+            const int e = lane >> hd[u].x;
+            if (e < hd[u].z) v[u] = __ldcg(A.px + eb[hd[u].y + e] + (lane & ((1 << hd[u].x) - 1)) * P.px_stride);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (r0 + u * NW >= P.n_frow) continue;  // warp-uniform
+          for (int m = 1; m < (1 << hd[u].x); m <<= 1) v[u] = cadd(v[u], shfl_xor2(v[u], m));
+          const int e = lane >> hd[u].x;
+          if ((lane & ((1 << hd[u].x) - 1)) == 0 && e < hd[u].z) xg[hd[u].w + e] = v[u];
+        }
+      }
+    }
+      if (P.fh_bytes) mbar_wait(&bar[3], 0);
+      __syncthreads();
+      cta_colsum(nodes, P.flat_first, P.flat_first + P.n_flat, shk,
+                 [&](const TNode& nd, const double2*& M, int& R, int& w, const double2*& in, double2*& out) {
+                   if (nd.k == 0) return false;
+                   M = sm + nd.s_pay;
+                   R = nd.s_rows;
+                   w = nd.k;
+                   in = xg + nd.xg;
+                   out = sm + nd.xh + yoff;
+                   return true;
+                 });
+      __syncthreads();
+      if (tid < nodes[0].k) {
+        double2 a = make_double2(0.0, 0.0);
+        for (int j = 0; j < P.n_flat; ++j) a = cadd(a, sm[nodes[P.flat_first + j].xh + yoff + tid]);
+        gv[tid] = a;
+      }
+    } else {
+      const int32_t wd = P.wait_down;
+      wait_flags(A.flags_down, &wd, 1, want, A.ctrl);
+      __syncthreads();
+      tmark(A, 6);
+      if (warp == 0) {
+        const TNode nd = nodes[0];
+        const int64_t gx = (int64_t)(uint32_t)nd.gx_lo | ((int64_t)nd.gx_hi << 32);
+        for (int j = lane; j < nd.k; j += 32) gv[j] = __ldcg(A.yhat + gx + j);
+      }
     }
     __syncthreads();
     if (A.trace_levels >= 4) tmark(A, 11);
@@ -582,6 +710,18 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
   if (A.trace_levels >= 4) tmark(A, 12);
   if (P.y_n > 0 && tid == 0) {  // y[rows] += the assembled far field: one bulk reduce-add
     const int64_t yg = (int64_t)(uint32_t)P.y_g_lo | ((int64_t)P.y_g_hi << 32);
+    if (A.wait_zeroed > 0) {  // the near-field CTAs have zeroed their rows of y (long ago, normally)
+      for (long spins = 0;; ++spins) {
+        uint32_t v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&A.ctrl->pad[0]) : "memory");
+        if (v >= (uint32_t)A.wait_zeroed) break;
+        if (spins > (1l << 24)) {
+          atomicExch(&A.ctrl->error, 3u);
+          break;
+        }
+        __nanosleep(100);
+      }
+    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the generic-proxy stores above
     asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(A.y + yg),
                  "r"(smem_u32(sm + P.y_smem)), "r"(16u * (uint32_t)P.y_n)
@@ -597,6 +737,7 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
   if (tid == 0) {
     if (atomicAdd(&A.ctrl->exited, 1u) == gridDim.x - 1) {  // last CTA out advances the epoch
       A.ctrl->exited = 0;
+      A.ctrl->pad[0] = 0;  // the near-field kernel's "y zeroed" count, for the next launch
       __threadfence();
       A.ctrl->epoch = want;
     }
@@ -614,6 +755,10 @@ struct TreePlan {
   std::vector<int32_t> waits;
   std::vector<TNode> nodes_all;   // staged from a device copy (TS_NODES)
   std::vector<int32_t> gidx_all;  // staged from a device copy (TS_GIDX), 4 per 16-byte element
+  std::vector<double2> flat_all;  // flat top: transfer chains and H panels (TS_FM / TS_FH)
+  int64_t px_elems = 0;           // flat top: partial x̂ area (elements)
+  int64_t n_rows_total = 0;       // N (rows of y)
+  bool flat = false;
   int smem_max = 0;               // bytes
   int ls = 0, lt = 0, n_bottom = 0, n_top = 0;
 };
@@ -650,9 +795,90 @@ bool tree_shape_ok(const h2b_ctx* h) {
   return true;
 }
 
+// Flat top (r02): instead of top programs walking the levels above the split level ls (five
+// dependent level steps up, the couplings, five down and two more flag hand-offs at cfg2, all
+// latency), every bottom program c carries, for each ancestor t_d at level ls - d,
+//   M_d = T-chain from c up to t_d (k_c x k_t):  x̂_t = Σ_c M_dᵀ x̂_c,  ŷ_c += M_d ŷ_t, and
+//   H_d = Sᵀ_panel(t_d) M_dᵀ ((Σ_s k_s) x k_c): ŷ_c += H_dᵀ [x̂_s]_s  (couplings of t_d, then down).
+// Up: c writes its partials M_dᵀ x̂_c to px (fixed slots, no atomics), then ONE flag hand-off;
+// down: c sums the partials of the programs below each source (fixed order) and applies H_d
+// like a coupling panel (a pseudo node of the program).  The products M and H are formed on
+// the host from the uploaded T and Sᵀ (double precision; the reference applies the factors one
+// after the other, arith.py:68-99, so results agree to rounding, not bitwise).
+struct FlatAnc {
+  int d = 0, t = 0, kt = 0, rows = 0;
+  std::vector<double2> M, H;   // k_c x kt ; rows x k_c
+  std::vector<int32_t> ebase;  // per gathered row: px index of its first partial
+};
+
 struct Builder {
   const h2b_ctx* h;
   TreePlan& tp;
+  // flat top: host copies of T and Sᵀ, the split / top levels, programs and the px row stride
+  const double2* hT = nullptr;
+  const double2* hS = nullptr;
+  int ls = 0, lt = 0, nb = 0, kp = 0;
+  bool flat = false;
+
+  std::vector<FlatAnc> flat_ancestors(int root) const {
+    std::vector<FlatAnc> out;
+    const int i = root - h->level_ptr[ls];
+    const int kc = h->c_rank[root];
+    if (kc == 0) return out;  // nothing flows through a rank-0 root (its px slots stay zero)
+    std::vector<double2> M;  // k_c x kprev
+    int kprev = kc;
+    for (int d = 1; d <= ls - lt; ++d) {
+      const int t = h->level_ptr[ls - d] + (i >> d);
+      const int child = h->level_ptr[ls - d + 1] + (i >> (d - 1));
+      const int kt = h->c_rank[t], kch = h->c_rank[child];
+      const int r0 = ((i >> (d - 1)) & 1) ? h->c_rank[h->c_child_lo[t]] : 0;
+      const double2* T = hT + h->c_toff[t];
+      std::vector<double2> Mn((size_t)kc * kt, make_double2(0.0, 0.0));
+      for (int b = 0; b < kc; ++b)
+        for (int a = 0; a < kt; ++a) {
+          double2 acc = make_double2(0.0, 0.0);
+          if (d == 1) {
+            acc = T[(size_t)(r0 + b) * kt + a];
+          } else {
+            for (int j = 0; j < kch; ++j) {
+              const double2 m = M[(size_t)b * kprev + j], tv = T[(size_t)(r0 + j) * kt + a];
+              acc.x += m.x * tv.x - m.y * tv.y;
+              acc.y += m.x * tv.y + m.y * tv.x;
+            }
+          }
+          Mn[(size_t)b * kt + a] = acc;
+        }
+      M.swap(Mn);
+      kprev = kt;
+      if (kt == 0) break;  // the chain ends: nothing flows through a rank-0 ancestor
+      FlatAnc fa;
+      fa.d = d;
+      fa.t = t;
+      fa.kt = kt;
+      fa.M = M;
+      const int64_t b0 = h->s_row_ptr[t], b1 = h->s_row_ptr[t + 1];
+      for (int64_t b = b0; b < b1; ++b) {
+        const int sc = h->s_col[b], ks = h->c_rank[sc];
+        const double2* St = hS + h->s_off[b];  // Sᵀ block: k_s x k_t
+        const int64_t si = sc - h->level_ptr[ls - d];
+        for (int r = 0; r < ks; ++r) {
+          for (int bb = 0; bb < kc; ++bb) {
+            double2 acc = make_double2(0.0, 0.0);
+            for (int a = 0; a < kt; ++a) {
+              const double2 sv = St[(size_t)r * kt + a], m = M[(size_t)bb * kt + a];
+              acc.x += sv.x * m.x - sv.y * m.y;
+              acc.y += sv.x * m.y + sv.y * m.x;
+            }
+            fa.H.push_back(acc);
+          }
+          fa.ebase.push_back((int32_t)((((int64_t)(d - 1) * nb + (si << d)) * kp) + r));
+        }
+        fa.rows += ks;
+      }
+      out.push_back(std::move(fa));
+    }
+    return out;
+  }
   // one program: the subtree of cluster `root` over levels [root level, last] (last inclusive);
   // ext: the level below `last` is external (x̂ from / ŷ to global)
   bool build(int root, int last, bool bottom, int budget_elems) {
@@ -678,16 +904,31 @@ struct Builder {
     const int nn = (int)nd_p.size();
     std::map<int, int> idx_of;
     for (int i = 0; i < nn; ++i) idx_of[nd_p[i]] = i;
+    // flat top: one pseudo node per ancestor above the split level (behind the real nodes)
+    std::vector<FlatAnc> fl;
+    if (flat && bottom) fl = flat_ancestors(root);
+    const int nfl = (int)fl.size();
+    // gather rows of the flat ancestors: 32 >> d entries per row of 2^d partials each
+    std::vector<int32_t> frow, ebase_all;
+    std::vector<int> fl_efirst(nfl, 0);
+    for (int f = 0; f < nfl; ++f) {
+      fl_efirst[f] = (int)ebase_all.size();
+      ebase_all.insert(ebase_all.end(), fl[f].ebase.begin(), fl[f].ebase.end());
+    }
     // smem layout (double2 elements): nodes | gather idx | x | V | T | S | x̂ | ŷ | x̂g
-    int off = 4 * nn;  // 64-byte nodes
-    std::vector<TNode> nodes(nn);
+    int off = 4 * (nn + nfl);  // 64-byte nodes
+    std::vector<TNode> nodes(nn + nfl);
     std::vector<int32_t> gl;  // gather list (global x̂ index, or ~smem offset for own nodes)
     // coupling rows first (their count sizes the gather list)
-    std::vector<int> xh_of(nn, 0);
+    std::vector<int> xh_of(nn + nfl, 0);
     int xh_total = 0;
     for (int i = 0; i < nn; ++i) {
       xh_of[i] = xh_total;
       xh_total += h->c_rank[nd_p[i]];
+    }
+    for (int f = 0; f < nfl; ++f) {  // a ŷ slot per pseudo node (k_root entries)
+      xh_of[nn + f] = xh_total;
+      xh_total += h->c_rank[root];
     }
     const int own_end = bottom ? nn : lev_first[nl - 1];  // nodes the program computes
     int n_rows = 0;
@@ -698,6 +939,12 @@ struct Builder {
     }
     const int gidx_smem = off;
     off += (n_rows + 3) / 4;
+    int n_frow = 0;
+    for (int f = 0; f < nfl; ++f) n_frow += (fl[f].rows + (32 >> fl[f].d) - 1) / (32 >> fl[f].d);
+    const int frow_smem = off;
+    off += n_frow;
+    const int ebase_smem = off;
+    off += ((int)ebase_all.size() + 3) / 4;
     int x_smem = -1, v_smem = -1;
     auto push_copy = [&](int kind, int64_t src, int elems, int smem) {
       if (elems <= 0) return;
@@ -711,7 +958,7 @@ struct Builder {
       tp.copies.push_back(TCopy{src, kind, elems, smem, 0});
     };
     P.copy_first = (int)tp.copies.size();
-    push_copy(TS_NODES, (int64_t)tp.nodes_all.size() * 4, 4 * nn, 0);
+    push_copy(TS_NODES, (int64_t)tp.nodes_all.size() * 4, 4 * (nn + nfl), 0);
     if (bottom) {  // x of the subtree's points
       x_smem = off;
       push_copy(TS_X, h->c_start[root], h->c_size[root], off);
@@ -811,17 +1058,120 @@ struct Builder {
         xg_rows += h->c_rank[s];
       }
     }
+    // flat top: pseudo nodes; their H panels go where the staged coupling panels were (behind the
+    // transfer chains F of the split down pass, see below), their chains M into the x̂g area
+    // (consumed before the first gather); gather-row headers
+    P.n_flat = nfl;
+    P.flat_first = nn;
+    P.n_frow = n_frow;
+    P.frow_smem = frow_smem;
+    P.ebase_smem = ebase_smem;
+    P.px_stride = kp;
+    const int n_xg_real = xg_rows;
+    int m_total = 0, flat_f_base = 0, flat_f_stride = 0;
+    if (nfl > 0) {
+      const int kc = h->c_rank[root];
+      int kmax_all = 0;
+      for (int i = 0; i < nn; ++i) kmax_all = std::max(kmax_all, h->c_rank[nd_p[i]]);
+      const int64_t need_f = 0;  // (the chains F are staged, not formed in the program)
+      int64_t h_off = s_first + need_f, h_total = 0;
+      for (int f = 0; f < nfl; ++f) h_total += (int64_t)fl[f].rows * kc;
+      if (!stage_s || kc == 0 || need_f + h_total > s_total || kmax_all > 32) return false;
+      for (int f = 0; f < nfl; ++f) {
+        TNode& n = nodes[nn + f];
+        const FlatAnc& fa = fl[f];
+        n.k = kc;
+        n.kind = 3;
+        n.R = fa.kt;
+        n.sh = shpow(fa.kt);
+        n.s_rows = fa.rows;
+        n.xg = xg_rows;
+        n.s_pay = (int32_t)h_off;
+        n.pad = 0;
+        if (fa.rows * kc > 0) {
+          tp.copies.push_back(TCopy{(int64_t)tp.flat_all.size(), TS_FH, fa.rows * kc, (int32_t)h_off, 0});
+          tp.flat_all.insert(tp.flat_all.end(), fa.H.begin(), fa.H.end());
+          h_off += fa.rows * kc;
+        }
+        const int per = 32 >> fa.d;
+        for (int e0 = 0; e0 < fa.rows; e0 += per) {
+          frow.push_back(fa.d);
+          frow.push_back(fl_efirst[f] + e0);
+          frow.push_back(std::min(per, fa.rows - e0));
+          frow.push_back(xg_rows + e0);
+        }
+        xg_rows += fa.rows;
+        const int64_t px = ((int64_t)(fa.d - 1) * nb + (root - h->level_ptr[ls])) * kp;
+        n.gx_lo = (int32_t)(uint32_t)px;
+        n.gx_hi = (int32_t)(px >> 32);
+        m_total += kc * fa.kt;
+      }
+      // chains F_leaf = T...T from the root down to every leaf (k_leaf x k_c), behind the H panels
+      {
+        std::vector<std::vector<double2>> F(nn);
+        F[0].assign((size_t)kc * kc, make_double2(0.0, 0.0));
+        for (int j = 0; j < kc; ++j) F[0][(size_t)j * kc + j].x = 1.0;
+        for (int lv = 1; lv < nl; ++lv)
+          for (int i = lev_first[lv]; i < lev_first[lv + 1]; ++i) {
+            const int pi = lev_first[lv - 1] + (i - lev_first[lv]) / 2, hi = (i - lev_first[lv]) & 1;
+            const int pp = nd_p[pi], kpar = h->c_rank[pp], kch = h->c_rank[nd_p[i]];
+            const int r0 = hi ? h->c_rank[h->c_child_lo[pp]] : 0;
+            const double2* T = hT + h->c_toff[pp];
+            F[i].assign((size_t)kch * kc, make_double2(0.0, 0.0));
+            for (int r = 0; r < kch; ++r)
+              for (int c = 0; c < kc; ++c) {
+                double2 acc = make_double2(0.0, 0.0);
+                for (int j = 0; j < kpar; ++j) {
+                  const double2 tv = T[(size_t)(r0 + r) * kpar + j], fv = F[pi][(size_t)j * kc + c];
+                  acc.x += tv.x * fv.x - tv.y * fv.y;
+                  acc.y += tv.x * fv.y + tv.y * fv.x;
+                }
+                F[i][(size_t)r * kc + c] = acc;
+              }
+          }
+        int kleaf = 0;
+        for (int i = lev_first[nl - 1]; i < nn; ++i) kleaf = std::max(kleaf, h->c_rank[nd_p[i]]);
+        const int fs = kleaf * kc, a = lev_first[nl - 1];
+        if (need_f + h_total + (int64_t)(nn - a) * fs > s_total || fs == 0) return false;
+        flat_f_base = (int)h_off - a * fs;
+        flat_f_stride = fs;
+        for (int i = a; i < nn; ++i) {
+          std::vector<double2> blk((size_t)fs, make_double2(0.0, 0.0));
+          std::copy(F[i].begin(), F[i].end(), blk.begin());
+          if (i > a && tp.copies.back().kind == TS_FF)  // one bulk copy for all leaves
+            tp.copies.back().elems += fs;
+          else
+            tp.copies.push_back(TCopy{(int64_t)tp.flat_all.size(), TS_FF, fs, (int32_t)h_off, 0});
+          tp.flat_all.insert(tp.flat_all.end(), blk.begin(), blk.end());
+          h_off += fs;
+          h_total += fs;
+        }
+      }
+      P.fh_bytes = (int32_t)(16 * h_total);
+    }
     // x̂ and ŷ areas, x̂g
     const int xh_base = off;
-    for (int i = 0; i < nn; ++i) nodes[i].xh = xh_base + xh_of[i];
+    for (int i = 0; i < nn + nfl; ++i) nodes[i].xh = xh_base + xh_of[i];
     for (int i = 0; i < own_end; ++i)  // internal nodes read [x̂_lo; x̂_hi] (adjacent)
       if (nodes[i].kind == 1) nodes[i].in = nodes[lo_idx[i]].xh;
     off += xh_total;
     P.yoff = xh_total;
     off += xh_total;
     P.xg_smem = off;
-    off += xg_rows;
-    P.n_xg = xg_rows;
+    {  // flat top: the chains M_d are staged into the x̂g area
+      int m_off = off;
+      for (int f = 0; f < nfl; ++f) {
+        const int e = h->c_rank[root] * fl[f].kt;
+        nodes[nn + f].pay = m_off;
+        if (e > 0) {
+          tp.copies.push_back(TCopy{(int64_t)tp.flat_all.size(), TS_FM, e, m_off, 0});
+          tp.flat_all.insert(tp.flat_all.end(), fl[f].M.begin(), fl[f].M.end());
+          m_off += e;
+        }
+      }
+    }
+    off += std::max(xg_rows, m_total);
+    P.n_xg = n_xg_real;
     for (int32_t& g : gl)
       if (g <= -2) {
         const int v = -2 - g;
@@ -835,18 +1185,23 @@ struct Builder {
     if (off > budget_elems) return false;
     // gather list: staged as 16-byte elements (4 indices each)
     P.gidx_smem = gidx_smem;
-    if (!gl.empty()) {
+    if (!gl.empty() || !frow.empty()) {  // [gather list | flat gather-row headers | entry bases]
       while (tp.gidx_all.size() % 4) tp.gidx_all.push_back(0);
       const int64_t first = (int64_t)tp.gidx_all.size() / 4;
+      gl.resize((size_t)(n_rows + 3) / 4 * 4, 0);
       tp.gidx_all.insert(tp.gidx_all.end(), gl.begin(), gl.end());
+      tp.gidx_all.insert(tp.gidx_all.end(), frow.begin(), frow.end());
+      tp.gidx_all.insert(tp.gidx_all.end(), ebase_all.begin(), ebase_all.end());
       while (tp.gidx_all.size() % 4) tp.gidx_all.push_back(0);
-      push_copy(TS_GIDX, first, (int)((gl.size() + 3) / 4), gidx_smem);
+      push_copy(TS_GIDX, first, (int)((int64_t)tp.gidx_all.size() / 4 - first), gidx_smem);
     }
     P.n_copy = (int)tp.copies.size() - P.copy_first;
-    int64_t bytes = 0, sbytes = 0, tbytes = 0;
+    int64_t bytes = 0, sbytes = 0, tbytes = 0, fhbytes = 0;
     for (int c = P.copy_first; c < (int)tp.copies.size(); ++c)
       if (tp.copies[c].kind != TS_S || tp.copies[c].smem >= 0)
-        (tp.copies[c].kind == TS_S ? sbytes : tp.copies[c].kind == TS_T ? tbytes : bytes) +=
+        (tp.copies[c].kind == TS_S ? sbytes
+         : ts_late(tp.copies[c].kind) ? fhbytes
+         : (tp.copies[c].kind == TS_T || tp.copies[c].kind == TS_FM) ? tbytes : bytes) +=
             16 * (int64_t)tp.copies[c].elems;
     if (sbytes >= (1 << 20) || tbytes >= (1 << 20)) return false;
     P.pad[1] = (int32_t)tbytes;
@@ -856,8 +1211,9 @@ struct Builder {
     {  // threads per node of the CTA-wide level operations: 2^shk >= every rank (column ops),
        // 2^shr >= every row count up to 32 (row ops loop over the rest)
       int kmax = 1, rmax = 1;
-      for (int i = 0; i < nn; ++i) kmax = std::max(kmax, nodes[i].k);
+      for (int i = 0; i < nn + nfl; ++i) kmax = std::max(kmax, nodes[i].k);
       for (int i = 0; i < own_end; ++i) rmax = std::max(rmax, nodes[i].R);
+      for (const FlatAnc& fa : fl) kmax = std::max(kmax, fa.kt);
       int shk = 0, shr = 0;
       while ((1 << shk) < kmax) ++shk;
       while ((1 << shr) < rmax && shr < 5) ++shr;
@@ -865,7 +1221,7 @@ struct Builder {
       P.pad[2] = shk | (shr << 8);
     }
     P.smem_elems = off;
-    P.n_nodes = nn;
+    P.n_nodes = nn + nfl;
     P.nlev = nl;
     // transfer chains of a bottom program (see k_far_tree): in the staged coupling panels' region
     // (dead once the couplings are done) when it is large enough, else none
@@ -880,13 +1236,18 @@ struct Builder {
       P.y_g_lo = (int32_t)(uint32_t)(int64_t)h->c_start[root];
       P.y_g_hi = (int32_t)((int64_t)h->c_start[root] >> 32);
     }
-    if (bottom && stage_s && s_total > 0 && !getenv("H2B_TREE_NO_SPLIT")) {
+    if (nfl > 0) {
+      P.f_base = flat_f_base;
+      P.f_stride = flat_f_stride;
+      P.split_mode = 2;
+    } else if (bottom && stage_s && s_total > 0 && !getenv("H2B_TREE_NO_SPLIT")) {
       int kmax = 0;
       for (int i = 0; i < nn; ++i) kmax = std::max(kmax, nodes[i].k);
       const int64_t need = (int64_t)nn * kmax * nodes[0].k;
       if (need > 0 && need <= s_total && nodes[0].k > 0 && kmax <= 32) {
         P.f_base = s_first;
         P.f_stride = kmax * nodes[0].k;
+        P.split_mode = 1;
       }
     }
     for (int d = 0; d <= nl; ++d) P.lev_first[d] = lev_first[d];
@@ -902,7 +1263,8 @@ struct Builder {
 
 // Plan the tree far field for handle h (q = 1).  Returns false when the tree does not qualify or
 // the programs do not fit (the caller keeps the task-graph kernel).
-bool h2b_plan_tree(const h2b_ctx* h, int max_ctas, int budget_bytes, TreePlan& tp) {
+bool h2b_plan_tree(const h2b_ctx* h, int max_ctas, int budget_bytes, int flat_budget_bytes, const double2* hT,
+                   const double2* hS, TreePlan& tp) {
   if (getenv("H2B_NO_TREE") || h->K == 0 || !tree_shape_ok(h)) return false;
   const int L = h->depth;
   int lt = -1;
@@ -915,13 +1277,42 @@ bool h2b_plan_tree(const h2b_ctx* h, int max_ctas, int budget_bytes, TreePlan& t
   if (lt < 0) return false;
   const int budget = budget_bytes / 16;
   for (int ls = L - 1; ls >= lt; --ls) {  // the deepest split whose programs fit the grid
-    const int nb = 1 << ls, nt = ls > lt ? (1 << lt) : 0;
+    const int nb = 1 << ls;
+    int nt = ls > lt ? (1 << lt) : 0;
     if (nb + nt > max_ctas) continue;
     TreePlan cand;
-    Builder B{h, cand};
-    bool ok = true;
-    for (int i = 0; i < nb && ok; ++i) ok = B.build(h->level_ptr[ls] + i, L - 1, true, budget);
-    for (int i = 0; i < nt && ok; ++i) ok = B.build(h->level_ptr[lt] + i, ls - 1, false, budget);
+    bool ok = false;
+    // flat top first (no top programs): up to 5 levels above the split (2^d partials per gathered
+    // entry sit on one warp's lanes), ranks <= 32 there
+    if (ls > lt && ls - lt <= 5 && hT && hS && flat_budget_bytes > 0 && !getenv("H2B_TREE_NO_FLAT")) {
+      int kp = 0;
+      for (int p = h->level_ptr[lt]; p < h->level_ptr[ls]; ++p) kp = std::max(kp, h->c_rank[p]);
+      if (kp <= 32 && kp > 0) {
+        Builder B{h, cand};
+        B.hT = hT;
+        B.hS = hS;
+        B.ls = ls;
+        B.lt = lt;
+        B.nb = nb;
+        B.kp = kp;
+        B.flat = true;
+        ok = true;
+        for (int i = 0; i < nb && ok; ++i) ok = B.build(h->level_ptr[ls] + i, L - 1, true, flat_budget_bytes / 16);
+        if (ok) {
+          cand.flat = true;
+          cand.px_elems = (int64_t)(ls - lt) * nb * kp;
+          nt = 0;
+        } else {
+          cand = TreePlan();
+        }
+      }
+    }
+    if (!ok) {
+      Builder B{h, cand};
+      ok = true;
+      for (int i = 0; i < nb && ok; ++i) ok = B.build(h->level_ptr[ls] + i, L - 1, true, budget);
+      for (int i = 0; i < nt && ok; ++i) ok = B.build(h->level_ptr[lt] + i, ls - 1, false, budget);
+    }
     if (!ok) continue;
     // dependencies: program of each cluster (bottom: level >= ls; top: lt <= level < ls)
     std::vector<int> prog_of(h->P, -1);
@@ -949,16 +1340,32 @@ bool h2b_plan_tree(const h2b_ctx* h, int max_ctas, int budget_bytes, TreePlan& t
             if (h->c_rank[s] > 0 && prog_of[s] != pi) up.insert(prog_of[s]);
           }
         }
+      std::set<int> far;
+      if (cand.flat)  // the bottom programs below every source of every ancestor (their partials)
+        for (int d = 1; d <= ls - lt; ++d) {
+          const int t = h->level_ptr[ls - d] + (pi >> d);
+          if (h->c_rank[t] == 0) break;
+          for (int64_t b = h->s_row_ptr[t]; b < h->s_row_ptr[t + 1]; ++b) {
+            const int s = h->s_col[b];
+            if (h->c_rank[s] == 0) continue;
+            const int si = s - h->level_ptr[ls - d];
+            for (int j = 0; j < (1 << d); ++j)
+              if ((si << d) + j != pi) far.insert((si << d) + j);
+          }
+        }
       P.wait_up_first = (int)cand.waits.size();
       P.n_wait_up = (int)up.size();
       cand.waits.insert(cand.waits.end(), up.begin(), up.end());
+      P.wait_far_first = (int)cand.waits.size();
+      P.n_wait_far = (int)far.size();
+      cand.waits.insert(cand.waits.end(), far.begin(), far.end());
       if (!bottom) {  // external children: the bottom programs under this top program
         P.ext_wait_first = (int)cand.waits.size();
         const int d = ls - lt;
         const int first = (root - h->level_ptr[lt]) << d;
         P.n_ext_wait = 1 << d;
         for (int j = 0; j < (1 << d); ++j) cand.waits.push_back(first + j);
-      } else if (ls > lt) {
+      } else if (ls > lt && !cand.flat) {
         const int parent_top = nb + (pi >> (ls - lt));
         // only when the parent carries rank (otherwise the top writes nothing for this root)
         int par = h->level_ptr[ls - 1] + (pi >> 1);
@@ -967,6 +1374,7 @@ bool h2b_plan_tree(const h2b_ctx* h, int max_ctas, int budget_bytes, TreePlan& t
     }
     cand.ls = ls;
     cand.lt = lt;
+    cand.n_rows_total = h->n;
     cand.n_bottom = nb;
     cand.n_top = nt;
     tp = std::move(cand);
@@ -982,10 +1390,13 @@ struct TreeDev {
   int32_t* waits = nullptr;
   TNode* nodes = nullptr;
   int32_t* gidx = nullptr;
+  double2* flat = nullptr;    // flat top: transfer chains and H panels
+  double2* px = nullptr;      // flat top: partial x̂ (zero where a chain ends at a rank-0 ancestor)
   uint32_t* flags = nullptr;  // up [n], down [n]
   MegaCtrl* ctrl = nullptr;
   uint64_t* trace = nullptr;
   int n_progs = 0, smem = 0;
+  bool zero_ok = false;
 };
 
 namespace {
@@ -1005,6 +1416,12 @@ int h2b_tree_upload(const TreePlan& tp, TreeDev** out, int64_t* bytes) {
   if (!rc) rc = upload_vec(&d->waits, tp.waits);
   if (!rc) rc = upload_vec(&d->nodes, tp.nodes_all);
   if (!rc) rc = upload_vec(&d->gidx, tp.gidx_all);
+  if (!rc) rc = upload_vec(&d->flat, tp.flat_all);
+  if (!rc) {
+    const size_t pb = 16 * (size_t)std::max<int64_t>(tp.px_elems, 1);
+    H2B_CUDA_TRY(cudaMalloc((void**)&d->px, pb));
+    H2B_CUDA_TRY(cudaMemset(d->px, 0, pb));
+  }
   d->n_progs = (int)tp.progs.size();
   if (!rc) {
     const cudaError_t e1 = cudaMalloc(&d->flags, sizeof(uint32_t) * 2 * std::max(d->n_progs, 1));
@@ -1018,12 +1435,22 @@ int h2b_tree_upload(const TreePlan& tp, TreeDev** out, int64_t* bytes) {
     }
   }
   d->smem = tp.smem_max;
+  {
+    int64_t rows = 0;
+    bool all = true;
+    for (const TProg& P : tp.progs)
+      if (P.bottom) {
+        all = all && P.y_n > 0;
+        rows += P.y_n;
+      }
+    d->zero_ok = all && rows == tp.n_rows_total;
+  }
   if (!rc && getenv("H2B_TREE_TRACE")) {
     cudaMalloc(&d->trace, sizeof(uint64_t) * 32 * std::max(d->n_progs, 1));
     cudaMemset(d->trace, 0, sizeof(uint64_t) * 32 * std::max(d->n_progs, 1));
   }
   if (!rc) {
-    const cudaError_t e = cudaFuncSetAttribute(k_far_tree, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 13800);
+    const cudaError_t e = cudaFuncSetAttribute(k_far_tree, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 14000);
     cudaFuncSetAttribute(k_far_tree, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) {
       h2b_set_error(std::string("k_far_tree attributes: ") + cudaGetErrorString(e));
@@ -1031,14 +1458,15 @@ int h2b_tree_upload(const TreePlan& tp, TreeDev** out, int64_t* bytes) {
     }
   }
   *bytes = (int64_t)(sizeof(TProg) * tp.progs.size() + sizeof(TCopy) * tp.copies.size() +
-                     sizeof(TNode) * tp.nodes_all.size() + 4 * tp.gidx_all.size());
+                     sizeof(TNode) * tp.nodes_all.size() + 4 * tp.gidx_all.size() + 16 * tp.flat_all.size() +
+                     16 * tp.px_elems);
   *out = d;
   return rc;
 }
 
 void h2b_tree_free(TreeDev* d) {
   if (!d) return;
-  void* ptrs[] = {d->progs, d->copies, d->waits, d->nodes, d->gidx, d->flags, d->ctrl, d->trace};
+  void* ptrs[] = {d->progs, d->copies, d->waits, d->nodes, d->gidx, d->flat, d->px, d->flags, d->ctrl, d->trace};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete d;
@@ -1074,19 +1502,37 @@ int h2b_tree_prepare(h2b_ctx* h, int max_ctas, int budget_bytes, int64_t* bytes,
   *planned = 0;
   *bytes = 0;
   TreePlan tp;
-  if (!h2b_plan_tree(h, max_ctas, budget_bytes, tp)) return H2B_OK;
+  // flat top: host copies of the transfer matrices and the (already transposed) coupling panels
+  std::vector<double2> hT, hS;
+  const int flat_budget = getenv("H2B_TREE_NO_FLAT") ? 0 : budget_bytes + TREE_FLAT_EXTRA;
+  if (flat_budget > 0 && h->sec_elems[1] > 0 && h->sec_elems[2] > 0 &&
+      h->sec_elems[1] + h->sec_elems[2] <= (int64_t)(1 << 26)) {
+    hT.resize((size_t)h->sec_elems[1]);
+    hS.resize((size_t)h->sec_elems[2]);
+    H2B_CUDA_TRY(cudaMemcpy(hT.data(), h->buf[H2B_SEC_T], 16 * hT.size(), cudaMemcpyDeviceToHost));
+    H2B_CUDA_TRY(cudaMemcpy(hS.data(), h->buf[H2B_SEC_S], 16 * hS.size(), cudaMemcpyDeviceToHost));
+  }
+  if (!h2b_plan_tree(h, max_ctas, budget_bytes, flat_budget, hT.empty() ? nullptr : hT.data(),
+                     hS.empty() ? nullptr : hS.data(), tp))
+    return H2B_OK;
   H2B_TRY(h2b_tree_upload(tp, &h->tree, bytes));
   h->tree_ls = tp.ls;
   h->tree_lt = tp.lt;
   h->tree_progs = (int)tp.progs.size();
   h->tree_smem = tp.smem_max;
+  h->tree_flat = tp.flat ? 1 : 0;
   *planned = 1;
   return H2B_OK;
 }
 
 // one launch of the far field on `st` (cooperative: the programs wait on one another)
-int h2b_launch_tree(h2b_ctx* h, const TreeDev* d, const double2* xp, double2* yp, cudaStream_t st) {
+// the "y zeroed" count of the near-field kernel's CTAs (see h2b_launch_mega), when every far-field
+// contribution to y is a bottom program's bulk add (which waits for the count); else nullptr
+uint32_t* h2b_tree_zeroed_counter(const TreeDev* d) { return d && d->zero_ok ? &d->ctrl->pad[0] : nullptr; }
+
+int h2b_launch_tree(h2b_ctx* h, const TreeDev* d, const double2* xp, double2* yp, cudaStream_t st, int wait_zeroed) {
   TreeArgs A;
+  A.wait_zeroed = wait_zeroed;
   A.progs = d->progs;
   A.copies = d->copies;
   A.waits = d->waits;
@@ -1096,6 +1542,10 @@ int h2b_launch_tree(h2b_ctx* h, const TreeDev* d, const double2* xp, double2* yp
   A.src[TS_S] = h->buf[H2B_SEC_S];
   A.src[TS_NODES] = d->nodes;
   A.src[TS_GIDX] = d->gidx;
+  A.src[TS_FM] = d->flat;
+  A.src[TS_FH] = d->flat;
+  A.src[TS_FF] = d->flat;
+  A.px = d->px;
   A.xhat = h->xhat;
   A.yhat = h->yhat;
   A.y = yp;
@@ -1108,6 +1558,8 @@ int h2b_launch_tree(h2b_ctx* h, const TreeDev* d, const double2* xp, double2* yp
     A.trace_levels = e ? atoi(e) : 0;
     const char* d = getenv("H2B_TREE_DEFER_S");  // A/B aid
     A.defer_s = d ? atoi(d) : 1;  // measured: step 40.3 vs 41.0 us at cfg2
+    const char* g = getenv("H2B_TREE_DBG");
+    A.dbg = g ? atoi(g) : 0;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(d->n_progs);

@@ -1,0 +1,45 @@
+"""Where the q=1 step's time outside its two kernels goes: event-timed cold steps with parts of
+the step switched off (H2B_OPT_DEBUG bits: 2 no far kernel, 4 no near kernel, 8 no y memset;
+results are then wrong).  Development aid.  Usage: python tools/overhead_probe.py [2]"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.chdir(ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from bench import load  # noqa: E402
+from paper_1703_01175_b200 import H2Operator, _abi  # noqa: E402
+from paper_1703_01175_b200.timing import L2Flusher  # noqa: E402
+
+k = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+pk, ex = load(k)
+fl = L2Flusher("cuda")
+names = {0: "memset + near + far", 8: "near + far (no memset)", 2: "memset + near", 10: "near",
+         4: "memset + far", 12: "far", 6: "memset only", 14: "empty graph"}
+sel = [int(v) for v in os.environ.get("PROBE_MODES", "").split(",") if v] or list(names)
+for graphs in (1,):
+    for dbg in sel:
+        nm = names[dbg]
+        op = H2Operator(pk)
+        L = _abi.lib()
+        _abi.check(L.h2b_set_option(op.handle, _abi.OPT_GRAPHS, graphs))
+        _abi.check(L.h2b_set_option(op.handle, _abi.OPT_DEBUG, dbg))
+        x = torch.from_numpy(ex["x"][pk.perm, 0].copy()).cuda()
+        y = torch.empty_like(x)
+        for _ in range(5):
+            op.matvec_perm(x, out=y)
+        ts = []
+        for _ in range(60):
+            fl.flush()
+            _abi.check(L.h2b_spin_ns(20000, torch.cuda.current_stream().cuda_stream))
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            op.matvec_perm(x, out=y)
+            e.record()
+            torch.cuda.synchronize()
+            ts.append(s.elapsed_time(e) * 1e3)
+        print(f"graphs={graphs} {nm:26s} mean {np.mean(ts):6.2f} us  median {np.median(ts):6.1f}  min {np.min(ts):6.1f}")
+        op.close()

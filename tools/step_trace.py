@@ -25,6 +25,8 @@ pk, ex = load_packed(os.path.join(ROOT, "fixtures", name + ".npz"), with_extra=T
 op = H2Operator(pk, device=0)
 x = torch.from_numpy(ex["x"][pk.perm, 0].copy()).cuda()
 y = torch.empty_like(x)
+if os.environ.get("STEP_DEBUG"):
+    _abi.check(_abi.lib().h2b_set_option(op.handle, _abi.OPT_DEBUG, int(os.environ["STEP_DEBUG"])))
 op.matvec_perm(x, out=y)
 L = _abi.lib()
 L.h2b_near_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
@@ -32,17 +34,30 @@ L.h2b_tree_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
 v = C.c_int64()
 _abi.check(L.h2b_query(op.handle, _abi.Q_TREE, C.byref(v)))
 nprog = v.value & 0xffff
+if int(os.environ.get("STEP_DEBUG", "0")) & 2:
+    nprog = 0  # no far kernel: its stamps are stale
+v2 = C.c_int64()
+_abi.check(L.h2b_query(op.handle, _abi.Q_NEAR_SMEM, C.byref(v2)))
+v3 = C.c_int64()
+_abi.check(L.h2b_query(op.handle, _abi.Q_NEAR_STAGES, C.byref(v3)))
+print(f"tree programs {nprog}, tree smem {v.value >> 32} B, near smem {v2.value} B, near stages {v3.value}")
 ncta = torch.cuda.get_device_properties(0).multi_processor_count
 flush = L2Flusher("cuda")
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+L.h2b_stamp_ns.argtypes = [C.c_void_p, C.c_void_p]
+stamps = torch.zeros(2, dtype=torch.int64, device="cuda")
+cur = torch.cuda.current_stream().cuda_stream
 rows = []
 for rep in range(10):
     flush.flush()
     torch.cuda._sleep(2_000_000)  # keep the host ahead of the device: launch overhead hidden
     s.record()
+    _abi.check(L.h2b_stamp_ns(stamps.data_ptr(), cur))
     op.matvec_perm(x, out=y)
+    _abi.check(L.h2b_stamp_ns(stamps.data_ptr() + 8, cur))
     e.record()
     torch.cuda.synchronize()
+    st = stamps.cpu().numpy()
     nt = np.zeros((ncta, 24), dtype=np.int64)
     _abi.check(L.h2b_near_trace(op.handle, nt.ctypes.data, ncta))
     tt = np.zeros((nprog, 32), dtype=np.int64) if nprog else None
@@ -53,7 +68,7 @@ for rep in range(10):
     t0 = nt[:, 0].min()
     if nprog:
         t0 = min(t0, tt[:, 0][tt[:, 0] > 0].min())
-    r = {"event_us": s.elapsed_time(e) * 1e3}
+    r = {"event_us": s.elapsed_time(e) * 1e3, "stamp.before.min": (st[0] - t0) / 1e3, "stamp.after.min": (st[1] - t0) / 1e3}
     rel = (nt[:, :6] - t0) / 1e3
     for j, nm in enumerate(["entry", "rec0", "issued_all", "landed0", "consumed_all", "exit"]):
         r[f"near.{nm}.min"] = rel[:, j].min()

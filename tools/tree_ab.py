@@ -73,7 +73,7 @@ for name in sys.argv[1:] or ["cfg2"]:
         tn = timed(lambda: op.matvec_perm(x, out=y), 30, flush)
         _abi.check(_abi.lib().h2b_set_option(op.handle, _abi.OPT_DEBUG, 0))
         tr = q(op, _abi.Q_TREE)
-        print(f"{name} tree={tree} (progs {tr & 0xffff} ls {(tr >> 16) & 255} lt {tr >> 24}) relerr {err:.2e} "
+        print(f"{name} tree={tree} (progs {tr & 0xffff} ls {(tr >> 16) & 255} lt {(tr >> 24) & 63} flat {(tr >> 30) & 1}) relerr {err:.2e} "
               f"repeatable {same} step {t:.1f} us far-only {tf:.1f} us near-only {tn:.1f} us "
               f"B_alg/step {pk.algorithmic_bytes() / t / 1e3:.0f} GB/s err {q(op, _abi.Q_DEVICE_ERROR)} near stages {q(op, _abi.Q_NEAR_STAGES)}",
               flush=True)
