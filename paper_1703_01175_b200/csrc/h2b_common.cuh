@@ -190,6 +190,23 @@ struct NearTask {
 struct CoupleGroup {
   int32_t item_first, n_items, cta_mode, pad;
 };
+// Zeroing of y without a memset node (q = 1 tree step, r02).  Every row of y gets exactly one
+// far-field contribution (the bulk add of the bottom program covering it, at that program's
+// end) and one near-field contribution (from the one near-field CTA owning it).  Each bottom
+// program zeroes its own rows at its START (no atomics, behind its staging wait) and then sets
+// flag[c][j] = 1 (release) for every near-field CTA c whose rows overlap its own (it is the j-th
+// program of that CTA's range); CTA c waits for its flags before its consumers start — while
+// its producer fills the ring, before the first block can have landed — and clears them for the
+// next step (it is their only reader).  Nothing is added to either kernel's critical path and
+// nothing inside the near-field consumer loop.  Ordering: the far-field kernel is launched
+// first, so it also runs first when launches are serialised (profilers); a near-field CTA whose
+// flags never come (bounded wait) reports device error 4 instead of hanging.
+// H2B_Y_MEMSET=1 selects the memset node instead.
+constexpr int ZS_SLOTS = 4;  // programs a near-field CTA's rows may span
+struct ZeroSync {
+  uint32_t flag[NEAR_MAXG + 8][ZS_SLOTS];
+};
+
 struct MegaCtrl {
   uint32_t next, exited, epoch, error;  // far-field task graph
   uint32_t near_next, near_exited;      // near-field stream: task claim counter, CTAs done
@@ -303,7 +320,7 @@ struct h2b_ctx {
   // far field as subtree programs (h2b_tree.cu): replaces k_mega beside k_near_stream when set
   TreeDev* tree = nullptr;
   int use_tree = 1;  // H2B_OPT_TREE
-  int tree_ls = 0, tree_lt = 0, tree_progs = 0, tree_smem = 0, tree_flat = 0;
+  int tree_ls = 0, tree_lt = 0, tree_progs = 0, tree_smem = 0, tree_flat = 0, tree_rows_per_prog = 0;
   // flattened bottom tier (0 = off): W buffer and the deep spans' y_deep
   int mega_flat = 0;
   double2* wbuf = nullptr;

@@ -90,11 +90,10 @@ struct NearArgs {
   // block instead of three: at kernel start the far kernel's staging burst makes each ~2 us)
   int early;
   // no memset of y before the step (r02): with the static split every row of y is updated by
-  // exactly one CTA, which zeroes its rows [zero_row[c].x, + zero_row[c].y) first and then counts
-  // itself in *zeroed (release); the far-field kernel adds into y only after all CTAs counted
-  uint32_t* zeroed;  // nullptr: y is zeroed by the caller
+  // exactly one CTA; the far-field programs zero y (ZeroSync in h2b_common.cuh)
+  ZeroSync* zeroed;  // nullptr: y is zeroed by the caller
   int2 first_rec[NEAR_MAXG];
-  int2 zero_row[NEAR_MAXG];
+  int2 zero_n[NEAR_MAXG];  // .x: flags CTA c waits for (programs covering its rows)
   longlong2 first_blk[NEAR_MAXG];
 };
 
@@ -183,18 +182,26 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
     }
   }
   __syncthreads();
+  // y is zeroed by the far-field programs at their start (ZeroSync, h2b_common.cuh): the
+  // consumers wait here — while the producer fills the ring and before the first block can have
+  // landed — for the flags of the programs covering the CTA's rows, and clear them.  (Nothing of
+  // this inside the consumer loop: it is latency-bound, every instruction there costs rate.)
   if (A.zeroed && threadIdx.x < MNT) {
-    // the consumers zero the CTA's rows while the producer fills the ring (their first update of
-    // y comes after the first block has landed and been summed); the count follows a consumer-only
-    // barrier, so every zero store of the CTA is ordered before it
-    const int2 zr = A.zero_row[blockIdx.x];
-    for (int i = threadIdx.x; i < zr.y; i += MNT) A.y[zr.x + i] = make_double2(0.0, 0.0);
-    __threadfence();
-    asm volatile("bar.sync 1, %0;" ::"n"(MNT) : "memory");
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(A.zeroed, 1u);
+    if (threadIdx.x < A.zero_n[blockIdx.x].x) {
+      uint32_t* f = &A.zeroed->flag[blockIdx.x][threadIdx.x];
+      for (long spins = 0;; ++spins) {
+        uint32_t v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if (v == 1u) break;
+        if (spins > (1l << 22)) {
+          atomicExch(&A.ctrl->error, 4u);
+          break;
+        }
+        __nanosleep(100);
+      }
+      *(volatile uint32_t*)f = 0u;
     }
+    asm volatile("bar.sync 1, %0;" ::"n"(MNT) : "memory");
   }
   if (threadIdx.x >= MNT) {
     // ---------------- producer (one lane) ----------------
@@ -797,20 +804,18 @@ int h2b_near_stream_set_smem(int ns, int r, int bytes) {
   return H2B_OK;
 }
 
-int h2b_launch_tree(h2b_ctx* h, const TreeDev* d, const double2* xp, double2* yp, cudaStream_t st, int wait_zeroed);
-uint32_t* h2b_tree_zeroed_counter(const TreeDev* d);
+int h2b_launch_tree(h2b_ctx* h, const TreeDev* d, const double2* xp, double2* yp, cudaStream_t st, int near_ctas);
+ZeroSync* h2b_tree_zero_sync(h2b_ctx* h, TreeDev* d);
 
 // y = 0; then k_near_stream on st and k_mega (or the tree programs) on h->far_stream,
 // concurrently (fork / join)
 int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st) {
   const bool run_far = h->mega_grid > 0 && !(h->mega_debug & 2);
   const bool run_near = h->n_near_tasks > 0 && !(h->mega_debug & 4);
-  // No memset node (r02): when every row of y belongs to exactly one near CTA (static split),
-  // the near kernel zeroes its own rows and the tree kernel's bulk adds wait for all near CTAs'
-  // counts (k_near_stream / k_far_tree); the near kernel never waits on the tree kernel, so the
-  // two can start in any order.
-  static const bool nozero_off = getenv("H2B_Y_MEMSET") != nullptr;
-  uint32_t* zeroed = run_far && run_near && h->tree && h->near_zero_ok && !nozero_off ? h2b_tree_zeroed_counter(h->tree) : nullptr;
+  // No memset node (r02): when every row of y belongs to exactly one near CTA (static split) and
+  // one bottom program, the programs zero their rows at their start (ZeroSync, h2b_common.cuh).
+  const bool nozero_off = getenv("H2B_Y_MEMSET") != nullptr;  // A/B aid and tests (read per capture)
+  ZeroSync* zeroed = run_far && run_near && h->tree && h->near_zero_ok && !nozero_off ? h2b_tree_zero_sync(h, h->tree) : nullptr;
   if (!zeroed && !(h->mega_debug & 8)) H2B_CUDA_TRY(cudaMemsetAsync(yp, 0, sizeof(double2) * h->n, st));
   if (run_far && h->tree) {  // subtree programs (h2b_tree.cu) in k_mega's place
     H2B_CUDA_TRY(cudaEventRecord(h->ev_fork, st));
@@ -888,7 +893,11 @@ int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st)
     N.early = h->near_static && h->near_early && h->near_grid <= NEAR_MAXG;
     N.zeroed = zeroed;
     if (zeroed)
-      for (int c = 0; c < h->near_grid; ++c) N.zero_row[c] = h->near_zero_row[c];
+      for (int c = 0; c < h->near_grid; ++c) {
+        const int2 zr = h->near_zero_row[c];
+        const int rpp = std::max(1, h->tree_rows_per_prog);
+        N.zero_n[c] = int2{zr.y > 0 ? (zr.x + zr.y - 1) / rpp - zr.x / rpp + 1 : 0, 0};
+      }
     if (N.early)
       for (int c = 0; c < h->near_grid; ++c) {
         N.first_rec[c] = h->near_first_rec[c];

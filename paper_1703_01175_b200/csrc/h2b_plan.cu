@@ -25,6 +25,7 @@ int h2b_near_stream_static_smem(int ns, int r, int* bytes);
 int h2b_near_stream_set_smem(int ns, int r, int bytes);
 int h2b_near_rows_per_item(int ns, int r);
 int h2b_tree_prepare(h2b_ctx* h, int max_ctas, int budget_bytes, int64_t* bytes, int* planned);
+int h2b_tree_prepare_zero(h2b_ctx* h, TreeDev* d);
 int h2b_tree_static_smem();
 constexpr int TREE_BUDGET = 168 * 1024;  // shared memory of one subtree program (bytes)
 
@@ -1397,6 +1398,7 @@ int h2b_prepare(h2b_ctx* h) {
       if (h->mega && h->use_tree) H2B_TRY(h2b_tree_prepare(h, sms, TREE_BUDGET, &tb, &planned));
       if (planned) {
         acc += tb;
+        H2B_TRY(h2b_tree_prepare_zero(h, h->tree));
         const int tree_total = h->tree_smem + h2b_tree_static_smem() + 1024;
         int tnst = stg > 0 ? std::min(8, (sm_total - tree_total - near_static - rec_bytes) / stg) : 0;
         if (const char* e = getenv("H2B_DEBUG_NEAR_NST")) tnst = std::min(tnst, std::max(2, atoi(e)));

@@ -98,9 +98,12 @@ struct TreeArgs {
   uint32_t* flags_down;
   MegaCtrl* ctrl;
   uint64_t* trace;  // optional (H2B_TREE_TRACE): 16 timestamps per program
-  int wait_zeroed;   // > 0: y is zeroed by the near-field kernel's CTAs; bulk adds wait for this many counts
+  // y zeroed by the bottom programs at their start (ZeroSync in h2b_common.cuh; nullptr: by the
+  // caller); zrows[c] = the rows {first, count} of near-field CTA c, c < near_ctas
+  ZeroSync* zs;
+  const int2* zrows;
+  int near_ctas;
   int defer_s;       // request the staged coupling panels after the up-pass operands
-  int dbg;           // profiling only (H2B_TREE_DBG, results wrong): 1 exit once staged, 2 idle 25 us then exit
   int trace_levels;  // H2B_TREE_TRACE=2: stamps 9-14 per level of the upward pass; 3: of the downward pass
 };
 
@@ -321,6 +324,11 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int NW = TNT / 32;
   tmark(A, 0);
+  if (A.trace && threadIdx.x == 0) {
+    uint32_t sid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(sid));
+    A.trace[32 * blockIdx.x + 15] = sid;
+  }
   const TProg* gP = A.progs + blockIdx.x;
   if (tid == 0) {
     s_epoch = *(volatile uint32_t*)&A.ctrl->epoch;
@@ -344,6 +352,20 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
   // they are requested once the up-pass operands have landed, so that the launch burst (the
   // near-field stream starts at the same time) is smaller
   const bool defer_s = A.defer_s && P.pad[0] > 0;
+  // y = 0 on this program's rows (ZeroSync, h2b_common.cuh): stores, fence, barrier and the flags
+  // of the near-field CTAs whose rows overlap them, first thing (the near-field CTAs wait for the flags before their first block lands)
+  if (A.zs && P.y_n > 0) {
+    const int64_t yg = (int64_t)(uint32_t)P.y_g_lo | ((int64_t)P.y_g_hi << 32);
+    int2 zr = make_int2(0, 0);
+    if (tid < A.near_ctas) zr = A.zrows[tid];
+    for (int i = tid; i < P.y_n; i += TNT) A.y[yg + i] = make_double2(0.0, 0.0);
+    __threadfence();
+    __syncthreads();
+    if (zr.y > 0 && (int64_t)zr.x < yg + P.y_n && (int64_t)zr.x + zr.y > yg) {
+      const int slot = (int)blockIdx.x - zr.x / P.y_n;  // programs are in row order, y_n rows each
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&A.zs->flag[tid][slot]), "r"(1u) : "memory");
+    }
+  }
   for (int i = tid; i < n_copy; i += TNT) {
     const TCopy c = i == tid ? cp0 : A.copies[c0 + i];
     if (ts_late(c.kind)) {  // requested later, into the coupling panels' place
@@ -372,28 +394,6 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
       const TCopy c = i == tid ? cp0 : A.copies[c0 + i];
       if (c.kind == TS_S) bulk_g2s(sm + c.smem, (const double2*)A.src[TS_S] + c.src, 16u * (uint32_t)c.elems, &bar[1]);
     }
-  if (A.dbg) {  // profiling: how much the resident (idle) programs alone slow the near-field stream
-    if (P.pad[0]) mbar_wait(&bar[1], 0);
-    mbar_wait(&bar[2], 0);
-    if (A.dbg == 2 && tid == 0) {
-      uint64_t t0, t;
-      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
-      do {
-        __nanosleep(200);
-        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-      } while (t - t0 < 22000);
-    }
-    __syncthreads();
-    tmark(A, 7);
-    tmark(A, 8);
-    if (tid == 0 && atomicAdd(&A.ctrl->exited, 1u) == gridDim.x - 1) {
-      A.ctrl->exited = 0;
-      A.ctrl->pad[0] = 0;
-      __threadfence();
-      A.ctrl->epoch = want;
-    }
-    return;
-  }
   const TNode* nodes = reinterpret_cast<const TNode*>(sm);
   const int32_t* gidx = reinterpret_cast<const int32_t*>(sm + P.gidx_smem);
   const int yoff = P.yoff;
@@ -710,18 +710,6 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
   if (A.trace_levels >= 4) tmark(A, 12);
   if (P.y_n > 0 && tid == 0) {  // y[rows] += the assembled far field: one bulk reduce-add
     const int64_t yg = (int64_t)(uint32_t)P.y_g_lo | ((int64_t)P.y_g_hi << 32);
-    if (A.wait_zeroed > 0) {  // the near-field CTAs have zeroed their rows of y (long ago, normally)
-      for (long spins = 0;; ++spins) {
-        uint32_t v;
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&A.ctrl->pad[0]) : "memory");
-        if (v >= (uint32_t)A.wait_zeroed) break;
-        if (spins > (1l << 24)) {
-          atomicExch(&A.ctrl->error, 3u);
-          break;
-        }
-        __nanosleep(100);
-      }
-    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the generic-proxy stores above
     asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(A.y + yg),
                  "r"(smem_u32(sm + P.y_smem)), "r"(16u * (uint32_t)P.y_n)
@@ -737,7 +725,6 @@ __global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
   if (tid == 0) {
     if (atomicAdd(&A.ctrl->exited, 1u) == gridDim.x - 1) {  // last CTA out advances the epoch
       A.ctrl->exited = 0;
-      A.ctrl->pad[0] = 0;  // the near-field kernel's "y zeroed" count, for the next launch
       __threadfence();
       A.ctrl->epoch = want;
     }
@@ -1397,6 +1384,10 @@ struct TreeDev {
   uint64_t* trace = nullptr;
   int n_progs = 0, smem = 0;
   bool zero_ok = false;
+  ZeroSync* zsync = nullptr;  // h2b_tree_prepare_zero
+  int2* zrows = nullptr;      // the near-field CTAs' rows of y
+  int zrows_n = 0;
+  int rows_per_prog = 0;      // rows of y per bottom program (equal for all when zero_ok)
 };
 
 namespace {
@@ -1443,7 +1434,17 @@ int h2b_tree_upload(const TreePlan& tp, TreeDev** out, int64_t* bytes) {
         all = all && P.y_n > 0;
         rows += P.y_n;
       }
-    d->zero_ok = all && rows == tp.n_rows_total;
+    // (programs in row order, equal row counts: the near-field CTAs map rows to programs by division)
+    int rpp = 0;
+    for (size_t i = 0; i < tp.progs.size(); ++i) {
+      const TProg& P = tp.progs[i];
+      if (!P.bottom) continue;
+      if (rpp == 0) rpp = P.y_n;
+      const int64_t yg = (int64_t)(uint32_t)P.y_g_lo | ((int64_t)P.y_g_hi << 32);
+      all = all && P.y_n == rpp && yg == (int64_t)i * rpp;
+    }
+    d->zero_ok = all && rows == tp.n_rows_total && rpp > 0;
+    d->rows_per_prog = rpp;
   }
   if (!rc && getenv("H2B_TREE_TRACE")) {
     cudaMalloc(&d->trace, sizeof(uint64_t) * 32 * std::max(d->n_progs, 1));
@@ -1466,7 +1467,8 @@ int h2b_tree_upload(const TreePlan& tp, TreeDev** out, int64_t* bytes) {
 
 void h2b_tree_free(TreeDev* d) {
   if (!d) return;
-  void* ptrs[] = {d->progs, d->copies, d->waits, d->nodes, d->gidx, d->flat, d->px, d->flags, d->ctrl, d->trace};
+  void* ptrs[] = {d->progs, d->copies, d->waits, d->nodes, d->gidx, d->flat, d->px, d->flags, d->ctrl, d->trace,
+                  d->zsync, d->zrows};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete d;
@@ -1521,18 +1523,40 @@ int h2b_tree_prepare(h2b_ctx* h, int max_ctas, int budget_bytes, int64_t* bytes,
   h->tree_progs = (int)tp.progs.size();
   h->tree_smem = tp.smem_max;
   h->tree_flat = tp.flat ? 1 : 0;
+  h->tree_rows_per_prog = h->tree->rows_per_prog;
   *planned = 1;
   return H2B_OK;
 }
 
 // one launch of the far field on `st` (cooperative: the programs wait on one another)
-// the "y zeroed" count of the near-field kernel's CTAs (see h2b_launch_mega), when every far-field
-// contribution to y is a bottom program's bulk add (which waits for the count); else nullptr
-uint32_t* h2b_tree_zeroed_counter(const TreeDev* d) { return d && d->zero_ok ? &d->ctrl->pad[0] : nullptr; }
+// the zeroing protocol's state (ZeroSync, h2b_common.cuh) when every far-field contribution to
+// y is a bottom program's bulk add (which checks its rows' ranges first); else nullptr.  Allocated
+// here on first use (never inside a capture: h2b_launch_mega is reached through h2b_prepare'd
+// handles whose first matvec runs this before capturing — cudaMalloc is legal in thread-local
+// capture mode only outside the capturing stream, so it is done in h2b_tree_prepare_zero).
+ZeroSync* h2b_tree_zero_sync(h2b_ctx* h, TreeDev* d) {
+  (void)h;
+  return d && d->zero_ok ? d->zsync : nullptr;
+}
 
-int h2b_launch_tree(h2b_ctx* h, const TreeDev* d, const double2* xp, double2* yp, cudaStream_t st, int wait_zeroed) {
+int h2b_tree_prepare_zero(h2b_ctx* h, TreeDev* d) {
+  if (!d || !d->zero_ok || d->zsync || !h->near_zero_ok || h->near_grid > NEAR_MAXG) return H2B_OK;
+  for (const int2& zr : h->near_zero_row)  // a CTA's rows span at most ZS_SLOTS programs
+    if (zr.y > 0 && (zr.x + zr.y - 1) / d->rows_per_prog - zr.x / d->rows_per_prog + 1 > ZS_SLOTS) return H2B_OK;
+  H2B_CUDA_TRY(cudaMalloc((void**)&d->zsync, sizeof(ZeroSync)));
+  H2B_CUDA_TRY(cudaMemset(d->zsync, 0, sizeof(ZeroSync)));
+  H2B_CUDA_TRY(cudaMalloc((void**)&d->zrows, sizeof(int2) * std::max<size_t>(h->near_zero_row.size(), 1)));
+  H2B_CUDA_TRY(cudaMemcpy(d->zrows, h->near_zero_row.data(), sizeof(int2) * h->near_zero_row.size(),
+                          cudaMemcpyHostToDevice));
+  d->zrows_n = (int)h->near_zero_row.size();
+  return H2B_OK;
+}
+
+int h2b_launch_tree(h2b_ctx* h, const TreeDev* d, const double2* xp, double2* yp, cudaStream_t st, int near_ctas) {
   TreeArgs A;
-  A.wait_zeroed = wait_zeroed;
+  A.zs = near_ctas > 0 ? d->zsync : nullptr;
+  A.zrows = d->zrows;
+  A.near_ctas = A.zs ? std::min(near_ctas, d->zrows_n) : 0;
   A.progs = d->progs;
   A.copies = d->copies;
   A.waits = d->waits;
@@ -1558,8 +1582,6 @@ int h2b_launch_tree(h2b_ctx* h, const TreeDev* d, const double2* xp, double2* yp
     A.trace_levels = e ? atoi(e) : 0;
     const char* d = getenv("H2B_TREE_DEFER_S");  // A/B aid
     A.defer_s = d ? atoi(d) : 1;  // measured: step 40.3 vs 41.0 us at cfg2
-    const char* g = getenv("H2B_TREE_DBG");
-    A.dbg = g ? atoi(g) : 0;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(d->n_progs);
@@ -1570,7 +1592,8 @@ int h2b_launch_tree(h2b_ctx* h, const TreeDev* d, const double2* xp, double2* yp
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  static const bool nocoop = getenv("H2B_TREE_NOCOOP") != nullptr;  // A/B aid
+  cfg.numAttrs = nocoop ? 0 : 1;
   H2B_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_far_tree, A));
   return H2B_OK;
 }

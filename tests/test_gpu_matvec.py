@@ -158,6 +158,41 @@ def C_int64():
     return ctypes.c_int64()
 
 
+@pytest.mark.parametrize("k", [2])
+def test_tree_far_field_variants_agree(k, monkeypatch):
+    """cfg2's far field as subtree programs: the flat top (transfer chains and folded ancestor
+    panels, no top programs) and the top-program plan, with y zeroed by the near kernel's CTAs
+    or by a memset node — all within rounding of the reference's own output, the tree plan
+    taken in every case."""
+    from paper_1703_01175_b200 import H2Operator, _abi
+    pk, ex = load_config(k)
+    L = _abi.lib()
+    outs = {}
+    for no_flat in (0, 1):
+        for memset in (0, 1):
+            monkeypatch.delenv("H2B_TREE_NO_FLAT", raising=False)
+            monkeypatch.delenv("H2B_Y_MEMSET", raising=False)
+            if no_flat:
+                monkeypatch.setenv("H2B_TREE_NO_FLAT", "1")
+            if memset:
+                monkeypatch.setenv("H2B_Y_MEMSET", "1")
+            op = H2Operator(pk)
+            y = op.matvec(ex["x"][:, 0])
+            y2 = op.matvec(ex["x"][:, 0])
+            assert np.array_equal(y, y2)
+            assert rel(y, ex["y"][:, 0]) <= 1e-12, (no_flat, memset)
+            tq, err = C_int64(), C_int64()
+            _abi.check(L.h2b_query(op.handle, _abi.Q_TREE, tq))
+            assert tq.value != 0 and ((tq.value >> 30) & 1) == 1 - no_flat
+            _abi.check(L.h2b_query(op.handle, _abi.Q_DEVICE_ERROR, err))
+            assert err.value == 0
+            outs[(no_flat, memset)] = y
+            op.close()
+    # the zeroing variant does not change a bit; the flat top reassociates the top-tier products
+    assert np.array_equal(outs[(0, 0)], outs[(0, 1)]) and np.array_equal(outs[(1, 0)], outs[(1, 1)])
+    assert rel(outs[(0, 0)], outs[(1, 0)]) <= 1e-13
+
+
 @pytest.mark.parametrize("k", [1, 2])
 def test_persistent_kernel_repeated_launches(k):
     """Epoch-stamped flags: many back-to-back launches stay correct and deterministic."""

@@ -42,4 +42,7 @@ for graphs in (1,):
             torch.cuda.synchronize()
             ts.append(s.elapsed_time(e) * 1e3)
         print(f"graphs={graphs} {nm:26s} mean {np.mean(ts):6.2f} us  median {np.median(ts):6.1f}  min {np.min(ts):6.1f}")
+        if os.environ.get("PROBE_HIST"):
+            v, c = np.unique(np.round(ts, 1), return_counts=True)
+            print("   ", ", ".join(f"{a:.1f}x{b}" for a, b in zip(v, c)))
         op.close()

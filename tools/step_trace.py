@@ -63,6 +63,11 @@ for rep in range(10):
     tt = np.zeros((nprog, 32), dtype=np.int64) if nprog else None
     if nprog:
         _abi.check(L.h2b_tree_trace(op.handle, tt.ctypes.data, nprog))
+    if rep == 9 and nprog:
+        far_sm = set(int(v) for v in tt[:, 15])
+        near_sm = nt[:, 7]
+        free = [c for c in range(ncta) if int(near_sm[c]) not in far_sm]
+        print(f"near CTAs on SMs without a far program: {len(free)}: {free}")
     if rep < 2:
         continue
     t0 = nt[:, 0].min()
