@@ -4,7 +4,7 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 -lineinfo --extended-lambda $(ARCH) -Xcompiler -fPIC,-O3,-Wall -Xptxas -v
 SRC := $(wildcard paper_1703_01175_b200/csrc/*.cu)
-HDR := $(wildcard paper_1703_01175_b200/csrc/*.cuh) include/h2b.h
+HDR := $(wildcard paper_1703_01175_b200/csrc/*.cuh) $(wildcard paper_1703_01175_b200/csrc/*.inc) include/h2b.h
 OBJ := $(patsubst paper_1703_01175_b200/csrc/%.cu,build/%.o,$(SRC))
 LIB := paper_1703_01175_b200/libh2b.so
 

@@ -152,7 +152,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // at most 80 registers: its 9 warps sit beside the far kernel's 8 (<= 128 registers) within each
 // scheduler's 16K-register share (warp i runs on scheduler i % 4: scheduler 0 holds 3 near
 // warps).  Over budget, most near CTAs wait for the far kernel to exit (measured: step 82 us)
-template <int NS, int R>
+// TR: the per-CTA timeline (H2B_NEAR_TRACE) is compiled into a second instantiation only: the
+// stamps' predicated clock reads sat on the consumer's per-block chain (~5 % of its stall samples)
+template <int NS, int R, bool TR = false>
 __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
   // dynamic shared memory: [ring: nst stages][NRB record buffers]
   extern __shared__ __align__(16) double2 sm[];
@@ -165,7 +167,7 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
   const int nst = NS > 0 ? A.nst : 0;
   int4* rbuf0 = reinterpret_cast<int4*>(sm + (size_t)nst * STG);
   auto rbuf = [&](int b) { return rbuf0 + (size_t)b * A.rec_slots; };
-  uint64_t* tr = A.trace ? A.trace + 24 * blockIdx.x : nullptr;
+  uint64_t* tr = TR && A.trace ? A.trace + 24 * blockIdx.x : nullptr;
   uint64_t cw[4] = {0, 0, 0, 0};  // trace: wait cycles (see h2b_near_trace)
   if (threadIdx.x == 0) {
     if (tr) {
@@ -794,12 +796,16 @@ int h2b_near_stream_set_smem(int ns, int r, int bytes) {
   if (ns == a && r == b) {                                                                                \
     H2B_CUDA_TRY(cudaFuncSetAttribute(k_near_stream<a, b>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)); \
     H2B_CUDA_TRY(cudaFuncSetAttribute(k_near_stream<a, b>, cudaFuncAttributePreferredSharedMemoryCarveout, 100)); \
+    H2B_CUDA_TRY(cudaFuncSetAttribute(k_near_stream<a, b, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)); \
+    H2B_CUDA_TRY(cudaFuncSetAttribute(k_near_stream<a, b, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100)); \
   }
   NEAR_VARIANTS(X)
 #undef X
   if (ns != 32 && ns != 64) {
     H2B_CUDA_TRY(cudaFuncSetAttribute(k_near_stream<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     H2B_CUDA_TRY(cudaFuncSetAttribute(k_near_stream<0, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    H2B_CUDA_TRY(cudaFuncSetAttribute(k_near_stream<0, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    H2B_CUDA_TRY(cudaFuncSetAttribute(k_near_stream<0, 1, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   }
   return H2B_OK;
 }
@@ -907,12 +913,20 @@ int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st)
     bool launched = false;
 #define X(a, b)                                                                            \
   if (!launched && ns == a && r == b) {                                                    \
-    k_near_stream<a, b><<<h->near_grid, NEAR_THREADS, h->near_smem, st>>>(N);                       \
+    if (N.trace)                                                                           \
+      k_near_stream<a, b, true><<<h->near_grid, NEAR_THREADS, h->near_smem, st>>>(N);               \
+    else                                                                                   \
+      k_near_stream<a, b><<<h->near_grid, NEAR_THREADS, h->near_smem, st>>>(N);                     \
     launched = true;                                                                       \
   }
     NEAR_VARIANTS(X)
 #undef X
-    if (!launched) k_near_stream<0, 1><<<h->near_grid, NEAR_THREADS, h->near_smem, st>>>(N);
+    if (!launched) {
+      if (N.trace)
+        k_near_stream<0, 1, true><<<h->near_grid, NEAR_THREADS, h->near_smem, st>>>(N);
+      else
+        k_near_stream<0, 1><<<h->near_grid, NEAR_THREADS, h->near_smem, st>>>(N);
+    }
     H2B_CHECK_LAUNCH();
   }
   if (run_far) {

@@ -315,421 +315,20 @@ __device__ __forceinline__ void cta_rowdot(const TNode* nodes, int a, int b, int
 
 // at most 128 registers: 2 warps per scheduler (8192 registers) leave the near-field stream's 3
 // warps on scheduler 0 their 80 each within the scheduler's 16K (both kernels co-resident)
-__global__ void __maxnreg__(128) k_far_tree(TreeArgs A) {
-  extern __shared__ __align__(16) double2 sm[];
-  // [0]: nodes, gather list, x, V (the leaf level)  [1]: staged S panels  [2]: T (internal levels)
-  __shared__ __align__(8) uint64_t bar[4];
-  __shared__ uint32_t s_epoch;
-  __shared__ TProg P;  // the program header (global loads would recur after every fence)
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int NW = TNT / 32;
-  tmark(A, 0);
-  if (A.trace && threadIdx.x == 0) {
-    uint32_t sid;
-    asm volatile("mov.u32 %0, %smid;" : "=r"(sid));
-    A.trace[32 * blockIdx.x + 15] = sid;
-  }
-  const TProg* gP = A.progs + blockIdx.x;
-  if (tid == 0) {
-    s_epoch = *(volatile uint32_t*)&A.ctrl->epoch;
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    mbar_init(&bar[2], 1);
-    mbar_init(&bar[3], 1);
-  }
-  for (int i = tid; i < (int)(sizeof(TProg) / 4); i += TNT)
-    reinterpret_cast<int32_t*>(&P)[i] = reinterpret_cast<const int32_t*>(gP)[i];
-  // this thread's bulk copies (up-pass operands complete on bar[0], coupling panels on bar[1])
-  const int n_copy = gP->n_copy, c0 = gP->copy_first;
-  TCopy cp0 = tid < n_copy ? A.copies[c0 + tid] : TCopy{};
-  __syncthreads();
-  if (tid == 0) {
-    mbar_arrive_expect_tx(&bar[0], (uint32_t)P.stage_bytes);
-    mbar_arrive_expect_tx(&bar[1], (uint32_t)P.pad[0]);  // staged coupling panels (0: from L2)
-    mbar_arrive_expect_tx(&bar[2], (uint32_t)P.pad[1]);  // transfer matrices
-  }
-  // coupling panels (about half of the staged bytes at cfg2) are needed last: with A.defer_s
-  // they are requested once the up-pass operands have landed, so that the launch burst (the
-  // near-field stream starts at the same time) is smaller
-  const bool defer_s = A.defer_s && P.pad[0] > 0;
-  // y = 0 on this program's rows (ZeroSync, h2b_common.cuh): stores, fence, barrier and the flags
-  // of the near-field CTAs whose rows overlap them, first thing (the near-field CTAs wait for the flags before their first block lands)
-  if (A.zs && P.y_n > 0) {
-    const int64_t yg = (int64_t)(uint32_t)P.y_g_lo | ((int64_t)P.y_g_hi << 32);
-    int2 zr = make_int2(0, 0);
-    if (tid < A.near_ctas) zr = A.zrows[tid];
-    for (int i = tid; i < P.y_n; i += TNT) A.y[yg + i] = make_double2(0.0, 0.0);
-    __threadfence();
-    __syncthreads();
-    if (zr.y > 0 && (int64_t)zr.x < yg + P.y_n && (int64_t)zr.x + zr.y > yg) {
-      const int slot = (int)blockIdx.x - zr.x / P.y_n;  // programs are in row order, y_n rows each
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&A.zs->flag[tid][slot]), "r"(1u) : "memory");
-    }
-  }
-  for (int i = tid; i < n_copy; i += TNT) {
-    const TCopy c = i == tid ? cp0 : A.copies[c0 + i];
-    if (ts_late(c.kind)) {  // requested later, into the coupling panels' place
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const double2*)A.src[TS_FH] + c.src),
-                   "r"(16u * (uint32_t)c.elems) : "memory");
-      continue;
-    }
-    if (defer_s && c.kind == TS_S) continue;
-    if (c.kind == TS_S && c.smem < 0) {  // coupling panels read from L2 by the couplings: warm them
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const double2*)A.src[TS_S] + c.src),
-                   "r"(16u * (uint32_t)c.elems) : "memory");
-      continue;
-    }
-    const void* base = c.kind == TS_X ? A.src[TS_X] : c.kind == TS_V ? A.src[TS_V] : c.kind == TS_T ? A.src[TS_T]
-                     : c.kind == TS_S ? A.src[TS_S] : c.kind == TS_NODES ? A.src[TS_NODES]
-                     : c.kind == TS_GIDX ? A.src[TS_GIDX] : A.src[TS_FM];
-    bulk_g2s(sm + c.smem, (const double2*)base + c.src, 16u * (uint32_t)c.elems,
-             &bar[c.kind == TS_S ? 1 : (c.kind == TS_T || c.kind == TS_FM) ? 2 : 0]);
-  }
-  const uint32_t want = s_epoch + 1;
-  mbar_wait(&bar[0], 0);
-  tmark(A, 1);
-  if (defer_s)
-#pragma unroll 1
-    for (int i = tid; i < n_copy; i += TNT) {
-      const TCopy c = i == tid ? cp0 : A.copies[c0 + i];
-      if (c.kind == TS_S) bulk_g2s(sm + c.smem, (const double2*)A.src[TS_S] + c.src, 16u * (uint32_t)c.elems, &bar[1]);
-    }
-  const TNode* nodes = reinterpret_cast<const TNode*>(sm);
-  const int32_t* gidx = reinterpret_cast<const int32_t*>(sm + P.gidx_smem);
-  const int yoff = P.yoff;
-  const int nlev = P.nlev;
-  const int shk = P.pad[2] & 255, shr = (P.pad[2] >> 8) & 255;  // threads per node: 2^shk (columns), 2^shr (rows)
-  // ---- top programs: the external children's x̂ (bottom programs' roots) ----
-  if (P.n_ext_wait) {
-    wait_flags(A.flags_up, A.waits + P.ext_wait_first, P.n_ext_wait, want, A.ctrl);
-    __syncthreads();
-    tmark(A, 2);
-    // one L2 round trip, not one per node: a warp issues the loads of U nodes before any store
-    // (the stores to shared memory would otherwise order each next load behind them)
-    const int e0 = P.lev_first[nlev - 1], e1 = P.lev_first[nlev];
-    constexpr int U = 4;
-    for (int i0 = e0 + warp; i0 < e1; i0 += NW * U) {
-      double2 v[U];
-      int dst[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * NW;
-        dst[u] = -1;
-        if (i < e1) {
-          const TNode nd = nodes[i];
-          const int64_t gx = (int64_t)(uint32_t)nd.gx_lo | ((int64_t)nd.gx_hi << 32);
-          if (lane < nd.k) {
-            v[u] = __ldcg(A.xhat + gx + lane);
-            dst[u] = nd.xh + lane;
-          }
-#pragma unroll 1
-          for (int j = lane + 32; j < nd.k; j += 32) sm[nd.xh + j] = __ldcg(A.xhat + gx + j);  // k > 32
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (dst[u] >= 0) sm[dst[u]] = v[u];
-    }
-    __syncthreads();
-  }
-  // ---- upward pass, deepest level first (the transfer matrices land during the leaf level) ----
-  bool t_ready = false;
-  for (int lv = nlev - 1; lv >= 0; --lv) {
-    const int a = P.lev_first[lv], b = P.lev_first[lv + 1];
-    if (!t_ready && (!P.bottom || lv < nlev - 1)) {
-      mbar_wait(&bar[2], 0);
-      t_ready = true;
-    }
-    for (int i = a + warp; i < b; i += NW) {
-      const TNode nd = nodes[i];
-      if (nd.kind != 2 && nd.k > 0) colsum(sm + nd.pay, nd.R, nd.k, nd.sh, sm + nd.in, sm + nd.xh);
-    }
-    __syncthreads();
-    if (lv >= nlev - 6 && A.trace_levels == 2) tmark(A, 9 + (nlev - 1 - lv));
-  }
-  // ---- flat top: this program's share of every ancestor's x̂ (M_dᵀ x̂_root), one warp each ----
-  if (P.n_flat) {
-    if (!t_ready) {
-      mbar_wait(&bar[2], 0);
-      t_ready = true;
-    }
-    const TNode rt = nodes[0];
-    for (int j = warp; j < P.n_flat; j += NW) {
-      const TNode nd = nodes[P.flat_first + j];
-      const int64_t gx = (int64_t)(uint32_t)nd.gx_lo | ((int64_t)nd.gx_hi << 32);
-      colsum(sm + nd.pay, rt.k, nd.R, nd.sh, sm + rt.xh, A.px + gx);
-    }
-  }
-  // ---- publish x̂ of the program's own nodes ----
-  {
-    const int e = P.bottom ? P.lev_first[nlev] : P.lev_first[nlev - 1];
-    for (int i = warp; i < e; i += NW) {
-      const TNode nd = nodes[i];
-      const int64_t gx = (int64_t)(uint32_t)nd.gx_lo | ((int64_t)nd.gx_hi << 32);
-#pragma unroll 1
-      for (int j = lane; j < nd.k; j += 32) A.xhat[gx + j] = sm[nd.xh + j];
-    }
-    __syncthreads();  // the CTA's x̂ stores happen before thread 0's (cumulative) release
-    if (tid == 0) st_rel(A.flags_up + blockIdx.x, want);
-    tmark(A, 3);
-  }
-  // ---- couplings: gather x̂ of the sources (own smem or other programs' published x̂) ----
-  wait_flags(A.flags_up, A.waits + P.wait_up_first, P.n_wait_up, want, A.ctrl);
-  if (P.pad[0]) mbar_wait(&bar[1], 0);
-  if (!t_ready) mbar_wait(&bar[2], 0);
-  __syncthreads();
-  tmark(A, 4);
-  double2* xg = sm + P.xg_smem;
-  {
-    constexpr int U = 4;  // loads of U elements in flight per thread before their stores
-    for (int i0 = tid; i0 < P.n_xg; i0 += TNT * U) {
-      double2 v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * TNT;
-        if (i < P.n_xg) {
-          const int g = gidx[i];
-          v[u] = g >= 0 ? __ldcg(A.xhat + g) : sm[~g];
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (i0 + u * TNT < P.n_xg) xg[i0 + u * TNT] = v[u];
-    }
-  }
-  __syncthreads();
-  if (A.trace_levels == 3) tmark(A, 9);
-  cta_colsum(nodes, 0, P.bottom ? P.lev_first[nlev] : P.lev_first[nlev - 1], shk,
-             [&](const TNode& nd, const double2*& M, int& R, int& w, const double2*& in, double2*& out) {
-               if (nd.k == 0) return false;
-               const int64_t so = (int64_t)(uint32_t)nd.s_pay | ((int64_t)nd.pad << 32);
-               M = P.pad[0] ? sm + so : (const double2*)A.src[TS_S] + so;  // staged or L2
-               R = nd.s_rows;  // 0: no couplings (ŷ = 0)
-               w = nd.k;
-               in = xg + nd.xg;
-               out = sm + nd.xh + yoff;
-               return true;
-             });
-#pragma unroll 1
-  for (int i = tid; i < P.y_n; i += TNT) sm[P.y_smem + i] = make_double2(0.0, 0.0);  // x is dead
-  if (A.trace_levels == 3) {
-    __syncthreads();
-    tmark(A, 10);
-  }
-  const bool split = P.bottom && (P.wait_down >= 0 || P.n_flat) && P.split_mode > 0;
-  if (P.fh_bytes) {
-    // flat top: the H panels take the place of the staged coupling panels (dead once every
-    // thread is past the couplings above); they were prefetched to L2 at launch
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_expect_tx(&bar[3], (uint32_t)P.fh_bytes);
-    }
-    __syncthreads();
-#pragma unroll 1
-    for (int i = tid; i < n_copy; i += TNT) {
-      const TCopy c = i == tid ? cp0 : A.copies[c0 + i];
-      if (ts_late(c.kind)) bulk_g2s(sm + c.smem, (const double2*)A.src[TS_FH] + c.src, 16u * (uint32_t)c.elems, &bar[3]);
-    }
-  }
-  if (P.wait_down >= 0 && !split) {
-    const int32_t wd = P.wait_down;
-    tmark(A, 5);
-    wait_flags(A.flags_down, &wd, 1, want, A.ctrl);
-    __syncthreads();  // also orders the coupling writes above
-    tmark(A, 6);
-    if (warp == 0) {
-      const TNode nd = nodes[0];
-      const int64_t gx = (int64_t)(uint32_t)nd.gx_lo | ((int64_t)nd.gx_hi << 32);
-      for (int j = lane; j < nd.k; j += 32) {
-        const double2 v = __ldcg(A.yhat + gx + j);
-        double2& o = sm[nd.xh + yoff + j];
-        o = cadd(o, v);
-      }
-    }
-  }
-  __syncthreads();
-  // ---- downward pass, root level first: children ŷ += T ŷ_parent; leaves: y += V ŷ ----
-  for (int lv = 0; lv < nlev; ++lv) {
-    const int a = P.lev_first[lv], b = P.lev_first[lv + 1];
-    for (int i = a + warp; i < b; i += NW) {
-      const TNode nd = nodes[i];
-      if (nd.k == 0 || nd.kind == 2) continue;
-      if (split && nd.kind == 0) continue;  // leaves wait for the root's contribution (below)
-      const double2* yp = sm + nd.xh + yoff;
-      const int64_t g = (int64_t)(uint32_t)nd.gy_lo | ((int64_t)nd.gy_hi << 32);
-      for (int r = lane; r < nd.R; r += 32) {
-        const double2 v = rowdot(sm + nd.pay, r, nd.k, yp);
-        if (nd.kind == 0) {  // leaf back-transform into y (k_near_stream adds concurrently)
-          if (P.y_n > 0) {
-            sm[nd.in + r] = v;  // the program's y rows (bulk-added below)
-          } else {
-            atomicAdd(&A.y[g + r].x, v.x);
-            atomicAdd(&A.y[g + r].y, v.y);
-          }
-        } else if (nd.ext) {  // external children: their parent contribution to global ŷ
-          A.yhat[g + r] = v;
-        } else {  // [ŷ_lo; ŷ_hi] are adjacent, right behind [x̂_lo; x̂_hi]
-          double2& o = sm[nd.in + yoff + r];
-          o = cadd(o, v);
-        }
-      }
-    }
-    __syncthreads();
-    if (A.trace_levels == 3 && lv < 4) tmark(A, 11 + lv);
-  }
-  if (split) {
-    // F_root = I; F_c = T_parent[rows of c] F_parent (k_c x k_root), level by level
-    const int kr = nodes[0].k, fs = P.f_stride;
-    double2* F = sm + P.f_base;
-    for (int lv = 0; lv < (P.split_mode == 1 ? nlev : 0); ++lv) {
-      const int a = P.lev_first[lv], b = P.lev_first[lv + 1];
-      for (int i = a + warp; i < b; i += NW) {
-        const int kc = nodes[i].k;
-        double2* Fi = F + (int64_t)i * fs;
-        if (lv == 0) {
-#pragma unroll 1
-          for (int e = lane; e < kc * kr; e += 32) Fi[e] = make_double2(e / kr == e % kr ? 1.0 : 0.0, 0.0);
-          continue;
-        }
-        const int pi = P.lev_first[lv - 1] + (i - a) / 2, hi = (i - a) & 1;
-        const TNode pn = nodes[pi];
-        const int kp = pn.k, r0 = hi ? nodes[a + 2 * (pi - P.lev_first[lv - 1])].k : 0;
-        const double2* Fp = F + (int64_t)pi * fs;
-        for (int e = lane; e < kc * kr; e += 32) {
-          const int r = e / kr, c = e % kr;
-          double2 s = make_double2(0.0, 0.0);
-#pragma unroll 1
-          for (int j = 0; j < kp; ++j) cfma(s, sm[pn.pay + (r0 + r) * kp + j], Fp[j * kr + c]);
-          Fi[e] = s;
-        }
-      }
-      __syncthreads();
-    }
-    // g = the root's parent contribution (k_root <= 32 in split mode; the root's own ŷ slot may be
-    // a leaf's, still needed)
-    __shared__ double2 gsh[32];
-    double2* gv = gsh;
-    tmark(A, 5);
-    if (P.n_flat) {
-      // flat top: the partials of the programs below every source of every ancestor, then the
-      // ancestors' couplings and the way down to this root in one panel product per ancestor
-      wait_flags(A.flags_up, A.waits + P.wait_far_first, P.n_wait_far, want, A.ctrl);
-      __syncthreads();
-      tmark(A, 6);
-    if (P.n_frow) {
-      // x̂ of the ancestors' sources: the sum of the partials of the bottom programs below each
-      // source, 2^d partials per entry on adjacent lanes (butterfly: a fixed summation order)
-      const int4* fr = reinterpret_cast<const int4*>(sm + P.frow_smem);
-      const int32_t* eb = reinterpret_cast<const int32_t*>(sm + P.ebase_smem);
-      constexpr int U = 4;
-      for (int r0 = warp; r0 < P.n_frow; r0 += NW * U) {
-        double2 v[U];
-        int4 hd[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int r = r0 + u * NW;
-          v[u] = make_double2(0.0, 0.0);
-          hd[u] = make_int4(0, 0, 0, 0);
-          if (r < P.n_frow) {
-            hd[u] = fr[r];
-            const int e = lane >> hd[u].x;
-            if (e < hd[u].z) v[u] = __ldcg(A.px + eb[hd[u].y + e] + (lane & ((1 << hd[u].x) - 1)) * P.px_stride);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (r0 + u * NW >= P.n_frow) continue;  // warp-uniform
-          for (int m = 1; m < (1 << hd[u].x); m <<= 1) v[u] = cadd(v[u], shfl_xor2(v[u], m));
-          const int e = lane >> hd[u].x;
-          if ((lane & ((1 << hd[u].x) - 1)) == 0 && e < hd[u].z) xg[hd[u].w + e] = v[u];
-        }
-      }
-    }
-      if (P.fh_bytes) mbar_wait(&bar[3], 0);
-      __syncthreads();
-      cta_colsum(nodes, P.flat_first, P.flat_first + P.n_flat, shk,
-                 [&](const TNode& nd, const double2*& M, int& R, int& w, const double2*& in, double2*& out) {
-                   if (nd.k == 0) return false;
-                   M = sm + nd.s_pay;
-                   R = nd.s_rows;
-                   w = nd.k;
-                   in = xg + nd.xg;
-                   out = sm + nd.xh + yoff;
-                   return true;
-                 });
-      __syncthreads();
-      if (tid < nodes[0].k) {
-        double2 a = make_double2(0.0, 0.0);
-        for (int j = 0; j < P.n_flat; ++j) a = cadd(a, sm[nodes[P.flat_first + j].xh + yoff + tid]);
-        gv[tid] = a;
-      }
-    } else {
-      const int32_t wd = P.wait_down;
-      wait_flags(A.flags_down, &wd, 1, want, A.ctrl);
-      __syncthreads();
-      tmark(A, 6);
-      if (warp == 0) {
-        const TNode nd = nodes[0];
-        const int64_t gx = (int64_t)(uint32_t)nd.gx_lo | ((int64_t)nd.gx_hi << 32);
-        for (int j = lane; j < nd.k; j += 32) gv[j] = __ldcg(A.yhat + gx + j);
-      }
-    }
-    __syncthreads();
-    if (A.trace_levels >= 4) tmark(A, 11);
-    // leaves: u = ŷ_leaf (local part) + F_leaf g, then y += V u — one contribution per element
-    // of y from the far field, as without the split (two addends in y: deterministic)
-    const int a = P.lev_first[nlev - 1], b = P.lev_first[nlev];
-    for (int rep = 0; rep < (A.trace_levels == 5 ? 2 : 1); ++rep) {  // 5: profiling (results wrong)
-    for (int i = a + warp; i < b; i += NW) {
-      const TNode nd = nodes[i];
-      if (nd.k == 0) continue;
-      double2* u = sm + nd.xh + yoff;
-      const double2* Fi = F + (int64_t)i * fs;
-      if (lane < nd.k) {
-        double2 s = u[lane];
-        for (int c = 0; c < kr; ++c) cfma(s, Fi[lane * kr + c], gv[c]);
-        u[lane] = s;
-      }
-      __syncwarp();
-      const int64_t g = (int64_t)(uint32_t)nd.gy_lo | ((int64_t)nd.gy_hi << 32);
-      for (int r = lane; r < nd.R; r += 32) {
-        const double2 v = rowdot(sm + nd.pay, r, nd.k, u);
-        if (P.y_n > 0) {
-          sm[nd.in + r] = v;
-        } else {
-          atomicAdd(&A.y[g + r].x, v.x);
-          atomicAdd(&A.y[g + r].y, v.y);
-        }
-      }
-    }
-    __syncthreads();
-    if (rep == 0 && A.trace_levels == 5) tmark(A, 13);
-    }
-  }
-  if (A.trace_levels >= 4) tmark(A, 12);
-  if (P.y_n > 0 && tid == 0) {  // y[rows] += the assembled far field: one bulk reduce-add
-    const int64_t yg = (int64_t)(uint32_t)P.y_g_lo | ((int64_t)P.y_g_hi << 32);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the generic-proxy stores above
-    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(A.y + yg),
-                 "r"(smem_u32(sm + P.y_smem)), "r"(16u * (uint32_t)P.y_n)
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem stays valid until read
-  }
-  tmark(A, 7);
-  if (!P.bottom) {  // hand the external children's ŷ to the bottom programs (cumulative release)
-    if (tid == 0) st_rel(A.flags_down + blockIdx.x, want);
-  }
-  tmark(A, 8);
-  if (tid == 0) {
-    if (atomicAdd(&A.ctrl->exited, 1u) == gridDim.x - 1) {  // last CTA out advances the epoch
-      A.ctrl->exited = 0;
-      __threadfence();
-      A.ctrl->epoch = want;
-    }
-  }
-}
+#define H2B_TREE_KERNEL k_far_tree
+#define H2B_TREE_TR 0
+#define H2B_TMARK(A, i) ((void)0)
+#include "h2b_tree_kernel.inc"
+#undef H2B_TREE_KERNEL
+#undef H2B_TREE_TR
+#undef H2B_TMARK
+#define H2B_TREE_KERNEL k_far_tree_traced
+#define H2B_TREE_TR 1
+#define H2B_TMARK(A, i) tmark(A, i)
+#include "h2b_tree_kernel.inc"
+#undef H2B_TREE_KERNEL
+#undef H2B_TREE_TR
+#undef H2B_TMARK
 
 }  // namespace
 
@@ -1453,6 +1052,8 @@ int h2b_tree_upload(const TreePlan& tp, TreeDev** out, int64_t* bytes) {
   if (!rc) {
     const cudaError_t e = cudaFuncSetAttribute(k_far_tree, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 14000);
     cudaFuncSetAttribute(k_far_tree, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_far_tree_traced, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 14000);
+    cudaFuncSetAttribute(k_far_tree_traced, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) {
       h2b_set_error(std::string("k_far_tree attributes: ") + cudaGetErrorString(e));
       rc = H2B_ECUDA;
@@ -1594,7 +1195,10 @@ int h2b_launch_tree(h2b_ctx* h, const TreeDev* d, const double2* xp, double2* yp
   cfg.attrs = attr;
   static const bool nocoop = getenv("H2B_TREE_NOCOOP") != nullptr;  // A/B aid
   cfg.numAttrs = nocoop ? 0 : 1;
-  H2B_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_far_tree, A));
+  if (A.trace)
+    H2B_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_far_tree_traced, A));
+  else
+    H2B_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_far_tree, A));
   return H2B_OK;
 }
 
