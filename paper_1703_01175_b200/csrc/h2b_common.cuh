@@ -423,6 +423,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   for (uint32_t spins = 0; !mbar_try_wait(bar, phase);)
     if (++spins == (1u << 26)) __trap();
 }
+// The same on shared-window addresses computed once (smem_u32 before a loop): inside a
+// latency-bound loop the generic-to-shared conversion of every call re-reads SR_CgaCtaId
+// (S2UR + ULEA + IMAD, ~10 % of the near-field consumer's stall samples)
+__device__ __forceinline__ void mbar_arrive_expect_tx_a(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_a(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait_a(uint32_t bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t phase) {
+  for (uint32_t spins = 0; !mbar_try_wait_a(bar, phase);)
+    if (++spins == (1u << 26)) __trap();
+}
 // global -> shared bulk copy completing on `bar` (bytes % 16 == 0, 16-B aligned)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(

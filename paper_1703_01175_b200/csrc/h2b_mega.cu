@@ -105,6 +105,18 @@ struct NearArgs {
 // tasks are.
 constexpr int NRB = NEAR_NRB;  // record buffers: the consumer's task and up to NRB - 1 claimed ahead
 
+__device__ __forceinline__ void bulk_g2s_hint_a(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_a(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
 template <int NS, int R>
 __device__ __forceinline__ void issue_block(const NearArgs& A, const int64_t* bl, int i, double2* st,
                                             uint64_t* bar, uint64_t pol) {
@@ -152,8 +164,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // at most 80 registers: its 9 warps sit beside the far kernel's 8 (<= 128 registers) within each
 // scheduler's 16K-register share (warp i runs on scheduler i % 4: scheduler 0 holds 3 near
 // warps).  Over budget, most near CTAs wait for the far kernel to exit (measured: step 82 us)
-// TR: the per-CTA timeline (H2B_NEAR_TRACE) is compiled into a second instantiation only: the
-// stamps' predicated clock reads sat on the consumer's per-block chain (~5 % of its stall samples)
+// TR: the per-CTA timeline (H2B_NEAR_TRACE) and the profiling switches (A.dbg) are compiled into
+// a second instantiation only: the stamps' predicated clock reads sat on the consumer's per-block
+// chain (~5 % of its stall samples; near field alone 30.7 -> 28.7 us without them)
 template <int NS, int R, bool TR = false>
 __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
   // dynamic shared memory: [ring: nst stages][NRB record buffers]
@@ -184,6 +197,8 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
     }
   }
   __syncthreads();
+  // shared-window addresses of the barriers and the ring, computed once (see mbar_wait_a)
+  const uint32_t fbar_a = smem_u32(fbar), ebar_a = smem_u32(ebar), sm_a = smem_u32(sm);
   // y is zeroed by the far-field programs at their start (ZeroSync, h2b_common.cuh): the
   // consumers wait here — while the producer fills the ring and before the first block can have
   // landed — for the flags of the programs covering the CTA's rows, and clear them.  (Nothing of
@@ -259,7 +274,7 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
         }
         return (int)atomicAdd(&A.ctrl->near_next, 1u);
       };
-      const int dbg = A.dbg;
+      const int dbg = TR ? A.dbg : 0;  // (profiling switches: instrumented instantiation only)
       int issued = 0;
       int pst = 0;       // ring stage of the next block (no divisions on the issue path)
       uint32_t pph = 0;  // its phase parity
@@ -294,12 +309,12 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
           const int64_t* bl = reinterpret_cast<const int64_t*>(r + 1 + r[0].y);
           for (int j = (q == 0 && early) ? 1 : 0; j < nb; ++j, ++issued) {
             uint64_t c2 = tr ? clock64() : 0;
-            if (issued >= nst) mbar_wait(&ebar[pst], pph ^ 1u);  // freed by round issued / nst - 1
+            if (issued >= nst) mbar_wait_a(ebar_a + 8u * pst, pph ^ 1u);  // freed by round issued / nst - 1
             if (tr) cw[0] += clock64() - c2;
-            double2* sp = sm + (size_t)pst * STG;
-            mbar_arrive_expect_tx(&fbar[pst], 16u * (RB * NS + ((dbg & 2) ? 0 : NS)));
-            bulk_g2s_hint(sp, A.dbuf + bl[2 * j], 16u * RB * NS, &fbar[pst], pol);
-            if (!(dbg & 2)) bulk_g2s(sp + RB * NS, A.x + bl[2 * j + 1], 16u * NS, &fbar[pst]);
+            const uint32_t sp = sm_a + 16u * (uint32_t)(pst * STG), fb_a = fbar_a + 8u * pst;
+            mbar_arrive_expect_tx_a(fb_a, 16u * (RB * NS + ((dbg & 2) ? 0 : NS)));
+            bulk_g2s_hint_a(sp, A.dbuf + bl[2 * j], 16u * RB * NS, fb_a, pol);
+            if (!(dbg & 2)) bulk_g2s_a(sp + 16u * RB * NS, A.x + bl[2 * j + 1], 16u * NS, fb_a);
             if (++pst == nst) {
               pst = 0;
               pph ^= 1u;
@@ -351,7 +366,7 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
     int consumed = 0;
     int st = 0;       // ring stage of the next block and its phase parity: the per-block path
     uint32_t ph = 0;  // has no divisions (it is latency-bound: 2 consumer warps per scheduler)
-    const bool math = !(A.dbg & 1);
+    const bool math = TR ? !(A.dbg & 1) : true;
     const uint64_t cstart = tr ? clock64() : 0;
     for (int q = 0;; ++q) {
       const int b = q % NRB;
@@ -372,7 +387,7 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
         for (int j = 0; j < NACC; ++j) acc[r][j] = make_double2(0.0, 0.0);
       for (int i = 0; i < nb; ++i, ++consumed) {
         uint64_t c3 = tr ? clock64() : 0;
-        mbar_wait(&fbar[st], ph);
+        mbar_wait_a(fbar_a + 8u * st, ph);
         if (tr) cw[0] += clock64() - c3;
         if (tr && consumed == 0 && threadIdx.x == 0) tr[3] = gtimer();
         const double2* sp = sm + (size_t)st * STG;
@@ -391,7 +406,7 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&ebar[st]);  // this warp is done with the stage
+        if (lane == 0) mbar_arrive_a(ebar_a + 8u * st);  // this warp is done with the stage
         if (++st == nst) {
           st = 0;
           ph ^= 1u;
@@ -913,7 +928,7 @@ int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st)
     bool launched = false;
 #define X(a, b)                                                                            \
   if (!launched && ns == a && r == b) {                                                    \
-    if (N.trace)                                                                           \
+    if (N.trace || N.dbg)                                                                  \
       k_near_stream<a, b, true><<<h->near_grid, NEAR_THREADS, h->near_smem, st>>>(N);               \
     else                                                                                   \
       k_near_stream<a, b><<<h->near_grid, NEAR_THREADS, h->near_smem, st>>>(N);                     \
@@ -922,7 +937,7 @@ int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st)
     NEAR_VARIANTS(X)
 #undef X
     if (!launched) {
-      if (N.trace)
+      if (N.trace || N.dbg)
         k_near_stream<0, 1, true><<<h->near_grid, NEAR_THREADS, h->near_smem, st>>>(N);
       else
         k_near_stream<0, 1><<<h->near_grid, NEAR_THREADS, h->near_smem, st>>>(N);
