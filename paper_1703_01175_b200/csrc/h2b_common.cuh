@@ -178,7 +178,7 @@ struct Task {
 //   couple: {n_items, cta_mode, 0, 0} | n_items x CoupleItem (2 slots each)
 constexpr int REC_SLOTS = 256;  // 4 KB per record buffer
 constexpr int NEAR_NRB = 8;      // near-field stream: record buffers (the task in use + NRB - 1 claimed ahead)
-constexpr int NEAR_MAXG = 152;  // CTAs of the near stream with kernel-parameter first copies
+constexpr int NEAR_MAXG = 192;  // CTAs of the near stream with kernel-parameter first copies
 constexpr int NEAR_REC_MAXB = 160;
 struct DepRange {
   int32_t lo, hi;           // task ids [lo, hi) that must be complete

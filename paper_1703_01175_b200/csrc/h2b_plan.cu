@@ -1337,8 +1337,9 @@ int h2b_prepare(h2b_ctx* h) {
       h->near_static = 1;
       if (const char* e = getenv("H2B_NEAR_STATIC")) h->near_static = atoi(e) ? 1 : 0;  // tuning aid
       if (const char* e = getenv("H2B_NEAR_DBG")) h->near_dbg = atoi(e);  // profiling only
-      if (const char* e = getenv("H2B_NEAR_GRID")) h->near_grid = std::max(1, std::min(sms, atoi(e)));  // tuning aid
+      if (const char* e = getenv("H2B_NEAR_GRID")) h->near_grid = std::max(1, std::min(NEAR_MAXG, atoi(e)));  // tuning aid
       // each CTA's first record and first block (static split): kernel parameters
+      auto near_cta_tables = [&]() {  // (again below when the tree plan changes the grid)
       h->near_early = 0;
       auto leaf_has_near = [&](int t) { return h->d_row_ptr[t + 1] > h->d_row_ptr[t]; };
       h->near_first_rec.assign(h->near_grid, int2{0, 0});
@@ -1385,9 +1386,11 @@ int h2b_prepare(h2b_ctx* h) {
         }
         h->near_zero_ok = ok && next == h->n ? 1 : 0;
       }
+      };
+      near_cta_tables();
       if (getenv("H2B_NEAR_TRACE") && !h->near_trace) {  // development aid (h2b_near_trace)
-        H2B_CUDA_TRY(cudaMalloc(&h->near_trace, sizeof(uint64_t) * 24 * sms));
-        H2B_CUDA_TRY(cudaMemset(h->near_trace, 0, sizeof(uint64_t) * 24 * sms));
+        H2B_CUDA_TRY(cudaMalloc(&h->near_trace, sizeof(uint64_t) * 24 * std::max(sms, NEAR_MAXG)));
+        H2B_CUDA_TRY(cudaMemset(h->near_trace, 0, sizeof(uint64_t) * 24 * std::max(sms, NEAR_MAXG)));
       }
       h->mega = (per_sm > 0 && h->mega_grid <= per_sm * sms) ? 1 : 0;
       h->mega_est_us = mp.est_makespan;
@@ -1398,6 +1401,17 @@ int h2b_prepare(h2b_ctx* h) {
       if (h->mega && h->use_tree) H2B_TRY(h2b_tree_prepare(h, sms, TREE_BUDGET, &tb, &planned));
       if (planned) {
         acc += tb;
+        // one more near-field CTA on every SM without a program: a program's 174 KB leave room
+        // for exactly one near-field CTA beside it, so the extra CTAs can only land on the free
+        // SMs, which then stream with two consumer chains (cfg2: 168 CTAs, the near CTAs' last
+        // exit 31.9 -> 30.8 us in the step)
+        if (!getenv("H2B_NEAR_GRID") && mp.ns > 0 && h->near_static) {
+          const int extra = std::max(0, sms - h->tree_progs);
+          if (extra > 0 && sms + extra <= NEAR_MAXG) {
+            h->near_grid = sms + extra;
+            near_cta_tables();
+          }
+        }
         H2B_TRY(h2b_tree_prepare_zero(h, h->tree));
         const int tree_total = h->tree_smem + h2b_tree_static_smem() + 1024;
         int tnst = stg > 0 ? std::min(8, (sm_total - tree_total - near_static - rec_bytes) / stg) : 0;

@@ -41,7 +41,7 @@ _abi.check(L.h2b_query(op.handle, _abi.Q_NEAR_SMEM, C.byref(v2)))
 v3 = C.c_int64()
 _abi.check(L.h2b_query(op.handle, _abi.Q_NEAR_STAGES, C.byref(v3)))
 print(f"tree programs {nprog}, tree smem {v.value >> 32} B, near smem {v2.value} B, near stages {v3.value}")
-ncta = torch.cuda.get_device_properties(0).multi_processor_count
+ncta = int(os.environ.get("H2B_NEAR_GRID", torch.cuda.get_device_properties(0).multi_processor_count))
 flush = L2Flusher("cuda")
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 L.h2b_stamp_ns.argtypes = [C.c_void_p, C.c_void_p]
