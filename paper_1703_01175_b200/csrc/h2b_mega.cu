@@ -167,11 +167,15 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // TR: the per-CTA timeline (H2B_NEAR_TRACE) and the profiling switches (A.dbg) are compiled into
 // a second instantiation only: the stamps' predicated clock reads sat on the consumer's per-block
 // chain (~5 % of its stall samples; near field alone 30.7 -> 28.7 us without them)
-template <int NS, int R, bool TR = false>
+// NG: consumer groups.  NG = 2 (r02): warps 0-3 and 4-7 take the leaves of the stream in turn
+// (a leaf's blocks all go to one group, so every row of y still gets one update); the per-block
+// chain of a group is a little longer (each thread two rows), but two blocks are worked on at
+// once — the stream of a CTA is bound by that chain, not by the ring or by HBM.
+template <int NS, int R, bool TR = false, int NG = 1>
 __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
   // dynamic shared memory: [ring: nst stages][NRB record buffers]
   extern __shared__ __align__(16) double2 sm[];
-  __shared__ uint64_t fbar[NST_MAX], ebar[NST_MAX], rbar[NRB], rfree[NRB];
+  __shared__ uint64_t fbar[NG * NST_MAX], ebar[NST_MAX], rbar[NRB], rfree[NRB];  // fbar: per consumer group and stage
   __shared__ int s_task[NRB];
   constexpr int LPR = NS > 0 ? NS / 2 : 1;
   constexpr int RPP = MNT / LPR;
@@ -188,8 +192,8 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
       tr[7] = smid();
     }
     for (int i = 0; i < NST_MAX; ++i) {
-      mbar_init(&fbar[i], 1);
-      mbar_init(&ebar[i], MNT / 32);
+      for (int g = 0; g < NG; ++g) mbar_init(&fbar[g * NST_MAX + i], 1);
+      mbar_init(&ebar[i], MNT / 32 / NG);  // the warps of the group that consumes the stage's block
     }
     for (int b = 0; b < NRB; ++b) {
       mbar_init(&rbar[b], 1);
@@ -276,6 +280,7 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
       };
       const int dbg = TR ? A.dbg : 0;  // (profiling switches: instrumented instantiation only)
       int issued = 0;
+      int pturn = 0;     // NG = 2: consumer group of the leaf being issued
       int pst = 0;       // ring stage of the next block (no divisions on the issue path)
       uint32_t pph = 0;  // its phase parity
       const bool early = A.early && s_first < s_end && NS > 0;
@@ -307,11 +312,28 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
           const int4* r = rbuf(b);
           const int nb = r[0].x;
           const int64_t* bl = reinterpret_cast<const int64_t*>(r + 1 + r[0].y);
-          for (int j = (q == 0 && early) ? 1 : 0; j < nb; ++j, ++issued) {
+          // NG = 2: a block completes on the full barrier of the group that consumes its leaf
+          // (the leaves of the stream go to the groups in turn), so every group sees every phase
+          // of the barriers it waits on — a parity wait tells only adjacent phases apart
+          const int64_t* plv = reinterpret_cast<const int64_t*>(r + 1);  // {y_off, blocks} per leaf
+          int pl = 0, prem = NG > 1 ? (int)plv[1] : 0;
+          if (NG > 1 && q > 0) pturn ^= 1;
+          for (int j = 0; j < nb; ++j) {
+            if constexpr (NG > 1) {
+              while (prem == 0) {
+                ++pl;
+                prem = (int)plv[2 * pl + 1];
+                pturn ^= 1;
+              }
+              --prem;
+            }
+            if (j == 0 && q == 0 && early) continue;  // issued above (the first leaf: group 0)
+            ++issued;
             uint64_t c2 = tr ? clock64() : 0;
-            if (issued >= nst) mbar_wait_a(ebar_a + 8u * pst, pph ^ 1u);  // freed by round issued / nst - 1
+            if (issued > nst) mbar_wait_a(ebar_a + 8u * pst, pph ^ 1u);  // freed by round (issued - 1) / nst - 1
             if (tr) cw[0] += clock64() - c2;
-            const uint32_t sp = sm_a + 16u * (uint32_t)(pst * STG), fb_a = fbar_a + 8u * pst;
+            const uint32_t sp = sm_a + 16u * (uint32_t)(pst * STG),
+                           fb_a = fbar_a + 8u * (uint32_t)((NG > 1 ? pturn * NST_MAX : 0) + pst);
             mbar_arrive_expect_tx_a(fb_a, 16u * (RB * NS + ((dbg & 2) ? 0 : NS)));
             bulk_g2s_hint_a(sp, A.dbuf + bl[2 * j], 16u * RB * NS, fb_a, pol);
             if (!(dbg & 2)) bulk_g2s_a(sp + 16u * RB * NS, A.x + bl[2 * j + 1], 16u * NS, fb_a);
@@ -350,6 +372,81 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
       near_task_generic(A, rbuf(b)[0].x);
       __syncwarp();
       if (lane == 0) mbar_arrive(&rfree[b]);
+    }
+  } else if constexpr (NG == 2) {
+    constexpr int GT = MNT / NG;                      // threads of a group
+    constexpr int EPT = RB * NS / GT;                 // slice elements per thread
+    constexpr int CPL = EPT < 4 ? EPT : 4;
+    constexpr int LPRC = NS / CPL;
+    constexpr int RPPC = GT / LPRC;
+    constexpr int RR = EPT / CPL;
+    static_assert(RR * RPPC == RB && CPL * LPRC == NS, "near consumer mapping (two groups)");
+    const int grp = threadIdx.x / GT, gt = threadIdx.x % GT;
+    const int r0 = gt / LPRC, c0 = gt % LPRC;
+    int st = 0;         // ring stage of the stream's next block (both groups count all blocks)
+    uint32_t phs = 0;   // bit s: parity of this group's next phase of its full barrier of stage s
+    const uint32_t gbar_a = fbar_a + 8u * (uint32_t)(grp * NST_MAX);
+    int turn = 0;       // group of the stream's next leaf
+    int consumed = 0;
+    for (int q = 0;; ++q) {
+      const int b = q % NRB;
+      mbar_wait(&rbar[b], (q / NRB) & 1u);
+      if (s_task[b] >= A.n_tasks) break;
+      const int4* rec = rbuf(b);
+      const int nl = rec[0].y, row0 = rec[0].z;
+      const int64_t* lv = reinterpret_cast<const int64_t*>(rec + 1);  // {y_off, nb} per leaf
+      for (int li = 0; li < nl; ++li) {
+        const int nbl = (int)lv[2 * li + 1];
+        const bool mine = turn == grp;
+        turn ^= 1;
+        if (!mine) {  // the other group's leaf (its blocks complete on that group's barriers)
+          st += nbl;
+          while (st >= nst) st -= nst;
+          continue;
+        }
+        constexpr int NACC = CPL < 2 ? 1 : 2;
+        double2 acc[RR][NACC];
+#pragma unroll
+        for (int r = 0; r < RR; ++r)
+#pragma unroll
+          for (int j = 0; j < NACC; ++j) acc[r][j] = make_double2(0.0, 0.0);
+        for (int i = 0; i < nbl; ++i, ++consumed) {
+          mbar_wait_a(gbar_a + 8u * st, (phs >> st) & 1u);
+          phs ^= 1u << st;
+          if (TR && tr && consumed == 0 && gt == 0 && grp == 0) tr[3] = gtimer();
+          const double2* sp = sm + (size_t)st * STG;
+          double2 xv[CPL];
+#pragma unroll
+          for (int j = 0; j < CPL; ++j) xv[j] = sp[RB * NS + c0 + j * LPRC];
+#pragma unroll
+          for (int r = 0; r < RR; ++r) {
+            double2 dv[CPL];
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) dv[j] = sp[(r0 + r * RPPC) * NS + c0 + j * LPRC];
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) cfma(acc[r][j % NACC], dv[j], xv[j]);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive_a(ebar_a + 8u * st);  // this warp is done with the stage
+          if (++st == nst) st = 0;
+        }
+        const int64_t y_off = lv[2 * li];
+#pragma unroll
+        for (int r = 0; r < RR; ++r) {
+          double2 a = acc[r][0];
+#pragma unroll
+          for (int j = 1; j < NACC; ++j) a = cadd(a, acc[r][j]);
+#pragma unroll
+          for (int m = LPRC / 2; m > 0; m >>= 1) a = cadd(a, shfl_xor2(a, m));
+          if (c0 == 0) atomic_add2(A.y + y_off + row0 + r0 + r * RPPC, a);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&rfree[b]);  // this warp is done with the record
+    }
+    if (TR && tr && threadIdx.x == 0) {
+      tr[4] = gtimer();
+      tr[6] = consumed;
     }
   } else {
     // consumer mapping: each thread owns CPL interleaved columns (c0 + j LPRC: conflict-free
@@ -777,8 +874,9 @@ int h2b_mega_set_smem(int, int, int bytes) {
 int h2b_near_stream_static_smem(int ns, int r, int* bytes) {
   cudaFuncAttributes fa;
   cudaError_t e = cudaErrorInvalidValue;
+  // (the instantiation with the most static shared memory and registers: two consumer groups, instrumented)
 #define X(a, b) \
-  if (ns == a && r == b) e = cudaFuncGetAttributes(&fa, k_near_stream<a, b>);
+  if (ns == a && r == b) e = cudaFuncGetAttributes(&fa, k_near_stream<a, b, true, (a == 32 ? 2 : 1)>);
   NEAR_VARIANTS(X)
 #undef X
   if (ns != 32 && ns != 64) e = cudaFuncGetAttributes(&fa, k_near_stream<0, 1>);
@@ -795,7 +893,7 @@ int h2b_near_stream_regs(int ns, int r) {
   cudaFuncAttributes fa;
   cudaError_t e = cudaErrorInvalidValue;
 #define X(a, b) \
-  if (ns == a && r == b) e = cudaFuncGetAttributes(&fa, k_near_stream<a, b>);
+  if (ns == a && r == b) e = cudaFuncGetAttributes(&fa, k_near_stream<a, b, false, (a == 32 ? 2 : 1)>);
   NEAR_VARIANTS(X)
 #undef X
   if (ns != 32 && ns != 64) e = cudaFuncGetAttributes(&fa, k_near_stream<0, 1>);
@@ -813,6 +911,10 @@ int h2b_near_stream_set_smem(int ns, int r, int bytes) {
     H2B_CUDA_TRY(cudaFuncSetAttribute(k_near_stream<a, b>, cudaFuncAttributePreferredSharedMemoryCarveout, 100)); \
     H2B_CUDA_TRY(cudaFuncSetAttribute(k_near_stream<a, b, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)); \
     H2B_CUDA_TRY(cudaFuncSetAttribute(k_near_stream<a, b, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100)); \
+    H2B_CUDA_TRY(cudaFuncSetAttribute(k_near_stream<a, b, false, (a == 32 ? 2 : 1)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)); \
+    H2B_CUDA_TRY(cudaFuncSetAttribute(k_near_stream<a, b, false, (a == 32 ? 2 : 1)>, cudaFuncAttributePreferredSharedMemoryCarveout, 100)); \
+    H2B_CUDA_TRY(cudaFuncSetAttribute(k_near_stream<a, b, true, (a == 32 ? 2 : 1)>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)); \
+    H2B_CUDA_TRY(cudaFuncSetAttribute(k_near_stream<a, b, true, (a == 32 ? 2 : 1)>, cudaFuncAttributePreferredSharedMemoryCarveout, 100)); \
   }
   NEAR_VARIANTS(X)
 #undef X
@@ -926,9 +1028,16 @@ int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st)
       }
     const int ns = h->mega_ns, r = h->mega_r;
     bool launched = false;
+    // two consumer groups for 32-point leaves (cfg2: near alone 28.8 -> 27.0 us, its last CTA out
+    // 30.8 -> 27.9 us in the step); H2B_NEAR_NG=1: one group (A/B aid)
+    static const bool ng2 = getenv("H2B_NEAR_NG") ? atoi(getenv("H2B_NEAR_NG")) == 2 : true;
 #define X(a, b)                                                                            \
   if (!launched && ns == a && r == b) {                                                    \
-    if (N.trace || N.dbg)                                                                  \
+    if (a == 32 && ng2 && (N.trace || N.dbg))                                              \
+      k_near_stream<a, b, true, (a == 32 ? 2 : 1)><<<h->near_grid, NEAR_THREADS, h->near_smem, st>>>(N);  \
+    else if (a == 32 && ng2)                                                               \
+      k_near_stream<a, b, false, (a == 32 ? 2 : 1)><<<h->near_grid, NEAR_THREADS, h->near_smem, st>>>(N); \
+    else if (N.trace || N.dbg)                                                             \
       k_near_stream<a, b, true><<<h->near_grid, NEAR_THREADS, h->near_smem, st>>>(N);               \
     else                                                                                   \
       k_near_stream<a, b><<<h->near_grid, NEAR_THREADS, h->near_smem, st>>>(N);                     \
