@@ -317,13 +317,13 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
           // of the barriers it waits on — a parity wait tells only adjacent phases apart
           const int64_t* plv = reinterpret_cast<const int64_t*>(r + 1);  // {y_off, blocks} per leaf
           int pl = 0, prem = NG > 1 ? (int)plv[1] : 0;
-          if (NG > 1 && q > 0) pturn ^= 1;
+          if (NG > 1 && q > 0) pturn = (pturn + 1) & (NG - 1);
           for (int j = 0; j < nb; ++j) {
             if constexpr (NG > 1) {
               while (prem == 0) {
                 ++pl;
                 prem = (int)plv[2 * pl + 1];
-                pturn ^= 1;
+                pturn = (pturn + 1) & (NG - 1);
               }
               --prem;
             }
@@ -373,7 +373,7 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&rfree[b]);
     }
-  } else if constexpr (NG == 2) {
+  } else if constexpr (NG >= 2) {
     constexpr int GT = MNT / NG;                      // threads of a group
     constexpr int EPT = RB * NS / GT;                 // slice elements per thread
     constexpr int CPL = EPT < 4 ? EPT : 4;
@@ -398,7 +398,7 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
       for (int li = 0; li < nl; ++li) {
         const int nbl = (int)lv[2 * li + 1];
         const bool mine = turn == grp;
-        turn ^= 1;
+        turn = (turn + 1) & (NG - 1);
         if (!mine) {  // the other group's leaf (its blocks complete on that group's barriers)
           st += nbl;
           while (st >= nst) st -= nst;
@@ -1030,7 +1030,7 @@ int h2b_launch_mega(h2b_ctx* h, const double2* xp, double2* yp, cudaStream_t st)
     bool launched = false;
     // two consumer groups for 32-point leaves (cfg2: near alone 28.8 -> 27.0 us, its last CTA out
     // 30.8 -> 27.9 us in the step); H2B_NEAR_NG=1: one group (A/B aid)
-    static const bool ng2 = getenv("H2B_NEAR_NG") ? atoi(getenv("H2B_NEAR_NG")) == 2 : true;
+    static const bool ng2 = getenv("H2B_NEAR_NG") ? atoi(getenv("H2B_NEAR_NG")) == 2 : true;  // (four groups: no gain)
 #define X(a, b)                                                                            \
   if (!launched && ns == a && r == b) {                                                    \
     if (a == 32 && ng2 && (N.trace || N.dbg))                                              \
