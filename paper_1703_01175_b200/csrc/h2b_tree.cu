@@ -623,7 +623,15 @@ struct Builder {
       n.s_pay = (int32_t)(uint32_t)so;
       n.pad = (int32_t)(so >> 32);
       if (stage_s) {
-        tp.copies.push_back(TCopy{h->s_off[b0], TS_S, rows * n.k, off, 0});
+        // consecutive targets' panels are adjacent in sbuf and here: one bulk copy per run (a
+        // program's ~30 panel copies become ~5: fewer, larger requests on the SM's copy queue,
+        // which the near-field ring shares)
+        if ((int)tp.copies.size() > P.copy_first && tp.copies.back().kind == TS_S && tp.copies.back().smem >= 0 &&
+            tp.copies.back().src + tp.copies.back().elems == h->s_off[b0] &&
+            tp.copies.back().smem + tp.copies.back().elems == off && tp.copies.back().elems + rows * n.k <= 32768)
+          tp.copies.back().elems += rows * n.k;
+        else
+          tp.copies.push_back(TCopy{h->s_off[b0], TS_S, rows * n.k, off, 0});
         off += rows * n.k;
       } else {  // L2 prefetch range (merged with the previous target's when contiguous)
         TCopy pc{h->s_off[b0], TS_S, rows * n.k, -1, 0};
