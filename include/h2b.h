@@ -107,7 +107,13 @@ int64_t h2b_device_bytes(h2b_handle h);
 /* y_perm = S x_perm for q right-hand sides, DEVICE pointers, (N, q) row-major.
  * Replaces arith._apply_perm (arith.py:52-104).  Stream-ordered on `stream`
  * (a cudaStream_t; NULL = legacy default).  No allocation after the first
- * call with a given q.  x_perm and y_perm must not alias. */
+ * call with a given q.  x_perm and y_perm must not alias.  y_perm is overwritten
+ * (it need not be initialised: at q = 1 on small operators the two persistent
+ * kernels of the step zero it themselves, rows by rows, before they accumulate
+ * into it; elsewhere a memset node does).  Environment switches for A/B runs:
+ * H2B_Y_MEMSET=1 (memset node), H2B_TREE_NO_FLAT=1 (top programs instead of the
+ * flattened top tier), H2B_NEAR_NG=1 (one near-field consumer group),
+ * H2B_NEAR_GRID=n (near-field CTAs), H2B_NO_TREE=1 (task-graph far field). */
 int h2b_matvec_perm(h2b_handle h, const void* x_perm, void* y_perm, int q, void* stream);
 
 /* y = S x with HOST buffers in the ORIGINAL ordering, (N, q) row-major:
