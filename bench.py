@@ -500,6 +500,9 @@ def run_single(a, pk, ex, rank, world, local, steps=None, extras=True):
 
     for _ in range(max(3, a.warmup)):
         mv()
+    # the warm-up steps proper are the timed step itself (L2 flush, spin, step), untimed: the first
+    # flushed step of a process is a one-off (~80 us measured: first cold pass over the tables)
+    timed(mv, max(3, a.warmup))
     torch.cuda.synchronize(dev)
     if world > 1:
         torch.distributed.barrier()
