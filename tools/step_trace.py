@@ -68,6 +68,13 @@ for rep in range(10):
         near_sm = nt[:, 7]
         free = [c for c in range(ncta) if int(near_sm[c]) not in far_sm]
         print(f"near CTAs on SMs without a far program: {len(free)}: {free}")
+        ex = (nt[:, 5] - min(nt[:, 0].min(), tt[:, 0][tt[:, 0] > 0].min())) / 1e3
+        fs = set(free)
+        a = np.array([ex[c] for c in range(ncta) if c in fs])
+        b = np.array([ex[c] for c in range(ncta) if c not in fs])
+        if len(a) and len(b):
+            print(f"near exit (us) on SMs without a program: min {a.min():.1f} med {np.median(a):.1f} max {a.max():.1f}; "
+                  f"beside a program: min {b.min():.1f} med {np.median(b):.1f} max {b.max():.1f}")
     if rep < 2:
         continue
     t0 = nt[:, 0].min()
