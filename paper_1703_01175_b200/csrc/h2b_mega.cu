@@ -1,11 +1,13 @@
 // Persistent single-RHS H² matvec for sm_100a: two concurrent persistent kernels.
 //
 // `_apply_perm` (reference arith.py:52-104) splits into two independent halves whose
-// results are both added into y (zeroed first):
+// results are both added into y (zeroed first: by a memset node, or — tree far field — by the
+// far-field programs themselves, ZeroSync in h2b_common.cuh):
 //   * k_near_stream  the near field y += D x (arith.py:100-104), bandwidth-bound: one CTA
-//                    per SM streams D row panels through a TMA ring; tasks (row panels of
-//                    a few leaves) are claimed dynamically from an atomic counter, one task
-//                    ahead, so all SMs finish within one task of each other.
+//                    per SM (plus one per SM without a far-field program) streams D row
+//                    panels through a TMA ring; tasks (row panels of a few leaves) are split
+//                    statically over the CTAs (or claimed from an atomic counter); for
+//                    32-point leaves two consumer groups take the stream's leaves in turn.
 //   * k_mega         the far field (arith.py:58-99), latency-bound: a task graph planned on
 //                    the host (h2b_plan.cu) of T_SPAN forward/backward span programs
 //                    (subtrees or upper tiers of the cluster tree, staged with TMA bulk
@@ -13,9 +15,11 @@
 //                    One CTA per SM runs a static, topologically sorted task list from its
 //                    own bulk-loaded "blob"; tasks wait on epoch-stamped completion flags.
 // Both kernels run at the same time (one CTA of each per SM: the planner splits the shared
-// memory), neither waits on the other, and each y element receives exactly one near and at
-// most one far contribution through atomicAdd, so the sum is deterministic (two-term
-// floating-point addition commutes).
+// memory); with the memset node neither waits on the other (without it the near-field CTAs wait
+// for the far-field programs' zeroing flags before their consumers start).  Each y element
+// receives exactly one near and at most one far contribution, so the sum is deterministic
+// (two-term floating-point addition commutes).  For complete binary trees the far field is
+// k_far_tree (h2b_tree.cu) in k_mega's place.
 #include "h2b_span.cuh"
 
 namespace {

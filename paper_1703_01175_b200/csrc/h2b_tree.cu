@@ -20,7 +20,8 @@
 //   bottom up  -> [flag up] -> top up, top couplings (after the other top programs' flags),
 //   top down -> [flag down] -> bottom down; bottom couplings wait only for the neighbouring
 //   bottom programs' x̂ and run while the top works.
-// The near field runs concurrently in k_near_stream (h2b_mega.cu); both add into a zeroed y.
+// The near field runs concurrently in k_near_stream (h2b_mega.cu); both add into y, which the
+// bottom programs zero at their start (ZeroSync, h2b_common.cuh) unless a memset node did.
 #include <algorithm>
 #include <cstring>
 #include <map>
