@@ -20,6 +20,9 @@
 //   bottom up  -> [flag up] -> top up, top couplings (after the other top programs' flags),
 //   top down -> [flag down] -> bottom down; bottom couplings wait only for the neighbouring
 //   bottom programs' x̂ and run while the top works.
+// With the flat top (r02, see FlatAnc below; at most five levels above the split) there are no
+// top programs: every bottom program carries the folded operators of its ancestors and the
+// levels above the split cost ONE hand-off (the programs' shares of the ancestors' x̂).
 // The near field runs concurrently in k_near_stream (h2b_mega.cu); both add into y, which the
 // bottom programs zero at their start (ZeroSync, h2b_common.cuh) unless a memset node did.
 #include <algorithm>
