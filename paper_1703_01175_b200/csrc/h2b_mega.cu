@@ -290,9 +290,12 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
       const bool early = A.early && s_first < s_end && NS > 0;
       if (early) {  // the first block before any record (its offsets are kernel parameters)
         const longlong2 fb = A.first_blk[blockIdx.x];
-        mbar_arrive_expect_tx(&fbar[0], 16u * (RB * NS + ((dbg & 2) ? 0 : NS)));
+        // (NG > 1: the consumers read the partner's x segment from global memory themselves — it is
+        // L2-resident — one block ahead; the second bulk request per block cost a 2 us timer tick)
+        constexpr bool XC = NG == 1;
+        mbar_arrive_expect_tx(&fbar[0], 16u * (RB * NS + ((dbg & 2) || !XC ? 0 : NS)));
         bulk_g2s_hint(sm, A.dbuf + fb.x, 16u * RB * NS, &fbar[0], pol);
-        if (!(dbg & 2)) bulk_g2s(sm + RB * NS, A.x + fb.y, 16u * NS, &fbar[0]);
+        if (!(dbg & 2) && XC) bulk_g2s(sm + RB * NS, A.x + fb.y, 16u * NS, &fbar[0]);
         issued = 1;
         pst = nst == 1 ? 0 : 1;
         pph = nst == 1 ? 1u : 0u;
@@ -338,9 +341,10 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
             if (tr) cw[0] += clock64() - c2;
             const uint32_t sp = sm_a + 16u * (uint32_t)(pst * STG),
                            fb_a = fbar_a + 8u * (uint32_t)((NG > 1 ? pturn * NST_MAX : 0) + pst);
-            mbar_arrive_expect_tx_a(fb_a, 16u * (RB * NS + ((dbg & 2) ? 0 : NS)));
+            constexpr bool XC = NG == 1;
+            mbar_arrive_expect_tx_a(fb_a, 16u * (RB * NS + ((dbg & 2) || !XC ? 0 : NS)));
             bulk_g2s_hint_a(sp, A.dbuf + bl[2 * j], 16u * RB * NS, fb_a, pol);
-            if (!(dbg & 2)) bulk_g2s_a(sp + 16u * RB * NS, A.x + bl[2 * j + 1], 16u * NS, fb_a);
+            if (!(dbg & 2) && XC) bulk_g2s_a(sp + 16u * RB * NS, A.x + bl[2 * j + 1], 16u * NS, fb_a);
             if (++pst == nst) {
               pst = 0;
               pph ^= 1u;
@@ -399,6 +403,8 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
       const int4* rec = rbuf(b);
       const int nl = rec[0].y, row0 = rec[0].z;
       const int64_t* lv = reinterpret_cast<const int64_t*>(rec + 1);  // {y_off, nb} per leaf
+      const int64_t* blx = lv + 2 * nl + 1;  // block list {D offset, x offset}: the x offsets
+      int bofs = 0;                          // first block of the leaf in the record's list
       for (int li = 0; li < nl; ++li) {
         const int nbl = (int)lv[2 * li + 1];
         const bool mine = turn == grp;
@@ -406,6 +412,7 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
         if (!mine) {  // the other group's leaf (its blocks complete on that group's barriers)
           st += nbl;
           while (st >= nst) st -= nst;
+          bofs += nbl;
           continue;
         }
         constexpr int NACC = CPL < 2 ? 1 : 2;
@@ -415,13 +422,18 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
 #pragma unroll
           for (int j = 0; j < NACC; ++j) acc[r][j] = make_double2(0.0, 0.0);
         for (int i = 0; i < nbl; ++i, ++consumed) {
+          // the partner's x segment straight from global memory (L2), requested before the wait
+          // for the block so that its latency hides behind it
+          double2 xv[CPL];
+          {
+            const double2* xs = A.x + blx[2 * (bofs + i)] + c0;
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) xv[j] = __ldg(xs + j * LPRC);
+          }
           mbar_wait_a(gbar_a + 8u * st, (phs >> st) & 1u);
           phs ^= 1u << st;
           if (TR && tr && consumed == 0 && gt == 0 && grp == 0) tr[3] = gtimer();
           const double2* sp = sm + (size_t)st * STG;
-          double2 xv[CPL];
-#pragma unroll
-          for (int j = 0; j < CPL; ++j) xv[j] = sp[RB * NS + c0 + j * LPRC];
 #pragma unroll
           for (int r = 0; r < RR; ++r) {
             double2 dv[CPL];
@@ -444,6 +456,7 @@ __global__ void __maxnreg__(80) k_near_stream(NearArgs A) {
           for (int m = LPRC / 2; m > 0; m >>= 1) a = cadd(a, shfl_xor2(a, m));
           if (c0 == 0) atomic_add2(A.y + y_off + row0 + r0 + r * RPPC, a);
         }
+        bofs += nbl;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&rfree[b]);  // this warp is done with the record
