@@ -1194,7 +1194,9 @@ int h2b_launch_tree(h2b_ctx* h, const TreeDev* d, const double2* xp, double2* yp
     const char* e = getenv("H2B_TREE_TRACE");
     A.trace_levels = e ? atoi(e) : 0;
     const char* d = getenv("H2B_TREE_DEFER_S");  // A/B aid
-    A.defer_s = d ? atoi(d) : 1;  // measured: step 40.3 vs 41.0 us at cfg2
+    // bit 0: coupling panels, bit 2: transfers and chains requested once the leaf-level operands
+    // have landed (measured at cfg2: panels 40.3 vs 41.0 us; transfers too: mean 33.6 -> 33.0 us)
+    A.defer_s = d ? atoi(d) : 5;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(d->n_progs);
